@@ -1,0 +1,105 @@
+/*
+ * ranklab_gpu.h -- C ABI of the B200-native CUP library (libranklab_gpu.so).
+ *
+ * Drop-in boundary for the reference's hot path (paths relative to
+ * /root/reference).  Plain pointers and sizes only; matrices are row-major
+ * uint32 with leading dimension `ld` (>= cols), entries canonical in [0, p),
+ * p prime, 2 <= p < 2^31 (proj/include/ranklab/field.hpp:38-49).  Every entry
+ * point returns an RL_* status; the C++ shim rethrows the
+ * matching ranklab::Error subclass (proj/include/ranklab/errors.hpp:9-66).
+ *
+ * Functions taking host pointers copy to the device, compute there and copy
+ * back; the *_dev variants take device pointers and a cudaStream_t (as void*,
+ * NULL = legacy default stream) and keep all compute on the GPU.  There is no
+ * CPU fallback: without a usable CUDA device every call returns RL_ECUDA.
+ */
+#ifndef RANKLAB_GPU_H
+#define RANKLAB_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    RL_OK = 0,
+    RL_EDIM = 1,       /* ranklab::DimensionMismatch */
+    RL_EOVERLAP = 2,   /* ranklab::OverlapError */
+    RL_ESINGULAR = 3,  /* ranklab::SingularMatrix / SingularDiagonal */
+    RL_EFIELD = 4,     /* ranklab::NotPrime / ModulusOutOfRange */
+    RL_ECUDA = 5,      /* CUDA runtime failure (ranklab::Error) */
+    RL_ENCCL = 6,      /* NCCL failure (ranklab::Error) */
+    RL_EINVAL = 7,     /* invalid argument (null pointer, ld < cols, ...) */
+    RL_ENOMEM = 8      /* device allocation failed */
+};
+
+/* Field-op tallies in the order of ranklab::OpCounter (field.hpp:16-34):
+ * ops[0] = n_mul, ops[1] = n_addsub, ops[2] = n_divinv, ops[3] = n_ztest.
+ * Filled exactly from the recursion skeleton, the row profile and the pivot
+ * positions (no counting on the device). */
+
+/* In-place CUP: A <- packed [C\U], returns rank, row rank profile rrp[0..rank)
+ * (capacity min(m,n)) and the column permutation sigma[0..n) with
+ * A = C * U * P, column j of A*P^T = column sigma[j] of A.
+ * Replaces: PackedCup ranklab::cup(MatView a, OpCounter& ctr)
+ *           proj/include/ranklab/factor.hpp:34, proj/src/factor.cpp:85.
+ * Any of rank/rrp/sigma/ops may be NULL. */
+int rl_cup_u32(uint32_t* A, int64_t m, int64_t n, int64_t lda, uint32_t p, int64_t* rank,
+               uint32_t* rrp, uint32_t* sigma, uint64_t* ops);
+
+/* Same on a device-resident matrix; outputs are HOST pointers (may be NULL).
+ * No host synchronisation happens before the outputs are requested. */
+int rl_cup_u32_dev(uint32_t* dA, int64_t m, int64_t n, int64_t lda, uint32_t p,
+                   int64_t* rank, uint32_t* rrp, uint32_t* sigma, uint64_t* ops,
+                   void* stream);
+
+/* Batched CUP of `batch` independent m x n matrices stored contiguously
+ * (matrix t at dA + t*stride), device pointers; ranks[t] on the host.
+ * rrp (batch x min(m,n)) and sigma (batch x n) are host arrays or NULL. */
+int rl_cup_batched_u32_dev(uint32_t* dA, int64_t batch, int64_t m, int64_t n, int64_t stride,
+                           uint32_t p, int64_t* ranks, uint32_t* rrp, uint32_t* sigma,
+                           void* stream);
+
+/* C <- alpha*A*B + beta*C (mod p); A m x l, B l x n, C m x n.
+ * Replaces: void ranklab::mm(ConstMatView a, ConstMatView b, MatView c,
+ *           Elem alpha, Elem beta, OpCounter&)  proj/include/ranklab/kernels.hpp:26-27
+ *           (the library's declared substitution seam, kernels.hpp:13-19).
+ * RL_EOVERLAP when C overlaps A or B (kernels.cpp:38-39).  ops may be NULL. */
+int rl_mm_u32(const uint32_t* A, int64_t lda, const uint32_t* B, int64_t ldb, uint32_t* C,
+              int64_t ldc, int64_t m, int64_t l, int64_t n, uint32_t alpha, uint32_t beta,
+              uint32_t p, uint64_t* ops);
+int rl_mm_u32_dev(const uint32_t* dA, int64_t lda, const uint32_t* dB, int64_t ldb,
+                  uint32_t* dC, int64_t ldc, int64_t m, int64_t l, int64_t n, uint32_t alpha,
+                  uint32_t beta, uint32_t p, void* stream);
+
+/* Replaces: std::pair<size_t, std::vector<uint32_t>> ranklab::rank_and_profile(MatView,
+ *           OpCounter&)  proj/include/ranklab/solvers.hpp:13-14 (input consumed). */
+int rl_rank_and_profile_u32(uint32_t* A, int64_t m, int64_t n, int64_t lda, uint32_t p,
+                            int64_t* rank, uint32_t* rrp);
+
+/* Replaces: Elem ranklab::determinant(MatView, OpCounter&)  solvers.hpp:16
+ * (sign(P) * product of pivots; input consumed). */
+int rl_determinant_u32(uint32_t* A, int64_t n, int64_t lda, uint32_t p, uint32_t* det);
+
+/* Seeded inputs generated on the device, bit-identical to
+ * ranklab::random_matrix(m, n, seed, GF(p))  proj/src/reference.cpp:246-253. */
+int rl_random_matrix_u32_dev(uint32_t* dA, int64_t m, int64_t n, int64_t lda, uint64_t seed,
+                             uint32_t p, void* stream);
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* rl_last_error(void);
+
+/* Library version (major*10000 + minor*100 + patch). */
+int rl_version(void);
+
+/* Introspection for benchmarks: number of GEMM / tensor-core GEMM / panel /
+ * leaf-TRSM launches of the last CUP plan built for (m, n, lda, p), and its
+ * GEMM workspace in bytes.  stats[0..4]. */
+int rl_cup_plan_stats(int64_t m, int64_t n, int64_t lda, uint32_t p, int64_t* stats);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RANKLAB_GPU_H */

@@ -1,0 +1,297 @@
+"""paper_1112_5717_b200 -- B200-native CUP decomposition over GF(p).
+
+Host-side mirror of the reference's hot-path interface (``ranklab``,
+/root/reference/proj/include/ranklab) over the C ABI of ``libranklab_gpu.so``
+(``include/ranklab_gpu.h``).  Same names, argument meaning and error behaviour:
+
+=====================  =====================================================
+this module            reference
+=====================  =====================================================
+``cup``                ``PackedCup cup(MatView, OpCounter&)``  factor.hpp:34
+``mm``                 ``void mm(a, b, c, alpha, beta, OpCounter&)``  kernels.hpp:26
+``rank_and_profile``   ``rank_and_profile(MatView, OpCounter&)``  solvers.hpp:13
+``determinant``        ``Elem determinant(MatView, OpCounter&)``  solvers.hpp:16
+``PackedCup``          ``struct PackedCup``  factor.hpp:15-19
+``OpCounter``          ``struct OpCounter``  field.hpp:16-34
+errors                 ``errors.hpp:9-66`` (``Error`` and subclasses)
+=====================  =====================================================
+
+Matrices are numpy ``uint32`` arrays (row-major, like ``ranklab::Mat``), or
+device buffers given as ``torch`` tensors for the ``*_dev`` entry points.
+There is no CPU fallback: importing this package on a machine where the CUDA
+library cannot be loaded raises, and every compute call without a GPU returns
+``RL_ECUDA`` -> :class:`CudaError`.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+__all__ = [
+    "Error", "DimensionMismatch", "OverlapError", "SingularMatrix", "NotPrime", "CudaError",
+    "OpCounter", "PackedCup", "cup", "cup_dev", "cup_batched_dev", "mm", "mm_dev",
+    "rank_and_profile", "determinant", "random_matrix_dev", "LIB_PATH", "lib",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libranklab_gpu.so")
+
+
+# ----------------------------------------------------------------- errors
+class Error(RuntimeError):
+    """ranklab::Error (errors.hpp:9)."""
+
+
+class DimensionMismatch(Error):
+    pass
+
+
+class OverlapError(Error):
+    pass
+
+
+class SingularMatrix(Error):
+    pass
+
+
+class NotPrime(Error):
+    """NotPrime / ModulusOutOfRange (errors.hpp:14-24)."""
+
+
+class CudaError(Error):
+    pass
+
+
+class InvalidArgument(Error):
+    pass
+
+
+_STATUS = {1: DimensionMismatch, 2: OverlapError, 3: SingularMatrix, 4: NotPrime,
+           5: CudaError, 6: Error, 7: InvalidArgument, 8: CudaError}
+
+
+# ------------------------------------------------------------------ types
+@dataclass
+class OpCounter:
+    """Per-bucket field-op tallies (field.hpp:16-34)."""
+    n_mul: int = 0
+    n_addsub: int = 0
+    n_divinv: int = 0
+    n_ztest: int = 0
+
+    def arith_total(self) -> int:
+        return self.n_mul + self.n_addsub + self.n_divinv
+
+    def full_total(self) -> int:
+        return self.arith_total() + self.n_ztest
+
+    def _add(self, ops: np.ndarray) -> None:
+        self.n_mul += int(ops[0])
+        self.n_addsub += int(ops[1])
+        self.n_divinv += int(ops[2])
+        self.n_ztest += int(ops[3])
+
+
+@dataclass
+class PackedCup:
+    """Metadata of a packed [C\\U] factorization (factor.hpp:15-19)."""
+    rank: int = 0
+    row_profile: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint32))
+    col_perm: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint32))
+
+
+# ---------------------------------------------------------------- loading
+_lib = None
+_u32p = np.ctypeslib.ndpointer(dtype=np.uint32, flags="C_CONTIGUOUS")
+_u64p = np.ctypeslib.ndpointer(dtype=np.uint64, flags="C_CONTIGUOUS")
+_i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+_i64 = C.c_int64
+_u32 = C.c_uint32
+_vp = C.c_void_p
+
+#: every symbol include/ranklab_gpu.h declares
+EXPORTS = ["rl_cup_u32", "rl_cup_u32_dev", "rl_cup_batched_u32_dev", "rl_mm_u32",
+           "rl_mm_u32_dev", "rl_rank_and_profile_u32", "rl_determinant_u32",
+           "rl_random_matrix_u32_dev", "rl_last_error", "rl_version", "rl_cup_plan_stats"]
+
+
+def lib():
+    """Load libranklab_gpu.so (raises if it was not built -- no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(LIB_PATH)
+    L.rl_cup_u32.argtypes = [_vp, _i64, _i64, _i64, _u32, C.POINTER(_i64), _vp, _vp, _vp]
+    L.rl_cup_u32_dev.argtypes = [_vp, _i64, _i64, _i64, _u32, C.POINTER(_i64), _vp, _vp, _vp, _vp]
+    L.rl_cup_batched_u32_dev.argtypes = [_vp, _i64, _i64, _i64, _i64, _u32, _vp, _vp, _vp, _vp]
+    L.rl_mm_u32.argtypes = [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _u32, _u32, _u32, _vp]
+    L.rl_mm_u32_dev.argtypes = [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _u32, _u32, _u32,
+                                _vp]
+    L.rl_rank_and_profile_u32.argtypes = [_vp, _i64, _i64, _i64, _u32, C.POINTER(_i64), _vp]
+    L.rl_determinant_u32.argtypes = [_vp, _i64, _i64, _u32, C.POINTER(_u32)]
+    L.rl_random_matrix_u32_dev.argtypes = [_vp, _i64, _i64, _i64, C.c_uint64, _u32, _vp]
+    L.rl_last_error.restype = C.c_char_p
+    L.rl_cup_plan_stats.argtypes = [_i64, _i64, _i64, _u32, _vp]
+    _lib = L
+    return L
+
+
+def _check(code: int) -> None:
+    if code != 0:
+        msg = lib().rl_last_error().decode(errors="replace")
+        raise _STATUS.get(code, Error)(msg or f"status {code}")
+
+
+def _ptr(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _as_u32_matrix(a: np.ndarray) -> np.ndarray:
+    if not isinstance(a, np.ndarray) or a.dtype != np.uint32 or a.ndim != 2:
+        raise InvalidArgument("expected a 2-D numpy uint32 array")
+    if a.strides[1] != 4 or a.strides[0] % 4:
+        raise InvalidArgument("rows must be contiguous uint32")
+    return a
+
+
+def _ld(a: np.ndarray) -> int:
+    return max(a.strides[0] // 4, a.shape[1])
+
+
+# -------------------------------------------------------------------- API
+def cup(a: np.ndarray, p: int, ctr: OpCounter | None = None) -> PackedCup:
+    """In-place CUP of ``a`` over GF(p): ``a`` <- packed [C\\U], A = C*U*P.
+
+    Mirrors ``ranklab::cup`` (factor.hpp:30-34): any shape including empty,
+    rank deficiency is an output.  ``ctr`` receives the reference's exact
+    op counts.
+    """
+    a = _as_u32_matrix(a)
+    m, n = a.shape
+    rank = _i64(0)
+    rrp = np.zeros(max(1, min(m, n)), np.uint32)
+    sigma = np.zeros(max(1, n), np.uint32)
+    ops = np.zeros(4, np.uint64)
+    _check(lib().rl_cup_u32(_ptr(a), m, n, _ld(a), int(p), C.byref(rank), _ptr(rrp), _ptr(sigma),
+                            _ptr(ops)))
+    if ctr is not None:
+        ctr._add(ops)
+    r = rank.value
+    return PackedCup(r, rrp[:r].copy(), sigma[:n].copy())
+
+
+def cup_dev(d_a, m: int, n: int, p: int, lda: int | None = None, stream=None,
+            ctr: OpCounter | None = None, want_perm: bool = True) -> PackedCup:
+    """CUP of a device-resident matrix (``torch`` tensor or raw pointer)."""
+    ptr = d_a.data_ptr() if hasattr(d_a, "data_ptr") else int(d_a)
+    lda = n if lda is None else lda
+    rank = _i64(0)
+    rrp = np.zeros(max(1, min(m, n)), np.uint32)
+    sigma = np.zeros(max(1, n), np.uint32) if want_perm else None
+    ops = np.zeros(4, np.uint64) if ctr is not None else None
+    _check(lib().rl_cup_u32_dev(C.c_void_p(ptr), m, n, lda, int(p), C.byref(rank), _ptr(rrp),
+                                _ptr(sigma), _ptr(ops), _stream_ptr(stream)))
+    if ctr is not None:
+        ctr._add(ops)
+    r = rank.value
+    return PackedCup(r, rrp[:r].copy(), sigma[:n].copy() if want_perm else np.zeros(0, np.uint32))
+
+
+def cup_batched_dev(d_a, batch: int, m: int, n: int, p: int, stride: int | None = None,
+                    stream=None, want_meta: bool = True):
+    """Batched CUP of ``batch`` contiguous m x n device matrices.
+
+    Returns (ranks int64[batch], rrp uint32[batch, min(m,n)], sigma uint32[batch, n])
+    or None when ``want_meta`` is False (fully asynchronous)."""
+    ptr = d_a.data_ptr() if hasattr(d_a, "data_ptr") else int(d_a)
+    stride = m * n if stride is None else stride
+    k = max(1, min(m, n))
+    if want_meta:
+        ranks = np.zeros(batch, np.int64)
+        rrp = np.zeros((batch, k), np.uint32)
+        sigma = np.zeros((batch, max(n, 1)), np.uint32)
+        _check(lib().rl_cup_batched_u32_dev(C.c_void_p(ptr), batch, m, n, stride, int(p),
+                                            _ptr(ranks), _ptr(rrp), _ptr(sigma), _stream_ptr(stream)))
+        return ranks, rrp, sigma[:, :n]
+    _check(lib().rl_cup_batched_u32_dev(C.c_void_p(ptr), batch, m, n, stride, int(p), None, None,
+                                        None, _stream_ptr(stream)))
+    return None
+
+
+def mm(a: np.ndarray, b: np.ndarray, c: np.ndarray, alpha: int, beta: int, p: int,
+       ctr: OpCounter | None = None) -> None:
+    """C <- alpha*A*B + beta*C (mod p), the reference's mm seam (kernels.hpp:26-27)."""
+    a, b, c = _as_u32_matrix(a), _as_u32_matrix(b), _as_u32_matrix(c)
+    m, l = a.shape
+    if b.shape[0] != l or c.shape != (m, b.shape[1]):
+        raise DimensionMismatch(f"mm {a.shape} * {b.shape} -> {c.shape}")
+    n = b.shape[1]
+    ops = np.zeros(4, np.uint64)
+    _check(lib().rl_mm_u32(_ptr(a), _ld(a), _ptr(b), _ld(b), _ptr(c), _ld(c), m, l, n,
+                           int(alpha), int(beta), int(p), _ptr(ops)))
+    if ctr is not None:
+        ctr._add(ops)
+
+
+def mm_dev(d_a, d_b, d_c, m, l, n, alpha, beta, p, lda=None, ldb=None, ldc=None, stream=None):
+    pa = d_a.data_ptr() if hasattr(d_a, "data_ptr") else int(d_a)
+    pb = d_b.data_ptr() if hasattr(d_b, "data_ptr") else int(d_b)
+    pc = d_c.data_ptr() if hasattr(d_c, "data_ptr") else int(d_c)
+    _check(lib().rl_mm_u32_dev(C.c_void_p(pa), lda or l, C.c_void_p(pb), ldb or n, C.c_void_p(pc),
+                               ldc or n, m, l, n, int(alpha), int(beta), int(p),
+                               _stream_ptr(stream)))
+
+
+def rank_and_profile(a: np.ndarray, p: int):
+    """(rank, row rank profile); the input is consumed (solvers.hpp:13-14)."""
+    a = _as_u32_matrix(a)
+    m, n = a.shape
+    rank = _i64(0)
+    rrp = np.zeros(max(1, min(m, n)), np.uint32)
+    _check(lib().rl_rank_and_profile_u32(_ptr(a), m, n, _ld(a), int(p), C.byref(rank), _ptr(rrp)))
+    return rank.value, rrp[:rank.value].copy()
+
+
+def determinant(a: np.ndarray, p: int) -> int:
+    """sign(P) * product of pivots; the input is consumed (solvers.hpp:16)."""
+    a = _as_u32_matrix(a)
+    if a.shape[0] != a.shape[1]:
+        raise DimensionMismatch("determinant of non-square matrix")
+    d = _u32(0)
+    _check(lib().rl_determinant_u32(_ptr(a), a.shape[0], _ld(a), int(p), C.byref(d)))
+    return d.value
+
+
+def random_matrix_dev(d_a, m: int, n: int, seed: int, p: int, lda: int | None = None,
+                      stream=None) -> None:
+    """Device-side ranklab::random_matrix(m, n, seed, GF(p)) (reference.cpp:246-253)."""
+    ptr = d_a.data_ptr() if hasattr(d_a, "data_ptr") else int(d_a)
+    _check(lib().rl_random_matrix_u32_dev(C.c_void_p(ptr), m, n, lda or n,
+                                          C.c_uint64(seed & (2**64 - 1)), int(p),
+                                          _stream_ptr(stream)))
+
+
+def plan_stats(m: int, n: int, p: int, lda: int | None = None) -> dict:
+    st = np.zeros(5, np.int64)
+    _check(lib().rl_cup_plan_stats(m, n, lda or n, int(p), _ptr(st)))
+    return dict(gemms=int(st[0]), tc_gemms=int(st[1]), panels=int(st[2]), trsm_leaves=int(st[3]),
+                workspace_bytes=int(st[4]))
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        return None
+    if hasattr(stream, "cuda_stream"):
+        return C.c_void_p(stream.cuda_stream)
+    return C.c_void_p(int(stream))
+
+
+def model_ops(m: int, n: int, r: int) -> float:
+    """The reference's CUP cost model W(m,n,r) = 2mnr - (m+n)r^2 + (2/3)r^3
+    (proj/src/bench.cpp:12-13)."""
+    return 2.0 * m * n * r - (m + n) * r * r + (2.0 / 3.0) * r ** 3

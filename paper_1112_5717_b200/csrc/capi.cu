@@ -1,0 +1,464 @@
+// capi.cu -- the extern "C" boundary (include/ranklab_gpu.h).
+//
+// Maps the reference's C++ contracts onto plain pointers: validation and error
+// codes follow proj/include/ranklab/errors.hpp (DimensionMismatch, OverlapError,
+// SingularMatrix, NotPrime/ModulusOutOfRange), field validation follows
+// PrimeField (proj/src/field.cpp:24-58).  Engines (plans + workspaces + graphs)
+// are cached per (m, n, lda, p) behind a mutex; calls are re-entrant per stream.
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/ranklab_gpu.h"
+#include "cup.h"
+#include "kernels.cuh"
+#include "runtime.h"
+
+namespace rl {
+void cup_batched(u32* dA, i64 batch, i32 m, i32 n, i64 stride, u32 p, i32* d_ranks, i32* d_rrp,
+                 i32* d_ipiv, i32 kcap, cudaStream_t s);
+}
+
+using namespace rl;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+u64 mulmod_host(u64 a, u64 b, u64 m) { return (u64)((unsigned __int128)a * b % m); }
+u64 powmod_host(u64 a, u64 e, u64 m) {
+    u64 r = 1 % m;
+    a %= m;
+    while (e) {
+        if (e & 1) r = mulmod_host(r, a, m);
+        a = mulmod_host(a, a, m);
+        e >>= 1;
+    }
+    return r;
+}
+// Deterministic Miller-Rabin (the witness set decides all 64-bit inputs).
+bool is_prime(u64 n) {
+    if (n < 2) return false;
+    for (u64 q : {2ull, 3ull, 5ull, 7ull, 11ull, 13ull, 17ull, 19ull, 23ull, 29ull, 31ull, 37ull})
+        if (n % q == 0) return n == q;
+    u64 d = n - 1;
+    int s = 0;
+    while ((d & 1) == 0) {
+        d >>= 1;
+        ++s;
+    }
+    for (u64 a : {2ull, 3ull, 5ull, 7ull, 11ull, 13ull, 17ull, 19ull, 23ull, 29ull, 31ull, 37ull}) {
+        u64 x = powmod_host(a, d, n);
+        if (x == 1 || x == n - 1) continue;
+        bool comp = true;
+        for (int i = 1; i < s; ++i) {
+            x = mulmod_host(x, x, n);
+            if (x == n - 1) {
+                comp = false;
+                break;
+            }
+        }
+        if (comp) return false;
+    }
+    return true;
+}
+
+void check_field(u32 p) {
+    if (p < 2 || p >= (1u << 31)) throw Error(RL_EFIELD, "modulus outside [2, 2^31)");
+    if (!is_prime(p)) throw Error(RL_EFIELD, "modulus is not prime");
+}
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        g_last_error.clear();
+        return RL_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc& e) {
+        g_last_error = "host allocation failed";
+        return RL_ENOMEM;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return RL_EINVAL;
+    }
+}
+
+struct Key {
+    i64 m, n, lda;
+    u32 p;
+    bool operator<(const Key& o) const {
+        return std::tie(m, n, lda, p) < std::tie(o.m, o.n, o.lda, o.p);
+    }
+};
+
+std::mutex g_mu;
+std::map<Key, std::unique_ptr<CupEngine>> g_engines;
+
+CupEngine& engine_for(i64 m, i64 n, i64 lda, u32 p) {
+    Key k{m, n, lda, p};
+    auto it = g_engines.find(k);
+    if (it != g_engines.end()) return *it->second;
+    if (g_engines.size() > 16) g_engines.clear();
+    auto e = std::make_unique<CupEngine>((i32)m, (i32)n, lda, p);
+    CupEngine& ref = *e;
+    g_engines.emplace(k, std::move(e));
+    return ref;
+}
+
+// Device scratch buffers reused across host-pointer calls.
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t cap = 0;
+    void* get(size_t bytes) {
+        if (bytes > cap) {
+            if (ptr) cudaFree(ptr);
+            ptr = nullptr;
+            cap = 0;
+            if (cudaMalloc(&ptr, bytes) != cudaSuccess) throw Error(RL_ENOMEM, "cudaMalloc failed");
+            cap = bytes;
+        }
+        return ptr;
+    }
+};
+DevBuf g_bufA, g_bufB, g_bufC, g_bufI;
+
+void require_device() {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+        throw Error(RL_ECUDA, "no CUDA device (the GPU path has no CPU fallback)");
+}
+
+void check_dims(i64 m, i64 n, i64 ld) {
+    if (m < 0 || n < 0) throw Error(RL_EDIM, "negative dimension");
+    if (m > (1ll << 30) || n > (1ll << 30)) throw Error(RL_EDIM, "dimension too large");
+    if (n > 0 && ld < n) throw Error(RL_EINVAL, "leading dimension smaller than column count");
+}
+
+// Byte-range rectangle overlap of two row-major windows (ConstMatView::overlaps,
+// matrix.hpp:54-59, generalised to raw pointers).
+bool windows_overlap(const u32* a, i64 ar, i64 ac, i64 lda, const u32* c, i64 cr, i64 cc, i64 ldc) {
+    if (ar == 0 || ac == 0 || cr == 0 || cc == 0) return false;
+    const char* a0 = (const char*)a;
+    const char* a1 = (const char*)(a + (ar - 1) * lda + ac);
+    const char* c0 = (const char*)c;
+    const char* c1 = (const char*)(c + (cr - 1) * ldc + cc);
+    if (a1 <= c0 || c1 <= a0) return false;
+    if (lda != ldc) return true;  // conservative
+    const i64 off = (i64)(c - a);  // element offset of C's origin in A's frame
+    const i64 orow = off >= 0 ? off / lda : -((-off + lda - 1) / lda);
+    const i64 ocol = off - orow * lda;
+    // C occupies rows [orow, orow+cr), cols [ocol, ocol+cc) of A's frame
+    // (cols may spill past lda only if ocol + cc > lda: treat conservatively)
+    if (ocol + cc > lda) return true;
+    const bool row_hit = orow < ar && 0 < orow + cr;
+    const bool col_hit = ocol < ac && 0 < ocol + cc;
+    return row_hit && col_hit;
+}
+
+void cup_dev_impl(u32* dA, i64 m, i64 n, i64 lda, u32 p, i64* rank, u32* rrp, u32* sigma,
+                  u64* ops, cudaStream_t s) {
+    check_field(p);
+    check_dims(m, n, lda);
+    if (m == 0 || n == 0) {  // factor.cpp:32: rank 0, identity, storage untouched
+        if (rank) *rank = 0;
+        if (sigma) for (i64 j = 0; j < n; ++j) sigma[j] = (u32)j;
+        if (ops) std::fill(ops, ops + 4, 0ull);
+        return;
+    }
+    require_device();
+    i64 r = 0;
+    std::vector<u32> rrp_h((size_t)std::min(m, n)), ipiv_h((size_t)std::min(m, n));
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        CupEngine& e = engine_for(m, n, lda, p);
+        e.run(dA, s, /*use_graph=*/true);
+        e.results(&r, rrp_h.data(), ipiv_h.data(), s);
+    }
+    if (rank) *rank = r;
+    if (rrp) std::copy(rrp_h.begin(), rrp_h.begin() + r, rrp);
+    if (sigma) sigma_from_ipiv(n, r, ipiv_h.data(), sigma);
+    if (ops) cup_opcount(m, n, r, rrp_h.data(), ipiv_h.data(), ops);
+}
+
+void copy_h2d_2d(u32* d, i64 dld, const u32* h, i64 hld, i64 rows, i64 cols, cudaStream_t s) {
+    if (rows == 0 || cols == 0) return;
+    RL_CUDA_CHECK(cudaMemcpy2DAsync(d, dld * 4, h, hld * 4, cols * 4, rows, cudaMemcpyHostToDevice, s));
+}
+void copy_d2h_2d(u32* h, i64 hld, const u32* d, i64 dld, i64 rows, i64 cols, cudaStream_t s) {
+    if (rows == 0 || cols == 0) return;
+    RL_CUDA_CHECK(cudaMemcpy2DAsync(h, hld * 4, d, dld * 4, cols * 4, rows, cudaMemcpyDeviceToHost, s));
+}
+
+__global__ void scale_kernel(u32* C, i64 ldc, i64 m, i64 n, u32 beta, Fp f) {
+    const i64 total = m * n;
+    for (i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (i64)gridDim.x * blockDim.x) {
+        u32* c = C + (t / n) * ldc + (t % n);
+        *c = beta == 0 ? 0u : mulmod(*c, beta, f);
+    }
+}
+
+void mm_dev_impl(const u32* dA, i64 lda, const u32* dB, i64 ldb, u32* dC, i64 ldc, i64 m, i64 l,
+                 i64 n, u32 alpha, u32 beta, u32 p, cudaStream_t s) {
+    if (m == 0 || n == 0) return;
+    const Fp f = make_fp(p);
+    if (alpha == 0 || l == 0) {  // kernels.cpp:43-52: product short-circuited
+        if (beta == 1 % p) return;
+        scale_kernel<<<(int)std::min<i64>((m * n + 255) / 256, 4096), 256, 0, s>>>(dC, ldc, m, n,
+                                                                                beta, f);
+        RL_CUDA_CHECK(cudaGetLastError());
+        return;
+    }
+    const int L = limbs_for(p);
+    const i64 kmax = tc_kmax(L);
+    // Chunk K so every s32 accumulator stays exact; later chunks accumulate (beta = 1).
+    for (i64 k0 = 0; k0 < l; k0 += kmax) {
+        const i64 kc = std::min(kmax, l - k0);
+        GemmArgs g{};
+        g.A = dA + k0;
+        g.lda = lda;
+        g.a_row0 = 0;
+        g.B = dB + k0 * ldb;
+        g.ldb = ldb;
+        g.gather = nullptr;
+        g.C = dC;
+        g.ldc = ldc;
+        g.c_row0 = 0;
+        g.M = (i32)m;
+        g.k_lo = dyn_c(0);
+        g.k_hi = dyn_c((i32)kc);
+        g.n_lo = dyn_c(0);
+        g.n_hi = dyn_c((i32)n);
+        g.rp = nullptr;
+        g.alpha = alpha;
+        g.beta = k0 == 0 ? beta : 1 % p;
+        g.f = f;
+        const bool tc = kc >= 32 && n >= 32 && m >= 32;
+        if (tc) {
+            static DevBuf a2, b2;
+            uint8_t* pa = (uint8_t*)a2.get(tc_a2_bytes(L, m, kc));
+            uint8_t* pb = (uint8_t*)b2.get(tc_b2_bytes(L, n, kc));
+            gemm_tc(g, L, kc, n, pa, pb, s);
+        } else {
+            gemm_simt(g, kc, n, s);
+        }
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int rl_version(void) { return 100; }
+
+const char* rl_last_error(void) { return g_last_error.c_str(); }
+
+int rl_cup_u32_dev(uint32_t* dA, int64_t m, int64_t n, int64_t lda, uint32_t p, int64_t* rank,
+                   uint32_t* rrp, uint32_t* sigma, uint64_t* ops, void* stream) {
+    return guard([&] {
+        if (!dA && m * n > 0) throw Error(RL_EINVAL, "null matrix");
+        cup_dev_impl(dA, m, n, lda, p, rank, rrp, sigma, ops, (cudaStream_t)stream);
+    });
+}
+
+int rl_cup_u32(uint32_t* A, int64_t m, int64_t n, int64_t lda, uint32_t p, int64_t* rank,
+               uint32_t* rrp, uint32_t* sigma, uint64_t* ops) {
+    return guard([&] {
+        if (!A && m * n > 0) throw Error(RL_EINVAL, "null matrix");
+        check_field(p);
+        check_dims(m, n, lda);
+        if (m == 0 || n == 0) {
+            cup_dev_impl(nullptr, m, n, lda, p, rank, rrp, sigma, ops, nullptr);
+            return;
+        }
+        require_device();
+        std::lock_guard<std::mutex> lk(g_mu);
+        cudaStream_t s = cudaStreamPerThread;
+        u32* dA = (u32*)g_bufA.get((size_t)m * n * 4);
+        copy_h2d_2d(dA, n, A, lda, m, n, s);
+        i64 r = 0;
+        std::vector<u32> rrp_h((size_t)std::min(m, n)), ipiv_h((size_t)std::min(m, n));
+        CupEngine& e = engine_for(m, n, n, p);
+        e.run(dA, s, true);
+        copy_d2h_2d(A, lda, dA, n, m, n, s);
+        e.results(&r, rrp_h.data(), ipiv_h.data(), s);  // synchronises s
+        if (rank) *rank = r;
+        if (rrp) std::copy(rrp_h.begin(), rrp_h.begin() + r, rrp);
+        if (sigma) sigma_from_ipiv(n, r, ipiv_h.data(), sigma);
+        if (ops) cup_opcount(m, n, r, rrp_h.data(), ipiv_h.data(), ops);
+    });
+}
+
+int rl_rank_and_profile_u32(uint32_t* A, int64_t m, int64_t n, int64_t lda, uint32_t p,
+                            int64_t* rank, uint32_t* rrp) {
+    return rl_cup_u32(A, m, n, lda, p, rank, rrp, nullptr, nullptr);
+}
+
+int rl_determinant_u32(uint32_t* A, int64_t n, int64_t lda, uint32_t p, uint32_t* det) {
+    return guard([&] {
+        check_field(p);
+        check_dims(n, n, lda);
+        if (!det) throw Error(RL_EINVAL, "null det");
+        std::vector<u32> sigma((size_t)n);
+        i64 r = 0;
+        int st = rl_cup_u32(A, n, n, lda, p, &r, nullptr, sigma.data(), nullptr);
+        if (st != RL_OK) throw Error(st, g_last_error);
+        if (r < n) {
+            *det = 0;
+            return;
+        }
+        if (n == 0) {
+            *det = 1 % p;
+            return;
+        }
+        u64 d = A[0];
+        for (i64 j = 1; j < n; ++j) d = d * A[j * lda + j] % p;  // solvers.cpp:18-19
+        // sign of sigma by cycle decomposition (perm.cpp:50-63)
+        std::vector<uint8_t> seen((size_t)n, 0);
+        i64 transp = 0;
+        for (i64 s0 = 0; s0 < n; ++s0) {
+            if (seen[s0]) continue;
+            i64 len = 0;
+            for (i64 j = s0; !seen[j]; j = sigma[j]) {
+                seen[j] = 1;
+                ++len;
+            }
+            transp += len - 1;
+        }
+        if (transp % 2) d = d == 0 ? 0 : p - d;
+        *det = (u32)d;
+    });
+}
+
+int rl_mm_u32_dev(const uint32_t* dA, int64_t lda, const uint32_t* dB, int64_t ldb, uint32_t* dC,
+                  int64_t ldc, int64_t m, int64_t l, int64_t n, uint32_t alpha, uint32_t beta,
+                  uint32_t p, void* stream) {
+    return guard([&] {
+        check_field(p);
+        if (m < 0 || l < 0 || n < 0) throw Error(RL_EDIM, "negative dimension");
+        if (alpha >= p || beta >= p) throw Error(RL_EINVAL, "alpha/beta not canonical");
+        require_device();
+        std::lock_guard<std::mutex> lk(g_mu);
+        mm_dev_impl(dA, lda, dB, ldb, dC, ldc, m, l, n, alpha, beta, p, (cudaStream_t)stream);
+    });
+}
+
+int rl_mm_u32(const uint32_t* A, int64_t lda, const uint32_t* B, int64_t ldb, uint32_t* C,
+              int64_t ldc, int64_t m, int64_t l, int64_t n, uint32_t alpha, uint32_t beta,
+              uint32_t p, uint64_t* ops) {
+    return guard([&] {
+        check_field(p);
+        if (m < 0 || l < 0 || n < 0) throw Error(RL_EDIM, "negative dimension");
+        if (alpha >= p || beta >= p) throw Error(RL_EINVAL, "alpha/beta not canonical");
+        if (windows_overlap(A, m, l, lda, C, m, n, ldc)) throw Error(RL_EOVERLAP, "mm: C overlaps A");
+        if (windows_overlap(B, l, n, ldb, C, m, n, ldc)) throw Error(RL_EOVERLAP, "mm: C overlaps B");
+        if (ops) {  // exact charges of kernels.cpp:41-74
+            std::fill(ops, ops + 4, 0ull);
+            const u64 e = (u64)m * (u64)n;
+            const u32 one = 1 % p, neg = p - 1;
+            if (alpha == 0 || l == 0) {
+                if (beta != 0 && beta != one) ops[0] += e;
+            } else {
+                ops[0] += e * (u64)l;
+                ops[1] += e * (u64)(l - 1);
+                if (alpha != one && alpha != neg) ops[0] += e;
+                if (beta == 0) {
+                    if (alpha == neg && alpha != one) ops[1] += e;
+                } else if (beta == one) {
+                    ops[1] += e;
+                } else {
+                    ops[0] += e;
+                    ops[1] += e;
+                }
+            }
+        }
+        if (m == 0 || n == 0) return;
+        require_device();
+        std::lock_guard<std::mutex> lk(g_mu);
+        cudaStream_t s = cudaStreamPerThread;
+        u32* dA = (u32*)g_bufA.get((size_t)std::max<i64>(m * l, 1) * 4);
+        u32* dB = (u32*)g_bufB.get((size_t)std::max<i64>(l * n, 1) * 4);
+        u32* dC = (u32*)g_bufC.get((size_t)m * n * 4);
+        copy_h2d_2d(dA, l, A, lda, m, l, s);
+        copy_h2d_2d(dB, n, B, ldb, l, n, s);
+        copy_h2d_2d(dC, n, C, ldc, m, n, s);
+        mm_dev_impl(dA, l, dB, n, dC, n, m, l, n, alpha, beta, p, s);
+        copy_d2h_2d(C, ldc, dC, n, m, n, s);
+        RL_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int rl_random_matrix_u32_dev(uint32_t* dA, int64_t m, int64_t n, int64_t lda, uint64_t seed,
+                             uint32_t p, void* stream) {
+    return guard([&] {
+        check_field(p);
+        check_dims(m, n, lda);
+        require_device();
+        gen_random_matrix(dA, lda, m, n, seed, p, (cudaStream_t)stream);
+    });
+}
+
+int rl_cup_batched_u32_dev(uint32_t* dA, int64_t batch, int64_t m, int64_t n, int64_t stride,
+                           uint32_t p, int64_t* ranks, uint32_t* rrp, uint32_t* sigma,
+                           void* stream) {
+    return guard([&] {
+        check_field(p);
+        check_dims(m, n, n);
+        if (batch < 0) throw Error(RL_EDIM, "negative batch");
+        if (stride < m * n) throw Error(RL_EINVAL, "stride smaller than m*n");
+        const i64 kcap = std::max<i64>(1, std::min(m, n));
+        if (batch == 0) return;
+        if (m == 0 || n == 0) {
+            for (i64 t = 0; t < batch; ++t) {
+                if (ranks) ranks[t] = 0;
+                if (sigma) for (i64 j = 0; j < n; ++j) sigma[t * n + j] = (u32)j;
+            }
+            return;
+        }
+        require_device();
+        std::lock_guard<std::mutex> lk(g_mu);
+        cudaStream_t s = (cudaStream_t)stream;
+        i32* dmeta = (i32*)g_bufI.get((size_t)batch * (1 + 2 * kcap) * 4);
+        i32* d_ranks = dmeta;
+        i32* d_rrp = dmeta + batch;
+        i32* d_ipiv = d_rrp + batch * kcap;
+        cup_batched(dA, batch, (i32)m, (i32)n, stride, p, d_ranks, d_rrp, d_ipiv, (i32)kcap, s);
+        if (!ranks && !rrp && !sigma) return;  // stays asynchronous
+        std::vector<i32> h((size_t)batch * (1 + 2 * kcap));
+        RL_CUDA_CHECK(cudaMemcpyAsync(h.data(), dmeta, h.size() * 4, cudaMemcpyDeviceToHost, s));
+        RL_CUDA_CHECK(cudaStreamSynchronize(s));
+        for (i64 t = 0; t < batch; ++t) {
+            const i64 r = h[t];
+            if (ranks) ranks[t] = r;
+            const u32* rp_t = (const u32*)&h[batch + t * kcap];
+            const u32* ip_t = (const u32*)&h[batch + batch * kcap + t * kcap];
+            if (rrp) for (i64 j = 0; j < r; ++j) rrp[t * kcap + j] = rp_t[j];
+            if (sigma) sigma_from_ipiv(n, r, ip_t, sigma + t * n);
+        }
+    });
+}
+
+int rl_cup_plan_stats(int64_t m, int64_t n, int64_t lda, uint32_t p, int64_t* stats) {
+    return guard([&] {
+        check_field(p);
+        check_dims(m, n, lda);
+        std::lock_guard<std::mutex> lk(g_mu);
+        CupEngine& e = engine_for(m, n, lda, p);
+        const auto& st = e.stats();
+        stats[0] = st.gemms;
+        stats[1] = st.tc_gemms;
+        stats[2] = st.panels;
+        stats[3] = st.trsm_leaves;
+        stats[4] = (int64_t)e.workspace_bytes();
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,90 @@
+// common.cuh -- shared device helpers for the B200 CUP library.
+//
+// Field arithmetic follows ranklab::PrimeField (proj/include/ranklab/field.hpp:45-107):
+// elements are canonical uint32 in [0,p), 2 <= p < 2^31.  Reduction of 64-bit
+// intermediates uses a Barrett constant m64 = floor((2^64-1)/p): q = hi64(x*m64)
+// underestimates floor(x/p) by at most 1, so one conditional subtract yields the
+// canonical remainder for every x < 2^64.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+typedef uint32_t u32;
+typedef uint64_t u64;
+typedef int32_t i32;
+typedef int64_t i64;
+
+struct Fp {
+    u32 p;
+    u32 m32;  // floor((2^32-1)/p): 32-bit Barrett for x < 2^32
+    u64 m64;  // floor((2^64-1)/p)
+};
+
+static inline Fp make_fp(u32 p) {
+    Fp f;
+    f.p = p;
+    f.m32 = (u32)(0xFFFFFFFFu / p);
+    f.m64 = ~0ull / (u64)p;
+    return f;
+}
+
+__device__ __forceinline__ u32 red64(u64 x, const Fp& f) {
+    u64 q = __umul64hi(x, f.m64);
+    u64 r = x - q * (u64)f.p;
+    return (u32)(r >= f.p ? r - f.p : r);
+}
+
+// x < 2^32
+__device__ __forceinline__ u32 red32(u32 x, const Fp& f) {
+    u32 q = __umulhi(x, f.m32);
+    u32 r = x - q * f.p;
+    return r >= f.p ? r - f.p : r;
+}
+
+__device__ __forceinline__ u32 mulmod(u32 a, u32 b, const Fp& f) {
+    return red64((u64)a * b, f);
+}
+
+__device__ __forceinline__ u32 addmod(u32 a, u32 b, const Fp& f) {
+    u32 s = a + b;  // a,b < 2^31 so no wrap
+    return s >= f.p ? s - f.p : s;
+}
+
+__device__ __forceinline__ u32 submod(u32 a, u32 b, const Fp& f) {
+    return a >= b ? a - b : a + (f.p - b);
+}
+
+__device__ __forceinline__ u32 negmod(u32 a, const Fp& f) { return a == 0 ? 0 : f.p - a; }
+
+// Modular inverse of a != 0 by Fermat (p prime).  Any inverse algorithm yields
+// the same element (field.cpp:60-76 uses extended Euclid).
+__device__ __forceinline__ u32 invmod(u32 a, const Fp& f) {
+    u32 r = 1 % f.p, b = a, e = f.p - 2;
+    while (e) {
+        if (e & 1) r = mulmod(r, b, f);
+        b = mulmod(b, b, f);
+        e >>= 1;
+    }
+    return r;
+}
+
+// A device-evaluated index: value = (idx >= 0 ? rp[idx] : 0) + cst.  All
+// rank-dependent shapes of the CUP recursion are expressed this way, so the
+// whole launch sequence is static (graph-capturable) while the sizes come from
+// the device-resident rank prefix rp[i] = rank of rows [0, i).
+struct Dyn {
+    i32 idx;
+    i32 cst;
+};
+__host__ __device__ inline Dyn dyn_c(i32 c) { return Dyn{-1, c}; }
+__host__ __device__ inline Dyn dyn_rp(i32 i, i32 c = 0) { return Dyn{i, c}; }
+
+__device__ __forceinline__ i32 dyn_eval(const Dyn& d, const i32* rp) {
+    return (d.idx >= 0 ? __ldcg(rp + d.idx) : 0) + d.cst;
+}
+
+#define RL_CUDA_CHECK(x)                                                  \
+    do {                                                                  \
+        cudaError_t _e = (x);                                             \
+        if (_e != cudaSuccess) throw rl::CudaError(_e, #x, __FILE__, __LINE__); \
+    } while (0)

@@ -1,0 +1,325 @@
+// cup.cu -- host driver of the device-resident CUP recursion.
+//
+// Follows the reference's row-halving recursion cup_rec (proj/src/factor.cpp:30-81)
+// with the same split k = m/2 down to leaves of <= PB rows, but every
+// rank-dependent extent (r1, column origins, widths) is a Dyn expression over
+// the device-resident rank prefix rp[]: the host walks a STATIC skeleton and
+// enqueues kernels without ever reading a rank back, so one factorization is a
+// single host-sync-free launch sequence (captured once into a CUDA graph and
+// replayed).  Deviations from the reference's data movement, all value-neutral:
+//   * U rows are not shifted up at every level (factor.cpp:62-70); they stay in
+//     their pivot rows and are gathered through rrp[] when used as the B
+//     operand, then placed once at the end (compact_u_rows).
+//   * sigma is kept as the transposition list ipiv[] (perm.cpp:21-26) and
+//     composed on the host at the end (factor.cpp:78-79).
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+#include <vector>
+
+#include "cup.h"
+#include "kernels.cuh"
+#include "runtime.h"
+
+namespace rl {
+
+int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        RL_CUDA_CHECK(cudaGetDevice(&dev));
+        RL_CUDA_CHECK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return n;
+}
+
+CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_(p) {
+    f_ = make_fp(p);
+    L_ = limbs_for(p);
+    // dry run to size the GEMM workspaces
+    dry_ = true;
+    if (m_ > 0 && n_ > 0) node(0, m_);
+    dry_ = false;
+    const i32 k = std::min(m_, n_);
+    RL_CUDA_CHECK(cudaMalloc(&rp_, sizeof(i32) * (m_ + 1)));
+    RL_CUDA_CHECK(cudaMalloc(&rrp_, sizeof(i32) * (k + 1)));
+    RL_CUDA_CHECK(cudaMalloc(&ipiv_, sizeof(i32) * (k + 1)));
+    RL_CUDA_CHECK(cudaMalloc(&ps_, sizeof(PanelScratch)));
+    RL_CUDA_CHECK(cudaMemset(ps_, 0, sizeof(PanelScratch)));
+    if (a2_cap_) RL_CUDA_CHECK(cudaMalloc(&a2_, a2_cap_));
+    if (b2_cap_) RL_CUDA_CHECK(cudaMalloc(&b2_, b2_cap_));
+}
+
+CupEngine::~CupEngine() {
+    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+    cudaFree(rp_);
+    cudaFree(rrp_);
+    cudaFree(ipiv_);
+    cudaFree(ps_);
+    cudaFree(a2_);
+    cudaFree(b2_);
+}
+
+void CupEngine::gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nmax) {
+    // K = pivots of rows [x0, x1) = [rp[x0], rp[x1]); split along the skeleton
+    // while the s32 exactness bound could be exceeded.
+    const i64 Kmax = x1 - x0;
+    if (Kmax <= 0 || M <= 0 || Nmax <= 0) return;
+    if (Kmax > tc_kmax(L_)) {
+        const i32 xm = x0 + (x1 - x0) / 2;
+        gemm(row0, M, x0, xm, n_lo, n_hi, Nmax);
+        gemm(row0, M, xm, x1, n_lo, n_hi, Nmax);
+        return;
+    }
+    GemmArgs g{};
+    g.A = A_;
+    g.lda = lda_;
+    g.a_row0 = row0;
+    g.B = A_;
+    g.ldb = lda_;
+    g.gather = rrp_;
+    g.C = A_;
+    g.ldc = lda_;
+    g.c_row0 = row0;
+    g.M = M;
+    g.k_lo = dyn_rp(x0);
+    g.k_hi = dyn_rp(x1);
+    g.n_lo = n_lo;
+    g.n_hi = n_hi;
+    g.rp = rp_;
+    g.alpha = p_ - 1;  // C <- C - A*B  (mm(..., neg_one, one), factor.cpp:51)
+    g.beta = 1 % p_;
+    g.f = f_;
+    const bool tc = use_tc_ && Kmax >= 64 && Nmax >= 64 && M >= 64;
+    if (dry_) {
+        if (tc) {
+            a2_cap_ = std::max(a2_cap_, tc_a2_bytes(L_, M, Kmax));
+            b2_cap_ = std::max(b2_cap_, tc_b2_bytes(L_, Nmax, Kmax));
+        }
+        return;
+    }
+    ++stats_.gemms;
+    if (tc) {
+        ++stats_.tc_gemms;
+        gemm_tc(g, L_, Kmax, Nmax, a2_, b2_, s_);
+    } else {
+        gemm_simt(g, Kmax, Nmax, s_);
+    }
+}
+
+void CupEngine::panel(i32 i0, i32 b) {
+    if (dry_) return;
+    PanelArgs a{};
+    a.A = A_;
+    a.lda = lda_;
+    a.i0 = i0;
+    a.b = b;
+    a.N = n_;
+    a.rp = rp_;
+    a.rrp = rrp_;
+    a.ipiv = ipiv_;
+    a.ps = ps_;
+    a.f = f_;
+    panel_window(a, s_);
+    panel_tail(a, s_);
+    stats_.panels++;
+}
+
+void CupEngine::swaps_range(i32 row0, i32 M, Dyn j_lo, Dyn j_hi) {
+    if (dry_ || M <= 0) return;
+    SwapArgs a{};
+    a.A = A_;
+    a.lda = lda_;
+    a.row0 = row0;
+    a.M = M;
+    a.gather = nullptr;
+    a.j_lo = j_lo;
+    a.j_hi = j_hi;
+    a.rp = rp_;
+    a.ipiv = ipiv_;
+    a.Mmax = M;
+    apply_swaps(a, s_);
+}
+
+void CupEngine::swaps_gather(Dyn g_lo, Dyn g_hi, i32 Mmax, Dyn j_lo, Dyn j_hi) {
+    if (dry_ || Mmax <= 0) return;
+    SwapArgs a{};
+    a.A = A_;
+    a.lda = lda_;
+    a.gather = rrp_;
+    a.g_lo = g_lo;
+    a.g_hi = g_hi;
+    a.j_lo = j_lo;
+    a.j_hi = j_hi;
+    a.rp = rp_;
+    a.ipiv = ipiv_;
+    a.Mmax = Mmax;
+    apply_swaps(a, s_);
+}
+
+// G <- G * U_X^{-1} for the unit upper block of node X = rows [x0, x0+mx)
+// (trsm Right/Upper/Unit, kernels.cpp:149-154, recursing along X's own skeleton).
+void CupEngine::trsm_right(i32 r0, i32 M, i32 x0, i32 mx) {
+    if (mx <= PB) {
+        if (dry_) return;
+        TrsmLeafArgs a{};
+        a.A = A_;
+        a.lda = lda_;
+        a.row0 = r0;
+        a.M = M;
+        a.j_lo = dyn_rp(x0);
+        a.j_hi = dyn_rp(x0 + mx);
+        a.rp = rp_;
+        a.rrp = rrp_;
+        a.f = f_;
+        trsm_leaf(a, s_);
+        stats_.trsm_leaves++;
+        return;
+    }
+    const i32 kx = mx / 2;
+    trsm_right(r0, M, x0, kx);
+    gemm(r0, M, x0, x0 + kx, dyn_rp(x0 + kx), dyn_rp(x0 + mx), mx - kx);
+    trsm_right(r0, M, x0 + kx, mx - kx);
+}
+
+void CupEngine::node(i32 i0, i32 mm) {
+    if (mm <= PB) {
+        panel(i0, mm);
+        return;
+    }
+    const i32 k = mm / 2;                    // factor.cpp:35
+    node(i0, k);                             // factor.cpp:39
+    const i32 b0 = i0 + k, bm = mm - k;
+    swaps_range(b0, bm, dyn_rp(i0), dyn_rp(b0));                     // factor.cpp:42
+    trsm_right(b0, bm, i0, k);                                        // factor.cpp:45-46
+    gemm(b0, bm, i0, b0, dyn_rp(b0), dyn_c(n_), n_);                  // factor.cpp:51-52
+    node(b0, bm);                                                     // factor.cpp:53
+    swaps_gather(dyn_rp(i0), dyn_rp(b0), k, dyn_rp(b0), dyn_rp(i0 + mm));  // factor.cpp:56
+}
+
+void CupEngine::enqueue(u32* dA, cudaStream_t s) {
+    A_ = dA;
+    s_ = s;
+    stats_ = Stats{};
+    fill_rp0(rp_, s);
+    if (m_ > 0 && n_ > 0) {
+        node(0, m_);
+        compact_u_rows(A_, lda_, m_, n_, rp_, rrp_, s);
+    }
+}
+
+void CupEngine::run(u32* dA, cudaStream_t s, bool use_graph) {
+    if (!use_graph) {
+        enqueue(dA, s);
+        return;
+    }
+    if (!graph_exec_ || graph_A_ != dA) {
+        if (graph_exec_) {
+            cudaGraphExecDestroy(graph_exec_);
+            graph_exec_ = nullptr;
+        }
+        cudaStream_t cs;
+        RL_CUDA_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        cudaGraph_t graph;
+        RL_CUDA_CHECK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        try {
+            enqueue(dA, cs);
+        } catch (...) {
+            cudaStreamEndCapture(cs, &graph);
+            cudaStreamDestroy(cs);
+            throw;
+        }
+        RL_CUDA_CHECK(cudaStreamEndCapture(cs, &graph));
+        RL_CUDA_CHECK(cudaGraphInstantiate(&graph_exec_, graph, 0));
+        RL_CUDA_CHECK(cudaGraphDestroy(graph));
+        RL_CUDA_CHECK(cudaStreamDestroy(cs));
+        graph_A_ = dA;
+    }
+    RL_CUDA_CHECK(cudaGraphLaunch(graph_exec_, s));
+}
+
+void CupEngine::results(i64* rank, u32* rrp_host, u32* ipiv_host, cudaStream_t s) {
+    i32 r = 0;
+    if (m_ > 0 && n_ > 0) {
+        RL_CUDA_CHECK(cudaMemcpyAsync(&r, rp_ + m_, sizeof(i32), cudaMemcpyDeviceToHost, s));
+        RL_CUDA_CHECK(cudaStreamSynchronize(s));
+    }
+    *rank = r;
+    if (r > 0) {
+        if (rrp_host)
+            RL_CUDA_CHECK(cudaMemcpyAsync(rrp_host, rrp_, sizeof(i32) * r, cudaMemcpyDeviceToHost, s));
+        if (ipiv_host)
+            RL_CUDA_CHECK(cudaMemcpyAsync(ipiv_host, ipiv_, sizeof(i32) * r, cudaMemcpyDeviceToHost, s));
+        RL_CUDA_CHECK(cudaStreamSynchronize(s));
+    }
+}
+
+// sigma = identity, then swap(sigma[j], sigma[ipiv[j]]) for j = 0..r-1: the
+// composition perm_compose(P2.embed_at(r1,n), P1) of factor.cpp:78-79 unrolled
+// over the recursion (perm.cpp:41-79).
+void sigma_from_ipiv(i64 n, i64 r, const u32* ipiv, u32* sigma) {
+    for (i64 j = 0; j < n; ++j) sigma[j] = (u32)j;
+    for (i64 j = 0; j < r; ++j) std::swap(sigma[j], sigma[ipiv[j]]);
+}
+
+// Exact OpCounter of the reference cup (field.hpp:16-34) without counting on
+// the device: the charges are a pure function of the row-halving skeleton, the
+// row profile and the pivot positions.
+//   node of R=m-k bottom rows, width w, top rank r1:
+//     trsm Right/Upper/Unit: R*r1(r1-1)/2 mul and as many add/sub (kernels.cpp:92-101, 149-154)
+//     if r1 < w: Schur mm: R*(w-r1)*r1 mul and as many add/sub (kernels.cpp:54-68)
+//     if r1 == w: early return (factor.cpp:47)
+//   leaf row (factor.cpp:12-28): pivot j -> (ipiv[j]-j+1) ztest, 1 inv, (w-1) mul;
+//     no pivot -> w ztest.
+namespace {
+struct OpWalk {
+    const std::vector<i64>& rpre;  // rank prefix by row
+    const u32* ipiv;
+    u64 mul = 0, addsub = 0, divinv = 0, ztest = 0;
+    void walk(i64 i0, i64 m, i64 w) {
+        if (m == 0 || w == 0) return;
+        if (m == 1) {
+            const i64 j = rpre[i0];
+            if (rpre[i0 + 1] > j) {
+                ztest += (u64)(ipiv[j] - j + 1);
+                divinv += 1;
+                mul += (u64)(w - 1);
+            } else {
+                ztest += (u64)w;
+            }
+            return;
+        }
+        const i64 k = m / 2;
+        walk(i0, k, w);
+        const i64 r1 = rpre[i0 + k] - rpre[i0];
+        const i64 R = m - k;
+        const u64 t = (u64)R * (u64)r1 * (u64)(r1 > 0 ? r1 - 1 : 0) / 2;
+        mul += t;
+        addsub += t;
+        if (r1 == w) return;
+        const u64 s = (u64)R * (u64)(w - r1) * (u64)r1;
+        mul += s;
+        addsub += s;
+        walk(i0 + k, m - k, w - r1);
+    }
+};
+}  // namespace
+
+void cup_opcount(i64 m, i64 n, i64 r, const u32* rrp, const u32* ipiv, u64 ops[4]) {
+    std::vector<i64> rpre(m + 1, 0);
+    i64 j = 0;
+    for (i64 i = 0; i < m; ++i) {
+        rpre[i] = j;
+        if (j < r && (i64)rrp[j] == i) ++j;
+    }
+    rpre[m] = j;
+    OpWalk w{rpre, ipiv};
+    w.walk(0, m, n);
+    ops[0] = w.mul;
+    ops[1] = w.addsub;
+    ops[2] = w.divinv;
+    ops[3] = w.ztest;
+}
+
+}  // namespace rl

@@ -1,0 +1,70 @@
+// cup.h -- the device-resident CUP engine (host side).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace rl {
+
+struct PanelScratch;
+
+class CupEngine {
+public:
+    struct Stats {
+        long gemms = 0, tc_gemms = 0, panels = 0, trsm_leaves = 0;
+    };
+
+    CupEngine(i32 m, i32 n, i64 lda, u32 p);
+    ~CupEngine();
+    CupEngine(const CupEngine&) = delete;
+    CupEngine& operator=(const CupEngine&) = delete;
+
+    // Enqueue the full factorization of the device matrix dA (m x n, lda) on s.
+    // With use_graph the launch sequence is captured once per dA and replayed.
+    void run(u32* dA, cudaStream_t s, bool use_graph);
+    // rank (sync), then row profile / pivot positions (int32 on device) to host.
+    void results(i64* rank, u32* rrp_host, u32* ipiv_host, cudaStream_t s);
+
+    const Stats& stats() const { return stats_; }
+    i32 m() const { return m_; }
+    i32 n() const { return n_; }
+    i64 lda() const { return lda_; }
+    u32 p() const { return p_; }
+    int limbs() const { return L_; }
+    size_t workspace_bytes() const { return a2_cap_ + b2_cap_; }
+    void set_use_tc(bool v) { use_tc_ = v; }
+
+private:
+    void enqueue(u32* dA, cudaStream_t s);
+    void node(i32 i0, i32 m);
+    void panel(i32 i0, i32 b);
+    void trsm_right(i32 r0, i32 M, i32 x0, i32 mx);
+    void gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nmax);
+    void swaps_range(i32 row0, i32 M, Dyn j_lo, Dyn j_hi);
+    void swaps_gather(Dyn g_lo, Dyn g_hi, i32 Mmax, Dyn j_lo, Dyn j_hi);
+
+    i32 m_, n_;
+    i64 lda_;
+    u32 p_;
+    Fp f_;
+    int L_;
+    bool dry_ = false;
+    bool use_tc_ = true;
+    u32* A_ = nullptr;
+    cudaStream_t s_ = nullptr;
+    i32* rp_ = nullptr;
+    i32* rrp_ = nullptr;
+    i32* ipiv_ = nullptr;
+    PanelScratch* ps_ = nullptr;
+    uint8_t* a2_ = nullptr;
+    uint8_t* b2_ = nullptr;
+    size_t a2_cap_ = 0, b2_cap_ = 0;
+    cudaGraphExec_t graph_exec_ = nullptr;
+    u32* graph_A_ = nullptr;
+    Stats stats_;
+};
+
+void sigma_from_ipiv(i64 n, i64 r, const u32* ipiv, u32* sigma);
+void cup_opcount(i64 m, i64 n, i64 r, const u32* rrp, const u32* ipiv, u64 ops[4]);
+
+}  // namespace rl

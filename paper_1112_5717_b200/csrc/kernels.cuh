@@ -1,0 +1,132 @@
+// kernels.cuh -- argument blocks and launchers of every device kernel of the
+// CUP path.  All rank-dependent extents are Dyn expressions over the
+// device-resident rank prefix rp[], so launches never need a host sync.
+#pragma once
+#include "common.cuh"
+
+namespace rl {
+
+// ----------------------------------------------------------------------- GEMM
+// C(r, n) <- beta*C(r, n) + alpha * sum_k A(r, k) * B(k, n)   (mod p)
+//   A(r, k) = A[(a_row0 + r) * lda + k_lo + k]
+//   B(k, n) = B[g(k) * ldb + n_lo + n],  g(k) = gather ? gather[k_lo + k] : k_lo + k
+//   C(r, n) = C[(c_row0 + r) * ldc + n_lo + n]
+//   r < M (static), k < K = k_hi - k_lo, n < N = n_hi - n_lo.
+// This single form covers the reference mm seam (kernels.hpp:26-27) and every
+// multiply inside cup: the Schur update H <- H - G*V1 (factor.cpp:51-52) and the
+// TRSM-internal updates (kernels.cpp:149-154), where B rows are U rows gathered
+// through the row profile.
+struct GemmArgs {
+    const u32* A;
+    i64 lda;
+    i32 a_row0;
+    const u32* B;
+    i64 ldb;
+    const i32* gather;
+    u32* C;
+    i64 ldc;
+    i32 c_row0;
+    i32 M;
+    Dyn k_lo, k_hi, n_lo, n_hi;
+    const i32* rp;
+    u32 alpha, beta;
+    Fp f;
+};
+
+// Number of 8-bit limbs for canonical elements of GF(p).
+static inline int limbs_for(u32 p) {
+    u32 v = p - 1;
+    int bits = 0;
+    while (v) {
+        ++bits;
+        v >>= 1;
+    }
+    int L = (bits + 7) / 8;
+    return L < 1 ? 1 : L;
+}
+// Exactness bound: every s32 accumulator sums L*K products of two u8 limbs
+// (each <= 255^2), so L*K*65025 < 2^31.
+static inline i64 tc_kmax(int L) { return L <= 2 ? 16384 : 8192; }
+static inline int tc_nt(int L) { return L == 1 ? 256 : (L == 2 ? 128 : 64); }
+
+size_t tc_a2_bytes(int L, i64 M, i64 Kmax);
+size_t tc_b2_bytes(int L, i64 Nmax, i64 Kmax);
+
+// Packs A and B into limb tiles then runs the tcgen05 kernel.  `a2`/`b2` are
+// workspaces of tc_a2_bytes/tc_b2_bytes for the static bounds (Kmax, Nmax).
+void gemm_tc(const GemmArgs& g, int L, i64 Kmax, i64 Nmax, uint8_t* a2, uint8_t* b2,
+             cudaStream_t s);
+// CUDA-core fallback for skinny shapes (K or N tiny).
+void gemm_simt(const GemmArgs& g, i64 Kmax, i64 Nmax, cudaStream_t s);
+
+// ---------------------------------------------------------------------- panel
+constexpr int PB = 64;    // rows per leaf panel
+constexpr int PW = 128;   // leading window width
+
+struct PanelScratch {
+    i32 c0, W, w, r, b;
+    u32 flag;      // a window-dead row has a nonzero tail residual -> fallback
+    u32 counter;   // last-CTA detection in the tail kernel
+    i32 piv_of_row[PB];     // pivot index (local) of row i, -1 if dead
+    i32 rank_before[PB];
+    u32 pinv[PB];           // inverse of the true pivot j
+    u32 pivval[PB];         // true pivot j
+    u32 Cr[PB][PB];         // Cr[i][i'] = C(i, piv(i')) for pivot rows i' < i
+    u32 win_orig[PB][PW];   // original window (fallback restore)
+};
+
+struct PanelArgs {
+    u32* A;
+    i64 lda;
+    i32 i0, b, N;
+    i32* rp;
+    i32* rrp;
+    i32* ipiv;
+    PanelScratch* ps;
+    Fp f;
+};
+void panel_window(const PanelArgs& a, cudaStream_t s);
+void panel_tail(const PanelArgs& a, cudaStream_t s);
+
+// X <- X * U^{-1} for the unit upper block of one leaf's pivots J = [j_lo, j_hi)
+// (|J| <= PB): rows [row0, row0 + M) of A, columns J; U rows gathered via rrp.
+struct TrsmLeafArgs {
+    u32* A;
+    i64 lda;
+    i32 row0, M;
+    Dyn j_lo, j_hi;
+    const i32* rp;
+    const i32* rrp;
+    Fp f;
+};
+void trsm_leaf(const TrsmLeafArgs& a, cudaStream_t s);
+
+// ---------------------------------------------------------------- permutation
+// Apply the transpositions T_{j, ipiv[j]} for j in [j_lo, j_hi) in increasing j
+// to rows of A (perm_apply_cols of factor.cpp:42 / :56).  Rows are either the
+// range [row0, row0 + M) or, when `gather` is set, rows gather[g_lo .. g_hi).
+struct SwapArgs {
+    u32* A;
+    i64 lda;
+    i32 row0, M;
+    const i32* gather;
+    Dyn g_lo, g_hi;
+    Dyn j_lo, j_hi;
+    const i32* rp;
+    const i32* ipiv;
+    i32 Mmax;
+};
+void apply_swaps(const SwapArgs& a, cudaStream_t s);
+
+// Final placement of U rows (composed shifts of factor.cpp:62-70): for every
+// pivot j with rrp[j] != j, row j, columns (j, n) <- row rrp[j], and the source
+// is zero-filled; applied in increasing j per column.
+void compact_u_rows(u32* A, i64 lda, i32 m, i32 n, const i32* rp, const i32* rrp,
+                    cudaStream_t s);
+
+// Closed-form random_matrix (reference.cpp:246-253) generated on device.
+void gen_random_matrix(u32* A, i64 lda, i64 m, i64 n, u64 seed, u32 p, cudaStream_t s);
+
+void fill_rp0(i32* rp, cudaStream_t s);
+
+}  // namespace rl

@@ -1,0 +1,25 @@
+// runtime.h -- host-side runtime helpers: errors, device properties.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace rl {
+
+// Mirrors the reference error hierarchy (proj/include/ranklab/errors.hpp:9-66)
+// at the C-ABI boundary: every exception is mapped to an RL_E* status code.
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+struct CudaError : Error {
+    CudaError(cudaError_t e, const char* what, const char* file, int line)
+        : Error(5 /*RL_ECUDA*/, std::string("CUDA error ") + cudaGetErrorString(e) + " at " +
+                                    file + ":" + std::to_string(line) + " (" + what + ")") {}
+};
+
+int num_sms();
+
+}  // namespace rl
