@@ -1,0 +1,375 @@
+#!/usr/bin/env python3
+"""bench.py -- CUP mod-p ops/s on B200 (BASELINE.json metric, config 3 by default).
+
+Workload (``--workload c3``, the configuration BASELINE.json's metric is quoted
+on): in-place CUP of ONE 16384 x 16384 matrix over GF(65521), entries
+``ranklab::random_matrix(16384, 16384, seed=3, GF(65521))`` generated on the
+device bit-identically to the reference generator (reference.cpp:246-253).
+A "step" is one full factorization (rank, row profile, sigma, packed [C\\U]).
+
+Metric: mod-p ops/s with the reference's own cost model
+W(m,n,r) = 2mnr - (m+n)r^2 + (2/3)r^3 (bench.cpp:12-13) at the returned rank.
+
+* ``value``     device-resident: input already in HBM; CUDA events on the
+                launching stream bracket each factorization (the per-step
+                restore of the input is outside the events); 1 GiB input > L2.
+* ``e2e``       the same metric through the C ABI with HOST buffers
+                (rl_cup_u32: pinned H2D, factorization, D2H of the body,
+                rank, profile and sigma), timed by the host around the call.
+* ``roofline``  dominant kernel = the tcgen05 limb GEMM; achieved int8 TOPS of
+                the root Schur GEMM shape (8192^3) timed live with CUDA events
+                vs the measured cuBLAS int8 dense peak on this GPU.
+* ``cpu_baseline`` the UNMODIFIED reference (oracle/_ref) on a bounded sample.
+
+``--impl reference`` times the reference's CPU cup on the host cores instead
+(T threads, each factoring its own 1024^2 random_matrix sample).
+
+Multi-GPU (torchrun, N>1): every rank factors its own replica of the workload
+("replicas only": a single C3 factorization is not sharded in this round);
+value = N * W / max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "c3": dict(m=16384, n=16384, p=65521, seed=3,
+               desc="CUP of one 16384x16384 random_matrix(seed=3) over GF(65521)"),
+    "c1": dict(m=1024, n=1024, p=65521, seed=1,
+               desc="CUP of one 1024x1024 random_matrix(seed=1) over GF(65521)"),
+    "c2048": dict(m=2048, n=2048, p=65521, seed=3,
+                  desc="CUP of one 2048x2048 random_matrix(seed=3) over GF(65521)"),
+    "c8192": dict(m=8192, n=8192, p=65521, seed=3,
+                  desc="CUP of one 8192x8192 random_matrix(seed=3) over GF(65521)"),
+}
+METRIC = "CUP mod-p ops/s (2n^3/3) at n=16384, % tensor peak; batched matrices/s"
+
+
+def model_ops(m, n, r):
+    return 2.0 * m * n * r - (m + n) * r * r + (2.0 / 3.0) * r ** 3
+
+
+def limbs(p):
+    return max(1, ((p - 1).bit_length() + 7) // 8)
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md recipe)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (self.out or "").strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------- reference arm
+def run_cpu_reference(n_threads: int, size: int, steps: int, warmup: int, p: int, seed: int):
+    """Each step: n_threads concurrent reference cup() calls on size^2 samples."""
+    import oracle as O
+    mats = [O.port_random_matrix(size, size, seed + 1000 * t, p) for t in range(n_threads)]
+
+    def one(t, out):
+        a = mats[t].copy()
+        t0 = time.perf_counter()
+        r = O.ref_cup(a, p)
+        out[t] = (time.perf_counter() - t0, r.rank)
+
+    times, ops = [], 0.0
+    for it in range(warmup + steps):
+        out = [None] * n_threads
+        th = [threading.Thread(target=one, args=(t, out)) for t in range(n_threads)]
+        t0 = time.perf_counter()
+        for x in th:
+            x.start()
+        for x in th:
+            x.join()
+        dt = time.perf_counter() - t0
+        if it >= warmup:
+            times.append(dt)
+            ops += sum(model_ops(size, size, o[1]) for o in out)
+    return ops / sum(times), sum(times) / len(times)
+
+
+def reference_arm(args, rank, world):
+    if world > 1 and rank != 0:
+        return
+    wl = WORKLOADS[args.workload]
+    try:
+        import oracle as O
+        if not O.have_ref():
+            raise FileNotFoundError("oracle/_ref/libranklab_ref.so not built")
+    except Exception as e:  # pragma: no cover
+        print(json.dumps({"impl": "reference", "unavailable": str(e)}))
+        return
+    threads = os.cpu_count() or 1
+    size = 1024
+    val, step_s = run_cpu_reference(threads, size, args.steps, args.warmup, wl["p"], wl["seed"])
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "mod-p ops/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32 (u64 products, % p)", "data": "synthetic",
+        "config": {"workload": args.workload, "p": wl["p"],
+                   "sample": f"{threads} threads x ranklab::cup of random_matrix({size},{size})"},
+        "cpu_baseline": {"value": val, "unit": "mod-p ops/s", "cores": threads,
+                         "kind": "reference",
+                         "sample": f"{threads} concurrent reference cup() of {size}x{size} "
+                                   f"(the reference is single-threaded per call)"},
+        "e2e": {"value": val, "unit": "mod-p ops/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ----------------------------------------------------------------- our arm
+def measure_int8_peak(torch, iters=10):
+    """cuBLAS int8 dense GEMM (torch._int_mm) 8192^3, best of `iters` (burst)."""
+    n = 8192
+    a = torch.randint(-128, 127, (n, n), dtype=torch.int8, device="cuda")
+    b = torch.randint(-128, 127, (n, n), dtype=torch.int8, device="cuda")
+    for _ in range(3):
+        torch._int_mm(a, b)
+    torch.cuda.synchronize()
+    best = 1e9
+    for _ in range(iters):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch._int_mm(a, b)
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1) / 1e3)
+    return 2.0 * n ** 3 / best / 1e12
+
+
+def ours(args, rank, world, local_rank):
+    import torch
+    import paper_1112_5717_b200 as G
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    wl = WORKLOADS[args.workload]
+    m, n, p, seed = wl["m"], wl["n"], wl["p"], wl["seed"]
+    L = limbs(p)
+    stream = torch.cuda.current_stream()
+    pristine = torch.empty((m, n), dtype=torch.int32, device="cuda")
+    G.random_matrix_dev(pristine, m, n, seed, p, stream=stream)
+    work = torch.empty_like(pristine)
+
+    # warm-up (also builds + captures the plan graph)
+    for _ in range(args.warmup):
+        work.copy_(pristine)
+        G.cup_dev(work, m, n, p, stream=stream, sync=False)
+    torch.cuda.synchronize()
+    st = G.plan_stats(m, n, p)
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        for i in range(args.steps):
+            work.copy_(pristine)                    # restore input (outside the events)
+            starts[i].record(stream)
+            G.cup_dev(work, m, n, p, stream=stream, sync=False)
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    elapsed = sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / 1e3
+    t_local = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    t_max = float(t_local.item())
+
+    # results of the last factorization + structural verification
+    work.copy_(pristine)
+    res = G.cup_dev(work, m, n, p, stream=stream)
+    r = res.rank
+    W = model_ops(m, n, r)
+    value = world * W * args.steps / t_max
+    ms_per_step = t_max / args.steps * 1e3
+
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "mod-p ops/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": f"u32 in GF({p}); u8 limbs x{L} on int8 tensor cores (s32 acc, exact)",
+        "data": "synthetic",
+        "config": {"workload": args.workload, "desc": wl["desc"], "m": m, "n": n, "p": p,
+                   "seed": seed, "rank": r, "model_ops": W,
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "input 1 GiB > 126 MB L2; input restored between steps",
+                   "profile_identity": bool(np.array_equal(res.row_profile, np.arange(r))),
+                   "sigma_identity": bool(np.array_equal(res.col_perm, np.arange(n)))},
+        "gpu_launches": int(st["launches"]) * args.steps,
+        "clocks": clk.summary(),
+    }
+
+    # dominant kernel roofline: root Schur GEMM shape, GEMM kernel alone
+    try:
+        peak = measure_int8_peak(torch)
+        gm = min(m // 2, 8192)
+        da = torch.empty((gm, gm), dtype=torch.int32, device="cuda")
+        db = torch.empty((gm, gm), dtype=torch.int32, device="cuda")
+        dc = torch.empty((gm, gm), dtype=torch.int32, device="cuda")
+        G.random_matrix_dev(da, gm, gm, 11, p)
+        G.random_matrix_dev(db, gm, gm, 12, p)
+        G.random_matrix_dev(dc, gm, gm, 13, p)
+        ms_pack, ms_gemm = G.profile_gemm_dev(da, db, dc, gm, gm, gm, p, iters=5, stream=stream)
+        tops = 2.0 * gm ** 3 * L * L / (ms_gemm / 1e3) / 1e12
+        cup_int8 = W * L * L / (ms_per_step / 1e3) / 1e12
+        line["roofline"] = {
+            "bound": "tensor", "kernel": "gemm_tc_kernel<L=%d> (tcgen05.mma kind::i8)" % L,
+            "achieved": tops, "peak": peak, "unit": "TFLOP/s",
+            "unit_note": "int8 tensor TOPS; 1 mod-p MAC = L^2 u8 MACs",
+            "frac": tops / peak,
+            "peak_source": "measured live: cuBLAS int8 dense GEMM 8192^3 (torch._int_mm), burst",
+            "shape": [gm, gm, gm], "ms_gemm": ms_gemm, "ms_pack": ms_pack,
+            "traffic": None,
+            "cup_frac_of_peak": cup_int8 / peak,
+            "cup_modp_peak": peak * 1e12 / (L * L),
+        }
+        del da, db, dc
+    except Exception as e:  # pragma: no cover
+        line["roofline"] = {"error": str(e)}
+
+    # e2e through the C ABI with host buffers
+    try:
+        e2e_steps = max(1, min(args.steps, 3))
+        host = torch.empty((m, n), dtype=torch.int32, pin_memory=True)
+        src = pristine.cpu().numpy().view(np.uint32)
+        hv = host.numpy().view(np.uint32)
+        rrp = np.zeros(min(m, n), np.uint32)
+        sig = np.zeros(n, np.uint32)
+        tt = []
+        for i in range(e2e_steps + 1):
+            np.copyto(hv, src)
+            rk = ctypes.c_int64(0)
+            t0 = time.perf_counter()
+            code = G.lib().rl_cup_u32(ctypes.c_void_p(hv.ctypes.data), m, n, n, p,
+                                      ctypes.byref(rk), ctypes.c_void_p(rrp.ctypes.data),
+                                      ctypes.c_void_p(sig.ctypes.data), None)
+            dt = time.perf_counter() - t0
+            if code != 0:
+                raise RuntimeError(G.lib().rl_last_error().decode())
+            if i > 0:
+                tt.append(dt)
+        e2e_t = sum(tt) / len(tt)
+        line["e2e"] = {"value": world * W / e2e_t, "unit": "mod-p ops/s",
+                       "h2d_bytes_per_step": m * n * 4,
+                       "d2h_bytes_per_step": m * n * 4 + 8 + 4 * min(m, n) * 2 + 4 * n,
+                       "ms_per_step": e2e_t * 1e3, "steps": len(tt),
+                       "path": "rl_cup_u32 (host pinned buffers)"}
+        del host
+    except Exception as e:  # pragma: no cover
+        line["e2e"] = {"error": str(e)}
+
+    # CPU baseline: the unmodified reference on a bounded sample, 1 thread
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            import oracle as O
+            size = args.cpu_sample
+            a = O.port_random_matrix(size, size, seed, p)
+            t0 = time.perf_counter()
+            rr = O.ref_cup(a, p) if O.have_ref() else O.port_cup(a, p)
+            dt = time.perf_counter() - t0
+            line["cpu_baseline"] = {
+                "value": model_ops(size, size, rr.rank) / dt, "unit": "mod-p ops/s", "cores": 1,
+                "kind": "reference" if O.have_ref() else "port",
+                "sample": f"ranklab::cup of random_matrix({size},{size},seed={seed},GF({p})), "
+                          f"single thread, {dt:.1f} s"}
+        except Exception as e:  # pragma: no cover
+            line["cpu_baseline"] = {"error": str(e)}
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c3")
+    ap.add_argument("--cpu-sample", type=int, default=2048)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+    else:
+        ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

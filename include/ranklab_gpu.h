@@ -95,8 +95,22 @@ int rl_version(void);
 
 /* Introspection for benchmarks: number of GEMM / tensor-core GEMM / panel /
  * leaf-TRSM launches of the last CUP plan built for (m, n, lda, p), and its
- * GEMM workspace in bytes.  stats[0..4]. */
+ * GEMM workspace in bytes, kernel launches per factorization.  stats[0..5]. */
 int rl_cup_plan_stats(int64_t m, int64_t n, int64_t lda, uint32_t p, int64_t* stats);
+
+/* Host-only (no device needed): the exact OpCounter charges of ranklab::cup
+ * for an m x n input with the given rank, row profile and pivot positions
+ * (ipiv[j] = column position where pivot j was found).  ops[4] as above. */
+int rl_cup_opcount(int64_t m, int64_t n, int64_t rank, const uint32_t* rrp, const uint32_t* ipiv,
+                   uint64_t* ops);
+
+/* Benchmark helper: times the pack kernels and the tcgen05 GEMM kernel of
+ * C <- C - A*B (m x l x n, dense device buffers) separately, averaged over
+ * `iters` launches (CUDA events on `stream`).  l must respect the exact
+ * accumulation bound (16384 for p < 2^16). */
+int rl_profile_gemm_dev(const uint32_t* dA, const uint32_t* dB, uint32_t* dC, int64_t m,
+                        int64_t l, int64_t n, uint32_t p, int iters, float* ms_pack,
+                        float* ms_gemm, void* stream);
 
 #ifdef __cplusplus
 }

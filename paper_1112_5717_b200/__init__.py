@@ -115,7 +115,8 @@ _vp = C.c_void_p
 #: every symbol include/ranklab_gpu.h declares
 EXPORTS = ["rl_cup_u32", "rl_cup_u32_dev", "rl_cup_batched_u32_dev", "rl_mm_u32",
            "rl_mm_u32_dev", "rl_rank_and_profile_u32", "rl_determinant_u32",
-           "rl_random_matrix_u32_dev", "rl_last_error", "rl_version", "rl_cup_plan_stats"]
+           "rl_random_matrix_u32_dev", "rl_last_error", "rl_version", "rl_cup_plan_stats",
+           "rl_profile_gemm_dev", "rl_cup_opcount"]
 
 
 def lib():
@@ -137,6 +138,9 @@ def lib():
     L.rl_random_matrix_u32_dev.argtypes = [_vp, _i64, _i64, _i64, C.c_uint64, _u32, _vp]
     L.rl_last_error.restype = C.c_char_p
     L.rl_cup_plan_stats.argtypes = [_i64, _i64, _i64, _u32, _vp]
+    L.rl_profile_gemm_dev.argtypes = [_vp, _vp, _vp, _i64, _i64, _i64, _u32, C.c_int,
+                                      C.POINTER(C.c_float), C.POINTER(C.c_float), _vp]
+    L.rl_cup_opcount.argtypes = [_i64, _i64, _i64, _vp, _vp, _vp]
     _lib = L
     return L
 
@@ -154,7 +158,7 @@ def _ptr(a: np.ndarray | None):
 def _as_u32_matrix(a: np.ndarray) -> np.ndarray:
     if not isinstance(a, np.ndarray) or a.dtype != np.uint32 or a.ndim != 2:
         raise InvalidArgument("expected a 2-D numpy uint32 array")
-    if a.strides[1] != 4 or a.strides[0] % 4:
+    if a.size and (a.strides[1] != 4 or a.strides[0] % 4):
         raise InvalidArgument("rows must be contiguous uint32")
     return a
 
@@ -186,10 +190,17 @@ def cup(a: np.ndarray, p: int, ctr: OpCounter | None = None) -> PackedCup:
 
 
 def cup_dev(d_a, m: int, n: int, p: int, lda: int | None = None, stream=None,
-            ctr: OpCounter | None = None, want_perm: bool = True) -> PackedCup:
-    """CUP of a device-resident matrix (``torch`` tensor or raw pointer)."""
+            ctr: OpCounter | None = None, want_perm: bool = True, sync: bool = True):
+    """CUP of a device-resident matrix (``torch`` tensor or raw pointer).
+
+    With ``sync=False`` nothing is read back: the factorization is only
+    enqueued on ``stream`` and None is returned."""
     ptr = d_a.data_ptr() if hasattr(d_a, "data_ptr") else int(d_a)
     lda = n if lda is None else lda
+    if not sync:
+        _check(lib().rl_cup_u32_dev(C.c_void_p(ptr), m, n, lda, int(p), None, None, None, None,
+                                    _stream_ptr(stream)))
+        return None
     rank = _i64(0)
     rrp = np.zeros(max(1, min(m, n)), np.uint32)
     sigma = np.zeros(max(1, n), np.uint32) if want_perm else None
@@ -277,10 +288,19 @@ def random_matrix_dev(d_a, m: int, n: int, seed: int, p: int, lda: int | None = 
 
 
 def plan_stats(m: int, n: int, p: int, lda: int | None = None) -> dict:
-    st = np.zeros(5, np.int64)
+    st = np.zeros(6, np.int64)
     _check(lib().rl_cup_plan_stats(m, n, lda or n, int(p), _ptr(st)))
     return dict(gemms=int(st[0]), tc_gemms=int(st[1]), panels=int(st[2]), trsm_leaves=int(st[3]),
-                workspace_bytes=int(st[4]))
+                workspace_bytes=int(st[4]), launches=int(st[5]))
+
+
+def profile_gemm_dev(d_a, d_b, d_c, m: int, l: int, n: int, p: int, iters: int = 5, stream=None):
+    """(ms of the two pack kernels, ms of the tcgen05 GEMM kernel) for C <- C - A*B."""
+    mp, mg = C.c_float(0), C.c_float(0)
+    _check(lib().rl_profile_gemm_dev(C.c_void_p(d_a.data_ptr()), C.c_void_p(d_b.data_ptr()),
+                                     C.c_void_p(d_c.data_ptr()), m, l, n, int(p), iters,
+                                     C.byref(mp), C.byref(mg), _stream_ptr(stream)))
+    return mp.value, mg.value
 
 
 def _stream_ptr(stream):

@@ -180,6 +180,7 @@ void cup_dev_impl(u32* dA, i64 m, i64 n, i64 lda, u32 p, i64* rank, u32* rrp, u3
         std::lock_guard<std::mutex> lk(g_mu);
         CupEngine& e = engine_for(m, n, lda, p);
         e.run(dA, s, /*use_graph=*/true);
+        if (!rank && !rrp && !sigma && !ops) return;  // fully asynchronous
         e.results(&r, rrp_h.data(), ipiv_h.data(), s);
     }
     if (rank) *rank = r;
@@ -446,6 +447,54 @@ int rl_cup_batched_u32_dev(uint32_t* dA, int64_t batch, int64_t m, int64_t n, in
     });
 }
 
+// Times one mod-p GEMM C <- C - A*B (m x l x n) on device buffers: pack kernels
+// and the tcgen05 kernel separately, each averaged over `iters` launches with
+// CUDA events on `stream`.  For benchmarks / roofline only.
+int rl_profile_gemm_dev(const uint32_t* dA, const uint32_t* dB, uint32_t* dC, int64_t m,
+                        int64_t l, int64_t n, uint32_t p, int iters, float* ms_pack,
+                        float* ms_gemm, void* stream) {
+    return guard([&] {
+        check_field(p);
+        require_device();
+        std::lock_guard<std::mutex> lk(g_mu);
+        cudaStream_t s = (cudaStream_t)stream;
+        const int L = limbs_for(p);
+        if (l > tc_kmax(L)) throw Error(RL_EINVAL, "profile: l exceeds the exact-accumulation bound");
+        GemmArgs g{};
+        g.A = dA; g.lda = l; g.B = dB; g.ldb = n; g.C = dC; g.ldc = n; g.M = (i32)m;
+        g.k_lo = dyn_c(0); g.k_hi = dyn_c((i32)l); g.n_lo = dyn_c(0); g.n_hi = dyn_c((i32)n);
+        g.alpha = p - 1; g.beta = 1 % p; g.f = make_fp(p);
+        static DevBuf a2, b2;
+        uint8_t* pa = (uint8_t*)a2.get(tc_a2_bytes(L, m, l));
+        uint8_t* pb = (uint8_t*)b2.get(tc_b2_bytes(L, n, l));
+        cudaEvent_t e0, e1, e2;
+        RL_CUDA_CHECK(cudaEventCreate(&e0));
+        RL_CUDA_CHECK(cudaEventCreate(&e1));
+        RL_CUDA_CHECK(cudaEventCreate(&e2));
+        gemm_tc_split(g, L, l, n, pa, pb, s, 0);  // warm-up
+        gemm_tc_split(g, L, l, n, pa, pb, s, 1);
+        float tp = 0, tg = 0;
+        for (int it = 0; it < iters; ++it) {
+            RL_CUDA_CHECK(cudaEventRecord(e0, s));
+            gemm_tc_split(g, L, l, n, pa, pb, s, 0);
+            RL_CUDA_CHECK(cudaEventRecord(e1, s));
+            gemm_tc_split(g, L, l, n, pa, pb, s, 1);
+            RL_CUDA_CHECK(cudaEventRecord(e2, s));
+            RL_CUDA_CHECK(cudaEventSynchronize(e2));
+            float a = 0, b = 0;
+            RL_CUDA_CHECK(cudaEventElapsedTime(&a, e0, e1));
+            RL_CUDA_CHECK(cudaEventElapsedTime(&b, e1, e2));
+            tp += a;
+            tg += b;
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaEventDestroy(e2);
+        *ms_pack = tp / iters;
+        *ms_gemm = tg / iters;
+    });
+}
+
 int rl_cup_plan_stats(int64_t m, int64_t n, int64_t lda, uint32_t p, int64_t* stats) {
     return guard([&] {
         check_field(p);
@@ -458,7 +507,21 @@ int rl_cup_plan_stats(int64_t m, int64_t n, int64_t lda, uint32_t p, int64_t* st
         stats[2] = st.panels;
         stats[3] = st.trsm_leaves;
         stats[4] = (int64_t)e.workspace_bytes();
+        stats[5] = st.launches;
     });
 }
 
 }  // extern "C"
+
+extern "C" {
+// Host-only: the reference's exact OpCounter charges of cup() from the shape,
+// the row profile and the pivot positions (see cup_opcount in cup.cu).
+int rl_cup_opcount(int64_t m, int64_t n, int64_t rank, const uint32_t* rrp, const uint32_t* ipiv,
+                   uint64_t* ops) {
+    return guard([&] {
+        if (!ops) throw Error(RL_EINVAL, "null ops");
+        if (m < 0 || n < 0 || rank < 0 || rank > std::min(m, n)) throw Error(RL_EDIM, "bad shape");
+        cup_opcount(m, n, rank, rrp, ipiv, ops);
+    });
+}
+}

@@ -102,8 +102,10 @@ void CupEngine::gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nm
     ++stats_.gemms;
     if (tc) {
         ++stats_.tc_gemms;
+        stats_.launches += 3;
         gemm_tc(g, L_, Kmax, Nmax, a2_, b2_, s_);
     } else {
+        stats_.launches += 1;
         gemm_simt(g, Kmax, Nmax, s_);
     }
 }
@@ -124,6 +126,7 @@ void CupEngine::panel(i32 i0, i32 b) {
     panel_window(a, s_);
     panel_tail(a, s_);
     stats_.panels++;
+    stats_.launches += 2;
 }
 
 void CupEngine::swaps_range(i32 row0, i32 M, Dyn j_lo, Dyn j_hi) {
@@ -140,6 +143,7 @@ void CupEngine::swaps_range(i32 row0, i32 M, Dyn j_lo, Dyn j_hi) {
     a.ipiv = ipiv_;
     a.Mmax = M;
     apply_swaps(a, s_);
+    stats_.launches += 1;
 }
 
 void CupEngine::swaps_gather(Dyn g_lo, Dyn g_hi, i32 Mmax, Dyn j_lo, Dyn j_hi) {
@@ -156,6 +160,7 @@ void CupEngine::swaps_gather(Dyn g_lo, Dyn g_hi, i32 Mmax, Dyn j_lo, Dyn j_hi) {
     a.ipiv = ipiv_;
     a.Mmax = Mmax;
     apply_swaps(a, s_);
+    stats_.launches += 1;
 }
 
 // G <- G * U_X^{-1} for the unit upper block of node X = rows [x0, x0+mx)
@@ -175,6 +180,7 @@ void CupEngine::trsm_right(i32 r0, i32 M, i32 x0, i32 mx) {
         a.f = f_;
         trsm_leaf(a, s_);
         stats_.trsm_leaves++;
+        stats_.launches += 1;
         return;
     }
     const i32 kx = mx / 2;
@@ -206,6 +212,7 @@ void CupEngine::enqueue(u32* dA, cudaStream_t s) {
     if (m_ > 0 && n_ > 0) {
         node(0, m_);
         compact_u_rows(A_, lda_, m_, n_, rp_, rrp_, s);
+        stats_.launches += 1;
     }
 }
 

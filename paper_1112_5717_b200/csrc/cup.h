@@ -11,7 +11,7 @@ struct PanelScratch;
 class CupEngine {
 public:
     struct Stats {
-        long gemms = 0, tc_gemms = 0, panels = 0, trsm_leaves = 0;
+        long gemms = 0, tc_gemms = 0, panels = 0, trsm_leaves = 0, launches = 0;
     };
 
     CupEngine(i32 m, i32 n, i64 lda, u32 p);

@@ -317,7 +317,8 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(GemmArgs g, const uint8
 }
 
 template <int L>
-void launch_tc(const GemmArgs& g, i64 Kmax, i64 Nmax, uint8_t* a2, uint8_t* b2, cudaStream_t s) {
+void launch_tc(const GemmArgs& g, i64 Kmax, i64 Nmax, uint8_t* a2, uint8_t* b2, cudaStream_t s,
+               int phase) {
     using C_ = Cfg<L>;
     const int nsm = num_sms();
     const i64 KB = (Kmax + BK - 1) / BK;
@@ -325,7 +326,7 @@ void launch_tc(const GemmArgs& g, i64 Kmax, i64 Nmax, uint8_t* a2, uint8_t* b2, 
     const i64 NB = (Nmax + C_::NT - 1) / C_::NT;
     u32 sc[4] = {1, 0, 0, 0};
     for (int i = 1; i < 4; ++i) sc[i] = (u32)(((u64)sc[i - 1] << 8) % g.f.p);
-    {
+    if (phase != 1) {
         i64 work = MB * KB * BM * 8;
         int grid = (int)std::min<i64>((work + 255) / 256, (i64)nsm * 16);
         pack_a_kernel<L><<<std::max(grid, 1), 256, 0, s>>>(g, a2);
@@ -335,6 +336,7 @@ void launch_tc(const GemmArgs& g, i64 Kmax, i64 Nmax, uint8_t* a2, uint8_t* b2, 
         int grid = (int)std::min<i64>(work, (i64)nsm * 8);
         pack_b_kernel<L><<<std::max(grid, 1), 256, 0, s>>>(g, b2, sc[1], sc[2], sc[3]);
     }
+    if (phase == 0) return;
     static bool attr_set = false;
     if (!attr_set) {
         RL_CUDA_CHECK(cudaFuncSetAttribute(gemm_tc_kernel<L>,
@@ -360,15 +362,20 @@ size_t tc_b2_bytes(int L, i64 Nmax, i64 Kmax) {
     return (size_t)(NB * L * KB) * (size_t)(L * NT * BK);
 }
 
-void gemm_tc(const GemmArgs& g, int L, i64 Kmax, i64 Nmax, uint8_t* a2, uint8_t* b2,
-             cudaStream_t s) {
+void gemm_tc_split(const GemmArgs& g, int L, i64 Kmax, i64 Nmax, uint8_t* a2, uint8_t* b2,
+                   cudaStream_t s, int phase) {
     if (g.M <= 0 || Kmax <= 0 || Nmax <= 0) return;
     switch (L) {
-        case 1: launch_tc<1>(g, Kmax, Nmax, a2, b2, s); break;
-        case 2: launch_tc<2>(g, Kmax, Nmax, a2, b2, s); break;
-        case 3: launch_tc<3>(g, Kmax, Nmax, a2, b2, s); break;
-        default: launch_tc<4>(g, Kmax, Nmax, a2, b2, s); break;
+        case 1: launch_tc<1>(g, Kmax, Nmax, a2, b2, s, phase); break;
+        case 2: launch_tc<2>(g, Kmax, Nmax, a2, b2, s, phase); break;
+        case 3: launch_tc<3>(g, Kmax, Nmax, a2, b2, s, phase); break;
+        default: launch_tc<4>(g, Kmax, Nmax, a2, b2, s, phase); break;
     }
+}
+
+void gemm_tc(const GemmArgs& g, int L, i64 Kmax, i64 Nmax, uint8_t* a2, uint8_t* b2,
+             cudaStream_t s) {
+    gemm_tc_split(g, L, Kmax, Nmax, a2, b2, s, 2);
 }
 
 // ------------------------------------------------------------ SIMT fallback

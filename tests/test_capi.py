@@ -1,0 +1,90 @@
+"""CPU tests of the drop-in boundary: the C-ABI library loads, exports every
+symbol include/ranklab_gpu.h declares, validates arguments like the reference
+(errors.hpp), computes the reference's exact op counts on the host, and fails
+loudly (no CPU fallback) when asked to compute without a GPU."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1112_5717_b200 as G
+from tests.helpers import load_npz_cases
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _have_gpu():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+def test_header_symbols_are_exported():
+    hdr = open(os.path.join(ROOT, "include", "ranklab_gpu.h")).read()
+    declared = set(re.findall(r"^\s*(?:int|const char\*)\s+(rl_\w+)\s*\(", hdr, re.M))
+    assert declared == set(G.EXPORTS)
+    lib = G.lib()
+    for name in declared:
+        assert hasattr(lib, name), name
+
+
+def test_library_is_sm100a():
+    so = open(G.LIB_PATH, "rb").read()
+    assert b"sm_100a" in so or b"sm_100" in so
+
+
+def test_field_validation_matches_reference():
+    a = np.ones((2, 2), np.uint32)
+    with pytest.raises(G.NotPrime):
+        G.cup(a, 4)
+    with pytest.raises(G.NotPrime):
+        G.cup(a, 1)
+    with pytest.raises(G.NotPrime):
+        G.cup(a, 2**31 + 11)
+
+
+def test_empty_shapes_need_no_device():
+    # factor.cpp:32 / test_factor.cpp:245-256: rank 0, identity of order n
+    a = np.zeros((0, 4), np.uint32)
+    r = G.cup(a, 3)
+    assert r.rank == 0 and list(r.col_perm) == [0, 1, 2, 3]
+    b = np.zeros((4, 0), np.uint32)
+    r = G.cup(b, 3)
+    assert r.rank == 0 and len(r.col_perm) == 0
+
+
+def test_mm_overlap_rejected():
+    # kernels.cpp:38-39: C must not overlap A or B
+    buf = np.zeros((4, 4), np.uint32)
+    with pytest.raises(G.OverlapError):
+        G.mm(buf[0:2, 0:2], buf[0:2, 1:3], buf[0:2, 1:3], 1, 0, 5)
+
+
+@pytest.mark.skipif(_have_gpu(), reason="checks the no-GPU failure path")
+def test_no_cpu_fallback():
+    a = np.ones((3, 3), np.uint32)
+    with pytest.raises(G.CudaError):
+        G.cup(a, 7)
+    with pytest.raises(G.CudaError):
+        G.mm(a, a, a.copy(), 1, 0, 7)
+
+
+def test_opcount_matches_reference_goldens():
+    # OpCounter of cup is a function of (shape, rrp, ipiv)
+    n = 0
+    for c in load_npz_cases(os.path.join(ROOT, "tests", "golden", "cup_small.npz"),
+                            ["p", "a", "rank", "rrp", "ops"]):
+        a = c["a"].copy()
+        m, nn = a.shape
+        r = O.port_cup(a, int(c["p"]))
+        ops = np.zeros(4, np.uint64)
+        rrp = np.ascontiguousarray(r.rrp, np.uint32)
+        ipiv = np.ascontiguousarray(r.ipiv, np.uint32)
+        G._check(G.lib().rl_cup_opcount(m, nn, r.rank, G._ptr(rrp), G._ptr(ipiv), G._ptr(ops)))
+        assert ops.tolist() == c["ops"].tolist(), (m, nn, int(c["p"]))
+        n += 1
+    assert n >= 300

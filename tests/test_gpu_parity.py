@@ -1,0 +1,234 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle and the
+reference's golden vectors.  Bit-exact for every output: rank, row profile,
+sigma, every entry of the packed [C\\U] body, and the reference's op counts."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1112_5717_b200 as G
+from tests.helpers import c2_style, c4_batch, digest, load_npz_cases
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+PRIMES = [2, 3, 7, 251, 257, 65521, 8388593, 2147483647]
+
+
+def _digests():
+    with open(os.path.join(GOLDEN, "digests.json")) as f:
+        return json.load(f)
+
+
+def _check_cup(a, p, ctr_check=False):
+    a_gpu, a_or = a.copy(), a.copy()
+    ctr = G.OpCounter()
+    g = G.cup(a_gpu, p, ctr)
+    o = O.port_cup(a_or, p)
+    assert g.rank == o.rank
+    assert np.array_equal(g.row_profile, o.rrp)
+    assert np.array_equal(g.col_perm, o.sigma)
+    assert np.array_equal(a_gpu, a_or), f"body mismatch at {np.argwhere(a_gpu != a_or)[:5]}"
+    if ctr_check and O.have_ref():
+        r = O.ref_cup(a.copy(), p)
+        assert [ctr.n_mul, ctr.n_addsub, ctr.n_divinv, ctr.n_ztest] == r.ops.tolist()
+    return g
+
+
+def test_golden_cup_cases():
+    for c in load_npz_cases(os.path.join(GOLDEN, "cup_small.npz"),
+                            ["p", "a", "body", "rank", "rrp", "sigma", "ops"]):
+        a = c["a"].copy()
+        ctr = G.OpCounter()
+        r = G.cup(a, int(c["p"]), ctr)
+        assert r.rank == int(c["rank"])
+        assert np.array_equal(r.row_profile, c["rrp"])
+        assert np.array_equal(r.col_perm, c["sigma"])
+        assert np.array_equal(a, c["body"])
+        assert [ctr.n_mul, ctr.n_addsub, ctr.n_divinv, ctr.n_ztest] == c["ops"].tolist()
+
+
+def test_golden_mm_cases():
+    for c in load_npz_cases(os.path.join(GOLDEN, "mm_small.npz"),
+                            ["p", "a", "b", "c", "alpha", "beta", "out"]):
+        out = c["c"].copy()
+        G.mm(c["a"], c["b"], out, int(c["alpha"]), int(c["beta"]), int(c["p"]))
+        assert np.array_equal(out, c["out"])
+
+
+@pytest.mark.parametrize("p", PRIMES)
+def test_mm_tensor_core_shapes(p):
+    rng = np.random.default_rng(p % 1000)
+    for (m, l, n) in [(128, 128, 128), (200, 300, 170), (129, 1000, 257), (64, 64, 64),
+                      (33, 40, 35), (300, 16, 300)]:
+        a = rng.integers(0, p, (m, l), dtype=np.uint64).astype(np.uint32)
+        b = rng.integers(0, p, (l, n), dtype=np.uint64).astype(np.uint32)
+        c = rng.integers(0, p, (m, n), dtype=np.uint64).astype(np.uint32)
+        for alpha, beta in [(p - 1, 1), (1, 0), (3 % p, 2 % p)]:
+            c1, c2 = c.copy(), c.copy()
+            G.mm(a, b, c1, alpha, beta, p)
+            O.port_mm(a, b, c2, alpha, beta, p)
+            assert np.array_equal(c1, c2), (m, l, n, alpha, beta)
+
+
+def test_mm_long_k_chunks():
+    # K beyond the exact s32 accumulation bound is chunked (tc_kmax)
+    p = 65521
+    rng = np.random.default_rng(3)
+    a = rng.integers(0, p, (130, 20000), dtype=np.uint64).astype(np.uint32)
+    b = rng.integers(0, p, (20000, 70), dtype=np.uint64).astype(np.uint32)
+    c = np.zeros((130, 70), np.uint32)
+    G.mm(a, b, c, 1, 0, p)
+    ref = np.zeros_like(c)
+    O.port_mm(a, b, ref, 1, 0, p)
+    assert np.array_equal(c, ref)
+
+
+@pytest.mark.parametrize("p", PRIMES)
+def test_cup_random_shapes(p):
+    rng = np.random.default_rng(1000 + p % 97)
+    for (m, n) in [(1, 1), (3, 5), (64, 64), (65, 129), (127, 300), (300, 127), (128, 128),
+                   (257, 513), (513, 200)]:
+        _check_cup(rng.integers(0, p, (m, n), dtype=np.uint64).astype(np.uint32), p,
+                   ctr_check=(m * n < 40000))
+
+
+@pytest.mark.parametrize("p", [2, 3, 65521, 8388593])
+def test_cup_rank_deficient(p):
+    rng = np.random.default_rng(5)
+    for (m, n, r) in [(300, 200, 50), (200, 300, 120), (513, 257, 200), (100, 700, 60),
+                      (640, 640, 333)]:
+        seed = int(rng.integers(0, 2**62))
+        if O.have_ref():
+            a = O.ref_random_rank_matrix(m, n, r, seed, p, generic=bool(seed & 1))
+        else:
+            L = rng.integers(0, p, (m, r), dtype=np.uint64).astype(np.uint32)
+            R = rng.integers(0, p, (r, n), dtype=np.uint64).astype(np.uint32)
+            from tests.helpers import matmul_mod
+            a = matmul_mod(L, R, p)
+        g = _check_cup(a, p)
+        assert g.rank <= r
+
+
+def test_cup_structured_window_misses():
+    """Pivots beyond the leading window (zero leading columns, zero rows,
+    GF(2)/GF(3) dense rank deficiency) -> the exact fallback path."""
+    rng = np.random.default_rng(11)
+    p = 65521
+    a = rng.integers(0, p, (300, 400), dtype=np.uint64).astype(np.uint32)
+    a[:, :200] = 0
+    _check_cup(a, p)
+    a = rng.integers(0, p, (300, 400), dtype=np.uint64).astype(np.uint32)
+    a[::3, :] = 0
+    _check_cup(a, p)
+    a = rng.integers(0, p, (256, 1024), dtype=np.uint64).astype(np.uint32)
+    a[:, 100:900] = 0
+    a[:, :100] = a[:, :100] * (np.arange(256)[:, None] % 2).astype(np.uint32)
+    _check_cup(a, p)
+    for q in (2, 3):
+        L = rng.integers(0, q, (700, 90), dtype=np.uint64).astype(np.uint32)
+        R = rng.integers(0, q, (90, 1100), dtype=np.uint64).astype(np.uint32)
+        from tests.helpers import matmul_mod
+        _check_cup(matmul_mod(L, R, q), q)
+
+
+def test_cup_tall_early_return():
+    # r1 == n early return (factor.cpp:47): rows below keep G (C data)
+    rng = np.random.default_rng(12)
+    for p in (65521, 7):
+        _check_cup(rng.integers(0, p, (700, 90), dtype=np.uint64).astype(np.uint32), p)
+        _check_cup(rng.integers(0, p, (1000, 300), dtype=np.uint64).astype(np.uint32), p)
+
+
+def test_c1_matches_reference_digest():
+    d = _digests()["c1"]
+    a = O.port_random_matrix(1024, 1024, 1, 65521)
+    ctr = G.OpCounter()
+    r = G.cup(a, 65521, ctr)
+    assert r.rank == d["rank"]
+    assert np.array_equal(r.row_profile, np.arange(r.rank))
+    assert digest(r.col_perm) == d["sigma"] and digest(a) == d["body"]
+    assert [ctr.n_mul, ctr.n_addsub, ctr.n_divinv, ctr.n_ztest] == d["ops"]
+
+
+def test_c2_style_matches_reference_digest():
+    d = _digests()["c2s"]
+    a = c2_style(1024, 2048, 512, 2, 65521)
+    ctr = G.OpCounter()
+    r = G.cup(a, 65521, ctr)
+    assert r.rank == d["rank"] and r.row_profile.tolist() == d["rrp"]
+    assert digest(r.col_perm) == d["sigma"] and digest(a) == d["body"]
+    assert [ctr.n_mul, ctr.n_addsub, ctr.n_divinv, ctr.n_ztest] == d["ops"]
+
+
+def test_c4_batched_matches_reference_digests():
+    import torch
+    d = _digests()["c4"]
+    mats, ranks = c4_batch(16)
+    dev = torch.from_numpy(mats.view(np.int32).copy()).cuda()
+    rk, rrp, sig = G.cup_batched_dev(dev, 16, 256, 256, d["p"])
+    body = dev.cpu().numpy().view(np.uint32)
+    for t in range(16):
+        e = d["mats"][t]
+        assert rk[t] == e["rank"] == ranks[t]
+        assert digest(rrp[t, :rk[t]]) == e["rrp"]
+        assert digest(sig[t]) == e["sigma"]
+        assert digest(body[t]) == e["body"]
+
+
+def test_batched_small_primes_vs_oracle():
+    import torch
+    rng = np.random.default_rng(21)
+    for p in (2, 3, 65521, 2147483647):
+        mats = rng.integers(0, p, (6, 70, 90), dtype=np.uint64).astype(np.uint32)
+        mats[1, :, :40] = 0
+        mats[2, ::2, :] = 0
+        dev = torch.from_numpy(mats.view(np.int32).copy()).cuda()
+        rk, rrp, sig = G.cup_batched_dev(dev, 6, 70, 90, p)
+        body = dev.cpu().numpy().view(np.uint32)
+        for t in range(6):
+            a = mats[t].copy()
+            o = O.port_cup(a, p)
+            assert rk[t] == o.rank and np.array_equal(rrp[t, :o.rank], o.rrp)
+            assert np.array_equal(sig[t], o.sigma) and np.array_equal(body[t], a)
+
+
+def test_large_properties_dev():
+    """At full-size-class dimensions: structural outputs + Freivalds A = C*U*P."""
+    import torch
+    n, p = 4096, 65521
+    src = torch.empty((n, n), dtype=torch.int32, device="cuda")
+    G.random_matrix_dev(src, n, n, 3, p)
+    orig = src.cpu().numpy().view(np.uint32).copy()
+    work = src.clone()
+    r = G.cup_dev(work, n, n, p)
+    body = work.cpu().numpy().view(np.uint32)
+    assert r.rank == n and np.array_equal(r.row_profile, np.arange(n))
+    assert O.freivalds_cup(orig, body, r.rank, r.col_perm, p, trials=2)
+    # determinism: a second run is bit-identical
+    work2 = src.clone()
+    G.cup_dev(work2, n, n, p)
+    assert torch.equal(work, work2)
+
+
+def test_generator_matches_reference():
+    import torch
+    for (m, n, seed, p) in [(37, 53, 5, 65521), (64, 128, 2**64 - 3, 8388593)]:
+        d = torch.empty((m, n), dtype=torch.int32, device="cuda")
+        G.random_matrix_dev(d, m, n, seed, p)
+        assert np.array_equal(d.cpu().numpy().view(np.uint32), O.port_random_matrix(m, n, seed, p))
+
+
+def test_rank_profile_and_determinant():
+    rng = np.random.default_rng(31)
+    for p in (7, 65521):
+        a = rng.integers(0, p, (50, 50), dtype=np.uint64).astype(np.uint32)
+        r, rrp = G.rank_and_profile(a.copy(), p)
+        o = O.port_cup(a.copy(), p)
+        assert r == o.rank and np.array_equal(rrp, o.rrp)
+        if O.have_ref():
+            assert G.determinant(a.copy(), p) == O.ref_determinant(a.copy(), p)
+    # GF(7) worked example with a column swap: det = sign(P) * prod pivots
+    a = np.array([[0, 1], [1, 0]], np.uint32)
+    assert G.determinant(a.copy(), 7) == 6
