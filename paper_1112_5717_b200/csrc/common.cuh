@@ -18,6 +18,7 @@ struct Fp {
     u32 p;
     u32 m32;  // floor((2^32-1)/p): 32-bit Barrett for x < 2^32
     u64 m64;  // floor((2^64-1)/p)
+    u32 r32;  // 2^32 mod p
 };
 
 static inline Fp make_fp(u32 p) {
@@ -25,6 +26,7 @@ static inline Fp make_fp(u32 p) {
     f.p = p;
     f.m32 = (u32)(0xFFFFFFFFu / p);
     f.m64 = ~0ull / (u64)p;
+    f.r32 = (u32)((1ull << 32) % p);
     return f;
 }
 
@@ -39,6 +41,13 @@ __device__ __forceinline__ u32 red32(u32 x, const Fp& f) {
     u32 q = __umulhi(x, f.m32);
     u32 r = x - q * f.p;
     return r >= f.p ? r - f.p : r;
+}
+
+// Short-latency reduction for p <= 2^16 and x < 2^40 (lazy accumulators of at
+// most 2^8 products of canonical elements): x = hi*2^32 + lo with hi < 2^8.
+__device__ __forceinline__ u32 red_sp(u64 x, const Fp& f) {
+    const u32 t = red32((u32)x, f) + (u32)(x >> 32) * f.r32;  // < 2^25
+    return red32(t, f);
 }
 
 __device__ __forceinline__ u32 mulmod(u32 a, u32 b, const Fp& f) {
@@ -66,6 +75,23 @@ __device__ __forceinline__ u32 invmod(u32 a, const Fp& f) {
         e >>= 1;
     }
     return r;
+}
+
+// Asynchronous global -> shared copies (LDGSTS): a copy loop issues every load
+// before anything waits, instead of one memory round trip per iteration.
+// src_bytes = 0 zero-fills the destination (out-of-range elements).
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, bool valid) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(gmem),
+                 "r"(valid ? 4 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // A device-evaluated index: value = (idx >= 0 ? rp[idx] : 0) + cst.  All

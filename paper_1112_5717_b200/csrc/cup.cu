@@ -47,6 +47,12 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
     RL_CUDA_CHECK(cudaMalloc(&ipiv_, sizeof(i32) * (k + 1)));
     RL_CUDA_CHECK(cudaMalloc(&ps_, sizeof(PanelScratch)));
     RL_CUDA_CHECK(cudaMemset(ps_, 0, sizeof(PanelScratch)));
+    RL_CUDA_CHECK(cudaMalloc(&uinv_, sizeof(u32) * PB * PB * (leaf_of_.size() + 1)));
+    if (p_ <= 65536u) {
+        RL_CUDA_CHECK(cudaMalloc(&inv_table_, 65536 * sizeof(uint16_t)));
+        build_inv_table(inv_table_, p_, nullptr);
+        RL_CUDA_CHECK(cudaDeviceSynchronize());
+    }
     if (a2_cap_) RL_CUDA_CHECK(cudaMalloc(&a2_, a2_cap_));
     if (b2_cap_) RL_CUDA_CHECK(cudaMalloc(&b2_, b2_cap_));
 }
@@ -57,6 +63,8 @@ CupEngine::~CupEngine() {
     cudaFree(rrp_);
     cudaFree(ipiv_);
     cudaFree(ps_);
+    cudaFree(uinv_);
+    cudaFree(inv_table_);
     cudaFree(a2_);
     cudaFree(b2_);
 }
@@ -111,8 +119,13 @@ void CupEngine::gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nm
 }
 
 void CupEngine::panel(i32 i0, i32 b) {
-    if (dry_) return;
+    if (dry_) {
+        leaf_of_.emplace(i0, (i32)leaf_of_.size());
+        return;
+    }
     PanelArgs a{};
+    a.uinv = uinv_ + (size_t)leaf_of_.at(i0) * PB * PB;
+    a.inv_table = inv_table_;
     a.A = A_;
     a.lda = lda_;
     a.i0 = i0;
@@ -176,7 +189,7 @@ void CupEngine::trsm_right(i32 r0, i32 M, i32 x0, i32 mx) {
         a.j_lo = dyn_rp(x0);
         a.j_hi = dyn_rp(x0 + mx);
         a.rp = rp_;
-        a.rrp = rrp_;
+        a.uinv = uinv_ + (size_t)leaf_of_.at(x0) * PB * PB;
         a.f = f_;
         trsm_leaf(a, s_);
         stats_.trsm_leaves++;

@@ -2,6 +2,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <unordered_map>
+
 #include "common.cuh"
 
 namespace rl {
@@ -56,6 +58,9 @@ private:
     i32* rrp_ = nullptr;
     i32* ipiv_ = nullptr;
     PanelScratch* ps_ = nullptr;
+    u32* uinv_ = nullptr;                      // one PB x PB block per leaf
+    uint16_t* inv_table_ = nullptr;            // p < 2^16: x -> x^{-1} mod p
+    std::unordered_map<i32, i32> leaf_of_;     // leaf start row -> leaf index
     uint8_t* a2_ = nullptr;
     uint8_t* b2_ = nullptr;
     size_t a2_cap_ = 0, b2_cap_ = 0;

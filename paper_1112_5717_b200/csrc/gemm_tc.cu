@@ -112,6 +112,7 @@ __global__ void __launch_bounds__(256) pack_b_kernel(GemmArgs g, uint8_t* __rest
     constexpr int B_TILE = Cfg<L>::B_TILE;
     constexpr int KQ = 32;
     __shared__ u32 T[KQ][NT + 1];
+    __shared__ i32 s_rowoff[KQ];
     i32 K, N, k_lo, n_lo;
     dyn_shape(g, K, N, k_lo, n_lo);
     if (K <= 0 || N <= 0) return;
@@ -124,16 +125,20 @@ __global__ void __launch_bounds__(256) pack_b_kernel(GemmArgs g, uint8_t* __rest
         const i32 kb = (i32)((blk / 4) % KB);
         const i32 nb = (i32)(blk / (4 * KB));
         __syncthreads();
+        if (threadIdx.x < KQ) {
+            const i32 k = kb * BK + kq * KQ + threadIdx.x;
+            s_rowoff[threadIdx.x] =
+                k < K ? (g.gather ? __ldg(g.gather + k_lo + k) : k_lo + k) : -1;
+        }
+        __syncthreads();
+#pragma unroll 4
         for (int e = threadIdx.x; e < KQ * NT; e += blockDim.x) {
             const int kk = e / NT, nn = e % NT;
-            const i32 k = kb * BK + kq * KQ + kk, n = nb * NT + nn;
-            u32 val = 0;
-            if (k < K && n < N) {
-                const i32 row = g.gather ? __ldg(g.gather + k_lo + k) : k_lo + k;
-                val = __ldg(g.B + (i64)row * g.ldb + n_lo + n);
-            }
-            T[kk][nn] = val;
+            const i32 row = s_rowoff[kk], n = nb * NT + nn;
+            const bool ok = row >= 0 && n < N;
+            cp_async4(&T[kk][nn], ok ? g.B + (i64)row * g.ldb + n_lo + n : g.B, ok);
         }
+        cp_async_wait_all();
         __syncthreads();
         for (int e = threadIdx.x; e < NT * 2; e += blockDim.x) {
             const int nn = e % NT, ch = e / NT;  // chunk within this quarter
@@ -269,40 +274,83 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(GemmArgs g, const uint8
         const u32 alpha = g.alpha, beta = g.beta;
         int acc = 0;
         uint32_t aph = 0;
+        constexpr int NCH = NT / C_::CH;
         for (i32 tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
             const i32 mb = tile % MB, nb = tile / MB;
-            ptx::mbar_wait(&tfull[acc], aph);
-            ptx::tc_fence_after();
             const i32 row = mb * BM + rloc;
             const bool vrow = row < g.M;
             u32* crow = g.C + (i64)(g.c_row0 + (vrow ? row : 0)) * g.ldc + n_lo + nb * NT;
+            // 16-byte vector access when the row segment is aligned (the usual
+            // case: column origins are multiples of the leaf size)
+            const bool vec = ((reinterpret_cast<uintptr_t>(crow) & 15) == 0);
+            // C is independent of the accumulator: fetch chunk 0 before waiting
+            // on the MMA, and every later chunk one step ahead.
+            auto load_chunk = [&](int ch, u32 (&cb)[16]) {
+                const i32 c0 = nb * NT + ch * 16;
+                if (!vrow || beta == 0) return;
+                if (vec && c0 + 16 <= N) {
+                    const uint4* src = reinterpret_cast<const uint4*>(crow + ch * 16);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint4 t4 = src[q];
+                        cb[4 * q + 0] = t4.x;
+                        cb[4 * q + 1] = t4.y;
+                        cb[4 * q + 2] = t4.z;
+                        cb[4 * q + 3] = t4.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int t = 0; t < 16; ++t) cb[t] = (c0 + t < N) ? crow[ch * 16 + t] : 0u;
+                }
+            };
+            u32 cbuf[16];
+#pragma unroll
+            for (int t = 0; t < 16; ++t) cbuf[t] = 0;
+            load_chunk(0, cbuf);
+            ptx::mbar_wait(&tfull[acc], aph);
+            ptx::tc_fence_after();
 #pragma unroll 1
-            for (int ch = 0; ch < NT / C_::CH; ++ch) {
+            for (int ch = 0; ch < NCH; ++ch) {
                 uint32_t sv[L][16];
 #pragma unroll
                 for (int j = 0; j < L; ++j)
                     ptx::tmem_ld16(tmem + lane_base + acc * 256 + j * NT + ch * 16, sv[j]);
+                u32 cnext[16];
+#pragma unroll
+                for (int t = 0; t < 16; ++t) cnext[t] = 0;
+                if (ch + 1 < NCH) load_chunk(ch + 1, cnext);
                 ptx::tc_wait_ld();
                 const i32 c0 = nb * NT + ch * 16;
                 if (vrow) {
+                    u32 outv[16];
 #pragma unroll
                     for (int t = 0; t < 16; ++t) {
-                        if (c0 + t < N) {
-                            u64 x = sv[0][t];
-                            if (L > 1) x += (u64)sv[L > 1 ? 1 : 0][t] << 8;
-                            if (L > 2) x += (u64)sv[L > 2 ? 2 : 0][t] << 16;
-                            if (L > 3) x += (u64)sv[L > 3 ? 3 : 0][t] << 24;
-                            u32 r = red64(x, f);
-                            u32* cp = crow + ch * 16 + t;
-                            u32 cv = beta == 0 ? 0u : (beta == 1 ? *cp : mulmod(*cp, beta, f));
-                            u32 out;
-                            if (alpha == f.p - 1) out = submod(cv, r, f);
-                            else if (alpha == 1) out = addmod(cv, r, f);
-                            else out = addmod(cv, mulmod(r, alpha, f), f);
-                            *cp = out;
-                        }
+                        u64 x = sv[0][t];
+                        if (L > 1) x += (u64)sv[L > 1 ? 1 : 0][t] << 8;
+                        if (L > 2) x += (u64)sv[L > 2 ? 2 : 0][t] << 16;
+                        if (L > 3) x += (u64)sv[L > 3 ? 3 : 0][t] << 24;
+                        const u32 r = red64(x, f);
+                        const u32 cv = (beta == 0 || beta == 1) ? cbuf[t] : mulmod(cbuf[t], beta, f);
+                        u32 out;
+                        if (alpha == f.p - 1) out = submod(cv, r, f);
+                        else if (alpha == 1) out = addmod(cv, r, f);
+                        else out = addmod(cv, mulmod(r, alpha, f), f);
+                        outv[t] = out;
+                    }
+                    if (vec && c0 + 16 <= N) {
+                        uint4* dst = reinterpret_cast<uint4*>(crow + ch * 16);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            dst[q] = make_uint4(outv[4 * q], outv[4 * q + 1], outv[4 * q + 2],
+                                                outv[4 * q + 3]);
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < 16; ++t)
+                            if (c0 + t < N) crow[ch * 16 + t] = outv[t];
                     }
                 }
+#pragma unroll
+                for (int t = 0; t < 16; ++t) cbuf[t] = cnext[t];
             }
             ptx::tc_fence_before();
             ptx::mbar_arrive(&tempty[acc]);
@@ -399,23 +447,22 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
             for (int b = 0; b < 4; ++b) acc[a][b] = 0;
         for (i32 k0 = 0; k0 < K; k0 += 32) {
             __syncthreads();
+#pragma unroll
             for (int e = threadIdx.x; e < 64 * 32; e += 256) {
                 const int r = e / 32, kk = e % 32;
                 const i32 row = mb * 64 + r, k = k0 + kk;
-                As[r][kk] = (row < g.M && k < K)
-                                ? __ldg(g.A + (i64)(g.a_row0 + row) * g.lda + k_lo + k)
-                                : 0u;
+                const bool ok = row < g.M && k < K;
+                cp_async4(&As[r][kk], ok ? g.A + (i64)(g.a_row0 + row) * g.lda + k_lo + k : g.A, ok);
             }
+#pragma unroll
             for (int e = threadIdx.x; e < 32 * 64; e += 256) {
                 const int kk = e / 64, nn = e % 64;
                 const i32 k = k0 + kk, n = nb * 64 + nn;
-                u32 v = 0;
-                if (k < K && n < N) {
-                    const i32 row = g.gather ? __ldg(g.gather + k_lo + k) : k_lo + k;
-                    v = __ldg(g.B + (i64)row * g.ldb + n_lo + n);
-                }
-                Bs[kk][nn] = v;
+                const bool ok = k < K && n < N;
+                const i32 row = ok ? (g.gather ? __ldg(g.gather + k_lo + k) : k_lo + k) : 0;
+                cp_async4(&Bs[kk][nn], ok ? g.B + (i64)row * g.ldb + n_lo + n : g.B, ok);
             }
+            cp_async_wait_all();
             __syncthreads();
 #pragma unroll 8
             for (int kk = 0; kk < 32; ++kk) {

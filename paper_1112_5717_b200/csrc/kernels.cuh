@@ -63,18 +63,19 @@ void gemm_tc_split(const GemmArgs& g, int L, i64 Kmax, i64 Nmax, uint8_t* a2, ui
 void gemm_simt(const GemmArgs& g, i64 Kmax, i64 Nmax, cudaStream_t s);
 
 // ---------------------------------------------------------------------- panel
-constexpr int PB = 64;    // rows per leaf panel
-constexpr int PW = 128;   // leading window width
+constexpr int PB = 64;        // rows per leaf panel
+constexpr int PW = 128;       // leading window width (pivot search)
+constexpr int WT = PW + PB;   // window + identity block (row transform)
 
 struct PanelScratch {
     i32 c0, W, w, r, b;
     u32 flag;      // a window-dead row has a nonzero tail residual -> fallback
     u32 counter;   // last-CTA detection in the tail kernel
+    u64 dead_mask;          // bit i: row i of the leaf has no pivot in the window
     i32 piv_of_row[PB];     // pivot index (local) of row i, -1 if dead
     i32 rank_before[PB];
-    u32 pinv[PB];           // inverse of the true pivot j
-    u32 pivval[PB];         // true pivot j
-    u32 Cr[PB][PB];         // Cr[i][i'] = C(i, piv(i')) for pivot rows i' < i
+    u32 Minv[PB][PB];       // row transform: V = Minv * P (U rows / residuals)
+    u32 Mr[PB][PB];         // its inverse: P = Mr * V (fallback restore)
     u32 win_orig[PB][PW];   // original window (fallback restore)
 };
 
@@ -86,20 +87,25 @@ struct PanelArgs {
     i32* rrp;
     i32* ipiv;
     PanelScratch* ps;
+    u32* uinv;     // PB x PB: inverse of this leaf's unit upper pivot block
+    const uint16_t* inv_table;  // p < 2^16: inv_table[x] = x^{-1} mod p (else unused)
     Fp f;
 };
+// inv_table[x] = x^{-1} mod p for x in [1, p) (p <= 65536), inv_table[0] = 0.
+void build_inv_table(uint16_t* table, u32 p, cudaStream_t s);
 void panel_window(const PanelArgs& a, cudaStream_t s);
 void panel_tail(const PanelArgs& a, cudaStream_t s);
 
 // X <- X * U^{-1} for the unit upper block of one leaf's pivots J = [j_lo, j_hi)
-// (|J| <= PB): rows [row0, row0 + M) of A, columns J; U rows gathered via rrp.
+// (|J| <= PB): rows [row0, row0 + M) of A, columns J; U^{-1} precomputed by
+// the leaf's panel (uinv, PB x PB row-major).
 struct TrsmLeafArgs {
     u32* A;
     i64 lda;
     i32 row0, M;
     Dyn j_lo, j_hi;
     const i32* rp;
-    const i32* rrp;
+    const u32* uinv;
     Fp f;
 };
 void trsm_leaf(const TrsmLeafArgs& a, cudaStream_t s);

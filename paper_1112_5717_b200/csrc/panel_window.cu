@@ -1,0 +1,553 @@
+// panel_window.cu -- pivot discovery for one CUP leaf (the sequential critical
+// path of the whole factorization).  See panel.cu for the leaf schedule.
+//
+// Reference semantics (proj/src/factor.cpp:12-28, 30-81): row i's pivot is the
+// first nonzero at positions >= rank so far, swapped in by a transposition; the
+// C entry C(k, j) is row k's value at pivot column j after eliminating pivots
+// < j; U row j is the pivot row divided by its pivot beyond position j.
+//
+// Layout: the b x w window (w <= PW) plus a b x b identity block is held in
+// registers as 64-bit LAZY accumulators; warp k%8 owns row k, lane l owns
+// positions l + 32q (q < 4 window, q = 4, 5 identity).  Eliminating row k by
+// pivot j (pivot row U_j unnormalised, inverse pinv_j) adds mult * U_j[x] with
+// mult = -C(k,j) * pinv_j to every position (positions <= j become stale: C
+// entries are kept exactly in s_C), so a step is one 64-bit multiply-add per
+// element; only C(k,j) and the searched row are reduced mod p.  The C entries
+// of a warp's 8 rows are gathered by shuffles and turned into multipliers by 8
+// lanes in parallel.  Inverses: a shared-memory table for p < 2^16, Fermat
+// otherwise.  Lockstep with lookahead: in step i the owner of row i+1 first
+// applies pivot i to it, reduces and searches it (warp ballot) and publishes
+// pivot i+1, then every warp updates its remaining rows; one CTA barrier per
+// row.  The identity block yields the row transform Minv: V = Minv * P gives
+// the U rows (pivot rows) and residuals (window-dead rows) of ANY column.
+#include <algorithm>
+
+#include "kernels.cuh"
+#include "runtime.h"
+
+namespace rl {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+template <class T>
+__device__ __forceinline__ T sel4(const T (&v)[6], int q) {
+    T t = v[0];
+    t = (q == 1) ? v[1] : t;
+    t = (q == 2) ? v[2] : t;
+    t = (q == 3) ? v[3] : t;
+    return t;
+}
+template <class T>
+__device__ __forceinline__ void put4(T (&v)[6], int x, T val, int lane) {
+    if (lane == (x & 31)) {
+        const int q = x >> 5;
+        v[0] = (q == 0) ? val : v[0];
+        v[1] = (q == 1) ? val : v[1];
+        v[2] = (q == 2) ? val : v[2];
+        v[3] = (q == 3) ? val : v[3];
+    }
+}
+__device__ __forceinline__ u64 shfl64(u64 v, int src) {
+    const u32 lo = __shfl_sync(FULL, (u32)v, src);
+    const u32 hi = __shfl_sync(FULL, (u32)(v >> 32), src);
+    return ((u64)hi << 32) | lo;
+}
+__device__ __forceinline__ u64 get64(const u64 (&v)[6], int x) { return shfl64(sel4(v, x >> 5), x & 31); }
+__device__ __forceinline__ u32 get32(const u32 (&v)[6], int x) {
+    return __shfl_sync(FULL, sel4(v, x >> 5), x & 31);
+}
+__device__ __forceinline__ void swap64(u64 (&v)[6], int x, int y, int lane) {
+    const u64 vx = get64(v, x), vy = get64(v, y);
+    put4(v, x, vy, lane);
+    put4(v, y, vx, lane);
+}
+__device__ __forceinline__ void swap32(u32 (&v)[6], int x, int y, int lane) {
+    const u32 vx = get32(v, x), vy = get32(v, y);
+    put4(v, x, vy, lane);
+    put4(v, y, vx, lane);
+}
+
+template <bool SP>
+__device__ __forceinline__ void axpy_row(u64 (&acc)[6], u32 mult, const u32 (&U)[6], const Fp& f) {
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+        if (SP) acc[q] += (u64)mult * U[q];
+        else acc[q] = red64(acc[q] + (u64)mult * U[q], f);
+    }
+}
+
+struct WinShared {
+    u32* s_R;            // [PB][WT] row values at search time (reduced)
+    const uint16_t* s_inv;
+    u32 (*s_C)[PB + 1];  // exact C entries C(k, j)
+    int* s_c;            // [2] pivot column of the last searched row (-1: dead)
+    u32* s_pinv;         // [2] its inverse
+    u32* s_pv;           // [PB] pivot values
+    u32* s_pinvA;        // [PB] their inverses
+};
+
+// Reduce row k, find its pivot (first nonzero window position >= rn), publish.
+template <bool SP>
+__device__ __forceinline__ void search_publish(const u64 (&acc)[6], int k, int rn, int w,
+                                               const WinShared& S, int lane, const Fp& f) {
+    u32 vals[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) vals[q] = SP ? red_sp(acc[q], f) : red64(acc[q], f);
+    int c = -1;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int x = lane + 32 * q;
+        const unsigned msk = __ballot_sync(FULL, x >= rn && x < w && vals[q] != 0);
+        if (c < 0 && msk) c = 32 * q + __ffs(msk) - 1;
+    }
+    u32 pinv = 0;
+    if (c >= 0) {
+        if (c != rn) swap32(vals, rn, c, lane);
+        const u32 pv = get32(vals, rn);
+        pinv = SP ? (u32)S.s_inv[pv] : invmod(pv, f);
+        if (lane == 0) {
+            S.s_pv[rn] = pv;
+            S.s_pinvA[rn] = pinv;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q) S.s_R[k * WT + lane + 32 * q] = vals[q];
+    if (lane == 0) {
+        S.s_c[k & 1] = c;
+        S.s_pinv[k & 1] = pinv;
+    }
+}
+
+// Row inext: apply pivot (r, c, pinv, U) if any, then search and publish.
+template <bool SP>
+__device__ __forceinline__ void prio_step(u64 (&acc)[6], int k, bool piv, int r, int c, u32 pinv,
+                                          const u32 (&U)[6], int rn, int w, const WinShared& S,
+                                          int lane, const Fp& f) {
+    if (piv) {
+        if (c != r) swap64(acc, r, c, lane);
+        const u64 ckr = get64(acc, r);
+        const u32 ck = SP ? red_sp(ckr, f) : red64(ckr, f);
+        if (lane == 0) S.s_C[k][r] = ck;
+        const u32 mult = ck ? f.p - mulmod(ck, pinv, f) : 0u;
+        axpy_row<SP>(acc, mult, U, f);
+    }
+    search_publish<SP>(acc, k, rn, w, S, lane, f);
+}
+
+constexpr int NW = 16;      // warps
+constexpr int RW = PB / NW; // rows per warp (row k -> warp k % NW, slot k / NW)
+constexpr int LB = 8;       // leaf block of the speculative LU
+
+// (p - m) * u summed lazily: acc + (p - m) * u
+template <bool SP>
+__device__ __forceinline__ u64 fms(u64 acc, u32 m, u32 u, const Fp& f) {
+    const u32 nm = m ? f.p - m : 0u;
+    if (SP) return acc + (u64)nm * u;
+    return acc + mulmod(nm, u, f);
+}
+// acc + nm * u (nm already negated)
+template <bool SP>
+__device__ __forceinline__ u64 fmsn(u64 acc, u32 nm, u32 u, const Fp& f) {
+    if (SP) return acc + (u64)nm * u;
+    return acc + mulmod(nm, u, f);
+}
+template <bool SP>
+__device__ __forceinline__ u32 fred(u64 x, const Fp& f) {
+    return SP ? red_sp(x, f) : red64(x, f);
+}
+
+// Speculative pivot discovery for GENERIC leaves: blocked right-looking LU of
+// the window without pivoting, in shared memory (s_R = [window | identity],
+// reduced values).  If every diagonal value is nonzero, row i's first nonzero
+// at positions >= i is position i itself, so this IS the CUP of the leaf
+// (rrp = identity, no transpositions).  Leaf blocks of 8 rows are factored by
+// one warp; the block rows' right part is a column-parallel forward
+// substitution; the rows below get their C entries by a row-parallel
+// triangular solve and a rank-8 lazy update.  Returns false (uniformly) on the
+// first zero pivot; the caller then runs the exact lockstep path.
+template <bool SP>
+__device__ bool spec_lu(u32* s_R, u32 (*s_C)[PB + 1], u32* s_pv, u32* s_pinvA,
+                        const uint16_t* s_inv, u32 (*s_M)[LB], int* s_fail, int b, int w,
+                        const Fp& f) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nt = blockDim.x;
+    if (w < b) return false;
+    for (int r0 = 0; r0 < b; r0 += LB) {
+        const int bt = min(LB, b - r0);
+        // (a) leaf: bt x bt diagonal block, element (k, c): lane (k&3)*8 + c, v0 (k<4) / v1
+        if (warp == 0) {
+            const int cc = lane & 7, k0 = lane >> 3, k1 = k0 + 4;
+            u32 v0 = (k0 < bt && cc < bt) ? s_R[(r0 + k0) * WT + r0 + cc] : 0u;
+            u32 v1 = (k1 < bt && cc < bt) ? s_R[(r0 + k1) * WT + r0 + cc] : 0u;
+            int fail = 0;
+            for (int j = 0; j < bt; ++j) {
+                const u32 pv = __shfl_sync(FULL, j < 4 ? v0 : v1, (j & 3) * 8 + j);
+                if (pv == 0) {
+                    fail = 1;
+                    break;
+                }
+                const u32 pinv = SP ? (u32)s_inv[pv] : invmod(pv, f);
+                const u32 c0v = __shfl_sync(FULL, v0, k0 * 8 + j);         // C(k0, j)
+                const u32 c1v = __shfl_sync(FULL, v1, (k1 - 4) * 8 + j);   // C(k1, j)
+                const u32 uj = __shfl_sync(FULL, j < 4 ? v0 : v1, (j & 3) * 8 + cc);
+                const u32 m0 = mulmod(c0v, pinv, f), m1 = mulmod(c1v, pinv, f);
+                if (cc == j) {  // this lane holds C(k, j) for its rows
+                    if (k0 > j && k0 < bt) s_M[r0 + k0][j] = m0 ? f.p - m0 : 0u;
+                    if (k1 > j && k1 < bt) s_M[r0 + k1][j] = m1 ? f.p - m1 : 0u;
+                }
+                if (k0 > j && cc > j) v0 = fred<SP>(fms<SP>(v0, m0, uj, f), f);
+                if (k1 > j && cc > j) v1 = fred<SP>(fms<SP>(v1, m1, uj, f), f);
+                if (lane == 0) {
+                    s_pv[r0 + j] = pv;
+                    s_pinvA[r0 + j] = pinv;
+                }
+            }
+            if (k0 < bt && cc < bt) {
+                s_R[(r0 + k0) * WT + r0 + cc] = v0;
+                if (cc < k0) s_C[r0 + k0][r0 + cc] = v0;
+            }
+            if (k1 < bt && cc < bt) {
+                s_R[(r0 + k1) * WT + r0 + cc] = v1;
+                if (cc < k1) s_C[r0 + k1][r0 + cc] = v1;
+            }
+            if (lane == 0) *s_fail = fail;
+        }
+        __syncthreads();
+        if (*s_fail) return false;
+        const int x0 = r0 + bt;  // first column right of the block
+        // Columns still needed: the rest of the pivot block [x0, b) and the identity
+        // block [PW, WT); window columns >= b hold no pivot on this path (the tail
+        // kernel computes them as V = Minv * P).
+        const int Xw = max(0, b - x0);
+        const int X = Xw + PB;
+        const int R = b - x0;  // rows below the block
+        if (tid < X) {
+            // (b) block rows, column x: forward substitution down the block
+            const int x = tid < Xw ? x0 + tid : PW + (tid - Xw);
+            u32 col[LB];
+#pragma unroll
+            for (int k = 0; k < LB; ++k) {
+                if (k < bt) {
+                    u64 acc = s_R[(r0 + k) * WT + x];
+#pragma unroll
+                    for (int j = 0; j < k; ++j) acc = fmsn<SP>(acc, s_M[r0 + k][j], col[j], f);
+                    col[k] = fred<SP>(acc, f);
+                    s_R[(r0 + k) * WT + x] = col[k];
+                }
+            }
+        } else if (tid >= 256 && tid - 256 < R) {
+            // (c) rows below: C entries against the block and their multipliers
+            const int k = x0 + tid - 256;
+            u32 nm[LB];
+#pragma unroll
+            for (int j = 0; j < LB; ++j) {
+                u64 acc = s_R[k * WT + r0 + j];
+#pragma unroll
+                for (int j2 = 0; j2 < j; ++j2) acc = fmsn<SP>(acc, nm[j2], s_R[(r0 + j2) * WT + r0 + j], f);
+                const u32 cv = fred<SP>(acc, f);
+                s_C[k][r0 + j] = cv;
+                const u32 m = mulmod(cv, s_pinvA[r0 + j], f);
+                nm[j] = m ? f.p - m : 0u;
+            }
+            uint4* dst = reinterpret_cast<uint4*>(&s_M[k][0]);
+            dst[0] = make_uint4(nm[0], nm[1], nm[2], nm[3]);
+            dst[1] = make_uint4(nm[4], nm[5], nm[6], nm[7]);
+        }
+        __syncthreads();
+        // (d) rank-8 update of the rows below (a block with rows below is full: bt == LB)
+        if (R > 0) {
+            const int G = max(1, nt / X);
+            for (int e = tid; e < X * G; e += nt) {
+                const int ex = e % X, g = e / X;
+                const int x = ex < Xw ? x0 + ex : PW + (ex - Xw);
+                u32 u[LB];
+#pragma unroll
+                for (int j = 0; j < LB; ++j) u[j] = s_R[(r0 + j) * WT + x];
+                for (int k = x0 + g; k < b; k += G) {
+                    const uint4* mrow = reinterpret_cast<const uint4*>(&s_M[k][0]);
+                    const uint4 m0 = mrow[0], m1 = mrow[1];
+                    u64 acc = s_R[k * WT + x];
+                    acc = fmsn<SP>(acc, m0.x, u[0], f);
+                    acc = fmsn<SP>(acc, m0.y, u[1], f);
+                    acc = fmsn<SP>(acc, m0.z, u[2], f);
+                    acc = fmsn<SP>(acc, m0.w, u[3], f);
+                    acc = fmsn<SP>(acc, m1.x, u[4], f);
+                    acc = fmsn<SP>(acc, m1.y, u[5], f);
+                    acc = fmsn<SP>(acc, m1.z, u[6], f);
+                    acc = fmsn<SP>(acc, m1.w, u[7], f);
+                    s_R[k * WT + x] = fred<SP>(acc, f);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    return true;
+}
+
+template <bool SP>
+__global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
+    extern __shared__ __align__(16) uint8_t dsm[];
+    __shared__ u32 s_C[PB][PB + 1];
+    __shared__ i32 s_pos[PB], s_rrp[PB], s_rb[PB], s_por[PB];
+    __shared__ u32 s_pv[PB], s_pinvA[PB];
+    __shared__ i32 s_sig[PW];
+    __shared__ int s_c[2];
+    __shared__ u32 s_pinv[2];
+    __shared__ __align__(16) u32 s_M[PB][LB];
+    __shared__ int s_fail;
+    WinShared S;
+    S.s_R = reinterpret_cast<u32*>(dsm);
+    S.s_inv = reinterpret_cast<const uint16_t*>(dsm + PB * WT * 4);
+    S.s_C = s_C;
+    S.s_c = s_c;
+    S.s_pinv = s_pinv;
+    S.s_pv = s_pv;
+    S.s_pinvA = s_pinvA;
+    u32* s_R = S.s_R;
+    PanelScratch* ps = a.ps;
+    const Fp f = a.f;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const i32 c0 = __ldcg(a.rp + a.i0);
+    const i32 W = a.N - c0;
+    const int b = a.b;
+    if (tid == 0) {
+        ps->flag = 0;
+        ps->counter = 0;
+        ps->c0 = c0;
+        ps->b = b;
+        ps->W = W > 0 ? W : 0;
+    }
+    if (W <= 0) {  // rank already n: the rows keep their C data (factor.cpp:47)
+        for (int i = tid; i < b; i += blockDim.x) a.rp[a.i0 + 1 + i] = c0;
+        if (tid == 0) {
+            ps->w = 0;
+            ps->r = 0;
+            ps->dead_mask = 0;
+        }
+        return;
+    }
+    const int w = W < PW ? W : PW;
+    if (SP) {  // 128 KB inverse table
+        const uint4* src = reinterpret_cast<const uint4*>(a.inv_table);
+        uint4* dst = reinterpret_cast<uint4*>(dsm + PB * WT * 4);
+#pragma unroll 4
+        for (int e = tid; e < 65536 * 2 / 16; e += blockDim.x) cp_async16(dst + e, src + e);
+    }
+    u64 acc[RW][6];
+#pragma unroll
+    for (int s = 0; s < RW; ++s) {
+        const int k = warp + NW * s;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int x = lane + 32 * q;
+            u32 val = 0;
+            if (k < b && x < w) val = __ldcg(a.A + (i64)(a.i0 + k) * a.lda + c0 + x);
+            acc[s][q] = val;
+            if (k < b) ps->win_orig[k][x] = val;
+        }
+        acc[s][4] = (lane == k) ? 1u : 0u;
+        acc[s][5] = (lane + 32 == k) ? 1u : 0u;
+    }
+    // stage [window | identity] for the speculative (generic-case) path
+#pragma unroll
+    for (int s = 0; s < RW; ++s) {
+        const int k = warp + NW * s;
+        if (k < b) {
+#pragma unroll
+            for (int q = 0; q < 6; ++q) s_R[k * WT + lane + 32 * q] = (u32)acc[s][q];
+        }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    const bool spec = spec_lu<SP>(s_R, s_C, s_pv, s_pinvA, S.s_inv, s_M, &s_fail, b, w, f);
+    int r = 0;
+    if (spec) {
+        r = b;
+        for (int e = tid; e < b; e += blockDim.x) {
+            s_pos[e] = e;
+            s_rrp[e] = e;
+            s_rb[e] = e;
+            s_por[e] = e;
+        }
+        __syncthreads();
+    } else {
+    // exact lockstep path (any pivot structure): registers still hold the window
+    if (warp == 0) search_publish<SP>(acc[0], 0, 0, w, S, lane, f);
+    __syncthreads();
+    for (int i = 0; i < b; ++i) {
+        const int c = s_c[i & 1];
+        const u32 pinv = s_pinv[i & 1];
+        const bool piv = c >= 0;
+        if (tid == 0) {
+            s_rb[i] = r;
+            s_por[i] = piv ? r : -1;
+            if (piv) {
+                s_pos[r] = c;
+                s_rrp[r] = i;
+            }
+        }
+        u32 U[6];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) U[q] = piv ? s_R[i * WT + lane + 32 * q] : 0u;
+        const int inext = i + 1;
+        const int rn = r + (piv ? 1 : 0);
+        if (inext < b && warp == (inext % NW)) {  // lookahead: row i+1 first
+            switch (inext / NW) {
+#define RL_PRIO(S_)                                                                 \
+    case S_:                                                                       \
+        prio_step<SP>(acc[S_], inext, piv, r, c, pinv, U, rn, w, S, lane, f);     \
+        break;
+                RL_PRIO(0) RL_PRIO(1) RL_PRIO(2) RL_PRIO(3)
+#undef RL_PRIO
+            }
+        }
+        if (piv && warp + NW * (RW - 1) > inext) {
+            // the other rows of this warp (k = warp + NW*s > i+1), branch-free:
+            // ineligible rows get a zero multiplier.
+            if (c != r) {
+#pragma unroll
+                for (int s = 0; s < RW; ++s) {
+                    const int k = warp + NW * s;
+                    if (k > inext && k < b) swap64(acc[s], r, c, lane);
+                }
+            }
+            // gather C(k, r) of the RW rows: lane s receives row s's value
+            u64 mine = 0;
+            const int qr = r >> 5, src = r & 31;
+#pragma unroll
+            for (int s = 0; s < RW; ++s) {
+                const u64 v = shfl64(sel4(acc[s], qr), src);
+                mine = (lane == s) ? v : mine;
+            }
+            u32 mult = 0;
+            {
+                const int k = warp + NW * lane;
+                if (lane < RW && k > inext && k < b) {
+                    const u32 ck = SP ? red_sp(mine, f) : red64(mine, f);
+                    s_C[k][r] = ck;
+                    mult = ck ? f.p - mulmod(ck, pinv, f) : 0u;
+                }
+            }
+#pragma unroll
+            for (int s = 0; s < RW; ++s) axpy_row<SP>(acc[s], __shfl_sync(FULL, mult, s), U, f);
+        }
+        r = rn;
+        __syncthreads();
+    }
+    }  // exact path
+
+    // ------------------------------------------------------------ finalize
+    const int rt = r;
+    if (warp == 1 && lane == 0) {  // window column permutation
+        for (int x = 0; x < PW; ++x) s_sig[x] = x;
+        for (int j = 0; j < rt; ++j) {
+            const int cc = s_pos[j];
+            const int t = s_sig[j];
+            s_sig[j] = s_sig[cc];
+            s_sig[cc] = t;
+        }
+    } else if (warp >= 2 && warp < 4) {  // later transpositions onto the pivot rows
+        const int j = tid - 64;
+        if (j < rt) {
+            u32* Ur = s_R + s_rrp[j] * WT;
+            for (int j2 = j + 1; j2 < rt; ++j2) {
+                const int cc = s_pos[j2];
+                if (cc != j2) {
+                    const u32 t = Ur[j2];
+                    Ur[j2] = Ur[cc];
+                    Ur[cc] = t;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    // (a) pivot-column region [c0, c0 + rt): C entries, raw pivots, normalised U
+    // (b) [c0 + rt, c0 + w): original values in the final column order (the tail
+    //     kernel replaces them with V = Minv * P)
+    for (int e = tid; e < b * PW; e += blockDim.x) {
+        const int k = e / PW, x = e % PW;
+        if (x >= w) continue;
+        u32 val;
+        if (x < rt) {
+            const int rb = s_rb[k], j = s_por[k];
+            if (x < rb) val = s_C[k][x];
+            else if (j < 0) val = 0;
+            else if (x == j) val = s_R[k * WT + x];
+            else val = mulmod(s_R[k * WT + x], s_pinvA[j], f);
+        } else {
+            val = ps->win_orig[k][s_sig[x]];
+        }
+        a.A[(i64)(a.i0 + k) * a.lda + c0 + x] = val;
+    }
+    for (int e = tid; e < PB * PB; e += blockDim.x) {
+        const int k = e / PB, i = e % PB;
+        u32 mi = 0, mr = 0;
+        if (k < b && i < b) {
+            const int j = s_por[k];
+            mi = s_R[k * WT + PW + i];
+            if (j >= 0) mi = mulmod(mi, s_pinvA[j], f);
+            if (i == k) {
+                mr = j >= 0 ? s_pv[j] : 1u % f.p;
+            } else if (i < k) {
+                const int ji = s_por[i];
+                if (ji >= 0) mr = s_C[k][ji];
+            }
+        }
+        ps->Minv[k][i] = mi;
+        ps->Mr[k][i] = mr;
+    }
+    for (int e = tid; e < PB; e += blockDim.x) {
+        const bool real = e < b;
+        ps->piv_of_row[e] = real ? s_por[e] : -1;
+        ps->rank_before[e] = real ? s_rb[e] : rt;
+        if (e < rt) {
+            a.rrp[c0 + e] = a.i0 + s_rrp[e];
+            a.ipiv[c0 + e] = c0 + s_pos[e];
+        }
+        if (real) a.rp[a.i0 + 1 + e] = c0 + s_rb[e] + (s_por[e] >= 0 ? 1 : 0);
+    }
+    if (warp == 0) {
+        u64 mask = 0;
+        for (int k = lane; k < b; k += 32)
+            if (s_por[k] < 0) mask |= 1ull << k;
+        for (int off = 16; off > 0; off >>= 1) mask |= __shfl_xor_sync(FULL, mask, off);
+        if (lane == 0) {
+            ps->dead_mask = mask;
+            ps->w = w;
+            ps->r = rt;
+        }
+    }
+}
+
+__global__ void inv_table_kernel(uint16_t* t, u32 p, Fp f) {
+    const u32 x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x < 65536) t[x] = (x == 0 || x >= p) ? 0 : (uint16_t)invmod(x, f);
+}
+
+}  // namespace
+
+void build_inv_table(uint16_t* table, u32 p, cudaStream_t s) {
+    inv_table_kernel<<<256, 256, 0, s>>>(table, p, make_fp(p));
+    RL_CUDA_CHECK(cudaGetLastError());
+}
+
+void panel_window(const PanelArgs& a, cudaStream_t s) {
+    const bool sp = a.f.p <= 65536u;
+    const size_t smem = sizeof(u32) * PB * WT + (sp ? 65536 * 2 : 0);
+    static bool attr = false;
+    if (!attr) {
+        RL_CUDA_CHECK(cudaFuncSetAttribute(panel_window_kernel<true>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)(sizeof(u32) * PB * WT + 65536 * 2)));
+        RL_CUDA_CHECK(cudaFuncSetAttribute(panel_window_kernel<false>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)(sizeof(u32) * PB * WT)));
+        attr = true;
+    }
+    if (sp) panel_window_kernel<true><<<1, NW * 32, smem, s>>>(a);
+    else panel_window_kernel<false><<<1, NW * 32, smem, s>>>(a);
+    RL_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace rl

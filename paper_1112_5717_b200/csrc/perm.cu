@@ -1,0 +1,138 @@
+// perm.cu -- permutation application, final U-row placement and the seeded
+// input generator.
+//
+// perm_apply_cols (proj/src/perm.cpp:115-125) is applied as the ordered list of
+// transpositions T_{j, ipiv[j]} recorded by the pivot rule (perm.cpp:21-26,
+// factor.cpp:23-24): every row applies the non-trivial ones in increasing j
+// (the list is compacted in shared memory so the common all-identity case
+// costs one scan).  The shift of factor.cpp:62-70, composed over the whole
+// recursion, is one pass at the end (compact_kernel): per column, increasing j.
+#include <algorithm>
+
+#include "kernels.cuh"
+#include "runtime.h"
+
+namespace rl {
+
+namespace {
+
+// Ordered compaction of {j in [lo, hi) : pred(j)} into list[], 256 threads.
+// Returns the count (uniform).  Entries keep increasing order.
+template <class Pred>
+__device__ int collect_ordered(i32 lo, i32 hi, Pred pred, i32* list, int* warp_cnt) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const i32 j = lo + tid;
+    const bool take = j < hi && pred(j);
+    const unsigned msk = __ballot_sync(0xffffffffu, take);
+    if (lane == 0) warp_cnt[warp] = __popc(msk);
+    __syncthreads();
+    int off = 0, tot = 0;
+    for (int w2 = 0; w2 < 8; ++w2) {
+        if (w2 < warp) off += warp_cnt[w2];
+        tot += warp_cnt[w2];
+    }
+    if (take) list[off + __popc(msk & ((1u << lane) - 1))] = j;
+    __syncthreads();
+    return tot;
+}
+
+__global__ void __launch_bounds__(256) swaps_kernel(SwapArgs a) {
+    __shared__ i32 list[256];
+    __shared__ int warp_cnt[8];
+    const i32 j_lo = dyn_eval(a.j_lo, a.rp), j_hi = dyn_eval(a.j_hi, a.rp);
+    if (j_hi <= j_lo) return;
+    i32 M, g_lo = 0;
+    if (a.gather) {
+        g_lo = dyn_eval(a.g_lo, a.rp);
+        M = dyn_eval(a.g_hi, a.rp) - g_lo;
+    } else {
+        M = a.M;
+    }
+    if (M <= 0) return;
+    const i32 row_t = blockIdx.x * blockDim.x + threadIdx.x;
+    // rows handled by this thread: row_t, row_t + stride, ...
+    for (i32 j0 = j_lo; j0 < j_hi; j0 += 256) {
+        const i32* ip = a.ipiv;
+        const int cnt = collect_ordered(
+            j0, min(j_hi, j0 + 256), [ip](i32 j) { return __ldcg(ip + j) != j; }, list, warp_cnt);
+        if (cnt) {
+            for (i32 t = row_t; t < M; t += gridDim.x * blockDim.x) {
+                const i32 row = a.gather ? __ldcg(a.gather + g_lo + t) : a.row0 + t;
+                u32* rr = a.A + (i64)row * a.lda;
+                for (int q = 0; q < cnt; ++q) {
+                    const i32 j = list[q];
+                    const i32 c = __ldcg(ip + j);
+                    const u32 tmp = rr[j];
+                    rr[j] = rr[c];
+                    rr[c] = tmp;
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(256) compact_kernel(u32* A, i64 lda, i32 m, i32 n, const i32* rp,
+                                                      const i32* rrp) {
+    __shared__ i32 list[256];
+    __shared__ int warp_cnt[8];
+    const i32 r = __ldcg(rp + m);
+    const i32 c = blockIdx.x * blockDim.x + threadIdx.x;
+    for (i32 j0 = 0; j0 < r; j0 += 256) {
+        if (j0 >= (i32)((blockIdx.x + 1) * blockDim.x)) break;  // uniform: no column here > j0
+        const int cnt = collect_ordered(
+            j0, min(r, j0 + 256), [rrp](i32 j) { return __ldcg(rrp + j) != j; }, list, warp_cnt);
+        if (c < n) {
+            for (int q = 0; q < cnt; ++q) {
+                const i32 j = list[q];
+                if (c > j) {
+                    const i32 src = __ldcg(rrp + j);
+                    A[(i64)j * lda + c] = A[(i64)src * lda + c];
+                    A[(i64)src * lda + c] = 0;
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void gen_kernel(u32* A, i64 lda, i64 m, i64 n, u64 seed, Fp f) {
+    const i64 total = m * n;
+    for (i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (i64)gridDim.x * blockDim.x) {
+        u64 z = seed + (u64)(t + 1) * 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z = z ^ (z >> 31);
+        const i64 i = t / n, j = t % n;
+        A[i * lda + j] = red64(z, f);
+    }
+}
+
+}  // namespace
+
+void apply_swaps(const SwapArgs& a, cudaStream_t s) {
+    if (a.Mmax <= 0) return;
+    const int grid = std::max(1, std::min((a.Mmax + 255) / 256, 2 * num_sms()));
+    swaps_kernel<<<grid, 256, 0, s>>>(a);
+    RL_CUDA_CHECK(cudaGetLastError());
+}
+
+void compact_u_rows(u32* A, i64 lda, i32 m, i32 n, const i32* rp, const i32* rrp,
+                    cudaStream_t s) {
+    if (m <= 0 || n <= 0) return;
+    compact_kernel<<<(n + 255) / 256, 256, 0, s>>>(A, lda, m, n, rp, rrp);
+    RL_CUDA_CHECK(cudaGetLastError());
+}
+
+void gen_random_matrix(u32* A, i64 lda, i64 m, i64 n, u64 seed, u32 p, cudaStream_t s) {
+    if (m <= 0 || n <= 0) return;
+    const i64 total = m * n;
+    const int grid = (int)std::min<i64>((total + 255) / 256, (i64)num_sms() * 32);
+    gen_kernel<<<grid, 256, 0, s>>>(A, lda, m, n, seed, make_fp(p));
+    RL_CUDA_CHECK(cudaGetLastError());
+}
+
+void fill_rp0(i32* rp, cudaStream_t s) { RL_CUDA_CHECK(cudaMemsetAsync(rp, 0, sizeof(i32), s)); }
+
+}  // namespace rl
