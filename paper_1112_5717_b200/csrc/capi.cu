@@ -179,7 +179,7 @@ void cup_dev_impl(u32* dA, i64 m, i64 n, i64 lda, u32 p, i64* rank, u32* rrp, u3
     {
         std::lock_guard<std::mutex> lk(g_mu);
         CupEngine& e = engine_for(m, n, lda, p);
-        e.run(dA, s, /*use_graph=*/true);
+        e.run(dA, s, /*use_graph=*/m * n >= (1 << 18));  // capture pays off for large plans
         if (!rank && !rrp && !sigma && !ops) return;  // fully asynchronous
         e.results(&r, rrp_h.data(), ipiv_h.data(), s);
     }
@@ -285,10 +285,30 @@ int rl_cup_u32(uint32_t* A, int64_t m, int64_t n, int64_t lda, uint32_t p, int64
         cudaStream_t s = cudaStreamPerThread;
         u32* dA = (u32*)g_bufA.get((size_t)m * n * 4);
         copy_h2d_2d(dA, n, A, lda, m, n, s);
+        if (m <= 64 && n <= 256) {
+            // Small matrices: the whole factorization in one CTA (one launch), the
+            // same pivot rule and placement as the recursive path.
+            const i64 kcap = std::min(m, n);
+            i32* dmeta = (i32*)g_bufI.get((size_t)(1 + 2 * kcap) * 4);
+            cup_batched(dA, 1, (i32)m, (i32)n, m * n, p, dmeta, dmeta + 1, dmeta + 1 + kcap,
+                        (i32)kcap, s);
+            copy_d2h_2d(A, lda, dA, n, m, n, s);
+            std::vector<i32> meta((size_t)(1 + 2 * kcap));
+            RL_CUDA_CHECK(cudaMemcpyAsync(meta.data(), dmeta, meta.size() * 4, cudaMemcpyDeviceToHost, s));
+            RL_CUDA_CHECK(cudaStreamSynchronize(s));
+            const i64 r = meta[0];
+            const u32* rrp_h = (const u32*)&meta[1];
+            const u32* ipiv_h = (const u32*)&meta[1 + kcap];
+            if (rank) *rank = r;
+            if (rrp) std::copy(rrp_h, rrp_h + r, rrp);
+            if (sigma) sigma_from_ipiv(n, r, ipiv_h, sigma);
+            if (ops) cup_opcount(m, n, r, rrp_h, ipiv_h, ops);
+            return;
+        }
         i64 r = 0;
         std::vector<u32> rrp_h((size_t)std::min(m, n)), ipiv_h((size_t)std::min(m, n));
         CupEngine& e = engine_for(m, n, n, p);
-        e.run(dA, s, true);
+        e.run(dA, s, m * n >= (1 << 18));
         copy_d2h_2d(A, lda, dA, n, m, n, s);
         e.results(&r, rrp_h.data(), ipiv_h.data(), s);  // synchronises s
         if (rank) *rank = r;

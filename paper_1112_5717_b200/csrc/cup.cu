@@ -178,7 +178,39 @@ void CupEngine::swaps_gather(Dyn g_lo, Dyn g_hi, i32 Mmax, Dyn j_lo, Dyn j_hi) {
 
 // G <- G * U_X^{-1} for the unit upper block of node X = rows [x0, x0+mx)
 // (trsm Right/Upper/Unit, kernels.cpp:149-154, recursing along X's own skeleton).
+static void collect_leaves(i32 x0, i32 mx, std::vector<std::pair<i32, i32>>& out) {
+    if (mx <= PB) {
+        out.emplace_back(x0, mx);
+        return;
+    }
+    collect_leaves(x0, mx / 2, out);
+    collect_leaves(x0 + mx / 2, mx - mx / 2, out);
+}
+
 void CupEngine::trsm_right(i32 r0, i32 M, i32 x0, i32 mx) {
+    if (fused_trsm_ && mx <= TN_MAXLEAF * PB) {  // <= 4 leaves: one fused kernel
+        if (dry_) return;
+        std::vector<std::pair<i32, i32>> lv;
+        collect_leaves(x0, mx, lv);
+        TrsmNodeArgs a{};
+        a.A = A_;
+        a.lda = lda_;
+        a.row0 = r0;
+        a.M = M;
+        a.nleaf = (int)lv.size();
+        for (int l = 0; l < a.nleaf; ++l) {
+            a.j_lo[l] = dyn_rp(lv[l].first);
+            a.j_hi[l] = dyn_rp(lv[l].first + lv[l].second);
+            a.uinv[l] = uinv_ + (size_t)leaf_of_.at(lv[l].first) * PB * PB;
+        }
+        a.rp = rp_;
+        a.rrp = rrp_;
+        a.f = f_;
+        trsm_node(a, s_);
+        stats_.trsm_leaves++;
+        stats_.launches += 1;
+        return;
+    }
     if (mx <= PB) {
         if (dry_) return;
         TrsmLeafArgs a{};

@@ -52,6 +52,7 @@ private:
     int L_;
     bool dry_ = false;
     bool use_tc_ = true;
+    bool fused_trsm_ = true;
     u32* A_ = nullptr;
     cudaStream_t s_ = nullptr;
     i32* rp_ = nullptr;

@@ -110,6 +110,24 @@ struct TrsmLeafArgs {
 };
 void trsm_leaf(const TrsmLeafArgs& a, cudaStream_t s);
 
+// G <- G * U_X^{-1} for a skeleton node X of <= 4 leaves (<= 256 rows, pivots
+// J = [j_lo[0], j_hi[nleaf-1]) contiguous): block forward substitution fused in
+// one kernel (per 64-row tile of G: G_l = (B_l - sum_{l'<l} G_l' U_{l'l}) Uinv_l),
+// replacing nleaf leaf solves and nleaf-1 GEMMs.
+constexpr int TN_MAXLEAF = 4;
+struct TrsmNodeArgs {
+    u32* A;
+    i64 lda;
+    i32 row0, M;
+    int nleaf;
+    Dyn j_lo[TN_MAXLEAF], j_hi[TN_MAXLEAF];
+    const u32* uinv[TN_MAXLEAF];
+    const i32* rp;
+    const i32* rrp;
+    Fp f;
+};
+void trsm_node(const TrsmNodeArgs& a, cudaStream_t s);
+
 // ---------------------------------------------------------------- permutation
 // Apply the transpositions T_{j, ipiv[j]} for j in [j_lo, j_hi) in increasing j
 // to rows of A (perm_apply_cols of factor.cpp:42 / :56).  Rows are either the

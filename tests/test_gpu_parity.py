@@ -21,15 +21,31 @@ def _digests():
         return json.load(f)
 
 
+def _cup_recursive(a, p, ctr=None):
+    """The device entry point always runs the recursive engine (the host entry
+    routes small matrices to the single-CTA kernel)."""
+    import torch
+    m, n = a.shape
+    if m * n == 0:
+        return G.cup(a, p, ctr)
+    d = torch.from_numpy(a.view(np.int32).copy()).cuda()
+    r = G.cup_dev(d, m, n, p, ctr=ctr)
+    a[...] = d.cpu().numpy().view(np.uint32)
+    return r
+
+
 def _check_cup(a, p, ctr_check=False):
-    a_gpu, a_or = a.copy(), a.copy()
-    ctr = G.OpCounter()
-    g = G.cup(a_gpu, p, ctr)
-    o = O.port_cup(a_or, p)
-    assert g.rank == o.rank
-    assert np.array_equal(g.row_profile, o.rrp)
-    assert np.array_equal(g.col_perm, o.sigma)
-    assert np.array_equal(a_gpu, a_or), f"body mismatch at {np.argwhere(a_gpu != a_or)[:5]}"
+    o_body = a.copy()
+    o = O.port_cup(o_body, p)
+    for fn in (G.cup, _cup_recursive):
+        a_gpu = a.copy()
+        ctr = G.OpCounter()
+        g = fn(a_gpu, p, ctr)
+        assert g.rank == o.rank, fn.__name__
+        assert np.array_equal(g.row_profile, o.rrp), fn.__name__
+        assert np.array_equal(g.col_perm, o.sigma), fn.__name__
+        assert np.array_equal(a_gpu, o_body), f"{fn.__name__}: body mismatch at {np.argwhere(a_gpu != o_body)[:5]}"
+    a_gpu, a_or = a_gpu, o_body
     if ctr_check and O.have_ref():
         r = O.ref_cup(a.copy(), p)
         assert [ctr.n_mul, ctr.n_addsub, ctr.n_divinv, ctr.n_ztest] == r.ops.tolist()
@@ -39,14 +55,15 @@ def _check_cup(a, p, ctr_check=False):
 def test_golden_cup_cases():
     for c in load_npz_cases(os.path.join(GOLDEN, "cup_small.npz"),
                             ["p", "a", "body", "rank", "rrp", "sigma", "ops"]):
-        a = c["a"].copy()
-        ctr = G.OpCounter()
-        r = G.cup(a, int(c["p"]), ctr)
-        assert r.rank == int(c["rank"])
-        assert np.array_equal(r.row_profile, c["rrp"])
-        assert np.array_equal(r.col_perm, c["sigma"])
-        assert np.array_equal(a, c["body"])
-        assert [ctr.n_mul, ctr.n_addsub, ctr.n_divinv, ctr.n_ztest] == c["ops"].tolist()
+        for fn in (G.cup, _cup_recursive):
+            a = c["a"].copy()
+            ctr = G.OpCounter()
+            r = fn(a, int(c["p"]), ctr)
+            assert r.rank == int(c["rank"])
+            assert np.array_equal(r.row_profile, c["rrp"])
+            assert np.array_equal(r.col_perm, c["sigma"])
+            assert np.array_equal(a, c["body"])
+            assert [ctr.n_mul, ctr.n_addsub, ctr.n_divinv, ctr.n_ztest] == c["ops"].tolist()
 
 
 def test_golden_mm_cases():
