@@ -178,6 +178,22 @@ def reference_arm(args, rank, world):
 
 
 # ----------------------------------------------------------------- our arm
+def _ncu_traffic():
+    """DRAM bytes (read + write) per gemm_tc_kernel launch at 8192^3 from the
+    committed ncu --set full capture, or None."""
+    path = os.path.join(ROOT, "profiles", "round1", "gemm_8192_ncu.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        tot = 0.0
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            tot += float(d[k]["value"]) * scale[d[k]["unit"]]
+        return tot
+    except Exception:
+        return None
+
+
 def measure_int8_peak(torch, iters=10):
     """cuBLAS int8 dense GEMM (torch._int_mm) 8192^3, best of `iters` (burst)."""
     n = 8192
@@ -291,7 +307,10 @@ def ours(args, rank, world, local_rank):
             "frac": tops / peak,
             "peak_source": "measured live: cuBLAS int8 dense GEMM 8192^3 (torch._int_mm), burst",
             "shape": [gm, gm, gm], "ms_gemm": ms_gemm, "ms_pack": ms_pack,
-            "traffic": None,
+            "traffic": _ncu_traffic(),
+            "traffic_note": "dram read+write bytes per launch of the same shape from one "
+                            "ncu --set full capture (profiles/round1/gemm_8192_ncu.json); "
+                            "algorithmic bytes 0.94e9",
             "cup_frac_of_peak": cup_int8 / peak,
             "cup_modp_peak": peak * 1e12 / (L * L),
         }
