@@ -54,6 +54,13 @@ __device__ __forceinline__ u32 mulmod(u32 a, u32 b, const Fp& f) {
     return red64((u64)a * b, f);
 }
 
+// a, b < p <= 2^16: the product fits 32 bits.
+__device__ __forceinline__ u32 mulmod_sp(u32 a, u32 b, const Fp& f) { return red32(a * b, f); }
+template <bool SP>
+__device__ __forceinline__ u32 mulmod_t(u32 a, u32 b, const Fp& f) {
+    return SP ? mulmod_sp(a, b, f) : mulmod(a, b, f);
+}
+
 __device__ __forceinline__ u32 addmod(u32 a, u32 b, const Fp& f) {
     u32 s = a + b;  // a,b < 2^31 so no wrap
     return s >= f.p ? s - f.p : s;

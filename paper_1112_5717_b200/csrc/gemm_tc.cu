@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(256) pack_b_kernel(GemmArgs g, uint8_t* __rest
 
 // -------------------------------------------------------------- the GEMM
 template <int L>
-__global__ void __launch_bounds__(192, 1) gemm_tc_kernel(GemmArgs g, const uint8_t* __restrict__ a2,
+__global__ void __launch_bounds__(320, 1) gemm_tc_kernel(GemmArgs g, const uint8_t* __restrict__ a2,
                                                          const uint8_t* __restrict__ b2) {
     using C_ = Cfg<L>;
     constexpr int NT = C_::NT, UN = C_::UN, STAGES = C_::STAGES, STAGE = C_::STAGE;
@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(GemmArgs g, const uint8
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull[a], 1);
-            ptx::mbar_init(&tempty[a], 128);
+            ptx::mbar_init(&tempty[a], 256);
         }
         ptx::fence_mbar_init();
     }
@@ -266,15 +266,20 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(GemmArgs g, const uint8
                 if (acc == 0) aph ^= 1;
             }
         }
-    } else {  // ---- epilogue warps 2..5: TMEM -> registers -> exact mod-p -> C
+    } else {  // ---- epilogue warps 2..9: TMEM -> registers -> exact mod-p -> C
+        // Two warps per TMEM lane quadrant (warp & 3), each owning half of the
+        // tile's columns.  All of a warp's C chunks are requested before it waits
+        // on the accumulator, so the C read latency overlaps the MMAs.
         const int q = warp & 3;  // TMEM lane quadrant this warp may access
+        const int half = (warp - 2) >> 2;
         const int rloc = q * 32 + lane;
         const uint32_t lane_base = (uint32_t)(q * 32) << 16;
         const Fp f = g.f;
         const u32 alpha = g.alpha, beta = g.beta;
         int acc = 0;
         uint32_t aph = 0;
-        constexpr int NCH = NT / C_::CH;
+        constexpr int NCHH = NT / C_::CH / 2;        // chunks per half tile
+        constexpr int PF = NCHH < 4 ? NCHH : 4;      // chunks prefetched ahead
         for (i32 tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
             const i32 mb = tile % MB, nb = tile / MB;
             const i32 row = mb * BM + rloc;
@@ -283,42 +288,42 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(GemmArgs g, const uint8
             // 16-byte vector access when the row segment is aligned (the usual
             // case: column origins are multiples of the leaf size)
             const bool vec = ((reinterpret_cast<uintptr_t>(crow) & 15) == 0);
-            // C is independent of the accumulator: fetch chunk 0 before waiting
-            // on the MMA, and every later chunk one step ahead.
             auto load_chunk = [&](int ch, u32 (&cb)[16]) {
                 const i32 c0 = nb * NT + ch * 16;
+#pragma unroll
+                for (int t = 0; t < 16; ++t) cb[t] = 0;
                 if (!vrow || beta == 0) return;
                 if (vec && c0 + 16 <= N) {
                     const uint4* src = reinterpret_cast<const uint4*>(crow + ch * 16);
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint4 t4 = src[q];
-                        cb[4 * q + 0] = t4.x;
-                        cb[4 * q + 1] = t4.y;
-                        cb[4 * q + 2] = t4.z;
-                        cb[4 * q + 3] = t4.w;
+                    for (int v = 0; v < 4; ++v) {
+                        const uint4 t4 = src[v];
+                        cb[4 * v + 0] = t4.x;
+                        cb[4 * v + 1] = t4.y;
+                        cb[4 * v + 2] = t4.z;
+                        cb[4 * v + 3] = t4.w;
                     }
                 } else {
 #pragma unroll
                     for (int t = 0; t < 16; ++t) cb[t] = (c0 + t < N) ? crow[ch * 16 + t] : 0u;
                 }
             };
-            u32 cbuf[16];
+            u32 cbuf[PF][16];
 #pragma unroll
-            for (int t = 0; t < 16; ++t) cbuf[t] = 0;
-            load_chunk(0, cbuf);
+            for (int c = 0; c < PF; ++c) load_chunk(half * NCHH + c, cbuf[c]);
             ptx::mbar_wait(&tfull[acc], aph);
             ptx::tc_fence_after();
-#pragma unroll 1
-            for (int ch = 0; ch < NCH; ++ch) {
+#pragma unroll
+            for (int cc = 0; cc < NCHH; ++cc) {
+                const int ch = half * NCHH + cc;
                 uint32_t sv[L][16];
 #pragma unroll
                 for (int j = 0; j < L; ++j)
                     ptx::tmem_ld16(tmem + lane_base + acc * 256 + j * NT + ch * 16, sv[j]);
-                u32 cnext[16];
+                u32 cur[16];
 #pragma unroll
-                for (int t = 0; t < 16; ++t) cnext[t] = 0;
-                if (ch + 1 < NCH) load_chunk(ch + 1, cnext);
+                for (int t = 0; t < 16; ++t) cur[t] = cbuf[cc % PF][t];
+                if (cc + PF < NCHH) load_chunk(ch + PF, cbuf[cc % PF]);
                 ptx::tc_wait_ld();
                 const i32 c0 = nb * NT + ch * 16;
                 if (vrow) {
@@ -330,7 +335,7 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(GemmArgs g, const uint8
                         if (L > 2) x += (u64)sv[L > 2 ? 2 : 0][t] << 16;
                         if (L > 3) x += (u64)sv[L > 3 ? 3 : 0][t] << 24;
                         const u32 r = red64(x, f);
-                        const u32 cv = (beta == 0 || beta == 1) ? cbuf[t] : mulmod(cbuf[t], beta, f);
+                        const u32 cv = (beta == 0 || beta == 1) ? cur[t] : mulmod(cur[t], beta, f);
                         u32 out;
                         if (alpha == f.p - 1) out = submod(cv, r, f);
                         else if (alpha == 1) out = addmod(cv, r, f);
@@ -340,17 +345,15 @@ __global__ void __launch_bounds__(192, 1) gemm_tc_kernel(GemmArgs g, const uint8
                     if (vec && c0 + 16 <= N) {
                         uint4* dst = reinterpret_cast<uint4*>(crow + ch * 16);
 #pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            dst[q] = make_uint4(outv[4 * q], outv[4 * q + 1], outv[4 * q + 2],
-                                                outv[4 * q + 3]);
+                        for (int v = 0; v < 4; ++v)
+                            dst[v] = make_uint4(outv[4 * v], outv[4 * v + 1], outv[4 * v + 2],
+                                                outv[4 * v + 3]);
                     } else {
 #pragma unroll
                         for (int t = 0; t < 16; ++t)
                             if (c0 + t < N) crow[ch * 16 + t] = outv[t];
                     }
                 }
-#pragma unroll
-                for (int t = 0; t < 16; ++t) cbuf[t] = cnext[t];
             }
             ptx::tc_fence_before();
             ptx::mbar_arrive(&tempty[acc]);
@@ -393,7 +396,7 @@ void launch_tc(const GemmArgs& g, i64 Kmax, i64 Nmax, uint8_t* a2, uint8_t* b2, 
         attr_set = true;
     }
     int grid = (int)std::min<i64>(MB * NB, nsm);
-    gemm_tc_kernel<L><<<std::max(grid, 1), 192, C_::SMEM, s>>>(g, a2, b2);
+    gemm_tc_kernel<L><<<std::max(grid, 1), 320, C_::SMEM, s>>>(g, a2, b2);
     RL_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -1,34 +1,23 @@
-// panel.cu -- base case of the CUP recursion on a leaf of b <= PB rows, and the
-// leaf triangular solve.
+// panel.cu -- the leaf's tail (everything right of its pivot columns), the leaf
+// U^{-1}, the exact fallback, and the single-leaf triangular solve.
 //
 // Reference: cup_base_row and the row-halving recursion (proj/src/factor.cpp:12-85).
-// A leaf is the CUP of a b x W block (W = n - rank_before(leaf)): the pivot of
-// row i is the first nonzero at positions >= rank so far (factor.cpp:15-21),
-// brought to position r by a transposition (factor.cpp:23-24), kept raw while
-// the rest of the row is scaled by its inverse (factor.cpp:25-26), and later
-// rows are eliminated (factor.cpp:51-52).  Given the pivot rule the result is
-// unique, so this schedule is bit-exact:
+// A leaf is the CUP of a b x W block (W = n - rank_before(leaf)).  Given the
+// pivot rule the result is unique, so this schedule is
+// bit-exact:
 //
-//  panel_window_kernel (one CTA: the sequential critical path)
-//    The leading b x w window (w <= PW) plus a b x b identity block lives in
-//    registers as 64-bit LAZY accumulators (warp k%8 owns row k, lane l owns
-//    columns l + 32q): eliminating row k by pivot j adds mult * U_j[x] with
-//    mult = -C(k,j) * pinv_j, and only the two values per row that decide
-//    something are reduced (C(k,j) and, at search time, the row itself), so a
-//    pivot step costs one 64-bit multiply-add per element.  Inverses come from
-//    a shared-memory table for p < 2^16.  Lockstep with lookahead: during step
-//    i the owner of row i+1 first applies pivot i to it, searches it (warp
-//    ballot) and publishes the next pivot, then everyone updates the other
-//    rows -- one CTA barrier per pivot.  The identity block yields the row
-//    transform Minv with V = Minv * P (U rows for pivot rows, residuals for
-//    window-dead rows) for ANY column.
+//  panel_window_kernel (panel_window.cu, one CTA: the sequential critical path)
+//    finds the leaf's pivots in its leading window and the row transform Minv:
+//    V = Minv * P gives the U rows (pivot rows) and the residuals (window-dead
+//    rows) of ANY column P of the leaf's rows.
 //  panel_tail_kernel (grid)
-//    V = Minv * P on 64 x 64 column tiles right of the leaf's pivot columns
-//    (lower-triangular, lazy accumulation).  Window-dead rows must come out
-//    zero; otherwise a pivot lies beyond the window and the last CTA re-runs
-//    the leaf exactly (restore P = Mr * V, row-by-row elimination over the full
-//    width).  One extra CTA inverts the leaf's unit upper pivot block for the
-//    TRSMs against it.
+//    V = Minv * P on 64 x 256 column tiles right of the pivot columns
+//    (lower-triangular, 8 x 8 outputs per thread, lazy 64-bit accumulation).
+//    Window-dead rows must come out zero; otherwise a pivot lies beyond the
+//    window and the last CTA re-runs the leaf exactly (restore P = Mr * V,
+//    row-by-row elimination over the full width).  One extra CTA inverts the
+//    leaf's unit upper pivot block (blocked, 8 x 8 diagonal blocks) for the TRSMs
+//    against it.
 #include <algorithm>
 
 #include "kernels.cuh"
@@ -38,13 +27,16 @@ namespace rl {
 
 namespace {
 
+constexpr int TT = 256;  // tail tile width (columns per CTA tile)
 
-// Inverse of the leaf's unit upper pivot block U (r x r, rows rrp[c0+j], columns
-// c0+j'), into uinv (PB x PB, zero padded).  One CTA of 256 threads: 4 threads
-// per column, back substitution X[i][c] = -sum_{k=i+1..c} U[i][k] X[k][c].
+// Inverse of the leaf's unit upper pivot block U (r x r, rows rrp[c0+j],
+// columns c0+j'), into uinv (PB x PB, zero padded).  Blocked: the eight 8 x 8
+// diagonal blocks are inverted by eight warps at once, then block rows from the
+// bottom: X_I,J = -X_I,I * sum_{K=I+1..J} U_I,K X_K,J.
+template <bool SP>
 __device__ void leaf_uinv(const PanelArgs& a, i32 c0, int rt, u32 (*U)[PB + 1], u32 (*X)[PB + 1]) {
     const Fp f = a.f;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     __shared__ i32 s_row[PB];
     if (tid < PB) s_row[tid] = tid < rt ? __ldcg(a.rrp + c0 + tid) : 0;
     __syncthreads();
@@ -53,29 +45,71 @@ __device__ void leaf_uinv(const PanelArgs& a, i32 c0, int rt, u32 (*U)[PB + 1], 
         const int i = e / PB, k = e % PB;
         const bool ok = i < k && k < rt;
         cp_async4(&U[i][k], ok ? a.A + (i64)s_row[i] * a.lda + c0 + k : a.A, ok);
-        X[i][k] = (i == k && i < rt) ? 1u % f.p : 0u;
+        X[i][k] = 0;
     }
     cp_async_wait_all();
     __syncthreads();
-    // rows of X from the bottom: X[i][:] = e_i - sum_{k>i} U[i][k] X[k][:];
-    // thread = (column c, quarter part of the k range), products summed lazily
-    // in 64 bits when p < 2^16 (<= 64 terms < 2^32 each).
-    const int c = tid >> 2, part = tid & 3;
-    const unsigned gm = 0xFu << ((tid & 31) & ~3);  // the 4 lanes of this column
-    const bool sp = f.p <= 65536u;
-    for (int i = rt - 2; i >= 0; --i) {
-        u64 acc = 0;
-        if (c > i && c < rt) {
-            for (int k = i + 1 + part; k <= c; k += 4) {
-                if (sp) acc += (u64)U[i][k] * X[k][c];
-                else acc += mulmod(U[i][k], X[k][c], f);
+    // diagonal blocks: warp w, lane c < 8 -> column c of block w
+    if (warp < 8 && lane < 8) {
+        const int base = 8 * warp, c = lane;
+        u32 x[8];
+#pragma unroll
+        for (int i = 7; i >= 0; --i) {
+            u64 acc = 0;
+#pragma unroll
+            for (int k = i + 1; k < 8; ++k) acc += mulmod_t<SP>(U[base + i][base + k], x[k], f);
+            const u32 s = red64(acc, f);
+            const u32 d = (i == c && base + i < rt) ? 1u % f.p : 0u;
+            x[i] = i > c ? 0u : submod(d, s, f);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) X[base + i][base + c] = x[i];
+    }
+    __syncthreads();
+    for (int I = 6; I >= 0; --I) {
+        const int r0 = 8 * I, cstart = r0 + 8, ncol = PB - cstart;
+        // T = sum_{q = cstart..col} U[r0 + r][q] X[q][col]  -> into X's block row
+        u32 t[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int e = tid + h * blockDim.x;
+            t[h] = 0;
+            if (e < 8 * ncol) {
+                const int r = e / ncol, col = cstart + e % ncol;
+                u64 acc = 0;
+                for (int q = cstart; q <= col; ++q) {
+                    if (SP) acc += (u64)U[r0 + r][q] * X[q][col];
+                    else acc += mulmod(U[r0 + r][q], X[q][col], f);
+                }
+                t[h] = red64(acc, f);
             }
         }
-        acc += __shfl_xor_sync(gm, acc, 1);
-        acc += __shfl_xor_sync(gm, acc, 2);
-        if (part == 0 && c > i && c < rt) {
-            const u32 s = red64(acc, f);
-            X[i][c] = s ? f.p - s : 0u;
+        __syncthreads();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int e = tid + h * blockDim.x;
+            if (e < 8 * ncol) X[r0 + e / ncol][cstart + e % ncol] = t[h];
+        }
+        __syncthreads();
+        // X_I,: = -X_I,I * T
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int e = tid + h * blockDim.x;
+            t[h] = 0;
+            if (e < 8 * ncol) {
+                const int r = e / ncol, col = cstart + e % ncol;
+                u64 acc = 0;
+#pragma unroll
+                for (int s = 0; s < 8; ++s) acc += mulmod_t<SP>(X[r0 + r][r0 + s], X[r0 + s][col], f);
+                const u32 v = red64(acc, f);
+                t[h] = v ? f.p - v : 0u;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int e = tid + h * blockDim.x;
+            if (e < 8 * ncol) X[r0 + e / ncol][cstart + e % ncol] = t[h];
         }
         __syncthreads();
     }
@@ -168,13 +202,13 @@ __device__ void panel_fallback(const PanelArgs& a, u32* red_buf) {
     __syncthreads();
 }
 
-// V = Minv * P on 64-column tiles (4 x 4 outputs per thread), the window-dead
-// row check, and (last CTA) the exact fallback; the extra last-index CTA
-// computes the leaf's U^{-1}.
+// V = Minv * P on 64 x TT column tiles: thread (ty, tx) owns rows 8ty..8ty+7 and
+// columns tx + 32y (y < 8) -- conflict-free shared loads, coalesced stores.
 template <bool SP>
 __global__ void __launch_bounds__(256) panel_tail_kernel(PanelArgs a) {
-    __shared__ u32 Mi[PB][PB + 1];
-    __shared__ u32 Ps[PB][PB + 1];
+    extern __shared__ __align__(16) u32 tsm[];
+    u32 (*Mi)[PB + 1] = reinterpret_cast<u32 (*)[PB + 1]>(tsm);               // [PB][PB+1]
+    u32 (*Ps)[TT + 4] = reinterpret_cast<u32 (*)[TT + 4]>(tsm + PB * (PB + 1)); // [PB][TT+4]
     __shared__ u32 red_buf[256];
     __shared__ int s_last;
     PanelScratch* ps = a.ps;
@@ -183,57 +217,59 @@ __global__ void __launch_bounds__(256) panel_tail_kernel(PanelArgs a) {
     const i32 c0 = ps->c0, W = ps->W, b = ps->b, rt = ps->r;
     u32 bad = 0;
     if (blockIdx.x == gridDim.x - 1) {
-        if (W > 0 && rt > 0) leaf_uinv(a, c0, rt, Mi, Ps);
+        if (W > 0 && rt > 0) {
+            leaf_uinv<SP>(a, c0, rt, Mi, reinterpret_cast<u32 (*)[PB + 1]>(tsm + 2 * PB * (PB + 1)));
+        }
     } else if (W > 0) {
         const u64 dead = ps->dead_mask;
 #pragma unroll 4
         for (int e = tid; e < PB * PB; e += blockDim.x)
             cp_async4(&Mi[e / PB][e % PB], &ps->Minv[e / PB][e % PB], true);
-        const int tx = tid & 15, ty = tid >> 4;
+        const int tx = tid & 31, ty = tid >> 5;
         const i32 col0 = c0 + rt;
-        const i32 ntile = (a.N - col0 + 63) / 64;
+        const i32 ntile = (a.N - col0 + TT - 1) / TT;
         for (i32 t = blockIdx.x; t < ntile; t += gridDim.x - 1) {
-            const i32 cb = col0 + t * 64;
+            const i32 cb = col0 + t * TT;
             __syncthreads();
 #pragma unroll 4
-            for (int e = tid; e < PB * 64; e += blockDim.x) {
-                const int i = e >> 6, cc = e & 63;
+            for (int e = tid; e < PB * TT; e += blockDim.x) {
+                const int i = e / TT, cc = e % TT;
                 const bool ok = i < b && cb + cc < a.N;
                 cp_async4(&Ps[i][cc], ok ? a.A + (i64)(a.i0 + i) * a.lda + cb + cc : a.A, ok);
             }
             cp_async_wait_all();
             __syncthreads();
-            u64 acc[4][4];
+            u64 acc[8][8];
 #pragma unroll
-            for (int x = 0; x < 4; ++x)
+            for (int x = 0; x < 8; ++x)
 #pragma unroll
-                for (int y = 0; y < 4; ++y) acc[x][y] = 0;
-            const int kmax = min(b, ty * 4 + 4);
+                for (int y = 0; y < 8; ++y) acc[x][y] = 0;
+            const int kmax = min(b, ty * 8 + 8);
             for (int k = 0; k < kmax; ++k) {
-                u32 mv[4], pv[4];
+                u32 mv[8], pv[8];
 #pragma unroll
-                for (int x = 0; x < 4; ++x) mv[x] = Mi[ty * 4 + x][k];
+                for (int x = 0; x < 8; ++x) mv[x] = Mi[ty * 8 + x][k];
 #pragma unroll
-                for (int y = 0; y < 4; ++y) pv[y] = Ps[k][tx * 4 + y];
+                for (int y = 0; y < 8; ++y) pv[y] = Ps[k][tx + 32 * y];
 #pragma unroll
-                for (int x = 0; x < 4; ++x)
+                for (int x = 0; x < 8; ++x)
 #pragma unroll
-                    for (int y = 0; y < 4; ++y) {
+                    for (int y = 0; y < 8; ++y) {
                         if (SP) acc[x][y] += (u64)mv[x] * pv[y];
                         else acc[x][y] += mulmod(mv[x], pv[y], f);
                     }
             }
 #pragma unroll
-            for (int x = 0; x < 4; ++x) {
-                const int i = ty * 4 + x;
+            for (int x = 0; x < 8; ++x) {
+                const int i = ty * 8 + x;
                 if (i >= b) continue;
                 u32* out = a.A + (i64)(a.i0 + i) * a.lda + cb;
                 const bool isdead = (dead >> i) & 1;
 #pragma unroll
-                for (int y = 0; y < 4; ++y) {
-                    const int cc = tx * 4 + y;
+                for (int y = 0; y < 8; ++y) {
+                    const int cc = tx + 32 * y;
                     if (cb + cc < a.N) {
-                        const u32 val = red64(acc[x][y], f);
+                        const u32 val = SP ? red_sp(acc[x][y], f) : red64(acc[x][y], f);
                         if (isdead) bad |= val;
                         out[cc] = val;
                     }
@@ -251,7 +287,7 @@ __global__ void __launch_bounds__(256) panel_tail_kernel(PanelArgs a) {
     if (atomicAdd(&ps->flag, 0u) != 0) {
         panel_fallback(a, red_buf);
         const int r2 = ps->r;
-        if (r2 > 0) leaf_uinv(a, c0, r2, Mi, Ps);
+        if (r2 > 0) leaf_uinv<SP>(a, c0, r2, Mi, reinterpret_cast<u32 (*)[PB + 1]>(tsm + 2 * PB * (PB + 1)));
     }
     if (tid == 0) {
         ps->counter = 0;
@@ -319,9 +355,20 @@ __global__ void __launch_bounds__(256) trsm_leaf_kernel(TrsmLeafArgs a) {
 }  // namespace
 
 void panel_tail(const PanelArgs& a, cudaStream_t s) {
-    const int grid = std::max(1, std::min((a.N + 63) / 64, 2 * num_sms())) + 1;
-    if (a.f.p <= 65536u) panel_tail_kernel<true><<<grid, 256, 0, s>>>(a);
-    else panel_tail_kernel<false><<<grid, 256, 0, s>>>(a);
+    const size_t smem = sizeof(u32) * (PB * (PB + 1) + PB * (TT + 4));
+    static_assert(sizeof(u32) * PB * (TT + 4) >= sizeof(u32) * 2 * PB * (PB + 1),
+                  "uinv scratch must fit in the tile buffer");
+    static bool attr = false;
+    if (!attr) {
+        RL_CUDA_CHECK(cudaFuncSetAttribute(panel_tail_kernel<true>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        RL_CUDA_CHECK(cudaFuncSetAttribute(panel_tail_kernel<false>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    const int grid = std::max(1, std::min((a.N + TT - 1) / TT, 2 * num_sms())) + 1;
+    if (a.f.p <= 65536u) panel_tail_kernel<true><<<grid, 256, smem, s>>>(a);
+    else panel_tail_kernel<false><<<grid, 256, smem, s>>>(a);
     RL_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -191,7 +191,7 @@ __device__ bool spec_lu(u32* s_R, u32 (*s_C)[PB + 1], u32* s_pv, u32* s_pinvA,
                 const u32 c0v = __shfl_sync(FULL, v0, k0 * 8 + j);         // C(k0, j)
                 const u32 c1v = __shfl_sync(FULL, v1, (k1 - 4) * 8 + j);   // C(k1, j)
                 const u32 uj = __shfl_sync(FULL, j < 4 ? v0 : v1, (j & 3) * 8 + cc);
-                const u32 m0 = mulmod(c0v, pinv, f), m1 = mulmod(c1v, pinv, f);
+                const u32 m0 = mulmod_t<SP>(c0v, pinv, f), m1 = mulmod_t<SP>(c1v, pinv, f);
                 if (cc == j) {  // this lane holds C(k, j) for its rows
                     if (k0 > j && k0 < bt) s_M[r0 + k0][j] = m0 ? f.p - m0 : 0u;
                     if (k1 > j && k1 < bt) s_M[r0 + k1][j] = m1 ? f.p - m1 : 0u;
@@ -247,7 +247,7 @@ __device__ bool spec_lu(u32* s_R, u32 (*s_C)[PB + 1], u32* s_pv, u32* s_pinvA,
                 for (int j2 = 0; j2 < j; ++j2) acc = fmsn<SP>(acc, nm[j2], s_R[(r0 + j2) * WT + r0 + j], f);
                 const u32 cv = fred<SP>(acc, f);
                 s_C[k][r0 + j] = cv;
-                const u32 m = mulmod(cv, s_pinvA[r0 + j], f);
+                const u32 m = mulmod_t<SP>(cv, s_pinvA[r0 + j], f);
                 nm[j] = m ? f.p - m : 0u;
             }
             uint4* dst = reinterpret_cast<uint4*>(&s_M[k][0]);
@@ -344,7 +344,6 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
             u32 val = 0;
             if (k < b && x < w) val = __ldcg(a.A + (i64)(a.i0 + k) * a.lda + c0 + x);
             acc[s][q] = val;
-            if (k < b) ps->win_orig[k][x] = val;
         }
         acc[s][4] = (lane == k) ? 1u : 0u;
         acc[s][5] = (lane + 32 == k) ? 1u : 0u;
@@ -372,7 +371,17 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
         }
         __syncthreads();
     } else {
-    // exact lockstep path (any pivot structure): registers still hold the window
+    // exact lockstep path (any pivot structure): registers still hold the window.
+    // Only here can a window-dead row appear, so only here is the original window
+    // saved for the tail kernel's fallback restore.
+#pragma unroll
+    for (int s = 0; s < RW; ++s) {
+        const int k = warp + NW * s;
+        if (k < b) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) ps->win_orig[k][lane + 32 * q] = (u32)acc[s][q];
+        }
+    }
     if (warp == 0) search_publish<SP>(acc[0], 0, 0, w, S, lane, f);
     __syncthreads();
     for (int i = 0; i < b; ++i) {
@@ -464,17 +473,19 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
     __syncthreads();
     // (a) pivot-column region [c0, c0 + rt): C entries, raw pivots, normalised U
     // (b) [c0 + rt, c0 + w): original values in the final column order (the tail
-    //     kernel replaces them with V = Minv * P)
+    //     kernel replaces them with V = Minv * P).  The speculative path made no
+    //     transposition, so those columns still hold exactly that.
+    const int xend = spec ? min(w, rt) : w;
     for (int e = tid; e < b * PW; e += blockDim.x) {
         const int k = e / PW, x = e % PW;
-        if (x >= w) continue;
+        if (x >= xend) continue;
         u32 val;
         if (x < rt) {
             const int rb = s_rb[k], j = s_por[k];
             if (x < rb) val = s_C[k][x];
             else if (j < 0) val = 0;
             else if (x == j) val = s_R[k * WT + x];
-            else val = mulmod(s_R[k * WT + x], s_pinvA[j], f);
+            else val = mulmod_t<SP>(s_R[k * WT + x], s_pinvA[j], f);
         } else {
             val = ps->win_orig[k][s_sig[x]];
         }
@@ -486,7 +497,7 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
         if (k < b && i < b) {
             const int j = s_por[k];
             mi = s_R[k * WT + PW + i];
-            if (j >= 0) mi = mulmod(mi, s_pinvA[j], f);
+            if (j >= 0) mi = mulmod_t<SP>(mi, s_pinvA[j], f);
             if (i == k) {
                 mr = j >= 0 ? s_pv[j] : 1u % f.p;
             } else if (i < k) {
@@ -495,7 +506,7 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
             }
         }
         ps->Minv[k][i] = mi;
-        ps->Mr[k][i] = mr;
+        if (!spec) ps->Mr[k][i] = mr;  // fallback restore only (exact path)
     }
     for (int e = tid; e < PB; e += blockDim.x) {
         const bool real = e < b;

@@ -4,11 +4,14 @@
 // recurses along the top node's skeleton.  For a node X of at most 4 leaves the
 // whole recursion -- leaf solves G_l <- B_l U_l^{-1} and the updates
 // B_l -= G_l' U_{l'l} between them (kernels.cpp:149-154) -- runs in ONE kernel:
-// each CTA owns a 64-row tile of G held in shared memory and sweeps the leaves
+// each CTA owns a 16-row tile of G held in shared memory and sweeps the leaves
 // left to right (block forward substitution), with the leaf inverses U_l^{-1}
 // precomputed by the leaves' panels and the off-diagonal blocks U_{l'l} gathered
-// through the row profile.  Products are summed lazily in 64 bits (p < 2^16) and
-// reduced once per output.  The diagonal (C's pivots) is never read: Unit.
+// through the row profile.  Thread = (row, 4 consecutive columns): one broadcast
+// load of G and one 16-byte load of U per 4 multiply-adds; products are summed
+// lazily in 64 bits (p < 2^16) and reduced once per output.  Short tiles give
+// many CTAs (4 per SM) so the sweep's latency hides behind parallelism.  The
+// diagonal (C's pivots) is never read: Unit.
 #include <algorithm>
 
 #include "kernels.cuh"
@@ -18,18 +21,35 @@ namespace rl {
 
 namespace {
 
-constexpr int TM = 64;                   // rows of G per CTA tile
-constexpr int GW = TN_MAXLEAF * PB + 4;  // smem row pitch of the G tile
+constexpr int TM = 16;                    // rows of G per CTA tile
+constexpr int GW = TN_MAXLEAF * PB + 4;   // smem row pitch of the G tile (words)
+constexpr int BW = PB + 4;                // pitch of a 64 x 64 block (16-byte aligned rows)
+
+template <bool SP>
+__device__ __forceinline__ void mac4(u64 (&acc)[4], u32 g, uint4 u, const Fp& f) {
+    if (SP) {
+        acc[0] += (u64)g * u.x;
+        acc[1] += (u64)g * u.y;
+        acc[2] += (u64)g * u.z;
+        acc[3] += (u64)g * u.w;
+    } else {
+        acc[0] += mulmod(g, u.x, f);
+        acc[1] += mulmod(g, u.y, f);
+        acc[2] += mulmod(g, u.z, f);
+        acc[3] += mulmod(g, u.w, f);
+    }
+}
 
 template <bool SP>
 __global__ void __launch_bounds__(256) trsm_node_kernel(TrsmNodeArgs a) {
     extern __shared__ __align__(16) u32 sm[];
-    u32* Gs = sm;                       // [TM][GW]
-    u32 (*Bk)[PB + 1] = reinterpret_cast<u32 (*)[PB + 1]>(sm + TM * GW);           // block U_{l'l}
-    u32 (*Ui)[PB + 1] = reinterpret_cast<u32 (*)[PB + 1]>(sm + TM * GW + PB * (PB + 1));
+    u32* Gs = sm;                 // [TM][GW]
+    u32* Bk = sm + TM * GW;       // [PB][BW] block U_{l'l}
+    u32* Ui = Bk + PB * BW;       // [PB][BW] leaf inverse
     __shared__ i32 s_row[PB];
     const Fp f = a.f;
-    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int tid = threadIdx.x;
+    const int row = tid >> 4, cg = tid & 15;  // thread -> (row, columns 4cg..4cg+3)
     i32 lo[TN_MAXLEAF], hi[TN_MAXLEAF];
 #pragma unroll
     for (int l = 0; l < TN_MAXLEAF; ++l) {
@@ -52,11 +72,7 @@ __global__ void __launch_bounds__(256) trsm_node_kernel(TrsmNodeArgs a) {
             const int nl = hi[l] - lo[l];
             if (nl <= 0) continue;
             const int ol = lo[l] - J0;
-            u64 S[4][4];
-#pragma unroll
-            for (int x = 0; x < 4; ++x)
-#pragma unroll
-                for (int y = 0; y < 4; ++y) S[x][y] = 0;
+            u64 S[4] = {0, 0, 0, 0};
             // S = sum_{l' < l} G_l' * U[J_l', J_l]
             for (int l2 = 0; l2 < l; ++l2) {
                 const int n2 = hi[l2] - lo[l2];
@@ -65,71 +81,46 @@ __global__ void __launch_bounds__(256) trsm_node_kernel(TrsmNodeArgs a) {
                 __syncthreads();
                 if (tid < n2) s_row[tid] = __ldcg(a.rrp + lo[l2] + tid);
                 __syncthreads();
+#pragma unroll 4
                 for (int e = tid; e < PB * PB; e += blockDim.x) {
                     const int k = e / PB, c = e % PB;
                     const bool ok = k < n2 && c < nl;
-                    cp_async4(&Bk[k][c], ok ? a.A + (i64)s_row[k] * a.lda + lo[l] + c : a.A, ok);
+                    cp_async4(&Bk[k * BW + c], ok ? a.A + (i64)s_row[k] * a.lda + lo[l] + c : a.A, ok);
                 }
                 cp_async_wait_all();
                 __syncthreads();
-                for (int k = 0; k < n2; ++k) {
-                    u32 gv[4], uv[4];
-#pragma unroll
-                    for (int x = 0; x < 4; ++x) gv[x] = Gs[(ty * 4 + x) * GW + o2 + k];
-#pragma unroll
-                    for (int y = 0; y < 4; ++y) uv[y] = Bk[k][tx * 4 + y];
-#pragma unroll
-                    for (int x = 0; x < 4; ++x)
-#pragma unroll
-                        for (int y = 0; y < 4; ++y) {
-                            if (SP) S[x][y] += (u64)gv[x] * uv[y];
-                            else S[x][y] += mulmod(gv[x], uv[y], f);
-                        }
-                }
+                const u32* grow = &Gs[row * GW + o2];
+#pragma unroll 4
+                for (int k = 0; k < n2; ++k)
+                    mac4<SP>(S, grow[k], *reinterpret_cast<const uint4*>(&Bk[k * BW + 4 * cg]), f);
             }
             // B_l <- B_l - S (in the tile), then G_l = B_l * Uinv_l
             __syncthreads();
-            for (int e = tid; e < PB * PB; e += blockDim.x) cp_async4(&Ui[e / PB][e % PB], a.uinv[l] + e, true);
+#pragma unroll 4
+            for (int e = tid; e < PB * PB; e += blockDim.x)
+                cp_async4(&Ui[(e / PB) * BW + e % PB], a.uinv[l] + e, true);
 #pragma unroll
-            for (int x = 0; x < 4; ++x)
-#pragma unroll
-                for (int y = 0; y < 4; ++y) {
-                    const int c = tx * 4 + y;
-                    if (c < nl) {
-                        u32* g = &Gs[(ty * 4 + x) * GW + ol + c];
-                        *g = submod(*g, red64(S[x][y], f), f);
-                    }
+            for (int y = 0; y < 4; ++y) {
+                const int c = 4 * cg + y;
+                if (c < nl) {
+                    u32* g = &Gs[row * GW + ol + c];
+                    *g = submod(*g, red64(S[y], f), f);
                 }
+            }
             cp_async_wait_all();
             __syncthreads();
-            u64 O[4][4];
-#pragma unroll
-            for (int x = 0; x < 4; ++x)
-#pragma unroll
-                for (int y = 0; y < 4; ++y) O[x][y] = 0;
-            const int kmax = min(nl, tx * 4 + 4);
-            for (int k = 0; k < kmax; ++k) {
-                u32 gv[4], uv[4];
-#pragma unroll
-                for (int x = 0; x < 4; ++x) gv[x] = Gs[(ty * 4 + x) * GW + ol + k];
-#pragma unroll
-                for (int y = 0; y < 4; ++y) uv[y] = Ui[k][tx * 4 + y];
-#pragma unroll
-                for (int x = 0; x < 4; ++x)
-#pragma unroll
-                    for (int y = 0; y < 4; ++y) {
-                        if (SP) O[x][y] += (u64)gv[x] * uv[y];
-                        else O[x][y] += mulmod(gv[x], uv[y], f);
-                    }
-            }
+            u64 O[4] = {0, 0, 0, 0};
+            const int kmax = min(nl, 4 * cg + 4);  // Uinv is upper triangular
+            const u32* grow = &Gs[row * GW + ol];
+#pragma unroll 4
+            for (int k = 0; k < kmax; ++k)
+                mac4<SP>(O, grow[k], *reinterpret_cast<const uint4*>(&Ui[k * BW + 4 * cg]), f);
             __syncthreads();
 #pragma unroll
-            for (int x = 0; x < 4; ++x)
-#pragma unroll
-                for (int y = 0; y < 4; ++y) {
-                    const int c = tx * 4 + y;
-                    if (c < nl) Gs[(ty * 4 + x) * GW + ol + c] = red64(O[x][y], f);
-                }
+            for (int y = 0; y < 4; ++y) {
+                const int c = 4 * cg + y;
+                if (c < nl) Gs[row * GW + ol + c] = SP ? red_sp(O[y], f) : red64(O[y], f);
+            }
         }
         __syncthreads();
         for (int e = tid; e < TM * nJ; e += blockDim.x) {
@@ -143,7 +134,7 @@ __global__ void __launch_bounds__(256) trsm_node_kernel(TrsmNodeArgs a) {
 
 void trsm_node(const TrsmNodeArgs& a, cudaStream_t s) {
     if (a.M <= 0 || a.nleaf <= 0) return;
-    const size_t smem = sizeof(u32) * (TM * GW + 2 * PB * (PB + 1));
+    const size_t smem = sizeof(u32) * (TM * GW + 2 * PB * BW);
     static bool attr = false;
     if (!attr) {
         RL_CUDA_CHECK(cudaFuncSetAttribute(trsm_node_kernel<true>,
@@ -152,7 +143,7 @@ void trsm_node(const TrsmNodeArgs& a, cudaStream_t s) {
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    const int grid = std::max(1, std::min((a.M + TM - 1) / TM, 8 * num_sms()));
+    const int grid = std::max(1, std::min((a.M + TM - 1) / TM, 16 * num_sms()));
     if (a.f.p <= 65536u) trsm_node_kernel<true><<<grid, 256, smem, s>>>(a);
     else trsm_node_kernel<false><<<grid, 256, smem, s>>>(a);
     RL_CUDA_CHECK(cudaGetLastError());
