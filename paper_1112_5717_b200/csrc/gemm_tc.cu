@@ -20,7 +20,7 @@
 // with row%8), so the GEMM moves each stage with two 1-D bulk async copies
 // (TMA engine, UBLKCP) into 1024-aligned smem and feeds tcgen05.mma.kind::i8
 // (M=128, N=L*NT, K=32) from an elected thread; accumulators live in TMEM
-// (2 x 256 columns, double buffered) and 4 epilogue warps drain them with
+// (2 x 256 columns, double buffered) and 16 epilogue warps drain them with
 // tcgen05.ld while the next tile's MMAs run.  Persistent grid (<= #SMs).
 #include <algorithm>
 #include <cstdio>
@@ -32,6 +32,23 @@
 namespace rl {
 
 namespace {
+
+#ifdef RL_GEMM_TRACE  // tools/gemm_trace.cu: per-CTA phase timestamps
+__device__ unsigned long long g_gemm_trace[1024][8];
+__device__ __forceinline__ void gemm_trace(int i) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (blockIdx.x < 1024) g_gemm_trace[blockIdx.x][i] = t;
+}
+#define GEMM_TRACE(i, cond) \
+    do {                    \
+        if (cond) gemm_trace(i); \
+    } while (0)
+#else
+#define GEMM_TRACE(i, cond) \
+    do {                    \
+    } while (0)
+#endif
 
 constexpr int BM = 128;    // tile rows = UMMA M
 constexpr int BK = 128;    // K bytes per stage (one SW128 atom row)
@@ -171,10 +188,14 @@ __global__ void __launch_bounds__(256) pack_b_kernel(GemmArgs g, uint8_t* __rest
     }
 }
 
+constexpr int EPW = 16;                    // epilogue warps (4 per TMEM lane quadrant)
+constexpr int NTHR = 64 + 32 * EPW;        // producer warp + MMA warp + epilogue
+
 // -------------------------------------------------------------- the GEMM
 template <int L>
-__global__ void __launch_bounds__(320, 1) gemm_tc_kernel(GemmArgs g, const uint8_t* __restrict__ a2,
-                                                         const uint8_t* __restrict__ b2) {
+__global__ void __launch_bounds__(NTHR, 1)
+    gemm_tc_kernel(GemmArgs g, const uint8_t* __restrict__ a2, const uint8_t* __restrict__ b2, u32 s1,
+                   u32 s2, u32 s3) {
     using C_ = Cfg<L>;
     constexpr int NT = C_::NT, UN = C_::UN, STAGES = C_::STAGES, STAGE = C_::STAGE;
     extern __shared__ uint8_t smem_raw[];
@@ -203,15 +224,17 @@ __global__ void __launch_bounds__(320, 1) gemm_tc_kernel(GemmArgs g, const uint8
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull[a], 1);
-            ptx::mbar_init(&tempty[a], 256);
+            ptx::mbar_init(&tempty[a], 32 * EPW);
         }
         ptx::fence_mbar_init();
     }
+    GEMM_TRACE(0, threadIdx.x == 0);
     if (warp == 1) ptx::tmem_alloc(tmem_slot, 512);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    GEMM_TRACE(1, threadIdx.x == 0);
 
     if (warp == 0) {
         if (lane == 0) {  // ---- producer: bulk async copies of pre-swizzled tiles
@@ -247,6 +270,7 @@ __global__ void __launch_bounds__(320, 1) gemm_tc_kernel(GemmArgs g, const uint8
                 const uint32_t d = tmem + acc * 256;
                 for (i32 kt = 0; kt < KT; ++kt) {
                     ptx::mbar_wait(&full[s], ph);
+                    GEMM_TRACE(2, tile == blockIdx.x && kt == 0);
                     ptx::tc_fence_after();
                     const uint32_t sa = ptx::smem_u32(smem + s * STAGE);
                     const uint32_t sb = sa + A_TILE;
@@ -262,24 +286,25 @@ __global__ void __launch_bounds__(320, 1) gemm_tc_kernel(GemmArgs g, const uint8
                     }
                 }
                 ptx::tc_commit(&tfull[acc]);
+                GEMM_TRACE(3, tile == blockIdx.x);
                 acc ^= 1;
                 if (acc == 0) aph ^= 1;
             }
         }
-    } else {  // ---- epilogue warps 2..9: TMEM -> registers -> exact mod-p -> C
-        // Two warps per TMEM lane quadrant (warp & 3), each owning half of the
-        // tile's columns.  All of a warp's C chunks are requested before it waits
-        // on the accumulator, so the C read latency overlaps the MMAs.
+    } else {  // ---- epilogue warps 2..2+EPW: TMEM -> registers -> exact mod-p -> C
+        // EPW/4 warps per TMEM lane quadrant (warp & 3), each owning a slice of
+        // the tile's columns.  A warp's first C chunks are requested before it
+        // waits on the accumulator, so the C read latency overlaps the MMAs.
         const int q = warp & 3;  // TMEM lane quadrant this warp may access
-        const int half = (warp - 2) >> 2;
+        const int part = (warp - 2) >> 2;
         const int rloc = q * 32 + lane;
         const uint32_t lane_base = (uint32_t)(q * 32) << 16;
         const Fp f = g.f;
         const u32 alpha = g.alpha, beta = g.beta;
         int acc = 0;
         uint32_t aph = 0;
-        constexpr int NCHH = NT / C_::CH / 2;        // chunks per half tile
-        constexpr int PF = NCHH < 4 ? NCHH : 4;      // chunks prefetched ahead
+        constexpr int NCHP = NT / C_::CH / (EPW / 4);  // chunks per warp slice
+        constexpr int PF = NCHP < 2 ? NCHP : 2;       // chunks prefetched ahead
         for (i32 tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
             const i32 mb = tile % MB, nb = tile / MB;
             const i32 row = mb * BM + rloc;
@@ -310,12 +335,13 @@ __global__ void __launch_bounds__(320, 1) gemm_tc_kernel(GemmArgs g, const uint8
             };
             u32 cbuf[PF][16];
 #pragma unroll
-            for (int c = 0; c < PF; ++c) load_chunk(half * NCHH + c, cbuf[c]);
+            for (int c = 0; c < PF; ++c) load_chunk(part * NCHP + c, cbuf[c]);
             ptx::mbar_wait(&tfull[acc], aph);
+            GEMM_TRACE(4, warp == 2 && lane == 0 && tile == blockIdx.x);
             ptx::tc_fence_after();
 #pragma unroll
-            for (int cc = 0; cc < NCHH; ++cc) {
-                const int ch = half * NCHH + cc;
+            for (int cc = 0; cc < NCHP; ++cc) {
+                const int ch = part * NCHP + cc;
                 uint32_t sv[L][16];
 #pragma unroll
                 for (int j = 0; j < L; ++j)
@@ -323,18 +349,26 @@ __global__ void __launch_bounds__(320, 1) gemm_tc_kernel(GemmArgs g, const uint8
                 u32 cur[16];
 #pragma unroll
                 for (int t = 0; t < 16; ++t) cur[t] = cbuf[cc % PF][t];
-                if (cc + PF < NCHH) load_chunk(ch + PF, cbuf[cc % PF]);
+                if (cc + PF < NCHP) load_chunk(ch + PF, cbuf[cc % PF]);
                 ptx::tc_wait_ld();
                 const i32 c0 = nb * NT + ch * 16;
                 if (vrow) {
                     u32 outv[16];
 #pragma unroll
                     for (int t = 0; t < 16; ++t) {
-                        u64 x = sv[0][t];
-                        if (L > 1) x += (u64)sv[L > 1 ? 1 : 0][t] << 8;
-                        if (L > 2) x += (u64)sv[L > 2 ? 2 : 0][t] << 16;
-                        if (L > 3) x += (u64)sv[L > 3 ? 3 : 0][t] << 24;
-                        const u32 r = red64(x, f);
+                        // x = sum_j S_j 2^(8j); L <= 2 means p <= 2^16 and x < 2^40
+                        u32 r;
+                        if (L == 1) {
+                            r = red32(sv[0][t], f);
+                        } else if (L == 2) {
+                            r = red_sp((u64)sv[0][t] + ((u64)sv[L > 1 ? 1 : 0][t] << 8), f);
+                        } else {
+                            u64 x = sv[0][t];
+                            x += (u64)sv[L > 1 ? 1 : 0][t] << 8;
+                            x += (u64)sv[L > 2 ? 2 : 0][t] << 16;
+                            if (L > 3) x += (u64)sv[L > 3 ? 3 : 0][t] << 24;
+                            r = red64(x, f);
+                        }
                         const u32 cv = (beta == 0 || beta == 1) ? cur[t] : mulmod(cur[t], beta, f);
                         u32 out;
                         if (alpha == f.p - 1) out = submod(cv, r, f);
@@ -357,6 +391,7 @@ __global__ void __launch_bounds__(320, 1) gemm_tc_kernel(GemmArgs g, const uint8
             }
             ptx::tc_fence_before();
             ptx::mbar_arrive(&tempty[acc]);
+            GEMM_TRACE(5, warp == 2 && lane == 0 && tile == blockIdx.x);
             acc ^= 1;
             if (acc == 0) aph ^= 1;
         }
@@ -365,6 +400,7 @@ __global__ void __launch_bounds__(320, 1) gemm_tc_kernel(GemmArgs g, const uint8
     __syncthreads();
     ptx::tc_fence_after();
     if (warp == 1) ptx::tmem_dealloc(tmem, 512);
+    GEMM_TRACE(6, threadIdx.x == 0);
 }
 
 template <int L>
@@ -377,15 +413,18 @@ void launch_tc(const GemmArgs& g, i64 Kmax, i64 Nmax, uint8_t* a2, uint8_t* b2, 
     const i64 NB = (Nmax + C_::NT - 1) / C_::NT;
     u32 sc[4] = {1, 0, 0, 0};
     for (int i = 1; i < 4; ++i) sc[i] = (u32)(((u64)sc[i - 1] << 8) % g.f.p);
+    const int grid = (int)std::max<i64>(1, std::min<i64>(MB * NB, nsm));
     if (phase != 1) {
-        i64 work = MB * KB * BM * 8;
-        int grid = (int)std::min<i64>((work + 255) / 256, (i64)nsm * 16);
-        pack_a_kernel<L><<<std::max(grid, 1), 256, 0, s>>>(g, a2);
-    }
-    {
-        i64 work = KB * 4 * NB;
-        int grid = (int)std::min<i64>(work, (i64)nsm * 8);
-        pack_b_kernel<L><<<std::max(grid, 1), 256, 0, s>>>(g, b2, sc[1], sc[2], sc[3]);
+        {
+            i64 work = MB * KB * BM * 8;
+            int pg = (int)std::min<i64>((work + 255) / 256, (i64)nsm * 16);
+            pack_a_kernel<L><<<std::max(pg, 1), 256, 0, s>>>(g, a2);
+        }
+        {
+            i64 work = KB * 4 * NB;
+            int pg = (int)std::min<i64>(work, (i64)nsm * 8);
+            pack_b_kernel<L><<<std::max(pg, 1), 256, 0, s>>>(g, b2, sc[1], sc[2], sc[3]);
+        }
     }
     if (phase == 0) return;
     static bool attr_set = false;
@@ -395,8 +434,7 @@ void launch_tc(const GemmArgs& g, i64 Kmax, i64 Nmax, uint8_t* a2, uint8_t* b2, 
                                            (int)C_::SMEM));
         attr_set = true;
     }
-    int grid = (int)std::min<i64>(MB * NB, nsm);
-    gemm_tc_kernel<L><<<std::max(grid, 1), 320, C_::SMEM, s>>>(g, a2, b2);
+    gemm_tc_kernel<L><<<grid, NTHR, C_::SMEM, s>>>(g, a2, b2, sc[1], sc[2], sc[3]);
     RL_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -428,6 +466,7 @@ void gemm_tc(const GemmArgs& g, int L, i64 Kmax, i64 Nmax, uint8_t* a2, uint8_t*
              cudaStream_t s) {
     gemm_tc_split(g, L, Kmax, Nmax, a2, b2, s, 2);
 }
+
 
 // ------------------------------------------------------------ SIMT fallback
 namespace {

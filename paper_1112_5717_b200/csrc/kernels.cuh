@@ -56,7 +56,8 @@ size_t tc_b2_bytes(int L, i64 Nmax, i64 Kmax);
 // workspaces of tc_a2_bytes/tc_b2_bytes for the static bounds (Kmax, Nmax).
 void gemm_tc(const GemmArgs& g, int L, i64 Kmax, i64 Nmax, uint8_t* a2, uint8_t* b2,
              cudaStream_t s);
-// phase 0: only the two pack kernels; phase 1: only the tcgen05 kernel (profiling).
+// phase 0: only the two pack kernels; phase 1: only the tcgen05 kernel (profiling);
+// 2: both.
 void gemm_tc_split(const GemmArgs& g, int L, i64 Kmax, i64 Nmax, uint8_t* a2, uint8_t* b2,
                    cudaStream_t s, int phase);
 // CUDA-core fallback for skinny shapes (K or N tiny).

@@ -17,6 +17,7 @@ c = torch.empty((m, n), dtype=torch.int32, device="cuda")
 G.random_matrix_dev(a, m, l, 11, p)
 G.random_matrix_dev(b, l, n, 12, p)
 G.random_matrix_dev(c, m, n, 13, p)
-mp, mg = G.profile_gemm_dev(a, b, c, m, l, n, p, iters=3)
+iters = int(sys.argv[5]) if len(sys.argv) > 5 else 3
+mp, mg = G.profile_gemm_dev(a, b, c, m, l, n, p, iters=iters)
 L = max(1, ((p - 1).bit_length() + 7) // 8)
-print(f"pack {mp:.3f} ms  gemm {mg:.3f} ms  {2*m*n*l*L*L/mg/1e9:.1f} int8 TOPS")
+print(f"{m}x{l}x{n} p={p}: pack {mp*1e3:.1f} us  gemm {mg*1e3:.1f} us  ({2*m*n*l*L*L/mg/1e9:.1f} int8 TOPS)")
