@@ -82,6 +82,51 @@ int rl_rank_and_profile_u32(uint32_t* A, int64_t m, int64_t n, int64_t lda, uint
  * (sign(P) * product of pivots; input consumed). */
 int rl_determinant_u32(uint32_t* A, int64_t n, int64_t lda, uint32_t p, uint32_t* det);
 
+/* Column echelon transforms: cup, then (echelon.cpp:5-21) the body becomes
+ * [C\X] with X the strict upper part of U^{-1}; with reduced != 0
+ * (echelon.cpp:23-47) it becomes [[X1, X2], [R2, 0]] after the pivot-row
+ * compression.  rank/rrp/sigma as rl_cup_u32; ops (NULL ok) = the exact
+ * charges of cup plus the reduction.
+ * Replaces: EchelonTransform ranklab::col_ech_trans(MatView, OpCounter&) and
+ *           ReducedEchelonTransform ranklab::red_col_ech_trans(MatView, OpCounter&)
+ *           proj/include/ranklab/echelon.hpp:28-29. */
+int rl_col_ech_trans_u32(uint32_t* A, int64_t m, int64_t n, int64_t lda, uint32_t p,
+                         int reduced, int64_t* rank, uint32_t* rrp, uint32_t* sigma,
+                         uint64_t* ops);
+int rl_col_ech_trans_u32_dev(uint32_t* dA, int64_t m, int64_t n, int64_t lda, uint32_t p,
+                             int reduced, int64_t* rank, uint32_t* rrp, uint32_t* sigma,
+                             uint64_t* ops, void* stream);
+
+/* A <- A^{-1} in place (n x n).  RL_ESINGULAR when rank < n; the body then
+ * holds red_col_ech_trans's output, as in the reference.
+ * Replaces: void ranklab::invert_in_place(MatView, OpCounter&)
+ *           proj/include/ranklab/solvers.hpp:19-22, proj/src/solvers.cpp:24-31. */
+int rl_invert_u32(uint32_t* A, int64_t n, int64_t lda, uint32_t p, uint64_t* ops);
+int rl_invert_u32_dev(uint32_t* dA, int64_t n, int64_t lda, uint32_t p, uint64_t* ops,
+                      void* stream);
+
+/* Triangular solve B <- T^{-1} B (side 0 = Left, T m x m) or B T^{-1}
+ * (side 1 = Right, T n x n); uplo 0 = Upper, 1 = Lower; diag 1 = Unit (the
+ * stored diagonal is never read), 0 = NonUnit.  B is m x n.  RL_EOVERLAP when
+ * T overlaps B; RL_ESINGULAR for a zero NonUnit diagonal (B untouched; the
+ * message names the index the reference would report).  ops (NULL ok) are
+ * the reference's charges at `threshold`.
+ * Replaces: void ranklab::trsm(Side, UpLo, Diag, ConstMatView t, MatView b,
+ *           OpCounter&, size_t threshold)  proj/include/ranklab/kernels.hpp:37-38. */
+int rl_trsm_u32(int side, int uplo, int diag, const uint32_t* T, int64_t ldt, uint32_t* B,
+                int64_t ldb, int64_t m, int64_t n, uint32_t p, int64_t threshold,
+                uint64_t* ops);
+int rl_trsm_u32_dev(int side, int uplo, int diag, const uint32_t* dT, int64_t ldt,
+                    uint32_t* dB, int64_t ldb, int64_t m, int64_t n, uint32_t p,
+                    int64_t threshold, uint64_t* ops, void* stream);
+
+/* Host-only op tallies (no device needed): the reference's trsm charges, and
+ * what col_ech_trans (reduced: red_col_ech_trans) charges after its cup for
+ * an m x n input of rank r. */
+int rl_trsm_opcount(int side, int uplo, int diag, int64_t m, int64_t n, int64_t threshold,
+                    uint64_t* ops);
+int rl_echelon_opcount(int64_t m, int64_t n, int64_t r, int reduced, uint64_t* ops);
+
 /* Seeded inputs generated on the device, bit-identical to
  * ranklab::random_matrix(m, n, seed, GF(p))  proj/src/reference.cpp:246-253. */
 int rl_random_matrix_u32_dev(uint32_t* dA, int64_t m, int64_t n, int64_t lda, uint64_t seed,

@@ -107,8 +107,8 @@ def ref_lib():
                                                  C.POINTER(_i64), _u32p]
         lib.ref_determinant_u32.argtypes = [_u32p, _i64, _i64, _u32, C.POINTER(_u32)]
         lib.ref_col_ech_trans_u32.argtypes = [_u32p, _i64, _i64, _i64, _u32, C.c_int,
-                                              C.POINTER(_i64), _u32p, _u32p]
-        lib.ref_invert_u32.argtypes = [_u32p, _i64, _i64, _u32]
+                                              C.POINTER(_i64), _u32p, _u32p, _u64p]
+        lib.ref_invert_u32.argtypes = [_u32p, _i64, _i64, _u32, _u64p]
         lib.ref_random_matrix_u32.argtypes = [_i64, _i64, _u64, _u32, _u32p]
         lib.ref_random_rank_matrix_u32.argtypes = [_i64, _i64, _i64, _u64, _u32, C.c_int,
                                                    _u32p]
@@ -191,14 +191,14 @@ def ref_mm(a, b, c, alpha, beta, p):
     return c
 
 
-def ref_trsm(side: str, uplo: str, diag: str, t, b, p, threshold=1):
+def ref_trsm(side: str, uplo: str, diag: str, t, b, p, threshold=1, return_ops=False):
     k = t.shape[0]
     m, n = b.shape
     ops = np.zeros(4, np.uint64)
     _check(ref_lib().ref_trsm_u32(int(side == "right"), int(uplo == "lower"),
                                   int(diag == "unit"), t, max(k, 1), k, b, max(n, 1), m, n,
                                   p, threshold, ops))
-    return b
+    return (b, ops) if return_ops else b
 
 
 def ref_rank_and_profile(a, p):
@@ -216,20 +216,28 @@ def ref_determinant(a, p):
     return d.value
 
 
-def ref_col_ech_trans(a, p, reduced=False):
+def ref_col_ech_trans(a, p, reduced=False, return_ops=False):
     m, n = a.shape
     rank = _i64(0)
     rrp = np.zeros(max(1, min(m, n)), np.uint32)
     sigma = np.zeros(max(n, 1), np.uint32)
+    ops = np.zeros(4, np.uint64)
     _check(ref_lib().ref_col_ech_trans_u32(a, m, n, max(n, 1), p, int(reduced),
-                                           C.byref(rank), rrp, sigma))
+                                           C.byref(rank), rrp, sigma, ops))
     r = rank.value
-    return CupResult(r, rrp[:r].copy(), sigma[:n].copy())
+    res = CupResult(r, rrp[:r].copy(), sigma[:n].copy())
+    return (res, ops) if return_ops else res
 
 
-def ref_invert(a, p):
+def ref_invert(a, p, return_ops=False):
+    """invert_in_place; returns the status (0 ok, 3 singular) with the ops
+    when return_ops, else raises on a nonzero status."""
     n = a.shape[0]
-    _check(ref_lib().ref_invert_u32(a, n, max(n, 1), p))
+    ops = np.zeros(4, np.uint64)
+    st = ref_lib().ref_invert_u32(a, n, max(n, 1), p, ops)
+    if return_ops:
+        return st, ops
+    _check(st)
     return a
 
 

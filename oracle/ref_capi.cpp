@@ -143,7 +143,8 @@ int ref_determinant_u32(std::uint32_t* a, std::int64_t n, std::int64_t lda,
 
 int ref_col_ech_trans_u32(std::uint32_t* a, std::int64_t m, std::int64_t n,
                           std::int64_t lda, std::uint32_t p, int reduced,
-                          std::int64_t* rank, std::uint32_t* rrp, std::uint32_t* sigma) {
+                          std::int64_t* rank, std::uint32_t* rrp, std::uint32_t* sigma,
+                          std::uint64_t* ops) {
     return guard([&] {
         PrimeField f(p);
         OpCounter c;
@@ -161,15 +162,19 @@ int ref_col_ech_trans_u32(std::uint32_t* a, std::int64_t m, std::int64_t n,
             for (std::size_t j = 0; j < t.col_perm.order(); ++j) sigma[j] = t.col_perm[j];
         }
         *rank = static_cast<std::int64_t>(r);
+        put_ops(c, ops);
     });
 }
 
-int ref_invert_u32(std::uint32_t* a, std::int64_t n, std::int64_t lda, std::uint32_t p) {
-    return guard([&] {
+int ref_invert_u32(std::uint32_t* a, std::int64_t n, std::int64_t lda, std::uint32_t p,
+                   std::uint64_t* ops) {
+    OpCounter c;
+    const int st = guard([&] {
         PrimeField f(p);
-        OpCounter c;
         invert_in_place(view_of(f, a, n, n, lda), c);
     });
+    put_ops(c, ops);
+    return st;
 }
 
 int ref_random_matrix_u32(std::int64_t m, std::int64_t n, std::uint64_t seed,

@@ -11,6 +11,10 @@ this module            reference
 ``mm``                 ``void mm(a, b, c, alpha, beta, OpCounter&)``  kernels.hpp:26
 ``rank_and_profile``   ``rank_and_profile(MatView, OpCounter&)``  solvers.hpp:13
 ``determinant``        ``Elem determinant(MatView, OpCounter&)``  solvers.hpp:16
+``col_ech_trans``      ``EchelonTransform col_ech_trans(MatView, OpCounter&)``  echelon.hpp:28
+``red_col_ech_trans``  ``ReducedEchelonTransform red_col_ech_trans(...)``  echelon.hpp:29
+``invert_in_place``    ``void invert_in_place(MatView, OpCounter&)``  solvers.hpp:22
+``trsm``               ``void trsm(Side, UpLo, Diag, t, b, OpCounter&, threshold)``  kernels.hpp:37
 ``PackedCup``          ``struct PackedCup``  factor.hpp:15-19
 ``OpCounter``          ``struct OpCounter``  field.hpp:16-34
 errors                 ``errors.hpp:9-66`` (``Error`` and subclasses)
@@ -34,6 +38,9 @@ __all__ = [
     "Error", "DimensionMismatch", "OverlapError", "SingularMatrix", "NotPrime", "CudaError",
     "OpCounter", "PackedCup", "cup", "cup_dev", "cup_batched_dev", "mm", "mm_dev",
     "rank_and_profile", "determinant", "random_matrix_dev", "LIB_PATH", "lib",
+    "EchelonTransform", "ReducedEchelonTransform", "col_ech_trans", "red_col_ech_trans",
+    "col_ech_trans_dev", "invert_in_place", "invert_dev", "trsm", "trsm_dev",
+    "Side", "UpLo", "Diag",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -116,7 +123,9 @@ _vp = C.c_void_p
 EXPORTS = ["rl_cup_u32", "rl_cup_u32_dev", "rl_cup_batched_u32_dev", "rl_mm_u32",
            "rl_mm_u32_dev", "rl_rank_and_profile_u32", "rl_determinant_u32",
            "rl_random_matrix_u32_dev", "rl_last_error", "rl_version", "rl_cup_plan_stats",
-           "rl_profile_gemm_dev", "rl_cup_opcount"]
+           "rl_profile_gemm_dev", "rl_cup_opcount", "rl_col_ech_trans_u32",
+           "rl_col_ech_trans_u32_dev", "rl_invert_u32", "rl_invert_u32_dev", "rl_trsm_u32",
+           "rl_trsm_u32_dev", "rl_trsm_opcount", "rl_echelon_opcount"]
 
 
 def lib():
@@ -141,6 +150,18 @@ def lib():
     L.rl_profile_gemm_dev.argtypes = [_vp, _vp, _vp, _i64, _i64, _i64, _u32, C.c_int,
                                       C.POINTER(C.c_float), C.POINTER(C.c_float), _vp]
     L.rl_cup_opcount.argtypes = [_i64, _i64, _i64, _vp, _vp, _vp]
+    L.rl_col_ech_trans_u32.argtypes = [_vp, _i64, _i64, _i64, _u32, C.c_int, C.POINTER(_i64), _vp,
+                                       _vp, _vp]
+    L.rl_col_ech_trans_u32_dev.argtypes = [_vp, _i64, _i64, _i64, _u32, C.c_int, C.POINTER(_i64),
+                                           _vp, _vp, _vp, _vp]
+    L.rl_invert_u32.argtypes = [_vp, _i64, _i64, _u32, _vp]
+    L.rl_invert_u32_dev.argtypes = [_vp, _i64, _i64, _u32, _vp, _vp]
+    L.rl_trsm_u32.argtypes = [C.c_int, C.c_int, C.c_int, _vp, _i64, _vp, _i64, _i64, _i64, _u32,
+                              _i64, _vp]
+    L.rl_trsm_u32_dev.argtypes = [C.c_int, C.c_int, C.c_int, _vp, _i64, _vp, _i64, _i64, _i64,
+                                  _u32, _i64, _vp, _vp]
+    L.rl_trsm_opcount.argtypes = [C.c_int, C.c_int, C.c_int, _i64, _i64, _i64, _vp]
+    L.rl_echelon_opcount.argtypes = [_i64, _i64, _i64, C.c_int, _vp]
     _lib = L
     return L
 
@@ -256,6 +277,148 @@ def mm_dev(d_a, d_b, d_c, m, l, n, alpha, beta, p, lda=None, ldb=None, ldc=None,
     _check(lib().rl_mm_u32_dev(C.c_void_p(pa), lda or l, C.c_void_p(pb), ldb or n, C.c_void_p(pc),
                                ldc or n, m, l, n, int(alpha), int(beta), int(p),
                                _stream_ptr(stream)))
+
+
+@dataclass
+class EchelonTransform:
+    """echelon.hpp:12-16: after col_ech_trans the body holds [C\\X], X the strict
+    upper part of U^{-1}; A*P^T*X = C with X unit upper triangular."""
+    rank: int = 0
+    row_profile: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint32))
+    col_perm: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint32))
+
+
+@dataclass
+class ReducedEchelonTransform(EchelonTransform):
+    """echelon.hpp:18-26: the body holds [[X1, X2], [R2, 0]]."""
+
+
+def _echelon(a: np.ndarray, p: int, reduced: bool, ctr: OpCounter | None):
+    a = _as_u32_matrix(a)
+    m, n = a.shape
+    rank = _i64(0)
+    rrp = np.zeros(max(1, min(m, n)), np.uint32)
+    sigma = np.zeros(max(1, n), np.uint32)
+    ops = np.zeros(4, np.uint64)
+    _check(lib().rl_col_ech_trans_u32(_ptr(a), m, n, _ld(a), int(p), int(reduced), C.byref(rank),
+                                      _ptr(rrp), _ptr(sigma), _ptr(ops)))
+    if ctr is not None:
+        ctr._add(ops)
+    r = rank.value
+    cls = ReducedEchelonTransform if reduced else EchelonTransform
+    return cls(r, rrp[:r].copy(), sigma[:n].copy())
+
+
+def col_ech_trans(a: np.ndarray, p: int, ctr: OpCounter | None = None) -> EchelonTransform:
+    """In place: ``a`` <- [C\\X] (echelon.cpp:5-21)."""
+    return _echelon(a, p, False, ctr)
+
+
+def red_col_ech_trans(a: np.ndarray, p: int,
+                      ctr: OpCounter | None = None) -> ReducedEchelonTransform:
+    """In place: ``a`` <- [[X1, X2], [R2, 0]] (echelon.cpp:23-47)."""
+    return _echelon(a, p, True, ctr)
+
+
+def col_ech_trans_dev(d_a, m: int, n: int, p: int, reduced: bool = False, lda: int | None = None,
+                      stream=None, ctr: OpCounter | None = None) -> EchelonTransform:
+    """col_ech_trans / red_col_ech_trans of a device-resident matrix."""
+    ptr = d_a.data_ptr() if hasattr(d_a, "data_ptr") else int(d_a)
+    rank = _i64(0)
+    rrp = np.zeros(max(1, min(m, n)), np.uint32)
+    sigma = np.zeros(max(1, n), np.uint32)
+    ops = np.zeros(4, np.uint64)
+    _check(lib().rl_col_ech_trans_u32_dev(C.c_void_p(ptr), m, n, lda or n, int(p), int(reduced),
+                                          C.byref(rank), _ptr(rrp), _ptr(sigma), _ptr(ops),
+                                          _stream_ptr(stream)))
+    if ctr is not None:
+        ctr._add(ops)
+    r = rank.value
+    cls = ReducedEchelonTransform if reduced else EchelonTransform
+    return cls(r, rrp[:r].copy(), sigma[:n].copy())
+
+
+def invert_in_place(a: np.ndarray, p: int, ctr: OpCounter | None = None) -> None:
+    """``a`` <- a^{-1} (solvers.cpp:24-31); raises :class:`SingularMatrix` when
+    rank < n, leaving red_col_ech_trans's body in ``a`` like the reference."""
+    a = _as_u32_matrix(a)
+    if a.shape[0] != a.shape[1]:
+        raise DimensionMismatch("inverse of non-square matrix")
+    ops = np.zeros(4, np.uint64)
+    try:
+        _check(lib().rl_invert_u32(_ptr(a), a.shape[0], _ld(a), int(p), _ptr(ops)))
+    finally:
+        if ctr is not None:
+            ctr._add(ops)
+
+
+def invert_dev(d_a, n: int, p: int, lda: int | None = None, stream=None,
+               ctr: OpCounter | None = None) -> None:
+    """invert_in_place of a device-resident n x n matrix."""
+    ptr = d_a.data_ptr() if hasattr(d_a, "data_ptr") else int(d_a)
+    ops = np.zeros(4, np.uint64)
+    _check(lib().rl_invert_u32_dev(C.c_void_p(ptr), n, lda or n, int(p), _ptr(ops),
+                                   _stream_ptr(stream)))
+    if ctr is not None:
+        ctr._add(ops)
+
+
+class Side:
+    Left, Right = 0, 1
+
+
+class UpLo:
+    Upper, Lower = 0, 1
+
+
+class Diag:
+    NonUnit, Unit = 0, 1
+
+
+def trsm(side: int, uplo: int, diag: int, t: np.ndarray, b: np.ndarray, p: int,
+         ctr: OpCounter | None = None, threshold: int = 1) -> None:
+    """B <- T^{-1} B (Side.Left) or B T^{-1} (Side.Right), kernels.hpp:37-38.
+
+    A NonUnit zero diagonal raises :class:`SingularMatrix` (the reference's
+    SingularDiagonal) with ``b`` untouched."""
+    t, b = _as_u32_matrix(t), _as_u32_matrix(b)
+    m, n = b.shape
+    k = m if side == Side.Left else n
+    if t.shape != (k, k):
+        raise DimensionMismatch(f"triangular operand {t.shape} vs {k}")
+    ops = np.zeros(4, np.uint64)
+    _check(lib().rl_trsm_u32(int(side), int(uplo), int(diag), _ptr(t), max(_ld(t), 1), _ptr(b),
+                             max(_ld(b), 1), m, n, int(p), int(threshold), _ptr(ops)))
+    if ctr is not None:
+        ctr._add(ops)
+
+
+def trsm_dev(side: int, uplo: int, diag: int, d_t, d_b, m: int, n: int, p: int,
+             ldt: int | None = None, ldb: int | None = None, stream=None,
+             ctr: OpCounter | None = None, threshold: int = 1) -> None:
+    pt = d_t.data_ptr() if hasattr(d_t, "data_ptr") else int(d_t)
+    pb = d_b.data_ptr() if hasattr(d_b, "data_ptr") else int(d_b)
+    k = m if side == Side.Left else n
+    ops = np.zeros(4, np.uint64)
+    _check(lib().rl_trsm_u32_dev(int(side), int(uplo), int(diag), C.c_void_p(pt), ldt or k,
+                                 C.c_void_p(pb), ldb or n, m, n, int(p), int(threshold), _ptr(ops),
+                                 _stream_ptr(stream)))
+    if ctr is not None:
+        ctr._add(ops)
+
+
+def trsm_opcount(side: int, uplo: int, diag: int, m: int, n: int, threshold: int = 1) -> np.ndarray:
+    """The reference's trsm charges (host-only, no device needed)."""
+    ops = np.zeros(4, np.uint64)
+    _check(lib().rl_trsm_opcount(int(side), int(uplo), int(diag), m, n, int(threshold), _ptr(ops)))
+    return ops
+
+
+def echelon_opcount(m: int, n: int, r: int, reduced: bool) -> np.ndarray:
+    """Charges of col_ech_trans / red_col_ech_trans after the cup (host-only)."""
+    ops = np.zeros(4, np.uint64)
+    _check(lib().rl_echelon_opcount(m, n, r, int(reduced), _ptr(ops)))
+    return ops
 
 
 def rank_and_profile(a: np.ndarray, p: int):

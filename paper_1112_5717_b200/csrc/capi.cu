@@ -18,6 +18,7 @@
 #include "cup.h"
 #include "kernels.cuh"
 #include "runtime.h"
+#include "tri.h"
 
 namespace rl {
 void cup_batched(u32* dA, i64 batch, i32 m, i32 n, i64 stride, u32 p, i32* d_ranks, i32* d_rrp,
@@ -114,20 +115,6 @@ CupEngine& engine_for(i64 m, i64 n, i64 lda, u32 p) {
 }
 
 // Device scratch buffers reused across host-pointer calls.
-struct DevBuf {
-    void* ptr = nullptr;
-    size_t cap = 0;
-    void* get(size_t bytes) {
-        if (bytes > cap) {
-            if (ptr) cudaFree(ptr);
-            ptr = nullptr;
-            cap = 0;
-            if (cudaMalloc(&ptr, bytes) != cudaSuccess) throw Error(RL_ENOMEM, "cudaMalloc failed");
-            cap = bytes;
-        }
-        return ptr;
-    }
-};
 DevBuf g_bufA, g_bufB, g_bufC, g_bufI;
 
 void require_device() {
@@ -198,62 +185,163 @@ void copy_d2h_2d(u32* h, i64 hld, const u32* d, i64 dld, i64 rows, i64 cols, cud
     RL_CUDA_CHECK(cudaMemcpy2DAsync(h, hld * 4, d, dld * 4, cols * 4, rows, cudaMemcpyDeviceToHost, s));
 }
 
-__global__ void scale_kernel(u32* C, i64 ldc, i64 m, i64 n, u32 beta, Fp f) {
-    const i64 total = m * n;
-    for (i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-         t += (i64)gridDim.x * blockDim.x) {
-        u32* c = C + (t / n) * ldc + (t % n);
-        *c = beta == 0 ? 0u : mulmod(*c, beta, f);
-    }
-}
-
 void mm_dev_impl(const u32* dA, i64 lda, const u32* dB, i64 ldb, u32* dC, i64 ldc, i64 m, i64 l,
                  i64 n, u32 alpha, u32 beta, u32 p, cudaStream_t s) {
-    if (m == 0 || n == 0) return;
-    const Fp f = make_fp(p);
-    if (alpha == 0 || l == 0) {  // kernels.cpp:43-52: product short-circuited
-        if (beta == 1 % p) return;
-        scale_kernel<<<(int)std::min<i64>((m * n + 255) / 256, 4096), 256, 0, s>>>(dC, ldc, m, n,
-                                                                                beta, f);
-        RL_CUDA_CHECK(cudaGetLastError());
+    mm_dense(dA, lda, dB, ldb, dC, ldc, m, l, n, alpha, beta, make_fp(p), s);
+}
+
+// cup of a device matrix, results on the host (synchronises s).  Small shapes
+// run as one CTA (one launch), larger ones through the cached engine.
+void factor_on_device(u32* dA, i64 m, i64 n, i64 lda, u32 p, cudaStream_t s, i64* r,
+                      std::vector<u32>& rrp_h, std::vector<u32>& ipiv_h) {
+    const i64 kcap = std::min(m, n);
+    rrp_h.assign((size_t)kcap, 0);
+    ipiv_h.assign((size_t)kcap, 0);
+    if (m <= 64 && n <= 256 && lda == n) {
+        i32* dmeta = (i32*)g_bufI.get((size_t)(1 + 2 * kcap) * 4);
+        cup_batched(dA, 1, (i32)m, (i32)n, m * n, p, dmeta, dmeta + 1, dmeta + 1 + kcap, (i32)kcap, s);
+        std::vector<i32> meta((size_t)(1 + 2 * kcap));
+        RL_CUDA_CHECK(cudaMemcpyAsync(meta.data(), dmeta, meta.size() * 4, cudaMemcpyDeviceToHost, s));
+        RL_CUDA_CHECK(cudaStreamSynchronize(s));
+        *r = meta[0];
+        std::copy((const u32*)&meta[1], (const u32*)&meta[1] + *r, rrp_h.begin());
+        std::copy((const u32*)&meta[1 + kcap], (const u32*)&meta[1 + kcap] + *r, ipiv_h.begin());
         return;
     }
-    const int L = limbs_for(p);
-    const i64 kmax = tc_kmax(L);
-    // Chunk K so every s32 accumulator stays exact; later chunks accumulate (beta = 1).
-    for (i64 k0 = 0; k0 < l; k0 += kmax) {
-        const i64 kc = std::min(kmax, l - k0);
-        GemmArgs g{};
-        g.A = dA + k0;
-        g.lda = lda;
-        g.a_row0 = 0;
-        g.B = dB + k0 * ldb;
-        g.ldb = ldb;
-        g.gather = nullptr;
-        g.C = dC;
-        g.ldc = ldc;
-        g.c_row0 = 0;
-        g.M = (i32)m;
-        g.k_lo = dyn_c(0);
-        g.k_hi = dyn_c((i32)kc);
-        g.n_lo = dyn_c(0);
-        g.n_hi = dyn_c((i32)n);
-        g.rp = nullptr;
-        g.alpha = alpha;
-        g.beta = k0 == 0 ? beta : 1 % p;
-        g.f = f;
-        const bool tc = kc >= 32 && n >= 32 && m >= 32;
-        if (tc) {
-            static DevBuf a2, b2;
-            uint8_t* pa = (uint8_t*)a2.get(tc_a2_bytes(L, m, kc));
-            uint8_t* pb = (uint8_t*)b2.get(tc_b2_bytes(L, n, kc));
-            gemm_tc(g, L, kc, n, pa, pb, s);
-        } else {
-            gemm_simt(g, kc, n, s);
+    CupEngine& e = engine_for(m, n, lda, p);
+    e.run(dA, s, m * n >= (1 << 18));
+    e.results(r, rrp_h.data(), ipiv_h.data(), s);  // synchronises s
+}
+
+// The reductions after cup on a device matrix (echelon.cpp:5-47): body
+// [C\U] -> [C\X] (col_ech_trans) or [[X1, X2], [R2, 0]] (reduced).
+void echelon_after_cup(u32* dA, i64 m, i64 n, i64 lda, u32 p, i64 r, const u32* rrp_h,
+                       bool reduced, cudaStream_t s) {
+    if (r == 0) return;
+    const Fp f = make_fp(p);
+    static DevBuf xbuf, ybuf, tbuf, ibuf;
+    // X <- U1^{-1} (unit upper); X2 <- -U1^{-1} U2; strict triangle of U1 <- X's
+    u32* X = (u32*)xbuf.get((size_t)r * r * 4);
+    tri_extract(X, r, dA, lda, (i32)r, /*upper=*/true, /*unit=*/true, p, s);
+    tri_inverse(X, r, (i32)r, /*upper=*/true, f, s);
+    if (n > r) {
+        u32* T = (u32*)tbuf.get((size_t)r * (n - r) * 4);
+        mm_dense(X, r, dA + r, lda, T, n - r, r, r, n - r, p - 1, 0, f, s);
+        RL_CUDA_CHECK(cudaMemcpy2DAsync(dA + r, lda * 4, T, (n - r) * 4, (n - r) * 4, r,
+                                        cudaMemcpyDeviceToDevice, s));
+    }
+    tri_store_strict(dA, lda, X, r, (i32)r, /*upper=*/true, s);
+    if (!reduced) return;
+    // pivot rows of C onto the diagonal, then R2 <- L2 L1^{-1}, X1 <- U1^{-1} L1^{-1}
+    i32* d_rrp = (i32*)ibuf.get((size_t)r * 4);
+    RL_CUDA_CHECK(cudaMemcpyAsync(d_rrp, rrp_h, (size_t)r * 4, cudaMemcpyHostToDevice, s));
+    compress_pivot_rows(dA, lda, (i32)r, d_rrp, s);
+    u32* Y = (u32*)ybuf.get((size_t)r * r * 4);
+    tri_extract(Y, r, dA, lda, (i32)r, /*upper=*/false, /*unit=*/false, p, s);
+    tri_inverse(Y, r, (i32)r, /*upper=*/false, f, s);
+    if (m > r) {
+        u32* T = (u32*)tbuf.get((size_t)(m - r) * r * 4);
+        mm_dense(dA + r * lda, lda, Y, r, T, r, m - r, r, r, 1 % p, 0, f, s);
+        RL_CUDA_CHECK(cudaMemcpy2DAsync(dA + r * lda, lda * 4, T, r * 4, r * 4, m - r,
+                                        cudaMemcpyDeviceToDevice, s));
+    }
+    mm_dense(X, r, Y, r, dA, lda, r, r, r, 1 % p, 0, f, s);
+}
+
+// new row i <- old row sigma^{-1}(i): A^{-1} = P^T X (solvers.cpp:29-30).
+void rows_by_inverse_perm(u32* dA, i64 n, i64 lda, const u32* sigma, cudaStream_t s) {
+    std::vector<i32> idx;
+    for (i64 j = 0; j < n; ++j)
+        if ((i64)sigma[j] != j) {  // new row sigma[j] <- old row j
+            idx.push_back((i32)sigma[j]);
+            idx.push_back((i32)j);
         }
+    if (idx.empty()) return;
+    static DevBuf ibuf;
+    i32* d = (i32*)ibuf.get(idx.size() * 4);
+    RL_CUDA_CHECK(cudaMemcpyAsync(d, idx.data(), idx.size() * 4, cudaMemcpyHostToDevice, s));
+    move_rows(dA, lda, n, d, (i32)(idx.size() / 2), s);
+    RL_CUDA_CHECK(cudaStreamSynchronize(s));  // idx must outlive the copy
+}
+
+void col_ech_dev_impl(u32* dA, i64 m, i64 n, i64 lda, u32 p, bool reduced, i64* rank, u32* rrp,
+                      u32* sigma, u64* ops, cudaStream_t s) {
+    i64 r = 0;
+    std::vector<u32> rrp_h, ipiv_h;
+    factor_on_device(dA, m, n, lda, p, s, &r, rrp_h, ipiv_h);
+    echelon_after_cup(dA, m, n, lda, p, r, rrp_h.data(), reduced, s);
+    if (rank) *rank = r;
+    if (rrp) std::copy(rrp_h.begin(), rrp_h.begin() + r, rrp);
+    if (sigma) sigma_from_ipiv(n, r, ipiv_h.data(), sigma);
+    if (ops) {
+        cup_opcount(m, n, r, rrp_h.data(), ipiv_h.data(), ops);
+        OpTally t;
+        tally_echelon(t, m, n, r, reduced);
+        ops[0] += t.mul;
+        ops[1] += t.addsub;
+        ops[2] += t.divinv;
+        ops[3] += t.ztest;
     }
 }
 
+// trsm seam (kernels.hpp:37-38): B <- T^{-1} B (left) or B T^{-1} (right), via
+// the dense inverse of the triangle and one GEMM.
+void trsm_dev_impl(int side, int uplo, int diag, const u32* dT, i64 ldt, u32* dB, i64 ldb, i64 m,
+                   i64 n, u32 p, cudaStream_t s) {
+    const i64 k = side == SIDE_LEFT ? m : n;
+    if (k == 0 || m == 0 || n == 0) return;
+    const Fp f = make_fp(p);
+    static DevBuf xbuf, tbuf;
+    u32* X = (u32*)xbuf.get((size_t)k * k * 4);
+    const bool upper = uplo == UPLO_UPPER;
+    tri_extract(X, k, dT, ldt, (i32)k, upper, diag != 0, p, s);
+    tri_inverse(X, k, (i32)k, upper, f, s);
+    u32* T = (u32*)tbuf.get((size_t)m * n * 4);
+    if (side == SIDE_LEFT) mm_dense(X, k, dB, ldb, T, n, m, k, n, 1 % p, 0, f, s);
+    else mm_dense(dB, ldb, X, k, T, n, m, k, n, 1 % p, 0, f, s);
+    RL_CUDA_CHECK(cudaMemcpy2DAsync(dB, ldb * 4, T, n * 4, n * 4, m, cudaMemcpyDeviceToDevice, s));
+}
+
+// The reference raises SingularDiagonal(d) at the first zero pivot its
+// traversal meets (kernels.cpp:87-90): ascending for Right/Upper and
+// Left/Lower, descending for the other two.
+i64 first_zero_diagonal(int side, int uplo, const std::vector<u32>& diag) {
+    const bool ascending = (side == SIDE_RIGHT) == (uplo == UPLO_UPPER);
+    const i64 k = (i64)diag.size();
+    for (i64 t = 0; t < k; ++t) {
+        const i64 d = ascending ? t : k - 1 - t;
+        if (diag[d] == 0) return d;
+    }
+    return -1;
+}
+
+void check_trsm_args(int side, int uplo, int diag, i64 m, i64 n, i64 ldt, i64 ldb) {
+    if (side < 0 || side > 1 || uplo < 0 || uplo > 1 || diag < 0 || diag > 1)
+        throw Error(RL_EINVAL, "trsm: side/uplo/diag out of range");
+    if (m < 0 || n < 0) throw Error(RL_EDIM, "negative dimension");
+    const i64 k = side == SIDE_LEFT ? m : n;
+    if (k > 0 && ldt < k) throw Error(RL_EINVAL, "trsm: ldt smaller than the triangle");
+    if (n > 0 && ldb < n) throw Error(RL_EINVAL, "trsm: ldb smaller than the column count");
+}
+
+void trsm_ops(int side, int uplo, int diag, i64 m, i64 n, i64 threshold, u64* ops) {
+    if (!ops) return;
+    OpTally t;
+    tally_trsm(t, side, uplo, diag != 0, side == SIDE_LEFT ? m : n, m, n, threshold);
+    ops[0] = t.mul;
+    ops[1] = t.addsub;
+    ops[2] = t.divinv;
+    ops[3] = t.ztest;
+}
+
+// invert_in_place (solvers.cpp:24-31) on a device matrix.
+void invert_dev_impl(u32* dA, i64 n, i64 lda, u32 p, u64* ops, cudaStream_t s) {
+    i64 r = 0;
+    std::vector<u32> sigma((size_t)n);
+    col_ech_dev_impl(dA, n, n, lda, p, /*reduced=*/true, &r, nullptr, sigma.data(), ops, s);
+    if (r < n) throw Error(RL_ESINGULAR, "singular matrix");  // body = red_col_ech_trans's
+    rows_by_inverse_perm(dA, n, lda, sigma.data(), s);
+}
 }  // namespace
 
 extern "C" {
@@ -285,36 +373,172 @@ int rl_cup_u32(uint32_t* A, int64_t m, int64_t n, int64_t lda, uint32_t p, int64
         cudaStream_t s = cudaStreamPerThread;
         u32* dA = (u32*)g_bufA.get((size_t)m * n * 4);
         copy_h2d_2d(dA, n, A, lda, m, n, s);
-        if (m <= 64 && n <= 256) {
-            // Small matrices: the whole factorization in one CTA (one launch), the
-            // same pivot rule and placement as the recursive path.
-            const i64 kcap = std::min(m, n);
-            i32* dmeta = (i32*)g_bufI.get((size_t)(1 + 2 * kcap) * 4);
-            cup_batched(dA, 1, (i32)m, (i32)n, m * n, p, dmeta, dmeta + 1, dmeta + 1 + kcap,
-                        (i32)kcap, s);
-            copy_d2h_2d(A, lda, dA, n, m, n, s);
-            std::vector<i32> meta((size_t)(1 + 2 * kcap));
-            RL_CUDA_CHECK(cudaMemcpyAsync(meta.data(), dmeta, meta.size() * 4, cudaMemcpyDeviceToHost, s));
-            RL_CUDA_CHECK(cudaStreamSynchronize(s));
-            const i64 r = meta[0];
-            const u32* rrp_h = (const u32*)&meta[1];
-            const u32* ipiv_h = (const u32*)&meta[1 + kcap];
-            if (rank) *rank = r;
-            if (rrp) std::copy(rrp_h, rrp_h + r, rrp);
-            if (sigma) sigma_from_ipiv(n, r, ipiv_h, sigma);
-            if (ops) cup_opcount(m, n, r, rrp_h, ipiv_h, ops);
-            return;
-        }
         i64 r = 0;
-        std::vector<u32> rrp_h((size_t)std::min(m, n)), ipiv_h((size_t)std::min(m, n));
-        CupEngine& e = engine_for(m, n, n, p);
-        e.run(dA, s, m * n >= (1 << 18));
+        std::vector<u32> rrp_h, ipiv_h;
+        factor_on_device(dA, m, n, n, p, s, &r, rrp_h, ipiv_h);
         copy_d2h_2d(A, lda, dA, n, m, n, s);
-        e.results(&r, rrp_h.data(), ipiv_h.data(), s);  // synchronises s
+        RL_CUDA_CHECK(cudaStreamSynchronize(s));
         if (rank) *rank = r;
         if (rrp) std::copy(rrp_h.begin(), rrp_h.begin() + r, rrp);
         if (sigma) sigma_from_ipiv(n, r, ipiv_h.data(), sigma);
         if (ops) cup_opcount(m, n, r, rrp_h.data(), ipiv_h.data(), ops);
+    });
+}
+
+int rl_col_ech_trans_u32_dev(uint32_t* dA, int64_t m, int64_t n, int64_t lda, uint32_t p,
+                             int reduced, int64_t* rank, uint32_t* rrp, uint32_t* sigma,
+                             uint64_t* ops, void* stream) {
+    return guard([&] {
+        check_field(p);
+        check_dims(m, n, lda);
+        if (m == 0 || n == 0) {  // cup's degenerate return; nothing to reduce
+            cup_dev_impl(nullptr, m, n, lda, p, rank, rrp, sigma, ops, nullptr);
+            return;
+        }
+        if (!dA) throw Error(RL_EINVAL, "null matrix");
+        require_device();
+        std::lock_guard<std::mutex> lk(g_mu);
+        col_ech_dev_impl(dA, m, n, lda, p, reduced != 0, rank, rrp, sigma, ops, (cudaStream_t)stream);
+    });
+}
+
+int rl_col_ech_trans_u32(uint32_t* A, int64_t m, int64_t n, int64_t lda, uint32_t p, int reduced,
+                         int64_t* rank, uint32_t* rrp, uint32_t* sigma, uint64_t* ops) {
+    return guard([&] {
+        check_field(p);
+        check_dims(m, n, lda);
+        if (m == 0 || n == 0) {
+            cup_dev_impl(nullptr, m, n, lda, p, rank, rrp, sigma, ops, nullptr);
+            return;
+        }
+        if (!A) throw Error(RL_EINVAL, "null matrix");
+        require_device();
+        std::lock_guard<std::mutex> lk(g_mu);
+        cudaStream_t s = cudaStreamPerThread;
+        u32* dA = (u32*)g_bufA.get((size_t)m * n * 4);
+        copy_h2d_2d(dA, n, A, lda, m, n, s);
+        col_ech_dev_impl(dA, m, n, n, p, reduced != 0, rank, rrp, sigma, ops, s);
+        copy_d2h_2d(A, lda, dA, n, m, n, s);
+        RL_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int rl_invert_u32_dev(uint32_t* dA, int64_t n, int64_t lda, uint32_t p, uint64_t* ops,
+                      void* stream) {
+    return guard([&] {
+        check_field(p);
+        check_dims(n, n, lda);
+        if (ops) std::fill(ops, ops + 4, 0ull);
+        if (n == 0) return;
+        if (!dA) throw Error(RL_EINVAL, "null matrix");
+        require_device();
+        std::lock_guard<std::mutex> lk(g_mu);
+        invert_dev_impl(dA, n, lda, p, ops, (cudaStream_t)stream);
+    });
+}
+
+int rl_invert_u32(uint32_t* A, int64_t n, int64_t lda, uint32_t p, uint64_t* ops) {
+    return guard([&] {
+        check_field(p);
+        check_dims(n, n, lda);
+        if (ops) std::fill(ops, ops + 4, 0ull);
+        if (n == 0) return;
+        if (!A) throw Error(RL_EINVAL, "null matrix");
+        require_device();
+        std::lock_guard<std::mutex> lk(g_mu);
+        cudaStream_t s = cudaStreamPerThread;
+        u32* dA = (u32*)g_bufA.get((size_t)n * n * 4);
+        copy_h2d_2d(dA, n, A, lda, n, n, s);
+        int st = RL_OK;
+        try {
+            invert_dev_impl(dA, n, n, p, ops, s);
+        } catch (const Error& e) {
+            if (e.code != RL_ESINGULAR) throw;
+            st = RL_ESINGULAR;  // the body still holds the reduced transform (as the reference)
+        }
+        copy_d2h_2d(A, lda, dA, n, n, n, s);
+        RL_CUDA_CHECK(cudaStreamSynchronize(s));
+        if (st != RL_OK) throw Error(st, "singular matrix");
+    });
+}
+
+int rl_trsm_u32_dev(int side, int uplo, int diag, const uint32_t* dT, int64_t ldt, uint32_t* dB,
+                    int64_t ldb, int64_t m, int64_t n, uint32_t p, int64_t threshold, uint64_t* ops,
+                    void* stream) {
+    return guard([&] {
+        check_field(p);
+        check_trsm_args(side, uplo, diag, m, n, ldt, ldb);
+        const i64 k = side == SIDE_LEFT ? m : n;
+        if (m == 0 || n == 0) {
+            if (ops) std::fill(ops, ops + 4, 0ull);
+            return;
+        }
+        require_device();
+        std::lock_guard<std::mutex> lk(g_mu);
+        cudaStream_t s = (cudaStream_t)stream;
+        if (!diag) {
+            std::vector<u32> dg((size_t)k);
+            RL_CUDA_CHECK(cudaMemcpy2DAsync(dg.data(), 4, dT, (ldt + 1) * 4, 4, k,
+                                            cudaMemcpyDeviceToHost, s));
+            RL_CUDA_CHECK(cudaStreamSynchronize(s));
+            const i64 d = first_zero_diagonal(side, uplo, dg);
+            if (d >= 0) throw Error(RL_ESINGULAR, "singular diagonal at " + std::to_string(d));
+        }
+        trsm_ops(side, uplo, diag, m, n, threshold, ops);
+        trsm_dev_impl(side, uplo, diag, dT, ldt, dB, ldb, m, n, p, s);
+    });
+}
+
+int rl_trsm_u32(int side, int uplo, int diag, const uint32_t* T, int64_t ldt, uint32_t* B,
+                int64_t ldb, int64_t m, int64_t n, uint32_t p, int64_t threshold, uint64_t* ops) {
+    return guard([&] {
+        check_field(p);
+        check_trsm_args(side, uplo, diag, m, n, ldt, ldb);
+        const i64 k = side == SIDE_LEFT ? m : n;
+        if (windows_overlap(T, k, k, ldt, B, m, n, ldb)) throw Error(RL_EOVERLAP, "trsm: T overlaps B");
+        if (m == 0 || n == 0) {
+            if (ops) std::fill(ops, ops + 4, 0ull);
+            return;
+        }
+        if (!diag) {
+            std::vector<u32> dg((size_t)k);
+            for (i64 d = 0; d < k; ++d) dg[d] = T[d * ldt + d];
+            const i64 d = first_zero_diagonal(side, uplo, dg);
+            if (d >= 0) throw Error(RL_ESINGULAR, "singular diagonal at " + std::to_string(d));
+        }
+        trsm_ops(side, uplo, diag, m, n, threshold, ops);
+        require_device();
+        std::lock_guard<std::mutex> lk(g_mu);
+        cudaStream_t s = cudaStreamPerThread;
+        u32* dT = (u32*)g_bufA.get((size_t)k * k * 4);
+        u32* dB = (u32*)g_bufB.get((size_t)m * n * 4);
+        copy_h2d_2d(dT, k, T, ldt, k, k, s);
+        copy_h2d_2d(dB, n, B, ldb, m, n, s);
+        trsm_dev_impl(side, uplo, diag, dT, k, dB, n, m, n, p, s);
+        copy_d2h_2d(B, ldb, dB, n, m, n, s);
+        RL_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int rl_trsm_opcount(int side, int uplo, int diag, int64_t m, int64_t n, int64_t threshold,
+                    uint64_t* ops) {
+    return guard([&] {
+        check_trsm_args(side, uplo, diag, m, n, side == SIDE_LEFT ? m : n, n);
+        if (!ops) throw Error(RL_EINVAL, "null ops");
+        trsm_ops(side, uplo, diag, m, n, threshold, ops);
+    });
+}
+
+int rl_echelon_opcount(int64_t m, int64_t n, int64_t r, int reduced, uint64_t* ops) {
+    return guard([&] {
+        if (!ops) throw Error(RL_EINVAL, "null ops");
+        if (m < 0 || n < 0 || r < 0 || r > std::min(m, n)) throw Error(RL_EDIM, "bad shape/rank");
+        OpTally t;
+        tally_echelon(t, m, n, r, reduced != 0);
+        ops[0] = t.mul;
+        ops[1] = t.addsub;
+        ops[2] = t.divinv;
+        ops[3] = t.ztest;
     });
 }
 

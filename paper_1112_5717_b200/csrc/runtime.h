@@ -22,4 +22,21 @@ struct CudaError : Error {
 
 int num_sms();
 
+// Growable device scratch buffer (workspaces of the host-pointer entry points
+// and of the dense/triangular helpers; callers hold the C-ABI mutex).
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t cap = 0;
+    void* get(size_t bytes) {
+        if (bytes > cap) {
+            if (ptr) cudaFree(ptr);
+            ptr = nullptr;
+            cap = 0;
+            if (cudaMalloc(&ptr, bytes) != cudaSuccess) throw Error(8 /*RL_ENOMEM*/, "cudaMalloc failed");
+            cap = bytes;
+        }
+        return ptr;
+    }
+};
+
 }  // namespace rl
