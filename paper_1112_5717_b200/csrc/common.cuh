@@ -7,7 +7,24 @@
 // canonical remainder for every x < 2^64.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
+
+// Timeline tracing (tools/trace_cup.py, `make trace`): kernels print per-CTA
+// %globaltimer stamps for the leaf at row RL_TRACE_I0.  Compiled out otherwise.
+#ifdef RL_TRACE
+#ifndef RL_TRACE_I0
+#define RL_TRACE_I0 8192
+#endif
+__device__ __forceinline__ unsigned long long rl_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define RL_STAMP(var) const unsigned long long var = rl_now()
+#else
+#define RL_STAMP(var)
+#endif
 
 typedef uint32_t u32;
 typedef uint64_t u64;
@@ -96,6 +113,13 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem, bool val
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem) : "memory");
+}
+// 16-byte copy of which the first src_bytes (0..16) come from gmem, the rest
+// zero-filled (gmem must be 16-byte aligned; it is not read when src_bytes = 0).
+__device__ __forceinline__ void cp_async16z(void* smem, const void* gmem, int src_bytes) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gmem), "r"(src_bytes)
+                 : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.wait_all;" ::: "memory");

@@ -42,14 +42,27 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
     if (m_ > 0 && n_ > 0) node(0, m_);
     dry_ = false;
     const i32 k = std::min(m_, n_);
-    RL_CUDA_CHECK(cudaMalloc(&rp_, sizeof(i32) * (m_ + 1)));
-    RL_CUDA_CHECK(cudaMalloc(&rrp_, sizeof(i32) * (k + 1)));
-    RL_CUDA_CHECK(cudaMalloc(&ipiv_, sizeof(i32) * (k + 1)));
-    RL_CUDA_CHECK(cudaMalloc(&ps_, sizeof(PanelScratch)));
+    // All per-factorization metadata (rank prefix, profile, transpositions, panel
+    // scratch, leaf inverses, inverse table) in ONE allocation: the latency-bound
+    // panel kernels touch all of it, and one mapping keeps their TLB footprint small.
+    auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
+    const size_t o_rp = 0;
+    const size_t o_rrp = o_rp + up(sizeof(i32) * (m_ + 1));
+    const size_t o_ipiv = o_rrp + up(sizeof(i32) * (k + 1));
+    const size_t o_ps = o_ipiv + up(sizeof(i32) * (k + 1));
+    const size_t o_uinv = o_ps + up(sizeof(PanelScratch));
+    const size_t o_tab = o_uinv + up(sizeof(u32) * PB * PB * (leaf_of_.size() + 1));
+    const size_t total = o_tab + (p_ <= 65536u ? 65536 * sizeof(uint16_t) : 0);
+    RL_CUDA_CHECK(cudaMalloc(&meta_, total));
+    char* base = static_cast<char*>(meta_);
+    rp_ = reinterpret_cast<i32*>(base + o_rp);
+    rrp_ = reinterpret_cast<i32*>(base + o_rrp);
+    ipiv_ = reinterpret_cast<i32*>(base + o_ipiv);
+    ps_ = reinterpret_cast<PanelScratch*>(base + o_ps);
     RL_CUDA_CHECK(cudaMemset(ps_, 0, sizeof(PanelScratch)));
-    RL_CUDA_CHECK(cudaMalloc(&uinv_, sizeof(u32) * PB * PB * (leaf_of_.size() + 1)));
+    uinv_ = reinterpret_cast<u32*>(base + o_uinv);
     if (p_ <= 65536u) {
-        RL_CUDA_CHECK(cudaMalloc(&inv_table_, 65536 * sizeof(uint16_t)));
+        inv_table_ = reinterpret_cast<uint16_t*>(base + o_tab);
         build_inv_table(inv_table_, p_, nullptr);
         RL_CUDA_CHECK(cudaDeviceSynchronize());
     }
@@ -59,12 +72,7 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
 
 CupEngine::~CupEngine() {
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
-    cudaFree(rp_);
-    cudaFree(rrp_);
-    cudaFree(ipiv_);
-    cudaFree(ps_);
-    cudaFree(uinv_);
-    cudaFree(inv_table_);
+    cudaFree(meta_);
     cudaFree(a2_);
     cudaFree(b2_);
 }

@@ -55,6 +55,7 @@ private:
     bool fused_trsm_ = true;
     u32* A_ = nullptr;
     cudaStream_t s_ = nullptr;
+    void* meta_ = nullptr;                     // one allocation for everything below
     i32* rp_ = nullptr;
     i32* rrp_ = nullptr;
     i32* ipiv_ = nullptr;

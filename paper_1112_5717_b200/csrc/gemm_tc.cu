@@ -418,11 +418,13 @@ void launch_tc(const GemmArgs& g, i64 Kmax, i64 Nmax, uint8_t* a2, uint8_t* b2, 
         {
             i64 work = MB * KB * BM * 8;
             int pg = (int)std::min<i64>((work + 255) / 256, (i64)nsm * 16);
+            RL_ONCE_MAX_SMEM(pack_a_kernel<L>);
             pack_a_kernel<L><<<std::max(pg, 1), 256, 0, s>>>(g, a2);
         }
         {
             i64 work = KB * 4 * NB;
             int pg = (int)std::min<i64>(work, (i64)nsm * 8);
+            RL_ONCE_MAX_SMEM(pack_b_kernel<L>);
             pack_b_kernel<L><<<std::max(pg, 1), 256, 0, s>>>(g, b2, sc[1], sc[2], sc[3]);
         }
     }
@@ -434,6 +436,7 @@ void launch_tc(const GemmArgs& g, i64 Kmax, i64 Nmax, uint8_t* a2, uint8_t* b2, 
                                            (int)C_::SMEM));
         attr_set = true;
     }
+    RL_ONCE_MAX_SMEM(gemm_tc_kernel<L>);
     gemm_tc_kernel<L><<<grid, NTHR, C_::SMEM, s>>>(g, a2, b2, sc[1], sc[2], sc[3]);
     RL_CUDA_CHECK(cudaGetLastError());
 }
@@ -548,6 +551,8 @@ void gemm_simt(const GemmArgs& g, i64 Kmax, i64 Nmax, cudaStream_t s) {
     if (g.M <= 0 || Kmax <= 0 || Nmax <= 0) return;
     const i64 tiles = ((g.M + 63) / 64) * ((Nmax + 63) / 64);
     int grid = (int)std::min<i64>(tiles, (i64)num_sms() * 4);
+    RL_ONCE_MAX_SMEM(gemm_simt_kernel<true>);
+    RL_ONCE_MAX_SMEM(gemm_simt_kernel<false>);
     if (g.f.p <= 65536u && Kmax <= (1ll << 31))
         gemm_simt_kernel<true><<<std::max(grid, 1), 256, 0, s>>>(g);
     else

@@ -27,21 +27,23 @@ namespace rl {
 
 namespace {
 
-constexpr int TT = 256;  // tail tile width (columns per CTA tile)
+constexpr int TT = 64;   // tail tile width (columns per CTA tile)
 
 // Inverse of the leaf's unit upper pivot block U (r x r, rows rrp[c0+j],
-// columns c0+j'), into uinv (PB x PB, zero padded).  Blocked: the eight 8 x 8
-// diagonal blocks are inverted by eight warps at once, then block rows from the
-// bottom: X_I,J = -X_I,I * sum_{K=I+1..J} U_I,K X_K,J.
+// columns c0+j'), into uinv (PB x PB, zero padded).  Recursive doubling: the
+// eight 8 x 8 diagonal blocks are inverted by eight warps at once, then pairs
+// of s x s blocks merge (s = 8, 16, 32) through X_AB = -X_AA * (U_AB * X_BB),
+// two fully parallel products per level (3 levels, 6 barriers).
 template <bool SP>
-__device__ void leaf_uinv(const PanelArgs& a, i32 c0, int rt, u32 (*U)[PB + 1], u32 (*X)[PB + 1]) {
+__device__ void leaf_uinv(const PanelArgs& a, i32 c0, int rt, u32 (*U)[PB + 1], u32 (*X)[PB + 1],
+                          u32 (*T)[PB + 1]) {
     const Fp f = a.f;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nt = blockDim.x;
     __shared__ i32 s_row[PB];
     if (tid < PB) s_row[tid] = tid < rt ? __ldcg(a.rrp + c0 + tid) : 0;
     __syncthreads();
 #pragma unroll 4
-    for (int e = tid; e < PB * PB; e += blockDim.x) {
+    for (int e = tid; e < PB * PB; e += nt) {
         const int i = e / PB, k = e % PB;
         const bool ok = i < k && k < rt;
         cp_async4(&U[i][k], ok ? a.A + (i64)s_row[i] * a.lda + c0 + k : a.A, ok);
@@ -58,62 +60,42 @@ __device__ void leaf_uinv(const PanelArgs& a, i32 c0, int rt, u32 (*U)[PB + 1], 
             u64 acc = 0;
 #pragma unroll
             for (int k = i + 1; k < 8; ++k) acc += mulmod_t<SP>(U[base + i][base + k], x[k], f);
-            const u32 s = red64(acc, f);
+            const u32 sum = red64(acc, f);
             const u32 d = (i == c && base + i < rt) ? 1u % f.p : 0u;
-            x[i] = i > c ? 0u : submod(d, s, f);
+            x[i] = i > c ? 0u : submod(d, sum, f);
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) X[base + i][base + c] = x[i];
     }
     __syncthreads();
-    for (int I = 6; I >= 0; --I) {
-        const int r0 = 8 * I, cstart = r0 + 8, ncol = PB - cstart;
-        // T = sum_{q = cstart..col} U[r0 + r][q] X[q][col]  -> into X's block row
-        u32 t[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int e = tid + h * blockDim.x;
-            t[h] = 0;
-            if (e < 8 * ncol) {
-                const int r = e / ncol, col = cstart + e % ncol;
-                u64 acc = 0;
-                for (int q = cstart; q <= col; ++q) {
-                    if (SP) acc += (u64)U[r0 + r][q] * X[q][col];
-                    else acc += mulmod(U[r0 + r][q], X[q][col], f);
-                }
-                t[h] = red64(acc, f);
+    for (int sz = 8; sz < PB; sz *= 2) {
+        const int nout = (PB / (2 * sz)) * sz * sz;
+        // T_AB = U_AB * X_BB (X_BB upper triangular: u <= j)
+        for (int e = tid; e < nout; e += nt) {
+            const int pb = e / (sz * sz), rem = e % (sz * sz), i = rem / sz, j = rem % sz;
+            const int A0 = pb * 2 * sz, B0 = A0 + sz;
+            u64 acc = 0;
+            for (int u = 0; u <= j; ++u) {
+                if (SP) acc += (u64)U[A0 + i][B0 + u] * X[B0 + u][B0 + j];
+                else acc += mulmod(U[A0 + i][B0 + u], X[B0 + u][B0 + j], f);
             }
+            T[A0 + i][B0 + j] = SP ? red_sp(acc, f) : red64(acc, f);
         }
         __syncthreads();
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int e = tid + h * blockDim.x;
-            if (e < 8 * ncol) X[r0 + e / ncol][cstart + e % ncol] = t[h];
-        }
-        __syncthreads();
-        // X_I,: = -X_I,I * T
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int e = tid + h * blockDim.x;
-            t[h] = 0;
-            if (e < 8 * ncol) {
-                const int r = e / ncol, col = cstart + e % ncol;
-                u64 acc = 0;
-#pragma unroll
-                for (int s = 0; s < 8; ++s) acc += mulmod_t<SP>(X[r0 + r][r0 + s], X[r0 + s][col], f);
-                const u32 v = red64(acc, f);
-                t[h] = v ? f.p - v : 0u;
+        // X_AB = -X_AA * T_AB (X_AA upper triangular: u >= i)
+        for (int e = tid; e < nout; e += nt) {
+            const int pb = e / (sz * sz), rem = e % (sz * sz), i = rem / sz, j = rem % sz;
+            const int A0 = pb * 2 * sz, B0 = A0 + sz;
+            u64 acc = 0;
+            for (int u = i; u < sz; ++u) {
+                if (SP) acc += (u64)X[A0 + i][A0 + u] * T[A0 + u][B0 + j];
+                else acc += mulmod(X[A0 + i][A0 + u], T[A0 + u][B0 + j], f);
             }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int e = tid + h * blockDim.x;
-            if (e < 8 * ncol) X[r0 + e / ncol][cstart + e % ncol] = t[h];
+            X[A0 + i][B0 + j] = negmod(SP ? red_sp(acc, f) : red64(acc, f), f);
         }
         __syncthreads();
     }
-    for (int e = tid; e < PB * PB; e += blockDim.x) a.uinv[e] = X[e / PB][e % PB];
+    for (int e = tid; e < PB * PB; e += nt) a.uinv[e] = X[e / PB][e % PB];
     __syncthreads();
 }
 
@@ -202,15 +184,19 @@ __device__ void panel_fallback(const PanelArgs& a, u32* red_buf) {
     __syncthreads();
 }
 
-// V = Minv * P on 64 x TT column tiles: thread (ty, tx) owns rows 8ty..8ty+7 and
-// columns tx + 32y (y < 8) -- conflict-free shared loads, coalesced stores.
+// V = Minv * P on 64 x TT column tiles: thread (ty, tx) owns rows ty + 16x
+// (x < 4, balancing the triangle) and columns 4tx..4tx+3 (one 16-byte shared
+// load of P per 16 products).  Small tiles give many resident CTAs per SM.
 template <bool SP>
 __global__ void __launch_bounds__(256) panel_tail_kernel(PanelArgs a) {
     extern __shared__ __align__(16) u32 tsm[];
     u32 (*Mi)[PB + 1] = reinterpret_cast<u32 (*)[PB + 1]>(tsm);               // [PB][PB+1]
     u32 (*Ps)[TT + 4] = reinterpret_cast<u32 (*)[TT + 4]>(tsm + PB * (PB + 1)); // [PB][TT+4]
+    u32 (*Xs)[PB + 1] = reinterpret_cast<u32 (*)[PB + 1]>(tsm + PB * (PB + 1));  // uinv scratch
+    u32 (*Ts)[PB + 1] = reinterpret_cast<u32 (*)[PB + 1]>(tsm + 2 * PB * (PB + 1));
     __shared__ u32 red_buf[256];
     __shared__ int s_last;
+    RL_STAMP(t_enter);
     PanelScratch* ps = a.ps;
     const Fp f = a.f;
     const int tid = threadIdx.x;
@@ -218,14 +204,14 @@ __global__ void __launch_bounds__(256) panel_tail_kernel(PanelArgs a) {
     u32 bad = 0;
     if (blockIdx.x == gridDim.x - 1) {
         if (W > 0 && rt > 0) {
-            leaf_uinv<SP>(a, c0, rt, Mi, reinterpret_cast<u32 (*)[PB + 1]>(tsm + 2 * PB * (PB + 1)));
+            leaf_uinv<SP>(a, c0, rt, Mi, Xs, Ts);
         }
     } else if (W > 0) {
         const u64 dead = ps->dead_mask;
 #pragma unroll 4
         for (int e = tid; e < PB * PB; e += blockDim.x)
             cp_async4(&Mi[e / PB][e % PB], &ps->Minv[e / PB][e % PB], true);
-        const int tx = tid & 31, ty = tid >> 5;
+        const int tx = tid & 15, ty = tid >> 4;
         const i32 col0 = c0 + rt;
         const i32 ntile = (a.N - col0 + TT - 1) / TT;
         for (i32 t = blockIdx.x; t < ntile; t += gridDim.x - 1) {
@@ -239,55 +225,68 @@ __global__ void __launch_bounds__(256) panel_tail_kernel(PanelArgs a) {
             }
             cp_async_wait_all();
             __syncthreads();
-            u64 acc[8][8];
+            // rows ty + 16x interleave short and long rows of the triangle
+            u64 acc[4][4];
 #pragma unroll
-            for (int x = 0; x < 8; ++x)
+            for (int x = 0; x < 4; ++x)
 #pragma unroll
-                for (int y = 0; y < 8; ++y) acc[x][y] = 0;
-            const int kmax = min(b, ty * 8 + 8);
+                for (int y = 0; y < 4; ++y) acc[x][y] = 0;
+            const int kmax = min(b, ty + 49);
+#pragma unroll 4
             for (int k = 0; k < kmax; ++k) {
-                u32 mv[8], pv[8];
+                const uint4 pv = *reinterpret_cast<const uint4*>(&Ps[k][4 * tx]);
 #pragma unroll
-                for (int x = 0; x < 8; ++x) mv[x] = Mi[ty * 8 + x][k];
-#pragma unroll
-                for (int y = 0; y < 8; ++y) pv[y] = Ps[k][tx + 32 * y];
-#pragma unroll
-                for (int x = 0; x < 8; ++x)
-#pragma unroll
-                    for (int y = 0; y < 8; ++y) {
-                        if (SP) acc[x][y] += (u64)mv[x] * pv[y];
-                        else acc[x][y] += mulmod(mv[x], pv[y], f);
+                for (int x = 0; x < 4; ++x) {
+                    const u32 mv = Mi[ty + 16 * x][k];
+                    if (SP) {
+                        acc[x][0] += (u64)mv * pv.x;
+                        acc[x][1] += (u64)mv * pv.y;
+                        acc[x][2] += (u64)mv * pv.z;
+                        acc[x][3] += (u64)mv * pv.w;
+                    } else {
+                        acc[x][0] += mulmod(mv, pv.x, f);
+                        acc[x][1] += mulmod(mv, pv.y, f);
+                        acc[x][2] += mulmod(mv, pv.z, f);
+                        acc[x][3] += mulmod(mv, pv.w, f);
                     }
+                }
             }
 #pragma unroll
-            for (int x = 0; x < 8; ++x) {
-                const int i = ty * 8 + x;
+            for (int x = 0; x < 4; ++x) {
+                const int i = ty + 16 * x;
                 if (i >= b) continue;
-                u32* out = a.A + (i64)(a.i0 + i) * a.lda + cb;
+                u32* out = a.A + (i64)(a.i0 + i) * a.lda + cb + 4 * tx;
                 const bool isdead = (dead >> i) & 1;
 #pragma unroll
-                for (int y = 0; y < 8; ++y) {
-                    const int cc = tx + 32 * y;
-                    if (cb + cc < a.N) {
+                for (int y = 0; y < 4; ++y) {
+                    if (cb + 4 * tx + y < a.N) {
                         const u32 val = SP ? red_sp(acc[x][y], f) : red64(acc[x][y], f);
                         if (isdead) bad |= val;
-                        out[cc] = val;
+                        out[y] = val;
                     }
                 }
             }
         }
     }
+    RL_STAMP(t_work);
     if (__syncthreads_or(bad != 0) && tid == 0) atomicOr(&ps->flag, 1u);
     __threadfence();
     __syncthreads();
     if (tid == 0) s_last = (atomicAdd(&ps->counter, 1u) == gridDim.x - 1);
     __syncthreads();
+#ifdef RL_TRACE
+    if (a.i0 == RL_TRACE_I0 && tid == 0) {
+        RL_STAMP(t_exit);
+        printf("TRACE tail cta %d/%d enter %llu work %llu exit %llu\n", blockIdx.x, gridDim.x, t_enter,
+               t_work, t_exit);
+    }
+#endif
     if (!s_last) return;
     __threadfence();
     if (atomicAdd(&ps->flag, 0u) != 0) {
         panel_fallback(a, red_buf);
         const int r2 = ps->r;
-        if (r2 > 0) leaf_uinv<SP>(a, c0, r2, Mi, reinterpret_cast<u32 (*)[PB + 1]>(tsm + 2 * PB * (PB + 1)));
+        if (r2 > 0) leaf_uinv<SP>(a, c0, r2, Mi, Xs, Ts);
     }
     if (tid == 0) {
         ps->counter = 0;
@@ -355,9 +354,8 @@ __global__ void __launch_bounds__(256) trsm_leaf_kernel(TrsmLeafArgs a) {
 }  // namespace
 
 void panel_tail(const PanelArgs& a, cudaStream_t s) {
-    const size_t smem = sizeof(u32) * (PB * (PB + 1) + PB * (TT + 4));
-    static_assert(sizeof(u32) * PB * (TT + 4) >= sizeof(u32) * 2 * PB * (PB + 1),
-                  "uinv scratch must fit in the tile buffer");
+    // tiles: Minv + P tile; the U^{-1} CTA: U, X, T (3 blocks of PB x (PB+1))
+    const size_t smem = sizeof(u32) * std::max<size_t>(PB * (PB + 1) + PB * (TT + 4), 3 * PB * (PB + 1));
     static bool attr = false;
     if (!attr) {
         RL_CUDA_CHECK(cudaFuncSetAttribute(panel_tail_kernel<true>,
@@ -366,7 +364,9 @@ void panel_tail(const PanelArgs& a, cudaStream_t s) {
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    const int grid = std::max(1, std::min((a.N + TT - 1) / TT, 2 * num_sms())) + 1;
+    const int grid = std::max(1, std::min((a.N + TT - 1) / TT, 8 * num_sms())) + 1;
+    RL_ONCE_MAX_SMEM(panel_tail_kernel<true>);
+    RL_ONCE_MAX_SMEM(panel_tail_kernel<false>);
     if (a.f.p <= 65536u) panel_tail_kernel<true><<<grid, 256, smem, s>>>(a);
     else panel_tail_kernel<false><<<grid, 256, smem, s>>>(a);
     RL_CUDA_CHECK(cudaGetLastError());

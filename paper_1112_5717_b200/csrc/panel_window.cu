@@ -158,63 +158,82 @@ __device__ __forceinline__ u32 fred(u64 x, const Fp& f) {
     return SP ? red_sp(x, f) : red64(x, f);
 }
 
+// One warp factors the bt x bt diagonal block at rows/columns r0.. of s_R
+// (element (k, c): lane (k&3)*8 + c holds v0 for k < 4 and v1 for k >= 4, the
+// block's current values), writes back the block (U part reduced, C part raw),
+// the negated multipliers s_M and the pivots; fail = 1 on a zero pivot.
+template <bool SP>
+__device__ __forceinline__ void diag_factor(u32* s_R, u32 (*s_C)[PB + 1], u32* s_pv, u32* s_pinvA,
+                                            const uint16_t* s_inv, u32 (*s_M)[LB], int* s_fail,
+                                            int r0, int bt, u32 v0, u32 v1, int lane, const Fp& f) {
+    const int cc = lane & 7, k0 = lane >> 3, k1 = k0 + 4;
+    int fail = 0;
+    for (int j = 0; j < bt; ++j) {
+        const u32 pv = __shfl_sync(FULL, j < 4 ? v0 : v1, (j & 3) * 8 + j);
+        if (pv == 0) {
+            fail = 1;
+            break;
+        }
+        const u32 pinv = SP ? (u32)s_inv[pv] : invmod(pv, f);
+        const u32 c0v = __shfl_sync(FULL, v0, k0 * 8 + j);         // C(k0, j)
+        const u32 c1v = __shfl_sync(FULL, v1, (k1 - 4) * 8 + j);   // C(k1, j)
+        const u32 uj = __shfl_sync(FULL, j < 4 ? v0 : v1, (j & 3) * 8 + cc);
+        const u32 m0 = mulmod_t<SP>(c0v, pinv, f), m1 = mulmod_t<SP>(c1v, pinv, f);
+        if (cc == j) {  // this lane holds C(k, j) for its rows
+            if (k0 > j && k0 < bt) s_M[r0 + k0][j] = m0 ? f.p - m0 : 0u;
+            if (k1 > j && k1 < bt) s_M[r0 + k1][j] = m1 ? f.p - m1 : 0u;
+        }
+        if (k0 > j && cc > j) v0 = fred<SP>(fms<SP>(v0, m0, uj, f), f);
+        if (k1 > j && cc > j) v1 = fred<SP>(fms<SP>(v1, m1, uj, f), f);
+        if (lane == 0) {
+            s_pv[r0 + j] = pv;
+            s_pinvA[r0 + j] = pinv;
+        }
+    }
+    if (k0 < bt && cc < bt) {
+        s_R[(r0 + k0) * WT + r0 + cc] = v0;
+        if (cc < k0) s_C[r0 + k0][r0 + cc] = v0;
+    }
+    if (k1 < bt && cc < bt) {
+        s_R[(r0 + k1) * WT + r0 + cc] = v1;
+        if (cc < k1) s_C[r0 + k1][r0 + cc] = v1;
+    }
+    if (lane == 0) *s_fail = fail;
+}
+
 // Speculative pivot discovery for GENERIC leaves: blocked right-looking LU of
 // the window without pivoting, in shared memory (s_R = [window | identity],
 // reduced values).  If every diagonal value is nonzero, row i's first nonzero
 // at positions >= i is position i itself, so this IS the CUP of the leaf
-// (rrp = identity, no transpositions).  Leaf blocks of 8 rows are factored by
-// one warp; the block rows' right part is a column-parallel forward
-// substitution; the rows below get their C entries by a row-parallel
-// triangular solve and a rank-8 lazy update.  Returns false (uniformly) on the
-// first zero pivot; the caller then runs the exact lockstep path.
+// (rrp = identity, no transpositions).  Per 8-row block: the block rows' right
+// part is a column-parallel forward substitution, the rows below get their C
+// entries by a row-parallel triangular solve, then a rank-8 lazy update -- during
+// which warp 0 already updates and factors the NEXT diagonal block (lookahead),
+// so the serial 8 x 8 factorization is off the critical path.  Returns false
+// (uniformly) on the first zero pivot; the caller then runs the exact path.
 template <bool SP>
 __device__ bool spec_lu(u32* s_R, u32 (*s_C)[PB + 1], u32* s_pv, u32* s_pinvA,
-                        const uint16_t* s_inv, u32 (*s_M)[LB], int* s_fail, int b, int w,
+                        const uint16_t* s_inv, u32 (*s_M2)[PB][LB], int* s_fail, int b, int w,
                         const Fp& f) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nt = blockDim.x;
     if (w < b) return false;
-    for (int r0 = 0; r0 < b; r0 += LB) {
-        const int bt = min(LB, b - r0);
-        // (a) leaf: bt x bt diagonal block, element (k, c): lane (k&3)*8 + c, v0 (k<4) / v1
+    // multipliers double-buffered by block parity: warp 0 writes the next block's
+    // while the other warps still read the current block's
+    {
+        u32 (*s_M)[LB] = s_M2[0];
+        const int cc = lane & 7, k0 = lane >> 3, k1 = k0 + 4, bt = min(LB, b);
         if (warp == 0) {
-            const int cc = lane & 7, k0 = lane >> 3, k1 = k0 + 4;
-            u32 v0 = (k0 < bt && cc < bt) ? s_R[(r0 + k0) * WT + r0 + cc] : 0u;
-            u32 v1 = (k1 < bt && cc < bt) ? s_R[(r0 + k1) * WT + r0 + cc] : 0u;
-            int fail = 0;
-            for (int j = 0; j < bt; ++j) {
-                const u32 pv = __shfl_sync(FULL, j < 4 ? v0 : v1, (j & 3) * 8 + j);
-                if (pv == 0) {
-                    fail = 1;
-                    break;
-                }
-                const u32 pinv = SP ? (u32)s_inv[pv] : invmod(pv, f);
-                const u32 c0v = __shfl_sync(FULL, v0, k0 * 8 + j);         // C(k0, j)
-                const u32 c1v = __shfl_sync(FULL, v1, (k1 - 4) * 8 + j);   // C(k1, j)
-                const u32 uj = __shfl_sync(FULL, j < 4 ? v0 : v1, (j & 3) * 8 + cc);
-                const u32 m0 = mulmod_t<SP>(c0v, pinv, f), m1 = mulmod_t<SP>(c1v, pinv, f);
-                if (cc == j) {  // this lane holds C(k, j) for its rows
-                    if (k0 > j && k0 < bt) s_M[r0 + k0][j] = m0 ? f.p - m0 : 0u;
-                    if (k1 > j && k1 < bt) s_M[r0 + k1][j] = m1 ? f.p - m1 : 0u;
-                }
-                if (k0 > j && cc > j) v0 = fred<SP>(fms<SP>(v0, m0, uj, f), f);
-                if (k1 > j && cc > j) v1 = fred<SP>(fms<SP>(v1, m1, uj, f), f);
-                if (lane == 0) {
-                    s_pv[r0 + j] = pv;
-                    s_pinvA[r0 + j] = pinv;
-                }
-            }
-            if (k0 < bt && cc < bt) {
-                s_R[(r0 + k0) * WT + r0 + cc] = v0;
-                if (cc < k0) s_C[r0 + k0][r0 + cc] = v0;
-            }
-            if (k1 < bt && cc < bt) {
-                s_R[(r0 + k1) * WT + r0 + cc] = v1;
-                if (cc < k1) s_C[r0 + k1][r0 + cc] = v1;
-            }
-            if (lane == 0) *s_fail = fail;
+            const u32 v0 = (k0 < bt && cc < bt) ? s_R[k0 * WT + cc] : 0u;
+            const u32 v1 = (k1 < bt && cc < bt) ? s_R[k1 * WT + cc] : 0u;
+            diag_factor<SP>(s_R, s_C, s_pv, s_pinvA, s_inv, s_M, s_fail, 0, bt, v0, v1, lane, f);
         }
         __syncthreads();
+    }
+    for (int r0 = 0; r0 < b; r0 += LB) {
         if (*s_fail) return false;
+        u32 (*s_M)[LB] = s_M2[(r0 / LB) & 1];
+        u32 (*s_Mn)[LB] = s_M2[((r0 / LB) + 1) & 1];
+        const int bt = min(LB, b - r0);
         const int x0 = r0 + bt;  // first column right of the block
         // Columns still needed: the rest of the pivot block [x0, b) and the identity
         // block [PW, WT); window columns >= b hold no pivot on this path (the tail
@@ -255,28 +274,58 @@ __device__ bool spec_lu(u32* s_R, u32 (*s_C)[PB + 1], u32* s_pv, u32* s_pinvA,
             dst[1] = make_uint4(nm[4], nm[5], nm[6], nm[7]);
         }
         __syncthreads();
-        // (d) rank-8 update of the rows below (a block with rows below is full: bt == LB)
         if (R > 0) {
-            const int G = max(1, nt / X);
-            for (int e = tid; e < X * G; e += nt) {
-                const int ex = e % X, g = e / X;
-                const int x = ex < Xw ? x0 + ex : PW + (ex - Xw);
-                u32 u[LB];
+            const int nbt = min(LB, R);  // next diagonal block: rows/cols [x0, x0 + nbt)
+            if (warp == 0) {
+                // lookahead: rank-8 update of the next diagonal block, then factor it
+                const int cc = lane & 7, k0 = lane >> 3, k1 = k0 + 4;
+                u32 v0 = 0, v1 = 0;
+                if (k0 < nbt && cc < nbt) {
+                    const uint4* mr = reinterpret_cast<const uint4*>(&s_M[x0 + k0][0]);
+                    const uint4 m0 = mr[0], m1 = mr[1];
+                    const u32 nmv[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+                    u64 acc = s_R[(x0 + k0) * WT + x0 + cc];
 #pragma unroll
-                for (int j = 0; j < LB; ++j) u[j] = s_R[(r0 + j) * WT + x];
-                for (int k = x0 + g; k < b; k += G) {
-                    const uint4* mrow = reinterpret_cast<const uint4*>(&s_M[k][0]);
-                    const uint4 m0 = mrow[0], m1 = mrow[1];
-                    u64 acc = s_R[k * WT + x];
-                    acc = fmsn<SP>(acc, m0.x, u[0], f);
-                    acc = fmsn<SP>(acc, m0.y, u[1], f);
-                    acc = fmsn<SP>(acc, m0.z, u[2], f);
-                    acc = fmsn<SP>(acc, m0.w, u[3], f);
-                    acc = fmsn<SP>(acc, m1.x, u[4], f);
-                    acc = fmsn<SP>(acc, m1.y, u[5], f);
-                    acc = fmsn<SP>(acc, m1.z, u[6], f);
-                    acc = fmsn<SP>(acc, m1.w, u[7], f);
-                    s_R[k * WT + x] = fred<SP>(acc, f);
+                    for (int j = 0; j < LB; ++j) acc = fmsn<SP>(acc, nmv[j], s_R[(r0 + j) * WT + x0 + cc], f);
+                    v0 = fred<SP>(acc, f);
+                }
+                if (k1 < nbt && cc < nbt) {
+                    const uint4* mr = reinterpret_cast<const uint4*>(&s_M[x0 + k1][0]);
+                    const uint4 m0 = mr[0], m1 = mr[1];
+                    const u32 nmv[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+                    u64 acc = s_R[(x0 + k1) * WT + x0 + cc];
+#pragma unroll
+                    for (int j = 0; j < LB; ++j) acc = fmsn<SP>(acc, nmv[j], s_R[(r0 + j) * WT + x0 + cc], f);
+                    v1 = fred<SP>(acc, f);
+                }
+                diag_factor<SP>(s_R, s_C, s_pv, s_pinvA, s_inv, s_Mn, s_fail, x0, nbt, v0, v1, lane, f);
+            } else {
+                // (d) rank-8 update of the rows below (a block with rows below is
+                // full: bt == LB), except the next diagonal block (warp 0's)
+                const int t2 = tid - 32, n2 = nt - 32;
+                const int G = max(1, n2 / X);
+                for (int e = t2; e < X * G; e += n2) {
+                    const int ex = e % X, g = e / X;
+                    const int x = ex < Xw ? x0 + ex : PW + (ex - Xw);
+                    const bool diagcol = x < x0 + nbt;  // x in [x0, x0 + nbt)
+                    u32 u[LB];
+#pragma unroll
+                    for (int j = 0; j < LB; ++j) u[j] = s_R[(r0 + j) * WT + x];
+                    for (int k = x0 + g; k < b; k += G) {
+                        if (diagcol && k < x0 + nbt) continue;
+                        const uint4* mrow = reinterpret_cast<const uint4*>(&s_M[k][0]);
+                        const uint4 m0 = mrow[0], m1 = mrow[1];
+                        u64 acc = s_R[k * WT + x];
+                        acc = fmsn<SP>(acc, m0.x, u[0], f);
+                        acc = fmsn<SP>(acc, m0.y, u[1], f);
+                        acc = fmsn<SP>(acc, m0.z, u[2], f);
+                        acc = fmsn<SP>(acc, m0.w, u[3], f);
+                        acc = fmsn<SP>(acc, m1.x, u[4], f);
+                        acc = fmsn<SP>(acc, m1.y, u[5], f);
+                        acc = fmsn<SP>(acc, m1.z, u[6], f);
+                        acc = fmsn<SP>(acc, m1.w, u[7], f);
+                        s_R[k * WT + x] = fred<SP>(acc, f);
+                    }
                 }
             }
         }
@@ -294,7 +343,7 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
     __shared__ i32 s_sig[PW];
     __shared__ int s_c[2];
     __shared__ u32 s_pinv[2];
-    __shared__ __align__(16) u32 s_M[PB][LB];
+    __shared__ __align__(16) u32 s_M[2][PB][LB];
     __shared__ int s_fail;
     WinShared S;
     S.s_R = reinterpret_cast<u32*>(dsm);
@@ -304,6 +353,7 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
     S.s_pinv = s_pinv;
     S.s_pv = s_pv;
     S.s_pinvA = s_pinvA;
+    RL_STAMP(t_enter);
     u32* s_R = S.s_R;
     PanelScratch* ps = a.ps;
     const Fp f = a.f;
@@ -359,7 +409,9 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
     }
     cp_async_wait_all();
     __syncthreads();
+    RL_STAMP(t_loaded);
     const bool spec = spec_lu<SP>(s_R, s_C, s_pv, s_pinvA, S.s_inv, s_M, &s_fail, b, w, f);
+    RL_STAMP(t_lu);
     int r = 0;
     if (spec) {
         r = b;
@@ -447,8 +499,10 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
     }  // exact path
 
     // ------------------------------------------------------------ finalize
+    RL_STAMP(t_fact);
     const int rt = r;
-    if (warp == 1 && lane == 0) {  // window column permutation
+    // (the speculative path made no transposition: both loops are identities)
+    if (!spec && warp == 1 && lane == 0) {  // window column permutation
         for (int x = 0; x < PW; ++x) s_sig[x] = x;
         for (int j = 0; j < rt; ++j) {
             const int cc = s_pos[j];
@@ -456,7 +510,7 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
             s_sig[j] = s_sig[cc];
             s_sig[cc] = t;
         }
-    } else if (warp >= 2 && warp < 4) {  // later transpositions onto the pivot rows
+    } else if (!spec && warp >= 2 && warp < 4) {  // later transpositions onto the pivot rows
         const int j = tid - 64;
         if (j < rt) {
             u32* Ur = s_R + s_rrp[j] * WT;
@@ -472,10 +526,34 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
     }
     __syncthreads();
     // (a) pivot-column region [c0, c0 + rt): C entries, raw pivots, normalised U
-    // (b) [c0 + rt, c0 + w): original values in the final column order (the tail
-    //     kernel replaces them with V = Minv * P).  The speculative path made no
-    //     transposition, so those columns still hold exactly that.
-    const int xend = spec ? min(w, rt) : w;
+    // (b) exact path only: [c0 + rt, c0 + w) gets the original values in the final
+    //     column order (the tail kernel replaces them with V = Minv * P).  The
+    //     speculative path made no transposition, so those columns already hold that.
+#ifdef RL_TRACE
+    unsigned long long t_mid = 0;
+#endif
+    if (spec) {
+        // rrp = identity: row k's pivot is column k -- C left of it, the raw pivot,
+        // U = reduced value * pivot^{-1} right of it; Minv row k scaled likewise
+#pragma unroll 4
+        for (int e = tid; e < PB * PB; e += blockDim.x) {
+            const int k = e / PB, x = e % PB;
+            if (k < b && x < b) {
+                const u32 rv = s_R[k * WT + x];
+                const u32 val = x < k ? s_C[k][x] : (x == k ? rv : mulmod_t<SP>(rv, s_pinvA[k], f));
+                a.A[(i64)(a.i0 + k) * a.lda + c0 + x] = val;
+            }
+        }
+#ifdef RL_TRACE
+        t_mid = rl_now();
+#endif
+#pragma unroll 4
+        for (int e = tid; e < PB * PB; e += blockDim.x) {
+            const int k = e / PB, i = e % PB;
+            ps->Minv[k][i] = (k < b && i < b) ? mulmod_t<SP>(s_R[k * WT + PW + i], s_pinvA[k], f) : 0u;
+        }
+    } else {
+    const int xend = w;
     for (int e = tid; e < b * PW; e += blockDim.x) {
         const int k = e / PW, x = e % PW;
         if (x >= xend) continue;
@@ -506,8 +584,10 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
             }
         }
         ps->Minv[k][i] = mi;
-        if (!spec) ps->Mr[k][i] = mr;  // fallback restore only (exact path)
+        ps->Mr[k][i] = mr;  // fallback restore only (exact path)
     }
+    }
+    RL_STAMP(t_f2);
     for (int e = tid; e < PB; e += blockDim.x) {
         const bool real = e < b;
         ps->piv_of_row[e] = real ? s_por[e] : -1;
@@ -529,6 +609,13 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
             ps->r = rt;
         }
     }
+#ifdef RL_TRACE
+    if (a.i0 == RL_TRACE_I0 && tid == 0) {
+        RL_STAMP(t_exit);
+        printf("TRACE window enter %llu loaded %llu lu %llu fact %llu f1 %llu f2 %llu exit %llu spec %d\n",
+               t_enter, t_loaded, t_lu, t_fact, t_mid, t_f2, t_exit, (int)spec);
+    }
+#endif
 }
 
 __global__ void inv_table_kernel(uint16_t* t, u32 p, Fp f) {
@@ -556,6 +643,8 @@ void panel_window(const PanelArgs& a, cudaStream_t s) {
                                            (int)(sizeof(u32) * PB * WT)));
         attr = true;
     }
+    RL_ONCE_MAX_SMEM(panel_window_kernel<true>);
+    RL_ONCE_MAX_SMEM(panel_window_kernel<false>);
     if (sp) panel_window_kernel<true><<<1, NW * 32, smem, s>>>(a);
     else panel_window_kernel<false><<<1, NW * 32, smem, s>>>(a);
     RL_CUDA_CHECK(cudaGetLastError());

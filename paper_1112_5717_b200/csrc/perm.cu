@@ -114,6 +114,7 @@ __global__ void gen_kernel(u32* A, i64 lda, i64 m, i64 n, u64 seed, Fp f) {
 void apply_swaps(const SwapArgs& a, cudaStream_t s) {
     if (a.Mmax <= 0) return;
     const int grid = std::max(1, std::min((a.Mmax + 255) / 256, 2 * num_sms()));
+    RL_ONCE_MAX_SMEM(swaps_kernel);
     swaps_kernel<<<grid, 256, 0, s>>>(a);
     RL_CUDA_CHECK(cudaGetLastError());
 }
@@ -121,6 +122,7 @@ void apply_swaps(const SwapArgs& a, cudaStream_t s) {
 void compact_u_rows(u32* A, i64 lda, i32 m, i32 n, const i32* rp, const i32* rrp,
                     cudaStream_t s) {
     if (m <= 0 || n <= 0) return;
+    RL_ONCE_MAX_SMEM(compact_kernel);
     compact_kernel<<<(n + 255) / 256, 256, 0, s>>>(A, lda, m, n, rp, rrp);
     RL_CUDA_CHECK(cudaGetLastError());
 }

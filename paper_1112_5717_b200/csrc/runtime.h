@@ -22,6 +22,23 @@ struct CudaError : Error {
 
 int num_sms();
 
+// Every kernel of the CUP path prefers the maximum shared-memory carveout, so
+// consecutive launches (1 KB ... 200 KB of shared memory) never make an SM
+// reconfigure its L1/shared split between kernels.  Once per kernel.
+template <class F>
+inline void prefer_max_smem(F* kernel) {
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(kernel),
+                         cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+}
+#define RL_ONCE_MAX_SMEM(kernel)          \
+    do {                                  \
+        static bool once_ = false;        \
+        if (!once_) {                     \
+            prefer_max_smem(kernel);      \
+            once_ = true;                 \
+        }                                 \
+    } while (0)
+
 // Growable device scratch buffer (workspaces of the host-pointer entry points
 // and of the dense/triangular helpers; callers hold the C-ABI mutex).
 struct DevBuf {
