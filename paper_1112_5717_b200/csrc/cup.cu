@@ -52,7 +52,8 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
     const size_t o_ps = o_ipiv + up(sizeof(i32) * (k + 1));
     const size_t o_uinv = o_ps + up(sizeof(PanelScratch));
     const size_t o_tab = o_uinv + up(sizeof(u32) * PB * PB * (leaf_of_.size() + 1));
-    const size_t total = o_tab + (p_ <= 65536u ? 65536 * sizeof(uint16_t) : 0);
+    const size_t o_ninv = o_tab + up(p_ <= 65536u ? 65536 * sizeof(uint16_t) : 0);
+    const size_t total = o_ninv + sizeof(u32) * NINV_LD * NINV_LD * ninv_slot_.size();
     RL_CUDA_CHECK(cudaMalloc(&meta_, total));
     char* base = static_cast<char*>(meta_);
     rp_ = reinterpret_cast<i32*>(base + o_rp);
@@ -61,6 +62,7 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
     ps_ = reinterpret_cast<PanelScratch*>(base + o_ps);
     RL_CUDA_CHECK(cudaMemset(ps_, 0, sizeof(PanelScratch)));
     uinv_ = reinterpret_cast<u32*>(base + o_uinv);
+    ninv_ = ninv_slot_.empty() ? nullptr : reinterpret_cast<u32*>(base + o_ninv);
     if (p_ <= 65536u) {
         inv_table_ = reinterpret_cast<uint16_t*>(base + o_tab);
         build_inv_table(inv_table_, p_, nullptr);
@@ -195,9 +197,53 @@ static void collect_leaves(i32 x0, i32 mx, std::vector<std::pair<i32, i32>>& out
     collect_leaves(x0 + mx / 2, mx - mx / 2, out);
 }
 
+// G <- G * U_X^{-1} as one GEMM against the stored node inverse (in place: the
+// pack kernel snapshots G before the GEMM overwrites it, beta = 0).
+void CupEngine::gemm_ninv(i32 r0, i32 M, i32 x0, i32 mx, const u32* ninv) {
+    GemmArgs g{};
+    g.A = A_;
+    g.lda = lda_;
+    g.a_row0 = r0;
+    g.B = ninv;
+    g.ldb = NINV_LD;
+    g.gather = nullptr;
+    g.b_from0 = 1;
+    g.C = A_;
+    g.ldc = lda_;
+    g.c_row0 = r0;
+    g.M = M;
+    g.k_lo = dyn_rp(x0);
+    g.k_hi = dyn_rp(x0 + mx);
+    g.n_lo = dyn_rp(x0);
+    g.n_hi = dyn_rp(x0 + mx);
+    g.rp = rp_;
+    g.alpha = 1 % p_;
+    g.beta = 0;
+    g.f = f_;
+    ++stats_.gemms;
+    ++stats_.tc_gemms;
+    stats_.launches += 3;
+    gemm_tc(g, L_, mx, mx, a2_, b2_, s_);
+}
+
 void CupEngine::trsm_right(i32 r0, i32 M, i32 x0, i32 mx) {
     if (fused_trsm_ && mx <= TN_MAXLEAF * PB) {  // <= 4 leaves: one fused kernel
-        if (dry_) return;
+        const auto key = std::make_pair(x0, mx);
+        const bool gemm_ok = use_tc_ && M >= kNinvGemmMinRows && mx >= 2 * PB;
+        if (dry_) {
+            if (!ninv_slot_.count(key)) ninv_slot_.emplace(key, (i32)ninv_slot_.size());
+            if (gemm_ok) {
+                a2_cap_ = std::max(a2_cap_, tc_a2_bytes(L_, M, mx));
+                b2_cap_ = std::max(b2_cap_, tc_b2_bytes(L_, mx, mx));
+            }
+            return;
+        }
+        u32* ninv = ninv_ + (size_t)ninv_slot_.at(key) * NINV_LD * NINV_LD;
+        const bool have = ninv_done_.count(key) != 0;
+        if (have && gemm_ok) {
+            gemm_ninv(r0, M, x0, mx, ninv);
+            return;
+        }
         std::vector<std::pair<i32, i32>> lv;
         collect_leaves(x0, mx, lv);
         TrsmNodeArgs a{};
@@ -214,6 +260,8 @@ void CupEngine::trsm_right(i32 r0, i32 M, i32 x0, i32 mx) {
         a.rp = rp_;
         a.rrp = rrp_;
         a.f = f_;
+        a.ninv = have ? nullptr : ninv;  // first TRSM against X also leaves U_X^{-1}
+        ninv_done_.insert(key);
         trsm_node(a, s_);
         stats_.trsm_leaves++;
         stats_.launches += 1;
@@ -261,6 +309,7 @@ void CupEngine::enqueue(u32* dA, cudaStream_t s) {
     A_ = dA;
     s_ = s;
     stats_ = Stats{};
+    ninv_done_.clear();
     fill_rp0(rp_, s);
     if (m_ > 0 && n_ > 0) {
         node(0, m_);

@@ -2,7 +2,10 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <map>
+#include <set>
 #include <unordered_map>
+#include <utility>
 
 #include "common.cuh"
 
@@ -41,6 +44,7 @@ private:
     void node(i32 i0, i32 m);
     void panel(i32 i0, i32 b);
     void trsm_right(i32 r0, i32 M, i32 x0, i32 mx);
+    void gemm_ninv(i32 r0, i32 M, i32 x0, i32 mx, const u32* ninv);
     void gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nmax);
     void swaps_range(i32 row0, i32 M, Dyn j_lo, Dyn j_hi);
     void swaps_gather(Dyn g_lo, Dyn g_hi, i32 Mmax, Dyn j_lo, Dyn j_hi);
@@ -63,6 +67,13 @@ private:
     u32* uinv_ = nullptr;                      // one PB x PB block per leaf
     uint16_t* inv_table_ = nullptr;            // p < 2^16: x -> x^{-1} mod p
     std::unordered_map<i32, i32> leaf_of_;     // leaf start row -> leaf index
+    // node inverses U_X^{-1} of <= 4-leaf skeleton nodes X = (x0, mx): computed by
+    // the first TRSM against X (as a by-product of its sweep), then reused by the
+    // taller TRSMs above as one tensor-core GEMM each
+    std::map<std::pair<i32, i32>, i32> ninv_slot_;
+    std::set<std::pair<i32, i32>> ninv_done_;  // during one enqueue
+    u32* ninv_ = nullptr;
+    static constexpr i32 kNinvGemmMinRows = 512;  // taller G: tensor-core GEMM
     uint8_t* a2_ = nullptr;
     uint8_t* b2_ = nullptr;
     size_t a2_cap_ = 0, b2_cap_ = 0;

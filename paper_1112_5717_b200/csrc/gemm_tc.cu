@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(256) pack_b_kernel(GemmArgs g, uint8_t* __rest
         if (threadIdx.x < KQ) {
             const i32 k = kb * BK + kq * KQ + threadIdx.x;
             s_rowoff[threadIdx.x] =
-                k < K ? (g.gather ? __ldg(g.gather + k_lo + k) : k_lo + k) : -1;
+                k < K ? (g.gather ? __ldg(g.gather + k_lo + k) : (g.b_from0 ? k : k_lo + k)) : -1;
         }
         __syncthreads();
 #pragma unroll 4
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(256) pack_b_kernel(GemmArgs g, uint8_t* __rest
             const int kk = e / NT, nn = e % NT;
             const i32 row = s_rowoff[kk], n = nb * NT + nn;
             const bool ok = row >= 0 && n < N;
-            cp_async4(&T[kk][nn], ok ? g.B + (i64)row * g.ldb + n_lo + n : g.B, ok);
+            cp_async4(&T[kk][nn], ok ? g.B + (i64)row * g.ldb + (g.b_from0 ? 0 : n_lo) + n : g.B, ok);
         }
         cp_async_wait_all();
         __syncthreads();
@@ -504,8 +504,8 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
                 const int kk = e / 64, nn = e % 64;
                 const i32 k = k0 + kk, n = nb * 64 + nn;
                 const bool ok = k < K && n < N;
-                const i32 row = ok ? (g.gather ? __ldg(g.gather + k_lo + k) : k_lo + k) : 0;
-                cp_async4(&Bs[kk][nn], ok ? g.B + (i64)row * g.ldb + n_lo + n : g.B, ok);
+                const i32 row = ok ? (g.gather ? __ldg(g.gather + k_lo + k) : (g.b_from0 ? k : k_lo + k)) : 0;
+                cp_async4(&Bs[kk][nn], ok ? g.B + (i64)row * g.ldb + (g.b_from0 ? 0 : n_lo) + n : g.B, ok);
             }
             cp_async_wait_all();
             __syncthreads();

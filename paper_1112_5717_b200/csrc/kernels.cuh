@@ -31,6 +31,7 @@ struct GemmArgs {
     const i32* rp;
     u32 alpha, beta;
     Fp f;
+    int b_from0;   // B(k, n) = B[k * ldb + n]: a dense K x N operand (no k_lo/n_lo offsets)
 };
 
 // Number of 8-bit limbs for canonical elements of GF(p).
@@ -126,7 +127,9 @@ struct TrsmNodeArgs {
     const i32* rp;
     const i32* rrp;
     Fp f;
+    u32* ninv;     // optional: also solve I * U_X^{-1} into ninv (NINV_LD x NINV_LD)
 };
+constexpr int NINV_LD = TN_MAXLEAF * PB;   // 256: pitch of a node inverse
 void trsm_node(const TrsmNodeArgs& a, cudaStream_t s);
 
 // ---------------------------------------------------------------- permutation

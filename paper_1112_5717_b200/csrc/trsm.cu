@@ -71,6 +71,10 @@ __global__ void __launch_bounds__(256 * KS) trsm_node_kernel(TrsmNodeArgs a) {
     const i32 J0 = lo[0];
     const i32 nJ = hi[nl_ - 1] - J0;
     if (nJ <= 0 || a.M <= 0) return;
+    RL_STAMP(t_enter);
+#ifdef RL_TRACE
+    unsigned long long t_leaf[TN_MAXLEAF + 1] = {0, 0, 0, 0, 0};
+#endif
     // ---- stage all operand blocks once (one wait)
     for (int e = tid; e < (nl_ - 1) * PB; e += blockDim.x) {
         const int l = e / PB, t = e % PB;
@@ -106,6 +110,9 @@ __global__ void __launch_bounds__(256 * KS) trsm_node_kernel(TrsmNodeArgs a) {
         }
     }
     const bool gal = al && (J0 & 3) == 0;
+    // rows [M, M + nJ) are virtual: B = I over the node's pivots, so the sweep
+    // also yields the node inverse U_X^{-1} (written to a.ninv)
+    const i32 Mtot = a.M + (a.ninv ? nJ : 0);
     // partial sums of the other k-groups into group 0's accumulators
     auto gather = [&](u64 (&S)[TR][4]) {
         if (KS == 1) return;
@@ -126,9 +133,19 @@ __global__ void __launch_bounds__(256 * KS) trsm_node_kernel(TrsmNodeArgs a) {
                     for (int y = 0; y < 4; ++y) S[t][y] += Pt[((q - 1) * TM + rg + 16 * t) * PB + 4 * cg + y];
         }
     };
-    for (i32 r0 = blockIdx.x * TM; r0 < a.M; r0 += gridDim.x * TM) {
+    for (i32 r0 = blockIdx.x * TM; r0 < Mtot; r0 += gridDim.x * TM) {
         __syncthreads();
-        if (gal) {
+        if (r0 + TM > a.M && a.ninv) {  // tile touches the virtual identity rows
+            for (int e = tid; e < TM * (TN_MAXLEAF * PB); e += blockDim.x) {
+                const int rr = e / (TN_MAXLEAF * PB), j = e % (TN_MAXLEAF * PB);
+                const i32 r = r0 + rr;
+                if (r < a.M) {
+                    if (j < nJ) Gs[rr * GW + j] = a.A[(i64)(a.row0 + r) * a.lda + J0 + j];
+                } else {
+                    Gs[rr * GW + j] = (j == r - a.M) ? 1u % f.p : 0u;
+                }
+            }
+        } else if (gal) {
             for (int e = tid; e < TM * (TN_MAXLEAF * PB / 4); e += blockDim.x) {
                 const int rr = e / (TN_MAXLEAF * PB / 4), j = (e % (TN_MAXLEAF * PB / 4)) * 4;
                 const int bytes = r0 + rr < a.M ? 4 * max(0, min(4, nJ - j)) : 0;
@@ -144,6 +161,9 @@ __global__ void __launch_bounds__(256 * KS) trsm_node_kernel(TrsmNodeArgs a) {
         }
         cp_async_wait_all();
         __syncthreads();
+#ifdef RL_TRACE
+        t_leaf[0] = rl_now();
+#endif
         for (int l = 0; l < nl_; ++l) {
             const int nl = hi[l] - lo[l];
             if (nl <= 0) continue;
@@ -205,8 +225,18 @@ __global__ void __launch_bounds__(256 * KS) trsm_node_kernel(TrsmNodeArgs a) {
                     }
             }
             __syncthreads();
+#ifdef RL_TRACE
+            t_leaf[l + 1] = rl_now();
+#endif
         }
-        if (gal) {
+        if (r0 + TM > a.M && a.ninv) {
+            for (int e = tid; e < TM * nJ; e += blockDim.x) {
+                const int rr = e / nJ, j = e % nJ;
+                const i32 r = r0 + rr;
+                if (r < a.M) a.A[(i64)(a.row0 + r) * a.lda + J0 + j] = Gs[rr * GW + j];
+                else if (r < Mtot) a.ninv[(i64)(r - a.M) * NINV_LD + j] = Gs[rr * GW + j];
+            }
+        } else if (gal) {
             for (int e = tid; e < TM * (TN_MAXLEAF * PB / 4); e += blockDim.x) {
                 const int rr = e / (TN_MAXLEAF * PB / 4), j = (e % (TN_MAXLEAF * PB / 4)) * 4;
                 if (r0 + rr >= a.M || j >= nJ) continue;
@@ -227,6 +257,13 @@ __global__ void __launch_bounds__(256 * KS) trsm_node_kernel(TrsmNodeArgs a) {
             }
         }
     }
+#ifdef RL_TRACE
+    if (a.M == 256 && nl_ == 4 && a.row0 == 8448 && threadIdx.x == 0 && blockIdx.x < 2) {
+        RL_STAMP(t_exit);
+        printf("TRACE trsm cta %d enter %llu staged %llu l0 %llu l1 %llu l2 %llu l3 %llu exit %llu\n", blockIdx.x,
+               t_enter, t_leaf[0], t_leaf[1], t_leaf[2], t_leaf[3], t_leaf[4], t_exit);
+    }
+#endif
 }
 
 template <bool SP, int TR, int KS>
@@ -245,7 +282,8 @@ void launch_node(const TrsmNodeArgs& a, cudaStream_t s) {
     // one staging of the U blocks per CTA: about one CTA per SM, each looping
     // over its row tiles
     const int per_sm = nblk >= 6 ? 1 : (nblk >= 3 ? 2 : 4);
-    const int grid = std::max(1, std::min((a.M + TM - 1) / TM, per_sm * num_sms()));
+    const int rows = a.M + (a.ninv ? NINV_LD : 0);  // host bound; the kernel uses the live nJ
+    const int grid = std::max(1, std::min((rows + TM - 1) / TM, per_sm * num_sms()));
     trsm_node_kernel<SP, TR, KS><<<grid, 256 * KS, smem, s>>>(a);
     RL_CUDA_CHECK(cudaGetLastError());
 }

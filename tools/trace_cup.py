@@ -33,7 +33,7 @@ out = out.split("=== timed rep", 1)[-1]
 lines = [l for l in out.splitlines() if l.startswith("TRACE")]
 t0 = None
 for l in lines:
-    if l.startswith("TRACE window"):
+    if l.startswith("TRACE window") or l.startswith("TRACE trsm"):
         t0 = int(re.search(r"enter (\d+)", l).group(1))
         break
 if t0 is None:
@@ -42,7 +42,7 @@ if t0 is None:
 rel = lambda m: f"{(int(m.group(0)) - t0) / 1e3:8.2f}"
 tails = []
 for l in lines:
-    if l.startswith("TRACE window") or l.startswith("TRACE spec"):
+    if l.startswith("TRACE window") or l.startswith("TRACE spec") or l.startswith("TRACE trsm"):
         print(re.sub(r"\b(\d{12,})\b", lambda m: rel(m), l))
     else:
         tails.append([int(x) for x in re.findall(r"\b(\d{12,})\b", l)] + [l])
