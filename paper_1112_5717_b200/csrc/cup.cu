@@ -109,7 +109,9 @@ void CupEngine::gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nm
     g.alpha = p_ - 1;  // C <- C - A*B  (mm(..., neg_one, one), factor.cpp:51)
     g.beta = 1 % p_;
     g.f = f_;
-    const bool tc = use_tc_ && Kmax >= 64 && Nmax >= 64 && M >= 64;
+    // skinny K (one leaf): the SIMT kernel reads the operands directly and
+    // beats packing them for the tensor cores
+    const bool tc = use_tc_ && Kmax > PB && Nmax >= 64 && M >= 64;
     if (dry_) {
         if (tc) {
             a2_cap_ = std::max(a2_cap_, tc_a2_bytes(L_, M, Kmax));
@@ -120,7 +122,7 @@ void CupEngine::gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nm
     ++stats_.gemms;
     if (tc) {
         ++stats_.tc_gemms;
-        stats_.launches += 3;
+        stats_.launches += 2;
         gemm_tc(g, L_, Kmax, Nmax, a2_, b2_, s_);
     } else {
         stats_.launches += 1;
@@ -222,7 +224,7 @@ void CupEngine::gemm_ninv(i32 r0, i32 M, i32 x0, i32 mx, const u32* ninv) {
     g.f = f_;
     ++stats_.gemms;
     ++stats_.tc_gemms;
-    stats_.launches += 3;
+    stats_.launches += 2;
     gemm_tc(g, L_, mx, mx, a2_, b2_, s_);
 }
 

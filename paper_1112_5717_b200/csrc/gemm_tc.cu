@@ -76,15 +76,14 @@ __device__ __forceinline__ void dyn_shape(const GemmArgs& g, i32& K, i32& N, i32
 // ------------------------------------------------------------------ packing
 // A2 tile (mb, t = i*KB + kb): byte (r, kk) = limb_i(A(mb*128 + r, kb*128 + kk)).
 template <int L>
-__global__ void __launch_bounds__(256) pack_a_kernel(GemmArgs g, uint8_t* __restrict__ a2) {
+__device__ __forceinline__ void pack_a_body(const GemmArgs& g, uint8_t* __restrict__ a2, int bid, int nb) {
     i32 K, N, k_lo, n_lo;
     dyn_shape(g, K, N, k_lo, n_lo);
     if (K <= 0 || N <= 0) return;
     const i32 KB = (K + BK - 1) / BK;
     const i32 MB = (g.M + BM - 1) / BM;
     const i64 total = (i64)MB * KB * BM * 8;
-    for (i64 idx = (i64)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (i64)gridDim.x * blockDim.x) {
+    for (i64 idx = (i64)bid * blockDim.x + threadIdx.x; idx < total; idx += (i64)nb * blockDim.x) {
         const int c = (int)(idx & 7);
         const int r = (int)((idx >> 3) & 127);
         const i64 rest = idx >> 10;
@@ -121,8 +120,8 @@ __global__ void __launch_bounds__(256) pack_a_kernel(GemmArgs g, uint8_t* __rest
 
 // B2 tile (nb, t = i*KB + kb): row R = j*NT + nn, byte kk = limb_j(B(kb*128+kk, nb*NT+nn) * 2^(8i) mod p).
 template <int L>
-__global__ void __launch_bounds__(256) pack_b_kernel(GemmArgs g, uint8_t* __restrict__ b2,
-                                                     u32 s1, u32 s2, u32 s3) {
+__device__ __forceinline__ void pack_b_body(const GemmArgs& g, uint8_t* __restrict__ b2, u32 s1,
+                                            u32 s2, u32 s3, int bid, int nb) {
     // One CTA iteration handles 32 k-rows x NT columns of B (one quarter of a
     // 128-byte K-block): 2 of the 8 16-byte chunks of every tile row.
     constexpr int NT = Cfg<L>::NT;
@@ -137,7 +136,7 @@ __global__ void __launch_bounds__(256) pack_b_kernel(GemmArgs g, uint8_t* __rest
     const i32 NB = (N + NT - 1) / NT;
     const u32 sc[4] = {1u % g.f.p, s1, s2, s3};
     const i64 nblk = (i64)KB * 4 * NB;
-    for (i64 blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    for (i64 blk = bid; blk < nblk; blk += nb) {
         const i32 kq = (i32)(blk % 4);
         const i32 kb = (i32)((blk / 4) % KB);
         const i32 nb = (i32)(blk / (4 * KB));
@@ -186,6 +185,15 @@ __global__ void __launch_bounds__(256) pack_b_kernel(GemmArgs g, uint8_t* __rest
             }
         }
     }
+}
+
+// Both operands in one launch: blocks [0, ga) pack A, the rest pack B.
+template <int L>
+__global__ void __launch_bounds__(256) pack_kernel(GemmArgs g, uint8_t* __restrict__ a2,
+                                                   uint8_t* __restrict__ b2, u32 s1, u32 s2, u32 s3,
+                                                   int ga) {
+    if ((int)blockIdx.x < ga) pack_a_body<L>(g, a2, blockIdx.x, ga);
+    else pack_b_body<L>(g, b2, s1, s2, s3, blockIdx.x - ga, gridDim.x - ga);
 }
 
 constexpr int EPW = 16;                    // epilogue warps (4 per TMEM lane quadrant)
@@ -415,18 +423,12 @@ void launch_tc(const GemmArgs& g, i64 Kmax, i64 Nmax, uint8_t* a2, uint8_t* b2, 
     for (int i = 1; i < 4; ++i) sc[i] = (u32)(((u64)sc[i - 1] << 8) % g.f.p);
     const int grid = (int)std::max<i64>(1, std::min<i64>(MB * NB, nsm));
     if (phase != 1) {
-        {
-            i64 work = MB * KB * BM * 8;
-            int pg = (int)std::min<i64>((work + 255) / 256, (i64)nsm * 16);
-            RL_ONCE_MAX_SMEM(pack_a_kernel<L>);
-            pack_a_kernel<L><<<std::max(pg, 1), 256, 0, s>>>(g, a2);
-        }
-        {
-            i64 work = KB * 4 * NB;
-            int pg = (int)std::min<i64>(work, (i64)nsm * 8);
-            RL_ONCE_MAX_SMEM(pack_b_kernel<L>);
-            pack_b_kernel<L><<<std::max(pg, 1), 256, 0, s>>>(g, b2, sc[1], sc[2], sc[3]);
-        }
+        const i64 awork = MB * KB * BM * 8;
+        const int ga = (int)std::max<i64>(1, std::min<i64>((awork + 255) / 256, (i64)nsm * 8));
+        const int gb = (int)std::max<i64>(1, std::min<i64>(KB * 4 * NB, (i64)nsm * 8));
+        RL_ONCE_MAX_SMEM(pack_kernel<L>);
+        pack_kernel<L><<<ga + gb, 256, 0, s>>>(g, a2, b2, sc[1], sc[2], sc[3], ga);
+        RL_CUDA_CHECK(cudaGetLastError());
     }
     if (phase == 0) return;
     static bool attr_set = false;
@@ -475,14 +477,23 @@ void gemm_tc(const GemmArgs& g, int L, i64 Kmax, i64 Nmax, uint8_t* a2, uint8_t*
 namespace {
 template <bool SMALLP>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
-    __shared__ u32 As[64][33];
-    __shared__ u32 Bs[32][65];
+    // 64 x 64 output tile per CTA iteration, K in chunks of 64.  Thread (ty, tx)
+    // owns rows ty + 16a (a < 4) and columns 4tx..4tx+3: per k four broadcast
+    // loads of A and one 16-byte load of B feed 16 multiply-adds.  Operands
+    // move in 16-byte pieces whenever their rows are 16-byte aligned.
+    constexpr int SK = 64, SP_ = 68;
+    __shared__ __align__(16) u32 As[64][SP_];   // [row][k]
+    __shared__ __align__(16) u32 Bs[SK][SP_];   // [k][col]
+    __shared__ i32 s_brow[SK];
     i32 K, N, k_lo, n_lo;
     dyn_shape(g, K, N, k_lo, n_lo);
     if (K <= 0 || N <= 0 || g.M <= 0) return;
     const i32 MB = (g.M + 63) / 64, NB = (N + 63) / 64;
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const Fp f = g.f;
+    const i32 bcol0 = g.b_from0 ? 0 : n_lo;
+    const bool avec = ((g.lda & 3) == 0) && (((reinterpret_cast<uintptr_t>(g.A) >> 2) + g.a_row0 * g.lda + k_lo) % 4 == 0);
+    const bool bvec = ((g.ldb & 3) == 0) && (((reinterpret_cast<uintptr_t>(g.B) >> 2) + bcol0) % 4 == 0);
     for (i32 tile = blockIdx.x; tile < MB * NB; tile += gridDim.x) {
         const i32 mb = tile % MB, nb = tile / MB;
         u64 acc[4][4];
@@ -490,44 +501,70 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
         for (int a = 0; a < 4; ++a)
 #pragma unroll
             for (int b = 0; b < 4; ++b) acc[a][b] = 0;
-        for (i32 k0 = 0; k0 < K; k0 += 32) {
+        for (i32 k0 = 0; k0 < K; k0 += SK) {
             __syncthreads();
-#pragma unroll
-            for (int e = threadIdx.x; e < 64 * 32; e += 256) {
-                const int r = e / 32, kk = e % 32;
-                const i32 row = mb * 64 + r, k = k0 + kk;
-                const bool ok = row < g.M && k < K;
-                cp_async4(&As[r][kk], ok ? g.A + (i64)(g.a_row0 + row) * g.lda + k_lo + k : g.A, ok);
+            if (tid < SK) {
+                const i32 k = k0 + tid;
+                s_brow[tid] = k < K ? (g.gather ? __ldg(g.gather + k_lo + k) : (g.b_from0 ? k : k_lo + k)) : -1;
             }
-#pragma unroll
-            for (int e = threadIdx.x; e < 32 * 64; e += 256) {
-                const int kk = e / 64, nn = e % 64;
-                const i32 k = k0 + kk, n = nb * 64 + nn;
-                const bool ok = k < K && n < N;
-                const i32 row = ok ? (g.gather ? __ldg(g.gather + k_lo + k) : (g.b_from0 ? k : k_lo + k)) : 0;
-                cp_async4(&Bs[kk][nn], ok ? g.B + (i64)row * g.ldb + (g.b_from0 ? 0 : n_lo) + n : g.B, ok);
+            if (avec) {
+                for (int e = tid; e < 64 * SK / 4; e += 256) {
+                    const int r = e >> 4, kk = (e & 15) * 4;
+                    const i32 row = mb * 64 + r;
+                    const int bytes = row < g.M ? 4 * max(0, min(4, K - k0 - kk)) : 0;
+                    cp_async16z(&As[r][kk], bytes ? g.A + (i64)(g.a_row0 + row) * g.lda + k_lo + k0 + kk : g.A,
+                                bytes);
+                }
+            } else {
+                for (int e = tid; e < 64 * SK; e += 256) {
+                    const int r = e / SK, kk = e % SK;
+                    const i32 row = mb * 64 + r, k = k0 + kk;
+                    const bool ok = row < g.M && k < K;
+                    cp_async4(&As[r][kk], ok ? g.A + (i64)(g.a_row0 + row) * g.lda + k_lo + k : g.A, ok);
+                }
+            }
+            __syncthreads();  // s_brow
+            if (bvec) {
+                for (int e = tid; e < SK * 64 / 4; e += 256) {
+                    const int kk = e >> 4, nn = (e & 15) * 4;
+                    const i32 row = s_brow[kk], n = nb * 64 + nn;
+                    const int bytes = row >= 0 ? 4 * max(0, min(4, N - n)) : 0;
+                    cp_async16z(&Bs[kk][nn], bytes ? g.B + (i64)row * g.ldb + bcol0 + n : g.B, bytes);
+                }
+            } else {
+                for (int e = tid; e < SK * 64; e += 256) {
+                    const int kk = e / 64, nn = e % 64;
+                    const i32 row = s_brow[kk], n = nb * 64 + nn;
+                    const bool ok = row >= 0 && n < N;
+                    cp_async4(&Bs[kk][nn], ok ? g.B + (i64)row * g.ldb + bcol0 + n : g.B, ok);
+                }
             }
             cp_async_wait_all();
             __syncthreads();
-#pragma unroll 8
-            for (int kk = 0; kk < 32; ++kk) {
-                u32 av[4], bv[4];
+            const int kc = min(SK, K - k0);
+#pragma unroll 4
+            for (int kk = 0; kk < kc; ++kk) {
+                const uint4 bv = *reinterpret_cast<const uint4*>(&Bs[kk][4 * tx]);
 #pragma unroll
-                for (int a = 0; a < 4; ++a) av[a] = As[ty * 4 + a][kk];
-#pragma unroll
-                for (int b = 0; b < 4; ++b) bv[b] = Bs[kk][tx * 4 + b];
-#pragma unroll
-                for (int a = 0; a < 4; ++a)
-#pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        if (SMALLP) acc[a][b] += (u64)av[a] * bv[b];
-                        else acc[a][b] += mulmod(av[a], bv[b], f);
+                for (int a = 0; a < 4; ++a) {
+                    const u32 av = As[ty + 16 * a][kk];
+                    if (SMALLP) {
+                        acc[a][0] += (u64)av * bv.x;
+                        acc[a][1] += (u64)av * bv.y;
+                        acc[a][2] += (u64)av * bv.z;
+                        acc[a][3] += (u64)av * bv.w;
+                    } else {
+                        acc[a][0] += mulmod(av, bv.x, f);
+                        acc[a][1] += mulmod(av, bv.y, f);
+                        acc[a][2] += mulmod(av, bv.z, f);
+                        acc[a][3] += mulmod(av, bv.w, f);
                     }
+                }
             }
         }
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
-            const i32 row = mb * 64 + ty * 4 + a;
+            const i32 row = mb * 64 + ty + 16 * a;
             if (row >= g.M) continue;
             u32* crow = g.C + (i64)(g.c_row0 + row) * g.ldc + n_lo;
 #pragma unroll
@@ -550,7 +587,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
 void gemm_simt(const GemmArgs& g, i64 Kmax, i64 Nmax, cudaStream_t s) {
     if (g.M <= 0 || Kmax <= 0 || Nmax <= 0) return;
     const i64 tiles = ((g.M + 63) / 64) * ((Nmax + 63) / 64);
-    int grid = (int)std::min<i64>(tiles, (i64)num_sms() * 4);
+    int grid = (int)std::min<i64>(tiles, (i64)num_sms() * 8);
     RL_ONCE_MAX_SMEM(gemm_simt_kernel<true>);
     RL_ONCE_MAX_SMEM(gemm_simt_kernel<false>);
     if (g.f.p <= 65536u && Kmax <= (1ll << 31))
