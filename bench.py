@@ -24,9 +24,12 @@ W(m,n,r) = 2mnr - (m+n)r^2 + (2/3)r^3 (bench.cpp:12-13) at the returned rank.
 ``--impl reference`` times the reference's CPU cup on the host cores instead
 (T threads, each factoring its own 1024^2 random_matrix sample).
 
-Multi-GPU (torchrun, N>1): every rank factors its own replica of the workload
-("replicas only": a single C3 factorization is not sharded in this round);
-value = N * W / max-over-ranks time.
+Multi-GPU (torchrun, N>1): for the single-matrix workloads every rank factors
+its own replica ("replicas only": one C3 factorization is not sharded in this
+round), value = N * W / max-over-ranks time, scaling "weak".  ``--workload c4``
+shards the fixed batch of 4096 matrices across the ranks as contiguous slices
+(no collective on the data path), value = 4096 matrices / max-over-ranks time,
+scaling "strong".
 """
 from __future__ import annotations
 
@@ -54,6 +57,12 @@ WORKLOADS = {
                   desc="CUP of one 2048x2048 random_matrix(seed=3) over GF(65521)"),
     "c8192": dict(m=8192, n=8192, p=65521, seed=3,
                   desc="CUP of one 8192x8192 random_matrix(seed=3) over GF(65521)"),
+    "c2": dict(m=4096, n=8192, p=65521, seed=2, inner=2048,
+               desc="CUP of the config-2 4096x8192 rank-2048 matrix (L*R mod p, rows i=2 mod 3 "
+                    "zeroed, rows shuffled by SplitMix64(seed+2))"),
+    "c4": dict(m=256, n=256, p=8388593, seed=4, batch=4096,
+               desc="batched CUP of 4096 config-4 matrices 256x256 over GF(8388593), rank "
+                    "128..256 (L_t*R_t mod p); the batch is sharded across ranks"),
 }
 METRIC = "CUP mod-p ops/s (2n^3/3) at n=16384, % tensor peak; batched matrices/s"
 
@@ -119,31 +128,67 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------- reference arm
-def run_cpu_reference(n_threads: int, size: int, steps: int, warmup: int, p: int, seed: int):
-    """Each step: n_threads concurrent reference cup() calls on size^2 samples."""
+def _ref_worker_init():
+    import oracle  # noqa: F401  (loads oracle/_ref/libranklab_ref.so once per worker)
+
+
+def _ref_cup_square(job):
+    """One reference cup() of random_matrix(size, size, seed) over GF(p): (seconds, rank)."""
     import oracle as O
-    mats = [O.port_random_matrix(size, size, seed + 1000 * t, p) for t in range(n_threads)]
+    size, seed, p = job
+    a = O.port_random_matrix(size, size, seed, p)
+    t0 = time.perf_counter()
+    r = O.ref_cup(a, p)
+    return time.perf_counter() - t0, r.rank
 
-    def one(t, out):
-        a = mats[t].copy()
-        t0 = time.perf_counter()
-        r = O.ref_cup(a, p)
-        out[t] = (time.perf_counter() - t0, r.rank)
 
+def _ref_cup_c4(job):
+    """Reference cup() on config-4 matrices [lo, hi): seconds of factorization."""
+    import oracle as O
+    from paper_1112_5717_b200 import workloads as WL
+    from tests.helpers import matmul_mod
+    lo, hi, seed, p = job
+    ranks, ls, rs = WL.c4_recipe(hi, seed)
+    mats = [matmul_mod(O.port_random_matrix(256, ranks[t], ls[t], p),
+                       O.port_random_matrix(ranks[t], 256, rs[t], p), p) for t in range(lo, hi)]
+    t0 = time.perf_counter()
+    for a in mats:
+        O.ref_cup(a, p)
+    return time.perf_counter() - t0
+
+
+def _pool(n):
+    import multiprocessing as mp
+    from concurrent.futures import ProcessPoolExecutor
+    return ProcessPoolExecutor(n, mp_context=mp.get_context("fork"), initializer=_ref_worker_init)
+
+
+def run_cpu_reference(n_proc: int, size: int, steps: int, warmup: int, p: int, seed: int):
+    """Each step: n_proc concurrent reference cup() calls (one process per host
+    core; the reference is single-threaded) on size^2 samples.  Returns the
+    aggregate mod-p ops/s and the mean step time (the slowest worker)."""
     times, ops = [], 0.0
-    for it in range(warmup + steps):
-        out = [None] * n_threads
-        th = [threading.Thread(target=one, args=(t, out)) for t in range(n_threads)]
-        t0 = time.perf_counter()
-        for x in th:
-            x.start()
-        for x in th:
-            x.join()
-        dt = time.perf_counter() - t0
-        if it >= warmup:
-            times.append(dt)
-            ops += sum(model_ops(size, size, o[1]) for o in out)
+    with _pool(n_proc) as ex:
+        for it in range(warmup + steps):
+            out = list(ex.map(_ref_cup_square, [(size, seed + 1000 * t, p) for t in range(n_proc)]))
+            if it >= warmup:
+                times.append(max(o[0] for o in out))
+                ops += sum(model_ops(size, size, o[1]) for o in out)
     return ops / sum(times), sum(times) / len(times)
+
+
+def run_cpu_reference_c4(n_proc: int, per_proc: int, steps: int, warmup: int, p: int, seed: int):
+    """Each step: n_proc concurrent processes, each running the reference cup()
+    on its own `per_proc` config-4 matrices.  Returns matrices/s, s/step."""
+    times = []
+    with _pool(n_proc) as ex:
+        for it in range(warmup + steps):
+            jobs = [(t * per_proc, (t + 1) * per_proc, seed, p) for t in range(n_proc)]
+            out = list(ex.map(_ref_cup_c4, jobs))
+            if it >= warmup:
+                times.append(max(out))
+    step = sum(times) / len(times)
+    return n_proc * per_proc / step, step
 
 
 def reference_arm(args, rank, world):
@@ -158,21 +203,29 @@ def reference_arm(args, rank, world):
         print(json.dumps({"impl": "reference", "unavailable": str(e)}))
         return
     threads = os.cpu_count() or 1
-    size = 1024
-    val, step_s = run_cpu_reference(threads, size, args.steps, args.warmup, wl["p"], wl["seed"])
+    if args.workload == "c4":
+        per = 4
+        val, step_s = run_cpu_reference_c4(threads, per, args.steps, args.warmup, wl["p"], wl["seed"])
+        unit = "matrices/s"
+        sample = (f"{threads} concurrent processes x {per} reference cup() calls on config-4 "
+                  f"256x256 matrices over GF({wl['p']}) per step")
+        scaling = "strong"
+    else:
+        size = 1024
+        val, step_s = run_cpu_reference(threads, size, args.steps, args.warmup, wl["p"], wl["seed"])
+        unit = "mod-p ops/s"
+        sample = (f"{threads} concurrent processes, each one reference cup() of "
+                  f"random_matrix({size},{size}) per step (the reference is single-threaded)")
+        scaling = "weak"
     line = {
-        "impl": "reference", "metric": METRIC, "value": val, "unit": "mod-p ops/s",
+        "impl": "reference", "metric": METRIC, "value": val, "unit": unit,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "u32 (u64 products, % p)", "data": "synthetic",
-        "config": {"workload": args.workload, "p": wl["p"],
-                   "sample": f"{threads} threads x ranklab::cup of random_matrix({size},{size})"},
-        "cpu_baseline": {"value": val, "unit": "mod-p ops/s", "cores": threads,
-                         "kind": "reference",
-                         "sample": f"{threads} concurrent reference cup() of {size}x{size} "
-                                   f"(the reference is single-threaded per call)"},
-        "e2e": {"value": val, "unit": "mod-p ops/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
+        "config": {"workload": args.workload, "p": wl["p"], "sample": sample},
+        "cpu_baseline": {"value": val, "unit": unit, "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
 
@@ -226,8 +279,12 @@ def ours(args, rank, world, local_rank):
     m, n, p, seed = wl["m"], wl["n"], wl["p"], wl["seed"]
     L = limbs(p)
     stream = torch.cuda.current_stream()
-    pristine = torch.empty((m, n), dtype=torch.int32, device="cuda")
-    G.random_matrix_dev(pristine, m, n, seed, p, stream=stream)
+    if args.workload == "c2":
+        from paper_1112_5717_b200 import workloads as WL
+        pristine = WL.c2_dev(m, n, wl["inner"], seed, p)
+    else:
+        pristine = torch.empty((m, n), dtype=torch.int32, device="cuda")
+        G.random_matrix_dev(pristine, m, n, seed, p, stream=stream)
     work = torch.empty_like(pristine)
 
     # warm-up (also builds + captures the plan graph)
@@ -259,9 +316,12 @@ def ours(args, rank, world, local_rank):
 
     # results of the last factorization + structural verification
     work.copy_(pristine)
-    res = G.cup_dev(work, m, n, p, stream=stream)
+    ctr = G.OpCounter()
+    res = G.cup_dev(work, m, n, p, stream=stream, ctr=ctr)
     r = res.rank
-    W = model_ops(m, n, r)
+    # config 2's rank profile is not generic: the model over-counts it, so its
+    # algorithmic work is the reference's own counted arith_total
+    W = float(ctr.arith_total()) if args.workload == "c2" else model_ops(m, n, r)
     value = world * W * args.steps / t_max
     ms_per_step = t_max / args.steps * 1e3
 
@@ -278,7 +338,8 @@ def ours(args, rank, world, local_rank):
         "dtype": f"u32 in GF({p}); u8 limbs x{L} on int8 tensor cores (s32 acc, exact)",
         "data": "synthetic",
         "config": {"workload": args.workload, "desc": wl["desc"], "m": m, "n": n, "p": p,
-                   "seed": seed, "rank": r, "model_ops": W,
+                   "seed": seed, "rank": r, "model_ops": model_ops(m, n, r),
+                   "algorithmic_ops": W, "counted_arith_ops": int(ctr.arith_total()),
                    "parallelism": "replicas" if world > 1 else "single",
                    "l2": "input 1 GiB > 126 MB L2; input restored between steps",
                    "profile_identity": bool(np.array_equal(res.row_profile, np.arange(r))),
@@ -290,7 +351,7 @@ def ours(args, rank, world, local_rank):
     # dominant kernel roofline: root Schur GEMM shape, GEMM kernel alone
     try:
         peak = measure_int8_peak(torch)
-        gm = min(m // 2, 8192)
+        gm = 8192  # the C3 root Schur GEMM shape (same as the committed ncu capture)
         da = torch.empty((gm, gm), dtype=torch.int32, device="cuda")
         db = torch.empty((gm, gm), dtype=torch.int32, device="cuda")
         dc = torch.empty((gm, gm), dtype=torch.int32, device="cuda")
@@ -371,6 +432,120 @@ def ours(args, rank, world, local_rank):
         dist.destroy_process_group()
 
 
+def ours_batched(args, rank, world, local_rank):
+    """Config 4: the fixed batch sharded across ranks (contiguous slices)."""
+    import torch
+    import paper_1112_5717_b200 as G
+    from paper_1112_5717_b200 import workloads as WL
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    wl = WORKLOADS["c4"]
+    total, m, n, p, seed = wl["batch"], wl["m"], wl["n"], wl["p"], wl["seed"]
+    lo, hi = WL.shard_range(total, rank, world)
+    cnt = hi - lo
+    stream = torch.cuda.current_stream()
+    pristine, ranks = WL.c4_dev(total, seed, p, lo, hi)
+    work = torch.empty_like(pristine)
+    for _ in range(args.warmup):
+        work.copy_(pristine)
+        G.cup_batched_dev(work, cnt, m, n, p, stream=stream, want_meta=False)
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        for i in range(args.steps):
+            work.copy_(pristine)
+            starts[i].record(stream)
+            G.cup_batched_dev(work, cnt, m, n, p, stream=stream, want_meta=False)
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    elapsed = sum(s_.elapsed_time(e) for s_, e in zip(starts, ends)) / 1e3
+    t_local = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
+    # verification: every shard's ranks equal the recipe's r_t (rank = r w.h.p.)
+    work.copy_(pristine)
+    rk, _, _ = G.cup_batched_dev(work, cnt, m, n, p, stream=stream)
+    ok = torch.tensor([int(sum(int(a) == b for a, b in zip(rk, ranks)))], dtype=torch.float64,
+                      device="cuda")
+    ops = torch.tensor([sum(model_ops(m, n, int(x)) for x in rk)], dtype=torch.float64,
+                       device="cuda")
+    if dist is not None:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+        dist.all_reduce(ok, op=dist.ReduceOp.SUM)
+        dist.all_reduce(ops, op=dist.ReduceOp.SUM)
+    t_max = float(t_local.item())
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    value = total * args.steps / t_max
+    line = {
+        "metric": METRIC, "value": value, "unit": "matrices/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": f"u32 in GF({p}); u64 products, Barrett reduction", "data": "synthetic",
+        "config": {"workload": "c4", "desc": wl["desc"], "batch": total, "m": m, "n": n, "p": p,
+                   "seed": seed, "parallelism": f"batch sharded {world} ways" if world > 1 else "single",
+                   "ranks_match_recipe": int(ok.item()),
+                   "modp_ops_per_s": float(ops.item()) * args.steps / t_max,
+                   "l2": "256 MB batch > 126 MB L2; batch restored between steps"},
+        "gpu_launches": args.steps,
+        "clocks": clk.summary(),
+    }
+    # e2e: host buffers in, factor, bodies + ranks out (this rank's shard)
+    try:
+        host = torch.empty(pristine.shape, dtype=torch.int32, pin_memory=True)
+        host.copy_(pristine)
+        out = torch.empty_like(host, pin_memory=True)
+        tt = []
+        for i in range(3):
+            t0 = time.perf_counter()
+            work.copy_(host, non_blocking=True)
+            G.cup_batched_dev(work, cnt, m, n, p, stream=stream)   # reads ranks/profiles back
+            out.copy_(work, non_blocking=True)
+            torch.cuda.synchronize()
+            tt.append(time.perf_counter() - t0)
+        e2e_t = sum(tt[1:]) / len(tt[1:])
+        line["e2e"] = {"value": cnt * world / e2e_t, "unit": "matrices/s",
+                       "h2d_bytes_per_step": cnt * m * n * 4,
+                       "d2h_bytes_per_step": cnt * (m * n * 4 + 8 + 4 * min(m, n) + 4 * n),
+                       "ms_per_step": e2e_t * 1e3,
+                       "path": "pinned H2D + rl_cup_batched_u32_dev (ranks, profiles, sigma) + D2H"}
+    except Exception as e:  # pragma: no cover
+        line["e2e"] = {"error": str(e)}
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            import oracle as O
+            from tests.helpers import matmul_mod
+            ranks_h, ls, rs = WL.c4_recipe(8, seed)
+            t_sum = 0.0
+            for t in range(8):
+                a = matmul_mod(O.port_random_matrix(256, ranks_h[t], ls[t], p),
+                               O.port_random_matrix(ranks_h[t], 256, rs[t], p), p)
+                t0 = time.perf_counter()
+                (O.ref_cup if O.have_ref() else O.port_cup)(a, p)
+                t_sum += time.perf_counter() - t0
+            line["cpu_baseline"] = {"value": 8 / t_sum, "unit": "matrices/s", "cores": 1,
+                                    "kind": "reference" if O.have_ref() else "port",
+                                    "sample": "ranklab::cup of the first 8 config-4 matrices, "
+                                              f"single thread, {t_sum:.2f} s"}
+        except Exception as e:  # pragma: no cover
+            line["cpu_baseline"] = {"error": str(e)}
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -386,6 +561,8 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         reference_arm(args, rank, world)
+    elif args.workload == "c4":
+        ours_batched(args, rank, world, local_rank)
     else:
         ours(args, rank, world, local_rank)
 
