@@ -68,6 +68,14 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
         build_inv_table(inv_table_, p_, nullptr);
         RL_CUDA_CHECK(cudaDeviceSynchronize());
     }
+    // the critical path (s_, s3_) outranks the wide updates (s2_) at the CTA
+    // scheduler: a window CTA takes the first SM that frees up
+    int prio_lo = 0, prio_hi = 0;
+    RL_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    RL_CUDA_CHECK(cudaStreamCreateWithPriority(&s2_, cudaStreamNonBlocking, prio_lo));
+    RL_CUDA_CHECK(cudaStreamCreateWithPriority(&s3_, cudaStreamNonBlocking, prio_hi));
+    events_.resize(events_needed_ + 4);
+    for (auto& e : events_) RL_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     if (a2_cap_) RL_CUDA_CHECK(cudaMalloc(&a2_, a2_cap_));
     if (b2_cap_) RL_CUDA_CHECK(cudaMalloc(&b2_, b2_cap_));
 }
@@ -75,19 +83,31 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
 CupEngine::~CupEngine() {
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     cudaFree(meta_);
+    for (auto& e : events_) cudaEventDestroy(e);
+    if (s2_) cudaStreamDestroy(s2_);
+    if (s3_) cudaStreamDestroy(s3_);
     cudaFree(a2_);
     cudaFree(b2_);
 }
 
-void CupEngine::gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nmax) {
+cudaEvent_t CupEngine::fork_to(cudaStream_t from, cudaStream_t to) {
+    cudaEvent_t e = events_.at(next_event_++);
+    RL_CUDA_CHECK(cudaEventRecord(e, from));
+    RL_CUDA_CHECK(cudaStreamWaitEvent(to, e, 0));
+    return e;
+}
+
+void CupEngine::gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nmax, cudaStream_t st,
+                     i32 n_cap) {
+    if (!st) st = s_;
     // K = pivots of rows [x0, x1) = [rp[x0], rp[x1]); split along the skeleton
     // while the s32 exactness bound could be exceeded.
     const i64 Kmax = x1 - x0;
     if (Kmax <= 0 || M <= 0 || Nmax <= 0) return;
     if (Kmax > tc_kmax(L_)) {
         const i32 xm = x0 + (x1 - x0) / 2;
-        gemm(row0, M, x0, xm, n_lo, n_hi, Nmax);
-        gemm(row0, M, xm, x1, n_lo, n_hi, Nmax);
+        gemm(row0, M, x0, xm, n_lo, n_hi, Nmax, st, n_cap);
+        gemm(row0, M, xm, x1, n_lo, n_hi, Nmax, st, n_cap);
         return;
     }
     GemmArgs g{};
@@ -106,6 +126,9 @@ void CupEngine::gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nm
     g.n_lo = n_lo;
     g.n_hi = n_hi;
     g.rp = rp_;
+    g.n_cap = n_cap;
+    // on the side stream the persistent GEMM leaves one SM for the window kernel
+    g.max_ctas = (st == s2_) ? num_sms() - 1 : 0;
     g.alpha = p_ - 1;  // C <- C - A*B  (mm(..., neg_one, one), factor.cpp:51)
     g.beta = 1 % p_;
     g.f = f_;
@@ -123,16 +146,17 @@ void CupEngine::gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nm
     if (tc) {
         ++stats_.tc_gemms;
         stats_.launches += 2;
-        gemm_tc(g, L_, Kmax, Nmax, a2_, b2_, s_);
+        gemm_tc(g, L_, Kmax, Nmax, a2_, b2_, st);
     } else {
         stats_.launches += 1;
-        gemm_simt(g, Kmax, Nmax, s_);
+        gemm_simt(g, Kmax, Nmax, st);
     }
 }
 
 void CupEngine::panel(i32 i0, i32 b) {
     if (dry_) {
         leaf_of_.emplace(i0, (i32)leaf_of_.size());
+        events_needed_ += 2;
         return;
     }
     PanelArgs a{};
@@ -149,9 +173,14 @@ void CupEngine::panel(i32 i0, i32 b) {
     a.ps = ps_;
     a.f = f_;
     panel_window(a, s_);
+    fork_to(s_, s3_);                       // U^{-1} beside the tail
+    panel_uinv(a, s3_);
+    for (cudaEvent_t e : pending_joins_) RL_CUDA_CHECK(cudaStreamWaitEvent(s_, e, 0));
+    pending_joins_.clear();                 // the wide Schur update of these rows
     panel_tail(a, s_);
+    fork_to(s3_, s_);                       // trsm/next window need U^{-1} and ps
     stats_.panels++;
-    stats_.launches += 2;
+    stats_.launches += 3;
 }
 
 void CupEngine::swaps_range(i32 row0, i32 M, Dyn j_lo, Dyn j_hi) {
@@ -302,7 +331,24 @@ void CupEngine::node(i32 i0, i32 mm) {
     const i32 b0 = i0 + k, bm = mm - k;
     swaps_range(b0, bm, dyn_rp(i0), dyn_rp(b0));                     // factor.cpp:42
     trsm_right(b0, bm, i0, k);                                        // factor.cpp:45-46
-    gemm(b0, bm, i0, b0, dyn_rp(b0), dyn_c(n_), n_);                  // factor.cpp:51-52
+    // factor.cpp:51-52, split: the first window of the bottom half reads only
+    // columns [rp[b0], rp[b0] + PW), so that slice is updated first and the rest
+    // runs on s2_ beside that window (joined before its tail)
+    if (k > split_max_k_) {
+        gemm(b0, bm, i0, b0, dyn_rp(b0), dyn_c(n_), n_);
+    } else {
+        gemm(b0, bm, i0, b0, dyn_rp(b0), Dyn{b0, PW}, std::min<i64>(PW, n_), s_, n_);
+        if (dry_) {
+            events_needed_ += 2;
+            gemm(b0, bm, i0, b0, Dyn{b0, PW}, dyn_c(n_), n_, s2_);
+        } else {
+            fork_to(s_, s2_);
+            gemm(b0, bm, i0, b0, Dyn{b0, PW}, dyn_c(n_), n_, s2_);
+            cudaEvent_t e = events_.at(next_event_++);
+            RL_CUDA_CHECK(cudaEventRecord(e, s2_));
+            pending_joins_.push_back(e);
+        }
+    }
     node(b0, bm);                                                     // factor.cpp:53
     swaps_gather(dyn_rp(i0), dyn_rp(b0), k, dyn_rp(b0), dyn_rp(i0 + mm));  // factor.cpp:56
 }
@@ -312,9 +358,15 @@ void CupEngine::enqueue(u32* dA, cudaStream_t s) {
     s_ = s;
     stats_ = Stats{};
     ninv_done_.clear();
+    next_event_ = 0;
+    pending_joins_.clear();
     fill_rp0(rp_, s);
     if (m_ > 0 && n_ > 0) {
         node(0, m_);
+        for (cudaEvent_t e : pending_joins_) RL_CUDA_CHECK(cudaStreamWaitEvent(s_, e, 0));
+        pending_joins_.clear();
+        if (m_ > PB && split_max_k_ >= PB) fork_to(s2_, s_);  // s2_ joined the capture at a split
+        fork_to(s3_, s_);
         compact_u_rows(A_, lda_, m_, n_, rp_, rrp_, s);
         stats_.launches += 1;
     }
@@ -331,7 +383,9 @@ void CupEngine::run(u32* dA, cudaStream_t s, bool use_graph) {
             graph_exec_ = nullptr;
         }
         cudaStream_t cs;
-        RL_CUDA_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        int prio_lo = 0, prio_hi = 0;
+        RL_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        RL_CUDA_CHECK(cudaStreamCreateWithPriority(&cs, cudaStreamNonBlocking, prio_hi));
         cudaGraph_t graph;
         RL_CUDA_CHECK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
         try {

@@ -6,6 +6,7 @@
 #include <set>
 #include <unordered_map>
 #include <utility>
+#include <vector>
 
 #include "common.cuh"
 
@@ -45,7 +46,9 @@ private:
     void panel(i32 i0, i32 b);
     void trsm_right(i32 r0, i32 M, i32 x0, i32 mx);
     void gemm_ninv(i32 r0, i32 M, i32 x0, i32 mx, const u32* ninv);
-    void gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nmax);
+    void gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nmax, cudaStream_t st = nullptr,
+              i32 n_cap = 0);
+    cudaEvent_t fork_to(cudaStream_t from, cudaStream_t to);  // `to` waits for `from`'s work so far
     void swaps_range(i32 row0, i32 M, Dyn j_lo, Dyn j_hi);
     void swaps_gather(Dyn g_lo, Dyn g_hi, i32 Mmax, Dyn j_lo, Dyn j_hi);
 
@@ -59,6 +62,16 @@ private:
     bool fused_trsm_ = true;
     u32* A_ = nullptr;
     cudaStream_t s_ = nullptr;
+    // side streams of the captured DAG: s2_ runs the wide part of each Schur
+    // update while the next leaf's window kernel runs on s_; s3_ runs each
+    // leaf's U^{-1} beside its tail
+    cudaStream_t s2_ = nullptr, s3_ = nullptr;
+    std::vector<cudaEvent_t> events_;
+    size_t next_event_ = 0, events_needed_ = 0;
+    std::vector<cudaEvent_t> pending_joins_;   // joined before the next tail
+    // Schur updates with K <= this are split (window slice first, rest on s2_);
+    // above it the extra narrow GEMM costs more than the overlap wins
+    i32 split_max_k_ = 1024;
     void* meta_ = nullptr;                     // one allocation for everything below
     i32* rp_ = nullptr;
     i32* rrp_ = nullptr;

@@ -70,7 +70,8 @@ __device__ __forceinline__ void dyn_shape(const GemmArgs& g, i32& K, i32& N, i32
     k_lo = dyn_eval(g.k_lo, g.rp);
     K = dyn_eval(g.k_hi, g.rp) - k_lo;
     n_lo = dyn_eval(g.n_lo, g.rp);
-    N = dyn_eval(g.n_hi, g.rp) - n_lo;
+    const i32 nh = dyn_eval(g.n_hi, g.rp);
+    N = (g.n_cap > 0 && nh > g.n_cap ? g.n_cap : nh) - n_lo;
 }
 
 // ------------------------------------------------------------------ packing
@@ -421,7 +422,7 @@ void launch_tc(const GemmArgs& g, i64 Kmax, i64 Nmax, uint8_t* a2, uint8_t* b2, 
     const i64 NB = (Nmax + C_::NT - 1) / C_::NT;
     u32 sc[4] = {1, 0, 0, 0};
     for (int i = 1; i < 4; ++i) sc[i] = (u32)(((u64)sc[i - 1] << 8) % g.f.p);
-    const int grid = (int)std::max<i64>(1, std::min<i64>(MB * NB, nsm));
+    const int grid = (int)std::max<i64>(1, std::min<i64>(MB * NB, g.max_ctas > 0 ? g.max_ctas : nsm));
     if (phase != 1) {
         const i64 awork = MB * KB * BM * 8;
         const int ga = (int)std::max<i64>(1, std::min<i64>((awork + 255) / 256, (i64)nsm * 8));
@@ -587,7 +588,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
 void gemm_simt(const GemmArgs& g, i64 Kmax, i64 Nmax, cudaStream_t s) {
     if (g.M <= 0 || Kmax <= 0 || Nmax <= 0) return;
     const i64 tiles = ((g.M + 63) / 64) * ((Nmax + 63) / 64);
-    int grid = (int)std::min<i64>(tiles, (i64)num_sms() * 8);
+    int grid = (int)std::min<i64>(tiles, g.max_ctas > 0 ? (i64)g.max_ctas : (i64)num_sms() * 8);
     RL_ONCE_MAX_SMEM(gemm_simt_kernel<true>);
     RL_ONCE_MAX_SMEM(gemm_simt_kernel<false>);
     if (g.f.p <= 65536u && Kmax <= (1ll << 31))

@@ -32,6 +32,8 @@ struct GemmArgs {
     u32 alpha, beta;
     Fp f;
     int b_from0;   // B(k, n) = B[k * ldb + n]: a dense K x N operand (no k_lo/n_lo offsets)
+    i32 n_cap;     // > 0: the column range ends at min(n_hi, n_cap)
+    i32 max_ctas;  // > 0: grid bound (leave SMs free for a concurrent kernel)
 };
 
 // Number of 8-bit limbs for canonical elements of GF(p).
@@ -97,6 +99,10 @@ struct PanelArgs {
 void build_inv_table(uint16_t* table, u32 p, cudaStream_t s);
 void panel_window(const PanelArgs& a, cudaStream_t s);
 void panel_tail(const PanelArgs& a, cudaStream_t s);
+// The leaf's U^{-1} on its own (one CTA), for a stream parallel to the tail;
+// does nothing when the leaf has window-dead rows (the tail then computes it,
+// after a possible fallback).
+void panel_uinv(const PanelArgs& a, cudaStream_t s);
 
 // X <- X * U^{-1} for the unit upper block of one leaf's pivots J = [j_lo, j_hi)
 // (|J| <= PB): rows [row0, row0 + M) of A, columns J; U^{-1} precomputed by

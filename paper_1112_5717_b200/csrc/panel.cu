@@ -203,7 +203,9 @@ __global__ void __launch_bounds__(256) panel_tail_kernel(PanelArgs a) {
     const i32 c0 = ps->c0, W = ps->W, b = ps->b, rt = ps->r;
     u32 bad = 0;
     if (blockIdx.x == gridDim.x - 1) {
-        if (W > 0 && rt > 0) {
+        // U^{-1} here only for leaves with window-dead rows (otherwise the
+        // parallel panel_uinv kernel computes it)
+        if (W > 0 && rt > 0 && ps->dead_mask != 0) {
             leaf_uinv<SP>(a, c0, rt, Mi, Xs, Ts);
         }
     } else if (W > 0) {
@@ -351,7 +353,33 @@ __global__ void __launch_bounds__(256) trsm_leaf_kernel(TrsmLeafArgs a) {
     }
 }
 
+template <bool SP>
+__global__ void __launch_bounds__(256) panel_uinv_kernel(PanelArgs a) {
+    extern __shared__ __align__(16) u32 tsm[];
+    const PanelScratch* ps = a.ps;
+    const i32 c0 = ps->c0, W = ps->W, rt = ps->r;
+    if (W <= 0 || rt <= 0 || ps->dead_mask != 0) return;
+    leaf_uinv<SP>(a, c0, rt, reinterpret_cast<u32 (*)[PB + 1]>(tsm),
+                  reinterpret_cast<u32 (*)[PB + 1]>(tsm + PB * (PB + 1)),
+                  reinterpret_cast<u32 (*)[PB + 1]>(tsm + 2 * PB * (PB + 1)));
+}
+
 }  // namespace
+
+void panel_uinv(const PanelArgs& a, cudaStream_t s) {
+    const size_t smem = sizeof(u32) * 3 * PB * (PB + 1);
+    static bool attr = false;
+    if (!attr) {
+        RL_CUDA_CHECK(cudaFuncSetAttribute(panel_uinv_kernel<true>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        RL_CUDA_CHECK(cudaFuncSetAttribute(panel_uinv_kernel<false>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    if (a.f.p <= 65536u) panel_uinv_kernel<true><<<1, 256, smem, s>>>(a);
+    else panel_uinv_kernel<false><<<1, 256, smem, s>>>(a);
+    RL_CUDA_CHECK(cudaGetLastError());
+}
 
 void panel_tail(const PanelArgs& a, cudaStream_t s) {
     // tiles: Minv + P tile; the U^{-1} CTA: U, X, T (3 blocks of PB x (PB+1))

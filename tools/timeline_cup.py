@@ -54,3 +54,14 @@ for (a, b), g in sorted(gaps.items(), key=lambda x: -x[1])[:10]:
     print(f"  {g/1e3:8.2f} ms  {a[:40]} -> {b[:40]}")
 if out:
     json.dump([(s - t0, e - t0, nm) for s, e, nm in ks], open(out, "w"))
+# overlap of each panel_window with other kernels (concurrency achieved)
+wins = [k for k in ks if "panel_window" in k[2]]
+ov = 0.0
+for s0, e0, _ in wins:
+    for s1, e1, nm in ks:
+        if "panel_window" in nm:
+            continue
+        o = min(e0, e1) - max(s0, s1)
+        if o > 0:
+            ov += o
+print(f"window time overlapped by other kernels: {ov/1e3:.2f} ms of {sum(e-s for s,e,_ in wins)/1e3:.2f} ms")
