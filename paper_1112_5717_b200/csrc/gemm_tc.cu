@@ -197,6 +197,19 @@ __global__ void __launch_bounds__(256) pack_kernel(GemmArgs g, uint8_t* __restri
     else pack_b_body<L>(g, b2, s1, s2, s3, blockIdx.x - ga, gridDim.x - ga);
 }
 
+// Tile order of the persistent GEMM: bands of BAND M-tiles, M fastest within a
+// band, then N.  The ~#SM concurrent tiles cover a BAND x (#SM/BAND) rectangle,
+// the band's A panels stay L2-resident while the N panels stream past once per
+// band (instead of every A panel being re-streamed by every wave).
+constexpr int BAND = 16;
+__device__ __forceinline__ void tile_coords(i32 tile, i32 MB, i32 NB, i32& mb, i32& nb) {
+    const i32 band = MB < BAND ? MB : BAND;
+    const i32 b = tile / (band * NB), r = tile - b * band * NB;
+    const i32 rows = min(band, MB - b * band);
+    mb = b * band + r % rows;
+    nb = r / rows;
+}
+
 constexpr int EPW = 16;                    // epilogue warps (4 per TMEM lane quadrant)
 constexpr int NTHR = 64 + 32 * EPW;        // producer warp + MMA warp + epilogue
 
@@ -250,7 +263,8 @@ __global__ void __launch_bounds__(NTHR, 1)
             int s = 0;
             uint32_t ph = 0;
             for (i32 tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-                const i32 mb = tile % MB, nb = tile / MB;
+                i32 mb, nb;
+                tile_coords(tile, MB, NB, mb, nb);
                 const uint8_t* asrc = a2 + (i64)mb * KT * A_TILE;
                 const uint8_t* bsrc = b2 + (i64)nb * KT * C_::B_TILE;
                 for (i32 kt = 0; kt < KT; ++kt) {
@@ -315,7 +329,8 @@ __global__ void __launch_bounds__(NTHR, 1)
         constexpr int NCHP = NT / C_::CH / (EPW / 4);  // chunks per warp slice
         constexpr int PF = NCHP < 2 ? NCHP : 2;       // chunks prefetched ahead
         for (i32 tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-            const i32 mb = tile % MB, nb = tile / MB;
+            i32 mb, nb;
+            tile_coords(tile, MB, NB, mb, nb);
             const i32 row = mb * BM + rloc;
             const bool vrow = row < g.M;
             u32* crow = g.C + (i64)(g.c_row0 + (vrow ? row : 0)) * g.ldc + n_lo + nb * NT;
