@@ -88,14 +88,211 @@ __global__ void __launch_bounds__(256) cup_batched_kernel(u32* A, i64 stride, i3
     }
 }
 
+// ---------------------------------------------------------------------------
+// Blocked variant for n <= 256 (config 4): rows are taken in panels of PR = 32.
+// A panel is factored in shared memory row by row with the same pivot rule
+// (first nonzero at position >= r, transposition r <-> c applied to every row
+// that is not final, raw pivot, normalised U row), its rows kept as lazy 64-bit
+// sums that are reduced only when a row becomes the pivot candidate.  Every
+// trailing row is then updated once per panel by one warp (eager elimination
+// by the panel's pivots in order, lazy sums in registers, each multiplier
+// reduced exactly when it is read) instead of once per pivot through memory.
+// Lazy sums hold < 2^52 for p < 2^24 (at most 32 products < 2^46 per panel);
+// larger p reduce every product.
+constexpr int PR = 32;
+constexpr int BN = 256;
+
+template <bool LAZY>
+__device__ __forceinline__ u64 lazy_fma(u64 acc, u32 nf, u32 u, const Fp& f) {
+    if (LAZY) return acc + (u64)nf * u;
+    return addmod((u32)acc, mulmod(nf, u, f), f);
+}
+
+template <bool LAZY>
+__global__ void __launch_bounds__(256) cup_batched_blk_kernel(u32* A, i64 stride, i32 m, i32 n, Fp f,
+                                                              i32* ranks, i32* rrp_out, i32* ipiv_out,
+                                                              i32 kcap) {
+    extern __shared__ __align__(16) u64 P[];             // [PR][BN] panel rows, lazy sums
+    u32* wbuf = reinterpret_cast<u32*>(P + PR * BN);     // [8][BN] per-warp row buffer
+    __shared__ i32 s_rrp[BN], s_ipiv[BN], s_prow[PR];
+    __shared__ u32 s_f[PR];
+    __shared__ int s_wmin[8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    u32* a = A + (i64)blockIdx.x * stride;
+    const int nq = (n + 31) / 32;
+    int r = 0;
+    for (int i0 = 0; i0 < m && r < n; i0 += PR) {
+        const int pr = min(PR, m - i0);
+        const int r0 = r;
+        for (int e = tid; e < pr * n; e += 256) P[(e / n) * BN + e % n] = a[(i64)(i0 + e / n) * n + e % n];
+        __syncthreads();
+        // ---- panel: rows in order
+        for (int k = 0; k < pr && r < n; ++k) {
+            const int c = tid;
+            u32 v = 0;
+            if (c < n && c >= r) {
+                v = LAZY ? red64(P[k * BN + c], f) : (u32)P[k * BN + c];
+                P[k * BN + c] = v;
+            }
+            const unsigned msk = __ballot_sync(0xffffffffu, c < n && c >= r && v != 0);
+            if (lane == 0) s_wmin[warp] = msk ? warp * 32 + __ffs(msk) - 1 : BN;
+            __syncthreads();
+            int pc = s_wmin[0];
+#pragma unroll
+            for (int w = 1; w < 8; ++w) pc = min(pc, s_wmin[w]);
+            if (pc >= n) {  // no pivot: row k is zero at positions >= r
+                __syncthreads();
+                continue;
+            }
+            if (pc != r) {  // transposition r <-> pc on the panel rows and earlier U rows
+                for (int t = tid; t < pr; t += 256) {
+                    const u64 x = P[t * BN + r];
+                    P[t * BN + r] = P[t * BN + pc];
+                    P[t * BN + pc] = x;
+                }
+                for (int j = tid; j < r0; j += 256) {
+                    u32* row = a + (i64)s_rrp[j] * n;
+                    const u32 x = row[r];
+                    row[r] = row[pc];
+                    row[pc] = x;
+                }
+                __syncthreads();
+            }
+            const u32 pv = (u32)P[k * BN + r];
+            const u32 pinv = invmod(pv, f);
+            // normalised U row (reduced)
+            u32 u = 0;
+            if (c < n && c > r) {
+                u = mulmod((u32)P[k * BN + c], pinv, f);
+                P[k * BN + c] = u;
+            }
+            // multipliers of the panel rows below (exact), then their lazy update
+            if (tid > k && tid < pr) {
+                const u32 fk = LAZY ? red64(P[tid * BN + r], f) : (u32)P[tid * BN + r];
+                P[tid * BN + r] = fk;  // raw C entry
+                s_f[tid] = fk ? f.p - fk : 0u;
+            }
+            if (tid == 0) {
+                s_rrp[r] = i0 + k;
+                s_ipiv[r] = pc;
+                s_prow[r - r0] = k;
+            }
+            __syncthreads();
+            if (c < n && c > r) {
+                for (int t = k + 1; t < pr; ++t) P[t * BN + c] = lazy_fma<LAZY>(P[t * BN + c], s_f[t], u, f);
+            }
+            ++r;
+            __syncthreads();
+        }
+        // rows of the panel after the early return (r == n) keep their values;
+        // reduce everything that is still lazy and write the panel back
+        for (int e = tid; e < pr * n; e += 256) {
+            const u64 x = P[(e / n) * BN + e % n];
+            a[(i64)(i0 + e / n) * n + e % n] = LAZY ? red64(x, f) : (u32)x;
+        }
+        __syncthreads();
+        for (int e = tid; e < pr * n; e += 256) P[(e / n) * BN + e % n] = a[(i64)(i0 + e / n) * n + e % n];
+        __syncthreads();
+        // ---- trailing rows: eager elimination by the panel's pivots, one warp per row
+        const int np = r - r0;
+        if (np > 0) {
+            u32* wb = wbuf + warp * BN;
+            for (int k = i0 + pr + warp; k < m; k += 8) {
+                u32* row = a + (i64)k * n;
+                for (int q = 0; q < nq; ++q) {
+                    const int c = lane + 32 * q;
+                    if (c < n) wb[c] = row[c];
+                }
+                __syncwarp();
+                if (lane == 0)
+                    for (int j = r0; j < r; ++j)
+                        if (s_ipiv[j] != j) {
+                            const u32 x = wb[j];
+                            wb[j] = wb[s_ipiv[j]];
+                            wb[s_ipiv[j]] = x;
+                        }
+                __syncwarp();
+                u64 x[BN / 32];
+#pragma unroll
+                for (int q = 0; q < BN / 32; ++q) {
+                    const int c = lane + 32 * q;
+                    x[q] = (q < nq && c < n) ? wb[c] : 0u;
+                }
+                for (int j = 0; j < np; ++j) {
+                    const int cj = r0 + j;
+                    const int ql = cj >> 5, ll = cj & 31;
+                    u64 xv = 0;
+#pragma unroll
+                    for (int q = 0; q < BN / 32; ++q)
+                        if (q == ql) xv = x[q];
+                    u32 fj = LAZY ? red64(xv, f) : (u32)xv;
+                    fj = __shfl_sync(0xffffffffu, fj, ll);
+#pragma unroll
+                    for (int q = 0; q < BN / 32; ++q)
+                        if (q == ql && lane == ll) x[q] = fj;  // raw C entry
+                    const u32 nf = fj ? f.p - fj : 0u;
+                    const u64* U = P + s_prow[j] * BN;
+#pragma unroll
+                    for (int q = 0; q < BN / 32; ++q) {
+                        const int c = lane + 32 * q;
+                        if (q < nq && c > cj && c < n) x[q] = lazy_fma<LAZY>(x[q], nf, (u32)U[c], f);
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < BN / 32; ++q) {
+                    const int c = lane + 32 * q;
+                    if (q < nq && c < n) row[c] = LAZY ? red64(x[q], f) : (u32)x[q];
+                }
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+    }
+    if (tid == 0) ranks[blockIdx.x] = r;
+    for (int j = tid; j < r; j += 256) {
+        rrp_out[(i64)blockIdx.x * kcap + j] = s_rrp[j];
+        ipiv_out[(i64)blockIdx.x * kcap + j] = s_ipiv[j];
+    }
+    __syncthreads();
+    // place U rows: row j <- row rrp[j] on columns (j, n), zero-filling the source,
+    // in increasing j for every column (factor.cpp:62-70 composed)
+    for (int col = tid; col < n; col += 256) {
+        for (int j = 0; j < r && j < col; ++j) {
+            const i32 src = s_rrp[j];
+            if (src == j) continue;
+            a[(i64)j * n + col] = a[(i64)src * n + col];
+            a[(i64)src * n + col] = 0;
+        }
+    }
+}
+
 }  // namespace
 
 void cup_batched(u32* dA, i64 batch, i32 m, i32 n, i64 stride, u32 p, i32* d_ranks, i32* d_rrp,
                  i32* d_ipiv, i32 kcap, cudaStream_t s) {
     if (batch <= 0 || m <= 0 || n <= 0) return;
     // grid: one CTA per matrix (batch <= 2^31-1)
-    cup_batched_kernel<<<(unsigned)batch, 256, 0, s>>>(dA, stride, m, n, make_fp(p), d_ranks, d_rrp,
-                                                       d_ipiv, kcap);
+    const Fp f = make_fp(p);
+    if (n <= BN) {
+        const size_t smem = sizeof(u64) * PR * BN + sizeof(u32) * 8 * BN;
+        static bool attr = false;
+        if (!attr) {
+            RL_CUDA_CHECK(cudaFuncSetAttribute(cup_batched_blk_kernel<true>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            RL_CUDA_CHECK(cudaFuncSetAttribute(cup_batched_blk_kernel<false>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr = true;
+        }
+        if (p < (1u << 24))
+            cup_batched_blk_kernel<true><<<(unsigned)batch, 256, smem, s>>>(dA, stride, m, n, f, d_ranks,
+                                                                           d_rrp, d_ipiv, kcap);
+        else
+            cup_batched_blk_kernel<false><<<(unsigned)batch, 256, smem, s>>>(dA, stride, m, n, f, d_ranks,
+                                                                            d_rrp, d_ipiv, kcap);
+    } else {
+        cup_batched_kernel<<<(unsigned)batch, 256, 0, s>>>(dA, stride, m, n, f, d_ranks, d_rrp, d_ipiv,
+                                                           kcap);
+    }
     RL_CUDA_CHECK(cudaGetLastError());
 }
 
