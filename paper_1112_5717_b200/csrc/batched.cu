@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(256) cup_batched_kernel(u32* A, i64 stride, i3
             __syncthreads();
         }
         if (tid == 0) {
-            s_pinv = invmod(ri[r], f);
+            s_pinv = inv_euclid(ri[r], f.p);
             if (r < 1024) s_rrp[r] = i;
             rrp[r] = i;
             ipiv[r] = c;
@@ -117,6 +117,7 @@ __global__ void __launch_bounds__(256) cup_batched_blk_kernel(u32* A, i64 stride
     __shared__ i32 s_rrp[BN], s_ipiv[BN], s_prow[PR];
     __shared__ u32 s_f[PR];
     __shared__ int s_wmin[8];
+    __shared__ u32 s_pinv;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     u32* a = A + (i64)blockIdx.x * stride;
     const int nq = (n + 31) / 32;
@@ -158,8 +159,9 @@ __global__ void __launch_bounds__(256) cup_batched_blk_kernel(u32* A, i64 stride
                 }
                 __syncthreads();
             }
-            const u32 pv = (u32)P[k * BN + r];
-            const u32 pinv = invmod(pv, f);
+            if (tid == 0) s_pinv = inv_euclid((u32)P[k * BN + r], f.p);  // one thread
+            __syncthreads();
+            const u32 pinv = s_pinv;
             // normalised U row (reduced)
             u32 u = 0;
             if (c < n && c > r) {
