@@ -220,24 +220,21 @@ __global__ void __launch_bounds__(256) cup_batched_blk_kernel(u32* A, i64 stride
                     const int c = lane + 32 * q;
                     x[q] = (q < nq && c < n) ? wb[c] : 0u;
                 }
-                for (int j = 0; j < np; ++j) {
-                    const int cj = r0 + j;
-                    const int ql = cj >> 5, ll = cj & 31;
-                    u64 xv = 0;
+                // pivots in column order; column cj = r0 + j lives in register block
+                // Q = cj / 32 of lane cj % 32, so every index below is static
+                int j = 0;
 #pragma unroll
-                    for (int q = 0; q < BN / 32; ++q)
-                        if (q == ql) xv = x[q];
-                    u32 fj = LAZY ? red64(xv, f) : (u32)xv;
-                    fj = __shfl_sync(0xffffffffu, fj, ll);
+                for (int Q = 0; Q < BN / 32; ++Q) {
+                    for (; j < np && ((r0 + j) >> 5) == Q; ++j) {
+                        const int ll = (r0 + j) & 31;
+                        const u32 fj = __shfl_sync(0xffffffffu, LAZY ? red64(x[Q], f) : (u32)x[Q], ll);
+                        const u32 nf = fj ? f.p - fj : 0u;
+                        const u64* U = P + s_prow[j] * BN;
+                        if (lane == ll) x[Q] = fj;  // raw C entry
+                        else if (lane > ll) x[Q] = lazy_fma<LAZY>(x[Q], nf, (u32)U[32 * Q + lane], f);
 #pragma unroll
-                    for (int q = 0; q < BN / 32; ++q)
-                        if (q == ql && lane == ll) x[q] = fj;  // raw C entry
-                    const u32 nf = fj ? f.p - fj : 0u;
-                    const u64* U = P + s_prow[j] * BN;
-#pragma unroll
-                    for (int q = 0; q < BN / 32; ++q) {
-                        const int c = lane + 32 * q;
-                        if (q < nq && c > cj && c < n) x[q] = lazy_fma<LAZY>(x[q], nf, (u32)U[c], f);
+                        for (int q = Q + 1; q < BN / 32; ++q)
+                            x[q] = lazy_fma<LAZY>(x[q], nf, (u32)U[32 * q + lane], f);
                     }
                 }
 #pragma unroll
