@@ -57,6 +57,9 @@ WORKLOADS = {
                   desc="CUP of one 2048x2048 random_matrix(seed=3) over GF(65521)"),
     "c8192": dict(m=8192, n=8192, p=65521, seed=3,
                   desc="CUP of one 8192x8192 random_matrix(seed=3) over GF(65521)"),
+    "c5": dict(m=65536, n=65536, p=65521, seed=5,
+               desc="CUP of one 65536x65536 random_matrix(seed=5) over GF(65521) (17 GB, one GPU; "
+                    "N > 1 runs replicas, the 1D block-cyclic version is not built)"),
     "c2": dict(m=4096, n=8192, p=65521, seed=2, inner=2048,
                desc="CUP of the config-2 4096x8192 rank-2048 matrix (L*R mod p, rows i=2 mod 3 "
                     "zeroed, rows shuffled by SplitMix64(seed+2))"),

@@ -63,3 +63,37 @@ def load_npz_cases(path, prefix_keys):
     n = int(z["count"])
     for i in range(n):
         yield {k: z[f"{k}_{i}"] for k in prefix_keys}
+
+
+def freivalds_dev(orig, body, rank, sigma, p, trials=2, seed=1, block=2048):
+    """Device-side A*P^T*x == C*(U*x) mod p for torch int32 matrices holding
+    u32 values < p <= 2^16 (every partial sum < 2^53: exact in float64)."""
+    import torch
+    assert p <= 65536
+    m, n = orig.shape
+    r = int(rank)
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    sig = torch.as_tensor(np.asarray(sigma, dtype=np.int64), device=orig.device)
+    for _ in range(trials):
+        x = torch.randint(0, p, (n,), generator=g, dtype=torch.int64).to(orig.device)
+        y = torch.zeros(n, dtype=torch.int64, device=orig.device)
+        y[sig] = x
+        yd, xd = y.double(), x.double()
+        lhs = torch.empty(m, dtype=torch.int64, device=orig.device)
+        for i0 in range(0, m, block):
+            i1 = min(m, i0 + block)
+            lhs[i0:i1] = torch.remainder(orig[i0:i1].double() @ yd, p).long()
+        ux = torch.empty(r, dtype=torch.int64, device=orig.device)
+        for i0 in range(0, r, block):
+            i1 = min(r, i0 + block)
+            blk = torch.triu(body[i0:i1].double(), diagonal=i0 + 1)   # cols > row (unit diagonal implicit)
+            ux[i0:i1] = torch.remainder(blk @ xd + xd[i0:i1], p).long()
+        uxd = ux.double()
+        rhs = torch.empty(m, dtype=torch.int64, device=orig.device)
+        for i0 in range(0, m, block):
+            i1 = min(m, i0 + block)
+            blk = torch.tril(body[i0:i1, :r].double(), diagonal=i0)    # C: cols <= row, < r
+            rhs[i0:i1] = torch.remainder(blk @ uxd, p).long()
+        if not torch.equal(lhs, rhs):
+            return False
+    return True

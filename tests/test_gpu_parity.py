@@ -249,3 +249,22 @@ def test_rank_profile_and_determinant():
     # GF(7) worked example with a column swap: det = sign(P) * prod pivots
     a = np.array([[0, 1], [1, 0]], np.uint32)
     assert G.determinant(a.copy(), 7) == 6
+
+
+def test_large_cup_freivalds_on_device():
+    # a config-5-style instance at 32768^2 (4.3 GB): indexing beyond 2^31
+    # elements, the full recursion depth; reconstruction checked on the device
+    import torch
+    from tests.helpers import freivalds_dev
+    n, p = 32768, 65521
+    orig = torch.empty((n, n), dtype=torch.int32, device="cuda")
+    G.random_matrix_dev(orig, n, n, 5, p)
+    body = orig.clone()
+    r = G.cup_dev(body, n, n, p)
+    assert r.rank == n
+    assert freivalds_dev(orig, body, r.rank, r.col_perm, p, trials=2)
+    # a corrupted body must fail the same check
+    body[n // 2, n // 2 + 7] = (int(body[n // 2, n // 2 + 7]) + 1) % p
+    assert not freivalds_dev(orig, body, r.rank, r.col_perm, p, trials=1)
+    del orig, body
+    torch.cuda.empty_cache()
