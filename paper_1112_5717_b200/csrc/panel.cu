@@ -184,6 +184,32 @@ __device__ void panel_fallback(const PanelArgs& a, u32* red_buf) {
     __syncthreads();
 }
 
+// acc[x][.] += Minv[ty + 16x][k] * P[k][4tx .. 4tx+3] for k in [k0, k1), rows x >= X0.
+template <bool SP, int X0>
+__device__ __forceinline__ void tail_mac(u64 (&acc)[4][4], const u32 (*Mi)[PB + 1],
+                                         const u32 (*Ps)[TT + 4], int ty, int tx, int k0, int k1,
+                                         const Fp& f) {
+#pragma unroll 4
+    for (int k = k0; k < k1; ++k) {
+        const uint4 pv = *reinterpret_cast<const uint4*>(&Ps[k][4 * tx]);
+#pragma unroll
+        for (int x = X0; x < 4; ++x) {
+            const u32 mv = Mi[ty + 16 * x][k];
+            if (SP) {
+                acc[x][0] += (u64)mv * pv.x;
+                acc[x][1] += (u64)mv * pv.y;
+                acc[x][2] += (u64)mv * pv.z;
+                acc[x][3] += (u64)mv * pv.w;
+            } else {
+                acc[x][0] += mulmod(mv, pv.x, f);
+                acc[x][1] += mulmod(mv, pv.y, f);
+                acc[x][2] += mulmod(mv, pv.z, f);
+                acc[x][3] += mulmod(mv, pv.w, f);
+            }
+        }
+    }
+}
+
 // V = Minv * P on 64 x TT column tiles: thread (ty, tx) owns rows ty + 16x
 // (x < 4, balancing the triangle) and columns 4tx..4tx+3 (one 16-byte shared
 // load of P per 16 products).  Small tiles give many resident CTAs per SM.
@@ -233,26 +259,12 @@ __global__ void __launch_bounds__(256) panel_tail_kernel(PanelArgs a) {
             for (int x = 0; x < 4; ++x)
 #pragma unroll
                 for (int y = 0; y < 4; ++y) acc[x][y] = 0;
-            const int kmax = min(b, ty + 49);
-#pragma unroll 4
-            for (int k = 0; k < kmax; ++k) {
-                const uint4 pv = *reinterpret_cast<const uint4*>(&Ps[k][4 * tx]);
-#pragma unroll
-                for (int x = 0; x < 4; ++x) {
-                    const u32 mv = Mi[ty + 16 * x][k];
-                    if (SP) {
-                        acc[x][0] += (u64)mv * pv.x;
-                        acc[x][1] += (u64)mv * pv.y;
-                        acc[x][2] += (u64)mv * pv.z;
-                        acc[x][3] += (u64)mv * pv.w;
-                    } else {
-                        acc[x][0] += mulmod(mv, pv.x, f);
-                        acc[x][1] += mulmod(mv, pv.y, f);
-                        acc[x][2] += mulmod(mv, pv.z, f);
-                        acc[x][3] += mulmod(mv, pv.w, f);
-                    }
-                }
-            }
+            // Minv is lower triangular: row ty + 16x needs k <= ty + 16x only, so
+            // the k range splits into four phases with a static set of rows each
+            tail_mac<SP, 0>(acc, Mi, Ps, ty, tx, 0, min(b, ty + 1), f);
+            tail_mac<SP, 1>(acc, Mi, Ps, ty, tx, ty + 1, min(b, ty + 17), f);
+            tail_mac<SP, 2>(acc, Mi, Ps, ty, tx, ty + 17, min(b, ty + 33), f);
+            tail_mac<SP, 3>(acc, Mi, Ps, ty, tx, ty + 33, min(b, ty + 49), f);
 #pragma unroll
             for (int x = 0; x < 4; ++x) {
                 const int i = ty + 16 * x;
