@@ -491,20 +491,21 @@ void gemm_tc(const GemmArgs& g, int L, i64 Kmax, i64 Nmax, uint8_t* a2, uint8_t*
 
 // ------------------------------------------------------------ SIMT fallback
 namespace {
-template <bool SMALLP>
+template <bool SMALLP, int TM>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
-    // 64 x 64 output tile per CTA iteration, K in chunks of 64.  Thread (ty, tx)
-    // owns rows ty + 16a (a < 4) and columns 4tx..4tx+3: per k four broadcast
-    // loads of A and one 16-byte load of B feed 16 multiply-adds.  Operands
-    // move in 16-byte pieces whenever their rows are 16-byte aligned.
-    constexpr int SK = 64, SP_ = 68;
-    __shared__ __align__(16) u32 As[64][SP_];   // [row][k]
+    // TM x 64 output tile per CTA iteration (TM = 64, or 16 for GEMMs with few
+    // tiles), K in chunks of 64.  Thread (ty, tx) owns rows ty + 16a (a < TM/16)
+    // and columns 4tx..4tx+3: per k TM/16 broadcast loads of A and one 16-byte
+    // load of B feed 4*TM/16 multiply-adds.  Operands move in 16-byte pieces
+    // whenever their rows are 16-byte aligned.
+    constexpr int SK = 64, SP_ = 68, RT = TM / 16;
+    __shared__ __align__(16) u32 As[TM][SP_];   // [row][k]
     __shared__ __align__(16) u32 Bs[SK][SP_];   // [k][col]
     __shared__ i32 s_brow[SK];
     i32 K, N, k_lo, n_lo;
     dyn_shape(g, K, N, k_lo, n_lo);
     if (K <= 0 || N <= 0 || g.M <= 0) return;
-    const i32 MB = (g.M + 63) / 64, NB = (N + 63) / 64;
+    const i32 MB = (g.M + TM - 1) / TM, NB = (N + 63) / 64;
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const Fp f = g.f;
     const i32 bcol0 = g.b_from0 ? 0 : n_lo;
@@ -512,9 +513,9 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
     const bool bvec = ((g.ldb & 3) == 0) && (((reinterpret_cast<uintptr_t>(g.B) >> 2) + bcol0) % 4 == 0);
     for (i32 tile = blockIdx.x; tile < MB * NB; tile += gridDim.x) {
         const i32 mb = tile % MB, nb = tile / MB;
-        u64 acc[4][4];
+        u64 acc[RT][4];
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int a = 0; a < RT; ++a)
 #pragma unroll
             for (int b = 0; b < 4; ++b) acc[a][b] = 0;
         for (i32 k0 = 0; k0 < K; k0 += SK) {
@@ -524,17 +525,17 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
                 s_brow[tid] = k < K ? (g.gather ? __ldg(g.gather + k_lo + k) : (g.b_from0 ? k : k_lo + k)) : -1;
             }
             if (avec) {
-                for (int e = tid; e < 64 * SK / 4; e += 256) {
+                for (int e = tid; e < TM * SK / 4; e += 256) {
                     const int r = e >> 4, kk = (e & 15) * 4;
-                    const i32 row = mb * 64 + r;
+                    const i32 row = mb * TM + r;
                     const int bytes = row < g.M ? 4 * max(0, min(4, K - k0 - kk)) : 0;
                     cp_async16z(&As[r][kk], bytes ? g.A + (i64)(g.a_row0 + row) * g.lda + k_lo + k0 + kk : g.A,
                                 bytes);
                 }
             } else {
-                for (int e = tid; e < 64 * SK; e += 256) {
+                for (int e = tid; e < TM * SK; e += 256) {
                     const int r = e / SK, kk = e % SK;
-                    const i32 row = mb * 64 + r, k = k0 + kk;
+                    const i32 row = mb * TM + r, k = k0 + kk;
                     const bool ok = row < g.M && k < K;
                     cp_async4(&As[r][kk], ok ? g.A + (i64)(g.a_row0 + row) * g.lda + k_lo + k : g.A, ok);
                 }
@@ -562,7 +563,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
             for (int kk = 0; kk < kc; ++kk) {
                 const uint4 bv = *reinterpret_cast<const uint4*>(&Bs[kk][4 * tx]);
 #pragma unroll
-                for (int a = 0; a < 4; ++a) {
+                for (int a = 0; a < RT; ++a) {
                     const u32 av = As[ty + 16 * a][kk];
                     if (SMALLP) {
                         acc[a][0] += (u64)av * bv.x;
@@ -579,8 +580,8 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
             }
         }
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            const i32 row = mb * 64 + ty + 16 * a;
+        for (int a = 0; a < RT; ++a) {
+            const i32 row = mb * TM + ty + 16 * a;
             if (row >= g.M) continue;
             u32* crow = g.C + (i64)(g.c_row0 + row) * g.ldc + n_lo;
 #pragma unroll
@@ -602,14 +603,21 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
 
 void gemm_simt(const GemmArgs& g, i64 Kmax, i64 Nmax, cudaStream_t s) {
     if (g.M <= 0 || Kmax <= 0 || Nmax <= 0) return;
-    const i64 tiles = ((g.M + 63) / 64) * ((Nmax + 63) / 64);
-    int grid = (int)std::min<i64>(tiles, g.max_ctas > 0 ? (i64)g.max_ctas : (i64)num_sms() * 8);
-    RL_ONCE_MAX_SMEM(gemm_simt_kernel<true>);
-    RL_ONCE_MAX_SMEM(gemm_simt_kernel<false>);
-    if (g.f.p <= 65536u && Kmax <= (1ll << 31))
-        gemm_simt_kernel<true><<<std::max(grid, 1), 256, 0, s>>>(g);
-    else
-        gemm_simt_kernel<false><<<std::max(grid, 1), 256, 0, s>>>(g);
+    const i64 nb = (Nmax + 63) / 64;
+    const bool sp = g.f.p <= 65536u && Kmax <= (1ll << 31);
+    // few 64 x 64 tiles (e.g. the window slice of a leaf-pair update): 16-row
+    // tiles put 4x more CTAs (SMs) on the same work
+    if (((g.M + 63) / 64) * nb < num_sms()) {
+        const i64 tiles = ((g.M + 15) / 16) * nb;
+        const int grid = (int)std::min<i64>(tiles, g.max_ctas > 0 ? (i64)g.max_ctas : (i64)num_sms() * 8);
+        if (sp) gemm_simt_kernel<true, 16><<<std::max(grid, 1), 256, 0, s>>>(g);
+        else gemm_simt_kernel<false, 16><<<std::max(grid, 1), 256, 0, s>>>(g);
+    } else {
+        const i64 tiles = ((g.M + 63) / 64) * nb;
+        const int grid = (int)std::min<i64>(tiles, g.max_ctas > 0 ? (i64)g.max_ctas : (i64)num_sms() * 8);
+        if (sp) gemm_simt_kernel<true, 64><<<std::max(grid, 1), 256, 0, s>>>(g);
+        else gemm_simt_kernel<false, 64><<<std::max(grid, 1), 256, 0, s>>>(g);
+    }
     RL_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -29,6 +29,10 @@ namespace rl {
 
 namespace {
 
+// row pitch (words) of the staged window: WT = 192 would put every row of a
+// column in the same shared-memory bank
+constexpr int RP = WT + 4;
+
 constexpr unsigned FULL = 0xffffffffu;
 
 template <class T>
@@ -113,7 +117,7 @@ __device__ __forceinline__ void search_publish(const u64 (&acc)[6], int k, int r
         }
     }
 #pragma unroll
-    for (int q = 0; q < 6; ++q) S.s_R[k * WT + lane + 32 * q] = vals[q];
+    for (int q = 0; q < 6; ++q) S.s_R[k * RP + lane + 32 * q] = vals[q];
     if (lane == 0) {
         S.s_c[k & 1] = c;
         S.s_pinv[k & 1] = pinv;
@@ -191,11 +195,11 @@ __device__ __forceinline__ void diag_factor(u32* s_R, u32 (*s_C)[PB + 1], u32* s
         }
     }
     if (k0 < bt && cc < bt) {
-        s_R[(r0 + k0) * WT + r0 + cc] = v0;
+        s_R[(r0 + k0) * RP + r0 + cc] = v0;
         if (cc < k0) s_C[r0 + k0][r0 + cc] = v0;
     }
     if (k1 < bt && cc < bt) {
-        s_R[(r0 + k1) * WT + r0 + cc] = v1;
+        s_R[(r0 + k1) * RP + r0 + cc] = v1;
         if (cc < k1) s_C[r0 + k1][r0 + cc] = v1;
     }
     if (lane == 0) *s_fail = fail;
@@ -223,8 +227,8 @@ __device__ bool spec_lu(u32* s_R, u32 (*s_C)[PB + 1], u32* s_pv, u32* s_pinvA,
         u32 (*s_M)[LB] = s_M2[0];
         const int cc = lane & 7, k0 = lane >> 3, k1 = k0 + 4, bt = min(LB, b);
         if (warp == 0) {
-            const u32 v0 = (k0 < bt && cc < bt) ? s_R[k0 * WT + cc] : 0u;
-            const u32 v1 = (k1 < bt && cc < bt) ? s_R[k1 * WT + cc] : 0u;
+            const u32 v0 = (k0 < bt && cc < bt) ? s_R[k0 * RP + cc] : 0u;
+            const u32 v1 = (k1 < bt && cc < bt) ? s_R[k1 * RP + cc] : 0u;
             diag_factor<SP>(s_R, s_C, s_pv, s_pinvA, s_inv, s_M, s_fail, 0, bt, v0, v1, lane, f);
         }
         __syncthreads();
@@ -248,11 +252,11 @@ __device__ bool spec_lu(u32* s_R, u32 (*s_C)[PB + 1], u32* s_pv, u32* s_pinvA,
 #pragma unroll
             for (int k = 0; k < LB; ++k) {
                 if (k < bt) {
-                    u64 acc = s_R[(r0 + k) * WT + x];
+                    u64 acc = s_R[(r0 + k) * RP + x];
 #pragma unroll
                     for (int j = 0; j < k; ++j) acc = fmsn<SP>(acc, s_M[r0 + k][j], col[j], f);
                     col[k] = fred<SP>(acc, f);
-                    s_R[(r0 + k) * WT + x] = col[k];
+                    s_R[(r0 + k) * RP + x] = col[k];
                 }
             }
         } else if (tid >= 256 && tid - 256 < R) {
@@ -261,9 +265,9 @@ __device__ bool spec_lu(u32* s_R, u32 (*s_C)[PB + 1], u32* s_pv, u32* s_pinvA,
             u32 nm[LB];
 #pragma unroll
             for (int j = 0; j < LB; ++j) {
-                u64 acc = s_R[k * WT + r0 + j];
+                u64 acc = s_R[k * RP + r0 + j];
 #pragma unroll
-                for (int j2 = 0; j2 < j; ++j2) acc = fmsn<SP>(acc, nm[j2], s_R[(r0 + j2) * WT + r0 + j], f);
+                for (int j2 = 0; j2 < j; ++j2) acc = fmsn<SP>(acc, nm[j2], s_R[(r0 + j2) * RP + r0 + j], f);
                 const u32 cv = fred<SP>(acc, f);
                 s_C[k][r0 + j] = cv;
                 const u32 m = mulmod_t<SP>(cv, s_pinvA[r0 + j], f);
@@ -284,18 +288,18 @@ __device__ bool spec_lu(u32* s_R, u32 (*s_C)[PB + 1], u32* s_pv, u32* s_pinvA,
                     const uint4* mr = reinterpret_cast<const uint4*>(&s_M[x0 + k0][0]);
                     const uint4 m0 = mr[0], m1 = mr[1];
                     const u32 nmv[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
-                    u64 acc = s_R[(x0 + k0) * WT + x0 + cc];
+                    u64 acc = s_R[(x0 + k0) * RP + x0 + cc];
 #pragma unroll
-                    for (int j = 0; j < LB; ++j) acc = fmsn<SP>(acc, nmv[j], s_R[(r0 + j) * WT + x0 + cc], f);
+                    for (int j = 0; j < LB; ++j) acc = fmsn<SP>(acc, nmv[j], s_R[(r0 + j) * RP + x0 + cc], f);
                     v0 = fred<SP>(acc, f);
                 }
                 if (k1 < nbt && cc < nbt) {
                     const uint4* mr = reinterpret_cast<const uint4*>(&s_M[x0 + k1][0]);
                     const uint4 m0 = mr[0], m1 = mr[1];
                     const u32 nmv[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
-                    u64 acc = s_R[(x0 + k1) * WT + x0 + cc];
+                    u64 acc = s_R[(x0 + k1) * RP + x0 + cc];
 #pragma unroll
-                    for (int j = 0; j < LB; ++j) acc = fmsn<SP>(acc, nmv[j], s_R[(r0 + j) * WT + x0 + cc], f);
+                    for (int j = 0; j < LB; ++j) acc = fmsn<SP>(acc, nmv[j], s_R[(r0 + j) * RP + x0 + cc], f);
                     v1 = fred<SP>(acc, f);
                 }
                 diag_factor<SP>(s_R, s_C, s_pv, s_pinvA, s_inv, s_Mn, s_fail, x0, nbt, v0, v1, lane, f);
@@ -310,12 +314,12 @@ __device__ bool spec_lu(u32* s_R, u32 (*s_C)[PB + 1], u32* s_pv, u32* s_pinvA,
                     const bool diagcol = x < x0 + nbt;  // x in [x0, x0 + nbt)
                     u32 u[LB];
 #pragma unroll
-                    for (int j = 0; j < LB; ++j) u[j] = s_R[(r0 + j) * WT + x];
+                    for (int j = 0; j < LB; ++j) u[j] = s_R[(r0 + j) * RP + x];
                     for (int k = x0 + g; k < b; k += G) {
                         if (diagcol && k < x0 + nbt) continue;
                         const uint4* mrow = reinterpret_cast<const uint4*>(&s_M[k][0]);
                         const uint4 m0 = mrow[0], m1 = mrow[1];
-                        u64 acc = s_R[k * WT + x];
+                        u64 acc = s_R[k * RP + x];
                         acc = fmsn<SP>(acc, m0.x, u[0], f);
                         acc = fmsn<SP>(acc, m0.y, u[1], f);
                         acc = fmsn<SP>(acc, m0.z, u[2], f);
@@ -324,7 +328,7 @@ __device__ bool spec_lu(u32* s_R, u32 (*s_C)[PB + 1], u32* s_pv, u32* s_pinvA,
                         acc = fmsn<SP>(acc, m1.y, u[5], f);
                         acc = fmsn<SP>(acc, m1.z, u[6], f);
                         acc = fmsn<SP>(acc, m1.w, u[7], f);
-                        s_R[k * WT + x] = fred<SP>(acc, f);
+                        s_R[k * RP + x] = fred<SP>(acc, f);
                     }
                 }
             }
@@ -347,7 +351,7 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
     __shared__ int s_fail;
     WinShared S;
     S.s_R = reinterpret_cast<u32*>(dsm);
-    S.s_inv = reinterpret_cast<const uint16_t*>(dsm + PB * WT * 4);
+    S.s_inv = reinterpret_cast<const uint16_t*>(dsm + PB * RP * 4);
     S.s_C = s_C;
     S.s_c = s_c;
     S.s_pinv = s_pinv;
@@ -380,7 +384,7 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
     const int w = W < PW ? W : PW;
     if (SP) {  // 128 KB inverse table
         const uint4* src = reinterpret_cast<const uint4*>(a.inv_table);
-        uint4* dst = reinterpret_cast<uint4*>(dsm + PB * WT * 4);
+        uint4* dst = reinterpret_cast<uint4*>(dsm + PB * RP * 4);
 #pragma unroll 4
         for (int e = tid; e < 65536 * 2 / 16; e += blockDim.x) cp_async16(dst + e, src + e);
     }
@@ -404,7 +408,7 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
         const int k = warp + NW * s;
         if (k < b) {
 #pragma unroll
-            for (int q = 0; q < 6; ++q) s_R[k * WT + lane + 32 * q] = (u32)acc[s][q];
+            for (int q = 0; q < 6; ++q) s_R[k * RP + lane + 32 * q] = (u32)acc[s][q];
         }
     }
     cp_async_wait_all();
@@ -450,7 +454,7 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
         }
         u32 U[6];
 #pragma unroll
-        for (int q = 0; q < 6; ++q) U[q] = piv ? s_R[i * WT + lane + 32 * q] : 0u;
+        for (int q = 0; q < 6; ++q) U[q] = piv ? s_R[i * RP + lane + 32 * q] : 0u;
         const int inext = i + 1;
         const int rn = r + (piv ? 1 : 0);
         if (inext < b && warp == (inext % NW)) {  // lookahead: row i+1 first
@@ -513,7 +517,7 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
     } else if (!spec && warp >= 2 && warp < 4) {  // later transpositions onto the pivot rows
         const int j = tid - 64;
         if (j < rt) {
-            u32* Ur = s_R + s_rrp[j] * WT;
+            u32* Ur = s_R + s_rrp[j] * RP;
             for (int j2 = j + 1; j2 < rt; ++j2) {
                 const int cc = s_pos[j2];
                 if (cc != j2) {
@@ -539,7 +543,7 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
         for (int e = tid; e < PB * PB; e += blockDim.x) {
             const int k = e / PB, x = e % PB;
             if (k < b && x < b) {
-                const u32 rv = s_R[k * WT + x];
+                const u32 rv = s_R[k * RP + x];
                 const u32 val = x < k ? s_C[k][x] : (x == k ? rv : mulmod_t<SP>(rv, s_pinvA[k], f));
                 a.A[(i64)(a.i0 + k) * a.lda + c0 + x] = val;
             }
@@ -550,7 +554,7 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
 #pragma unroll 4
         for (int e = tid; e < PB * PB; e += blockDim.x) {
             const int k = e / PB, i = e % PB;
-            ps->Minv[k][i] = (k < b && i < b) ? mulmod_t<SP>(s_R[k * WT + PW + i], s_pinvA[k], f) : 0u;
+            ps->Minv[k][i] = (k < b && i < b) ? mulmod_t<SP>(s_R[k * RP + PW + i], s_pinvA[k], f) : 0u;
         }
     } else {
     const int xend = w;
@@ -562,8 +566,8 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
             const int rb = s_rb[k], j = s_por[k];
             if (x < rb) val = s_C[k][x];
             else if (j < 0) val = 0;
-            else if (x == j) val = s_R[k * WT + x];
-            else val = mulmod_t<SP>(s_R[k * WT + x], s_pinvA[j], f);
+            else if (x == j) val = s_R[k * RP + x];
+            else val = mulmod_t<SP>(s_R[k * RP + x], s_pinvA[j], f);
         } else {
             val = ps->win_orig[k][s_sig[x]];
         }
@@ -574,7 +578,7 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
         u32 mi = 0, mr = 0;
         if (k < b && i < b) {
             const int j = s_por[k];
-            mi = s_R[k * WT + PW + i];
+            mi = s_R[k * RP + PW + i];
             if (j >= 0) mi = mulmod_t<SP>(mi, s_pinvA[j], f);
             if (i == k) {
                 mr = j >= 0 ? s_pv[j] : 1u % f.p;
@@ -632,15 +636,15 @@ void build_inv_table(uint16_t* table, u32 p, cudaStream_t s) {
 
 void panel_window(const PanelArgs& a, cudaStream_t s) {
     const bool sp = a.f.p <= 65536u;
-    const size_t smem = sizeof(u32) * PB * WT + (sp ? 65536 * 2 : 0);
+    const size_t smem = sizeof(u32) * PB * RP + (sp ? 65536 * 2 : 0);
     static bool attr = false;
     if (!attr) {
         RL_CUDA_CHECK(cudaFuncSetAttribute(panel_window_kernel<true>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)(sizeof(u32) * PB * WT + 65536 * 2)));
+                                           (int)(sizeof(u32) * PB * RP + 65536 * 2)));
         RL_CUDA_CHECK(cudaFuncSetAttribute(panel_window_kernel<false>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)(sizeof(u32) * PB * WT)));
+                                           (int)(sizeof(u32) * PB * RP)));
         attr = true;
     }
     RL_ONCE_MAX_SMEM(panel_window_kernel<true>);
