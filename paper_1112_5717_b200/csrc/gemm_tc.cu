@@ -210,8 +210,12 @@ __device__ __forceinline__ void tile_coords(i32 tile, i32 MB, i32 NB, i32& mb, i
     nb = r / rows;
 }
 
-constexpr int EPW = 16;                    // epilogue warps (4 per TMEM lane quadrant)
-constexpr int NTHR = 64 + 32 * EPW;        // producer warp + MMA warp + epilogue
+constexpr int EPW = 16;                    // epilogue warps 0..15 (4 per TMEM lane quadrant)
+constexpr int NTHR = 64 + 32 * EPW;        // + the MMA warp and the producer warp
+// The two latency-critical single-thread roles take the HIGHEST warp ids: the
+// SMSP arbiter favours high warp ids, so the epilogue warps sharing their
+// schedulers never delay an MMA issue or a bulk copy.
+constexpr int MMA_WARP = EPW, PROD_WARP = EPW + 1;
 
 // -------------------------------------------------------------- the GEMM
 template <int L>
@@ -239,7 +243,7 @@ __global__ void __launch_bounds__(NTHR, 1)
     const i32 tiles = MB * NB;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (warp == 0 && lane == 0) {
+    if (warp == PROD_WARP && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
             ptx::mbar_init(&full[s], 1);
             ptx::mbar_init(&empty[s], 1);
@@ -251,14 +255,14 @@ __global__ void __launch_bounds__(NTHR, 1)
         ptx::fence_mbar_init();
     }
     GEMM_TRACE(0, threadIdx.x == 0);
-    if (warp == 1) ptx::tmem_alloc(tmem_slot, 512);
+    if (warp == MMA_WARP) ptx::tmem_alloc(tmem_slot, 512);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     GEMM_TRACE(1, threadIdx.x == 0);
 
-    if (warp == 0) {
+    if (warp == PROD_WARP) {
         if (lane == 0) {  // ---- producer: bulk async copies of pre-swizzled tiles
             int s = 0;
             uint32_t ph = 0;
@@ -280,7 +284,7 @@ __global__ void __launch_bounds__(NTHR, 1)
                 }
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == MMA_WARP) {
         if (lane == 0) {  // ---- MMA issuer (one thread issues for the CTA)
             constexpr uint32_t idesc = ptx::idesc_u8_s32(BM, UN);
             int s = 0;
@@ -314,12 +318,12 @@ __global__ void __launch_bounds__(NTHR, 1)
                 if (acc == 0) aph ^= 1;
             }
         }
-    } else {  // ---- epilogue warps 2..2+EPW: TMEM -> registers -> exact mod-p -> C
+    } else {  // ---- epilogue warps 0..EPW-1: TMEM -> registers -> exact mod-p -> C
         // EPW/4 warps per TMEM lane quadrant (warp & 3), each owning a slice of
         // the tile's columns.  A warp's first C chunks are requested before it
         // waits on the accumulator, so the C read latency overlaps the MMAs.
         const int q = warp & 3;  // TMEM lane quadrant this warp may access
-        const int part = (warp - 2) >> 2;
+        const int part = warp >> 2;
         const int rloc = q * 32 + lane;
         const uint32_t lane_base = (uint32_t)(q * 32) << 16;
         const Fp f = g.f;
@@ -423,7 +427,7 @@ __global__ void __launch_bounds__(NTHR, 1)
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
-    if (warp == 1) ptx::tmem_dealloc(tmem, 512);
+    if (warp == MMA_WARP) ptx::tmem_dealloc(tmem, 512);
     GEMM_TRACE(6, threadIdx.x == 0);
 }
 
