@@ -95,8 +95,20 @@ __device__ __forceinline__ void pack_a_body(const GemmArgs& g, uint8_t* __restri
         u32 v[16];
         if (row < g.M) {
             const u32* src = g.A + (i64)(g.a_row0 + row) * g.lda + k_lo + k0;
+            if (((reinterpret_cast<uintptr_t>(src) & 15) == 0) && k0 + 16 <= K) {
+                const uint4* s4 = reinterpret_cast<const uint4*>(src);
 #pragma unroll
-            for (int e = 0; e < 16; ++e) v[e] = (k0 + e < K) ? __ldg(src + e) : 0u;
+                for (int q = 0; q < 4; ++q) {
+                    const uint4 t4 = __ldg(s4 + q);
+                    v[4 * q] = t4.x;
+                    v[4 * q + 1] = t4.y;
+                    v[4 * q + 2] = t4.z;
+                    v[4 * q + 3] = t4.w;
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) v[e] = (k0 + e < K) ? __ldg(src + e) : 0u;
+            }
         } else {
 #pragma unroll
             for (int e = 0; e < 16; ++e) v[e] = 0;
@@ -128,7 +140,7 @@ __device__ __forceinline__ void pack_b_body(const GemmArgs& g, uint8_t* __restri
     constexpr int NT = Cfg<L>::NT;
     constexpr int B_TILE = Cfg<L>::B_TILE;
     constexpr int KQ = 32;
-    __shared__ u32 T[KQ][NT + 1];
+    __shared__ __align__(16) u32 T[KQ][NT + 4];
     __shared__ i32 s_rowoff[KQ];
     i32 K, N, k_lo, n_lo;
     dyn_shape(g, K, N, k_lo, n_lo);
@@ -148,12 +160,24 @@ __device__ __forceinline__ void pack_b_body(const GemmArgs& g, uint8_t* __restri
                 k < K ? (g.gather ? __ldg(g.gather + k_lo + k) : (g.b_from0 ? k : k_lo + k)) : -1;
         }
         __syncthreads();
+        const i32 bcol = (g.b_from0 ? 0 : n_lo) + nb * NT;
+        if ((g.ldb & 3) == 0 && (((reinterpret_cast<uintptr_t>(g.B) >> 2) + bcol) & 3) == 0) {
+            // rows 16-byte aligned: 16-byte pieces, zero-filled past N
+#pragma unroll 2
+            for (int e = threadIdx.x; e < KQ * NT / 4; e += blockDim.x) {
+                const int kk = e / (NT / 4), nn = (e % (NT / 4)) * 4;
+                const i32 row = s_rowoff[kk], n = nb * NT + nn;
+                const int bytes = row >= 0 ? 4 * max(0, min(4, N - n)) : 0;
+                cp_async16z(&T[kk][nn], bytes ? g.B + (i64)row * g.ldb + bcol + nn : g.B, bytes);
+            }
+        } else {
 #pragma unroll 4
-        for (int e = threadIdx.x; e < KQ * NT; e += blockDim.x) {
-            const int kk = e / NT, nn = e % NT;
-            const i32 row = s_rowoff[kk], n = nb * NT + nn;
-            const bool ok = row >= 0 && n < N;
-            cp_async4(&T[kk][nn], ok ? g.B + (i64)row * g.ldb + (g.b_from0 ? 0 : n_lo) + n : g.B, ok);
+            for (int e = threadIdx.x; e < KQ * NT; e += blockDim.x) {
+                const int kk = e / NT, nn = e % NT;
+                const i32 row = s_rowoff[kk], n = nb * NT + nn;
+                const bool ok = row >= 0 && n < N;
+                cp_async4(&T[kk][nn], ok ? g.B + (i64)row * g.ldb + bcol + nn : g.B, ok);
+            }
         }
         cp_async_wait_all();
         __syncthreads();
