@@ -78,7 +78,7 @@ struct PanelScratch {
     u64 dead_mask;          // bit i: row i of the leaf has no pivot in the window
     i32 piv_of_row[PB];     // pivot index (local) of row i, -1 if dead
     i32 rank_before[PB];
-    u32 Minv[PB][PB];       // row transform: V = Minv * P (U rows / residuals)
+    alignas(16) u32 Minv[PB][PB];  // row transform: V = Minv * P (U rows / residuals)
     u32 Mr[PB][PB];         // its inverse: P = Mr * V (fallback restore)
     u32 win_orig[PB][PW];   // original window (fallback restore)
 };
