@@ -178,7 +178,10 @@ void CupEngine::panel(i32 i0, i32 b) {
     for (cudaEvent_t e : pending_joins_) RL_CUDA_CHECK(cudaStreamWaitEvent(s_, e, 0));
     pending_joins_.clear();                 // the wide Schur update of these rows
     panel_tail(a, s_);
-    fork_to(s3_, s_);                       // trsm/next window need U^{-1} and ps
+    // U^{-1} (and the panel scratch it reads) is joined before the next TRSM,
+    // which always precedes the next window: the swaps in between overlap it
+    uinv_join_ = events_.at(next_event_++);
+    RL_CUDA_CHECK(cudaEventRecord(uinv_join_, s3_));
     stats_.panels++;
     stats_.launches += 3;
 }
@@ -330,6 +333,10 @@ void CupEngine::node(i32 i0, i32 mm) {
     node(i0, k);                             // factor.cpp:39
     const i32 b0 = i0 + k, bm = mm - k;
     swaps_range(b0, bm, dyn_rp(i0), dyn_rp(b0));                     // factor.cpp:42
+    if (!dry_ && uinv_join_) {
+        RL_CUDA_CHECK(cudaStreamWaitEvent(s_, uinv_join_, 0));
+        uinv_join_ = nullptr;
+    }
     trsm_right(b0, bm, i0, k);                                        // factor.cpp:45-46
     // factor.cpp:51-52, split: the first window of the bottom half reads only
     // columns [rp[b0], rp[b0] + PW), so that slice is updated first and the rest
@@ -360,6 +367,7 @@ void CupEngine::enqueue(u32* dA, cudaStream_t s) {
     ninv_done_.clear();
     next_event_ = 0;
     pending_joins_.clear();
+    uinv_join_ = nullptr;
     fill_rp0(rp_, s);
     if (m_ > 0 && n_ > 0) {
         node(0, m_);

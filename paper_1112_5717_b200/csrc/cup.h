@@ -69,6 +69,7 @@ private:
     std::vector<cudaEvent_t> events_;
     size_t next_event_ = 0, events_needed_ = 0;
     std::vector<cudaEvent_t> pending_joins_;   // joined before the next tail
+    cudaEvent_t uinv_join_ = nullptr;          // last leaf's U^{-1}, joined before the next TRSM
     // Schur updates with K <= this are split (window slice first, rest on s2_);
     // above it the extra narrow GEMM costs more than the overlap wins
     i32 split_max_k_ = 1024;

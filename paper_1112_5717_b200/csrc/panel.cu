@@ -283,6 +283,10 @@ __global__ void __launch_bounds__(256) panel_tail_kernel(PanelArgs a) {
         }
     }
     RL_STAMP(t_work);
+    // Without window-dead rows no residual can be nonzero and no fallback is
+    // possible: skip the grid-wide check (fence + last-CTA counter) entirely.
+    // The decision is uniform: every CTA reads the same dead_mask.
+    if (W > 0 && ps->dead_mask == 0) return;
     if (__syncthreads_or(bad != 0) && tid == 0) atomicOr(&ps->flag, 1u);
     __threadfence();
     __syncthreads();
