@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(256) trsm_leaf_kernel(TrsmLeafArgs a) {
 }
 
 template <bool SP>
-__global__ void __launch_bounds__(256) panel_uinv_kernel(PanelArgs a) {
+__global__ void __launch_bounds__(512) panel_uinv_kernel(PanelArgs a) {
     extern __shared__ __align__(16) u32 tsm[];
     const PanelScratch* ps = a.ps;
     const i32 c0 = ps->c0, W = ps->W, rt = ps->r;
@@ -392,8 +392,8 @@ void panel_uinv(const PanelArgs& a, cudaStream_t s) {
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    if (a.f.p <= 65536u) panel_uinv_kernel<true><<<1, 256, smem, s>>>(a);
-    else panel_uinv_kernel<false><<<1, 256, smem, s>>>(a);
+    if (a.f.p <= 65536u) panel_uinv_kernel<true><<<1, 512, smem, s>>>(a);
+    else panel_uinv_kernel<false><<<1, 512, smem, s>>>(a);
     RL_CUDA_CHECK(cudaGetLastError());
 }
 
