@@ -91,6 +91,7 @@ CupEngine::~CupEngine() {
 }
 
 cudaEvent_t CupEngine::fork_to(cudaStream_t from, cudaStream_t to) {
+    if (from == s_) flush_swaps();
     cudaEvent_t e = events_.at(next_event_++);
     RL_CUDA_CHECK(cudaEventRecord(e, from));
     RL_CUDA_CHECK(cudaStreamWaitEvent(to, e, 0));
@@ -142,6 +143,7 @@ void CupEngine::gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nm
         }
         return;
     }
+    if (st == s_) flush_swaps();
     ++stats_.gemms;
     if (tc) {
         ++stats_.tc_gemms;
@@ -159,6 +161,7 @@ void CupEngine::panel(i32 i0, i32 b) {
         events_needed_ += 2;
         return;
     }
+    flush_swaps();
     PanelArgs a{};
     a.uinv = uinv_ + (size_t)leaf_of_.at(i0) * PB * PB;
     a.inv_table = inv_table_;
@@ -199,8 +202,7 @@ void CupEngine::swaps_range(i32 row0, i32 M, Dyn j_lo, Dyn j_hi) {
     a.rp = rp_;
     a.ipiv = ipiv_;
     a.Mmax = M;
-    apply_swaps(a, s_);
-    stats_.launches += 1;
+    queue_swaps(a);
 }
 
 void CupEngine::swaps_gather(Dyn g_lo, Dyn g_hi, i32 Mmax, Dyn j_lo, Dyn j_hi) {
@@ -216,7 +218,20 @@ void CupEngine::swaps_gather(Dyn g_lo, Dyn g_hi, i32 Mmax, Dyn j_lo, Dyn j_hi) {
     a.rp = rp_;
     a.ipiv = ipiv_;
     a.Mmax = Mmax;
-    apply_swaps(a, s_);
+    queue_swaps(a);
+}
+
+// Swap jobs are queued and launched together right before the next kernel on
+// the critical path (consecutive jobs touch disjoint rows, see perm.cu).
+void CupEngine::queue_swaps(const SwapArgs& a) {
+    if (swap_jobs_.n == MAX_SWAP_JOBS) flush_swaps();
+    swap_jobs_.job[swap_jobs_.n++] = a;
+}
+
+void CupEngine::flush_swaps() {
+    if (dry_ || swap_jobs_.n == 0) return;
+    apply_swaps(swap_jobs_, s_);
+    swap_jobs_.n = 0;
     stats_.launches += 1;
 }
 
@@ -254,6 +269,7 @@ void CupEngine::gemm_ninv(i32 r0, i32 M, i32 x0, i32 mx, const u32* ninv) {
     g.alpha = 1 % p_;
     g.beta = 0;
     g.f = f_;
+    flush_swaps();
     ++stats_.gemms;
     ++stats_.tc_gemms;
     stats_.launches += 2;
@@ -294,6 +310,7 @@ void CupEngine::trsm_right(i32 r0, i32 M, i32 x0, i32 mx) {
         a.rp = rp_;
         a.rrp = rrp_;
         a.f = f_;
+        flush_swaps();
         a.ninv = have ? nullptr : ninv;  // first TRSM against X also leaves U_X^{-1}
         ninv_done_.insert(key);
         trsm_node(a, s_);
@@ -313,6 +330,7 @@ void CupEngine::trsm_right(i32 r0, i32 M, i32 x0, i32 mx) {
         a.rp = rp_;
         a.uinv = uinv_ + (size_t)leaf_of_.at(x0) * PB * PB;
         a.f = f_;
+        flush_swaps();
         trsm_leaf(a, s_);
         stats_.trsm_leaves++;
         stats_.launches += 1;
@@ -364,6 +382,7 @@ void CupEngine::enqueue(u32* dA, cudaStream_t s) {
     A_ = dA;
     s_ = s;
     stats_ = Stats{};
+    swap_jobs_.n = 0;
     ninv_done_.clear();
     next_event_ = 0;
     pending_joins_.clear();
@@ -375,6 +394,7 @@ void CupEngine::enqueue(u32* dA, cudaStream_t s) {
         pending_joins_.clear();
         if (m_ > PB && split_max_k_ >= PB) fork_to(s2_, s_);  // s2_ joined the capture at a split
         fork_to(s3_, s_);
+        flush_swaps();
         compact_u_rows(A_, lda_, m_, n_, rp_, rrp_, s);
         stats_.launches += 1;
     }

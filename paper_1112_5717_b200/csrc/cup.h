@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "kernels.cuh"
 
 namespace rl {
 
@@ -51,6 +52,8 @@ private:
     cudaEvent_t fork_to(cudaStream_t from, cudaStream_t to);  // `to` waits for `from`'s work so far
     void swaps_range(i32 row0, i32 M, Dyn j_lo, Dyn j_hi);
     void swaps_gather(Dyn g_lo, Dyn g_hi, i32 Mmax, Dyn j_lo, Dyn j_hi);
+    void queue_swaps(const SwapArgs& a);
+    void flush_swaps();
 
     i32 m_, n_;
     i64 lda_;
@@ -70,6 +73,7 @@ private:
     size_t next_event_ = 0, events_needed_ = 0;
     std::vector<cudaEvent_t> pending_joins_;   // joined before the next tail
     cudaEvent_t uinv_join_ = nullptr;          // last leaf's U^{-1}, joined before the next TRSM
+    SwapJobs swap_jobs_{};                     // queued, launched by flush_swaps()
     // Schur updates with K <= this are split (window slice first, rest on s2_);
     // above it the extra narrow GEMM costs more than the overlap wins
     i32 split_max_k_ = 1024;

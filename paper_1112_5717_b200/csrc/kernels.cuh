@@ -153,7 +153,13 @@ struct SwapArgs {
     const i32* ipiv;
     i32 Mmax;
 };
-void apply_swaps(const SwapArgs& a, cudaStream_t s);
+constexpr int MAX_SWAP_JOBS = 8;
+struct SwapJobs {
+    SwapArgs job[MAX_SWAP_JOBS];
+    int n;
+};
+// Row-disjoint swap jobs in one launch (applied in job order per row).
+void apply_swaps(const SwapJobs& jobs, cudaStream_t s);
 
 // Final placement of U rows (composed shifts of factor.cpp:62-70): for every
 // pivot j with rrp[j] != j, row j, columns (j, n) <- row rrp[j], and the source

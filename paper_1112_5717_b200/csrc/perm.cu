@@ -36,11 +36,10 @@ __device__ int collect_ordered(i32 lo, i32 hi, Pred pred, i32* list, int* warp_c
     return tot;
 }
 
-__global__ void __launch_bounds__(256) swaps_kernel(SwapArgs a) {
-    __shared__ i32 list[256];
-    __shared__ int warp_cnt[8];
+// One swap job: the ordered transpositions [j_lo, j_hi) on one set of rows.
+__device__ __forceinline__ void swap_job(const SwapArgs& a, i32* list, int* warp_cnt) {
     const i32 j_lo = dyn_eval(a.j_lo, a.rp), j_hi = dyn_eval(a.j_hi, a.rp);
-    if (j_hi <= j_lo) return;
+    if (j_hi <= j_lo) return;  // uniform
     i32 M, g_lo = 0;
     if (a.gather) {
         g_lo = dyn_eval(a.g_lo, a.rp);
@@ -48,7 +47,7 @@ __global__ void __launch_bounds__(256) swaps_kernel(SwapArgs a) {
     } else {
         M = a.M;
     }
-    if (M <= 0) return;
+    if (M <= 0) return;  // uniform
     const i32 row_t = blockIdx.x * blockDim.x + threadIdx.x;
     // rows handled by this thread: row_t, row_t + stride, ...
     for (i32 j0 = j_lo; j0 < j_hi; j0 += 256) {
@@ -70,6 +69,15 @@ __global__ void __launch_bounds__(256) swaps_kernel(SwapArgs a) {
         }
         __syncthreads();
     }
+}
+
+// Consecutive swap jobs of the recursion touch disjoint row sets (the top
+// halves of nested nodes, then a bottom half), so one launch runs them all;
+// within a job every row is owned by one thread, which keeps the order.
+__global__ void __launch_bounds__(256) swaps_kernel(SwapJobs jobs) {
+    __shared__ i32 list[256];
+    __shared__ int warp_cnt[8];
+    for (int q = 0; q < jobs.n; ++q) swap_job(jobs.job[q], list, warp_cnt);
 }
 
 __global__ void __launch_bounds__(256) compact_kernel(u32* A, i64 lda, i32 m, i32 n, const i32* rp,
@@ -111,11 +119,13 @@ __global__ void gen_kernel(u32* A, i64 lda, i64 m, i64 n, u64 seed, Fp f) {
 
 }  // namespace
 
-void apply_swaps(const SwapArgs& a, cudaStream_t s) {
-    if (a.Mmax <= 0) return;
-    const int grid = std::max(1, std::min((a.Mmax + 255) / 256, 2 * num_sms()));
+void apply_swaps(const SwapJobs& jobs, cudaStream_t s) {
+    int mmax = 0;
+    for (int q = 0; q < jobs.n; ++q) mmax = std::max(mmax, jobs.job[q].Mmax);
+    if (jobs.n <= 0 || mmax <= 0) return;
+    const int grid = std::max(1, std::min((mmax + 255) / 256, 2 * num_sms()));
     RL_ONCE_MAX_SMEM(swaps_kernel);
-    swaps_kernel<<<grid, 256, 0, s>>>(a);
+    swaps_kernel<<<grid, 256, 0, s>>>(jobs);
     RL_CUDA_CHECK(cudaGetLastError());
 }
 
