@@ -29,6 +29,40 @@ namespace {
 
 constexpr int TT = 64;   // tail tile width (columns per CTA tile)
 
+// One doubling level of the unit-upper inverse: for every pair of SZ x SZ
+// diagonal blocks (A, B): X_AB = -X_AA * (U_AB * X_BB).  The sums run over the
+// full block width (X is zero below its diagonal), so the loops are fixed-length
+// and unrolled -- no per-thread trip counts, shared loads pipelined.
+template <bool SP, int SZ>
+__device__ __forceinline__ void uinv_level(u32 (*U)[PB + 1], u32 (*X)[PB + 1], u32 (*T)[PB + 1], int tid,
+                                           int nt, const Fp& f) {
+    constexpr int NOUT = (PB / (2 * SZ)) * SZ * SZ;
+    for (int e = tid; e < NOUT; e += nt) {
+        const int pb = e / (SZ * SZ), rem = e % (SZ * SZ), i = rem / SZ, j = rem % SZ;
+        const int A0 = pb * 2 * SZ, B0 = A0 + SZ;
+        u64 acc = 0;
+#pragma unroll
+        for (int u = 0; u < SZ; ++u) {
+            if (SP) acc += (u64)U[A0 + i][B0 + u] * X[B0 + u][B0 + j];
+            else acc += mulmod(U[A0 + i][B0 + u], X[B0 + u][B0 + j], f);
+        }
+        T[A0 + i][B0 + j] = SP ? red_sp(acc, f) : red64(acc, f);
+    }
+    __syncthreads();
+    for (int e = tid; e < NOUT; e += nt) {
+        const int pb = e / (SZ * SZ), rem = e % (SZ * SZ), i = rem / SZ, j = rem % SZ;
+        const int A0 = pb * 2 * SZ, B0 = A0 + SZ;
+        u64 acc = 0;
+#pragma unroll
+        for (int u = 0; u < SZ; ++u) {
+            if (SP) acc += (u64)X[A0 + i][A0 + u] * T[A0 + u][B0 + j];
+            else acc += mulmod(X[A0 + i][A0 + u], T[A0 + u][B0 + j], f);
+        }
+        X[A0 + i][B0 + j] = negmod(SP ? red_sp(acc, f) : red64(acc, f), f);
+    }
+    __syncthreads();
+}
+
 // Inverse of the leaf's unit upper pivot block U (r x r, rows rrp[c0+j],
 // columns c0+j'), into uinv (PB x PB, zero padded).  Recursive doubling: the
 // eight 8 x 8 diagonal blocks are inverted by eight warps at once, then pairs
@@ -39,9 +73,11 @@ __device__ void leaf_uinv(const PanelArgs& a, i32 c0, int rt, u32 (*U)[PB + 1], 
                           u32 (*T)[PB + 1]) {
     const Fp f = a.f;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nt = blockDim.x;
+    RL_STAMP(u0);
     __shared__ i32 s_row[PB];
     if (tid < PB) s_row[tid] = tid < rt ? __ldcg(a.rrp + c0 + tid) : 0;
     __syncthreads();
+    RL_STAMP(u1);
 #pragma unroll 4
     for (int e = tid; e < PB * PB; e += nt) {
         const int i = e / PB, k = e % PB;
@@ -51,6 +87,7 @@ __device__ void leaf_uinv(const PanelArgs& a, i32 c0, int rt, u32 (*U)[PB + 1], 
     }
     cp_async_wait_all();
     __syncthreads();
+    RL_STAMP(u2);
     // diagonal blocks: warp w, lane c < 8 -> column c of block w
     if (warp < 8 && lane < 8) {
         const int base = 8 * warp, c = lane;
@@ -59,8 +96,9 @@ __device__ void leaf_uinv(const PanelArgs& a, i32 c0, int rt, u32 (*U)[PB + 1], 
         for (int i = 7; i >= 0; --i) {
             u64 acc = 0;
 #pragma unroll
-            for (int k = i + 1; k < 8; ++k) acc += mulmod_t<SP>(U[base + i][base + k], x[k], f);
-            const u32 sum = red64(acc, f);
+            for (int k = i + 1; k < 8; ++k)
+                acc += SP ? (u64)U[base + i][base + k] * x[k] : (u64)mulmod(U[base + i][base + k], x[k], f);
+            const u32 sum = SP ? red_sp(acc, f) : red64(acc, f);
             const u32 d = (i == c && base + i < rt) ? 1u % f.p : 0u;
             x[i] = i > c ? 0u : submod(d, sum, f);
         }
@@ -68,35 +106,20 @@ __device__ void leaf_uinv(const PanelArgs& a, i32 c0, int rt, u32 (*U)[PB + 1], 
         for (int i = 0; i < 8; ++i) X[base + i][base + c] = x[i];
     }
     __syncthreads();
-    for (int sz = 8; sz < PB; sz *= 2) {
-        const int nout = (PB / (2 * sz)) * sz * sz;
-        // T_AB = U_AB * X_BB (X_BB upper triangular: u <= j)
-        for (int e = tid; e < nout; e += nt) {
-            const int pb = e / (sz * sz), rem = e % (sz * sz), i = rem / sz, j = rem % sz;
-            const int A0 = pb * 2 * sz, B0 = A0 + sz;
-            u64 acc = 0;
-            for (int u = 0; u <= j; ++u) {
-                if (SP) acc += (u64)U[A0 + i][B0 + u] * X[B0 + u][B0 + j];
-                else acc += mulmod(U[A0 + i][B0 + u], X[B0 + u][B0 + j], f);
-            }
-            T[A0 + i][B0 + j] = SP ? red_sp(acc, f) : red64(acc, f);
-        }
-        __syncthreads();
-        // X_AB = -X_AA * T_AB (X_AA upper triangular: u >= i)
-        for (int e = tid; e < nout; e += nt) {
-            const int pb = e / (sz * sz), rem = e % (sz * sz), i = rem / sz, j = rem % sz;
-            const int A0 = pb * 2 * sz, B0 = A0 + sz;
-            u64 acc = 0;
-            for (int u = i; u < sz; ++u) {
-                if (SP) acc += (u64)X[A0 + i][A0 + u] * T[A0 + u][B0 + j];
-                else acc += mulmod(X[A0 + i][A0 + u], T[A0 + u][B0 + j], f);
-            }
-            X[A0 + i][B0 + j] = negmod(SP ? red_sp(acc, f) : red64(acc, f), f);
-        }
-        __syncthreads();
-    }
+    RL_STAMP(u3);
+    uinv_level<SP, 8>(U, X, T, tid, nt, f);
+    uinv_level<SP, 16>(U, X, T, tid, nt, f);
+    uinv_level<SP, 32>(U, X, T, tid, nt, f);
+    RL_STAMP(u4);
     for (int e = tid; e < PB * PB; e += nt) a.uinv[e] = X[e / PB][e % PB];
     __syncthreads();
+#ifdef RL_TRACE
+    if (a.i0 == RL_TRACE_I0 && tid == 0) {
+        RL_STAMP(u5);
+        printf("TRACE uinv row %llu load %llu diag %llu levels %llu store %llu\n", u1 - u0, u2 - u1, u3 - u2,
+               u4 - u3, u5 - u4);
+    }
+#endif
 }
 
 // Exact leaf CUP over the full width in global memory: used only when a pivot

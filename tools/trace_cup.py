@@ -44,6 +44,8 @@ tails = []
 for l in lines:
     if l.startswith("TRACE window") or l.startswith("TRACE spec") or l.startswith("TRACE trsm"):
         print(re.sub(r"\b(\d{12,})\b", lambda m: rel(m), l))
+    elif not l.startswith("TRACE tail"):
+        print(l)
     else:
         tails.append([int(x) for x in re.findall(r"\b(\d{12,})\b", l)] + [l])
 tails.sort(key=lambda t: t[2])
