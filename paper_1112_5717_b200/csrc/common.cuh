@@ -104,16 +104,19 @@ __device__ __forceinline__ u32 invmod(u32 a, const Fp& f) {
 // Inverse by the extended Euclidean algorithm (a in [1, p)): ~0.84 ln p division
 // steps on average, far shorter than Fermat's exponentiation chain.
 __device__ __forceinline__ u32 inv_euclid(u32 a, u32 p) {
-    long long r0 = p, r1 = a, t0 = 0, t1 = 1;
+    // 32-bit throughout: remainders < p < 2^31 and |coefficients| <= p
+    u32 r0 = p, r1 = a;
+    int t0 = 0, t1 = 1;
     while (r1 != 0) {
-        const long long q = r0 / r1;
-        const long long r2 = r0 - q * r1, t2 = t0 - q * t1;
+        const u32 q = r0 / r1;
+        const u32 r2 = r0 - q * r1;
+        const int t2 = t0 - (int)q * t1;
         r0 = r1;
         r1 = r2;
         t0 = t1;
         t1 = t2;
     }
-    return (u32)(t0 < 0 ? t0 + p : t0);
+    return (u32)(t0 < 0 ? t0 + (int)p : t0);
 }
 
 // Asynchronous global -> shared copies (LDGSTS): a copy loop issues every load
