@@ -268,3 +268,35 @@ def test_large_cup_freivalds_on_device():
     assert not freivalds_dev(orig, body, r.rank, r.col_perm, p, trials=1)
     del orig, body
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("p", [3, 8388593, 2147483647])
+def test_cup_mid_sizes_all_paths(p):
+    # >= 1024 rows: node inverses + their tensor-core GEMMs, split Schur updates,
+    # side streams; non-16-bit primes take the 64-bit reduction paths
+    rng = np.random.default_rng(77 + p % 1000)
+    a = rng.integers(0, p, (1100, 1300), dtype=np.uint64).astype(np.uint32)
+    _check_cup(a, p)
+    # rank deficient with a shuffled profile at the same scale
+    L = rng.integers(0, p, (1030, 700), dtype=np.uint64).astype(np.uint32)
+    R = rng.integers(0, p, (700, 1200), dtype=np.uint64).astype(np.uint32)
+    from tests.helpers import matmul_mod
+    b = matmul_mod(L, R, p)
+    b[1::4, :] = 0
+    _check_cup(np.ascontiguousarray(b[rng.permutation(1030)]), p)
+
+
+def test_cup_strided_view_large():
+    # a window of a larger allocation (lda > n) through the device entry point
+    import torch
+    p, m, n, ld = 65521, 1200, 1100, 1536
+    full = torch.empty((m, ld), dtype=torch.int32, device="cuda")
+    G.random_matrix_dev(full, m, ld, 9, p)
+    orig = full[:, :n].cpu().numpy().view(np.uint32).copy()
+    untouched = full[:, n:].clone()
+    r = G.cup_dev(full, m, n, p, lda=ld)
+    o_body = orig.copy()
+    o = O.port_cup(o_body, p)
+    assert r.rank == o.rank and np.array_equal(r.col_perm, o.sigma)
+    assert np.array_equal(full[:, :n].cpu().numpy().view(np.uint32), o_body)
+    assert torch.equal(full[:, n:], untouched)
