@@ -135,7 +135,8 @@ void CupEngine::gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nm
     g.f = f_;
     // skinny K (one leaf): the SIMT kernel reads the operands directly and
     // beats packing them for the tensor cores
-    const bool tc = use_tc_ && Kmax > PB && Nmax >= 64 && M >= 64;
+    // ... and so are the 128-column window slices of the split updates up to K = 256
+    const bool tc = use_tc_ && Kmax > PB && Nmax >= 64 && M >= 64 && !(Nmax <= PW && Kmax <= 4 * PB);
     if (dry_) {
         if (tc) {
             a2_cap_ = std::max(a2_cap_, tc_a2_bytes(L_, M, Kmax));
