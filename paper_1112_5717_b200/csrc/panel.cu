@@ -28,6 +28,7 @@ namespace rl {
 namespace {
 
 constexpr int TT = 64;   // tail tile width (columns per CTA tile)
+constexpr int MIP = PB + 4;  // Minv pitch in the tail (16-byte rows for cp.async)
 
 // One doubling level of the unit-upper inverse: for every pair of SZ x SZ
 // diagonal blocks (A, B): X_AB = -X_AA * (U_AB * X_BB).  The sums run over the
@@ -88,6 +89,9 @@ __device__ void leaf_uinv(const PanelArgs& a, i32 c0, int rt, u32 (*U)[PB + 1], 
     cp_async_wait_all();
     __syncthreads();
     RL_STAMP(u2);
+#ifdef RL_TRACE
+    const long long c2 = clock64();
+#endif
     // diagonal blocks: warp w, lane c < 8 -> column c of block w
     if (warp < 8 && lane < 8) {
         const int base = 8 * warp, c = lane;
@@ -107,6 +111,9 @@ __device__ void leaf_uinv(const PanelArgs& a, i32 c0, int rt, u32 (*U)[PB + 1], 
     }
     __syncthreads();
     RL_STAMP(u3);
+#ifdef RL_TRACE
+    const long long c3 = clock64();
+#endif
     uinv_level<SP, 8>(U, X, T, tid, nt, f);
     uinv_level<SP, 16>(U, X, T, tid, nt, f);
     uinv_level<SP, 32>(U, X, T, tid, nt, f);
@@ -116,8 +123,8 @@ __device__ void leaf_uinv(const PanelArgs& a, i32 c0, int rt, u32 (*U)[PB + 1], 
 #ifdef RL_TRACE
     if (a.i0 == RL_TRACE_I0 && tid == 0) {
         RL_STAMP(u5);
-        printf("TRACE uinv row %llu load %llu diag %llu levels %llu store %llu\n", u1 - u0, u2 - u1, u3 - u2,
-               u4 - u3, u5 - u4);
+        printf("TRACE uinv row %llu load %llu diag %llu levels %llu store %llu diag_cycles %lld\n", u1 - u0,
+               u2 - u1, u3 - u2, u4 - u3, u5 - u4, c3 - c2);
     }
 #endif
 }
@@ -209,7 +216,7 @@ __device__ void panel_fallback(const PanelArgs& a, u32* red_buf) {
 
 // acc[x][.] += Minv[ty + 16x][k] * P[k][4tx .. 4tx+3] for k in [k0, k1), rows x >= X0.
 template <bool SP, int X0>
-__device__ __forceinline__ void tail_mac(u64 (&acc)[4][4], const u32 (*Mi)[PB + 1],
+__device__ __forceinline__ void tail_mac(u64 (&acc)[4][4], const u32 (*Mi)[MIP],
                                          const u32 (*Ps)[TT + 4], int ty, int tx, int k0, int k1,
                                          const Fp& f) {
 #pragma unroll 4
@@ -239,9 +246,10 @@ __device__ __forceinline__ void tail_mac(u64 (&acc)[4][4], const u32 (*Mi)[PB + 
 template <bool SP>
 __global__ void __launch_bounds__(256) panel_tail_kernel(PanelArgs a) {
     extern __shared__ __align__(16) u32 tsm[];
-    u32 (*Mi)[PB + 1] = reinterpret_cast<u32 (*)[PB + 1]>(tsm);               // [PB][PB+1]
-    u32 (*Ps)[TT + 4] = reinterpret_cast<u32 (*)[TT + 4]>(tsm + PB * (PB + 1)); // [PB][TT+4]
-    u32 (*Xs)[PB + 1] = reinterpret_cast<u32 (*)[PB + 1]>(tsm + PB * (PB + 1));  // uinv scratch
+    u32 (*Mi)[MIP] = reinterpret_cast<u32 (*)[MIP]>(tsm);                     // [PB][MIP]
+    u32 (*Ps)[TT + 4] = reinterpret_cast<u32 (*)[TT + 4]>(tsm + PB * MIP);    // [PB][TT+4]
+    u32 (*Us)[PB + 1] = reinterpret_cast<u32 (*)[PB + 1]>(tsm);               // uinv scratch
+    u32 (*Xs)[PB + 1] = reinterpret_cast<u32 (*)[PB + 1]>(tsm + PB * (PB + 1));
     u32 (*Ts)[PB + 1] = reinterpret_cast<u32 (*)[PB + 1]>(tsm + 2 * PB * (PB + 1));
     __shared__ u32 red_buf[256];
     __shared__ int s_last;
@@ -250,32 +258,52 @@ __global__ void __launch_bounds__(256) panel_tail_kernel(PanelArgs a) {
     const Fp f = a.f;
     const int tid = threadIdx.x;
     const i32 c0 = ps->c0, W = ps->W, b = ps->b, rt = ps->r;
+    const u64 dead = ps->dead_mask;
     u32 bad = 0;
+#ifdef RL_TRACE
+    unsigned long long t_loaded = 0, t_mac = 0;
+#endif
     if (blockIdx.x == gridDim.x - 1) {
         // U^{-1} here only for leaves with window-dead rows (otherwise the
         // parallel panel_uinv kernel computes it)
-        if (W > 0 && rt > 0 && ps->dead_mask != 0) {
-            leaf_uinv<SP>(a, c0, rt, Mi, Xs, Ts);
+        if (W > 0 && rt > 0 && dead != 0) {
+            leaf_uinv<SP>(a, c0, rt, Us, Xs, Ts);
         }
     } else if (W > 0) {
-        const u64 dead = ps->dead_mask;
-#pragma unroll 4
-        for (int e = tid; e < PB * PB; e += blockDim.x)
-            cp_async4(&Mi[e / PB][e % PB], &ps->Minv[e / PB][e % PB], true);
+#pragma unroll
+        for (int e = tid; e < PB * PB / 4; e += blockDim.x)
+            cp_async16(&Mi[e / (PB / 4)][4 * (e % (PB / 4))], &ps->Minv[e / (PB / 4)][4 * (e % (PB / 4))]);
         const int tx = tid & 15, ty = tid >> 4;
         const i32 col0 = c0 + rt;
-        const i32 ntile = (a.N - col0 + TT - 1) / TT;
+        // 16-byte path: tiles start at col0 rounded down to 4 columns (the
+        // extra leading columns are computed but neither stored nor checked)
+        const bool vec = ((reinterpret_cast<uintptr_t>(a.A) & 15) == 0) && (a.lda & 3) == 0;
+        const i32 cbase = vec ? (col0 & ~3) : col0;
+        const i32 ntile = (a.N - cbase + TT - 1) / TT;
         for (i32 t = blockIdx.x; t < ntile; t += gridDim.x - 1) {
-            const i32 cb = col0 + t * TT;
+            const i32 cb = cbase + t * TT;
             __syncthreads();
+            if (vec) {
+#pragma unroll
+                for (int e = tid; e < PB * TT / 4; e += blockDim.x) {
+                    const int i = e / (TT / 4), cc = 4 * (e % (TT / 4));
+                    const int nb = i < b ? 4 * max(0, min(4, a.N - cb - cc)) : 0;
+                    cp_async16z(&Ps[i][cc], nb ? a.A + (i64)(a.i0 + i) * a.lda + cb + cc : a.A, nb);
+                }
+            } else {
 #pragma unroll 4
-            for (int e = tid; e < PB * TT; e += blockDim.x) {
-                const int i = e / TT, cc = e % TT;
-                const bool ok = i < b && cb + cc < a.N;
-                cp_async4(&Ps[i][cc], ok ? a.A + (i64)(a.i0 + i) * a.lda + cb + cc : a.A, ok);
+                for (int e = tid; e < PB * TT; e += blockDim.x) {
+                    const int i = e / TT, cc = e % TT;
+                    const bool ok = i < b && cb + cc < a.N;
+                    cp_async4(&Ps[i][cc], ok ? a.A + (i64)(a.i0 + i) * a.lda + cb + cc : a.A, ok);
+                }
             }
             cp_async_wait_all();
             __syncthreads();
+            RL_STAMP(t_ld);
+#ifdef RL_TRACE
+            t_loaded = t_ld;
+#endif
             // rows ty + 16x interleave short and long rows of the triangle
             u64 acc[4][4];
 #pragma unroll
@@ -288,18 +316,31 @@ __global__ void __launch_bounds__(256) panel_tail_kernel(PanelArgs a) {
             tail_mac<SP, 1>(acc, Mi, Ps, ty, tx, ty + 1, min(b, ty + 17), f);
             tail_mac<SP, 2>(acc, Mi, Ps, ty, tx, ty + 17, min(b, ty + 33), f);
             tail_mac<SP, 3>(acc, Mi, Ps, ty, tx, ty + 33, min(b, ty + 49), f);
+            RL_STAMP(t_m);
+#ifdef RL_TRACE
+            t_mac = t_m;
+#endif
+            const i32 cx = cb + 4 * tx;
+            const bool full = vec && cx >= col0 && cx + 4 <= a.N;
 #pragma unroll
             for (int x = 0; x < 4; ++x) {
                 const int i = ty + 16 * x;
                 if (i >= b) continue;
-                u32* out = a.A + (i64)(a.i0 + i) * a.lda + cb + 4 * tx;
+                u32* out = a.A + (i64)(a.i0 + i) * a.lda + cx;
                 const bool isdead = (dead >> i) & 1;
+                u32 v[4];
 #pragma unroll
-                for (int y = 0; y < 4; ++y) {
-                    if (cb + 4 * tx + y < a.N) {
-                        const u32 val = SP ? red_sp(acc[x][y], f) : red64(acc[x][y], f);
-                        if (isdead) bad |= val;
-                        out[y] = val;
+                for (int y = 0; y < 4; ++y) v[y] = SP ? red_sp(acc[x][y], f) : red64(acc[x][y], f);
+                if (full) {
+                    if (isdead) bad |= v[0] | v[1] | v[2] | v[3];
+                    *reinterpret_cast<uint4*>(out) = make_uint4(v[0], v[1], v[2], v[3]);
+                } else {
+#pragma unroll
+                    for (int y = 0; y < 4; ++y) {
+                        if (cx + y >= col0 && cx + y < a.N) {
+                            if (isdead) bad |= v[y];
+                            out[y] = v[y];
+                        }
                     }
                 }
             }
@@ -309,7 +350,12 @@ __global__ void __launch_bounds__(256) panel_tail_kernel(PanelArgs a) {
     // Without window-dead rows no residual can be nonzero and no fallback is
     // possible: skip the grid-wide check (fence + last-CTA counter) entirely.
     // The decision is uniform: every CTA reads the same dead_mask.
-    if (W > 0 && ps->dead_mask == 0) return;
+#ifdef RL_TRACE
+    if (a.i0 == RL_TRACE_I0 && tid == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 2))
+        printf("TRACE tailw cta %d/%d enter %llu loaded %llu mac %llu work %llu\n", blockIdx.x,
+               gridDim.x, t_enter, t_loaded, t_mac, t_work);
+#endif
+    if (W > 0 && dead == 0) return;
     if (__syncthreads_or(bad != 0) && tid == 0) atomicOr(&ps->flag, 1u);
     __threadfence();
     __syncthreads();
@@ -327,7 +373,7 @@ __global__ void __launch_bounds__(256) panel_tail_kernel(PanelArgs a) {
     if (atomicAdd(&ps->flag, 0u) != 0) {
         panel_fallback(a, red_buf);
         const int r2 = ps->r;
-        if (r2 > 0) leaf_uinv<SP>(a, c0, r2, Mi, Xs, Ts);
+        if (r2 > 0) leaf_uinv<SP>(a, c0, r2, Us, Xs, Ts);
     }
     if (tid == 0) {
         ps->counter = 0;
@@ -406,7 +452,10 @@ __global__ void __launch_bounds__(512) panel_uinv_kernel(PanelArgs a) {
 }  // namespace
 
 void panel_uinv(const PanelArgs& a, cudaStream_t s) {
-    const size_t smem = sizeof(u32) * 3 * PB * (PB + 1);
+    // The kernel needs 3 blocks of PB x (PB+1); it asks for 200 KB so that no
+    // tail-kernel CTA (launched right after it) shares its SM: this latency-bound
+    // chain ran ~3x slower beside the tail's multiply-add streams.
+    const size_t smem = std::max<size_t>(sizeof(u32) * 3 * PB * (PB + 1), 200 * 1024);
     static bool attr = false;
     if (!attr) {
         RL_CUDA_CHECK(cudaFuncSetAttribute(panel_uinv_kernel<true>,
@@ -422,7 +471,7 @@ void panel_uinv(const PanelArgs& a, cudaStream_t s) {
 
 void panel_tail(const PanelArgs& a, cudaStream_t s) {
     // tiles: Minv + P tile; the U^{-1} CTA: U, X, T (3 blocks of PB x (PB+1))
-    const size_t smem = sizeof(u32) * std::max<size_t>(PB * (PB + 1) + PB * (TT + 4), 3 * PB * (PB + 1));
+    const size_t smem = sizeof(u32) * std::max<size_t>(PB * MIP + PB * (TT + 4), 3 * PB * (PB + 1));
     static bool attr = false;
     if (!attr) {
         RL_CUDA_CHECK(cudaFuncSetAttribute(panel_tail_kernel<true>,

@@ -220,11 +220,17 @@ __device__ __forceinline__ void diag_factor(u32* s_R, u32 (*s_C)[PB + 1], u32* s
 // which the last warp already updates and factors the NEXT diagonal block (lookahead),
 // so the serial 8 x 8 factorization is off the critical path.  Returns false
 // (uniformly) on the first zero pivot; the caller then runs the exact path.
+#ifdef RL_TRACE
+__device__ unsigned long long g_wst[8][6];  // per 8-row block: start, (b)(c) done, lookahead done, end
+#define WST(blk, k) do { if ((blk) < 8) g_wst[(blk)][(k)] = rl_now(); } while (0)
+#else
+#define WST(blk, k)
+#endif
 template <bool SP>
 __device__ bool spec_lu(u32* s_R, u32 (*s_C)[PB + 1], u32* s_pv, u32* s_pinvA,
                         const uint16_t* s_inv, u32 (*s_M2)[PB][LB], int* s_fail, int b, int w,
                         const Fp& f) {
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nt = blockDim.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (w < b) return false;
     // multipliers double-buffered by block parity: warp 0 writes the next block's
     // while the other warps still read the current block's
@@ -240,6 +246,7 @@ __device__ bool spec_lu(u32* s_R, u32 (*s_C)[PB + 1], u32* s_pv, u32* s_pinvA,
     }
     for (int r0 = 0; r0 < b; r0 += LB) {
         if (*s_fail) return false;
+        if (tid == 0) WST(r0 / LB, 0);
         u32 (*s_M)[LB] = s_M2[(r0 / LB) & 1];
         u32 (*s_Mn)[LB] = s_M2[((r0 / LB) + 1) & 1];
         const int bt = min(LB, b - r0);
@@ -283,6 +290,7 @@ __device__ bool spec_lu(u32* s_R, u32 (*s_C)[PB + 1], u32* s_pv, u32* s_pinvA,
             dst[1] = make_uint4(nm[4], nm[5], nm[6], nm[7]);
         }
         __syncthreads();
+        if (tid == 0) WST(r0 / LB, 1);
         if (R > 0) {
             const int nbt = min(LB, R);  // next diagonal block: rows/cols [x0, x0 + nbt)
             // The serial lookahead runs on the HIGHEST warp id: the SMSP arbiter
@@ -310,38 +318,70 @@ __device__ bool spec_lu(u32* s_R, u32 (*s_C)[PB + 1], u32* s_pv, u32* s_pinvA,
                     for (int j = 0; j < LB; ++j) acc = fmsn<SP>(acc, nmv[j], s_R[(r0 + j) * RP + x0 + cc], f);
                     v1 = fred<SP>(acc, f);
                 }
+                if (lane == 0) WST(r0 / LB, 4);
                 diag_factor<SP>(s_R, s_C, s_pv, s_pinvA, s_inv, s_Mn, s_fail, x0, nbt, v0, v1, lane, f);
+                if (lane == 0) WST(r0 / LB, 2);
             } else {
                 // (d) rank-8 update of the rows below (a block with rows below is
                 // full: bt == LB), except the next diagonal block (the last warp's)
-                const int t2 = tid, n2 = nt - 32;
-                const int G = max(1, n2 / X);
-                for (int e = t2; e < X * G; e += n2) {
-                    const int ex = e % X, g = e / X;
-                    const int x = ex < Xw ? x0 + ex : PW + (ex - Xw);
-                    const bool diagcol = x < x0 + nbt;  // x in [x0, x0 + nbt)
-                    u32 u[LB];
+                // Thread = a column PAIR (x, x + 1) (window part [x0, b), identity
+                // part [PW, PW + PB)) and rows x0 + g (mod G): 8-byte shared loads and
+                // stores, two independent multiply-add chains per row.
+                const int t2 = tid, n2 = blockDim.x - 32;
+                const int Xw2 = (Xw + 1) >> 1;
+                const int X2 = Xw2 + PB / 2;
+                const int G = max(1, n2 / X2);
+                const int xd = x0 + nbt;  // diagonal-block columns/rows end
+                for (int e = t2; e < X2 * G; e += n2) {
+                    const int ex = e % X2, g = e / X2;
+                    const int x = ex < Xw2 ? x0 + 2 * ex : PW + 2 * (ex - Xw2);
+                    const bool two = ex >= Xw2 || x + 1 < b;
+                    const bool d0 = x < xd, d1 = x + 1 < xd;
+                    u32 ua[LB], ub[LB];
 #pragma unroll
-                    for (int j = 0; j < LB; ++j) u[j] = s_R[(r0 + j) * RP + x];
+                    for (int j = 0; j < LB; ++j) {
+                        const uint2 uu = *reinterpret_cast<const uint2*>(&s_R[(r0 + j) * RP + x]);
+                        ua[j] = uu.x;
+                        ub[j] = uu.y;
+                    }
                     for (int k = x0 + g; k < b; k += G) {
-                        if (diagcol && k < x0 + nbt) continue;
+                        const bool s0 = d0 && k < xd, s1 = !two || (d1 && k < xd);
+                        if (s0 && s1) continue;
                         const uint4* mrow = reinterpret_cast<const uint4*>(&s_M[k][0]);
                         const uint4 m0 = mrow[0], m1 = mrow[1];
-                        u64 acc = s_R[k * RP + x];
-                        acc = fmsn<SP>(acc, m0.x, u[0], f);
-                        acc = fmsn<SP>(acc, m0.y, u[1], f);
-                        acc = fmsn<SP>(acc, m0.z, u[2], f);
-                        acc = fmsn<SP>(acc, m0.w, u[3], f);
-                        acc = fmsn<SP>(acc, m1.x, u[4], f);
-                        acc = fmsn<SP>(acc, m1.y, u[5], f);
-                        acc = fmsn<SP>(acc, m1.z, u[6], f);
-                        acc = fmsn<SP>(acc, m1.w, u[7], f);
-                        s_R[k * RP + x] = fred<SP>(acc, f);
+                        const uint2 rv = *reinterpret_cast<const uint2*>(&s_R[k * RP + x]);
+                        u64 a0 = rv.x, a1 = rv.y;
+                        a0 = fmsn<SP>(a0, m0.x, ua[0], f);
+                        a1 = fmsn<SP>(a1, m0.x, ub[0], f);
+                        a0 = fmsn<SP>(a0, m0.y, ua[1], f);
+                        a1 = fmsn<SP>(a1, m0.y, ub[1], f);
+                        a0 = fmsn<SP>(a0, m0.z, ua[2], f);
+                        a1 = fmsn<SP>(a1, m0.z, ub[2], f);
+                        a0 = fmsn<SP>(a0, m0.w, ua[3], f);
+                        a1 = fmsn<SP>(a1, m0.w, ub[3], f);
+                        a0 = fmsn<SP>(a0, m1.x, ua[4], f);
+                        a1 = fmsn<SP>(a1, m1.x, ub[4], f);
+                        a0 = fmsn<SP>(a0, m1.y, ua[5], f);
+                        a1 = fmsn<SP>(a1, m1.y, ub[5], f);
+                        a0 = fmsn<SP>(a0, m1.z, ua[6], f);
+                        a1 = fmsn<SP>(a1, m1.z, ub[6], f);
+                        a0 = fmsn<SP>(a0, m1.w, ua[7], f);
+                        a1 = fmsn<SP>(a1, m1.w, ub[7], f);
+                        const u32 v0 = fred<SP>(a0, f), v1 = fred<SP>(a1, f);
+                        if (!s0 && !s1) {
+                            *reinterpret_cast<uint2*>(&s_R[k * RP + x]) = make_uint2(v0, v1);
+                        } else if (!s0) {
+                            s_R[k * RP + x] = v0;
+                        } else {
+                            s_R[k * RP + x + 1] = v1;
+                        }
                     }
                 }
+                if (tid == 0) WST(r0 / LB, 5);
             }
         }
         __syncthreads();
+        if (tid == 0) WST(r0 / LB, 3);
     }
     return true;
 }
@@ -626,6 +666,9 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
         RL_STAMP(t_exit);
         printf("TRACE window enter %llu loaded %llu lu %llu fact %llu f1 %llu f2 %llu exit %llu spec %d\n",
                t_enter, t_loaded, t_lu, t_fact, t_mid, t_f2, t_exit, (int)spec);
+        for (int k = 0; k < 8; ++k)
+            printf("TRACE wblk %d start %llu bc %llu laupd %llu la %llu d0 %llu end %llu\n", k, g_wst[k][0],
+                   g_wst[k][1], g_wst[k][4], g_wst[k][2], g_wst[k][5], g_wst[k][3]);
     }
 #endif
 }
