@@ -54,6 +54,19 @@ int rl_cup_u32_dev(uint32_t* dA, int64_t m, int64_t n, int64_t lda, uint32_t p,
                    int64_t* rank, uint32_t* rrp, uint32_t* sigma, uint64_t* ops,
                    void* stream);
 
+/* PLE, cup's column-split mirror, in place: A = P*L*E, body [L\E] (L unit lower,
+ * normalised; E row echelon with raw pivots).  col_profile (cap min(m,n)) =
+ * pivot columns, increasing; row_perm (order m) = P; ops (NULL ok) = the
+ * reference's exact charges.  Computed as cup(A^T)^T on the device (identical
+ * by construction, factor.cpp:87-156 mirrors factor.cpp:30-81).
+ * Replaces: PackedPle ranklab::ple(MatView a, OpCounter& ctr)
+ *           proj/include/ranklab/factor.hpp:37, proj/src/factor.cpp:156. */
+int rl_ple_u32(uint32_t* A, int64_t m, int64_t n, int64_t lda, uint32_t p, int64_t* rank,
+               uint32_t* col_profile, uint32_t* row_perm, uint64_t* ops);
+int rl_ple_u32_dev(uint32_t* dA, int64_t m, int64_t n, int64_t lda, uint32_t p,
+                   int64_t* rank, uint32_t* col_profile, uint32_t* row_perm, uint64_t* ops,
+                   void* stream);
+
 /* Batched CUP of `batch` independent m x n matrices stored contiguously
  * (matrix t at dA + t*stride), device pointers; ranks[t] on the host.
  * rrp (batch x min(m,n)) and sigma (batch x n) are host arrays or NULL. */

@@ -99,6 +99,8 @@ def ref_lib():
         lib = C.CDLL(REF_PATH)
         lib.ref_cup_u32.argtypes = [_u32p, _i64, _i64, _i64, _u32, C.POINTER(_i64), _u32p,
                                     _u32p, _u64p]
+        lib.ref_ple_u32.argtypes = [_u32p, _i64, _i64, _i64, _u32, C.POINTER(_i64), _u32p,
+                                    _u32p, _u64p]
         lib.ref_mm_u32.argtypes = [_u32p, _i64, _u32p, _i64, _u32p, _i64, _i64, _i64, _i64,
                                    _u32, _u32, _u32, _u64p]
         lib.ref_trsm_u32.argtypes = [C.c_int, C.c_int, C.c_int, _u32p, _i64, _i64, _u32p,
@@ -180,6 +182,19 @@ def ref_cup(a: np.ndarray, p: int) -> CupResult:
     _check(ref_lib().ref_cup_u32(a, m, n, max(n, 1), p, C.byref(rank), rrp, sigma, ops))
     r = rank.value
     return CupResult(r, rrp[:r].copy(), sigma[:n].copy(), ops)
+
+
+def ref_ple(a: np.ndarray, p: int):
+    """ranklab::ple on ``a`` in place (factor.cpp:87-156): (rank, col_profile, row_perm, ops)."""
+    assert a.dtype == np.uint32 and a.flags.c_contiguous
+    m, n = a.shape
+    rank = _i64(0)
+    prof = np.zeros(max(1, min(m, n)), np.uint32)
+    perm = np.zeros(max(m, 1), np.uint32)
+    ops = np.zeros(4, np.uint64)
+    _check(ref_lib().ref_ple_u32(a, m, n, max(n, 1), p, C.byref(rank), prof, perm, ops))
+    r = rank.value
+    return r, prof[:r].copy(), perm[:m].copy(), ops
 
 
 def ref_mm(a, b, c, alpha, beta, p):

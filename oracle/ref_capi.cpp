@@ -90,6 +90,21 @@ int ref_cup_u32(std::uint32_t* a, std::int64_t m, std::int64_t n, std::int64_t l
     });
 }
 
+// ranklab::ple (factor.hpp:37): rank, col_profile (cap min(m,n)), row_perm (order m).
+int ref_ple_u32(std::uint32_t* a, std::int64_t m, std::int64_t n, std::int64_t lda,
+                std::uint32_t p, std::int64_t* rank, std::uint32_t* prof,
+                std::uint32_t* perm, std::uint64_t* ops) {
+    return guard([&] {
+        PrimeField f(p);
+        OpCounter c;
+        PackedPle pp = ple(view_of(f, a, m, n, lda), c);
+        *rank = static_cast<std::int64_t>(pp.rank);
+        for (std::size_t j = 0; j < pp.rank; ++j) prof[j] = pp.col_profile[j];
+        for (std::size_t j = 0; j < pp.row_perm.order(); ++j) perm[j] = pp.row_perm[j];
+        put_ops(c, ops);
+    });
+}
+
 int ref_mm_u32(const std::uint32_t* a, std::int64_t lda, const std::uint32_t* b,
                std::int64_t ldb, std::uint32_t* c, std::int64_t ldc, std::int64_t m,
                std::int64_t l, std::int64_t n, std::uint32_t alpha, std::uint32_t beta,

@@ -110,6 +110,14 @@ class PackedCup:
     col_perm: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint32))
 
 
+@dataclass
+class PackedPle:
+    """Metadata of a packed [L\\E] factorization, A = P*L*E (factor.hpp:24-28)."""
+    rank: int = 0
+    col_profile: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint32))
+    row_perm: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint32))
+
+
 # ---------------------------------------------------------------- loading
 _lib = None
 _u32p = np.ctypeslib.ndpointer(dtype=np.uint32, flags="C_CONTIGUOUS")
@@ -125,7 +133,8 @@ EXPORTS = ["rl_cup_u32", "rl_cup_u32_dev", "rl_cup_batched_u32_dev", "rl_mm_u32"
            "rl_random_matrix_u32_dev", "rl_last_error", "rl_version", "rl_cup_plan_stats",
            "rl_profile_gemm_dev", "rl_cup_opcount", "rl_col_ech_trans_u32",
            "rl_col_ech_trans_u32_dev", "rl_invert_u32", "rl_invert_u32_dev", "rl_trsm_u32",
-           "rl_trsm_u32_dev", "rl_trsm_opcount", "rl_echelon_opcount"]
+           "rl_trsm_u32_dev", "rl_trsm_opcount", "rl_echelon_opcount", "rl_ple_u32",
+           "rl_ple_u32_dev"]
 
 
 def lib():
@@ -162,6 +171,8 @@ def lib():
                                   _u32, _i64, _vp, _vp]
     L.rl_trsm_opcount.argtypes = [C.c_int, C.c_int, C.c_int, _i64, _i64, _i64, _vp]
     L.rl_echelon_opcount.argtypes = [_i64, _i64, _i64, C.c_int, _vp]
+    L.rl_ple_u32.argtypes = [_vp, _i64, _i64, _i64, _u32, C.POINTER(_i64), _vp, _vp, _vp]
+    L.rl_ple_u32_dev.argtypes = [_vp, _i64, _i64, _i64, _u32, C.POINTER(_i64), _vp, _vp, _vp, _vp]
     _lib = L
     return L
 
@@ -232,6 +243,42 @@ def cup_dev(d_a, m: int, n: int, p: int, lda: int | None = None, stream=None,
         ctr._add(ops)
     r = rank.value
     return PackedCup(r, rrp[:r].copy(), sigma[:n].copy() if want_perm else np.zeros(0, np.uint32))
+
+
+def ple(a: np.ndarray, p: int, ctr: OpCounter | None = None) -> PackedPle:
+    """In-place PLE of ``a`` over GF(p): ``a`` <- packed [L\\E], A = P*L*E.
+
+    Mirrors ``ranklab::ple`` (factor.hpp:37, factor.cpp:87-156), cup's
+    column-split mirror; computed on the device as cup(A^T)^T."""
+    a = _as_u32_matrix(a)
+    m, n = a.shape
+    rank = _i64(0)
+    prof = np.zeros(max(1, min(m, n)), np.uint32)
+    perm = np.zeros(max(1, m), np.uint32)
+    ops = np.zeros(4, np.uint64)
+    _check(lib().rl_ple_u32(_ptr(a), m, n, _ld(a), int(p), C.byref(rank), _ptr(prof), _ptr(perm),
+                            _ptr(ops)))
+    if ctr is not None:
+        ctr._add(ops)
+    r = rank.value
+    return PackedPle(r, prof[:r].copy(), perm[:m].copy())
+
+
+def ple_dev(d_a, m: int, n: int, p: int, lda: int | None = None, stream=None,
+            ctr: OpCounter | None = None) -> PackedPle:
+    """PLE of a device-resident m x n matrix (``torch`` tensor or raw pointer)."""
+    ptr = d_a.data_ptr() if hasattr(d_a, "data_ptr") else int(d_a)
+    lda = n if lda is None else lda
+    rank = _i64(0)
+    prof = np.zeros(max(1, min(m, n)), np.uint32)
+    perm = np.zeros(max(1, m), np.uint32)
+    ops = np.zeros(4, np.uint64)
+    _check(lib().rl_ple_u32_dev(C.c_void_p(ptr), m, n, lda, int(p), C.byref(rank), _ptr(prof),
+                                _ptr(perm), _ptr(ops), _stream_ptr(stream)))
+    if ctr is not None:
+        ctr._add(ops)
+    r = rank.value
+    return PackedPle(r, prof[:r].copy(), perm[:m].copy())
 
 
 def cup_batched_dev(d_a, batch: int, m: int, n: int, p: int, stride: int | None = None,

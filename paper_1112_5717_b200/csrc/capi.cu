@@ -115,7 +115,7 @@ CupEngine& engine_for(i64 m, i64 n, i64 lda, u32 p) {
 }
 
 // Device scratch buffers reused across host-pointer calls.
-DevBuf g_bufA, g_bufB, g_bufC, g_bufI;
+DevBuf g_bufA, g_bufB, g_bufC, g_bufI, g_bufT;
 
 void require_device() {
     int n = 0;
@@ -211,6 +211,40 @@ void factor_on_device(u32* dA, i64 m, i64 n, i64 lda, u32 p, cudaStream_t s, i64
     CupEngine& e = engine_for(m, n, lda, p);
     e.run(dA, s, m * n >= (1 << 18));
     e.results(r, rrp_h.data(), ipiv_h.data(), s);  // synchronises s
+}
+
+// ple (factor.cpp:87-156) is cup's column-split mirror: the recursion splits
+// columns at k = n/2 where cup splits rows at m/2, the base case searches a
+// column where cup searches a row, L is normalised where U is, E keeps raw
+// pivots where C does, and the L-column move mirrors the U-row shift.  So
+// ple(A) = cup(A^T)^T exactly -- body, col_profile = cup's row profile, row_perm =
+// the inverse of cup's column permutation, and the same charges (trsm(Left,Lower,Unit) and
+// trsm(Right,Upper,Unit) charge alike, mm is symmetric).  The device path
+// transposes into a workspace, factors, and transposes back (lock held).
+void ple_on_device(u32* dA, i64 m, i64 n, i64 lda, u32 p, cudaStream_t s, i64* rank, u32* col_profile,
+                   u32* row_perm, u64* ops) {
+    u32* dT = (u32*)g_bufT.get((size_t)m * n * 4);
+    transpose(dT, m, dA, lda, m, n, s);
+    i64 r = 0;
+    std::vector<u32> rrp_h, ipiv_h;
+    factor_on_device(dT, n, m, m, p, s, &r, rrp_h, ipiv_h);
+    transpose(dA, lda, dT, m, n, m, s);
+    RL_CUDA_CHECK(cudaStreamSynchronize(s));
+    if (rank) *rank = r;
+    if (col_profile) std::copy(rrp_h.begin(), rrp_h.begin() + r, col_profile);
+    if (row_perm) {  // A^T = E^T L^T P^T: cup's column permutation is P^T
+        std::vector<u32> sig((size_t)m);
+        sigma_from_ipiv(m, r, ipiv_h.data(), sig.data());
+        for (i64 i = 0; i < m; ++i) row_perm[sig[i]] = (u32)i;
+    }
+    if (ops) cup_opcount(n, m, r, rrp_h.data(), ipiv_h.data(), ops);
+}
+
+// ple's degenerate return (factor.cpp:110): rank 0, identity of order m.
+void ple_empty(i64 m, i64* rank, u32* row_perm, u64* ops) {
+    if (rank) *rank = 0;
+    if (row_perm) for (i64 i = 0; i < m; ++i) row_perm[i] = (u32)i;
+    if (ops) std::fill(ops, ops + 4, 0ull);
 }
 
 // The reductions after cup on a device matrix (echelon.cpp:5-47): body
@@ -382,6 +416,37 @@ int rl_cup_u32(uint32_t* A, int64_t m, int64_t n, int64_t lda, uint32_t p, int64
         if (rrp) std::copy(rrp_h.begin(), rrp_h.begin() + r, rrp);
         if (sigma) sigma_from_ipiv(n, r, ipiv_h.data(), sigma);
         if (ops) cup_opcount(m, n, r, rrp_h.data(), ipiv_h.data(), ops);
+    });
+}
+
+int rl_ple_u32_dev(uint32_t* dA, int64_t m, int64_t n, int64_t lda, uint32_t p, int64_t* rank,
+                   uint32_t* col_profile, uint32_t* row_perm, uint64_t* ops, void* stream) {
+    return guard([&] {
+        check_field(p);
+        check_dims(m, n, lda);
+        if (m == 0 || n == 0) return ple_empty(m, rank, row_perm, ops);
+        if (!dA) throw Error(RL_EINVAL, "null matrix");
+        require_device();
+        std::lock_guard<std::mutex> lk(g_mu);
+        ple_on_device(dA, m, n, lda, p, (cudaStream_t)stream, rank, col_profile, row_perm, ops);
+    });
+}
+
+int rl_ple_u32(uint32_t* A, int64_t m, int64_t n, int64_t lda, uint32_t p, int64_t* rank,
+               uint32_t* col_profile, uint32_t* row_perm, uint64_t* ops) {
+    return guard([&] {
+        check_field(p);
+        check_dims(m, n, lda);
+        if (m == 0 || n == 0) return ple_empty(m, rank, row_perm, ops);
+        if (!A) throw Error(RL_EINVAL, "null matrix");
+        require_device();
+        std::lock_guard<std::mutex> lk(g_mu);
+        cudaStream_t s = cudaStreamPerThread;
+        u32* dA = (u32*)g_bufA.get((size_t)m * n * 4);
+        copy_h2d_2d(dA, n, A, lda, m, n, s);
+        ple_on_device(dA, m, n, n, p, s, rank, col_profile, row_perm, ops);
+        copy_d2h_2d(A, lda, dA, n, m, n, s);
+        RL_CUDA_CHECK(cudaStreamSynchronize(s));
     });
 }
 

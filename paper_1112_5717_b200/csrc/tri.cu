@@ -346,3 +346,32 @@ void tally_echelon(OpTally& t, i64 m, i64 n, i64 r, bool reduced) {
 }
 
 }  // namespace rl
+
+namespace rl {
+namespace {
+__global__ void __launch_bounds__(256) transpose_kernel(u32* D, i64 ldd, const u32* S, i64 lds, i64 rows,
+                                                        i64 cols) {
+    __shared__ u32 t[32][33];
+    const i64 r0 = (i64)blockIdx.y * 32, c0 = (i64)blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows per pass
+#pragma unroll
+    for (int k = 0; k < 32; k += 8) {
+        const i64 r = r0 + ty + k, c = c0 + tx;
+        if (r < rows && c < cols) t[ty + k][tx] = S[r * lds + c];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 32; k += 8) {
+        const i64 c = c0 + ty + k, r = r0 + tx;
+        if (r < rows && c < cols) D[c * ldd + r] = t[tx][ty + k];
+    }
+}
+}  // namespace
+
+void transpose(u32* D, i64 ldd, const u32* S, i64 lds, i64 rows, i64 cols, cudaStream_t s) {
+    if (rows <= 0 || cols <= 0) return;
+    const dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+    transpose_kernel<<<grid, 256, 0, s>>>(D, ldd, S, lds, rows, cols);
+    RL_CUDA_CHECK(cudaGetLastError());
+}
+}  // namespace rl

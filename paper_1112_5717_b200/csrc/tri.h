@@ -35,6 +35,10 @@ void compress_pivot_rows(u32* A, i64 lda, i32 r, const i32* d_rrp, cudaStream_t 
 // (perm_apply_rows, perm.cpp:103-113); d_idx holds pairs (i, tau[i]).
 void move_rows(u32* A, i64 lda, i64 ncols, const i32* d_idx, i32 count, cudaStream_t s);
 
+// D (cols x rows) <- S^T (S rows x cols); 32 x 32 shared-memory tiles, both
+// sides coalesced (HBM-bound: 8 bytes per element).
+void transpose(u32* D, i64 ldd, const u32* S, i64 lds, i64 rows, i64 cols, cudaStream_t s);
+
 // Operation charges of the reference's routines (field.hpp:63-98 buckets
 // {mul, addsub, divinv, ztest}), a pure function of the shapes and the
 // threshold: the reference never skips zeros.

@@ -55,6 +55,11 @@ def test_empty_shapes_need_no_device():
     b = np.zeros((4, 0), np.uint32)
     r = G.cup(b, 3)
     assert r.rank == 0 and len(r.col_perm) == 0
+    # ple's degenerate return (factor.cpp:110): identity row_perm of order m
+    pp = G.ple(b, 3)
+    assert pp.rank == 0 and list(pp.row_perm) == [0, 1, 2, 3]
+    pp = G.ple(a, 3)
+    assert pp.rank == 0 and len(pp.row_perm) == 0
 
 
 def test_mm_overlap_rejected():
@@ -71,6 +76,8 @@ def test_no_cpu_fallback():
         G.cup(a, 7)
     with pytest.raises(G.CudaError):
         G.mm(a, a, a.copy(), 1, 0, 7)
+    with pytest.raises(G.CudaError):
+        G.ple(a, 7)
 
 
 def test_opcount_matches_reference_goldens():
