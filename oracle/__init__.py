@@ -114,6 +114,8 @@ def ref_lib():
         lib.ref_random_matrix_u32.argtypes = [_i64, _i64, _u64, _u32, _u32p]
         lib.ref_random_rank_matrix_u32.argtypes = [_i64, _i64, _i64, _u64, _u32, C.c_int,
                                                    _u32p]
+        lib.ref_random_nonsingular_u32.argtypes = [_i64, _u64, _u32, _u32p]
+        lib.ref_random_triangular_u32.argtypes = [_i64, _u64, _u32, _u32p]
         lib.ref_naive_gauss_u32.argtypes = [_u32p, _i64, _i64, _u32, C.POINTER(_i64), _u32p]
         lib.ref_splitmix64.argtypes = [_u64, _i64, _u64p]
         _ref = lib
@@ -266,6 +268,18 @@ def ref_random_rank_matrix(m, n, r, seed, p, generic=False):
     out = np.zeros((max(m, 1), max(n, 1)), np.uint32)[:m, :n].copy()
     _check(ref_lib().ref_random_rank_matrix_u32(m, n, r, seed & (2**64 - 1), p,
                                                 int(generic), out))
+    return out
+
+
+def ref_random_nonsingular(n, seed, p):
+    out = np.zeros((n, n), np.uint32)
+    _check(ref_lib().ref_random_nonsingular_u32(n, seed & (2**64 - 1), p, out))
+    return out
+
+
+def ref_random_triangular(n, seed, p):
+    out = np.zeros((n, n), np.uint32)
+    _check(ref_lib().ref_random_triangular_u32(n, seed & (2**64 - 1), p, out))
     return out
 
 

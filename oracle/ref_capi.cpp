@@ -5,13 +5,14 @@
 // into oracle/_ref/libranklab_ref.so; nothing from the reference is copied
 // into this repository.  Every function forwards to the reference's own
 // public API on a MatView over the caller's buffer:
-//   ranklab::cup               proj/include/ranklab/factor.hpp:34
+//   ranklab::cup / ple         proj/include/ranklab/factor.hpp:34-37
 //   ranklab::mm / trsm         proj/include/ranklab/kernels.hpp:26-38
 //   ranklab::rank_and_profile  proj/include/ranklab/solvers.hpp:13
 //   ranklab::determinant       proj/include/ranklab/solvers.hpp:16
 //   ranklab::invert_in_place   proj/include/ranklab/solvers.hpp:22
 //   ranklab::col_ech_trans / red_col_ech_trans  proj/include/ranklab/echelon.hpp:28-29
-//   ranklab::random_matrix / random_rank_matrix / SplitMix64 / naive_gauss
+//   ranklab::random_matrix / random_rank_matrix / random_nonsingular_matrix /
+//   random_triangular_matrix / SplitMix64 / naive_gauss
 //                              proj/include/ranklab/reference.hpp
 #include <cstdint>
 #include <cstring>
@@ -210,6 +211,27 @@ int ref_random_rank_matrix_u32(std::int64_t m, std::int64_t n, std::int64_t r,
         Mat a = random_rank_matrix(m, n, r, seed, f,
                                    generic ? RankPlacement::Generic : RankPlacement::Spread);
         for (std::int64_t i = 0; i < m; ++i)
+            for (std::int64_t j = 0; j < n; ++j) out[i * n + j] = a(i, j);
+    });
+}
+
+// reference.cpp:255-287 generators (the CLI bench inputs).
+int ref_random_nonsingular_u32(std::int64_t n, std::uint64_t seed, std::uint32_t p,
+                               std::uint32_t* out) {
+    return guard([&] {
+        PrimeField f(p);
+        Mat a = random_nonsingular_matrix(n, seed, f);
+        for (std::int64_t i = 0; i < n; ++i)
+            for (std::int64_t j = 0; j < n; ++j) out[i * n + j] = a(i, j);
+    });
+}
+
+int ref_random_triangular_u32(std::int64_t n, std::uint64_t seed, std::uint32_t p,
+                              std::uint32_t* out) {
+    return guard([&] {
+        PrimeField f(p);
+        Mat a = random_triangular_matrix(n, UpLo::Upper, seed, f);
+        for (std::int64_t i = 0; i < n; ++i)
             for (std::int64_t j = 0; j < n; ++j) out[i * n + j] = a(i, j);
     });
 }

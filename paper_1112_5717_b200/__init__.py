@@ -40,7 +40,7 @@ __all__ = [
     "rank_and_profile", "determinant", "random_matrix_dev", "LIB_PATH", "lib",
     "EchelonTransform", "ReducedEchelonTransform", "col_ech_trans", "red_col_ech_trans",
     "col_ech_trans_dev", "invert_in_place", "invert_dev", "trsm", "trsm_dev",
-    "Side", "UpLo", "Diag",
+    "Side", "UpLo", "Diag", "PackedPle", "ple", "ple_dev",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
