@@ -18,7 +18,7 @@
 #endif
 __device__ __forceinline__ unsigned long long rl_now() {
     unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
     return t;
 }
 #define RL_STAMP(var) const unsigned long long var = rl_now()

@@ -223,8 +223,12 @@ __device__ __forceinline__ void diag_factor(u32* s_R, u32 (*s_C)[PB + 1], u32* s
 #ifdef RL_TRACE
 __device__ unsigned long long g_wst[8][6];  // per 8-row block: start, (b)(c) done, lookahead done, end
 #define WST(blk, k) do { if ((blk) < 8) g_wst[(blk)][(k)] = rl_now(); } while (0)
+#define WCLK(var) const long long var = clock64()
+#define WCYC(blk, k, v) do { if ((blk) < 8) g_wst[(blk)][(k)] = (unsigned long long)(v); } while (0)
 #else
 #define WST(blk, k)
+#define WCLK(var)
+#define WCYC(blk, k, v)
 #endif
 template <bool SP>
 __device__ bool spec_lu(u32* s_R, u32 (*s_C)[PB + 1], u32* s_pv, u32* s_pinvA,
@@ -252,10 +256,12 @@ __device__ bool spec_lu(u32* s_R, u32 (*s_C)[PB + 1], u32* s_pv, u32* s_pinvA,
         const int bt = min(LB, b - r0);
         const int x0 = r0 + bt;  // first column right of the block
         // Columns still needed: the rest of the pivot block [x0, b) and the identity
-        // block [PW, WT); window columns >= b hold no pivot on this path (the tail
-        // kernel computes them as V = Minv * P).
+        // block's first x0 columns [PW, PW + x0) -- its columns c >= x0 are still e_c
+        // and the block rows are zero there, so no update touches them; window
+        // columns >= b hold no pivot on this path (the tail kernel computes them as
+        // V = Minv * P).
         const int Xw = max(0, b - x0);
-        const int X = Xw + PB;
+        const int X = Xw + x0;
         const int R = b - x0;  // rows below the block
         if (tid < X) {
             // (b) block rows, column x: forward substitution down the block
@@ -291,6 +297,7 @@ __device__ bool spec_lu(u32* s_R, u32 (*s_C)[PB + 1], u32* s_pv, u32* s_pinvA,
         }
         __syncthreads();
         if (tid == 0) WST(r0 / LB, 1);
+        WCLK(cb0);
         if (R > 0) {
             const int nbt = min(LB, R);  // next diagonal block: rows/cols [x0, x0 + nbt)
             // The serial lookahead runs on the HIGHEST warp id: the SMSP arbiter
@@ -318,18 +325,20 @@ __device__ bool spec_lu(u32* s_R, u32 (*s_C)[PB + 1], u32* s_pv, u32* s_pinvA,
                     for (int j = 0; j < LB; ++j) acc = fmsn<SP>(acc, nmv[j], s_R[(r0 + j) * RP + x0 + cc], f);
                     v1 = fred<SP>(acc, f);
                 }
-                if (lane == 0) WST(r0 / LB, 4);
+                WCLK(cl1);
+                if (lane == 0) WCYC(r0 / LB, 4, cl1 - cb0);
                 diag_factor<SP>(s_R, s_C, s_pv, s_pinvA, s_inv, s_Mn, s_fail, x0, nbt, v0, v1, lane, f);
-                if (lane == 0) WST(r0 / LB, 2);
+                WCLK(cl2);
+                if (lane == 0) WCYC(r0 / LB, 2, cl2 - cb0);
             } else {
                 // (d) rank-8 update of the rows below (a block with rows below is
                 // full: bt == LB), except the next diagonal block (the last warp's)
                 // Thread = a column PAIR (x, x + 1) (window part [x0, b), identity
-                // part [PW, PW + PB)) and rows x0 + g (mod G): 8-byte shared loads and
+                // part [PW, PW + x0)) and rows x0 + g (mod G): 8-byte shared loads and
                 // stores, two independent multiply-add chains per row.
                 const int t2 = tid, n2 = blockDim.x - 32;
                 const int Xw2 = (Xw + 1) >> 1;
-                const int X2 = Xw2 + PB / 2;
+                const int X2 = Xw2 + x0 / 2;  // x0 is a multiple of LB here (R > 0)
                 const int G = max(1, n2 / X2);
                 const int xd = x0 + nbt;  // diagonal-block columns/rows end
                 for (int e = t2; e < X2 * G; e += n2) {
@@ -377,7 +386,8 @@ __device__ bool spec_lu(u32* s_R, u32 (*s_C)[PB + 1], u32* s_pv, u32* s_pinvA,
                         }
                     }
                 }
-                if (tid == 0) WST(r0 / LB, 5);
+                WCLK(cd);
+                if (tid == 0) WCYC(r0 / LB, 5, cd - cb0);
             }
         }
         __syncthreads();
@@ -667,8 +677,8 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
         printf("TRACE window enter %llu loaded %llu lu %llu fact %llu f1 %llu f2 %llu exit %llu spec %d\n",
                t_enter, t_loaded, t_lu, t_fact, t_mid, t_f2, t_exit, (int)spec);
         for (int k = 0; k < 8; ++k)
-            printf("TRACE wblk %d start %llu bc %llu laupd %llu la %llu d0 %llu end %llu\n", k, g_wst[k][0],
-                   g_wst[k][1], g_wst[k][4], g_wst[k][2], g_wst[k][5], g_wst[k][3]);
+            printf("TRACE wblk %d start %llu bc %llu end %llu | cycles: laupd %llu la %llu d(tid0) %llu\n", k,
+                   g_wst[k][0], g_wst[k][1], g_wst[k][3], g_wst[k][4], g_wst[k][2], g_wst[k][5]);
     }
 #endif
 }
