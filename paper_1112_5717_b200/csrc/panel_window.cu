@@ -210,6 +210,85 @@ __device__ __forceinline__ void diag_factor(u32* s_R, u32 (*s_C)[PB + 1], u32* s
     if (lane == 0) *s_fail = fail;
 }
 
+// Same contract as diag_factor, fraction-free: step j replaces row k by
+// pv_j * row_k - R_k[j] * row_j (pv_j the current, scaled pivot), so no inverse
+// sits on the serial chain (shuffle -> two independent products -> subtract).
+// Row k then carries the scale S_k = pv_0 ... pv_{k-1} and its entry at column
+// j < k the scale S_j; with T_j = S_j^{-1} the true values follow once per
+// block, off the chain: U part R * T_k, C part R * T_j, negated multiplier
+// -R_k[j] * pv_j^{-1} (the scales of rows j and k agree at step j), pivot
+// pv_j * T_j and its inverse pv_j^{-1} * S_j.  A zero scaled pivot is a zero
+// true pivot (the scales are products of nonzero pivots).
+template <bool SP>
+__device__ __forceinline__ void diag_factor_ff(u32* s_R, u32 (*s_C)[PB + 1], u32* s_pv, u32* s_pinvA,
+                                               const uint16_t* s_inv, u32 (*s_M)[LB], int* s_fail,
+                                               int r0, int bt, u32 v0, u32 v1, int lane, const Fp& f) {
+    const int cc = lane & 7, k0 = lane >> 3, k1 = k0 + 4;
+    int fail = 0;
+    u32 pvs[LB];
+    u32 S[LB + 1];
+    S[0] = 1u % f.p;
+    // branch-free: every lane runs every step, updates are selected
+#pragma unroll
+    for (int j = 0; j < LB; ++j) {
+        const u32 pv = __shfl_sync(FULL, j < 4 ? v0 : v1, (j & 3) * 8 + j);
+        const u32 c0v = __shfl_sync(FULL, v0, k0 * 8 + j);          // R(k0, j)
+        const u32 c1v = __shfl_sync(FULL, v1, (k1 - 4) * 8 + j);    // R(k1, j)
+        const u32 uj = __shfl_sync(FULL, j < 4 ? v0 : v1, (j & 3) * 8 + cc);
+        const bool live = j < bt;
+        fail |= (live && pv == 0) ? 1 : 0;
+        const u32 n0 = submod(mulmod_t<SP>(pv, v0, f), mulmod_t<SP>(c0v, uj, f), f);
+        const u32 n1 = submod(mulmod_t<SP>(pv, v1, f), mulmod_t<SP>(c1v, uj, f), f);
+        const bool up = live && cc > j;
+        v0 = (up && k0 > j) ? n0 : v0;
+        v1 = (up && k1 > j) ? n1 : v1;
+        pvs[j] = live ? pv : 1u % f.p;
+        S[j + 1] = live ? mulmod_t<SP>(S[j], pv, f) : S[j];
+    }
+    if (lane == 0) *s_fail = fail;
+    if (fail) return;  // uniform: the caller abandons the speculative path
+    // one inverse per block row (table lookups / Fermat, in parallel), then
+    // shuffles: lane j < bt holds pv_j^{-1} and T_j = S_j^{-1}
+    u32 my_ipv = 0, my_T = 0;
+    if (lane < bt) {
+        u32 pvl = pvs[0], Sl = S[0];
+#pragma unroll
+        for (int j = 1; j < LB; ++j)
+            if (lane == j) {
+                pvl = pvs[j];
+                Sl = S[j];
+            }
+        my_ipv = SP ? (u32)s_inv[pvl] : invmod(pvl, f);
+        my_T = SP ? (u32)s_inv[Sl] : invmod(Sl, f);
+        s_pv[r0 + lane] = mulmod_t<SP>(pvl, my_T, f);
+        s_pinvA[r0 + lane] = mulmod_t<SP>(my_ipv, Sl, f);
+    }
+    const u32 T_k0 = __shfl_sync(FULL, my_T, k0), T_k1 = __shfl_sync(FULL, my_T, k1);
+    const u32 T_c = __shfl_sync(FULL, my_T, cc), ipv_c = __shfl_sync(FULL, my_ipv, cc);
+    if (k0 < bt && cc < bt) {
+        if (cc < k0) {
+            const u32 m = mulmod_t<SP>(v0, ipv_c, f);
+            s_M[r0 + k0][cc] = m ? f.p - m : 0u;
+            v0 = mulmod_t<SP>(v0, T_c, f);
+            s_C[r0 + k0][r0 + cc] = v0;
+        } else {
+            v0 = mulmod_t<SP>(v0, T_k0, f);
+        }
+        s_R[(r0 + k0) * RP + r0 + cc] = v0;
+    }
+    if (k1 < bt && cc < bt) {
+        if (cc < k1) {
+            const u32 m = mulmod_t<SP>(v1, ipv_c, f);
+            s_M[r0 + k1][cc] = m ? f.p - m : 0u;
+            v1 = mulmod_t<SP>(v1, T_c, f);
+            s_C[r0 + k1][r0 + cc] = v1;
+        } else {
+            v1 = mulmod_t<SP>(v1, T_k1, f);
+        }
+        s_R[(r0 + k1) * RP + r0 + cc] = v1;
+    }
+}
+
 // Speculative pivot discovery for GENERIC leaves: blocked right-looking LU of
 // the window without pivoting, in shared memory (s_R = [window | identity],
 // reduced values).  If every diagonal value is nonzero, row i's first nonzero
@@ -244,7 +323,7 @@ __device__ bool spec_lu(u32* s_R, u32 (*s_C)[PB + 1], u32* s_pv, u32* s_pinvA,
         if (warp == NW - 1) {
             const u32 v0 = (k0 < bt && cc < bt) ? s_R[k0 * RP + cc] : 0u;
             const u32 v1 = (k1 < bt && cc < bt) ? s_R[k1 * RP + cc] : 0u;
-            diag_factor<SP>(s_R, s_C, s_pv, s_pinvA, s_inv, s_M, s_fail, 0, bt, v0, v1, lane, f);
+            diag_factor_ff<SP>(s_R, s_C, s_pv, s_pinvA, s_inv, s_M, s_fail, 0, bt, v0, v1, lane, f);
         }
         __syncthreads();
     }
@@ -327,7 +406,7 @@ __device__ bool spec_lu(u32* s_R, u32 (*s_C)[PB + 1], u32* s_pv, u32* s_pinvA,
                 }
                 WCLK(cl1);
                 if (lane == 0) WCYC(r0 / LB, 4, cl1 - cb0);
-                diag_factor<SP>(s_R, s_C, s_pv, s_pinvA, s_inv, s_Mn, s_fail, x0, nbt, v0, v1, lane, f);
+                diag_factor_ff<SP>(s_R, s_C, s_pv, s_pinvA, s_inv, s_Mn, s_fail, x0, nbt, v0, v1, lane, f);
                 WCLK(cl2);
                 if (lane == 0) WCYC(r0 / LB, 2, cl2 - cb0);
             } else {
@@ -471,6 +550,27 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
     }
     cp_async_wait_all();
     __syncthreads();
+#ifdef RL_TRACE
+    // solo timing of the lookahead's diagonal factorization (all other warps at
+    // the barrier): the same 8 x 8 block the first lookahead factors
+    unsigned long long solo = 0;
+    if (a.i0 == RL_TRACE_I0) {
+        if (warp == NW - 1) {
+            const int cc = lane & 7, k0 = lane >> 3, k1 = k0 + 4;
+            const u32 v0 = s_R[k0 * RP + cc], v1 = s_R[k1 * RP + cc];
+            __syncwarp();
+            const long long c0 = clock64();
+            diag_factor_ff<SP>(s_R, s_C, s_pv, s_pinvA, S.s_inv, s_M[1], &s_fail, 0, 8, v0, v1, lane, f);
+            __syncwarp();
+            solo = clock64() - c0;
+            // restore the staged block and the flag
+            s_R[k0 * RP + cc] = v0;
+            s_R[k1 * RP + cc] = v1;
+            if (lane == 0) { s_fail = 0; g_wst[7][4] = solo; }
+        }
+        __syncthreads();
+    }
+#endif
     RL_STAMP(t_loaded);
     const bool spec = spec_lu<SP>(s_R, s_C, s_pv, s_pinvA, S.s_inv, s_M, &s_fail, b, w, f);
     RL_STAMP(t_lu);
@@ -676,6 +776,7 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
         RL_STAMP(t_exit);
         printf("TRACE window enter %llu loaded %llu lu %llu fact %llu f1 %llu f2 %llu exit %llu spec %d\n",
                t_enter, t_loaded, t_lu, t_fact, t_mid, t_f2, t_exit, (int)spec);
+        printf("TRACE solo diag_factor %llu cycles\n", g_wst[7][4]);
         for (int k = 0; k < 8; ++k)
             printf("TRACE wblk %d start %llu bc %llu end %llu | cycles: laupd %llu la %llu d(tid0) %llu\n", k,
                    g_wst[k][0], g_wst[k][1], g_wst[k][3], g_wst[k][4], g_wst[k][2], g_wst[k][5]);

@@ -42,7 +42,7 @@ if t0 is None:
 rel = lambda m: f"{(int(m.group(0)) - t0) / 1e3:8.2f}"
 tails = []
 for l in lines:
-    if l.startswith(("TRACE window", "TRACE spec", "TRACE trsm", "TRACE tailw", "TRACE wblk")):
+    if l.startswith(("TRACE window", "TRACE spec", "TRACE trsm", "TRACE tailw", "TRACE wblk", "TRACE solo")):
         print(re.sub(r"\b(\d{12,})\b", lambda m: rel(m), l))
     elif not l.startswith("TRACE tail"):
         print(l)
