@@ -257,8 +257,28 @@ __global__ void __launch_bounds__(256) panel_tail_kernel(PanelArgs a) {
     PanelScratch* ps = a.ps;
     const Fp f = a.f;
     const int tid = threadIdx.x;
+    const bool vec = ((reinterpret_cast<uintptr_t>(a.A) & 15) == 0) && (a.lda & 3) == 0;
+    // Launched as a programmatic dependent of the window kernel: before its
+    // grid completes, prefetch this CTA's first tile on the assumption of the
+    // speculative path (rank b, no transposition -- the window then leaves
+    // columns >= c0 + b untouched; c0 = rp[i0] is older than the window).
+    const i32 c0_pre = __ldcg(a.rp + a.i0);
+    const i32 cb_pre = vec ? ((c0_pre + a.b) & ~3) : c0_pre + a.b;
+    const bool pre = vec && blockIdx.x < gridDim.x - 1 && cb_pre + (i32)blockIdx.x * TT < a.N;
+    if (pre) {
+        const i32 cb = cb_pre + blockIdx.x * TT;
+#pragma unroll
+        for (int e = tid; e < PB * TT / 4; e += blockDim.x) {
+            const int i = e / (TT / 4), cc = 4 * (e % (TT / 4));
+            const int nb = i < a.b ? 4 * max(0, min(4, a.N - cb - cc)) : 0;
+            cp_async16z(&Ps[i][cc], nb ? a.A + (i64)(a.i0 + i) * a.lda + cb + cc : a.A, nb);
+        }
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const i32 c0 = ps->c0, W = ps->W, b = ps->b, rt = ps->r;
     const u64 dead = ps->dead_mask;
+    const bool pre_ok = pre && ps->spec && rt == a.b && c0 == c0_pre && dead == 0;
+    if (pre && !pre_ok) cp_async_wait_all();  // drain before the tile is reloaded
     u32 bad = 0;
 #ifdef RL_TRACE
     unsigned long long t_loaded = 0, t_mac = 0;
@@ -277,13 +297,14 @@ __global__ void __launch_bounds__(256) panel_tail_kernel(PanelArgs a) {
         const i32 col0 = c0 + rt;
         // 16-byte path: tiles start at col0 rounded down to 4 columns (the
         // extra leading columns are computed but neither stored nor checked)
-        const bool vec = ((reinterpret_cast<uintptr_t>(a.A) & 15) == 0) && (a.lda & 3) == 0;
         const i32 cbase = vec ? (col0 & ~3) : col0;
         const i32 ntile = (a.N - cbase + TT - 1) / TT;
         for (i32 t = blockIdx.x; t < ntile; t += gridDim.x - 1) {
             const i32 cb = cbase + t * TT;
             __syncthreads();
-            if (vec) {
+            if (t == (i32)blockIdx.x && pre_ok) {
+                // the prefetched tile is this one (same rows, same columns)
+            } else if (vec) {
 #pragma unroll
                 for (int e = tid; e < PB * TT / 4; e += blockDim.x) {
                     const int i = e / (TT / 4), cc = 4 * (e % (TT / 4));
@@ -483,9 +504,20 @@ void panel_tail(const PanelArgs& a, cudaStream_t s) {
     const int grid = std::max(1, std::min((a.N + TT - 1) / TT, 8 * num_sms())) + 1;
     RL_ONCE_MAX_SMEM(panel_tail_kernel<true>);
     RL_ONCE_MAX_SMEM(panel_tail_kernel<false>);
-    if (a.f.p <= 65536u) panel_tail_kernel<true><<<grid, 256, smem, s>>>(a);
-    else panel_tail_kernel<false><<<grid, 256, smem, s>>>(a);
-    RL_CUDA_CHECK(cudaGetLastError());
+    // programmatic dependent launch: the CTAs start (and prefetch) while the
+    // window kernel finishes; griddepcontrol.wait orders everything else
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (a.f.p <= 65536u) RL_CUDA_CHECK(cudaLaunchKernelEx(&cfg, panel_tail_kernel<true>, a));
+    else RL_CUDA_CHECK(cudaLaunchKernelEx(&cfg, panel_tail_kernel<false>, a));
 }
 
 void trsm_leaf(const TrsmLeafArgs& a, cudaStream_t s) {

@@ -514,6 +514,7 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
         if (tid == 0) {
             ps->w = 0;
             ps->r = 0;
+            ps->spec = 0;
             ps->dead_mask = 0;
         }
         return;
@@ -662,6 +663,10 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
 
     // ------------------------------------------------------------ finalize
     RL_STAMP(t_fact);
+    // the tail kernel (a programmatic dependent launch) may start now: it only
+    // prefetches columns this kernel does not write on the speculative path,
+    // and waits for this grid's completion before reading anything else
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int rt = r;
     // (the speculative path made no transposition: both loops are identities)
     if (!spec && warp == 1 && lane == 0) {  // window column permutation
@@ -769,6 +774,7 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
             ps->dead_mask = mask;
             ps->w = w;
             ps->r = rt;
+            ps->spec = spec ? 1 : 0;
         }
     }
 #ifdef RL_TRACE
