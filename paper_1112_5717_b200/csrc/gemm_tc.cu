@@ -84,7 +84,9 @@ __device__ __forceinline__ void pack_a_body(const GemmArgs& g, uint8_t* __restri
     const i32 KB = (K + BK - 1) / BK;
     const i32 MB = (g.M + BM - 1) / BM;
     const i64 total = (i64)MB * KB * BM * 8;
-    for (i64 idx = (i64)bid * blockDim.x + threadIdx.x; idx < total; idx += (i64)nb * blockDim.x) {
+    // chunk idx = 16 consecutive k of one row; two chunks per iteration so that
+    // eight 16-byte loads are in flight per thread (the pass is HBM-bound)
+    auto load = [&](i64 idx, u32 (&v)[16]) {
         const int c = (int)(idx & 7);
         const int r = (int)((idx >> 3) & 127);
         const i64 rest = idx >> 10;
@@ -92,8 +94,7 @@ __device__ __forceinline__ void pack_a_body(const GemmArgs& g, uint8_t* __restri
         const i32 mb = (i32)(rest / KB);
         const i32 row = mb * BM + r;
         const i32 k0 = kb * BK + c * 16;
-        u32 v[16];
-        if (row < g.M) {
+        if (idx < total && row < g.M) {
             const u32* src = g.A + (i64)(g.a_row0 + row) * g.lda + k_lo + k0;
             if (((reinterpret_cast<uintptr_t>(src) & 15) == 0) && k0 + 16 <= K) {
                 const uint4* s4 = reinterpret_cast<const uint4*>(src);
@@ -113,6 +114,14 @@ __device__ __forceinline__ void pack_a_body(const GemmArgs& g, uint8_t* __restri
 #pragma unroll
             for (int e = 0; e < 16; ++e) v[e] = 0;
         }
+    };
+    auto store = [&](i64 idx, const u32 (&v)[16]) {
+        if (idx >= total) return;
+        const int c = (int)(idx & 7);
+        const int r = (int)((idx >> 3) & 127);
+        const i64 rest = idx >> 10;
+        const i32 kb = (i32)(rest % KB);
+        const i32 mb = (i32)(rest / KB);
         const int pc = c ^ (r & 7);
 #pragma unroll
         for (int i = 0; i < L; ++i) {
@@ -128,6 +137,14 @@ __device__ __forceinline__ void pack_a_body(const GemmArgs& g, uint8_t* __restri
             uint8_t* dst = a2 + ((i64)mb * (L * KB) + (i64)i * KB + kb) * A_TILE + r * BK + pc * 16;
             *reinterpret_cast<uint4*>(dst) = o;
         }
+    };
+    const i64 step = (i64)nb * blockDim.x;
+    for (i64 idx = (i64)bid * blockDim.x + threadIdx.x; idx < total; idx += 2 * step) {
+        u32 v0[16], v1[16];
+        load(idx, v0);
+        load(idx + step, v1);
+        store(idx, v0);
+        store(idx + step, v1);
     }
 }
 
@@ -191,7 +208,8 @@ __device__ __forceinline__ void pack_b_body(const GemmArgs& g, uint8_t* __restri
             for (int i = 0; i < L; ++i) {
                 u32 w[16];
 #pragma unroll
-                for (int t = 0; t < 16; ++t) w[t] = (i == 0) ? v[t] : mulmod(v[t], sc[i], g.f);
+                for (int t = 0; t < 16; ++t)  // L = 2: p <= 2^16, the product fits 32 bits
+                    w[t] = (i == 0) ? v[t] : (L == 2 ? mulmod_sp(v[t], sc[i], g.f) : mulmod(v[t], sc[i], g.f));
                 uint8_t* tile = b2 + ((i64)nb * (L * KB) + (i64)i * KB + kb) * B_TILE;
 #pragma unroll
                 for (int j = 0; j < L; ++j) {
