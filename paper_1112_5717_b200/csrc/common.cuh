@@ -154,6 +154,16 @@ struct Dyn {
 __host__ __device__ inline Dyn dyn_c(i32 c) { return Dyn{-1, c}; }
 __host__ __device__ inline Dyn dyn_rp(i32 i, i32 c = 0) { return Dyn{i, c}; }
 
+// Programmatic dependent launch (launch_pdl in runtime.h).  Protocol of every
+// kernel launched that way: touch no global memory produced by the previous
+// kernel before pdl_wait() (which waits for that grid's completion and memory
+// flush), and call pdl_trigger() only after it -- so when a kernel's CTAs
+// start early, every kernel before its predecessor has completed.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ i32 dyn_eval(const Dyn& d, const i32* rp) {
     return (d.idx >= 0 ? __ldcg(rp + d.idx) : 0) + d.cst;
 }

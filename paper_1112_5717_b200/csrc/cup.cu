@@ -179,6 +179,9 @@ void CupEngine::panel(i32 i0, i32 b) {
     panel_window(a, s_);
     fork_to(s_, s3_);                       // U^{-1} beside the tail
     panel_uinv(a, s3_);
+    // a joined side-stream kernel may become a programmatic predecessor of the
+    // tail and still be writing these rows when its CTAs start: no prefetch then
+    a.prefetch = pending_joins_.empty() ? 1 : 0;
     for (cudaEvent_t e : pending_joins_) RL_CUDA_CHECK(cudaStreamWaitEvent(s_, e, 0));
     pending_joins_.clear();                 // the wide Schur update of these rows
     panel_tail(a, s_);

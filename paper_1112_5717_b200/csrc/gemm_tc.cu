@@ -235,6 +235,8 @@ template <int L>
 __global__ void __launch_bounds__(256) pack_kernel(GemmArgs g, uint8_t* __restrict__ a2,
                                                    uint8_t* __restrict__ b2, u32 s1, u32 s2, u32 s3,
                                                    int ga) {
+    pdl_wait();
+    pdl_trigger();
     if ((int)blockIdx.x < ga) pack_a_body<L>(g, a2, blockIdx.x, ga);
     else pack_b_body<L>(g, b2, s1, s2, s3, blockIdx.x - ga, gridDim.x - ga);
 }
@@ -274,6 +276,8 @@ __global__ void __launch_bounds__(NTHR, 1)
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    pdl_wait();
+    pdl_trigger();
 
     i32 K, N, k_lo, n_lo;
     dyn_shape(g, K, N, k_lo, n_lo);
@@ -489,7 +493,7 @@ void launch_tc(const GemmArgs& g, i64 Kmax, i64 Nmax, uint8_t* a2, uint8_t* b2, 
         const int ga = (int)std::max<i64>(1, std::min<i64>((awork + 255) / 256, (i64)nsm * 8));
         const int gb = (int)std::max<i64>(1, std::min<i64>(KB * 4 * NB, (i64)nsm * 8));
         RL_ONCE_MAX_SMEM(pack_kernel<L>);
-        pack_kernel<L><<<ga + gb, 256, 0, s>>>(g, a2, b2, sc[1], sc[2], sc[3], ga);
+        launch_pdl(pack_kernel<L>, dim3(ga + gb), dim3(256), 0, s, g, a2, b2, sc[1], sc[2], sc[3], ga);
         RL_CUDA_CHECK(cudaGetLastError());
     }
     if (phase == 0) return;
@@ -501,7 +505,8 @@ void launch_tc(const GemmArgs& g, i64 Kmax, i64 Nmax, uint8_t* a2, uint8_t* b2, 
         attr_set = true;
     }
     RL_ONCE_MAX_SMEM(gemm_tc_kernel<L>);
-    gemm_tc_kernel<L><<<grid, NTHR, C_::SMEM, s>>>(g, a2, b2, sc[1], sc[2], sc[3]);
+    launch_pdl(gemm_tc_kernel<L>, dim3(grid), dim3(NTHR), C_::SMEM, s, g, (const uint8_t*)a2, (const uint8_t*)b2,
+               sc[1], sc[2], sc[3]);
     RL_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -547,6 +552,8 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
     constexpr int SK = 64, SP_ = 68, RT = TM / 16;
     __shared__ __align__(16) u32 As[TM][SP_];   // [row][k]
     __shared__ __align__(16) u32 Bs[SK][SP_];   // [k][col]
+    pdl_wait();
+    pdl_trigger();
     __shared__ i32 s_brow[SK];
     i32 K, N, k_lo, n_lo;
     dyn_shape(g, K, N, k_lo, n_lo);
@@ -656,13 +663,13 @@ void gemm_simt(const GemmArgs& g, i64 Kmax, i64 Nmax, cudaStream_t s) {
     if (((g.M + 63) / 64) * nb < num_sms()) {
         const i64 tiles = ((g.M + 15) / 16) * nb;
         const int grid = (int)std::min<i64>(tiles, g.max_ctas > 0 ? (i64)g.max_ctas : (i64)num_sms() * 8);
-        if (sp) gemm_simt_kernel<true, 16><<<std::max(grid, 1), 256, 0, s>>>(g);
-        else gemm_simt_kernel<false, 16><<<std::max(grid, 1), 256, 0, s>>>(g);
+        if (sp) launch_pdl(gemm_simt_kernel<true, 16>, dim3(std::max(grid, 1)), dim3(256), 0, s, g);
+        else launch_pdl(gemm_simt_kernel<false, 16>, dim3(std::max(grid, 1)), dim3(256), 0, s, g);
     } else {
         const i64 tiles = ((g.M + 63) / 64) * nb;
         const int grid = (int)std::min<i64>(tiles, g.max_ctas > 0 ? (i64)g.max_ctas : (i64)num_sms() * 8);
-        if (sp) gemm_simt_kernel<true, 64><<<std::max(grid, 1), 256, 0, s>>>(g);
-        else gemm_simt_kernel<false, 64><<<std::max(grid, 1), 256, 0, s>>>(g);
+        if (sp) launch_pdl(gemm_simt_kernel<true, 64>, dim3(std::max(grid, 1)), dim3(256), 0, s, g);
+        else launch_pdl(gemm_simt_kernel<false, 64>, dim3(std::max(grid, 1)), dim3(256), 0, s, g);
     }
     RL_CUDA_CHECK(cudaGetLastError());
 }

@@ -95,6 +95,10 @@ struct PanelArgs {
     u32* uinv;     // PB x PB: inverse of this leaf's unit upper pivot block
     const uint16_t* inv_table;  // p < 2^16: inv_table[x] = x^{-1} mod p (else unused)
     Fp f;
+    // tail only: the launch has no cross-stream join, so its programmatic
+    // predecessor (the window) is the only kernel that may still run when its
+    // CTAs start -- the tile prefetch before pdl_wait() is then safe
+    int prefetch;
 };
 // inv_table[x] = x^{-1} mod p for x in [1, p) (p <= 65536), inv_table[0] = 0.
 void build_inv_table(uint16_t* table, u32 p, cudaStream_t s);

@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(256) panel_tail_kernel(PanelArgs a) {
     // columns >= c0 + b untouched; c0 = rp[i0] is older than the window).
     const i32 c0_pre = __ldcg(a.rp + a.i0);
     const i32 cb_pre = vec ? ((c0_pre + a.b) & ~3) : c0_pre + a.b;
-    const bool pre = vec && blockIdx.x < gridDim.x - 1 && cb_pre + (i32)blockIdx.x * TT < a.N;
+    const bool pre = a.prefetch && vec && blockIdx.x < gridDim.x - 1 && cb_pre + (i32)blockIdx.x * TT < a.N;
     if (pre) {
         const i32 cb = cb_pre + blockIdx.x * TT;
 #pragma unroll
@@ -274,7 +274,8 @@ __global__ void __launch_bounds__(256) panel_tail_kernel(PanelArgs a) {
             cp_async16z(&Ps[i][cc], nb ? a.A + (i64)(a.i0 + i) * a.lda + cb + cc : a.A, nb);
         }
     }
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    pdl_wait();
+    pdl_trigger();
     const i32 c0 = ps->c0, W = ps->W, b = ps->b, rt = ps->r;
     const u64 dead = ps->dead_mask;
     const bool pre_ok = pre && ps->spec && rt == a.b && c0 == c0_pre && dead == 0;

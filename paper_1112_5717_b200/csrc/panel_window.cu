@@ -499,6 +499,15 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
     PanelScratch* ps = a.ps;
     const Fp f = a.f;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // the inverse table is static: start its copy before waiting for the
+    // previous kernel (programmatic dependent launch)
+    if (SP) {  // 128 KB inverse table
+        const uint4* src = reinterpret_cast<const uint4*>(a.inv_table);
+        uint4* dst = reinterpret_cast<uint4*>(dsm + PB * RP * 4);
+#pragma unroll 4
+        for (int e = tid; e < 65536 * 2 / 16; e += blockDim.x) cp_async16(dst + e, src + e);
+    }
+    pdl_wait();
     const i32 c0 = __ldcg(a.rp + a.i0);
     const i32 W = a.N - c0;
     const int b = a.b;
@@ -517,15 +526,10 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
             ps->spec = 0;
             ps->dead_mask = 0;
         }
+        cp_async_wait_all();
         return;
     }
     const int w = W < PW ? W : PW;
-    if (SP) {  // 128 KB inverse table
-        const uint4* src = reinterpret_cast<const uint4*>(a.inv_table);
-        uint4* dst = reinterpret_cast<uint4*>(dsm + PB * RP * 4);
-#pragma unroll 4
-        for (int e = tid; e < 65536 * 2 / 16; e += blockDim.x) cp_async16(dst + e, src + e);
-    }
     u64 acc[RW][6];
 #pragma unroll
     for (int s = 0; s < RW; ++s) {
@@ -666,7 +670,7 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
     // the tail kernel (a programmatic dependent launch) may start now: it only
     // prefetches columns this kernel does not write on the speculative path,
     // and waits for this grid's completion before reading anything else
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    pdl_trigger();
     const int rt = r;
     // (the speculative path made no transposition: both loops are identities)
     if (!spec && warp == 1 && lane == 0) {  // window column permutation
@@ -817,8 +821,8 @@ void panel_window(const PanelArgs& a, cudaStream_t s) {
     }
     RL_ONCE_MAX_SMEM(panel_window_kernel<true>);
     RL_ONCE_MAX_SMEM(panel_window_kernel<false>);
-    if (sp) panel_window_kernel<true><<<1, NW * 32, smem, s>>>(a);
-    else panel_window_kernel<false><<<1, NW * 32, smem, s>>>(a);
+    if (sp) launch_pdl(panel_window_kernel<true>, dim3(1), dim3(NW * 32), smem, s, a);
+    else launch_pdl(panel_window_kernel<false>, dim3(1), dim3(NW * 32), smem, s, a);
     RL_CUDA_CHECK(cudaGetLastError());
 }
 

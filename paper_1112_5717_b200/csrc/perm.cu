@@ -77,6 +77,8 @@ __device__ __forceinline__ void swap_job(const SwapArgs& a, i32* list, int* warp
 __global__ void __launch_bounds__(256) swaps_kernel(SwapJobs jobs) {
     __shared__ i32 list[256];
     __shared__ int warp_cnt[8];
+    pdl_wait();
+    pdl_trigger();
     for (int q = 0; q < jobs.n; ++q) swap_job(jobs.job[q], list, warp_cnt);
 }
 
@@ -84,6 +86,8 @@ __global__ void __launch_bounds__(256) compact_kernel(u32* A, i64 lda, i32 m, i3
                                                       const i32* rrp) {
     __shared__ i32 list[256];
     __shared__ int warp_cnt[8];
+    pdl_wait();
+    pdl_trigger();
     const i32 r = __ldcg(rp + m);
     const i32 c = blockIdx.x * blockDim.x + threadIdx.x;
     for (i32 j0 = 0; j0 < r; j0 += 256) {
@@ -125,7 +129,7 @@ void apply_swaps(const SwapJobs& jobs, cudaStream_t s) {
     if (jobs.n <= 0 || mmax <= 0) return;
     const int grid = std::max(1, std::min((mmax + 255) / 256, 2 * num_sms()));
     RL_ONCE_MAX_SMEM(swaps_kernel);
-    swaps_kernel<<<grid, 256, 0, s>>>(jobs);
+    launch_pdl(swaps_kernel, dim3(grid), dim3(256), 0, s, jobs);
     RL_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -133,7 +137,7 @@ void compact_u_rows(u32* A, i64 lda, i32 m, i32 n, const i32* rp, const i32* rrp
                     cudaStream_t s) {
     if (m <= 0 || n <= 0) return;
     RL_ONCE_MAX_SMEM(compact_kernel);
-    compact_kernel<<<(n + 255) / 256, 256, 0, s>>>(A, lda, m, n, rp, rrp);
+    launch_pdl(compact_kernel, dim3((n + 255) / 256), dim3(256), 0, s, A, lda, m, n, rp, rrp);
     RL_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -1,5 +1,6 @@
 // runtime.h -- host-side runtime helpers: errors, device properties.
 #pragma once
+#include <utility>
 #include <cuda_runtime.h>
 
 #include <stdexcept>
@@ -38,6 +39,26 @@ inline void prefer_max_smem(F* kernel) {
             once_ = true;                 \
         }                                 \
     } while (0)
+
+// Launch as a programmatic dependent of the previous kernel on the stream (the
+// kernel must follow the pdl_wait/pdl_trigger protocol, common.cuh): its CTAs
+// may start while the predecessor finishes, hiding launch latency inside the
+// captured graph's dependent chains.
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    RL_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 
 // Growable device scratch buffer (workspaces of the host-pointer entry points
 // and of the dense/triangular helpers; callers hold the C-ABI mutex).

@@ -62,6 +62,8 @@ __global__ void __launch_bounds__(256 * KS) trsm_node_kernel(TrsmNodeArgs a) {
     const int tid = threadIdx.x;
     const int kg = tid >> 8, t8 = tid & 255;
     const int rg = t8 >> 4, cg = t8 & 15;
+    pdl_wait();
+    pdl_trigger();
     i32 lo[TN_MAXLEAF], hi[TN_MAXLEAF];
 #pragma unroll
     for (int l = 0; l < TN_MAXLEAF; ++l) {
@@ -284,7 +286,7 @@ void launch_node(const TrsmNodeArgs& a, cudaStream_t s) {
     const int per_sm = nblk >= 6 ? 1 : (nblk >= 3 ? 2 : 4);
     const int rows = a.M + (a.ninv ? NINV_LD : 0);  // host bound; the kernel uses the live nJ
     const int grid = std::max(1, std::min((rows + TM - 1) / TM, per_sm * num_sms()));
-    trsm_node_kernel<SP, TR, KS><<<grid, 256 * KS, smem, s>>>(a);
+    launch_pdl(trsm_node_kernel<SP, TR, KS>, dim3(grid), dim3(256 * KS), smem, s, a);
     RL_CUDA_CHECK(cudaGetLastError());
 }
 
