@@ -214,6 +214,21 @@ __device__ void panel_fallback(const PanelArgs& a, u32* red_buf) {
     __syncthreads();
 }
 
+// Legacy warp-level tensor-core MMA: D(16x8, s32) += A(16x32, u8, row) *
+// B(32x8, u8, col).  Fragments (PTX ISA, mma.m16n8k32 .u8): lane = 4*g + t;
+// a0/a2: row g, a1/a3: row g+8, bytes k = 4t..4t+3 (+16 for a2/a3);
+// b0/b1: column g, bytes k = 4t..4t+3 (+16 for b1); d0/d1: row g, columns
+// 2t, 2t+1; d2/d3: row g+8.  About 2 K u8 MAC/clk/SM here (tools/imma_rate.cu),
+// against 23.6 IMAD.WIDE: the p < 2^16 tail runs on it with 2 byte limbs.
+__device__ __forceinline__ void imma16832(int (&d)[4], const u32 (&a)[4], const u32 (&b)[2]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+constexpr int BPI = 80;  // byte-plane row pitch (bytes): conflict-free fragment loads
+
 // acc[x][.] += Minv[ty + 16x][k] * P[k][4tx .. 4tx+3] for k in [k0, k1), rows x >= X0.
 template <bool SP, int X0>
 __device__ __forceinline__ void tail_mac(u64 (&acc)[4][4], const u32 (*Mi)[MIP],
@@ -248,6 +263,13 @@ __global__ void __launch_bounds__(256) panel_tail_kernel(PanelArgs a) {
     extern __shared__ __align__(16) u32 tsm[];
     u32 (*Mi)[MIP] = reinterpret_cast<u32 (*)[MIP]>(tsm);                     // [PB][MIP]
     u32 (*Ps)[TT + 4] = reinterpret_cast<u32 (*)[TT + 4]>(tsm + PB * MIP);    // [PB][TT+4]
+    // p < 2^16: byte planes of Minv (row-major, k contiguous) and of the P tile
+    // (transposed: column-major, k contiguous) for the tensor-core product
+    uint8_t* planes = reinterpret_cast<uint8_t*>(tsm + PB * MIP + PB * (TT + 4));
+    uint8_t (*Ml)[BPI] = reinterpret_cast<uint8_t (*)[BPI]>(planes);
+    uint8_t (*Mh)[BPI] = reinterpret_cast<uint8_t (*)[BPI]>(planes + PB * BPI);
+    uint8_t (*Pl)[BPI] = reinterpret_cast<uint8_t (*)[BPI]>(planes + 2 * PB * BPI);
+    uint8_t (*Ph)[BPI] = reinterpret_cast<uint8_t (*)[BPI]>(planes + 2 * PB * BPI + TT * BPI);
     u32 (*Us)[PB + 1] = reinterpret_cast<u32 (*)[PB + 1]>(tsm);               // uinv scratch
     u32 (*Xs)[PB + 1] = reinterpret_cast<u32 (*)[PB + 1]>(tsm + PB * (PB + 1));
     u32 (*Ts)[PB + 1] = reinterpret_cast<u32 (*)[PB + 1]>(tsm + 2 * PB * (PB + 1));
@@ -291,9 +313,21 @@ __global__ void __launch_bounds__(256) panel_tail_kernel(PanelArgs a) {
             leaf_uinv<SP>(a, c0, rt, Us, Xs, Ts);
         }
     } else if (W > 0) {
+        if (SP) {
 #pragma unroll
-        for (int e = tid; e < PB * PB / 4; e += blockDim.x)
-            cp_async16(&Mi[e / (PB / 4)][4 * (e % (PB / 4))], &ps->Minv[e / (PB / 4)][4 * (e % (PB / 4))]);
+            for (int e = tid; e < PB * PB / 4; e += blockDim.x) {
+                const int i = e / (PB / 4), k = 4 * (e % (PB / 4));
+                const uint4 v = __ldcg(reinterpret_cast<const uint4*>(&ps->Minv[i][k]));
+                *reinterpret_cast<u32*>(&Ml[i][k]) =
+                    (v.x & 0xff) | (v.y & 0xff) << 8 | (v.z & 0xff) << 16 | (v.w & 0xff) << 24;
+                *reinterpret_cast<u32*>(&Mh[i][k]) = (v.x >> 8 & 0xff) | (v.y >> 8 & 0xff) << 8 |
+                                                     (v.z >> 8 & 0xff) << 16 | (v.w >> 8 & 0xff) << 24;
+            }
+        } else {
+#pragma unroll
+            for (int e = tid; e < PB * PB / 4; e += blockDim.x)
+                cp_async16(&Mi[e / (PB / 4)][4 * (e % (PB / 4))], &ps->Minv[e / (PB / 4)][4 * (e % (PB / 4))]);
+        }
         const int tx = tid & 15, ty = tid >> 4;
         const i32 col0 = c0 + rt;
         // 16-byte path: tiles start at col0 rounded down to 4 columns (the
@@ -326,6 +360,77 @@ __global__ void __launch_bounds__(256) panel_tail_kernel(PanelArgs a) {
 #ifdef RL_TRACE
             t_loaded = t_ld;
 #endif
+            if constexpr (SP) {
+                // P tile -> transposed byte planes (column c: 64 k bytes)
+#pragma unroll
+                for (int e = tid; e < TT * (PB / 4); e += blockDim.x) {
+                    const int c = e % TT, k = 4 * (e / TT);
+                    const u32 v0 = Ps[k][c], v1 = Ps[k + 1][c], v2 = Ps[k + 2][c], v3 = Ps[k + 3][c];
+                    *reinterpret_cast<u32*>(&Pl[c][k]) =
+                        (v0 & 0xff) | (v1 & 0xff) << 8 | (v2 & 0xff) << 16 | (v3 & 0xff) << 24;
+                    *reinterpret_cast<u32*>(&Ph[c][k]) = (v0 >> 8 & 0xff) | (v1 >> 8 & 0xff) << 8 |
+                                                         (v2 >> 8 & 0xff) << 16 | (v3 >> 8 & 0xff) << 24;
+                }
+                __syncthreads();
+                // warp w: rows 16 (w & 3) .., columns 32 (w >> 2) .. (four n8 tiles);
+                // V = S0 + 2^8 S1 + 2^16 S2 with S0 = lo*lo, S1 = lo*hi + hi*lo, S2 = hi*hi
+                const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, tg = lane & 3;
+                const int rs = warp & 3, chn = warp >> 2;
+                int S0[4][4] = {}, S1[4][4] = {}, S2[4][4] = {};
+#pragma unroll
+                for (int ks = 0; ks < 2; ++ks) {
+                    if (ks == 1 && rs < 2) break;  // Minv rows < 32 vanish for k >= 32
+                    const int kk = 32 * ks + 4 * tg;
+                    const int r0 = 16 * rs + g;
+                    const u32 al[4] = {*reinterpret_cast<const u32*>(&Ml[r0][kk]),
+                                       *reinterpret_cast<const u32*>(&Ml[r0 + 8][kk]),
+                                       *reinterpret_cast<const u32*>(&Ml[r0][kk + 16]),
+                                       *reinterpret_cast<const u32*>(&Ml[r0 + 8][kk + 16])};
+                    const u32 ah[4] = {*reinterpret_cast<const u32*>(&Mh[r0][kk]),
+                                       *reinterpret_cast<const u32*>(&Mh[r0 + 8][kk]),
+                                       *reinterpret_cast<const u32*>(&Mh[r0][kk + 16]),
+                                       *reinterpret_cast<const u32*>(&Mh[r0 + 8][kk + 16])};
+#pragma unroll
+                    for (int nt = 0; nt < 4; ++nt) {
+                        const int n = 32 * chn + 8 * nt + g;
+                        const u32 bl[2] = {*reinterpret_cast<const u32*>(&Pl[n][kk]),
+                                           *reinterpret_cast<const u32*>(&Pl[n][kk + 16])};
+                        const u32 bh[2] = {*reinterpret_cast<const u32*>(&Ph[n][kk]),
+                                           *reinterpret_cast<const u32*>(&Ph[n][kk + 16])};
+                        imma16832(S0[nt], al, bl);
+                        imma16832(S1[nt], al, bh);
+                        imma16832(S1[nt], ah, bl);
+                        imma16832(S2[nt], ah, bh);
+                    }
+                }
+                RL_STAMP(t_m);
+#ifdef RL_TRACE
+                t_mac = t_m;
+#endif
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int i = 16 * rs + g + 8 * h;
+                        if (i >= b) continue;
+                        const i32 cx = cb + 32 * chn + 8 * nt + 2 * tg;
+                        const u32 v0 = red_sp((u64)(u32)S0[nt][2 * h] + ((u64)(u32)S1[nt][2 * h] << 8) +
+                                                  ((u64)(u32)S2[nt][2 * h] << 16), f);
+                        const u32 v1 = red_sp((u64)(u32)S0[nt][2 * h + 1] + ((u64)(u32)S1[nt][2 * h + 1] << 8) +
+                                                  ((u64)(u32)S2[nt][2 * h + 1] << 16), f);
+                        const bool ok0 = cx >= col0 && cx < a.N, ok1 = cx + 1 >= col0 && cx + 1 < a.N;
+                        u32* out = a.A + (i64)(a.i0 + i) * a.lda + cx;
+                        const bool isdead = (dead >> i) & 1;
+                        if (isdead) bad |= (ok0 ? v0 : 0u) | (ok1 ? v1 : 0u);
+                        if (vec && ok0 && ok1) {
+                            *reinterpret_cast<uint2*>(out) = make_uint2(v0, v1);
+                        } else {
+                            if (ok0) out[0] = v0;
+                            if (ok1) out[1] = v1;
+                        }
+                    }
+                }
+            } else {
             // rows ty + 16x interleave short and long rows of the triangle
             u64 acc[4][4];
 #pragma unroll
@@ -365,6 +470,7 @@ __global__ void __launch_bounds__(256) panel_tail_kernel(PanelArgs a) {
                         }
                     }
                 }
+            }
             }
         }
     }
@@ -493,7 +599,8 @@ void panel_uinv(const PanelArgs& a, cudaStream_t s) {
 
 void panel_tail(const PanelArgs& a, cudaStream_t s) {
     // tiles: Minv + P tile; the U^{-1} CTA: U, X, T (3 blocks of PB x (PB+1))
-    const size_t smem = sizeof(u32) * std::max<size_t>(PB * MIP + PB * (TT + 4), 3 * PB * (PB + 1));
+    const size_t smem = std::max<size_t>(sizeof(u32) * (PB * MIP + PB * (TT + 4)) + 2 * (PB + TT) * BPI,
+                                         sizeof(u32) * 3 * PB * (PB + 1));
     static bool attr = false;
     if (!attr) {
         RL_CUDA_CHECK(cudaFuncSetAttribute(panel_tail_kernel<true>,
