@@ -164,6 +164,19 @@ __device__ __forceinline__ void pdl_trigger() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// Legacy warp-level tensor-core MMA: D(16x8, s32) += A(16x32, u8, row) *
+// B(32x8, u8, col).  Fragments (PTX ISA, mma.m16n8k32 .u8): lane = 4*g + t;
+// a0/a2: row g, a1/a3: row g+8, bytes k = 4t..4t+3 (+16 for a2/a3);
+// b0/b1: column g, bytes k = 4t..4t+3 (+16 for b1); d0/d1: row g, columns
+// 2t, 2t+1; d2/d3: row g+8.  About 2 K u8 MAC/clk/SM here (tools/imma_rate.cu),
+// against 23.6 IMAD.WIDE: the p < 2^16 tail runs on it with 2 byte limbs.
+__device__ __forceinline__ void imma16832(int (&d)[4], const u32 (&a)[4], const u32 (&b)[2]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
 __device__ __forceinline__ i32 dyn_eval(const Dyn& d, const i32* rp) {
     return (d.idx >= 0 ? __ldcg(rp + d.idx) : 0) + d.cst;
 }

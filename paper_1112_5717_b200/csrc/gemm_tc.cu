@@ -32,6 +32,7 @@
 namespace rl {
 
 namespace {
+constexpr int BPI_G = 80;  // byte-plane row pitch (bytes), conflict-free mma fragments
 
 #ifdef RL_GEMM_TRACE  // tools/gemm_trace.cu: per-CTA phase timestamps
 __device__ unsigned long long g_gemm_trace[1024][8];
@@ -542,6 +543,159 @@ void gemm_tc(const GemmArgs& g, int L, i64 Kmax, i64 Nmax, uint8_t* a2, uint8_t*
 
 // ------------------------------------------------------------ SIMT fallback
 namespace {
+// p <= 2^16: the same contract as gemm_simt_kernel on the legacy tensor cores.
+// Per K chunk of 64 the operands are loaded straight into byte planes (A row-
+// major, B transposed, both k-contiguous; lo and hi byte of every element), and
+// every warp runs mma.sync m16n8k32 (u8 x u8 -> s32) over the four limb
+// products: S0 = lo*lo, S1 = lo*hi + hi*lo, S2 = hi*hi, each at most
+// 2*64*255^2 < 2^31 per chunk, folded into a 64-bit sum S0 + 2^8 S1 + 2^16 S2 per
+// chunk and reduced once.  TM = 64: warp = (16-row slab, 32 columns), four n8
+// tiles; TM = 16: warp = 8 columns, one n8 tile.
+template <int TM>
+__global__ void __launch_bounds__(256) gemm_imma_kernel(GemmArgs g) {
+    constexpr int SK = 64, NTW = TM == 64 ? 4 : 1;
+    __shared__ __align__(16) uint8_t Al[TM][BPI_G], Ah[TM][BPI_G];  // [row][k]
+    __shared__ __align__(16) uint8_t Bl[64][BPI_G], Bh[64][BPI_G];  // [col][k]
+    __shared__ i32 s_brow[SK];
+    pdl_wait();
+    pdl_trigger();
+    i32 K, N, k_lo, n_lo;
+    dyn_shape(g, K, N, k_lo, n_lo);
+    if (K <= 0 || N <= 0 || g.M <= 0) return;
+    const i32 MB = (g.M + TM - 1) / TM, NB = (N + 63) / 64;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tg = lane & 3;
+    const int rs = TM == 64 ? (warp & 3) : 0;
+    const int cbw = TM == 64 ? 32 * (warp >> 2) : 8 * warp;
+    const Fp f = g.f;
+    const i32 bcol0 = g.b_from0 ? 0 : n_lo;
+    const bool avec = ((g.lda & 3) == 0) && (((reinterpret_cast<uintptr_t>(g.A) >> 2) + g.a_row0 * g.lda + k_lo) % 4 == 0);
+    const bool bvec = ((g.ldb & 3) == 0) && (((reinterpret_cast<uintptr_t>(g.B) >> 2) + bcol0) % 4 == 0);
+    auto lo4 = [](uint4 v) {
+        return (v.x & 0xff) | (v.y & 0xff) << 8 | (v.z & 0xff) << 16 | (v.w & 0xff) << 24;
+    };
+    auto hi4 = [](uint4 v) {
+        return (v.x >> 8 & 0xff) | (v.y >> 8 & 0xff) << 8 | (v.z >> 8 & 0xff) << 16 | (v.w >> 8 & 0xff) << 24;
+    };
+    for (i32 tile = blockIdx.x; tile < MB * NB; tile += gridDim.x) {
+        const i32 mb = tile % MB, nb = tile / MB;
+        u64 acc[NTW][4];
+#pragma unroll
+        for (int t = 0; t < NTW; ++t)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[t][e] = 0;
+        for (i32 k0 = 0; k0 < K; k0 += SK) {
+            __syncthreads();
+            if (tid < SK) {
+                const i32 k = k0 + tid;
+                s_brow[tid] = k < K ? (g.gather ? __ldg(g.gather + k_lo + k) : (g.b_from0 ? k : k_lo + k)) : -1;
+            }
+            // A: item (row r, 16 k) -> 16 bytes per plane
+            for (int e = tid; e < TM * 4; e += 256) {
+                const int r = e >> 2, kq = (e & 3) * 16;
+                const i32 row = mb * TM + r;
+                uint4 v[4];
+                const u32* src = g.A + (i64)(g.a_row0 + row) * g.lda + k_lo + k0 + kq;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int kk = k0 + kq + 4 * q;
+                    if (row < g.M && avec && kk + 4 <= K) {
+                        v[q] = __ldcg(reinterpret_cast<const uint4*>(src + 4 * q));
+                    } else {
+                        u32 t[4];
+#pragma unroll
+                        for (int z = 0; z < 4; ++z) t[z] = (row < g.M && kk + z < K) ? __ldcg(src + 4 * q + z) : 0u;
+                        v[q] = make_uint4(t[0], t[1], t[2], t[3]);
+                    }
+                }
+                *reinterpret_cast<uint4*>(&Al[r][kq]) = make_uint4(lo4(v[0]), lo4(v[1]), lo4(v[2]), lo4(v[3]));
+                *reinterpret_cast<uint4*>(&Ah[r][kq]) = make_uint4(hi4(v[0]), hi4(v[1]), hi4(v[2]), hi4(v[3]));
+            }
+            __syncthreads();  // s_brow
+            // B: item (4 k, 4 n) -> column-major bytes
+            {
+                const int kq = (tid >> 4) * 4, nq = (tid & 15) * 4;
+                const i32 n = nb * 64 + nq;
+                uint4 v[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const i32 row = s_brow[kq + q];
+                    const u32* src = g.B + (i64)row * g.ldb + bcol0 + n;
+                    if (row >= 0 && bvec && n + 4 <= N) {
+                        v[q] = __ldcg(reinterpret_cast<const uint4*>(src));
+                    } else {
+                        u32 t[4];
+#pragma unroll
+                        for (int z = 0; z < 4; ++z) t[z] = (row >= 0 && n + z < N) ? __ldcg(src + z) : 0u;
+                        v[q] = make_uint4(t[0], t[1], t[2], t[3]);
+                    }
+                }
+                // transpose 4 x 4: column nq + c gets k bytes kq..kq+3
+                const uint4 c0 = make_uint4(v[0].x, v[1].x, v[2].x, v[3].x);
+                const uint4 c1 = make_uint4(v[0].y, v[1].y, v[2].y, v[3].y);
+                const uint4 c2 = make_uint4(v[0].z, v[1].z, v[2].z, v[3].z);
+                const uint4 c3 = make_uint4(v[0].w, v[1].w, v[2].w, v[3].w);
+                *reinterpret_cast<u32*>(&Bl[nq][kq]) = lo4(c0);
+                *reinterpret_cast<u32*>(&Bl[nq + 1][kq]) = lo4(c1);
+                *reinterpret_cast<u32*>(&Bl[nq + 2][kq]) = lo4(c2);
+                *reinterpret_cast<u32*>(&Bl[nq + 3][kq]) = lo4(c3);
+                *reinterpret_cast<u32*>(&Bh[nq][kq]) = hi4(c0);
+                *reinterpret_cast<u32*>(&Bh[nq + 1][kq]) = hi4(c1);
+                *reinterpret_cast<u32*>(&Bh[nq + 2][kq]) = hi4(c2);
+                *reinterpret_cast<u32*>(&Bh[nq + 3][kq]) = hi4(c3);
+            }
+            __syncthreads();
+            int S0[NTW][4] = {}, S1[NTW][4] = {}, S2[NTW][4] = {};
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+                const int kk = 32 * ks + 4 * tg;
+                const int r0 = 16 * rs + gq;
+                const u32 al[4] = {*reinterpret_cast<const u32*>(&Al[r0][kk]),
+                                   *reinterpret_cast<const u32*>(&Al[r0 + 8][kk]),
+                                   *reinterpret_cast<const u32*>(&Al[r0][kk + 16]),
+                                   *reinterpret_cast<const u32*>(&Al[r0 + 8][kk + 16])};
+                const u32 ah[4] = {*reinterpret_cast<const u32*>(&Ah[r0][kk]),
+                                   *reinterpret_cast<const u32*>(&Ah[r0 + 8][kk]),
+                                   *reinterpret_cast<const u32*>(&Ah[r0][kk + 16]),
+                                   *reinterpret_cast<const u32*>(&Ah[r0 + 8][kk + 16])};
+#pragma unroll
+                for (int t = 0; t < NTW; ++t) {
+                    const int n = cbw + 8 * t + gq;
+                    const u32 bl[2] = {*reinterpret_cast<const u32*>(&Bl[n][kk]),
+                                       *reinterpret_cast<const u32*>(&Bl[n][kk + 16])};
+                    const u32 bh[2] = {*reinterpret_cast<const u32*>(&Bh[n][kk]),
+                                       *reinterpret_cast<const u32*>(&Bh[n][kk + 16])};
+                    imma16832(S0[t], al, bl);
+                    imma16832(S1[t], al, bh);
+                    imma16832(S1[t], ah, bl);
+                    imma16832(S2[t], ah, bh);
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < NTW; ++t)
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    acc[t][e] += (u64)(u32)S0[t][e] + ((u64)(u32)S1[t][e] << 8) + ((u64)(u32)S2[t][e] << 16);
+        }
+#pragma unroll
+        for (int t = 0; t < NTW; ++t) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const i32 row = mb * TM + 16 * rs + gq + 8 * (e >> 1);
+                const i32 n = nb * 64 + cbw + 8 * t + 2 * tg + (e & 1);
+                if (row >= g.M || n >= N) continue;
+                u32* cp = g.C + (i64)(g.c_row0 + row) * g.ldc + n_lo + n;
+                const u32 r = red64(acc[t][e], f);
+                const u32 cv = g.beta == 0 ? 0u : (g.beta == 1 ? *cp : mulmod(*cp, g.beta, f));
+                u32 out;
+                if (g.alpha == f.p - 1) out = submod(cv, r, f);
+                else if (g.alpha == 1) out = addmod(cv, r, f);
+                else out = addmod(cv, mulmod(r, g.alpha, f), f);
+                *cp = out;
+            }
+        }
+    }
+}
+
 template <bool SMALLP, int TM>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
     // TM x 64 output tile per CTA iteration (TM = 64, or 16 for GEMMs with few
@@ -663,12 +817,12 @@ void gemm_simt(const GemmArgs& g, i64 Kmax, i64 Nmax, cudaStream_t s) {
     if (((g.M + 63) / 64) * nb < num_sms()) {
         const i64 tiles = ((g.M + 15) / 16) * nb;
         const int grid = (int)std::min<i64>(tiles, g.max_ctas > 0 ? (i64)g.max_ctas : (i64)num_sms() * 8);
-        if (sp) launch_pdl(gemm_simt_kernel<true, 16>, dim3(std::max(grid, 1)), dim3(256), 0, s, g);
+        if (sp) launch_pdl(gemm_imma_kernel<16>, dim3(std::max(grid, 1)), dim3(256), 0, s, g);
         else launch_pdl(gemm_simt_kernel<false, 16>, dim3(std::max(grid, 1)), dim3(256), 0, s, g);
     } else {
         const i64 tiles = ((g.M + 63) / 64) * nb;
         const int grid = (int)std::min<i64>(tiles, g.max_ctas > 0 ? (i64)g.max_ctas : (i64)num_sms() * 8);
-        if (sp) launch_pdl(gemm_simt_kernel<true, 64>, dim3(std::max(grid, 1)), dim3(256), 0, s, g);
+        if (sp) launch_pdl(gemm_imma_kernel<64>, dim3(std::max(grid, 1)), dim3(256), 0, s, g);
         else launch_pdl(gemm_simt_kernel<false, 64>, dim3(std::max(grid, 1)), dim3(256), 0, s, g);
     }
     RL_CUDA_CHECK(cudaGetLastError());
