@@ -1,0 +1,279 @@
+"""Multi-GPU CUP of ONE large matrix (config 5): 1D block-cyclic column tiles.
+
+SURVEY.md 8(e): the columns of the m x n matrix are cut into tiles of ``tile``
+columns; rank g owns the tiles t = g (mod world).  Rows are not split.  Each
+rank keeps its tiles as one local row-major m x n_g matrix (columns in
+increasing global position, so "global position >= c" is a suffix of the local
+columns).  The factorization walks row blocks R = rows [i0, i0 + b):
+
+1. every rank receives the active part of R (columns [r, n) in the current
+   column order, r = rank so far) -- one NCCL broadcast per owning rank;
+2. every rank factors R redundantly with the single-GPU CUP engine
+   (``rl_cup_u32_dev``): rank r_t, row profile, the block's column permutation
+   sigma_t, and R's packed [C\\U] block (the b x (n - r) CUP is the serial part);
+3. sigma_t is applied to the columns of the other rows (the transpositions of
+   the reference's ``perm_apply_cols``, factor.cpp:49-50/perm.cpp:115-125);
+   a column whose source lives on another rank travels by an all-reduce of a
+   zero-padded column buffer (rare: sigma_t = id for generic inputs);
+4. the U rows of R move to global rows [r, r + r_t) on every rank's columns
+   (the reference's U-row shift, factor.cpp:62-70, applied per step);
+5. the rows below R receive their C columns G = B1 * U11^{-1} (``trsm``,
+   factor.cpp:45-46), B1 broadcast by the owners of columns [r, r + r_t);
+6. every rank updates its own columns right of the pivots:
+   B2 <- B2 - G * U12 (the Schur complement, ``mm``, factor.cpp:51-53) -- the
+   tensor-core GEMM, embarrassingly parallel over the column tiles.
+
+The result is bit-exact with ``ranklab::cup`` (factor.cpp:30-85): with the
+reference's pivot rule (first nonzero of each row in the current column order)
+the packed [C\\U], the row profile and sigma are unique, and the row-block
+sweep is the same elimination in a different grouping (SURVEY.md 8(c),
+"iterative formulation").  The data path's collectives are the per-owner
+broadcasts of R and B1 and, for non-trivial sigma_t, the column exchange.
+
+Compute goes through ``ops`` (default :class:`DeviceOps`, the C ABI of
+libranklab_gpu.so on the rank's GPU); communication through ``torch.distributed``
+(NCCL on B200; the CPU tests drive the same code over gloo with the oracle as
+``ops``).  Storage is int32 (bit pattern of the canonical uint32 values, p < 2^31).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+__all__ = ["ColumnTiles", "DeviceOps", "DistCupResult", "dist_cup", "scatter_columns",
+           "gather_columns", "random_matrix_local"]
+
+
+class ColumnTiles:
+    """1D block-cyclic map of n columns over ``world`` ranks, tiles of ``tile``."""
+
+    def __init__(self, n: int, world: int, tile: int):
+        assert n >= 0 and world >= 1 and tile >= 1
+        self.n, self.world, self.tile = n, world, tile
+        cols = np.arange(n, dtype=np.int64)
+        self.owner = (cols // tile) % world
+        self.gpos = [cols[self.owner == g] for g in range(world)]
+        self.local = np.zeros(n, np.int64)
+        for g in range(world):
+            self.local[self.gpos[g]] = np.arange(self.gpos[g].size)
+
+    def width(self, g: int) -> int:
+        return int(self.gpos[g].size)
+
+    def lsuf(self, g: int, c: int) -> int:
+        """First local column of rank g whose global position is >= c."""
+        return int(np.searchsorted(self.gpos[g], c, side="left"))
+
+
+@dataclass
+class DistCupResult:
+    rank: int
+    row_profile: np.ndarray
+    col_perm: np.ndarray
+    steps: int
+
+
+class DeviceOps:
+    """The compute of one rank: the C ABI of libranklab_gpu.so on torch CUDA
+    views (int32 storage, unit column stride, ld = stride(0)).  No fallback."""
+
+    def __init__(self, p: int):
+        from . import cup_dev, mm_dev, trsm_dev
+        self.p = int(p)
+        self._cup, self._mm, self._trsm = cup_dev, mm_dev, trsm_dev
+
+    @staticmethod
+    def _stream():
+        return torch.cuda.current_stream()
+
+    def cup(self, t: torch.Tensor):
+        m, n = t.shape
+        res = self._cup(t, m, n, self.p, lda=t.stride(0), stream=self._stream())
+        return res.rank, res.row_profile.astype(np.int64), res.col_perm.astype(np.int64)
+
+    def trsm_right_upper_unit(self, u: torch.Tensor, b: torch.Tensor) -> None:
+        """b <- b * U^{-1}, U unit upper (only the strict upper part of u is read)."""
+        m, k = b.shape
+        self._trsm(1, 0, 1, u, b, m, k, self.p, ldt=u.stride(0), ldb=b.stride(0),
+                   stream=self._stream())
+
+    def mm_sub(self, a: torch.Tensor, b: torch.Tensor, c: torch.Tensor) -> None:
+        """c <- c - a * b (mod p)."""
+        m, k = a.shape
+        n = b.shape[1]
+        self._mm(a, b, c, m, k, n, self.p - 1, 1, self.p, lda=a.stride(0), ldb=b.stride(0),
+                 ldc=c.stride(0), stream=self._stream())
+
+
+def _comm():
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        return dist, dist.get_rank(), dist.get_world_size()
+    return None, 0, 1
+
+
+class _Engine:
+    def __init__(self, x: torch.Tensor, m: int, n: int, tiles: ColumnTiles, ops, rank: int,
+                 dist):
+        self.x, self.m, self.n, self.tiles, self.ops = x, m, n, tiles, ops
+        self.rank, self.dist, self.world = rank, dist, tiles.world
+        dev = x.device
+        self.gpos_t = [torch.as_tensor(gp, dtype=torch.int64, device=dev) for gp in tiles.gpos]
+        self.mine = tiles.gpos[rank]
+
+    def gather_cols(self, ra: int, rb: int, c0: int, c1: int) -> torch.Tensor:
+        """Rows [ra, rb) x global columns [c0, c1) in global order, on every rank
+        (one broadcast from each rank owning a piece)."""
+        out = torch.empty((rb - ra, c1 - c0), dtype=self.x.dtype, device=self.x.device)
+        if rb == ra or c1 == c0:
+            return out
+        for g in range(self.world):
+            la, lb = self.tiles.lsuf(g, c0), self.tiles.lsuf(g, c1)
+            if lb == la:
+                continue
+            if g == self.rank:
+                piece = self.x[ra:rb, la:lb].contiguous()
+            else:
+                piece = torch.empty((rb - ra, lb - la), dtype=self.x.dtype, device=self.x.device)
+            if self.world > 1:
+                self.dist.broadcast(piece, src=g)
+            if self.world == 1:
+                out.copy_(piece)
+            else:
+                out.index_copy_(1, self.gpos_t[g][la:lb] - c0, piece)
+        return out
+
+    def put_cols(self, full: torch.Tensor, ra: int, c0: int) -> None:
+        """Write this rank's columns of ``full`` (rows [ra, ..), global columns
+        [c0, c0 + full.shape[1])) back into the local matrix."""
+        rows, w = full.shape
+        la, lb = self.tiles.lsuf(self.rank, c0), self.tiles.lsuf(self.rank, c0 + w)
+        if lb == la or rows == 0:
+            return
+        if self.world == 1:
+            self.x[ra:ra + rows, la:lb].copy_(full)
+        else:
+            self.x[ra:ra + rows, la:lb].copy_(
+                full.index_select(1, self.gpos_t[self.rank][la:lb] - c0))
+
+    def permute_cols(self, r: int, sig: np.ndarray, row_ranges) -> None:
+        """New column r + i = old column r + sig[i] on the given row ranges."""
+        moved = np.nonzero(sig != np.arange(sig.size))[0]
+        if moved.size == 0:
+            return
+        dst = r + moved
+        src = r + sig[moved]
+        t = self.tiles
+        for ra, rb in row_ranges:
+            if rb <= ra:
+                continue
+            if self.world == 1:
+                li = torch.as_tensor(t.local[src], device=self.x.device)
+                lo = torch.as_tensor(t.local[dst], device=self.x.device)
+                self.x[ra:rb].index_copy_(1, lo, self.x[ra:rb].index_select(1, li))
+                continue
+            buf = torch.zeros((rb - ra, moved.size), dtype=self.x.dtype, device=self.x.device)
+            own_src = np.nonzero(t.owner[src] == self.rank)[0]
+            if own_src.size:
+                li = torch.as_tensor(t.local[src[own_src]], device=self.x.device)
+                buf.index_copy_(1, torch.as_tensor(own_src, device=self.x.device),
+                                self.x[ra:rb].index_select(1, li))
+            self.dist.all_reduce(buf)  # one nonzero contributor per column: exact
+            own_dst = np.nonzero(t.owner[dst] == self.rank)[0]
+            if own_dst.size:
+                lo = torch.as_tensor(t.local[dst[own_dst]], device=self.x.device)
+                self.x[ra:rb].index_copy_(
+                    1, lo, buf.index_select(1, torch.as_tensor(own_dst, device=self.x.device)))
+
+    def shift_u_rows(self, r: int, i0: int, rt: int) -> None:
+        """U row j of the block (row i0 + j) moves to row r + j on the columns at
+        global position > r + j; the vacated entries become 0 (factor.cpp:62-70)."""
+        if i0 == r or rt == 0:
+            return
+        ls = self.tiles.lsuf(self.rank, r + 1)
+        if ls == self.x.shape[1]:
+            return
+        gp = self.gpos_t[self.rank][ls:]
+        j = torch.arange(rt, device=self.x.device, dtype=torch.int64)
+        mask = gp[None, :] > (r + j)[:, None]
+        src = self.x[i0:i0 + rt, ls:]
+        moved = torch.where(mask, src, torch.zeros_like(src))
+        src.masked_fill_(mask, 0)
+        dst = self.x[r:r + rt, ls:]
+        dst.copy_(torch.where(mask, moved, dst))
+
+
+def dist_cup(x: torch.Tensor, m: int, n: int, p: int, tiles: ColumnTiles, block: int = 1024,
+             ops=None) -> DistCupResult:
+    """In-place distributed CUP; ``x`` is this rank's m x tiles.width(rank)
+    local matrix (int32, row-major, contiguous).  Collective: every rank of the
+    default process group calls it with the same (m, n, p, tiles, block).
+
+    Returns the global rank, row profile and sigma (identical on every rank);
+    ``x`` holds this rank's columns of the packed [C\\U] (factor.hpp:10-14)."""
+    dist, rank, world = _comm()
+    assert world == tiles.world and tiles.n == n
+    assert x.dim() == 2 and x.shape == (m, tiles.width(rank)) and x.is_contiguous()
+    if ops is None:
+        ops = DeviceOps(p)
+    eng = _Engine(x, m, n, tiles, ops, rank, dist)
+    sigma = np.arange(n, dtype=np.int64)
+    rrp: list[np.ndarray] = []
+    r, i0, steps = 0, 0, 0
+    while i0 < m and r < n:
+        bt = min(block, m - i0)
+        w = n - r
+        R = eng.gather_cols(i0, i0 + bt, r, n)                  # (1)
+        rt, rrp_t, sig_t = ops.cup(R)                           # (2)
+        eng.put_cols(R, i0, r)
+        eng.permute_cols(r, sig_t, [(0, r), (i0 + bt, m)])       # (3)
+        sigma[r:] = sigma[r + sig_t]
+        eng.shift_u_rows(r, i0, rt)                             # (4)
+        mb = m - i0 - bt
+        if rt and mb:
+            B1 = eng.gather_cols(i0 + bt, m, r, r + rt)         # (5)
+            ops.trsm_right_upper_unit(R[:rt, :rt], B1)
+            eng.put_cols(B1, i0 + bt, r)
+            ls = tiles.lsuf(rank, r + rt)
+            if ls < x.shape[1]:                                 # (6)
+                ops.mm_sub(B1, x[r:r + rt, ls:], x[i0 + bt:, ls:])
+        rrp.append(i0 + rrp_t[:rt])
+        r += rt
+        i0 += bt
+        steps += 1
+    prof = np.concatenate(rrp) if rrp else np.zeros(0, np.int64)
+    return DistCupResult(r, prof.astype(np.uint32), sigma.astype(np.uint32), steps)
+
+
+def scatter_columns(a: torch.Tensor, tiles: ColumnTiles, rank: int) -> torch.Tensor:
+    """This rank's local matrix (contiguous) from a full m x n matrix."""
+    idx = torch.as_tensor(tiles.gpos[rank], device=a.device)
+    return a.index_select(1, idx).contiguous()
+
+
+def gather_columns(x: torch.Tensor, m: int, tiles: ColumnTiles) -> torch.Tensor:
+    """The full m x n matrix on every rank from the local pieces."""
+    dist, rank, world = _comm()
+    eng = _Engine(x, m, tiles.n, tiles, None, rank, dist)
+    return eng.gather_cols(0, m, 0, tiles.n)
+
+
+def random_matrix_local(m: int, n: int, seed: int, p: int, tiles: ColumnTiles, rank: int,
+                        device, chunk_rows: int = 2048) -> torch.Tensor:
+    """This rank's columns of ``random_matrix(m, n, seed, GF(p))`` (the reference
+    generator, reference.cpp:246-253), generated on the device in row chunks."""
+    from . import random_matrix_dev
+    x = torch.empty((m, tiles.width(rank)), dtype=torch.int32, device=device)
+    idx = torch.as_tensor(tiles.gpos[rank], device=device)
+    # the closed form depends on (i*n + j): generate full rows, keep our columns
+    buf = torch.empty((min(chunk_rows, max(m, 1)), n), dtype=torch.int32, device=device)
+    for i in range(0, m, chunk_rows):
+        h = min(chunk_rows, m - i)
+        # rows [i, i+h) of the m x n matrix = rows of an (i+h) x n matrix:
+        # the generator's counter is i*n + j + 1, so shift the seed instead
+        shift = (i * n * 0x9E3779B97F4A7C15) & ((1 << 64) - 1)
+        random_matrix_dev(buf[:h], h, n, (seed + shift) & ((1 << 64) - 1), p, lda=n)
+        x[i:i + h].copy_(buf[:h].index_select(1, idx))
+    return x
