@@ -24,9 +24,12 @@ W(m,n,r) = 2mnr - (m+n)r^2 + (2/3)r^3 (bench.cpp:12-13) at the returned rank.
 ``--impl reference`` times the reference's CPU cup on the host cores instead
 (T threads, each factoring its own 1024^2 random_matrix sample).
 
-Multi-GPU (torchrun, N>1): for the single-matrix workloads every rank factors
-its own replica ("replicas only": one C3 factorization is not sharded in this
-round), value = N * W / max-over-ranks time, scaling "weak".  ``--workload c4``
+Multi-GPU (torchrun, N>1): ``--workload c5`` factors ONE 65536^2 matrix
+distributed over the ranks (paper_1112_5717_b200/dist.py: 1D block-cyclic column
+tiles, NCCL broadcasts of each row block and of its pivot columns, local
+tensor-core Schur updates), value = W / max-over-ranks time, scaling "strong";
+``--dist`` runs the same driver at N = 1.  For C1-C3 every rank factors its
+own replica ("replicas only"), value = N * W / max-over-ranks time, scaling "weak".  ``--workload c4``
 shards the fixed batch of 4096 matrices across the ranks as contiguous slices
 (no collective on the data path), value = 4096 matrices / max-over-ranks time,
 scaling "strong".
@@ -57,9 +60,10 @@ WORKLOADS = {
                   desc="CUP of one 2048x2048 random_matrix(seed=3) over GF(65521)"),
     "c8192": dict(m=8192, n=8192, p=65521, seed=3,
                   desc="CUP of one 8192x8192 random_matrix(seed=3) over GF(65521)"),
-    "c5": dict(m=65536, n=65536, p=65521, seed=5,
-               desc="CUP of one 65536x65536 random_matrix(seed=5) over GF(65521) (17 GB, one GPU; "
-                    "N > 1 runs replicas, the 1D block-cyclic version is not built)"),
+    "c5": dict(m=65536, n=65536, p=65521, seed=5, tile=1024, block=1024,
+               desc="CUP of one 65536x65536 random_matrix(seed=5) over GF(65521) (17 GB); one "
+                    "GPU: the recursive engine; N > 1 (or --dist): 1D block-cyclic column tiles "
+                    "over the ranks, NCCL broadcasts of the row block and the pivot columns"),
     "c2": dict(m=4096, n=8192, p=65521, seed=2, inner=2048,
                desc="CUP of the config-2 4096x8192 rank-2048 matrix (L*R mod p, rows i=2 mod 3 "
                     "zeroed, rows shuffled by SplitMix64(seed+2))"),
@@ -435,6 +439,109 @@ def ours(args, rank, world, local_rank):
         dist.destroy_process_group()
 
 
+def ours_dist(args, rank, world, local_rank):
+    """One matrix distributed over the ranks by column tiles (dist.py)."""
+    import torch
+    import paper_1112_5717_b200 as G
+    from paper_1112_5717_b200 import dist as D
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    wl = WORKLOADS[args.workload]
+    m, n, p, seed = wl["m"], wl["n"], wl["p"], wl["seed"]
+    tile, block = wl.get("tile", 1024), wl.get("block", 1024)
+    tiles = D.ColumnTiles(n, world, tile)
+    stream = torch.cuda.current_stream()
+    pristine = D.random_matrix_local(m, n, seed, p, tiles, rank, "cuda")
+    x = torch.empty_like(pristine)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        x.copy_(pristine)
+        res = D.dist_cup(x, m, n, p, tiles, block=block)
+    barrier()
+    times = []
+    with ClockSampler(local_rank) as clk:
+        for i in range(args.steps):
+            x.copy_(pristine)                     # restore input (outside the events)
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            res = D.dist_cup(x, m, n, p, tiles, block=block)
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+        barrier()
+    t_local = torch.tensor([sum(times)], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    t_max = float(t_local.item())
+    r = res.rank
+    W = model_ops(m, n, r)
+    # launches: the row-block CUP plans (graph-replayed) + per-step trsm/GEMM/copies
+    launches = 0
+    i0, rr = 0, 0
+    quantum = D._roundup(D._roundup(n, 12) // 12, 64)
+    while i0 < m and rr < n:
+        bt = min(block, m - i0)
+        wp = min(n, D._roundup(n - rr, quantum))
+        launches += int(G.plan_stats(bt, wp, p)["launches"]) + 4
+        i0 += bt
+        rr += bt
+    # e2e: this rank's columns from pinned host memory, factor, back to the host
+    e2e = None
+    try:
+        host = torch.empty(pristine.shape, dtype=torch.int32, pin_memory=True)
+        host.copy_(pristine)
+        barrier()
+        t0 = time.perf_counter()
+        x.copy_(host, non_blocking=True)
+        D.dist_cup(x, m, n, p, tiles, block=block)
+        host.copy_(x, non_blocking=True)
+        barrier()
+        et = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        if dist is not None:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": W / float(et.item()), "unit": "mod-p ops/s",
+               "h2d_bytes_per_step": m * n * 4, "d2h_bytes_per_step": m * n * 4,
+               "ms_per_step": float(et.item()) * 1e3, "steps": 1,
+               "path": "pinned host columns -> dist_cup (every rank) -> host; max over ranks"}
+        del host
+    except Exception as e:  # pragma: no cover
+        e2e = {"error": str(e)}
+    if rank == 0:
+        L = limbs(p)
+        line = {
+            "metric": METRIC, "value": W * args.steps / t_max, "unit": "mod-p ops/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": f"u32 in GF({p}); u8 limbs x{L} on int8 tensor cores (s32 acc, exact)",
+            "data": "synthetic",
+            "config": {"workload": args.workload, "desc": wl["desc"], "m": m, "n": n, "p": p,
+                       "seed": seed, "rank": r, "model_ops": W, "tile": tile, "block": block,
+                       "row_blocks": res.steps,
+                       "parallelism": f"1D block-cyclic column tiles over {world} rank(s)",
+                       "l2": "input 17 GB > 126 MB L2; input restored between steps",
+                       "profile_identity": bool(np.array_equal(res.row_profile, np.arange(r))),
+                       "sigma_identity": bool(np.array_equal(res.col_perm, np.arange(n)))},
+            "gpu_launches": launches * args.steps,
+            "clocks": clk.summary(),
+            "e2e": e2e,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def ours_batched(args, rank, world, local_rank):
     """Config 4: the fixed batch sharded across ranks (contiguous slices)."""
     import torch
@@ -558,6 +665,8 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c3")
     ap.add_argument("--cpu-sample", type=int, default=2048)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist", action="store_true",
+                    help="single-matrix workloads: the distributed column-tile driver even at N=1")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -566,6 +675,8 @@ def main():
         reference_arm(args, rank, world)
     elif args.workload == "c4":
         ours_batched(args, rank, world, local_rank)
+    elif args.dist or (args.workload == "c5" and world > 1):
+        ours_dist(args, rank, world, local_rank)
     else:
         ours(args, rank, world, local_rank)
 

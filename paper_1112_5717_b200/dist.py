@@ -107,6 +107,10 @@ class DeviceOps:
                  ldc=c.stride(0), stream=self._stream())
 
 
+def _roundup(a: int, q: int) -> int:
+    return -(-a // q) * q
+
+
 def _comm():
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized():
@@ -123,10 +127,11 @@ class _Engine:
         self.gpos_t = [torch.as_tensor(gp, dtype=torch.int64, device=dev) for gp in tiles.gpos]
         self.mine = tiles.gpos[rank]
 
-    def gather_cols(self, ra: int, rb: int, c0: int, c1: int) -> torch.Tensor:
+    def gather_cols(self, ra: int, rb: int, c0: int, c1: int, out=None) -> torch.Tensor:
         """Rows [ra, rb) x global columns [c0, c1) in global order, on every rank
-        (one broadcast from each rank owning a piece)."""
-        out = torch.empty((rb - ra, c1 - c0), dtype=self.x.dtype, device=self.x.device)
+        (one broadcast from each rank owning a piece), into ``out`` if given."""
+        if out is None:
+            out = torch.empty((rb - ra, c1 - c0), dtype=self.x.dtype, device=self.x.device)
         if rb == ra or c1 == c0:
             return out
         for g in range(self.world):
@@ -219,15 +224,25 @@ def dist_cup(x: torch.Tensor, m: int, n: int, p: int, tiles: ColumnTiles, block:
     if ops is None:
         ops = DeviceOps(p)
     eng = _Engine(x, m, n, tiles, ops, rank, dist)
+    # The row block is factored in one persistent buffer, its width padded to a
+    # few buckets with zero columns (zero columns never hold a pivot and stay
+    # in place): the CUP engine caches one plan + CUDA graph per (shape, buffer).
+    quantum = _roundup(_roundup(n, 12) // 12, 64)
+    rbuf = torch.empty(max(1, min(block, m) * n), dtype=x.dtype, device=x.device)
     sigma = np.arange(n, dtype=np.int64)
     rrp: list[np.ndarray] = []
     r, i0, steps = 0, 0, 0
     while i0 < m and r < n:
         bt = min(block, m - i0)
         w = n - r
-        R = eng.gather_cols(i0, i0 + bt, r, n)                  # (1)
+        wp = min(n, _roundup(w, quantum))
+        R = rbuf[:bt * wp].view(bt, wp)
+        if wp > w:
+            R[:, w:].zero_()
+        eng.gather_cols(i0, i0 + bt, r, n, out=R[:, :w])      # (1)
         rt, rrp_t, sig_t = ops.cup(R)                           # (2)
-        eng.put_cols(R, i0, r)
+        sig_t = sig_t[:w]
+        eng.put_cols(R[:, :w], i0, r)
         eng.permute_cols(r, sig_t, [(0, r), (i0 + bt, m)])       # (3)
         sigma[r:] = sigma[r + sig_t]
         eng.shift_u_rows(r, i0, rt)                             # (4)
