@@ -60,7 +60,7 @@ WORKLOADS = {
                   desc="CUP of one 2048x2048 random_matrix(seed=3) over GF(65521)"),
     "c8192": dict(m=8192, n=8192, p=65521, seed=3,
                   desc="CUP of one 8192x8192 random_matrix(seed=3) over GF(65521)"),
-    "c5": dict(m=65536, n=65536, p=65521, seed=5, tile=1024, block=1024,
+    "c5": dict(m=65536, n=65536, p=65521, seed=5, tile=1024, block=1024, superblock=8192,
                desc="CUP of one 65536x65536 random_matrix(seed=5) over GF(65521) (17 GB); one "
                     "GPU: the recursive engine; N > 1 (or --dist): 1D block-cyclic column tiles "
                     "over the ranks, NCCL broadcasts of the row block and the pivot columns"),
@@ -453,6 +453,7 @@ def ours_dist(args, rank, world, local_rank):
     wl = WORKLOADS[args.workload]
     m, n, p, seed = wl["m"], wl["n"], wl["p"], wl["seed"]
     tile, block = wl.get("tile", 1024), wl.get("block", 1024)
+    sb = wl.get("superblock", 8192)
     tiles = D.ColumnTiles(n, world, tile)
     stream = torch.cuda.current_stream()
     pristine = D.random_matrix_local(m, n, seed, p, tiles, rank, "cuda")
@@ -465,7 +466,7 @@ def ours_dist(args, rank, world, local_rank):
 
     for _ in range(args.warmup):
         x.copy_(pristine)
-        res = D.dist_cup(x, m, n, p, tiles, block=block)
+        res = D.dist_cup(x, m, n, p, tiles, block=block, superblock=sb)
     barrier()
     times = []
     with ClockSampler(local_rank) as clk:
@@ -474,7 +475,7 @@ def ours_dist(args, rank, world, local_rank):
             barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            res = D.dist_cup(x, m, n, p, tiles, block=block)
+            res = D.dist_cup(x, m, n, p, tiles, block=block, superblock=sb)
             e1.record(stream)
             e1.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
@@ -503,7 +504,7 @@ def ours_dist(args, rank, world, local_rank):
         barrier()
         t0 = time.perf_counter()
         x.copy_(host, non_blocking=True)
-        D.dist_cup(x, m, n, p, tiles, block=block)
+        D.dist_cup(x, m, n, p, tiles, block=block, superblock=sb)
         host.copy_(x, non_blocking=True)
         barrier()
         et = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
@@ -527,6 +528,7 @@ def ours_dist(args, rank, world, local_rank):
             "data": "synthetic",
             "config": {"workload": args.workload, "desc": wl["desc"], "m": m, "n": n, "p": p,
                        "seed": seed, "rank": r, "model_ops": W, "tile": tile, "block": block,
+                       "superblock": sb,
                        "row_blocks": res.steps,
                        "parallelism": f"1D block-cyclic column tiles over {world} rank(s)",
                        "l2": "input 17 GB > 126 MB L2; input restored between steps",

@@ -85,6 +85,12 @@ int rl_mm_u32(const uint32_t* A, int64_t lda, const uint32_t* B, int64_t ldb, ui
 int rl_mm_u32_dev(const uint32_t* dA, int64_t lda, const uint32_t* dB, int64_t ldb,
                   uint32_t* dC, int64_t ldc, int64_t m, int64_t l, int64_t n, uint32_t alpha,
                   uint32_t beta, uint32_t p, void* stream);
+/* rl_mm_u32_dev with the persistent GEMM grid bounded to max_ctas CTAs (0 = all
+ * SMs), so a latency-bound kernel on another stream (the distributed driver's
+ * lookahead row-block factorization) finds SMs free. */
+int rl_mm_u32_dev_grid(const uint32_t* dA, int64_t lda, const uint32_t* dB, int64_t ldb,
+                       uint32_t* dC, int64_t ldc, int64_t m, int64_t l, int64_t n, uint32_t alpha,
+                       uint32_t beta, uint32_t p, int max_ctas, void* stream);
 
 /* Replaces: std::pair<size_t, std::vector<uint32_t>> ranklab::rank_and_profile(MatView,
  *           OpCounter&)  proj/include/ranklab/solvers.hpp:13-14 (input consumed). */

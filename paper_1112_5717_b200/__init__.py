@@ -129,7 +129,7 @@ _vp = C.c_void_p
 
 #: every symbol include/ranklab_gpu.h declares
 EXPORTS = ["rl_cup_u32", "rl_cup_u32_dev", "rl_cup_batched_u32_dev", "rl_mm_u32",
-           "rl_mm_u32_dev", "rl_rank_and_profile_u32", "rl_determinant_u32",
+           "rl_mm_u32_dev", "rl_mm_u32_dev_grid", "rl_rank_and_profile_u32", "rl_determinant_u32",
            "rl_random_matrix_u32_dev", "rl_last_error", "rl_version", "rl_cup_plan_stats",
            "rl_profile_gemm_dev", "rl_cup_opcount", "rl_col_ech_trans_u32",
            "rl_col_ech_trans_u32_dev", "rl_invert_u32", "rl_invert_u32_dev", "rl_trsm_u32",
@@ -151,6 +151,8 @@ def lib():
     L.rl_mm_u32.argtypes = [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _u32, _u32, _u32, _vp]
     L.rl_mm_u32_dev.argtypes = [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _u32, _u32, _u32,
                                 _vp]
+    L.rl_mm_u32_dev_grid.argtypes = [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _u32, _u32,
+                                     _u32, C.c_int, _vp]
     L.rl_rank_and_profile_u32.argtypes = [_vp, _i64, _i64, _i64, _u32, C.POINTER(_i64), _vp]
     L.rl_determinant_u32.argtypes = [_vp, _i64, _i64, _u32, C.POINTER(_u32)]
     L.rl_random_matrix_u32_dev.argtypes = [_vp, _i64, _i64, _i64, C.c_uint64, _u32, _vp]
@@ -317,10 +319,18 @@ def mm(a: np.ndarray, b: np.ndarray, c: np.ndarray, alpha: int, beta: int, p: in
         ctr._add(ops)
 
 
-def mm_dev(d_a, d_b, d_c, m, l, n, alpha, beta, p, lda=None, ldb=None, ldc=None, stream=None):
+def mm_dev(d_a, d_b, d_c, m, l, n, alpha, beta, p, lda=None, ldb=None, ldc=None, stream=None,
+           max_ctas: int = 0):
+    """C <- alpha*A*B + beta*C (mod p) on device buffers; ``max_ctas`` > 0 bounds
+    the GEMM grid (rl_mm_u32_dev_grid) to leave SMs to a concurrent kernel."""
     pa = d_a.data_ptr() if hasattr(d_a, "data_ptr") else int(d_a)
     pb = d_b.data_ptr() if hasattr(d_b, "data_ptr") else int(d_b)
     pc = d_c.data_ptr() if hasattr(d_c, "data_ptr") else int(d_c)
+    if max_ctas:
+        _check(lib().rl_mm_u32_dev_grid(C.c_void_p(pa), lda or l, C.c_void_p(pb), ldb or n,
+                                        C.c_void_p(pc), ldc or n, m, l, n, int(alpha), int(beta),
+                                        int(p), int(max_ctas), _stream_ptr(stream)))
+        return
     _check(lib().rl_mm_u32_dev(C.c_void_p(pa), lda or l, C.c_void_p(pb), ldb or n, C.c_void_p(pc),
                                ldc or n, m, l, n, int(alpha), int(beta), int(p),
                                _stream_ptr(stream)))

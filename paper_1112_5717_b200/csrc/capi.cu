@@ -186,8 +186,8 @@ void copy_d2h_2d(u32* h, i64 hld, const u32* d, i64 dld, i64 rows, i64 cols, cud
 }
 
 void mm_dev_impl(const u32* dA, i64 lda, const u32* dB, i64 ldb, u32* dC, i64 ldc, i64 m, i64 l,
-                 i64 n, u32 alpha, u32 beta, u32 p, cudaStream_t s) {
-    mm_dense(dA, lda, dB, ldb, dC, ldc, m, l, n, alpha, beta, make_fp(p), s);
+                 i64 n, u32 alpha, u32 beta, u32 p, cudaStream_t s, int max_ctas = 0) {
+    mm_dense(dA, lda, dB, ldb, dC, ldc, m, l, n, alpha, beta, make_fp(p), s, max_ctas);
 }
 
 // cup of a device matrix, results on the host (synchronises s).  Small shapes
@@ -658,6 +658,21 @@ int rl_mm_u32_dev(const uint32_t* dA, int64_t lda, const uint32_t* dB, int64_t l
         require_device();
         std::lock_guard<std::mutex> lk(g_mu);
         mm_dev_impl(dA, lda, dB, ldb, dC, ldc, m, l, n, alpha, beta, p, (cudaStream_t)stream);
+    });
+}
+
+int rl_mm_u32_dev_grid(const uint32_t* dA, int64_t lda, const uint32_t* dB, int64_t ldb,
+                       uint32_t* dC, int64_t ldc, int64_t m, int64_t l, int64_t n, uint32_t alpha,
+                       uint32_t beta, uint32_t p, int max_ctas, void* stream) {
+    return guard([&] {
+        check_field(p);
+        if (m < 0 || l < 0 || n < 0) throw Error(RL_EDIM, "negative dimension");
+        if (alpha >= p || beta >= p) throw Error(RL_EINVAL, "alpha/beta not canonical");
+        if (max_ctas < 0) throw Error(RL_EINVAL, "negative grid bound");
+        require_device();
+        std::lock_guard<std::mutex> lk(g_mu);
+        mm_dev_impl(dA, lda, dB, ldb, dC, ldc, m, l, n, alpha, beta, p, (cudaStream_t)stream,
+                    max_ctas);
     });
 }
 

@@ -160,7 +160,7 @@ void tri_inv_rec(u32* X, i64 ldx, i32 k, bool upper, const Fp& f, DevBuf& wbuf, 
 }  // namespace
 
 void mm_dense(const u32* A, i64 lda, const u32* B, i64 ldb, u32* C, i64 ldc, i64 m, i64 l, i64 n,
-              u32 alpha, u32 beta, const Fp& f, cudaStream_t s) {
+              u32 alpha, u32 beta, const Fp& f, cudaStream_t s, int max_ctas) {
     if (m == 0 || n == 0) return;
     const u32 p = f.p;
     if (alpha == 0 || l == 0) {  // kernels.cpp:43-52: product short-circuited
@@ -193,6 +193,7 @@ void mm_dense(const u32* A, i64 lda, const u32* B, i64 ldb, u32* C, i64 ldc, i64
         g.alpha = alpha;
         g.beta = k0 == 0 ? beta : 1 % p;
         g.f = f;
+        g.max_ctas = max_ctas;
         const bool tc = kc >= 32 && n >= 32 && m >= 32;
         if (tc) {
             static DevBuf a2, b2;

@@ -12,9 +12,10 @@ namespace rl {
 
 // C <- beta*C + alpha*A*B (m x l x n, row-major, arbitrary leading dims), the
 // reference mm contract (kernels.hpp:26-27); K is chunked by the exact-
-// accumulation bound, tensor cores above 32 in every dimension.
+// accumulation bound, tensor cores above 32 in every dimension.  max_ctas > 0
+// bounds the persistent grid (leaves SMs to a kernel running beside it).
 void mm_dense(const u32* A, i64 lda, const u32* B, i64 ldb, u32* C, i64 ldc, i64 m, i64 l, i64 n,
-              u32 alpha, u32 beta, const Fp& f, cudaStream_t s);
+              u32 alpha, u32 beta, const Fp& f, cudaStream_t s, int max_ctas = 0);
 
 // X (k x k dense) <- the triangle of S: upper -> entries j > i, lower -> j < i,
 // the diagonal from S (unit = false) or 1 (unit = true), zeros elsewhere.  A

@@ -99,12 +99,14 @@ class DeviceOps:
         self._trsm(1, 0, 1, u, b, m, k, self.p, ldt=u.stride(0), ldb=b.stride(0),
                    stream=self._stream())
 
-    def mm_sub(self, a: torch.Tensor, b: torch.Tensor, c: torch.Tensor) -> None:
-        """c <- c - a * b (mod p)."""
+    def mm_sub(self, a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, max_ctas: int = 0) -> None:
+        """c <- c - a * b (mod p); max_ctas > 0 bounds the GEMM grid."""
         m, k = a.shape
         n = b.shape[1]
+        if m == 0 or n == 0:
+            return
         self._mm(a, b, c, m, k, n, self.p - 1, 1, self.p, lda=a.stride(0), ldb=b.stride(0),
-                 ldc=c.stride(0), stream=self._stream())
+                 ldc=c.stride(0), stream=self._stream(), max_ctas=max_ctas)
 
 
 def _roundup(a: int, q: int) -> int:
@@ -129,8 +131,12 @@ class _Engine:
 
     def gather_cols(self, ra: int, rb: int, c0: int, c1: int, out=None) -> torch.Tensor:
         """Rows [ra, rb) x global columns [c0, c1) in global order, on every rank
-        (one broadcast from each rank owning a piece), into ``out`` if given."""
+        (one broadcast from each rank owning a piece), into ``out`` if given.
+        With one rank and no ``out`` this is a view of the local matrix (the
+        callers solve/update it in place, ld = the local width)."""
         if out is None:
+            if self.world == 1:
+                return self.x[ra:rb, c0:c1]
             out = torch.empty((rb - ra, c1 - c0), dtype=self.x.dtype, device=self.x.device)
         if rb == ra or c1 == c0:
             return out
@@ -138,16 +144,15 @@ class _Engine:
             la, lb = self.tiles.lsuf(g, c0), self.tiles.lsuf(g, c1)
             if lb == la:
                 continue
+            if self.world == 1:
+                out.copy_(self.x[ra:rb, la:lb])
+                continue
             if g == self.rank:
                 piece = self.x[ra:rb, la:lb].contiguous()
             else:
                 piece = torch.empty((rb - ra, lb - la), dtype=self.x.dtype, device=self.x.device)
-            if self.world > 1:
-                self.dist.broadcast(piece, src=g)
-            if self.world == 1:
-                out.copy_(piece)
-            else:
-                out.index_copy_(1, self.gpos_t[g][la:lb] - c0, piece)
+            self.dist.broadcast(piece, src=g)
+            out.index_copy_(1, self.gpos_t[g][la:lb] - c0, piece)
         return out
 
     def put_cols(self, full: torch.Tensor, ra: int, c0: int) -> None:
@@ -158,10 +163,34 @@ class _Engine:
         if lb == la or rows == 0:
             return
         if self.world == 1:
-            self.x[ra:ra + rows, la:lb].copy_(full)
+            dst = self.x[ra:ra + rows, la:lb]
+            if dst.data_ptr() != full.data_ptr() or dst.stride() != full.stride():
+                dst.copy_(full)
         else:
             self.x[ra:ra + rows, la:lb].copy_(
                 full.index_select(1, self.gpos_t[self.rank][la:lb] - c0))
+
+    def solve_rows(self, ra: int, rb: int, c0: int, c1: int, U: torch.Tensor) -> torch.Tensor:
+        """G = B1 * U^{-1} for B1 = rows [ra, rb) x global columns [c0, c1), U unit
+        upper (c1 - c0 square); every rank solves one slice of the rows and the
+        slices are all-gathered, so G ends up complete on every rank."""
+        rows, k = rb - ra, c1 - c0
+        if self.world == 1:
+            B1 = self.gather_cols(ra, rb, c0, c1)
+            self.ops.trsm_right_upper_unit(U, B1)
+            return B1
+        B1 = self.gather_cols(ra, rb, c0, c1)
+        sl = _roundup(rows, self.world) // self.world
+        lo = min(rows, self.rank * sl)
+        hi = min(rows, lo + sl)
+        mine = torch.zeros((sl, k), dtype=self.x.dtype, device=self.x.device)
+        if hi > lo:
+            part = B1[lo:hi]
+            self.ops.trsm_right_upper_unit(U, part)
+            mine[:hi - lo].copy_(part)
+        out = torch.empty((sl * self.world, k), dtype=self.x.dtype, device=self.x.device)
+        self.dist.all_gather(list(out.split(sl)), mine)
+        return out[:rows]
 
     def permute_cols(self, r: int, sig: np.ndarray, row_ranges) -> None:
         """New column r + i = old column r + sig[i] on the given row ranges."""
@@ -211,16 +240,33 @@ class _Engine:
 
 
 def dist_cup(x: torch.Tensor, m: int, n: int, p: int, tiles: ColumnTiles, block: int = 1024,
-             ops=None) -> DistCupResult:
+             superblock: int = 4096, ops=None, lookahead: bool = True,
+             free_sms: int = 16) -> DistCupResult:
     """In-place distributed CUP; ``x`` is this rank's m x tiles.width(rank)
     local matrix (int32, row-major, contiguous).  Collective: every rank of the
-    default process group calls it with the same (m, n, p, tiles, block).
+    default process group calls it with the same (m, n, p, tiles, block,
+    superblock).
+
+    Two levels, like the top of the reference's row-halving recursion
+    (factor.cpp:35-53): row blocks of ``block`` rows are factored one after the
+    other inside a super-block of ``superblock`` rows (their TRSM and Schur
+    updates stop at the super-block's last row); the rows below a super-block
+    then receive one TRSM against the super-block's U11 and ONE Schur update
+    with K = the super-block's rank (large-K tensor-core GEMMs instead of K =
+    block; the G rows are solved in slices, one per rank, and all-gathered).
+
+    Lookahead (CUDA): every Schur update first updates the rows of the NEXT row
+    block, then the rest with the GEMM grid bounded to leave ``free_sms`` SMs;
+    the next block's gather and factorization run on a second (high-priority)
+    stream beside that GEMM -- the serial row-block chain overlaps the
+    embarrassingly parallel trailing update.
 
     Returns the global rank, row profile and sigma (identical on every rank);
     ``x`` holds this rank's columns of the packed [C\\U] (factor.hpp:10-14)."""
     dist, rank, world = _comm()
     assert world == tiles.world and tiles.n == n
     assert x.dim() == 2 and x.shape == (m, tiles.width(rank)) and x.is_contiguous()
+    superblock = max(superblock, block)
     if ops is None:
         ops = DeviceOps(p)
     eng = _Engine(x, m, n, tiles, ops, rank, dist)
@@ -229,35 +275,95 @@ def dist_cup(x: torch.Tensor, m: int, n: int, p: int, tiles: ColumnTiles, block:
     # in place): the CUP engine caches one plan + CUDA graph per (shape, buffer).
     quantum = _roundup(_roundup(n, 12) // 12, 64)
     rbuf = torch.empty(max(1, min(block, m) * n), dtype=x.dtype, device=x.device)
-    sigma = np.arange(n, dtype=np.int64)
-    rrp: list[np.ndarray] = []
-    r, i0, steps = 0, 0, 0
-    while i0 < m and r < n:
-        bt = min(block, m - i0)
+    cuda = x.is_cuda and lookahead
+    main = torch.cuda.current_stream(x.device) if cuda else None
+    side = torch.cuda.Stream(device=x.device, priority=-1) if cuda else None
+    max_ctas = 0
+    if cuda:
+        max_ctas = max(1, torch.cuda.get_device_properties(x.device).multi_processor_count - free_sms)
+
+    def factor_block(i0, bt, r):
         w = n - r
         wp = min(n, _roundup(w, quantum))
         R = rbuf[:bt * wp].view(bt, wp)
         if wp > w:
             R[:, w:].zero_()
-        eng.gather_cols(i0, i0 + bt, r, n, out=R[:, :w])      # (1)
-        rt, rrp_t, sig_t = ops.cup(R)                           # (2)
-        sig_t = sig_t[:w]
-        eng.put_cols(R[:, :w], i0, r)
-        eng.permute_cols(r, sig_t, [(0, r), (i0 + bt, m)])       # (3)
-        sigma[r:] = sigma[r + sig_t]
-        eng.shift_u_rows(r, i0, rt)                             # (4)
-        mb = m - i0 - bt
-        if rt and mb:
-            B1 = eng.gather_cols(i0 + bt, m, r, r + rt)         # (5)
-            ops.trsm_right_upper_unit(R[:rt, :rt], B1)
-            eng.put_cols(B1, i0 + bt, r)
-            ls = tiles.lsuf(rank, r + rt)
-            if ls < x.shape[1]:                                 # (6)
-                ops.mm_sub(B1, x[r:r + rt, ls:], x[i0 + bt:, ls:])
-        rrp.append(i0 + rrp_t[:rt])
-        r += rt
-        i0 += bt
-        steps += 1
+        eng.gather_cols(i0, i0 + bt, r, n, out=R[:, :w])          # (1)
+        rt, rrp_t, sig_t = ops.cup(R)                               # (2)
+        return R, w, rt, rrp_t, sig_t[:w]
+
+    def next_block(i_next, r_next, s_end):
+        if i_next >= m or r_next >= n:
+            return None
+        end = s_end if i_next < s_end else min(m, i_next + superblock)
+        return i_next, min(block, end - i_next), r_next
+
+    def update(G, ra, rb, ku0, ku1, nb):
+        """x[ra:rb, cols >= ku1] -= G * U (U = rows [ku0, ku1)); when the next
+        block nb = (i, bt, r) lies in [ra, rb): its rows first, then the rest
+        beside the next block's factorization.  Returns the factored block."""
+        ls = tiles.lsuf(rank, ku1)
+        U = x[ku0:ku1, ls:]
+        lo = hi = ra
+        if nb is not None and ra <= nb[0] < rb:
+            lo, hi = nb[0], min(rb, nb[0] + nb[1])
+        if hi > lo:
+            ops.mm_sub(G[lo - ra:hi - ra], U, x[lo:hi, ls:])
+        if not cuda or hi == lo:
+            if lo > ra:
+                ops.mm_sub(G[:lo - ra], U, x[ra:lo, ls:])
+            if rb > hi:
+                ops.mm_sub(G[hi - ra:], U, x[hi:rb, ls:])
+            return None
+        ev = main.record_event()
+        if lo > ra:
+            ops.mm_sub(G[:lo - ra], U, x[ra:lo, ls:], max_ctas=max_ctas)
+        if rb > hi:
+            ops.mm_sub(G[hi - ra:], U, x[hi:rb, ls:], max_ctas=max_ctas)
+        side.wait_event(ev)
+        with torch.cuda.stream(side):
+            return (nb, factor_block(*nb))
+
+    sigma = np.arange(n, dtype=np.int64)
+    rrp: list[np.ndarray] = []
+    r, i0, steps = 0, 0, 0
+    ahead = None
+    while i0 < m and r < n:
+        s_end = min(m, i0 + superblock)
+        r_s0 = r
+        while i0 < s_end and r < n:
+            bt = min(block, s_end - i0)
+            if ahead is not None:
+                assert ahead[0] == (i0, bt, r)
+                R, w, rt, rrp_t, sig_t = ahead[1]
+                main.wait_stream(side)
+                ahead = None
+            else:
+                R, w, rt, rrp_t, sig_t = factor_block(i0, bt, r)
+            eng.put_cols(R[:, :w], i0, r)
+            eng.permute_cols(r, sig_t, [(0, r), (i0 + bt, m)])       # (3)
+            sigma[r:] = sigma[r + sig_t]
+            eng.shift_u_rows(r, i0, rt)                             # (4)
+            nb = next_block(i0 + bt, r + rt, s_end)
+            if rt and s_end > i0 + bt:                              # (5) + (6) in the SB
+                B1 = eng.gather_cols(i0 + bt, s_end, r, r + rt)
+                ops.trsm_right_upper_unit(R[:rt, :rt], B1)
+                eng.put_cols(B1, i0 + bt, r)
+                if tiles.lsuf(rank, r + rt) < x.shape[1]:
+                    ahead = update(B1, i0 + bt, s_end, r, r + rt, nb)
+            rrp.append(i0 + rrp_t[:rt])
+            r += rt
+            i0 += bt
+            steps += 1
+        rs = r - r_s0
+        if rs and s_end < m:                                        # rows below the SB
+            U = eng.gather_cols(r_s0, r, r_s0, r)
+            G = eng.solve_rows(s_end, m, r_s0, r, U)
+            eng.put_cols(G, s_end, r_s0)
+            if tiles.lsuf(rank, r) < x.shape[1]:
+                ahead = update(G, s_end, m, r_s0, r, next_block(s_end, r, s_end))
+    if cuda:
+        main.wait_stream(side)
     prof = np.concatenate(rrp) if rrp else np.zeros(0, np.int64)
     return DistCupResult(r, prof.astype(np.uint32), sigma.astype(np.uint32), steps)
 

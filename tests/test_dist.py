@@ -79,11 +79,12 @@ def _cases():
     return out
 
 
-def _run_case(a, p, tile, block, world, rank):
+def _run_case(a, p, tile, block, world, rank, sb=None):
     tiles = D.ColumnTiles(a.shape[1], world, tile)
     full = torch.from_numpy(a.view(np.int32).copy())
     x = D.scatter_columns(full, tiles, rank)
-    res = D.dist_cup(x, a.shape[0], a.shape[1], p, tiles, block=block, ops=OracleOps(p))
+    res = D.dist_cup(x, a.shape[0], a.shape[1], p, tiles, block=block,
+                      superblock=sb or 3 * block, ops=OracleOps(p))
     body = D.gather_columns(x, a.shape[0], tiles).numpy().view(np.uint32)
     return res, body
 
@@ -155,3 +156,11 @@ def test_gloo_multi_rank_equals_reference(world):
     assert got == [c[0] for c in _cases()], got
     for pr in procs:
         assert pr.exitcode == 0
+
+
+@pytest.mark.parametrize("sb", [1, 2, 100])
+def test_single_rank_superblock_sizes(sb):
+    """Super-block = one row block (flat), two, and larger than the matrix."""
+    for name, a, p, tile, block in _cases()[:6]:
+        res, body = _run_case(a, p, tile, block, 1, 0, sb=sb * block)
+        _check_case(name, a, p, res, body)

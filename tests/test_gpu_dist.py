@@ -34,11 +34,12 @@ def _cases():
     return out
 
 
-def _run(a, p, tile, block, world, rank):
+def _run(a, p, tile, block, world, rank, sb=None):
     tiles = D.ColumnTiles(a.shape[1], world, tile)
     full = torch.from_numpy(a.view(np.int32).copy()).cuda()
     x = D.scatter_columns(full, tiles, rank)
-    res = D.dist_cup(x, a.shape[0], a.shape[1], p, tiles, block=block)
+    res = D.dist_cup(x, a.shape[0], a.shape[1], p, tiles, block=block,
+                      superblock=sb or 2 * block)
     body = D.gather_columns(x, a.shape[0], tiles).cpu().numpy().view(np.uint32)
     return res, body
 
