@@ -60,7 +60,7 @@ WORKLOADS = {
                   desc="CUP of one 2048x2048 random_matrix(seed=3) over GF(65521)"),
     "c8192": dict(m=8192, n=8192, p=65521, seed=3,
                   desc="CUP of one 8192x8192 random_matrix(seed=3) over GF(65521)"),
-    "c5": dict(m=65536, n=65536, p=65521, seed=5, tile=1024, block=1024, superblock=8192,
+    "c5": dict(m=65536, n=65536, p=65521, seed=5, tile=1024, block=1024, superblock=4096,
                desc="CUP of one 65536x65536 random_matrix(seed=5) over GF(65521) (17 GB); one "
                     "GPU: the recursive engine; N > 1 (or --dist): 1D block-cyclic column tiles "
                     "over the ranks, NCCL broadcasts of the row block and the pivot columns"),

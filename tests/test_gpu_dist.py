@@ -112,3 +112,21 @@ def test_dist_world2_gloo_on_one_gpu():
     for pr in procs:
         pr.join(timeout=120)
     assert got == [c[0] for c in _cases()], got
+
+
+@pytest.mark.parametrize("n,p,block,sb", [(8192, 65521, 1024, 4096), (6000, 8388593, 512, 2048)])
+def test_dist_world1_large_equals_engine(n, p, block, sb):
+    """Full-size-class sizes through the driver (super-blocks, lookahead, zero-copy
+    views): every body entry equals the single-GPU engine's on the device."""
+    torch.cuda.set_device(0)
+    src = torch.empty((n, n), dtype=torch.int32, device="cuda")
+    G.random_matrix_dev(src, n, n, 31, p)
+    eng = src.clone()
+    g = G.cup_dev(eng, n, n, p)
+    tiles = D.ColumnTiles(n, 1, 1024)
+    x = src.clone()
+    res = D.dist_cup(x, n, n, p, tiles, block=block, superblock=sb)
+    assert res.rank == g.rank
+    assert np.array_equal(res.row_profile, g.row_profile)
+    assert np.array_equal(res.col_perm, g.col_perm)
+    assert torch.equal(x, eng)
