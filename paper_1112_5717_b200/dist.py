@@ -99,6 +99,12 @@ class DeviceOps:
         self._trsm(1, 0, 1, u, b, m, k, self.p, ldt=u.stride(0), ldb=b.stride(0),
                    stream=self._stream())
 
+    def trsm_left_lower_nonunit(self, t: torch.Tensor, b: torch.Tensor) -> None:
+        """b <- T^{-1} b, T lower triangular with a nonzero diagonal."""
+        m, n = b.shape
+        self._trsm(0, 1, 0, t, b, m, n, self.p, ldt=t.stride(0), ldb=b.stride(0),
+                   stream=self._stream())
+
     def mm_sub(self, a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, max_ctas: int = 0) -> None:
         """c <- c - a * b (mod p); max_ctas > 0 bounds the GEMM grid."""
         m, k = a.shape
@@ -241,7 +247,7 @@ class _Engine:
 
 def dist_cup(x: torch.Tensor, m: int, n: int, p: int, tiles: ColumnTiles, block: int = 1024,
              superblock: int = 4096, ops=None, lookahead: bool = True,
-             free_sms: int = 16) -> DistCupResult:
+             free_sms: int = 16, window: int | None = None) -> DistCupResult:
     """In-place distributed CUP; ``x`` is this rank's m x tiles.width(rank)
     local matrix (int32, row-major, contiguous).  Collective: every rank of the
     default process group calls it with the same (m, n, p, tiles, block,
@@ -261,12 +267,22 @@ def dist_cup(x: torch.Tensor, m: int, n: int, p: int, tiles: ColumnTiles, block:
     stream beside that GEMM -- the serial row-block chain overlaps the
     embarrassingly parallel trailing update.
 
+    Window mode: a row block is factored on its first ``window`` (default 2 x
+    block) active columns only (every rank, redundantly -- the serial leaf
+    chain then runs on a narrow matrix); each rank then forms the block's U rows
+    on its OWN columns beyond the window, U_b = C_piv^{-1} * R_b[pivot rows]
+    (trsm Left/Lower/NonUnit), and checks that the block's non-pivot rows are
+    zero there (R_b - C * U_b = 0, one all-reduce).  If some rank finds a
+    nonzero (a pivot beyond the window) the block is refactored over its full
+    width.  Identical results either way (the CUP of the block is unique).
+
     Returns the global rank, row profile and sigma (identical on every rank);
     ``x`` holds this rank's columns of the packed [C\\U] (factor.hpp:10-14)."""
     dist, rank, world = _comm()
     assert world == tiles.world and tiles.n == n
     assert x.dim() == 2 and x.shape == (m, tiles.width(rank)) and x.is_contiguous()
     superblock = max(superblock, block)
+    window = 2 * block if window is None else window
     if ops is None:
         ops = DeviceOps(p)
     eng = _Engine(x, m, n, tiles, ops, rank, dist)
@@ -275,6 +291,7 @@ def dist_cup(x: torch.Tensor, m: int, n: int, p: int, tiles: ColumnTiles, block:
     # in place): the CUP engine caches one plan + CUDA graph per (shape, buffer).
     quantum = _roundup(_roundup(n, 12) // 12, 64)
     rbuf = torch.empty(max(1, min(block, m) * n), dtype=x.dtype, device=x.device)
+    wbuf = torch.empty(max(1, min(block, m) * min(n, window)), dtype=x.dtype, device=x.device)
     cuda = x.is_cuda and lookahead
     main = torch.cuda.current_stream(x.device) if cuda else None
     side = torch.cuda.Stream(device=x.device, priority=-1) if cuda else None
@@ -282,7 +299,7 @@ def dist_cup(x: torch.Tensor, m: int, n: int, p: int, tiles: ColumnTiles, block:
     if cuda:
         max_ctas = max(1, torch.cuda.get_device_properties(x.device).multi_processor_count - free_sms)
 
-    def factor_block(i0, bt, r):
+    def factor_full(i0, bt, r):
         w = n - r
         wp = min(n, _roundup(w, quantum))
         R = rbuf[:bt * wp].view(bt, wp)
@@ -290,7 +307,51 @@ def dist_cup(x: torch.Tensor, m: int, n: int, p: int, tiles: ColumnTiles, block:
             R[:, w:].zero_()
         eng.gather_cols(i0, i0 + bt, r, n, out=R[:, :w])          # (1)
         rt, rrp_t, sig_t = ops.cup(R)                               # (2)
-        return R, w, rt, rrp_t, sig_t[:w]
+        return R, w, rt, rrp_t, sig_t[:w], None
+
+    def factor_window(i0, bt, r, ww):
+        """The block on its first ww columns + this rank's U rows beyond them;
+        None when a pivot lies beyond the window (on any rank)."""
+        R = wbuf[:bt * ww].view(bt, ww)
+        eng.gather_cols(i0, i0 + bt, r, r + ww, out=R)
+        rt, rrp_t, sig_t = ops.cup(R)
+        ls = tiles.lsuf(rank, r + ww)
+        Rb = x[i0:i0 + bt, ls:]
+        bad = 0
+        Ub = None
+        if rt == 0:
+            bad = int(bool(torch.any(Rb != 0))) if Rb.numel() else 0
+        else:
+            piv = torch.as_tensor(rrp_t[:rt], device=x.device)
+            Ub = Rb.index_select(0, piv)                            # rt x beyond (copy)
+            Cp = torch.tril(R.index_select(0, piv)[:, :rt])         # C at the pivot rows
+            if Ub.shape[1]:
+                ops.trsm_left_lower_nonunit(Cp, Ub)
+            dead = np.setdiff1d(np.arange(bt), rrp_t[:rt])
+            if dead.size and Ub.shape[1]:
+                dv = torch.as_tensor(dead, device=x.device)
+                Cd = R.index_select(0, dv)[:, :rt].contiguous()
+                keep = torch.arange(rt, device=x.device)[None, :] <= dv[:, None]
+                Cd.masked_fill_(~keep, 0)                           # C(d, k) only for k <= d
+                D = Rb.index_select(0, dv)
+                ops.mm_sub(Cd, Ub, D)
+                bad = int(bool(torch.any(D != 0)))
+        if world > 1:
+            flag = torch.tensor([bad], dtype=torch.int32, device=x.device)
+            dist.all_reduce(flag)
+            bad = int(flag.item())
+        if bad:
+            return None
+        sig = np.concatenate([sig_t[:ww], np.arange(ww, n - r, dtype=np.int64)])
+        return R, ww, rt, rrp_t, sig, (ls, Ub)
+
+    def factor_block(i0, bt, r):
+        w = n - r
+        if window and window < w:
+            res = factor_window(i0, bt, r, window)
+            if res is not None:
+                return res
+        return factor_full(i0, bt, r)
 
     def next_block(i_next, r_next, s_end):
         if i_next >= m or r_next >= n:
@@ -335,12 +396,17 @@ def dist_cup(x: torch.Tensor, m: int, n: int, p: int, tiles: ColumnTiles, block:
             bt = min(block, s_end - i0)
             if ahead is not None:
                 assert ahead[0] == (i0, bt, r)
-                R, w, rt, rrp_t, sig_t = ahead[1]
+                R, wc, rt, rrp_t, sig_t, beyond = ahead[1]
                 main.wait_stream(side)
                 ahead = None
             else:
-                R, w, rt, rrp_t, sig_t = factor_block(i0, bt, r)
-            eng.put_cols(R[:, :w], i0, r)
+                R, wc, rt, rrp_t, sig_t, beyond = factor_block(i0, bt, r)
+            eng.put_cols(R[:, :wc], i0, r)
+            if beyond is not None:                                  # window mode
+                ls, Ub = beyond
+                if Ub is not None:
+                    x[i0:i0 + rt, ls:].copy_(Ub)
+                x[i0 + rt:i0 + bt, ls:].zero_()
             eng.permute_cols(r, sig_t, [(0, r), (i0 + bt, m)])       # (3)
             sigma[r:] = sigma[r + sig_t]
             eng.shift_u_rows(r, i0, rt)                             # (4)

@@ -47,7 +47,12 @@ class OracleOps:
         O.ref_trsm("right", "upper", "unit", uu, bb, self.p)
         self._back(b, bb)
 
-    def mm_sub(self, a, b, c):
+    def trsm_left_lower_nonunit(self, t, b):
+        tt, bb = self._np(t), self._np(b)
+        O.ref_trsm("left", "lower", "nonunit", tt, bb, self.p)
+        self._back(b, bb)
+
+    def mm_sub(self, a, b, c, max_ctas=0):
         aa, bb, cc = self._np(a), self._np(b), self._np(c)
         O.ref_mm(aa, bb, cc, self.p - 1, 1, self.p)
         self._back(c, cc)
@@ -79,12 +84,12 @@ def _cases():
     return out
 
 
-def _run_case(a, p, tile, block, world, rank, sb=None):
+def _run_case(a, p, tile, block, world, rank, sb=None, window=None):
     tiles = D.ColumnTiles(a.shape[1], world, tile)
     full = torch.from_numpy(a.view(np.int32).copy())
     x = D.scatter_columns(full, tiles, rank)
     res = D.dist_cup(x, a.shape[0], a.shape[1], p, tiles, block=block,
-                      superblock=sb or 3 * block, ops=OracleOps(p))
+                      superblock=sb or 3 * block, ops=OracleOps(p), window=window)
     body = D.gather_columns(x, a.shape[0], tiles).numpy().view(np.uint32)
     return res, body
 
@@ -163,4 +168,13 @@ def test_single_rank_superblock_sizes(sb):
     """Super-block = one row block (flat), two, and larger than the matrix."""
     for name, a, p, tile, block in _cases()[:6]:
         res, body = _run_case(a, p, tile, block, 1, 0, sb=sb * block)
+        _check_case(name, a, p, res, body)
+
+
+@pytest.mark.parametrize("window", [0, 1, 3, 8])
+def test_single_rank_window_widths(window):
+    """Window mode off (0), narrower than a block (pivots beyond it -> fallback)
+    and wider: identical results."""
+    for name, a, p, tile, block in _cases():
+        res, body = _run_case(a, p, tile, block, 1, 0, window=window * block)
         _check_case(name, a, p, res, body)
