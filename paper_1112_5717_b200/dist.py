@@ -267,8 +267,8 @@ def dist_cup(x: torch.Tensor, m: int, n: int, p: int, tiles: ColumnTiles, block:
     stream beside that GEMM -- the serial row-block chain overlaps the
     embarrassingly parallel trailing update.
 
-    Window mode: a row block is factored on its first ``window`` (default 2 x
-    block) active columns only (every rank, redundantly -- the serial leaf
+    Window mode (default with more than one rank): a row block is factored on
+    its first ``window`` (default 2 x block) active columns only (every rank, redundantly -- the serial leaf
     chain then runs on a narrow matrix); each rank then forms the block's U rows
     on its OWN columns beyond the window, U_b = C_piv^{-1} * R_b[pivot rows]
     (trsm Left/Lower/NonUnit), and checks that the block's non-pivot rows are
@@ -282,7 +282,8 @@ def dist_cup(x: torch.Tensor, m: int, n: int, p: int, tiles: ColumnTiles, block:
     assert world == tiles.world and tiles.n == n
     assert x.dim() == 2 and x.shape == (m, tiles.width(rank)) and x.is_contiguous()
     superblock = max(superblock, block)
-    window = 2 * block if window is None else window
+    # one rank has nothing redundant to save: full-width blocks (measured faster)
+    window = (2 * block if world > 1 else 0) if window is None else window
     if ops is None:
         ops = DeviceOps(p)
     eng = _Engine(x, m, n, tiles, ops, rank, dist)
