@@ -195,9 +195,102 @@ __global__ void __launch_bounds__(256) cup_batched_blk_kernel(u32* A, i64 stride
         __syncthreads();
         for (int e = tid; e < pr * n; e += 256) P[(e / n) * BN + e % n] = a[(i64)(i0 + e / n) * n + e % n];
         __syncthreads();
-        // ---- trailing rows: eager elimination by the panel's pivots, one warp per row
+        // ---- trailing rows
         const int np = r - r0;
-        if (np > 0) {
+        bool any_swap = false;
+        for (int j = r0; j < r; ++j) any_swap |= (s_ipiv[j] != j);
+        if (LAZY && np > 0 && !any_swap) {
+            // TRSM-then-GEMM form, two rows per warp: the multipliers of a row are
+            // f = x_piv * U_pp^{-1} (U_pp = the panel's unit upper pivot block,
+            // inverted once per panel), then x_rest -= f * U_rest.  Same values as
+            // the pivot-by-pivot elimination (the solve is unique); the U loads
+            // from shared memory are shared by the two rows, and no reduction
+            // sits between consecutive pivots.
+            u32* Uc = reinterpret_cast<u32*>(P);                   // [PR][BN], 0 left of r0+np
+            u32 (*X)[PR + 1] = reinterpret_cast<u32 (*)[PR + 1]>(Uc + PR * BN);   // U_pp^{-1}
+            u32 (*Up)[PR + 1] = X + PR;                                          // U_pp
+            const int cend = r0 + np;
+            for (int j = warp; j < np; j += 8) {
+                const u32* src = a + (i64)(i0 + s_prow[j]) * n;
+                for (int c = lane; c < BN; c += 32) {
+                    const u32 v = c < n ? src[c] : 0u;
+                    Uc[j * BN + c] = c >= cend ? v : 0u;
+                    if (c >= r0 && c < cend) Up[j][c - r0] = v;
+                }
+            }
+            __syncthreads();
+            if (tid < np) {  // column j of X = U_pp^{-1} (unit upper), back substitution
+                const int j = tid;
+                X[j][j] = 1u % f.p;
+                for (int k = j - 1; k >= 0; --k) {
+                    u64 acc = 0;
+                    for (int i = k + 1; i <= j; ++i) acc += (u64)Up[k][i] * X[i][j];
+                    const u32 s = red64(acc, f);
+                    X[k][j] = s ? f.p - s : 0u;
+                }
+                for (int k = j + 1; k < PR; ++k) X[k][j] = 0;
+            } else if (tid < PR) {
+                for (int k = 0; k < PR; ++k) X[k][tid] = 0;
+            }
+            __syncthreads();
+            const int cpos = r0 + lane, srcl = cpos & 31, qs = cpos >> 5;
+            for (int k0 = i0 + pr + 2 * warp; k0 < m; k0 += 16) {
+                const bool two = k0 + 1 < m;
+                u32* row0 = a + (i64)k0 * n;
+                u32* row1 = row0 + n;
+                u64 x0[BN / 32], x1[BN / 32];
+#pragma unroll
+                for (int q = 0; q < BN / 32; ++q) {
+                    const int c = lane + 32 * q;
+                    x0[q] = (q < nq && c < n) ? row0[c] : 0u;
+                    x1[q] = (two && q < nq && c < n) ? row1[c] : 0u;
+                }
+                // x at pivot column r0 + lane (values still reduced); every block is
+                // shuffled so that no register array is indexed dynamically
+                u32 pv0 = 0, pv1 = 0;
+#pragma unroll
+                for (int q = 0; q < BN / 32; ++q) {
+                    const u32 t0 = __shfl_sync(0xffffffffu, (u32)x0[q], srcl);
+                    const u32 t1 = __shfl_sync(0xffffffffu, (u32)x1[q], srcl);
+                    if (q == qs) {
+                        pv0 = t0;
+                        pv1 = t1;
+                    }
+                }
+                // f_j (lane j) = sum_k x_piv[k] * X[k][j]
+                u64 s0 = 0, s1 = 0;
+                for (int k = 0; k < np; ++k) {
+                    const u32 xk = X[k][lane];
+                    s0 += (u64)__shfl_sync(0xffffffffu, pv0, k) * xk;
+                    s1 += (u64)__shfl_sync(0xffffffffu, pv1, k) * xk;
+                }
+                const u32 f0 = red64(s0, f), f1 = red64(s1, f);
+                const u32 nf0 = f0 ? f.p - f0 : 0u, nf1 = f1 ? f.p - f1 : 0u;
+                for (int j = 0; j < np; ++j) {
+                    const u32 g0 = __shfl_sync(0xffffffffu, nf0, j);
+                    const u32 g1 = __shfl_sync(0xffffffffu, nf1, j);
+                    const u32* U = Uc + j * BN + lane;
+#pragma unroll
+                    for (int q = 0; q < BN / 32; ++q) {
+                        const u32 u = U[32 * q];
+                        x0[q] += (u64)g0 * u;
+                        x1[q] += (u64)g1 * u;
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < BN / 32; ++q) {
+                    const int c = lane + 32 * q;
+                    // pivot columns take the raw C entries f (lane c - r0 holds them)
+                    const u32 fc0 = __shfl_sync(0xffffffffu, f0, (c - r0) & 31);
+                    const u32 fc1 = __shfl_sync(0xffffffffu, f1, (c - r0) & 31);
+                    const bool piv = c >= r0 && c < cend;
+                    if (q < nq && c < n) {
+                        row0[c] = piv ? fc0 : red64(x0[q], f);
+                        if (two) row1[c] = piv ? fc1 : red64(x1[q], f);
+                    }
+                }
+            }
+        } else if (np > 0) {  // one warp per row, pivot by pivot (transpositions, large p)
             u32* wb = wbuf + warp * BN;
             for (int k = i0 + pr + warp; k < m; k += 8) {
                 u32* row = a + (i64)k * n;
