@@ -101,6 +101,9 @@ __global__ void __launch_bounds__(256) cup_batched_kernel(u32* A, i64 stride, i3
 // larger p reduce every product.
 constexpr int PR = 32;
 constexpr int BN = 256;
+#ifndef BATCHED_ROWS_PER_WARP
+#define BATCHED_ROWS_PER_WARP 1  // trailing rows per warp (more share the U loads, cost registers)
+#endif
 
 template <bool LAZY>
 __device__ __forceinline__ u64 lazy_fma(u64 acc, u32 nf, u32 u, const Fp& f) {
@@ -234,59 +237,69 @@ __global__ void __launch_bounds__(256) cup_batched_blk_kernel(u32* A, i64 stride
             }
             __syncthreads();
             const int cpos = r0 + lane, srcl = cpos & 31, qs = cpos >> 5;
-            for (int k0 = i0 + pr + 2 * warp; k0 < m; k0 += 16) {
-                const bool two = k0 + 1 < m;
-                u32* row0 = a + (i64)k0 * n;
-                u32* row1 = row0 + n;
-                u64 x0[BN / 32], x1[BN / 32];
+            constexpr int RW = BATCHED_ROWS_PER_WARP;
+            for (int k0 = i0 + pr + RW * warp; k0 < m; k0 += 8 * RW) {
+                u32* row[RW];
+                bool ok[RW];
+                u64 x[RW][BN / 32];
 #pragma unroll
-                for (int q = 0; q < BN / 32; ++q) {
-                    const int c = lane + 32 * q;
-                    x0[q] = (q < nq && c < n) ? row0[c] : 0u;
-                    x1[q] = (two && q < nq && c < n) ? row1[c] : 0u;
+                for (int t = 0; t < RW; ++t) {
+                    ok[t] = k0 + t < m;
+                    row[t] = a + (i64)(k0 + t) * n;
+#pragma unroll
+                    for (int q = 0; q < BN / 32; ++q) {
+                        const int c = lane + 32 * q;
+                        x[t][q] = (ok[t] && q < nq && c < n) ? row[t][c] : 0u;
+                    }
                 }
                 // x at pivot column r0 + lane (values still reduced); every block is
                 // shuffled so that no register array is indexed dynamically
-                u32 pv0 = 0, pv1 = 0;
+                u32 pv[RW];
 #pragma unroll
-                for (int q = 0; q < BN / 32; ++q) {
-                    const u32 t0 = __shfl_sync(0xffffffffu, (u32)x0[q], srcl);
-                    const u32 t1 = __shfl_sync(0xffffffffu, (u32)x1[q], srcl);
-                    if (q == qs) {
-                        pv0 = t0;
-                        pv1 = t1;
+                for (int t = 0; t < RW; ++t) {
+                    pv[t] = 0;
+#pragma unroll
+                    for (int q = 0; q < BN / 32; ++q) {
+                        const u32 v = __shfl_sync(0xffffffffu, (u32)x[t][q], srcl);
+                        if (q == qs) pv[t] = v;
                     }
                 }
                 // f_j (lane j) = sum_k x_piv[k] * X[k][j]
-                u64 s0 = 0, s1 = 0;
+                u64 sacc[RW];
+#pragma unroll
+                for (int t = 0; t < RW; ++t) sacc[t] = 0;
                 for (int k = 0; k < np; ++k) {
                     const u32 xk = X[k][lane];
-                    s0 += (u64)__shfl_sync(0xffffffffu, pv0, k) * xk;
-                    s1 += (u64)__shfl_sync(0xffffffffu, pv1, k) * xk;
+#pragma unroll
+                    for (int t = 0; t < RW; ++t) sacc[t] += (u64)__shfl_sync(0xffffffffu, pv[t], k) * xk;
                 }
-                const u32 f0 = red64(s0, f), f1 = red64(s1, f);
-                const u32 nf0 = f0 ? f.p - f0 : 0u, nf1 = f1 ? f.p - f1 : 0u;
+                u32 fv[RW], nf[RW];
+#pragma unroll
+                for (int t = 0; t < RW; ++t) {
+                    fv[t] = red64(sacc[t], f);
+                    nf[t] = fv[t] ? f.p - fv[t] : 0u;
+                }
                 for (int j = 0; j < np; ++j) {
-                    const u32 g0 = __shfl_sync(0xffffffffu, nf0, j);
-                    const u32 g1 = __shfl_sync(0xffffffffu, nf1, j);
+                    u32 g[RW];
+#pragma unroll
+                    for (int t = 0; t < RW; ++t) g[t] = __shfl_sync(0xffffffffu, nf[t], j);
                     const u32* U = Uc + j * BN + lane;
 #pragma unroll
                     for (int q = 0; q < BN / 32; ++q) {
                         const u32 u = U[32 * q];
-                        x0[q] += (u64)g0 * u;
-                        x1[q] += (u64)g1 * u;
+#pragma unroll
+                        for (int t = 0; t < RW; ++t) x[t][q] += (u64)g[t] * u;
                     }
                 }
 #pragma unroll
                 for (int q = 0; q < BN / 32; ++q) {
                     const int c = lane + 32 * q;
                     // pivot columns take the raw C entries f (lane c - r0 holds them)
-                    const u32 fc0 = __shfl_sync(0xffffffffu, f0, (c - r0) & 31);
-                    const u32 fc1 = __shfl_sync(0xffffffffu, f1, (c - r0) & 31);
                     const bool piv = c >= r0 && c < cend;
-                    if (q < nq && c < n) {
-                        row0[c] = piv ? fc0 : red64(x0[q], f);
-                        if (two) row1[c] = piv ? fc1 : red64(x1[q], f);
+#pragma unroll
+                    for (int t = 0; t < RW; ++t) {
+                        const u32 fc = __shfl_sync(0xffffffffu, fv[t], (c - r0) & 31);
+                        if (ok[t] && q < nq && c < n) row[t][c] = piv ? fc : red64(x[t][q], f);
                     }
                 }
             }
