@@ -6,6 +6,8 @@
 // U rows are placed at the end (factor.cpp:62-70 composed).  Outputs per
 // matrix: rank, row profile and pivot positions (sigma is composed on the host).
 #include <algorithm>
+#include <map>
+#include <mutex>
 
 #include "kernels.cuh"
 #include "runtime.h"
@@ -114,7 +116,7 @@ __device__ __forceinline__ u64 lazy_fma(u64 acc, u32 nf, u32 u, const Fp& f) {
 template <bool LAZY>
 __global__ void __launch_bounds__(256) cup_batched_blk_kernel(u32* A, i64 stride, i32 m, i32 n, Fp f,
                                                               i32* ranks, i32* rrp_out, i32* ipiv_out,
-                                                              i32 kcap) {
+                                                              i32 kcap, const u32* __restrict__ inv_tab) {
     extern __shared__ __align__(16) u64 P[];             // [PR][BN] panel rows, lazy sums
     u32* wbuf = reinterpret_cast<u32*>(P + PR * BN);     // [8][BN] per-warp row buffer
     __shared__ i32 s_rrp[BN], s_ipiv[BN], s_prow[PR];
@@ -128,7 +130,8 @@ __global__ void __launch_bounds__(256) cup_batched_blk_kernel(u32* A, i64 stride
     for (int i0 = 0; i0 < m && r < n; i0 += PR) {
         const int pr = min(PR, m - i0);
         const int r0 = r;
-        for (int e = tid; e < pr * n; e += 256) P[(e / n) * BN + e % n] = a[(i64)(i0 + e / n) * n + e % n];
+        for (int t = warp; t < pr; t += 8)
+            for (int c = lane; c < n; c += 32) P[t * BN + c] = a[(i64)(i0 + t) * n + c];
         __syncthreads();
         // ---- panel: rows in order
         for (int k = 0; k < pr && r < n; ++k) {
@@ -162,7 +165,10 @@ __global__ void __launch_bounds__(256) cup_batched_blk_kernel(u32* A, i64 stride
                 }
                 __syncthreads();
             }
-            if (tid == 0) s_pinv = inv_euclid((u32)P[k * BN + r], f.p);  // one thread
+            if (tid == 0) {  // one thread: table lookup (p < 2^24) or extended Euclid
+                const u32 pv = (u32)P[k * BN + r];
+                s_pinv = inv_tab ? __ldg(inv_tab + pv) : inv_euclid(pv, f.p);
+            }
             __syncthreads();
             const u32 pinv = s_pinv;
             // normalised U row (reduced)
@@ -191,12 +197,11 @@ __global__ void __launch_bounds__(256) cup_batched_blk_kernel(u32* A, i64 stride
         }
         // rows of the panel after the early return (r == n) keep their values;
         // reduce everything that is still lazy and write the panel back
-        for (int e = tid; e < pr * n; e += 256) {
-            const u64 x = P[(e / n) * BN + e % n];
-            a[(i64)(i0 + e / n) * n + e % n] = LAZY ? red64(x, f) : (u32)x;
-        }
-        __syncthreads();
-        for (int e = tid; e < pr * n; e += 256) P[(e / n) * BN + e % n] = a[(i64)(i0 + e / n) * n + e % n];
+        for (int t = warp; t < pr; t += 8)
+            for (int c = lane; c < n; c += 32) {
+                const u64 x = P[t * BN + c];
+                a[(i64)(i0 + t) * n + c] = LAZY ? red64(x, f) : (u32)x;
+            }
         __syncthreads();
         // ---- trailing rows
         const int np = r - r0;
@@ -304,6 +309,9 @@ __global__ void __launch_bounds__(256) cup_batched_blk_kernel(u32* A, i64 stride
                 }
             }
         } else if (np > 0) {  // one warp per row, pivot by pivot (transpositions, large p)
+            for (int t = warp; t < pr; t += 8)
+                for (int c = lane; c < n; c += 32) P[t * BN + c] = a[(i64)(i0 + t) * n + c];
+            __syncthreads();
             u32* wb = wbuf + warp * BN;
             for (int k = i0 + pr + warp; k < m; k += 8) {
                 u32* row = a + (i64)k * n;
@@ -371,6 +379,30 @@ __global__ void __launch_bounds__(256) cup_batched_blk_kernel(u32* A, i64 stride
     }
 }
 
+__global__ void inv_table_kernel(u32* tab, u32 p) {
+    for (u32 x = blockIdx.x * blockDim.x + threadIdx.x; x < p; x += gridDim.x * blockDim.x)
+        tab[x] = x ? inv_euclid(x, p) : 0u;
+}
+
+// x^{-1} mod p for every x < p (p < 2^24: at most 64 MB), built once per prime
+// and device, so a pivot inverse on the batched kernel's serial chain is one
+// cached load instead of an extended Euclid loop.
+const u32* inverse_table(u32 p, cudaStream_t s) {
+    static std::mutex mu;
+    static std::map<std::pair<int, u32>, u32*> tabs;
+    int dev = 0;
+    RL_CUDA_CHECK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = tabs.find({dev, p});
+    if (it != tabs.end()) return it->second;
+    u32* t = nullptr;
+    if (cudaMalloc(&t, sizeof(u32) * p) != cudaSuccess) throw Error(8, "cudaMalloc failed");
+    inv_table_kernel<<<4 * num_sms(), 256, 0, s>>>(t, p);
+    RL_CUDA_CHECK(cudaGetLastError());
+    tabs.emplace(std::make_pair(dev, p), t);
+    return t;
+}
+
 }  // namespace
 
 void cup_batched(u32* dA, i64 batch, i32 m, i32 n, i64 stride, u32 p, i32* d_ranks, i32* d_rrp,
@@ -390,10 +422,11 @@ void cup_batched(u32* dA, i64 batch, i32 m, i32 n, i64 stride, u32 p, i32* d_ran
         }
         if (p < (1u << 24))
             cup_batched_blk_kernel<true><<<(unsigned)batch, 256, smem, s>>>(dA, stride, m, n, f, d_ranks,
-                                                                           d_rrp, d_ipiv, kcap);
+                                                                           d_rrp, d_ipiv, kcap,
+                                                                           inverse_table(p, s));
         else
             cup_batched_blk_kernel<false><<<(unsigned)batch, 256, smem, s>>>(dA, stride, m, n, f, d_ranks,
-                                                                            d_rrp, d_ipiv, kcap);
+                                                                            d_rrp, d_ipiv, kcap, nullptr);
     } else {
         cup_batched_kernel<<<(unsigned)batch, 256, 0, s>>>(dA, stride, m, n, f, d_ranks, d_rrp, d_ipiv,
                                                            kcap);
