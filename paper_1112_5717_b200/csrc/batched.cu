@@ -165,12 +165,14 @@ __global__ void __launch_bounds__(256) cup_batched_blk_kernel(u32* A, i64 stride
                 }
                 __syncthreads();
             }
-            if (tid == 0) {  // one thread: table lookup (p < 2^24) or extended Euclid
-                const u32 pv = (u32)P[k * BN + r];
-                s_pinv = inv_tab ? __ldg(inv_tab + pv) : inv_euclid(pv, f.p);
+            u32 pinv;
+            if (inv_tab) {  // p < 2^24: every thread loads the inverse (one cached word)
+                pinv = __ldg(inv_tab + (u32)P[k * BN + r]);
+            } else {        // one thread runs the extended Euclid
+                if (tid == 0) s_pinv = inv_euclid((u32)P[k * BN + r], f.p);
+                __syncthreads();
+                pinv = s_pinv;
             }
-            __syncthreads();
-            const u32 pinv = s_pinv;
             // normalised U row (reduced)
             u32 u = 0;
             if (c < n && c > r) {
@@ -193,8 +195,10 @@ __global__ void __launch_bounds__(256) cup_batched_blk_kernel(u32* A, i64 stride
                 for (int t = k + 1; t < pr; ++t) P[t * BN + c] = lazy_fma<LAZY>(P[t * BN + c], s_f[t], u, f);
             }
             ++r;
-            __syncthreads();
+            // no barrier: the next row's pivot search reads only this thread's
+            // own column, and everything shared is written after the next barrier
         }
+        __syncthreads();
         // rows of the panel after the early return (r == n) keep their values;
         // reduce everything that is still lazy and write the panel back
         for (int t = warp; t < pr; t += 8)
