@@ -61,9 +61,10 @@ struct Cfg {
     static constexpr int UN = L * NT;                               // UMMA N
     static constexpr int B_TILE = UN * BK;
     static constexpr int STAGE = A_TILE + B_TILE;
-    static constexpr int STAGES = (200 * 1024) / STAGE;
+    static constexpr int STG = 16 * 32 * 16 * 4;  // epilogue staging: 16 warps x 32 rows x 16 cols
+    static constexpr int STAGES = (232448 - 1280 - STG) / STAGE;
     static constexpr int CH = 16;  // epilogue column chunk
-    static constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 256;
+    static constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 256 + STG;
 };
 
 __device__ __forceinline__ void dyn_shape(const GemmArgs& g, i32& K, i32& N, i32& k_lo,
@@ -367,43 +368,59 @@ __global__ void __launch_bounds__(NTHR, 1)
         }
     } else {  // ---- epilogue warps 0..EPW-1: TMEM -> registers -> exact mod-p -> C
         // EPW/4 warps per TMEM lane quadrant (warp & 3), each owning a slice of
-        // the tile's columns.  A warp's first C chunks are requested before it
-        // waits on the accumulator, so the C read latency overlaps the MMAs.
+        // the tile's columns; TMEM hands lane l row l, so a warp holds 32 rows x
+        // 16 columns per chunk.  C moves between HBM and the registers through a
+        // per-warp shared-memory staging block (32 rows x 64 B, 16-byte groups
+        // XOR-swizzled by (row >> 1) & 3: conflict-free both ways), so every
+        // global access is coalesced: one LDG/STG.128 covers 8 rows x 64 B
+        // (8 cache lines) instead of 32 rows x 16 B.  A warp's first C chunks are
+        // requested before it waits on the accumulator (C latency under the MMAs).
         const int q = warp & 3;  // TMEM lane quadrant this warp may access
         const int part = warp >> 2;
         const int rloc = q * 32 + lane;
         const uint32_t lane_base = (uint32_t)(q * 32) << 16;
         const Fp f = g.f;
         const u32 alpha = g.alpha, beta = g.beta;
+        uint8_t* stg = smem + STAGES * STAGE + 256 + warp * 2048;
+        // coalesced role of this lane: rows it*8 + (lane >> 2), 16-byte group lane & 3
+        const int crow_c = lane >> 2, cgrp = lane & 3;
+        auto stg_off = [](int row, int grp) { return row * 64 + ((grp ^ ((row >> 1) & 3)) << 4); };
         int acc = 0;
         uint32_t aph = 0;
         constexpr int NCHP = NT / C_::CH / (EPW / 4);  // chunks per warp slice
         constexpr int PF = NCHP < 2 ? NCHP : 2;       // chunks prefetched ahead
+        const bool ld_ok = (g.ldc & 3) == 0;
         for (i32 tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
             i32 mb, nb;
             tile_coords(tile, MB, NB, mb, nb);
             const i32 row = mb * BM + rloc;
             const bool vrow = row < g.M;
+            u32* cbase = g.C + (i64)(g.c_row0 + mb * BM + q * 32) * g.ldc + n_lo + nb * NT;
             u32* crow = g.C + (i64)(g.c_row0 + (vrow ? row : 0)) * g.ldc + n_lo + nb * NT;
-            // 16-byte vector access when the row segment is aligned (the usual
-            // case: column origins are multiples of the leaf size)
-            const bool vec = ((reinterpret_cast<uintptr_t>(crow) & 15) == 0);
+            // coalesced path: 16-byte aligned rows (the usual case: column origins
+            // are multiples of the leaf size and ldc of 4)
+            const bool vec = ld_ok && ((reinterpret_cast<uintptr_t>(cbase) & 15) == 0);
+            const i32 rows_here = min(32, g.M - (mb * BM + q * 32));  // may be <= 0
+            // chunk ch in coalesced form: cb[it*4 + k] = C(row it*8 + crow_c, col 4*cgrp + k)
             auto load_chunk = [&](int ch, u32 (&cb)[16]) {
                 const i32 c0 = nb * NT + ch * 16;
 #pragma unroll
                 for (int t = 0; t < 16; ++t) cb[t] = 0;
-                if (!vrow || beta == 0) return;
+                if (beta == 0) return;
                 if (vec && c0 + 16 <= N) {
-                    const uint4* src = reinterpret_cast<const uint4*>(crow + ch * 16);
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) {
-                        const uint4 t4 = src[v];
-                        cb[4 * v + 0] = t4.x;
-                        cb[4 * v + 1] = t4.y;
-                        cb[4 * v + 2] = t4.z;
-                        cb[4 * v + 3] = t4.w;
+                    for (int it = 0; it < 4; ++it) {
+                        const int rr = it * 8 + crow_c;
+                        if (rr < rows_here) {
+                            const uint4 t4 = *reinterpret_cast<const uint4*>(
+                                cbase + (i64)rr * g.ldc + ch * 16 + 4 * cgrp);
+                            cb[4 * it + 0] = t4.x;
+                            cb[4 * it + 1] = t4.y;
+                            cb[4 * it + 2] = t4.z;
+                            cb[4 * it + 3] = t4.w;
+                        }
                     }
-                } else {
+                } else if (vrow) {  // per-row scalar fallback (row layout)
 #pragma unroll
                     for (int t = 0; t < 16; ++t) cb[t] = (c0 + t < N) ? crow[ch * 16 + t] : 0u;
                 }
@@ -417,51 +434,76 @@ __global__ void __launch_bounds__(NTHR, 1)
 #pragma unroll
             for (int cc = 0; cc < NCHP; ++cc) {
                 const int ch = part * NCHP + cc;
+                const i32 c0 = nb * NT + ch * 16;
+                const bool full = vec && c0 + 16 <= N;
                 uint32_t sv[L][16];
 #pragma unroll
                 for (int j = 0; j < L; ++j)
                     ptx::tmem_ld16(tmem + lane_base + acc * 256 + j * NT + ch * 16, sv[j]);
                 u32 cur[16];
+                if (full) {  // coalesced -> row layout through the staging block
+                    __syncwarp();
 #pragma unroll
-                for (int t = 0; t < 16; ++t) cur[t] = cbuf[cc % PF][t];
+                    for (int it = 0; it < 4; ++it)
+                        *reinterpret_cast<uint4*>(stg + stg_off(it * 8 + crow_c, cgrp)) =
+                            make_uint4(cbuf[cc % PF][4 * it], cbuf[cc % PF][4 * it + 1],
+                                       cbuf[cc % PF][4 * it + 2], cbuf[cc % PF][4 * it + 3]);
+                    __syncwarp();
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        const uint4 t4 = *reinterpret_cast<const uint4*>(stg + stg_off(lane, v));
+                        cur[4 * v + 0] = t4.x;
+                        cur[4 * v + 1] = t4.y;
+                        cur[4 * v + 2] = t4.z;
+                        cur[4 * v + 3] = t4.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int t = 0; t < 16; ++t) cur[t] = cbuf[cc % PF][t];
+                }
                 if (cc + PF < NCHP) load_chunk(ch + PF, cbuf[cc % PF]);
                 ptx::tc_wait_ld();
-                const i32 c0 = nb * NT + ch * 16;
-                if (vrow) {
-                    u32 outv[16];
+                u32 (&outv)[16] = cur;  // transformed in place
 #pragma unroll
-                    for (int t = 0; t < 16; ++t) {
-                        // x = sum_j S_j 2^(8j); L <= 2 means p <= 2^16 and x < 2^40
-                        u32 r;
-                        if (L == 1) {
-                            r = red32(sv[0][t], f);
-                        } else if (L == 2) {
-                            r = red_sp((u64)sv[0][t] + ((u64)sv[L > 1 ? 1 : 0][t] << 8), f);
-                        } else {
-                            u64 x = sv[0][t];
-                            x += (u64)sv[L > 1 ? 1 : 0][t] << 8;
-                            x += (u64)sv[L > 2 ? 2 : 0][t] << 16;
-                            if (L > 3) x += (u64)sv[L > 3 ? 3 : 0][t] << 24;
-                            r = red64(x, f);
-                        }
-                        const u32 cv = (beta == 0 || beta == 1) ? cur[t] : mulmod(cur[t], beta, f);
-                        u32 out;
-                        if (alpha == f.p - 1) out = submod(cv, r, f);
-                        else if (alpha == 1) out = addmod(cv, r, f);
-                        else out = addmod(cv, mulmod(r, alpha, f), f);
-                        outv[t] = out;
-                    }
-                    if (vec && c0 + 16 <= N) {
-                        uint4* dst = reinterpret_cast<uint4*>(crow + ch * 16);
-#pragma unroll
-                        for (int v = 0; v < 4; ++v)
-                            dst[v] = make_uint4(outv[4 * v], outv[4 * v + 1], outv[4 * v + 2],
-                                                outv[4 * v + 3]);
+                for (int t = 0; t < 16; ++t) {
+                    // x = sum_j S_j 2^(8j); L <= 2 means p <= 2^16 and x < 2^40
+                    u32 r;
+                    if (L == 1) {
+                        r = red32(sv[0][t], f);
+                    } else if (L == 2) {
+                        r = red_sp((u64)sv[0][t] + ((u64)sv[L > 1 ? 1 : 0][t] << 8), f);
                     } else {
-#pragma unroll
-                        for (int t = 0; t < 16; ++t)
-                            if (c0 + t < N) crow[ch * 16 + t] = outv[t];
+                        u64 x = sv[0][t];
+                        x += (u64)sv[L > 1 ? 1 : 0][t] << 8;
+                        x += (u64)sv[L > 2 ? 2 : 0][t] << 16;
+                        if (L > 3) x += (u64)sv[L > 3 ? 3 : 0][t] << 24;
+                        r = red64(x, f);
                     }
+                    const u32 cv = (beta == 0 || beta == 1) ? cur[t] : mulmod(cur[t], beta, f);
+                    u32 out;
+                    if (alpha == f.p - 1) out = submod(cv, r, f);
+                    else if (alpha == 1) out = addmod(cv, r, f);
+                    else out = addmod(cv, mulmod(r, alpha, f), f);
+                    outv[t] = out;
+                }
+                if (full) {  // row layout -> coalesced stores through the staging block
+                    __syncwarp();
+#pragma unroll
+                    for (int v = 0; v < 4; ++v)
+                        *reinterpret_cast<uint4*>(stg + stg_off(lane, v)) =
+                            make_uint4(outv[4 * v], outv[4 * v + 1], outv[4 * v + 2], outv[4 * v + 3]);
+                    __syncwarp();
+#pragma unroll
+                    for (int it = 0; it < 4; ++it) {
+                        const int rr = it * 8 + crow_c;
+                        const uint4 t4 = *reinterpret_cast<const uint4*>(stg + stg_off(rr, cgrp));
+                        if (rr < rows_here)
+                            *reinterpret_cast<uint4*>(cbase + (i64)rr * g.ldc + ch * 16 + 4 * cgrp) = t4;
+                    }
+                } else if (vrow) {
+#pragma unroll
+                    for (int t = 0; t < 16; ++t)
+                        if (c0 + t < N) crow[ch * 16 + t] = outv[t];
                 }
             }
             ptx::tc_fence_before();
