@@ -82,27 +82,41 @@ __global__ void __launch_bounds__(256) swaps_kernel(SwapJobs jobs) {
     for (int q = 0; q < jobs.n; ++q) swap_job(jobs.job[q], list, warp_cnt);
 }
 
+// One CTA per 32-column block.  The moves "row j <- row rrp[j] on columns > j,
+// source zeroed" of a chunk of (up to 256) non-trivial pivots are done in three
+// parallel phases: read every source (they are original rows: rrp is strictly
+// increasing and rrp[j] >= j, so no earlier move wrote them), zero the sources,
+// write the destinations (a destination that is also a source of the same
+// chunk is zeroed first, as in the sequential order).  Many independent
+// coalesced loads are in flight instead of one dependent load per pivot.
 __global__ void __launch_bounds__(256) compact_kernel(u32* A, i64 lda, i32 m, i32 n, const i32* rp,
                                                       const i32* rrp) {
     __shared__ i32 list[256];
     __shared__ int warp_cnt[8];
+    __shared__ u32 S[256][32];
     pdl_wait();
     pdl_trigger();
     const i32 r = __ldcg(rp + m);
-    const i32 c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const i32 c = blockIdx.x * 32 + lane;
     for (i32 j0 = 0; j0 < r; j0 += 256) {
-        if (j0 >= (i32)((blockIdx.x + 1) * blockDim.x)) break;  // uniform: no column here > j0
+        if (j0 >= (i32)((blockIdx.x + 1) * 32)) break;  // uniform: no column here > j0
         const int cnt = collect_ordered(
             j0, min(r, j0 + 256), [rrp](i32 j) { return __ldcg(rrp + j) != j; }, list, warp_cnt);
-        if (c < n) {
-            for (int q = 0; q < cnt; ++q) {
-                const i32 j = list[q];
-                if (c > j) {
-                    const i32 src = __ldcg(rrp + j);
-                    A[(i64)j * lda + c] = A[(i64)src * lda + c];
-                    A[(i64)src * lda + c] = 0;
-                }
-            }
+        if (cnt == 0) continue;  // uniform
+        for (int q = warp; q < cnt; q += 8) {
+            const i32 j = list[q];
+            if (c < n && c > j) S[q][lane] = A[(i64)__ldcg(rrp + j) * lda + c];
+        }
+        __syncthreads();
+        for (int q = warp; q < cnt; q += 8) {
+            const i32 j = list[q];
+            if (c < n && c > j) A[(i64)__ldcg(rrp + j) * lda + c] = 0;
+        }
+        __syncthreads();
+        for (int q = warp; q < cnt; q += 8) {
+            const i32 j = list[q];
+            if (c < n && c > j) A[(i64)j * lda + c] = S[q][lane];
         }
         __syncthreads();
     }
@@ -137,7 +151,7 @@ void compact_u_rows(u32* A, i64 lda, i32 m, i32 n, const i32* rp, const i32* rrp
                     cudaStream_t s) {
     if (m <= 0 || n <= 0) return;
     RL_ONCE_MAX_SMEM(compact_kernel);
-    launch_pdl(compact_kernel, dim3((n + 255) / 256), dim3(256), 0, s, A, lda, m, n, rp, rrp);
+    launch_pdl(compact_kernel, dim3((n + 31) / 32), dim3(256), 0, s, A, lda, m, n, rp, rrp);
     RL_CUDA_CHECK(cudaGetLastError());
 }
 
