@@ -95,16 +95,17 @@ int guard(F&& f) {
 struct Key {
     i64 m, n, lda;
     u32 p;
+    bool split = false;  // host-buffer engine with the split H2D wait
     bool operator<(const Key& o) const {
-        return std::tie(m, n, lda, p) < std::tie(o.m, o.n, o.lda, o.p);
+        return std::tie(m, n, lda, p, split) < std::tie(o.m, o.n, o.lda, o.p, o.split);
     }
 };
 
 std::mutex g_mu;
 std::map<Key, std::unique_ptr<CupEngine>> g_engines;
 
-CupEngine& engine_for(i64 m, i64 n, i64 lda, u32 p) {
-    Key k{m, n, lda, p};
+CupEngine& engine_for(i64 m, i64 n, i64 lda, u32 p, bool split = false) {
+    Key k{m, n, lda, p, split};
     auto it = g_engines.find(k);
     if (it != g_engines.end()) return *it->second;
     if (g_engines.size() > 16) g_engines.clear();
@@ -406,11 +407,55 @@ int rl_cup_u32(uint32_t* A, int64_t m, int64_t n, int64_t lda, uint32_t p, int64
         std::lock_guard<std::mutex> lk(g_mu);
         cudaStream_t s = cudaStreamPerThread;
         u32* dA = (u32*)g_bufA.get((size_t)m * n * 4);
-        copy_h2d_2d(dA, n, A, lda, m, n, s);
         i64 r = 0;
         std::vector<u32> rrp_h, ipiv_h;
-        factor_on_device(dA, m, n, n, p, s, &r, rrp_h, ipiv_h);
-        copy_d2h_2d(A, lda, dA, n, m, n, s);
+        if (m * n >= (1 << 22) && m >= 256) {
+            // Rows [0, m/4) are copied first and factored while the rest is still
+            // crossing PCIe (in order, on a second stream: sharing the link would
+            // only delay the first quarter); the launch sequence waits for rows
+            // [m/4, m/2) at the top half's split and for [m/2, m) at the root's
+            // (the splits of factor.cpp:35), right before it first touches them.
+            static cudaStream_t cs = nullptr;
+            static cudaStream_t cs2 = nullptr;
+            static cudaEvent_t ev_h = nullptr, ev_q = nullptr, top = nullptr, done = nullptr;
+            if (!cs) {
+                RL_CUDA_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+                RL_CUDA_CHECK(cudaStreamCreateWithFlags(&cs2, cudaStreamNonBlocking));
+                RL_CUDA_CHECK(cudaEventCreateWithFlags(&ev_h, cudaEventDisableTiming));
+                RL_CUDA_CHECK(cudaEventCreateWithFlags(&ev_q, cudaEventDisableTiming));
+                RL_CUDA_CHECK(cudaEventCreateWithFlags(&top, cudaEventDisableTiming));
+                RL_CUDA_CHECK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+            }
+            const i64 k = m / 2, kq = k / 2;
+            copy_h2d_2d(dA, n, A, lda, kq, n, s);
+            RL_CUDA_CHECK(cudaEventRecord(top, s));
+            RL_CUDA_CHECK(cudaStreamWaitEvent(cs, top, 0));
+            copy_h2d_2d(dA + kq * n, n, A + kq * lda, lda, k - kq, n, cs);
+            RL_CUDA_CHECK(cudaEventRecord(ev_q, cs));
+            copy_h2d_2d(dA + k * n, n, A + k * lda, lda, m - k, n, cs);
+            RL_CUDA_CHECK(cudaEventRecord(ev_h, cs));
+            const i64 kcap = std::min(m, n);
+            rrp_h.assign((size_t)kcap, 0);
+            ipiv_h.assign((size_t)kcap, 0);
+            CupEngine& e = engine_for(m, n, n, p, true);
+            e.set_split_wait(ev_h, ev_q, done);
+            e.run(dA, s, true);
+            // the top half goes back while the bottom half is factored
+            RL_CUDA_CHECK(cudaStreamWaitEvent(cs2, done, 0));
+            copy_d2h_2d(A, lda, dA, n, k, n, cs2);
+            e.results(&r, rrp_h.data(), ipiv_h.data(), s);  // synchronises s
+            copy_d2h_2d(A + k * lda, lda, dA + k * n, n, m - k, n, s);
+            RL_CUDA_CHECK(cudaStreamSynchronize(cs2));
+            // rows [0, m/2) were final at that point unless a later transposition
+            // (sigma) or a U-row move (row profile) reached them: then copy again
+            bool ident = true;
+            for (i64 j = 0; j < r && ident; ++j) ident = ipiv_h[(size_t)j] == (u32)j && rrp_h[(size_t)j] == (u32)j;
+            if (!ident) copy_d2h_2d(A, lda, dA, n, k, n, s);
+        } else {
+            copy_h2d_2d(dA, n, A, lda, m, n, s);
+            factor_on_device(dA, m, n, n, p, s, &r, rrp_h, ipiv_h);
+            copy_d2h_2d(A, lda, dA, n, m, n, s);
+        }
         RL_CUDA_CHECK(cudaStreamSynchronize(s));
         if (rank) *rank = r;
         if (rrp) std::copy(rrp_h.begin(), rrp_h.begin() + r, rrp);

@@ -353,6 +353,14 @@ void CupEngine::node(i32 i0, i32 mm) {
     }
     const i32 k = mm / 2;                    // factor.cpp:35
     node(i0, k);                             // factor.cpp:39
+    if (!dry_ && i0 == 0) {  // rows below this split may still be arriving from the host
+        if (mm == m_ && split_done_) {  // the top half is factored: its copy back may start
+            flush_swaps();
+            RL_CUDA_CHECK(cudaEventRecordWithFlags(split_done_, s_, cudaEventRecordExternal));
+        }
+        cudaEvent_t ev = mm == m_ ? split_wait_ : (mm == m_ / 2 ? split_wait_q_ : nullptr);
+        if (ev) RL_CUDA_CHECK(cudaStreamWaitEvent(s_, ev, cudaEventWaitExternal));
+    }
     const i32 b0 = i0 + k, bm = mm - k;
     swaps_range(b0, bm, dyn_rp(i0), dyn_rp(b0));                     // factor.cpp:42
     if (!dry_ && uinv_join_) {
@@ -401,6 +409,18 @@ void CupEngine::enqueue(u32* dA, cudaStream_t s) {
         flush_swaps();
         compact_u_rows(A_, lda_, m_, n_, rp_, rrp_, s);
         stats_.launches += 1;
+    }
+}
+
+void CupEngine::set_split_wait(cudaEvent_t ev_half, cudaEvent_t ev_quarter, cudaEvent_t ev_top_done) {
+    if (ev_half == split_wait_ && ev_quarter == split_wait_q_ && ev_top_done == split_done_) return;
+    split_wait_ = ev_half;
+    split_wait_q_ = ev_quarter;
+    split_done_ = ev_top_done;
+    if (graph_exec_) {  // the captured sequence no longer matches
+        cudaGraphExecDestroy(graph_exec_);
+        graph_exec_ = nullptr;
+        graph_A_ = nullptr;
     }
 }
 

@@ -300,3 +300,24 @@ def test_cup_strided_view_large():
     assert r.rank == o.rank and np.array_equal(r.col_perm, o.sigma)
     assert np.array_equal(full[:, :n].cpu().numpy().view(np.uint32), o_body)
     assert torch.equal(full[:, n:], untouched)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n,p,rank", [(2048, 3000, 65521, None), (3000, 2048, 65521, 1500),
+                                        (4096, 1100, 8388593, None)])
+def test_host_path_split_copy_equals_device_path(m, n, p, rank):
+    """rl_cup_u32 overlaps the H2D copy of the rows below the root split with the
+    top half's factorization (external event wait inside the captured graph):
+    same bytes as the device-resident path, twice (graph replay)."""
+    import torch
+    a = O.port_random_matrix(m, n, 41, p) if rank is None else O.ref_random_rank_matrix(m, n, rank, 42, p)
+    d = torch.from_numpy(a.view(np.int32).copy()).cuda()
+    g_dev = G.cup_dev(d, m, n, p)
+    ref = d.cpu().numpy().view(np.uint32)
+    for _ in range(2):
+        h = a.copy()
+        g = G.cup(h, p)
+        assert g.rank == g_dev.rank
+        assert np.array_equal(g.row_profile, g_dev.row_profile)
+        assert np.array_equal(g.col_perm, g_dev.col_perm)
+        assert np.array_equal(h, ref)
