@@ -417,7 +417,7 @@ int rl_cup_u32(uint32_t* A, int64_t m, int64_t n, int64_t lda, uint32_t p, int64
             // (the splits of factor.cpp:35), right before it first touches them.
             static cudaStream_t cs = nullptr;
             static cudaStream_t cs2 = nullptr;
-            static cudaEvent_t ev_h = nullptr, ev_q = nullptr, top = nullptr, done = nullptr;
+            static cudaEvent_t ev_h = nullptr, ev_q = nullptr, top = nullptr, done = nullptr, done_b = nullptr;
             if (!cs) {
                 RL_CUDA_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
                 RL_CUDA_CHECK(cudaStreamCreateWithFlags(&cs2, cudaStreamNonBlocking));
@@ -425,6 +425,7 @@ int rl_cup_u32(uint32_t* A, int64_t m, int64_t n, int64_t lda, uint32_t p, int64
                 RL_CUDA_CHECK(cudaEventCreateWithFlags(&ev_q, cudaEventDisableTiming));
                 RL_CUDA_CHECK(cudaEventCreateWithFlags(&top, cudaEventDisableTiming));
                 RL_CUDA_CHECK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+                RL_CUDA_CHECK(cudaEventCreateWithFlags(&done_b, cudaEventDisableTiming));
             }
             const i64 k = m / 2, kq = k / 2;
             copy_h2d_2d(dA, n, A, lda, kq, n, s);
@@ -438,19 +439,24 @@ int rl_cup_u32(uint32_t* A, int64_t m, int64_t n, int64_t lda, uint32_t p, int64
             rrp_h.assign((size_t)kcap, 0);
             ipiv_h.assign((size_t)kcap, 0);
             CupEngine& e = engine_for(m, n, n, p, true);
-            e.set_split_wait(ev_h, ev_q, done);
+            e.set_split_wait(ev_h, ev_q, done, done_b);
             e.run(dA, s, true);
-            // the top half goes back while the bottom half is factored
+            // the top half goes back while the bottom half is factored, then rows
+            // [m/2, m/2 + kb) while the last quarter is
+            const i64 kb = (m - k) / 2;
             RL_CUDA_CHECK(cudaStreamWaitEvent(cs2, done, 0));
             copy_d2h_2d(A, lda, dA, n, k, n, cs2);
+            RL_CUDA_CHECK(cudaStreamWaitEvent(cs2, done_b, 0));
+            copy_d2h_2d(A + k * lda, lda, dA + k * n, n, kb, n, cs2);
             e.results(&r, rrp_h.data(), ipiv_h.data(), s);  // synchronises s
-            copy_d2h_2d(A + k * lda, lda, dA + k * n, n, m - k, n, s);
+            copy_d2h_2d(A + (k + kb) * lda, lda, dA + (k + kb) * n, n, m - k - kb, n, s);
             RL_CUDA_CHECK(cudaStreamSynchronize(cs2));
-            // rows [0, m/2) were final at that point unless a later transposition
-            // (sigma) or a U-row move (row profile) reached them: then copy again
+            // rows [0, m/2 + kb) were final at that point unless a later
+            // transposition (sigma) or a U-row move (row profile) reached them:
+            // then copy them again
             bool ident = true;
             for (i64 j = 0; j < r && ident; ++j) ident = ipiv_h[(size_t)j] == (u32)j && rrp_h[(size_t)j] == (u32)j;
-            if (!ident) copy_d2h_2d(A, lda, dA, n, k, n, s);
+            if (!ident) copy_d2h_2d(A, lda, dA, n, k + kb, n, s);
         } else {
             copy_h2d_2d(dA, n, A, lda, m, n, s);
             factor_on_device(dA, m, n, n, p, s, &r, rrp_h, ipiv_h);

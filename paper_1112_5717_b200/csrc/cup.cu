@@ -361,6 +361,10 @@ void CupEngine::node(i32 i0, i32 mm) {
         cudaEvent_t ev = mm == m_ ? split_wait_ : (mm == m_ / 2 ? split_wait_q_ : nullptr);
         if (ev) RL_CUDA_CHECK(cudaStreamWaitEvent(s_, ev, cudaEventWaitExternal));
     }
+    if (!dry_ && split_done_b_ && i0 == m_ / 2 && mm == m_ - m_ / 2) {  // rows [m/2, m/2 + k) factored
+        flush_swaps();
+        RL_CUDA_CHECK(cudaEventRecordWithFlags(split_done_b_, s_, cudaEventRecordExternal));
+    }
     const i32 b0 = i0 + k, bm = mm - k;
     swaps_range(b0, bm, dyn_rp(i0), dyn_rp(b0));                     // factor.cpp:42
     if (!dry_ && uinv_join_) {
@@ -412,8 +416,12 @@ void CupEngine::enqueue(u32* dA, cudaStream_t s) {
     }
 }
 
-void CupEngine::set_split_wait(cudaEvent_t ev_half, cudaEvent_t ev_quarter, cudaEvent_t ev_top_done) {
-    if (ev_half == split_wait_ && ev_quarter == split_wait_q_ && ev_top_done == split_done_) return;
+void CupEngine::set_split_wait(cudaEvent_t ev_half, cudaEvent_t ev_quarter, cudaEvent_t ev_top_done,
+                               cudaEvent_t ev_bq_done) {
+    if (ev_half == split_wait_ && ev_quarter == split_wait_q_ && ev_top_done == split_done_ &&
+        ev_bq_done == split_done_b_)
+        return;
+    split_done_b_ = ev_bq_done;
     split_wait_ = ev_half;
     split_wait_q_ = ev_quarter;
     split_done_ = ev_top_done;

@@ -50,7 +50,9 @@ public:
     // the row profile are the identity; the caller checks and re-copies
     // otherwise).  Captured as external event nodes: the events must outlive
     // the engine's graph.
-    void set_split_wait(cudaEvent_t ev_half, cudaEvent_t ev_quarter, cudaEvent_t ev_top_done);
+    // ev_bq_done: the same for rows [m/2, 3m/4) once the bottom half's top half is factored.
+    void set_split_wait(cudaEvent_t ev_half, cudaEvent_t ev_quarter, cudaEvent_t ev_top_done,
+                        cudaEvent_t ev_bq_done);
 
 private:
     void enqueue(u32* dA, cudaStream_t s);
@@ -88,7 +90,7 @@ private:
     // Schur updates with K <= this are split (window slice first, rest on s2_);
     // above it the extra narrow GEMM costs more than the overlap wins
     i32 split_max_k_ = 1024;
-    cudaEvent_t split_wait_ = nullptr, split_wait_q_ = nullptr, split_done_ = nullptr;
+    cudaEvent_t split_wait_ = nullptr, split_wait_q_ = nullptr, split_done_ = nullptr, split_done_b_ = nullptr;
     void* meta_ = nullptr;                     // one allocation for everything below
     i32* rp_ = nullptr;
     i32* rrp_ = nullptr;
