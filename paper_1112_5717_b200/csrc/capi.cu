@@ -409,54 +409,66 @@ int rl_cup_u32(uint32_t* A, int64_t m, int64_t n, int64_t lda, uint32_t p, int64
         u32* dA = (u32*)g_bufA.get((size_t)m * n * 4);
         i64 r = 0;
         std::vector<u32> rrp_h, ipiv_h;
-        if (m * n >= (1 << 22) && m >= 256) {
-            // Rows [0, m/4) are copied first and factored while the rest is still
-            // crossing PCIe (in order, on a second stream: sharing the link would
-            // only delay the first quarter); the launch sequence waits for rows
-            // [m/4, m/2) at the top half's split and for [m/2, m) at the root's
-            // (the splits of factor.cpp:35), right before it first touches them.
-            static cudaStream_t cs = nullptr;
-            static cudaStream_t cs2 = nullptr;
-            static cudaEvent_t ev_h = nullptr, ev_q = nullptr, top = nullptr, done = nullptr, done_b = nullptr;
+        if (m * n >= (1 << 22) && m >= 8 * PB) {  // every spine node below splits (> PB rows)
+            // PCIe overlapped with the factorization along the recursion's spines
+            // (the splits of factor.cpp:35).  In: rows [0, m/2^D) are copied first
+            // and factored while the rest crosses the link in order on a second
+            // stream; each left-spine node (0, mm) waits for its bottom rows right
+            // before it first touches them.  Out: each right-spine node's top half
+            // goes back as soon as it is factored (final unless a later
+            // transposition or U-row move reaches it: then it is copied again).
+            constexpr int D = 3;
+            static cudaStream_t cs = nullptr, cs2 = nullptr;
+            static cudaEvent_t top = nullptr;
+            static std::vector<cudaEvent_t> evw, evd;
             if (!cs) {
                 RL_CUDA_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
                 RL_CUDA_CHECK(cudaStreamCreateWithFlags(&cs2, cudaStreamNonBlocking));
-                RL_CUDA_CHECK(cudaEventCreateWithFlags(&ev_h, cudaEventDisableTiming));
-                RL_CUDA_CHECK(cudaEventCreateWithFlags(&ev_q, cudaEventDisableTiming));
                 RL_CUDA_CHECK(cudaEventCreateWithFlags(&top, cudaEventDisableTiming));
-                RL_CUDA_CHECK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
-                RL_CUDA_CHECK(cudaEventCreateWithFlags(&done_b, cudaEventDisableTiming));
+                evw.resize(D);
+                evd.resize(D);
+                for (int d = 0; d < D; ++d) {
+                    RL_CUDA_CHECK(cudaEventCreateWithFlags(&evw[d], cudaEventDisableTiming));
+                    RL_CUDA_CHECK(cudaEventCreateWithFlags(&evd[d], cudaEventDisableTiming));
+                }
             }
-            const i64 k = m / 2, kq = k / 2;
-            copy_h2d_2d(dA, n, A, lda, kq, n, s);
+            CupEngine::NodeEvents waits, dones;
+            // left spine: node (0, sz[d]), sz[0] = m, sz[d+1] = sz[d] / 2
+            i64 sz[D + 1];
+            sz[0] = m;
+            for (int d = 0; d < D; ++d) sz[d + 1] = sz[d] / 2;
+            copy_h2d_2d(dA, n, A, lda, sz[D], n, s);
             RL_CUDA_CHECK(cudaEventRecord(top, s));
             RL_CUDA_CHECK(cudaStreamWaitEvent(cs, top, 0));
-            copy_h2d_2d(dA + kq * n, n, A + kq * lda, lda, k - kq, n, cs);
-            RL_CUDA_CHECK(cudaEventRecord(ev_q, cs));
-            copy_h2d_2d(dA + k * n, n, A + k * lda, lda, m - k, n, cs);
-            RL_CUDA_CHECK(cudaEventRecord(ev_h, cs));
+            for (int d = D - 1; d >= 0; --d) {
+                copy_h2d_2d(dA + sz[d + 1] * n, n, A + sz[d + 1] * lda, lda, sz[d] - sz[d + 1], n, cs);
+                RL_CUDA_CHECK(cudaEventRecord(evw[d], cs));
+                waits[{0, (i32)sz[d]}] = evw[d];
+            }
+            // right spine: node (lo[d], len[d]); its top half [lo, lo + len/2) goes back
+            i64 lo[D], len[D], cut = 0;
+            for (int d = 0; d < D; ++d) {
+                lo[d] = d == 0 ? 0 : lo[d - 1] + len[d - 1] / 2;
+                len[d] = d == 0 ? m : len[d - 1] - len[d - 1] / 2;
+                dones[{(i32)lo[d], (i32)len[d]}] = evd[d];
+            }
             const i64 kcap = std::min(m, n);
             rrp_h.assign((size_t)kcap, 0);
             ipiv_h.assign((size_t)kcap, 0);
             CupEngine& e = engine_for(m, n, n, p, true);
-            e.set_split_wait(ev_h, ev_q, done, done_b);
+            e.set_host_overlap(waits, dones);
             e.run(dA, s, true);
-            // the top half goes back while the bottom half is factored, then rows
-            // [m/2, m/2 + kb) while the last quarter is
-            const i64 kb = (m - k) / 2;
-            RL_CUDA_CHECK(cudaStreamWaitEvent(cs2, done, 0));
-            copy_d2h_2d(A, lda, dA, n, k, n, cs2);
-            RL_CUDA_CHECK(cudaStreamWaitEvent(cs2, done_b, 0));
-            copy_d2h_2d(A + k * lda, lda, dA + k * n, n, kb, n, cs2);
+            for (int d = 0; d < D; ++d) {
+                RL_CUDA_CHECK(cudaStreamWaitEvent(cs2, evd[d], 0));
+                copy_d2h_2d(A + lo[d] * lda, lda, dA + lo[d] * n, n, len[d] / 2, n, cs2);
+                cut = lo[d] + len[d] / 2;
+            }
             e.results(&r, rrp_h.data(), ipiv_h.data(), s);  // synchronises s
-            copy_d2h_2d(A + (k + kb) * lda, lda, dA + (k + kb) * n, n, m - k - kb, n, s);
+            copy_d2h_2d(A + cut * lda, lda, dA + cut * n, n, m - cut, n, s);
             RL_CUDA_CHECK(cudaStreamSynchronize(cs2));
-            // rows [0, m/2 + kb) were final at that point unless a later
-            // transposition (sigma) or a U-row move (row profile) reached them:
-            // then copy them again
             bool ident = true;
             for (i64 j = 0; j < r && ident; ++j) ident = ipiv_h[(size_t)j] == (u32)j && rrp_h[(size_t)j] == (u32)j;
-            if (!ident) copy_d2h_2d(A, lda, dA, n, k + kb, n, s);
+            if (!ident) copy_d2h_2d(A, lda, dA, n, cut, n, s);
         } else {
             copy_h2d_2d(dA, n, A, lda, m, n, s);
             factor_on_device(dA, m, n, n, p, s, &r, rrp_h, ipiv_h);

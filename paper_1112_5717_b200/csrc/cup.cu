@@ -353,17 +353,16 @@ void CupEngine::node(i32 i0, i32 mm) {
     }
     const i32 k = mm / 2;                    // factor.cpp:35
     node(i0, k);                             // factor.cpp:39
-    if (!dry_ && i0 == 0) {  // rows below this split may still be arriving from the host
-        if (mm == m_ && split_done_) {  // the top half is factored: its copy back may start
+    if (!dry_ && !dones_.empty()) {  // this node's top half is factored
+        auto it = dones_.find({i0, mm});
+        if (it != dones_.end()) {
             flush_swaps();
-            RL_CUDA_CHECK(cudaEventRecordWithFlags(split_done_, s_, cudaEventRecordExternal));
+            RL_CUDA_CHECK(cudaEventRecordWithFlags(it->second, s_, cudaEventRecordExternal));
         }
-        cudaEvent_t ev = mm == m_ ? split_wait_ : (mm == m_ / 2 ? split_wait_q_ : nullptr);
-        if (ev) RL_CUDA_CHECK(cudaStreamWaitEvent(s_, ev, cudaEventWaitExternal));
     }
-    if (!dry_ && split_done_b_ && i0 == m_ / 2 && mm == m_ - m_ / 2) {  // rows [m/2, m/2 + k) factored
-        flush_swaps();
-        RL_CUDA_CHECK(cudaEventRecordWithFlags(split_done_b_, s_, cudaEventRecordExternal));
+    if (!dry_ && !waits_.empty()) {  // its bottom rows may still be arriving from the host
+        auto it = waits_.find({i0, mm});
+        if (it != waits_.end()) RL_CUDA_CHECK(cudaStreamWaitEvent(s_, it->second, cudaEventWaitExternal));
     }
     const i32 b0 = i0 + k, bm = mm - k;
     swaps_range(b0, bm, dyn_rp(i0), dyn_rp(b0));                     // factor.cpp:42
@@ -416,15 +415,10 @@ void CupEngine::enqueue(u32* dA, cudaStream_t s) {
     }
 }
 
-void CupEngine::set_split_wait(cudaEvent_t ev_half, cudaEvent_t ev_quarter, cudaEvent_t ev_top_done,
-                               cudaEvent_t ev_bq_done) {
-    if (ev_half == split_wait_ && ev_quarter == split_wait_q_ && ev_top_done == split_done_ &&
-        ev_bq_done == split_done_b_)
-        return;
-    split_done_b_ = ev_bq_done;
-    split_wait_ = ev_half;
-    split_wait_q_ = ev_quarter;
-    split_done_ = ev_top_done;
+void CupEngine::set_host_overlap(const NodeEvents& waits, const NodeEvents& dones) {
+    if (waits == waits_ && dones == dones_) return;
+    waits_ = waits;
+    dones_ = dones;
     if (graph_exec_) {  // the captured sequence no longer matches
         cudaGraphExecDestroy(graph_exec_);
         graph_exec_ = nullptr;

@@ -40,19 +40,16 @@ public:
     int limbs() const { return L_; }
     size_t workspace_bytes() const { return a2_cap_ + b2_cap_; }
     void set_use_tc(bool v) { use_tc_ = v; }
-    // Host-buffer path: the rows below the root split (m/2), and those below
-    // the top half's split (m/4), may still be in flight from the host when the
-    // factorization starts; the launch sequence waits on ev_half (rows
-    // [m/2, m)) / ev_quarter (rows [m/4, m/2)) right before it first touches
-    // them.  ev_top_done is recorded when the top half (rows [0, m/2)) is
-    // factored, so its copy back can start while the bottom half runs (valid
-    // when no later transposition or U-row move touches those rows: sigma and
-    // the row profile are the identity; the caller checks and re-copies
-    // otherwise).  Captured as external event nodes: the events must outlive
-    // the engine's graph.
-    // ev_bq_done: the same for rows [m/2, 3m/4) once the bottom half's top half is factored.
-    void set_split_wait(cudaEvent_t ev_half, cudaEvent_t ev_quarter, cudaEvent_t ev_top_done,
-                        cudaEvent_t ev_bq_done);
+    // Host-buffer path (PCIe overlapped with the factorization).  waits: node
+    // (i0, mm) -> event the launch sequence waits on right after that node's top
+    // half, before it first touches the node's bottom rows (they may still be
+    // arriving from the host).  dones: node -> event recorded once the node's
+    // top half is factored (its rows may go back to the host while the rest
+    // runs; valid when no later transposition or U-row move reaches them --
+    // sigma and the row profile are the identity -- which the caller checks).
+    // Captured as external event nodes: the events must outlive the graph.
+    using NodeEvents = std::map<std::pair<i32, i32>, cudaEvent_t>;
+    void set_host_overlap(const NodeEvents& waits, const NodeEvents& dones);
 
 private:
     void enqueue(u32* dA, cudaStream_t s);
@@ -90,7 +87,7 @@ private:
     // Schur updates with K <= this are split (window slice first, rest on s2_);
     // above it the extra narrow GEMM costs more than the overlap wins
     i32 split_max_k_ = 1024;
-    cudaEvent_t split_wait_ = nullptr, split_wait_q_ = nullptr, split_done_ = nullptr, split_done_b_ = nullptr;
+    NodeEvents waits_, dones_;
     void* meta_ = nullptr;                     // one allocation for everything below
     i32* rp_ = nullptr;
     i32* rrp_ = nullptr;

@@ -303,7 +303,7 @@ def test_cup_strided_view_large():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("m,n,p,rank", [(2048, 3000, 65521, None), (3000, 2048, 65521, 1500),
+@pytest.mark.parametrize("m,n,p,rank", [(2048, 3000, 65521, None), (3000, 2048, 65521, 1500), (520, 8100, 65521, None),
                                         (4096, 1100, 8388593, None)])
 def test_host_path_split_copy_equals_device_path(m, n, p, rank):
     """rl_cup_u32 overlaps the H2D copy of the rows below the root split with the
