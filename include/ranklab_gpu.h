@@ -73,6 +73,11 @@ int rl_ple_u32_dev(uint32_t* dA, int64_t m, int64_t n, int64_t lda, uint32_t p,
 int rl_cup_batched_u32_dev(uint32_t* dA, int64_t batch, int64_t m, int64_t n, int64_t stride,
                            uint32_t p, int64_t* ranks, uint32_t* rrp, uint32_t* sigma,
                            void* stream);
+/* Same on HOST matrices (in place): the batch is copied in, factored and copied
+ * back in chunks on three streams (PCIe both ways overlapped with the factoring;
+ * pinned host memory gets the full link rate). */
+int rl_cup_batched_u32(uint32_t* A, int64_t batch, int64_t m, int64_t n, int64_t stride,
+                       uint32_t p, int64_t* ranks, uint32_t* rrp, uint32_t* sigma);
 
 /* C <- alpha*A*B + beta*C (mod p); A m x l, B l x n, C m x n.
  * Replaces: void ranklab::mm(ConstMatView a, ConstMatView b, MatView c,

@@ -36,7 +36,7 @@ import numpy as np
 
 __all__ = [
     "Error", "DimensionMismatch", "OverlapError", "SingularMatrix", "NotPrime", "CudaError",
-    "OpCounter", "PackedCup", "cup", "cup_dev", "cup_batched_dev", "mm", "mm_dev",
+    "OpCounter", "PackedCup", "cup", "cup_dev", "cup_batched_dev", "cup_batched", "mm", "mm_dev",
     "rank_and_profile", "determinant", "random_matrix_dev", "LIB_PATH", "lib",
     "EchelonTransform", "ReducedEchelonTransform", "col_ech_trans", "red_col_ech_trans",
     "col_ech_trans_dev", "invert_in_place", "invert_dev", "trsm", "trsm_dev",
@@ -128,7 +128,7 @@ _u32 = C.c_uint32
 _vp = C.c_void_p
 
 #: every symbol include/ranklab_gpu.h declares
-EXPORTS = ["rl_cup_u32", "rl_cup_u32_dev", "rl_cup_batched_u32_dev", "rl_mm_u32",
+EXPORTS = ["rl_cup_u32", "rl_cup_u32_dev", "rl_cup_batched_u32_dev", "rl_cup_batched_u32", "rl_mm_u32",
            "rl_mm_u32_dev", "rl_mm_u32_dev_grid", "rl_rank_and_profile_u32", "rl_determinant_u32",
            "rl_random_matrix_u32_dev", "rl_last_error", "rl_version", "rl_cup_plan_stats",
            "rl_profile_gemm_dev", "rl_cup_opcount", "rl_col_ech_trans_u32",
@@ -148,6 +148,7 @@ def lib():
     L.rl_cup_u32.argtypes = [_vp, _i64, _i64, _i64, _u32, C.POINTER(_i64), _vp, _vp, _vp]
     L.rl_cup_u32_dev.argtypes = [_vp, _i64, _i64, _i64, _u32, C.POINTER(_i64), _vp, _vp, _vp, _vp]
     L.rl_cup_batched_u32_dev.argtypes = [_vp, _i64, _i64, _i64, _i64, _u32, _vp, _vp, _vp, _vp]
+    L.rl_cup_batched_u32.argtypes = [_vp, _i64, _i64, _i64, _i64, _u32, _vp, _vp, _vp]
     L.rl_mm_u32.argtypes = [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _u32, _u32, _u32, _vp]
     L.rl_mm_u32_dev.argtypes = [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _u32, _u32, _u32,
                                 _vp]
@@ -302,6 +303,23 @@ def cup_batched_dev(d_a, batch: int, m: int, n: int, p: int, stride: int | None 
     _check(lib().rl_cup_batched_u32_dev(C.c_void_p(ptr), batch, m, n, stride, int(p), None, None,
                                         None, _stream_ptr(stream)))
     return None
+
+
+def cup_batched(a: np.ndarray, p: int):
+    """Batched in-place CUP of host matrices ``a`` (batch x m x n, uint32,
+    C-contiguous; pinned memory gets the full PCIe rate): copied in, factored and
+    copied back in overlapped chunks (rl_cup_batched_u32).  Returns
+    (ranks int64[batch], rrp uint32[batch, min(m,n)], sigma uint32[batch, n])."""
+    if a.dtype != np.uint32 or a.ndim != 3 or not a.flags.c_contiguous:
+        raise Error("cup_batched expects a C-contiguous uint32 array of shape (batch, m, n)")
+    batch, m, n = a.shape
+    k = max(1, min(m, n))
+    ranks = np.zeros(batch, np.int64)
+    rrp = np.zeros((batch, k), np.uint32)
+    sigma = np.zeros((batch, max(n, 1)), np.uint32)
+    _check(lib().rl_cup_batched_u32(_ptr(a), batch, m, n, m * n, int(p), _ptr(ranks), _ptr(rrp),
+                                    _ptr(sigma)))
+    return ranks, rrp, sigma[:, :n]
 
 
 def mm(a: np.ndarray, b: np.ndarray, c: np.ndarray, alpha: int, beta: int, p: int,

@@ -834,6 +834,77 @@ int rl_cup_batched_u32_dev(uint32_t* dA, int64_t batch, int64_t m, int64_t n, in
     });
 }
 
+// Batched CUP of host-resident matrices: the batch crosses PCIe in chunks on a
+// copy stream, each chunk is factored as soon as it has landed and goes back on
+// a second copy stream while the next one is factored (three-stage pipeline;
+// both link directions and the SMs busy at once).
+int rl_cup_batched_u32(uint32_t* A, int64_t batch, int64_t m, int64_t n, int64_t stride, uint32_t p,
+                       int64_t* ranks, uint32_t* rrp, uint32_t* sigma) {
+    return guard([&] {
+        check_field(p);
+        check_dims(m, n, n);
+        if (batch < 0) throw Error(RL_EDIM, "negative batch");
+        if (stride < m * n) throw Error(RL_EINVAL, "stride smaller than m*n");
+        const i64 kcap = std::max<i64>(1, std::min(m, n));
+        if (batch == 0) return;
+        if (m == 0 || n == 0) {
+            for (i64 t = 0; t < batch; ++t) {
+                if (ranks) ranks[t] = 0;
+                if (sigma) for (i64 j = 0; j < n; ++j) sigma[t * n + j] = (u32)j;
+            }
+            return;
+        }
+        if (!A) throw Error(RL_EINVAL, "null matrix");
+        require_device();
+        std::lock_guard<std::mutex> lk(g_mu);
+        static cudaStream_t sh = nullptr, sc = nullptr, sd = nullptr;
+        if (!sh) {
+            RL_CUDA_CHECK(cudaStreamCreateWithFlags(&sh, cudaStreamNonBlocking));
+            RL_CUDA_CHECK(cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking));
+            RL_CUDA_CHECK(cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking));
+        }
+        u32* dA = (u32*)g_bufA.get((size_t)batch * stride * 4);
+        i32* dmeta = (i32*)g_bufI.get((size_t)batch * (1 + 2 * kcap) * 4);
+        i32* d_ranks = dmeta;
+        i32* d_rrp = dmeta + batch;
+        i32* d_ipiv = d_rrp + batch * kcap;
+        const i64 chunks = std::min<i64>(batch, 8);
+        std::vector<cudaEvent_t> ev_in((size_t)chunks), ev_out((size_t)chunks);
+        for (i64 c = 0; c < chunks; ++c) {
+            RL_CUDA_CHECK(cudaEventCreateWithFlags(&ev_in[c], cudaEventDisableTiming));
+            RL_CUDA_CHECK(cudaEventCreateWithFlags(&ev_out[c], cudaEventDisableTiming));
+        }
+        for (i64 c = 0; c < chunks; ++c) {
+            const i64 t0 = batch * c / chunks, t1 = batch * (c + 1) / chunks;
+            const size_t bytes = (size_t)(t1 - t0) * stride * 4;
+            RL_CUDA_CHECK(cudaMemcpyAsync(dA + t0 * stride, A + t0 * stride, bytes, cudaMemcpyHostToDevice, sh));
+            RL_CUDA_CHECK(cudaEventRecord(ev_in[c], sh));
+            RL_CUDA_CHECK(cudaStreamWaitEvent(sc, ev_in[c], 0));
+            cup_batched(dA + t0 * stride, t1 - t0, (i32)m, (i32)n, stride, p, d_ranks + t0,
+                        d_rrp + t0 * kcap, d_ipiv + t0 * kcap, (i32)kcap, sc);
+            RL_CUDA_CHECK(cudaEventRecord(ev_out[c], sc));
+            RL_CUDA_CHECK(cudaStreamWaitEvent(sd, ev_out[c], 0));
+            RL_CUDA_CHECK(cudaMemcpyAsync(A + t0 * stride, dA + t0 * stride, bytes, cudaMemcpyDeviceToHost, sd));
+        }
+        std::vector<i32> h((size_t)batch * (1 + 2 * kcap));
+        RL_CUDA_CHECK(cudaMemcpyAsync(h.data(), dmeta, h.size() * 4, cudaMemcpyDeviceToHost, sc));
+        RL_CUDA_CHECK(cudaStreamSynchronize(sc));
+        RL_CUDA_CHECK(cudaStreamSynchronize(sd));
+        for (i64 c = 0; c < chunks; ++c) {
+            cudaEventDestroy(ev_in[c]);
+            cudaEventDestroy(ev_out[c]);
+        }
+        for (i64 t = 0; t < batch; ++t) {
+            const i64 r = h[t];
+            if (ranks) ranks[t] = r;
+            const u32* rp_t = (const u32*)&h[batch + t * kcap];
+            const u32* ip_t = (const u32*)&h[batch + batch * kcap + t * kcap];
+            if (rrp) for (i64 j = 0; j < r; ++j) rrp[t * kcap + j] = rp_t[j];
+            if (sigma) sigma_from_ipiv(n, r, ip_t, sigma + t * n);
+        }
+    });
+}
+
 // Times one mod-p GEMM C <- C - A*B (m x l x n) on device buffers: pack kernels
 // and the tcgen05 kernel separately, each averaged over `iters` launches with
 // CUDA events on `stream`.  For benchmarks / roofline only.

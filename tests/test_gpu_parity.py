@@ -321,3 +321,19 @@ def test_host_path_split_copy_equals_device_path(m, n, p, rank):
         assert np.array_equal(g.row_profile, g_dev.row_profile)
         assert np.array_equal(g.col_perm, g_dev.col_perm)
         assert np.array_equal(h, ref)
+
+
+@pytest.mark.gpu
+def test_batched_host_pipeline_equals_device_path():
+    """rl_cup_batched_u32 (host matrices, chunked copy/factor/copy pipeline) gives
+    the device path's bytes and metadata, for a batch that is not a multiple of
+    the chunk count."""
+    import torch
+    mats, _ = c4_batch(19)
+    a = np.ascontiguousarray(np.stack(mats)).astype(np.uint32)
+    d = torch.from_numpy(a.view(np.int32).copy()).cuda()
+    rk_d, rrp_d, sg_d = G.cup_batched_dev(d, a.shape[0], 256, 256, 8388593)
+    h = a.copy()
+    rk, rrp, sg = G.cup_batched(h, 8388593)
+    assert np.array_equal(rk, rk_d) and np.array_equal(rrp, rrp_d) and np.array_equal(sg, sg_d)
+    assert np.array_equal(h, d.cpu().numpy().view(np.uint32))
