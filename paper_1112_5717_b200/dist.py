@@ -128,8 +128,9 @@ def _comm():
 
 class _Engine:
     def __init__(self, x: torch.Tensor, m: int, n: int, tiles: ColumnTiles, ops, rank: int,
-                 dist):
+                 dist, p: int = 0):
         self.x, self.m, self.n, self.tiles, self.ops = x, m, n, tiles, ops
+        self.wire = torch.float16 if 0 < p <= 65536 else x.dtype
         self.rank, self.dist, self.world = rank, dist, tiles.world
         dev = x.device
         self.gpos_t = [torch.as_tensor(gp, dtype=torch.int64, device=dev) for gp in tiles.gpos]
@@ -154,12 +155,25 @@ class _Engine:
                 out.copy_(self.x[ra:rb, la:lb])
                 continue
             if g == self.rank:
-                piece = self.x[ra:rb, la:lb].contiguous()
+                piece = self._pack(self.x[ra:rb, la:lb])
             else:
-                piece = torch.empty((rb - ra, lb - la), dtype=self.x.dtype, device=self.x.device)
+                piece = torch.empty((rb - ra, lb - la), dtype=self.wire, device=self.x.device)
             self.dist.broadcast(piece, src=g)
-            out.index_copy_(1, self.gpos_t[g][la:lb] - c0, piece)
+            out.index_copy_(1, self.gpos_t[g][la:lb] - c0, self._unpack(piece))
         return out
+
+    # p <= 2^16: field elements cross the links as 16-bit words (half the
+    # NVLink volume of the broadcasts and gathers): x - 2^15 fits int16 exactly,
+    # carried bit for bit in a 16-bit float tensor (collectives only move bytes)
+    def _pack(self, t: torch.Tensor) -> torch.Tensor:
+        if self.wire == torch.float16:
+            return (t - 32768).to(torch.int16).view(torch.float16)
+        return t.contiguous()
+
+    def _unpack(self, t: torch.Tensor) -> torch.Tensor:
+        if self.wire == torch.float16:
+            return t.view(torch.int16).to(torch.int32) + 32768
+        return t
 
     def put_cols(self, full: torch.Tensor, ra: int, c0: int) -> None:
         """Write this rank's columns of ``full`` (rows [ra, ..), global columns
@@ -189,14 +203,14 @@ class _Engine:
         sl = _roundup(rows, self.world) // self.world
         lo = min(rows, self.rank * sl)
         hi = min(rows, lo + sl)
-        mine = torch.zeros((sl, k), dtype=self.x.dtype, device=self.x.device)
+        mine = torch.zeros((sl, k), dtype=self.wire, device=self.x.device)
         if hi > lo:
             part = B1[lo:hi]
             self.ops.trsm_right_upper_unit(U, part)
-            mine[:hi - lo].copy_(part)
-        out = torch.empty((sl * self.world, k), dtype=self.x.dtype, device=self.x.device)
+            mine[:hi - lo].copy_(self._pack(part))
+        out = torch.empty((sl * self.world, k), dtype=self.wire, device=self.x.device)
         self.dist.all_gather(list(out.split(sl)), mine)
-        return out[:rows]
+        return self._unpack(out[:rows]).contiguous()
 
     def permute_cols(self, r: int, sig: np.ndarray, row_ranges) -> None:
         """New column r + i = old column r + sig[i] on the given row ranges."""
@@ -286,7 +300,7 @@ def dist_cup(x: torch.Tensor, m: int, n: int, p: int, tiles: ColumnTiles, block:
     window = (2 * block if world > 1 else 0) if window is None else window
     if ops is None:
         ops = DeviceOps(p)
-    eng = _Engine(x, m, n, tiles, ops, rank, dist)
+    eng = _Engine(x, m, n, tiles, ops, rank, dist, p)
     # The row block is factored in one persistent buffer, its width padded to a
     # few buckets with zero columns (zero columns never hold a pivot and stay
     # in place): the CUP engine caches one plan + CUDA graph per (shape, buffer).
