@@ -86,7 +86,10 @@ private:
     SwapJobs swap_jobs_{};                     // queued, launched by flush_swaps()
     // Schur updates with K <= this are split (window slice first, rest on s2_);
     // above it the extra narrow GEMM costs more than the overlap wins
-    i32 split_max_k_ = 1024;
+#ifndef RL_SPLIT_MAX_K
+#define RL_SPLIT_MAX_K 1024
+#endif
+    i32 split_max_k_ = RL_SPLIT_MAX_K;
     NodeEvents waits_, dones_;
     void* meta_ = nullptr;                     // one allocation for everything below
     i32* rp_ = nullptr;
@@ -102,7 +105,10 @@ private:
     std::map<std::pair<i32, i32>, i32> ninv_slot_;
     std::set<std::pair<i32, i32>> ninv_done_;  // during one enqueue
     u32* ninv_ = nullptr;
-    static constexpr i32 kNinvGemmMinRows = 512;  // taller G: tensor-core GEMM
+#ifndef RL_NINV_GEMM_MIN_ROWS
+#define RL_NINV_GEMM_MIN_ROWS 512
+#endif
+    static constexpr i32 kNinvGemmMinRows = RL_NINV_GEMM_MIN_ROWS;  // taller G: tensor-core GEMM
     uint8_t* a2_ = nullptr;
     uint8_t* b2_ = nullptr;
     size_t a2_cap_ = 0, b2_cap_ = 0;
