@@ -315,7 +315,9 @@ void CupEngine::trsm_right(i32 r0, i32 M, i32 x0, i32 mx) {
         a.rrp = rrp_;
         a.f = f_;
         flush_swaps();
-        a.ninv = have ? nullptr : ninv;  // first TRSM against X also leaves U_X^{-1}
+        // first TRSM against X also leaves U_X^{-1} -- only where a taller TRSM can
+        // use it (gemm_ninv needs >= 2 leaves): one-leaf solves skip the extra rows
+        a.ninv = (have || mx < 2 * PB) ? nullptr : ninv;
         ninv_done_.insert(key);
         trsm_node(a, s_);
         stats_.trsm_leaves++;
