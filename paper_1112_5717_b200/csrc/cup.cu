@@ -78,6 +78,12 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
     for (auto& e : events_) RL_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     if (a2_cap_) RL_CUDA_CHECK(cudaMalloc(&a2_, a2_cap_));
     if (b2_cap_) RL_CUDA_CHECK(cudaMalloc(&b2_, b2_cap_));
+    for (auto& kv : lanes_) {
+        Lane& l = kv.second;
+        RL_CUDA_CHECK(cudaStreamCreateWithPriority(&l.st, cudaStreamNonBlocking, prio_lo));
+        if (l.a2_cap) RL_CUDA_CHECK(cudaMalloc(&l.a2, l.a2_cap));
+        if (l.b2_cap) RL_CUDA_CHECK(cudaMalloc(&l.b2, l.b2_cap));
+    }
 }
 
 CupEngine::~CupEngine() {
@@ -88,6 +94,11 @@ CupEngine::~CupEngine() {
     if (s3_) cudaStreamDestroy(s3_);
     cudaFree(a2_);
     cudaFree(b2_);
+    for (auto& kv : lanes_) {
+        if (kv.second.st) cudaStreamDestroy(kv.second.st);
+        cudaFree(kv.second.a2);
+        cudaFree(kv.second.b2);
+    }
 }
 
 cudaEvent_t CupEngine::fork_to(cudaStream_t from, cudaStream_t to) {
@@ -100,7 +111,7 @@ cudaEvent_t CupEngine::fork_to(cudaStream_t from, cudaStream_t to) {
 
 void CupEngine::gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nmax, cudaStream_t st,
                      i32 n_cap) {
-    if (!st) st = s_;
+    if (!st) st = work_stream();
     // K = pivots of rows [x0, x1) = [rp[x0], rp[x1]); split along the skeleton
     // while the s32 exactness bound could be exceeded.
     const i64 Kmax = x1 - x0;
@@ -111,6 +122,8 @@ void CupEngine::gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nm
         gemm(row0, M, xm, x1, n_lo, n_hi, Nmax, st, n_cap);
         return;
     }
+    // side-lane work packs into its lane's own workspace
+    Lane* ln = (lane_ && st == lane_->st) ? lane_ : nullptr;
     GemmArgs g{};
     g.A = A_;
     g.lda = lda_;
@@ -129,7 +142,7 @@ void CupEngine::gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nm
     g.rp = rp_;
     g.n_cap = n_cap;
     // on the side stream the persistent GEMM leaves one SM for the window kernel
-    g.max_ctas = (st == s2_) ? num_sms() - 1 : 0;
+    g.max_ctas = (st == s_) ? 0 : (ln && lane_ctas_ > 0) ? lane_ctas_ : num_sms() - 1;
     g.alpha = p_ - 1;  // C <- C - A*B  (mm(..., neg_one, one), factor.cpp:51)
     g.beta = 1 % p_;
     g.f = f_;
@@ -139,8 +152,10 @@ void CupEngine::gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nm
     const bool tc = use_tc_ && Kmax > PB && Nmax >= 64 && M >= 64 && !(Nmax <= PW && Kmax <= 4 * PB);
     if (dry_) {
         if (tc) {
-            a2_cap_ = std::max(a2_cap_, tc_a2_bytes(L_, M, Kmax));
-            b2_cap_ = std::max(b2_cap_, tc_b2_bytes(L_, Nmax, Kmax));
+            size_t& ac = ln ? ln->a2_cap : a2_cap_;
+            size_t& bc = ln ? ln->b2_cap : b2_cap_;
+            ac = std::max(ac, tc_a2_bytes(L_, M, Kmax));
+            bc = std::max(bc, tc_b2_bytes(L_, Nmax, Kmax));
         }
         return;
     }
@@ -149,7 +164,7 @@ void CupEngine::gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nm
     if (tc) {
         ++stats_.tc_gemms;
         stats_.launches += 2;
-        gemm_tc(g, L_, Kmax, Nmax, a2_, b2_, st);
+        gemm_tc(g, L_, Kmax, Nmax, ln ? ln->a2 : a2_, ln ? ln->b2 : b2_, st);
     } else {
         stats_.launches += 1;
         gemm_simt(g, Kmax, Nmax, st);
@@ -277,7 +292,8 @@ void CupEngine::gemm_ninv(i32 r0, i32 M, i32 x0, i32 mx, const u32* ninv) {
     ++stats_.gemms;
     ++stats_.tc_gemms;
     stats_.launches += 2;
-    gemm_tc(g, L_, mx, mx, a2_, b2_, s_);
+    if (lane_) g.max_ctas = lane_ctas_ > 0 ? lane_ctas_ : num_sms() - 1;
+    gemm_tc(g, L_, mx, mx, lane_ ? lane_->a2 : a2_, lane_ ? lane_->b2 : b2_, work_stream());
 }
 
 void CupEngine::trsm_right(i32 r0, i32 M, i32 x0, i32 mx) {
@@ -287,8 +303,10 @@ void CupEngine::trsm_right(i32 r0, i32 M, i32 x0, i32 mx) {
         if (dry_) {
             if (!ninv_slot_.count(key)) ninv_slot_.emplace(key, (i32)ninv_slot_.size());
             if (gemm_ok) {
-                a2_cap_ = std::max(a2_cap_, tc_a2_bytes(L_, M, mx));
-                b2_cap_ = std::max(b2_cap_, tc_b2_bytes(L_, mx, mx));
+                size_t& ac = lane_ ? lane_->a2_cap : a2_cap_;
+                size_t& bc = lane_ ? lane_->b2_cap : b2_cap_;
+                ac = std::max(ac, tc_a2_bytes(L_, M, mx));
+                bc = std::max(bc, tc_b2_bytes(L_, mx, mx));
             }
             return;
         }
@@ -319,7 +337,7 @@ void CupEngine::trsm_right(i32 r0, i32 M, i32 x0, i32 mx) {
         // use it (gemm_ninv needs >= 2 leaves): one-leaf solves skip the extra rows
         a.ninv = (have || mx < 2 * PB) ? nullptr : ninv;
         ninv_done_.insert(key);
-        trsm_node(a, s_);
+        trsm_node(a, work_stream());
         stats_.trsm_leaves++;
         stats_.launches += 1;
         return;
@@ -337,7 +355,7 @@ void CupEngine::trsm_right(i32 r0, i32 M, i32 x0, i32 mx) {
         a.uinv = uinv_ + (size_t)leaf_of_.at(x0) * PB * PB;
         a.f = f_;
         flush_swaps();
-        trsm_leaf(a, s_);
+        trsm_leaf(a, work_stream());
         stats_.trsm_leaves++;
         stats_.launches += 1;
         return;
@@ -366,19 +384,48 @@ void CupEngine::node(i32 i0, i32 mm) {
         auto it = waits_.find({i0, mm});
         if (it != waits_.end()) RL_CUDA_CHECK(cudaStreamWaitEvent(s_, it->second, cudaEventWaitExternal));
     }
+    if (!dry_) {  // the lower rows' TRSM + Schur update ran on a side lane
+        auto it = row_joins_.find({i0, mm});
+        if (it != row_joins_.end()) {
+            RL_CUDA_CHECK(cudaStreamWaitEvent(s_, it->second, 0));
+            row_joins_.erase(it);
+        }
+    }
     const i32 b0 = i0 + k, bm = mm - k;
     swaps_range(b0, bm, dyn_rp(i0), dyn_rp(b0));                     // factor.cpp:42
     if (!dry_ && uinv_join_) {
         RL_CUDA_CHECK(cudaStreamWaitEvent(s_, uinv_join_, 0));
         uinv_join_ = nullptr;
     }
-    trsm_right(b0, bm, i0, k);                                        // factor.cpp:45-46
     // factor.cpp:51-52, split: the first window of the bottom half reads only
     // columns [rp[b0], rp[b0] + PW), so that slice is updated first and the rest
     // runs on s2_ beside that window (joined before its tail)
-    if (k > split_max_k_) {
+    if (k > split_max_k_ && row_split_min_ > 0 && bm >= row_split_min_ && bm > 2 * PB) {
+        // rows [b0, b0 + h) now; rows [b0 + h, b0 + bm) on the lane of height bm,
+        // joined in node(b0, bm) after its top half (rows [b0, b0 + h)) is factored
+        const i32 h = bm / 2;
+        trsm_right(b0, h, i0, k);                                     // factor.cpp:45-46
+        gemm(b0, h, i0, b0, dyn_rp(b0), dyn_c(n_), n_);
+        Lane& ln = lanes_[bm];
+        if (dry_) {
+            events_needed_ += 2;
+        } else {
+            fork_to(s_, ln.st);
+        }
+        lane_ = &ln;
+        trsm_right(b0 + h, bm - h, i0, k);
+        gemm(b0 + h, bm - h, i0, b0, dyn_rp(b0), dyn_c(n_), n_);
+        lane_ = nullptr;
+        if (!dry_) {
+            cudaEvent_t e = events_.at(next_event_++);
+            RL_CUDA_CHECK(cudaEventRecord(e, ln.st));
+            row_joins_[{b0, bm}] = e;
+        }
+    } else if (k > split_max_k_) {
+        trsm_right(b0, bm, i0, k);                                    // factor.cpp:45-46
         gemm(b0, bm, i0, b0, dyn_rp(b0), dyn_c(n_), n_);
     } else {
+        trsm_right(b0, bm, i0, k);                                    // factor.cpp:45-46
         gemm(b0, bm, i0, b0, dyn_rp(b0), Dyn{b0, PW}, std::min<i64>(PW, n_), s_, n_);
         if (dry_) {
             events_needed_ += 2;
@@ -404,6 +451,8 @@ void CupEngine::enqueue(u32* dA, cudaStream_t s) {
     next_event_ = 0;
     pending_joins_.clear();
     uinv_join_ = nullptr;
+    row_joins_.clear();
+    lane_ = nullptr;
     fill_rp0(rp_, s);
     if (m_ > 0 && n_ > 0) {
         node(0, m_);

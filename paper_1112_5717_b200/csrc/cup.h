@@ -112,6 +112,30 @@ private:
     uint8_t* a2_ = nullptr;
     uint8_t* b2_ = nullptr;
     size_t a2_cap_ = 0, b2_cap_ = 0;
+    // Row-split of the wide nodes (k > split_max_k_): the TRSM + Schur update of
+    // the bottom half's LOWER rows [b0 + bm/2, b0 + bm) is first read after the
+    // bottom half's own top half is factored, so it runs on a low-priority side
+    // lane (one stream + GEMM workspace per node height) beside that recursion
+    // and is joined right before the child node first touches those rows.
+#ifndef RL_ROW_SPLIT_MIN_ROWS
+#define RL_ROW_SPLIT_MIN_ROWS 4096
+#endif
+    i32 row_split_min_ = RL_ROW_SPLIT_MIN_ROWS;  // 0: off
+#ifndef RL_LANE_CTAS
+#define RL_LANE_CTAS 110
+#endif
+    i32 lane_ctas_ = RL_LANE_CTAS;               // persistent GEMM CTAs on a lane (0: all but one SM);
+                                                 // the rest stay free for the recursion beside it
+    struct Lane {
+        cudaStream_t st = nullptr;
+        uint8_t* a2 = nullptr;
+        uint8_t* b2 = nullptr;
+        size_t a2_cap = 0, b2_cap = 0;
+    };
+    std::map<i32, Lane> lanes_;                  // node height bm -> lane
+    Lane* lane_ = nullptr;                       // non-null while enqueueing side work
+    std::map<std::pair<i32, i32>, cudaEvent_t> row_joins_;  // child node -> side work done
+    cudaStream_t work_stream() const { return lane_ ? lane_->st : s_; }
     cudaGraphExec_t graph_exec_ = nullptr;
     u32* graph_A_ = nullptr;
     Stats stats_;

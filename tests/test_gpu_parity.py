@@ -337,3 +337,23 @@ def test_batched_host_pipeline_equals_device_path():
     rk, rrp, sg = G.cup_batched(h, 8388593)
     assert np.array_equal(rk, rk_d) and np.array_equal(rrp, rrp_d) and np.array_equal(sg, sg_d)
     assert np.array_equal(h, d.cpu().numpy().view(np.uint32))
+
+
+def test_cup_row_split_lanes_vs_oracle():
+    # 8192 rows: the root's bottom half (4096 rows, k = 4096 > the column-split
+    # bound) takes the row split -- its lower 2048 rows get their TRSM + Schur
+    # update on a side lane, joined when node(4096, 4096) first touches them.
+    # Rank-deficient with a thinned top half (r1 < w, so the root's Schur update
+    # is non-empty) and a shuffled profile, so the lane's extents are dynamic.
+    from tests.helpers import matmul_mod
+    p = 65521
+    rng = np.random.default_rng(5)
+    L = rng.integers(0, p, (8192, 900), dtype=np.uint64).astype(np.uint32)
+    R = rng.integers(0, p, (900, 1000), dtype=np.uint64).astype(np.uint32)
+    b = matmul_mod(L, R, p)
+    top = b[:4096]
+    top[rng.random(4096) < 0.9] = 0
+    b[4096:][2::3] = 0
+    b[:4096] = top[rng.permutation(4096)]
+    g = _check_cup(np.ascontiguousarray(b), p)
+    assert 0 < int(np.searchsorted(g.row_profile, 4096)) < g.rank

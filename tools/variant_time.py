@@ -1,6 +1,7 @@
 #!/usr/bin/env python3
 """Time C3 (16384^2, p = 65521) with an alternative build of the library
-(variant_time.py path/to/libranklab_gpu.so): engine tuning experiments."""
+(variant_time.py path/to/libranklab_gpu.so [n]): engine tuning experiments;
+n = 65536 times config 5 instead."""
 import os
 import sys
 
@@ -11,12 +12,13 @@ import torch  # noqa: E402
 import paper_1112_5717_b200 as G  # noqa: E402
 
 G.LIB_PATH = os.path.abspath(sys.argv[1])
-n, p = 16384, 65521
+n, p = (int(sys.argv[2]) if len(sys.argv) > 2 else 16384), 65521
 src = torch.empty((n, n), dtype=torch.int32, device="cuda")
 G.random_matrix_dev(src, n, n, 3, p)
 work = torch.empty_like(src)
 ts = []
-for i in range(6):
+nrep = 6 if n <= 16384 else 4
+for i in range(nrep):
     work.copy_(src)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
