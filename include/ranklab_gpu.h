@@ -12,6 +12,16 @@
  * back; the *_dev variants take device pointers and a cudaStream_t (as void*,
  * NULL = legacy default stream) and keep all compute on the GPU.  There is no
  * CPU fallback: without a usable CUDA device every call returns RL_ECUDA.
+ *
+ * Threading (proj/README.md:164-168): every entry point is re-entrant.  Plans,
+ * workspaces and copy streams are cached per (device, stream); host-pointer
+ * calls run on cudaStreamPerThread, so distinct host threads never share them
+ * and never wait for each other.  Calls on the same stream serialise.
+ * Host buffers may be pinned (cudaHostAlloc/cudaHostRegister: the copies run
+ * on copy streams overlapped with the factorization) or pageable (staged
+ * through a pinned ring by host threads); matrices of <= 512 entries take a
+ * one-launch path (input in the kernel parameters, outputs through mapped
+ * pinned memory).
  */
 #ifndef RANKLAB_GPU_H
 #define RANKLAB_GPU_H
@@ -155,6 +165,15 @@ int rl_echelon_opcount(int64_t m, int64_t n, int64_t r, int reduced, uint64_t* o
  * ranklab::random_matrix(m, n, seed, GF(p))  proj/src/reference.cpp:246-253. */
 int rl_random_matrix_u32_dev(uint32_t* dA, int64_t m, int64_t n, int64_t lda, uint64_t seed,
                              uint32_t p, void* stream);
+
+/* Order-independent 64-bit digest of a device matrix: the sum mod 2^64 of
+ * splitmix_mix(((i*n + j) << 32 | A[i][j]) + 0x9E3779B97F4A7C15) over all
+ * entries (splitmix_mix = the reference's SplitMix64 finaliser,
+ * reference.cpp:177-180).  Test helper: the parity tests compare the packed
+ * bodies of the benchmark configs (up to 17 GB) against CPU digests without
+ * copying them back. */
+int rl_digest_u32_dev(const uint32_t* dA, int64_t m, int64_t n, int64_t lda, uint64_t* digest,
+                      void* stream);
 
 /* Message of the last failing call on this thread ("" if none). */
 const char* rl_last_error(void);

@@ -157,6 +157,93 @@ int oracle_cup_u32(u32* a, int64_t m, int64_t n, int64_t lda, u32 p, int64_t* ra
     return 0;
 }
 
+/* Leaf of the blocked oracle (oracle/blocked.py): the same CUP as
+ * oracle_cup_u32 (same pivot rule, transpositions over all leaf rows, raw C
+ * entries, normalised U rows moved to the top), computed LEFT-looking with
+ * delayed reduction so a leaf of up to a few dozen rows costs one 64-bit
+ * multiply-add per (pivot, column) instead of a modulo.  Row i first forms
+ * its C entries C(i,j) = a_i[j] - sum_{j'<j} C(i,j') U_j'[j] (j < r, pivot
+ * order), then its residual a_i[c] + sum_j (p - C(i,j)) U_j[c] for c >= r in
+ * one u64 accumulator per column; the U rows U_j are the normalised pivot
+ * rows (factor.cpp:25-26).  acc is caller scratch of n words.
+ * Exact for p < 2^31: for p < 2^16 the lazy sum of <= 2^31 terms < 2^32 never
+ * overflows; otherwise every product is reduced before it is added. */
+int oracle_cup_leaf_u32(u32* a, int64_t m, int64_t n, int64_t lda, u32 p, int64_t* rank,
+                        u32* rrp, u32* sigma, u32* ipiv, u64* acc) {
+    int64_t r = 0;
+    const int lazy = p <= 65536u;
+    for (int64_t j = 0; j < n; ++j) sigma[j] = (u32)j;
+    if (m == 0 || n == 0) { *rank = 0; return 0; }
+    for (int64_t i = 0; i < m; ++i) {
+        u32* ri = a + i * lda;
+        /* C entries at the pivot positions found so far (once r == n these are
+         * all the row holds: the TRSM output G of factor.cpp:45-47) */
+        for (int64_t j = 0; j < r; ++j) {
+            const u32* uj;
+            u64 s = ri[j];
+            for (int64_t j2 = 0; j2 < j; ++j2) {
+                uj = a + (int64_t)rrp[j2] * lda;
+                s += (u64)(p - ri[j2]) * uj[j] % p;
+            }
+            ri[j] = (u32)(s % p);
+        }
+        if (r == n) continue; /* factor.cpp:47 */
+        /* residual on [r, n) */
+        for (int64_t c = r; c < n; ++c) acc[c] = ri[c];
+        for (int64_t j = 0; j < r; ++j) {
+            const u32 nm = ri[j] ? p - ri[j] : 0u;
+            if (!nm) continue;
+            const u32* uj = a + (int64_t)rrp[j] * lda;
+            if (lazy) {
+                for (int64_t c = r; c < n; ++c) acc[c] += (u64)nm * uj[c];
+            } else {
+                for (int64_t c = r; c < n; ++c) acc[c] = (acc[c] + (u64)nm * uj[c] % p) % p;
+            }
+        }
+        int64_t piv = -1;
+        for (int64_t c = r; c < n; ++c) {
+            ri[c] = (u32)(acc[c] % p);
+            if (piv < 0 && ri[c]) piv = c;
+        }
+        if (piv < 0) continue;
+        if (piv != r) { /* transposition on every leaf row (factor.cpp:23-24,42,56) */
+            for (int64_t k = 0; k < m; ++k) {
+                u32* rk = a + k * lda;
+                u32 t = rk[r]; rk[r] = rk[piv]; rk[piv] = t;
+            }
+            u32 t = sigma[r]; sigma[r] = sigma[piv]; sigma[piv] = t;
+        }
+        if (ipiv) ipiv[r] = (u32)piv;
+        rrp[r] = (u32)i;
+        const u32 pinv = invmod(ri[r], p);
+        for (int64_t c = r + 1; c < n; ++c) ri[c] = mulmod(ri[c], pinv, p);
+        ++r;
+    }
+    for (int64_t j = 0; j < r; ++j) { /* U rows to rows 0..r-1 (factor.cpp:62-70) */
+        int64_t src = rrp[j];
+        if (src == j) continue;
+        u32* d = a + j * lda;
+        u32* s = a + src * lda;
+        for (int64_t c = j + 1; c < n; ++c) { d[c] = s[c]; s[c] = 0; }
+    }
+    *rank = r;
+    return 0;
+}
+
+/* Order-independent 64-bit digest of an m x n matrix: the sum mod 2^64 of
+ * splitmix_mix(((i*n + j) << 32 | a[i][j]) + golden) over all entries (the
+ * same function as the device's rl_digest_u32_dev, so the GPU tests compare
+ * multi-GB bodies without copying them back). */
+u64 oracle_digest_u32(const u32* a, int64_t m, int64_t n, int64_t lda) {
+    u64 h = 0;
+    for (int64_t i = 0; i < m; ++i)
+        for (int64_t j = 0; j < n; ++j) {
+            const u64 e = (u64)(i * n + j);
+            h += splitmix_mix((e << 32 | a[i * lda + j]) + 0x9E3779B97F4A7C15ull);
+        }
+    return h;
+}
+
 /* The reference's cost model (bench.cpp:12-13):
  * W(m,n,r) = 2mnr - (m+n)r^2 + (2/3)r^3 field operations. */
 double oracle_cup_model_ops(int64_t m, int64_t n, int64_t r) {

@@ -40,7 +40,7 @@ __all__ = [
     "rank_and_profile", "determinant", "random_matrix_dev", "LIB_PATH", "lib",
     "EchelonTransform", "ReducedEchelonTransform", "col_ech_trans", "red_col_ech_trans",
     "col_ech_trans_dev", "invert_in_place", "invert_dev", "trsm", "trsm_dev",
-    "Side", "UpLo", "Diag", "PackedPle", "ple", "ple_dev",
+    "Side", "UpLo", "Diag", "PackedPle", "ple", "ple_dev", "digest_dev",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -134,7 +134,7 @@ EXPORTS = ["rl_cup_u32", "rl_cup_u32_dev", "rl_cup_batched_u32_dev", "rl_cup_bat
            "rl_profile_gemm_dev", "rl_cup_opcount", "rl_col_ech_trans_u32",
            "rl_col_ech_trans_u32_dev", "rl_invert_u32", "rl_invert_u32_dev", "rl_trsm_u32",
            "rl_trsm_u32_dev", "rl_trsm_opcount", "rl_echelon_opcount", "rl_ple_u32",
-           "rl_ple_u32_dev"]
+           "rl_ple_u32_dev", "rl_digest_u32_dev"]
 
 
 def lib():
@@ -176,6 +176,7 @@ def lib():
     L.rl_echelon_opcount.argtypes = [_i64, _i64, _i64, C.c_int, _vp]
     L.rl_ple_u32.argtypes = [_vp, _i64, _i64, _i64, _u32, C.POINTER(_i64), _vp, _vp, _vp]
     L.rl_ple_u32_dev.argtypes = [_vp, _i64, _i64, _i64, _u32, C.POINTER(_i64), _vp, _vp, _vp, _vp]
+    L.rl_digest_u32_dev.argtypes = [_vp, _i64, _i64, _i64, C.POINTER(C.c_uint64), _vp]
     _lib = L
     return L
 
@@ -523,6 +524,16 @@ def random_matrix_dev(d_a, m: int, n: int, seed: int, p: int, lda: int | None = 
     _check(lib().rl_random_matrix_u32_dev(C.c_void_p(ptr), m, n, lda or n,
                                           C.c_uint64(seed & (2**64 - 1)), int(p),
                                           _stream_ptr(stream)))
+
+
+def digest_dev(d_a, m: int, n: int, lda: int | None = None, stream=None) -> int:
+    """Order-independent 64-bit digest of a device matrix (rl_digest_u32_dev; the
+    oracle computes the same function on the host)."""
+    ptr = d_a.data_ptr() if hasattr(d_a, "data_ptr") else int(d_a)
+    h = C.c_uint64(0)
+    _check(lib().rl_digest_u32_dev(C.c_void_p(ptr), m, n, n if lda is None else lda, C.byref(h),
+                                   _stream_ptr(stream)))
+    return h.value
 
 
 def plan_stats(m: int, n: int, p: int, lda: int | None = None) -> dict:

@@ -390,24 +390,50 @@ __global__ void inv_table_kernel(u32* tab, u32 p) {
 
 // x^{-1} mod p for every x < p (p < 2^24: at most 64 MB), built once per prime
 // and device, so a pivot inverse on the batched kernel's serial chain is one
-// cached load instead of an extended Euclid loop.
+// cached load instead of an extended Euclid loop.  The build is synchronised
+// once (a consumer on any other stream then sees a finished table), and at most
+// kMaxTables tables live per process: a multi-modular caller cycling through
+// primes evicts the least recently used one (after a device synchronisation,
+// since an asynchronous batch may still read it).
 const u32* inverse_table(u32 p, cudaStream_t s) {
+    constexpr size_t kMaxTables = 4;
+    struct Tab {
+        u32* ptr;
+        unsigned long long used;
+    };
     static std::mutex mu;
-    static std::map<std::pair<int, u32>, u32*> tabs;
-    int dev = 0;
-    RL_CUDA_CHECK(cudaGetDevice(&dev));
+    static std::map<std::pair<int, u32>, Tab> tabs;
+    static unsigned long long tick = 0;
+    const int dev = current_device();
     std::lock_guard<std::mutex> lk(mu);
     auto it = tabs.find({dev, p});
-    if (it != tabs.end()) return it->second;
+    if (it != tabs.end()) {
+        it->second.used = ++tick;
+        return it->second.ptr;
+    }
+    if (tabs.size() >= kMaxTables) {
+        auto victim = tabs.begin();
+        for (auto j = tabs.begin(); j != tabs.end(); ++j)
+            if (j->second.used < victim->second.used) victim = j;
+        int cur = dev;
+        RL_CUDA_CHECK(cudaSetDevice(victim->first.first));
+        RL_CUDA_CHECK(cudaDeviceSynchronize());
+        cudaFree(victim->second.ptr);
+        RL_CUDA_CHECK(cudaSetDevice(cur));
+        tabs.erase(victim);
+    }
     u32* t = nullptr;
     if (cudaMalloc(&t, sizeof(u32) * p) != cudaSuccess) throw Error(8, "cudaMalloc failed");
     inv_table_kernel<<<4 * num_sms(), 256, 0, s>>>(t, p);
     RL_CUDA_CHECK(cudaGetLastError());
-    tabs.emplace(std::make_pair(dev, p), t);
+    RL_CUDA_CHECK(cudaStreamSynchronize(s));
+    tabs.emplace(std::make_pair(dev, p), Tab{t, ++tick});
     return t;
 }
 
 }  // namespace
+
+constexpr i64 kTableMinBatch = 64;
 
 void cup_batched(u32* dA, i64 batch, i32 m, i32 n, i64 stride, u32 p, i32* d_ranks, i32* d_rrp,
                  i32* d_ipiv, i32 kcap, cudaStream_t s) {
@@ -416,18 +442,19 @@ void cup_batched(u32* dA, i64 batch, i32 m, i32 n, i64 stride, u32 p, i32* d_ran
     const Fp f = make_fp(p);
     if (n <= BN) {
         const size_t smem = sizeof(u64) * PR * BN + sizeof(u32) * 8 * BN;
-        static bool attr = false;
-        if (!attr) {
+        static std::atomic<unsigned long long> attr_once{0};
+        if (first_on_device(attr_once)) {
             RL_CUDA_CHECK(cudaFuncSetAttribute(cup_batched_blk_kernel<true>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             RL_CUDA_CHECK(cudaFuncSetAttribute(cup_batched_blk_kernel<false>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr = true;
         }
+        // the per-prime table pays off for real batches; a handful of matrices
+        // take the in-kernel extended Euclid inverse (so does every p >= 2^24)
         if (p < (1u << 24))
-            cup_batched_blk_kernel<true><<<(unsigned)batch, 256, smem, s>>>(dA, stride, m, n, f, d_ranks,
-                                                                           d_rrp, d_ipiv, kcap,
-                                                                           inverse_table(p, s));
+            cup_batched_blk_kernel<true><<<(unsigned)batch, 256, smem, s>>>(
+                dA, stride, m, n, f, d_ranks, d_rrp, d_ipiv, kcap,
+                batch >= kTableMinBatch ? inverse_table(p, s) : nullptr);
         else
             cup_batched_blk_kernel<false><<<(unsigned)batch, 256, smem, s>>>(dA, stride, m, n, f, d_ranks,
                                                                             d_rrp, d_ipiv, kcap, nullptr);

@@ -6,11 +6,13 @@
 // PrimeField (proj/src/field.cpp:24-58).  Engines (plans + workspaces + graphs)
 // are cached per (m, n, lda, p) behind a mutex; calls are re-entrant per stream.
 #include <algorithm>
+#include <functional>
 #include <cstring>
 #include <map>
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -19,6 +21,7 @@
 #include "kernels.cuh"
 #include "runtime.h"
 #include "tri.h"
+#include "util.h"
 
 namespace rl {
 void cup_batched(u32* dA, i64 batch, i32 m, i32 n, i64 stride, u32 p, i32* d_ranks, i32* d_rrp,
@@ -92,31 +95,67 @@ int guard(F&& f) {
     }
 }
 
+// Engines (plan + workspaces + captured graph) are cached per (device, stream,
+// m, n, lda, p): a call on one stream never touches another stream's engine,
+// so concurrent factorizations on distinct streams run in parallel.  The cache
+// is bounded; an evicted engine waits for its last (possibly asynchronous) run.
 struct Key {
+    int dev;
+    cudaStream_t s;
+    std::thread::id tid;  // cudaStreamPerThread: one engine set per host thread
     i64 m, n, lda;
     u32 p;
     bool split = false;  // host-buffer engine with the split H2D wait
     bool operator<(const Key& o) const {
-        return std::tie(m, n, lda, p, split) < std::tie(o.m, o.n, o.lda, o.p, o.split);
+        return std::tie(dev, s, tid, m, n, lda, p, split) <
+               std::tie(o.dev, o.s, o.tid, o.m, o.n, o.lda, o.p, o.split);
     }
 };
+struct Cached {
+    std::shared_ptr<CupEngine> e;
+    unsigned long long used = 0;
+};
+std::mutex g_engines_mu;
+std::map<Key, Cached> g_engines;
+unsigned long long g_tick = 0;
+constexpr size_t kMaxEngines = 16;
 
-std::mutex g_mu;
-std::map<Key, std::unique_ptr<CupEngine>> g_engines;
-
-CupEngine& engine_for(i64 m, i64 n, i64 lda, u32 p, bool split = false) {
-    Key k{m, n, lda, p, split};
-    auto it = g_engines.find(k);
-    if (it != g_engines.end()) return *it->second;
-    if (g_engines.size() > 16) g_engines.clear();
-    auto e = std::make_unique<CupEngine>((i32)m, (i32)n, lda, p);
-    CupEngine& ref = *e;
-    g_engines.emplace(k, std::move(e));
-    return ref;
+std::shared_ptr<CupEngine> engine_for(i64 m, i64 n, i64 lda, u32 p, cudaStream_t s, bool split = false) {
+    Key k{current_device(), s, s == cudaStreamPerThread ? std::this_thread::get_id() : std::thread::id(),
+          m, n, lda, p, split};
+    std::shared_ptr<CupEngine> victim;  // destroyed outside the lock
+    {
+        std::lock_guard<std::mutex> lk(g_engines_mu);
+        auto it = g_engines.find(k);
+        if (it != g_engines.end()) {
+            it->second.used = ++g_tick;
+            return it->second.e;
+        }
+        if (g_engines.size() >= kMaxEngines) {
+            auto lru = g_engines.end();
+            for (auto j = g_engines.begin(); j != g_engines.end(); ++j)
+                if (j->second.e.use_count() == 1 && (lru == g_engines.end() || j->second.used < lru->second.used))
+                    lru = j;
+            if (lru != g_engines.end()) {
+                victim = std::move(lru->second.e);
+                g_engines.erase(lru);
+            }
+        }
+    }
+    victim.reset();
+    auto e = std::make_shared<CupEngine>((i32)m, (i32)n, lda, p);
+    std::lock_guard<std::mutex> lk(g_engines_mu);
+    auto res = g_engines.emplace(k, Cached{e, ++g_tick});
+    return res.first->second.e;
 }
 
-// Device scratch buffers reused across host-pointer calls.
-DevBuf g_bufA, g_bufB, g_bufC, g_bufI, g_bufT;
+// One C-ABI call's hold on its stream's context (workspaces, copy streams):
+// calls on the same stream serialise here, calls on distinct streams do not.
+struct Call {
+    Scratch& sc;
+    std::unique_lock<std::mutex> lk;
+    explicit Call(cudaStream_t s) : sc(scratch_for(s)), lk(sc.mu) {}
+};
 
 void require_device() {
     int n = 0;
@@ -165,11 +204,11 @@ void cup_dev_impl(u32* dA, i64 m, i64 n, i64 lda, u32 p, i64* rank, u32* rrp, u3
     i64 r = 0;
     std::vector<u32> rrp_h((size_t)std::min(m, n)), ipiv_h((size_t)std::min(m, n));
     {
-        std::lock_guard<std::mutex> lk(g_mu);
-        CupEngine& e = engine_for(m, n, lda, p);
-        e.run(dA, s, /*use_graph=*/m * n >= (1 << 18));  // capture pays off for large plans
+        Call call(s);
+        auto e = engine_for(m, n, lda, p, s);
+        e->run(dA, s, /*use_graph=*/m * n >= (1 << 18));  // capture pays off for large plans
         if (!rank && !rrp && !sigma && !ops) return;  // fully asynchronous
-        e.results(&r, rrp_h.data(), ipiv_h.data(), s);
+        e->results(&r, rrp_h.data(), ipiv_h.data(), s);
     }
     if (rank) *rank = r;
     if (rrp) std::copy(rrp_h.begin(), rrp_h.begin() + r, rrp);
@@ -199,7 +238,7 @@ void factor_on_device(u32* dA, i64 m, i64 n, i64 lda, u32 p, cudaStream_t s, i64
     rrp_h.assign((size_t)kcap, 0);
     ipiv_h.assign((size_t)kcap, 0);
     if (m <= 64 && n <= 256 && lda == n) {
-        i32* dmeta = (i32*)g_bufI.get((size_t)(1 + 2 * kcap) * 4);
+        i32* dmeta = (i32*)scratch_for(s).get(SS_META, (size_t)(1 + 2 * kcap) * 4);
         cup_batched(dA, 1, (i32)m, (i32)n, m * n, p, dmeta, dmeta + 1, dmeta + 1 + kcap, (i32)kcap, s);
         std::vector<i32> meta((size_t)(1 + 2 * kcap));
         RL_CUDA_CHECK(cudaMemcpyAsync(meta.data(), dmeta, meta.size() * 4, cudaMemcpyDeviceToHost, s));
@@ -209,9 +248,179 @@ void factor_on_device(u32* dA, i64 m, i64 n, i64 lda, u32 p, cudaStream_t s, i64
         std::copy((const u32*)&meta[1 + kcap], (const u32*)&meta[1 + kcap] + *r, ipiv_h.begin());
         return;
     }
-    CupEngine& e = engine_for(m, n, lda, p);
-    e.run(dA, s, m * n >= (1 << 18));
-    e.results(r, rrp_h.data(), ipiv_h.data(), s);  // synchronises s
+    auto e = engine_for(m, n, lda, p, s);
+    e->run(dA, s, m * n >= (1 << 18));
+    e->results(r, rrp_h.data(), ipiv_h.data(), s);  // synchronises s
+}
+
+// Is host memory at h page-locked (cudaHostAlloc / cudaHostRegister)?
+bool host_pinned(const void* h) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, h) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
+// RL_PAGEABLE_DIRECT=1: pageable buffers go straight to cudaMemcpy2DAsync (the
+// driver's own synchronous staging) -- kept for the benchmark comparison.
+bool pageable_direct() {
+    static const bool v = [] {
+        const char* e = getenv("RL_PAGEABLE_DIRECT");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
+// rows x cols words between row-strided host buffers, split over host threads
+// (a single core copies pageable memory at ~10 GB/s, well below PCIe).
+void par_copy_rows(u32* dst, i64 dld, const u32* src, i64 sld, i64 rows, i64 cols) {
+    const size_t bytes = (size_t)rows * cols * 4;
+    const int T = bytes >= (8u << 20) ? 8 : 1;
+    auto part = [&](int t) {
+        const i64 r0 = rows * t / T, r1 = rows * (t + 1) / T;
+        if (dld == cols && sld == cols) {
+            std::memcpy(dst + r0 * dld, src + r0 * sld, (size_t)(r1 - r0) * cols * 4);
+        } else {
+            for (i64 i = r0; i < r1; ++i) std::memcpy(dst + i * dld, src + i * sld, (size_t)cols * 4);
+        }
+    };
+    if (T == 1) return part(0);
+    std::vector<std::thread> th;
+    for (int t = 1; t < T; ++t) th.emplace_back(part, t);
+    part(0);
+    for (auto& x : th) x.join();
+}
+
+// Pageable host -> device through a ring of R pinned slots: host threads fill
+// slot k % R while the DMA of the previous chunks runs; a slot is refilled
+// only after the DMA that read it completed (its event).
+constexpr int kRing = 4;
+constexpr size_t kChunkBytes = 32u << 20;
+void staged_h2d(u32* d, i64 dld, const u32* h, i64 hld, i64 rows, i64 cols, Scratch& sc, cudaStream_t s) {
+    const i64 crow = std::max<i64>(1, (i64)(kChunkBytes / ((size_t)cols * 4)));
+    u32* ring = (u32*)sc.pinned_ring((size_t)kRing * crow * cols * 4);
+    i64 k = 0;
+    for (i64 r0 = 0; r0 < rows; r0 += crow, ++k) {
+        const i64 nr = std::min(crow, rows - r0);
+        const int slot = (int)(k % kRing);
+        u32* buf = ring + (size_t)slot * crow * cols;
+        if (k >= kRing) RL_CUDA_CHECK(cudaEventSynchronize(sc.event(slot)));
+        par_copy_rows(buf, cols, h + r0 * hld, hld, nr, cols);
+        RL_CUDA_CHECK(cudaMemcpy2DAsync(d + r0 * dld, dld * 4, buf, cols * 4, cols * 4, nr,
+                                        cudaMemcpyHostToDevice, s));
+        RL_CUDA_CHECK(cudaEventRecord(sc.event(slot), s));
+    }
+}
+
+// Device -> pageable host: the DMA of up to R chunks runs ahead of the host
+// threads draining the ring.
+void staged_d2h(u32* h, i64 hld, const u32* d, i64 dld, i64 rows, i64 cols, Scratch& sc, cudaStream_t s) {
+    const i64 crow = std::max<i64>(1, (i64)(kChunkBytes / ((size_t)cols * 4)));
+    u32* ring = (u32*)sc.pinned_ring((size_t)kRing * crow * cols * 4);
+    const i64 nchunks = (rows + crow - 1) / crow;
+    auto issue = [&](i64 k) {
+        const i64 r0 = k * crow, nr = std::min(crow, rows - r0);
+        const int slot = (int)(k % kRing);
+        RL_CUDA_CHECK(cudaMemcpy2DAsync(ring + (size_t)slot * crow * cols, cols * 4, d + r0 * dld, dld * 4,
+                                        cols * 4, nr, cudaMemcpyDeviceToHost, s));
+        RL_CUDA_CHECK(cudaEventRecord(sc.event(kRing + slot), s));
+    };
+    for (i64 k = 0; k < std::min<i64>(kRing, nchunks); ++k) issue(k);
+    for (i64 k = 0; k < nchunks; ++k) {
+        const i64 r0 = k * crow, nr = std::min(crow, rows - r0);
+        const int slot = (int)(k % kRing);
+        RL_CUDA_CHECK(cudaEventSynchronize(sc.event(kRing + slot)));
+        par_copy_rows(h + r0 * hld, hld, ring + (size_t)slot * crow * cols, cols, nr, cols);
+        if (k + kRing < nchunks) issue(k + kRing);
+    }
+}
+
+// One-launch CUP of a matrix of <= TINY_MAX entries (util.cu): the input rides
+// in the kernel parameters, the outputs come back through mapped pinned memory.
+void tiny_cup(const u32* A, i64 m, i64 n, i64 lda, u32 p, Scratch& sc, cudaStream_t s, i64* r,
+              std::vector<u32>& rrp_h, std::vector<u32>& ipiv_h) {
+    TinyIn in;
+    for (i64 i = 0; i < m; ++i)
+        for (i64 j = 0; j < n; ++j) in.a[i * n + j] = A[i * lda + j];
+    in.m = (i32)m;
+    in.n = (i32)n;
+    in.f = make_fp(p);
+    if (!sc.host_mapped)
+        RL_CUDA_CHECK(cudaHostAlloc(&sc.host_mapped, sizeof(TinyOut), cudaHostAllocMapped));
+    TinyOut* ho = (TinyOut*)sc.host_mapped;
+    TinyOut* dout = nullptr;
+    RL_CUDA_CHECK(cudaHostGetDevicePointer((void**)&dout, ho, 0));
+    cup_tiny(in, dout, s);
+    RL_CUDA_CHECK(cudaStreamSynchronize(s));
+    *r = ho->rank;
+    const i64 kcap = std::min(m, n);
+    rrp_h.assign((size_t)kcap, 0);
+    ipiv_h.assign((size_t)kcap, 0);
+    for (i64 j = 0; j < *r; ++j) {
+        rrp_h[j] = (u32)ho->rrp[j];
+        ipiv_h[j] = (u32)ho->ipiv[j];
+    }
+    u32* Aw = const_cast<u32*>(A);
+    for (i64 i = 0; i < m; ++i)
+        for (i64 j = 0; j < n; ++j) Aw[i * lda + j] = ho->body[i * n + j];
+}
+
+// Host-pinned CUP with PCIe overlapped along the recursion's spines (the
+// splits of factor.cpp:35).  In: rows [0, m/2^D) are copied first and factored
+// while the rest crosses the link in order on a second stream; each left-spine
+// node (0, mm) waits for its bottom rows right before it first touches them.
+// Out: each right-spine node's top half goes back as soon as it is factored
+// (final unless a later transposition or U-row move reaches it: then it is
+// copied again).  Copy streams and events belong to the calling stream's context.
+void cup_host_overlapped(u32* A, i64 m, i64 n, i64 lda, u32 p, u32* dA, Scratch& sc, cudaStream_t s, i64* r,
+                         std::vector<u32>& rrp_h, std::vector<u32>& ipiv_h) {
+    constexpr int D = 3;
+    cudaStream_t cs = sc.aux_stream(0), cs2 = sc.aux_stream(1);
+    cudaEvent_t top = sc.event(2 * kRing);
+    cudaEvent_t evw[D], evd[D];
+    for (int d = 0; d < D; ++d) {
+        evw[d] = sc.event(2 * kRing + 1 + d);
+        evd[d] = sc.event(2 * kRing + 1 + D + d);
+    }
+    CupEngine::NodeEvents waits, dones;
+    // left spine: node (0, sz[d]), sz[0] = m, sz[d+1] = sz[d] / 2
+    i64 sz[D + 1];
+    sz[0] = m;
+    for (int d = 0; d < D; ++d) sz[d + 1] = sz[d] / 2;
+    copy_h2d_2d(dA, n, A, lda, sz[D], n, s);
+    RL_CUDA_CHECK(cudaEventRecord(top, s));
+    RL_CUDA_CHECK(cudaStreamWaitEvent(cs, top, 0));
+    for (int d = D - 1; d >= 0; --d) {
+        copy_h2d_2d(dA + sz[d + 1] * n, n, A + sz[d + 1] * lda, lda, sz[d] - sz[d + 1], n, cs);
+        RL_CUDA_CHECK(cudaEventRecord(evw[d], cs));
+        waits[{0, (i32)sz[d]}] = evw[d];
+    }
+    // right spine: node (lo[d], len[d]); its top half [lo, lo + len/2) goes back
+    i64 lo[D], len[D], cut = 0;
+    for (int d = 0; d < D; ++d) {
+        lo[d] = d == 0 ? 0 : lo[d - 1] + len[d - 1] / 2;
+        len[d] = d == 0 ? m : len[d - 1] - len[d - 1] / 2;
+        dones[{(i32)lo[d], (i32)len[d]}] = evd[d];
+    }
+    const i64 kcap = std::min(m, n);
+    rrp_h.assign((size_t)kcap, 0);
+    ipiv_h.assign((size_t)kcap, 0);
+    auto e = engine_for(m, n, n, p, s, true);
+    e->set_host_overlap(waits, dones);
+    e->run(dA, s, true);
+    for (int d = 0; d < D; ++d) {
+        RL_CUDA_CHECK(cudaStreamWaitEvent(cs2, evd[d], 0));
+        copy_d2h_2d(A + lo[d] * lda, lda, dA + lo[d] * n, n, len[d] / 2, n, cs2);
+        cut = lo[d] + len[d] / 2;
+    }
+    e->results(r, rrp_h.data(), ipiv_h.data(), s);  // synchronises s
+    copy_d2h_2d(A + cut * lda, lda, dA + cut * n, n, m - cut, n, s);
+    RL_CUDA_CHECK(cudaStreamSynchronize(cs2));
+    bool ident = true;
+    for (i64 j = 0; j < *r && ident; ++j) ident = ipiv_h[(size_t)j] == (u32)j && rrp_h[(size_t)j] == (u32)j;
+    if (!ident) copy_d2h_2d(A, lda, dA, n, cut, n, s);
 }
 
 // ple (factor.cpp:87-156) is cup's column-split mirror: the recursion splits
@@ -224,7 +433,7 @@ void factor_on_device(u32* dA, i64 m, i64 n, i64 lda, u32 p, cudaStream_t s, i64
 // transposes into a workspace, factors, and transposes back (lock held).
 void ple_on_device(u32* dA, i64 m, i64 n, i64 lda, u32 p, cudaStream_t s, i64* rank, u32* col_profile,
                    u32* row_perm, u64* ops) {
-    u32* dT = (u32*)g_bufT.get((size_t)m * n * 4);
+    u32* dT = (u32*)scratch_for(s).get(SS_TRANS, (size_t)m * n * 4);
     transpose(dT, m, dA, lda, m, n, s);
     i64 r = 0;
     std::vector<u32> rrp_h, ipiv_h;
@@ -254,7 +463,8 @@ void echelon_after_cup(u32* dA, i64 m, i64 n, i64 lda, u32 p, i64 r, const u32* 
                        bool reduced, cudaStream_t s) {
     if (r == 0) return;
     const Fp f = make_fp(p);
-    static DevBuf xbuf, ybuf, tbuf, ibuf;
+    Scratch& sc = scratch_for(s);
+    DevBuf &xbuf = sc.buf[SS_X], &ybuf = sc.buf[SS_Y], &tbuf = sc.buf[SS_T], &ibuf = sc.buf[SS_IDX];
     // X <- U1^{-1} (unit upper); X2 <- -U1^{-1} U2; strict triangle of U1 <- X's
     u32* X = (u32*)xbuf.get((size_t)r * r * 4);
     tri_extract(X, r, dA, lda, (i32)r, /*upper=*/true, /*unit=*/true, p, s);
@@ -292,8 +502,7 @@ void rows_by_inverse_perm(u32* dA, i64 n, i64 lda, const u32* sigma, cudaStream_
             idx.push_back((i32)j);
         }
     if (idx.empty()) return;
-    static DevBuf ibuf;
-    i32* d = (i32*)ibuf.get(idx.size() * 4);
+    i32* d = (i32*)scratch_for(s).get(SS_PERM, idx.size() * 4);
     RL_CUDA_CHECK(cudaMemcpyAsync(d, idx.data(), idx.size() * 4, cudaMemcpyHostToDevice, s));
     move_rows(dA, lda, n, d, (i32)(idx.size() / 2), s);
     RL_CUDA_CHECK(cudaStreamSynchronize(s));  // idx must outlive the copy
@@ -326,28 +535,41 @@ void trsm_dev_impl(int side, int uplo, int diag, const u32* dT, i64 ldt, u32* dB
     const i64 k = side == SIDE_LEFT ? m : n;
     if (k == 0 || m == 0 || n == 0) return;
     const Fp f = make_fp(p);
-    static DevBuf xbuf, tbuf;
-    u32* X = (u32*)xbuf.get((size_t)k * k * 4);
+    Scratch& sc = scratch_for(s);
+    u32* X = (u32*)sc.get(SS_X, (size_t)k * k * 4);
     const bool upper = uplo == UPLO_UPPER;
     tri_extract(X, k, dT, ldt, (i32)k, upper, diag != 0, p, s);
     tri_inverse(X, k, (i32)k, upper, f, s);
-    u32* T = (u32*)tbuf.get((size_t)m * n * 4);
+    u32* T = (u32*)sc.get(SS_T, (size_t)m * n * 4);
     if (side == SIDE_LEFT) mm_dense(X, k, dB, ldb, T, n, m, k, n, 1 % p, 0, f, s);
     else mm_dense(dB, ldb, X, k, T, n, m, k, n, 1 % p, 0, f, s);
     RL_CUDA_CHECK(cudaMemcpy2DAsync(dB, ldb * 4, T, n * 4, n * 4, m, cudaMemcpyDeviceToDevice, s));
 }
 
 // The reference raises SingularDiagonal(d) at the first zero pivot its
-// traversal meets (kernels.cpp:87-90): ascending for Right/Upper and
-// Left/Lower, descending for the other two.
-i64 first_zero_diagonal(int side, int uplo, const std::vector<u32>& diag) {
+// traversal meets (kernels.cpp:87-90): trsm_rec halves the triangle (k = n/2)
+// down to blocks of <= threshold and visits them in ascending order for
+// Right/Upper and Left/Lower, descending for the other two, each block's
+// diagonal in the same direction -- and d is the index LOCAL to the base block
+// (trsm_base sees only its sub-view).  Returns -1 when the diagonal has no zero.
+i64 first_zero_diagonal(int side, int uplo, const std::vector<u32>& diag, i64 threshold) {
     const bool ascending = (side == SIDE_RIGHT) == (uplo == UPLO_UPPER);
-    const i64 k = (i64)diag.size();
-    for (i64 t = 0; t < k; ++t) {
-        const i64 d = ascending ? t : k - 1 - t;
-        if (diag[d] == 0) return d;
-    }
-    return -1;
+    const i64 th = threshold < 1 ? 1 : threshold;
+    std::function<i64(i64, i64)> rec = [&](i64 off, i64 n) -> i64 {
+        if (n == 0) return -1;
+        if (n <= th) {
+            for (i64 t = 0; t < n; ++t) {
+                const i64 d = ascending ? t : n - 1 - t;
+                if (diag[(size_t)(off + d)] == 0) return d;
+            }
+            return -1;
+        }
+        const i64 k = n / 2;
+        const i64 first = ascending ? rec(off, k) : rec(off + k, n - k);
+        if (first >= 0) return first;
+        return ascending ? rec(off + k, n - k) : rec(off, k);
+    };
+    return rec(0, (i64)diag.size());
 }
 
 void check_trsm_args(int side, int uplo, int diag, i64 m, i64 n, i64 ldt, i64 ldb) {
@@ -404,77 +626,30 @@ int rl_cup_u32(uint32_t* A, int64_t m, int64_t n, int64_t lda, uint32_t p, int64
             return;
         }
         require_device();
-        std::lock_guard<std::mutex> lk(g_mu);
         cudaStream_t s = cudaStreamPerThread;
-        u32* dA = (u32*)g_bufA.get((size_t)m * n * 4);
+        Call call(s);
+        Scratch& sc = call.sc;
         i64 r = 0;
         std::vector<u32> rrp_h, ipiv_h;
-        if (m * n >= (1 << 22) && m >= 8 * PB) {  // every spine node below splits (> PB rows)
-            // PCIe overlapped with the factorization along the recursion's spines
-            // (the splits of factor.cpp:35).  In: rows [0, m/2^D) are copied first
-            // and factored while the rest crosses the link in order on a second
-            // stream; each left-spine node (0, mm) waits for its bottom rows right
-            // before it first touches them.  Out: each right-spine node's top half
-            // goes back as soon as it is factored (final unless a later
-            // transposition or U-row move reaches it: then it is copied again).
-            constexpr int D = 3;
-            static cudaStream_t cs = nullptr, cs2 = nullptr;
-            static cudaEvent_t top = nullptr;
-            static std::vector<cudaEvent_t> evw, evd;
-            if (!cs) {
-                RL_CUDA_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-                RL_CUDA_CHECK(cudaStreamCreateWithFlags(&cs2, cudaStreamNonBlocking));
-                RL_CUDA_CHECK(cudaEventCreateWithFlags(&top, cudaEventDisableTiming));
-                evw.resize(D);
-                evd.resize(D);
-                for (int d = 0; d < D; ++d) {
-                    RL_CUDA_CHECK(cudaEventCreateWithFlags(&evw[d], cudaEventDisableTiming));
-                    RL_CUDA_CHECK(cudaEventCreateWithFlags(&evd[d], cudaEventDisableTiming));
-                }
-            }
-            CupEngine::NodeEvents waits, dones;
-            // left spine: node (0, sz[d]), sz[0] = m, sz[d+1] = sz[d] / 2
-            i64 sz[D + 1];
-            sz[0] = m;
-            for (int d = 0; d < D; ++d) sz[d + 1] = sz[d] / 2;
-            copy_h2d_2d(dA, n, A, lda, sz[D], n, s);
-            RL_CUDA_CHECK(cudaEventRecord(top, s));
-            RL_CUDA_CHECK(cudaStreamWaitEvent(cs, top, 0));
-            for (int d = D - 1; d >= 0; --d) {
-                copy_h2d_2d(dA + sz[d + 1] * n, n, A + sz[d + 1] * lda, lda, sz[d] - sz[d + 1], n, cs);
-                RL_CUDA_CHECK(cudaEventRecord(evw[d], cs));
-                waits[{0, (i32)sz[d]}] = evw[d];
-            }
-            // right spine: node (lo[d], len[d]); its top half [lo, lo + len/2) goes back
-            i64 lo[D], len[D], cut = 0;
-            for (int d = 0; d < D; ++d) {
-                lo[d] = d == 0 ? 0 : lo[d - 1] + len[d - 1] / 2;
-                len[d] = d == 0 ? m : len[d - 1] - len[d - 1] / 2;
-                dones[{(i32)lo[d], (i32)len[d]}] = evd[d];
-            }
-            const i64 kcap = std::min(m, n);
-            rrp_h.assign((size_t)kcap, 0);
-            ipiv_h.assign((size_t)kcap, 0);
-            CupEngine& e = engine_for(m, n, n, p, true);
-            e.set_host_overlap(waits, dones);
-            e.run(dA, s, true);
-            for (int d = 0; d < D; ++d) {
-                RL_CUDA_CHECK(cudaStreamWaitEvent(cs2, evd[d], 0));
-                copy_d2h_2d(A + lo[d] * lda, lda, dA + lo[d] * n, n, len[d] / 2, n, cs2);
-                cut = lo[d] + len[d] / 2;
-            }
-            e.results(&r, rrp_h.data(), ipiv_h.data(), s);  // synchronises s
-            copy_d2h_2d(A + cut * lda, lda, dA + cut * n, n, m - cut, n, s);
-            RL_CUDA_CHECK(cudaStreamSynchronize(cs2));
-            bool ident = true;
-            for (i64 j = 0; j < r && ident; ++j) ident = ipiv_h[(size_t)j] == (u32)j && rrp_h[(size_t)j] == (u32)j;
-            if (!ident) copy_d2h_2d(A, lda, dA, n, cut, n, s);
+        if (m * n <= TINY_MAX) {
+            tiny_cup(A, m, n, lda, p, sc, s, &r, rrp_h, ipiv_h);
         } else {
-            copy_h2d_2d(dA, n, A, lda, m, n, s);
-            factor_on_device(dA, m, n, n, p, s, &r, rrp_h, ipiv_h);
-            copy_d2h_2d(A, lda, dA, n, m, n, s);
+            u32* dA = (u32*)sc.get(SS_A, (size_t)m * n * 4);
+            if (!host_pinned(A) && !pageable_direct()) {
+                // pageable storage (ranklab::Mat is a std::vector, matrix.hpp:176): staged
+                // through the context's pinned ring by host threads, chunk by chunk
+                staged_h2d(dA, n, A, lda, m, n, sc, s);
+                factor_on_device(dA, m, n, n, p, s, &r, rrp_h, ipiv_h);
+                staged_d2h(A, lda, dA, n, m, n, sc, s);
+            } else if (m * n >= (1 << 22) && m >= 8 * PB) {
+                cup_host_overlapped(A, m, n, lda, p, dA, sc, s, &r, rrp_h, ipiv_h);
+            } else {
+                copy_h2d_2d(dA, n, A, lda, m, n, s);
+                factor_on_device(dA, m, n, n, p, s, &r, rrp_h, ipiv_h);
+                copy_d2h_2d(A, lda, dA, n, m, n, s);
+            }
+            RL_CUDA_CHECK(cudaStreamSynchronize(s));
         }
-        RL_CUDA_CHECK(cudaStreamSynchronize(s));
         if (rank) *rank = r;
         if (rrp) std::copy(rrp_h.begin(), rrp_h.begin() + r, rrp);
         if (sigma) sigma_from_ipiv(n, r, ipiv_h.data(), sigma);
@@ -490,7 +665,7 @@ int rl_ple_u32_dev(uint32_t* dA, int64_t m, int64_t n, int64_t lda, uint32_t p, 
         if (m == 0 || n == 0) return ple_empty(m, rank, row_perm, ops);
         if (!dA) throw Error(RL_EINVAL, "null matrix");
         require_device();
-        std::lock_guard<std::mutex> lk(g_mu);
+        Call call((cudaStream_t)stream);
         ple_on_device(dA, m, n, lda, p, (cudaStream_t)stream, rank, col_profile, row_perm, ops);
     });
 }
@@ -503,9 +678,9 @@ int rl_ple_u32(uint32_t* A, int64_t m, int64_t n, int64_t lda, uint32_t p, int64
         if (m == 0 || n == 0) return ple_empty(m, rank, row_perm, ops);
         if (!A) throw Error(RL_EINVAL, "null matrix");
         require_device();
-        std::lock_guard<std::mutex> lk(g_mu);
         cudaStream_t s = cudaStreamPerThread;
-        u32* dA = (u32*)g_bufA.get((size_t)m * n * 4);
+        Call call(s);
+        u32* dA = (u32*)call.sc.get(SS_A, (size_t)m * n * 4);
         copy_h2d_2d(dA, n, A, lda, m, n, s);
         ple_on_device(dA, m, n, n, p, s, rank, col_profile, row_perm, ops);
         copy_d2h_2d(A, lda, dA, n, m, n, s);
@@ -525,7 +700,7 @@ int rl_col_ech_trans_u32_dev(uint32_t* dA, int64_t m, int64_t n, int64_t lda, ui
         }
         if (!dA) throw Error(RL_EINVAL, "null matrix");
         require_device();
-        std::lock_guard<std::mutex> lk(g_mu);
+        Call call((cudaStream_t)stream);
         col_ech_dev_impl(dA, m, n, lda, p, reduced != 0, rank, rrp, sigma, ops, (cudaStream_t)stream);
     });
 }
@@ -541,9 +716,9 @@ int rl_col_ech_trans_u32(uint32_t* A, int64_t m, int64_t n, int64_t lda, uint32_
         }
         if (!A) throw Error(RL_EINVAL, "null matrix");
         require_device();
-        std::lock_guard<std::mutex> lk(g_mu);
         cudaStream_t s = cudaStreamPerThread;
-        u32* dA = (u32*)g_bufA.get((size_t)m * n * 4);
+        Call call(s);
+        u32* dA = (u32*)call.sc.get(SS_A, (size_t)m * n * 4);
         copy_h2d_2d(dA, n, A, lda, m, n, s);
         col_ech_dev_impl(dA, m, n, n, p, reduced != 0, rank, rrp, sigma, ops, s);
         copy_d2h_2d(A, lda, dA, n, m, n, s);
@@ -560,7 +735,7 @@ int rl_invert_u32_dev(uint32_t* dA, int64_t n, int64_t lda, uint32_t p, uint64_t
         if (n == 0) return;
         if (!dA) throw Error(RL_EINVAL, "null matrix");
         require_device();
-        std::lock_guard<std::mutex> lk(g_mu);
+        Call call((cudaStream_t)stream);
         invert_dev_impl(dA, n, lda, p, ops, (cudaStream_t)stream);
     });
 }
@@ -573,9 +748,9 @@ int rl_invert_u32(uint32_t* A, int64_t n, int64_t lda, uint32_t p, uint64_t* ops
         if (n == 0) return;
         if (!A) throw Error(RL_EINVAL, "null matrix");
         require_device();
-        std::lock_guard<std::mutex> lk(g_mu);
         cudaStream_t s = cudaStreamPerThread;
-        u32* dA = (u32*)g_bufA.get((size_t)n * n * 4);
+        Call call(s);
+        u32* dA = (u32*)call.sc.get(SS_A, (size_t)n * n * 4);
         copy_h2d_2d(dA, n, A, lda, n, n, s);
         int st = RL_OK;
         try {
@@ -602,14 +777,14 @@ int rl_trsm_u32_dev(int side, int uplo, int diag, const uint32_t* dT, int64_t ld
             return;
         }
         require_device();
-        std::lock_guard<std::mutex> lk(g_mu);
         cudaStream_t s = (cudaStream_t)stream;
+        Call call(s);
         if (!diag) {
             std::vector<u32> dg((size_t)k);
             RL_CUDA_CHECK(cudaMemcpy2DAsync(dg.data(), 4, dT, (ldt + 1) * 4, 4, k,
                                             cudaMemcpyDeviceToHost, s));
             RL_CUDA_CHECK(cudaStreamSynchronize(s));
-            const i64 d = first_zero_diagonal(side, uplo, dg);
+            const i64 d = first_zero_diagonal(side, uplo, dg, threshold);
             if (d >= 0) throw Error(RL_ESINGULAR, "singular diagonal at " + std::to_string(d));
         }
         trsm_ops(side, uplo, diag, m, n, threshold, ops);
@@ -631,15 +806,15 @@ int rl_trsm_u32(int side, int uplo, int diag, const uint32_t* T, int64_t ldt, ui
         if (!diag) {
             std::vector<u32> dg((size_t)k);
             for (i64 d = 0; d < k; ++d) dg[d] = T[d * ldt + d];
-            const i64 d = first_zero_diagonal(side, uplo, dg);
+            const i64 d = first_zero_diagonal(side, uplo, dg, threshold);
             if (d >= 0) throw Error(RL_ESINGULAR, "singular diagonal at " + std::to_string(d));
         }
         trsm_ops(side, uplo, diag, m, n, threshold, ops);
         require_device();
-        std::lock_guard<std::mutex> lk(g_mu);
         cudaStream_t s = cudaStreamPerThread;
-        u32* dT = (u32*)g_bufA.get((size_t)k * k * 4);
-        u32* dB = (u32*)g_bufB.get((size_t)m * n * 4);
+        Call call(s);
+        u32* dT = (u32*)call.sc.get(SS_A, (size_t)k * k * 4);
+        u32* dB = (u32*)call.sc.get(SS_B, (size_t)m * n * 4);
         copy_h2d_2d(dT, k, T, ldt, k, k, s);
         copy_h2d_2d(dB, n, B, ldb, m, n, s);
         trsm_dev_impl(side, uplo, diag, dT, k, dB, n, m, n, p, s);
@@ -719,7 +894,7 @@ int rl_mm_u32_dev(const uint32_t* dA, int64_t lda, const uint32_t* dB, int64_t l
         if (m < 0 || l < 0 || n < 0) throw Error(RL_EDIM, "negative dimension");
         if (alpha >= p || beta >= p) throw Error(RL_EINVAL, "alpha/beta not canonical");
         require_device();
-        std::lock_guard<std::mutex> lk(g_mu);
+        Call call((cudaStream_t)stream);
         mm_dev_impl(dA, lda, dB, ldb, dC, ldc, m, l, n, alpha, beta, p, (cudaStream_t)stream);
     });
 }
@@ -733,7 +908,7 @@ int rl_mm_u32_dev_grid(const uint32_t* dA, int64_t lda, const uint32_t* dB, int6
         if (alpha >= p || beta >= p) throw Error(RL_EINVAL, "alpha/beta not canonical");
         if (max_ctas < 0) throw Error(RL_EINVAL, "negative grid bound");
         require_device();
-        std::lock_guard<std::mutex> lk(g_mu);
+        Call call((cudaStream_t)stream);
         mm_dev_impl(dA, lda, dB, ldb, dC, ldc, m, l, n, alpha, beta, p, (cudaStream_t)stream,
                     max_ctas);
     });
@@ -770,11 +945,11 @@ int rl_mm_u32(const uint32_t* A, int64_t lda, const uint32_t* B, int64_t ldb, ui
         }
         if (m == 0 || n == 0) return;
         require_device();
-        std::lock_guard<std::mutex> lk(g_mu);
         cudaStream_t s = cudaStreamPerThread;
-        u32* dA = (u32*)g_bufA.get((size_t)std::max<i64>(m * l, 1) * 4);
-        u32* dB = (u32*)g_bufB.get((size_t)std::max<i64>(l * n, 1) * 4);
-        u32* dC = (u32*)g_bufC.get((size_t)m * n * 4);
+        Call call(s);
+        u32* dA = (u32*)call.sc.get(SS_A, (size_t)std::max<i64>(m * l, 1) * 4);
+        u32* dB = (u32*)call.sc.get(SS_B, (size_t)std::max<i64>(l * n, 1) * 4);
+        u32* dC = (u32*)call.sc.get(SS_C, (size_t)m * n * 4);
         copy_h2d_2d(dA, l, A, lda, m, l, s);
         copy_h2d_2d(dB, n, B, ldb, l, n, s);
         copy_h2d_2d(dC, n, C, ldc, m, n, s);
@@ -791,6 +966,26 @@ int rl_random_matrix_u32_dev(uint32_t* dA, int64_t m, int64_t n, int64_t lda, ui
         check_dims(m, n, lda);
         require_device();
         gen_random_matrix(dA, lda, m, n, seed, p, (cudaStream_t)stream);
+    });
+}
+
+int rl_digest_u32_dev(const uint32_t* dA, int64_t m, int64_t n, int64_t lda, uint64_t* digest,
+                      void* stream) {
+    return guard([&] {
+        check_dims(m, n, lda);
+        if (!digest) throw Error(RL_EINVAL, "null digest");
+        *digest = 0;
+        if (m == 0 || n == 0) return;
+        if (!dA) throw Error(RL_EINVAL, "null matrix");
+        require_device();
+        cudaStream_t s = (cudaStream_t)stream;
+        Call call(s);
+        auto* d = (unsigned long long*)call.sc.get(SS_DIGEST, sizeof(unsigned long long));
+        digest_u32(dA, lda, m, n, d, s);
+        unsigned long long h = 0;
+        RL_CUDA_CHECK(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, s));
+        RL_CUDA_CHECK(cudaStreamSynchronize(s));
+        *digest = h;
     });
 }
 
@@ -812,9 +1007,9 @@ int rl_cup_batched_u32_dev(uint32_t* dA, int64_t batch, int64_t m, int64_t n, in
             return;
         }
         require_device();
-        std::lock_guard<std::mutex> lk(g_mu);
         cudaStream_t s = (cudaStream_t)stream;
-        i32* dmeta = (i32*)g_bufI.get((size_t)batch * (1 + 2 * kcap) * 4);
+        Call call(s);
+        i32* dmeta = (i32*)call.sc.get(SS_META, (size_t)batch * (1 + 2 * kcap) * 4);
         i32* d_ranks = dmeta;
         i32* d_rrp = dmeta + batch;
         i32* d_ipiv = d_rrp + batch * kcap;
@@ -856,15 +1051,10 @@ int rl_cup_batched_u32(uint32_t* A, int64_t batch, int64_t m, int64_t n, int64_t
         }
         if (!A) throw Error(RL_EINVAL, "null matrix");
         require_device();
-        std::lock_guard<std::mutex> lk(g_mu);
-        static cudaStream_t sh = nullptr, sc = nullptr, sd = nullptr;
-        if (!sh) {
-            RL_CUDA_CHECK(cudaStreamCreateWithFlags(&sh, cudaStreamNonBlocking));
-            RL_CUDA_CHECK(cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking));
-            RL_CUDA_CHECK(cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking));
-        }
-        u32* dA = (u32*)g_bufA.get((size_t)batch * stride * 4);
-        i32* dmeta = (i32*)g_bufI.get((size_t)batch * (1 + 2 * kcap) * 4);
+        Call call(cudaStreamPerThread);
+        cudaStream_t sh = call.sc.aux_stream(0), sc = call.sc.aux_stream(1), sd = call.sc.aux_stream(2);
+        u32* dA = (u32*)call.sc.get(SS_A, (size_t)batch * stride * 4);
+        i32* dmeta = (i32*)call.sc.get(SS_META, (size_t)batch * (1 + 2 * kcap) * 4);
         i32* d_ranks = dmeta;
         i32* d_rrp = dmeta + batch;
         i32* d_ipiv = d_rrp + batch * kcap;
@@ -876,15 +1066,19 @@ int rl_cup_batched_u32(uint32_t* A, int64_t batch, int64_t m, int64_t n, int64_t
         }
         for (i64 c = 0; c < chunks; ++c) {
             const i64 t0 = batch * c / chunks, t1 = batch * (c + 1) / chunks;
-            const size_t bytes = (size_t)(t1 - t0) * stride * 4;
-            RL_CUDA_CHECK(cudaMemcpyAsync(dA + t0 * stride, A + t0 * stride, bytes, cudaMemcpyHostToDevice, sh));
+            // matrix t is the m*n words at A + t*stride: copy exactly those (the
+            // caller's buffer may end right after the last matrix's m*n words)
+            const size_t pitch = (size_t)stride * 4, width = (size_t)m * n * 4;
+            RL_CUDA_CHECK(cudaMemcpy2DAsync(dA + t0 * stride, pitch, A + t0 * stride, pitch, width, t1 - t0,
+                                            cudaMemcpyHostToDevice, sh));
             RL_CUDA_CHECK(cudaEventRecord(ev_in[c], sh));
             RL_CUDA_CHECK(cudaStreamWaitEvent(sc, ev_in[c], 0));
             cup_batched(dA + t0 * stride, t1 - t0, (i32)m, (i32)n, stride, p, d_ranks + t0,
                         d_rrp + t0 * kcap, d_ipiv + t0 * kcap, (i32)kcap, sc);
             RL_CUDA_CHECK(cudaEventRecord(ev_out[c], sc));
             RL_CUDA_CHECK(cudaStreamWaitEvent(sd, ev_out[c], 0));
-            RL_CUDA_CHECK(cudaMemcpyAsync(A + t0 * stride, dA + t0 * stride, bytes, cudaMemcpyDeviceToHost, sd));
+            RL_CUDA_CHECK(cudaMemcpy2DAsync(A + t0 * stride, pitch, dA + t0 * stride, pitch, width, t1 - t0,
+                                            cudaMemcpyDeviceToHost, sd));
         }
         std::vector<i32> h((size_t)batch * (1 + 2 * kcap));
         RL_CUDA_CHECK(cudaMemcpyAsync(h.data(), dmeta, h.size() * 4, cudaMemcpyDeviceToHost, sc));
@@ -914,17 +1108,16 @@ int rl_profile_gemm_dev(const uint32_t* dA, const uint32_t* dB, uint32_t* dC, in
     return guard([&] {
         check_field(p);
         require_device();
-        std::lock_guard<std::mutex> lk(g_mu);
         cudaStream_t s = (cudaStream_t)stream;
+        Call call(s);
         const int L = limbs_for(p);
         if (l > tc_kmax(L)) throw Error(RL_EINVAL, "profile: l exceeds the exact-accumulation bound");
         GemmArgs g{};
         g.A = dA; g.lda = l; g.B = dB; g.ldb = n; g.C = dC; g.ldc = n; g.M = (i32)m;
         g.k_lo = dyn_c(0); g.k_hi = dyn_c((i32)l); g.n_lo = dyn_c(0); g.n_hi = dyn_c((i32)n);
         g.alpha = p - 1; g.beta = 1 % p; g.f = make_fp(p);
-        static DevBuf a2, b2;
-        uint8_t* pa = (uint8_t*)a2.get(tc_a2_bytes(L, m, l));
-        uint8_t* pb = (uint8_t*)b2.get(tc_b2_bytes(L, n, l));
+        uint8_t* pa = (uint8_t*)call.sc.get(SS_PROF_A2, tc_a2_bytes(L, m, l));
+        uint8_t* pb = (uint8_t*)call.sc.get(SS_PROF_B2, tc_b2_bytes(L, n, l));
         cudaEvent_t e0, e1, e2;
         RL_CUDA_CHECK(cudaEventCreate(&e0));
         RL_CUDA_CHECK(cudaEventCreate(&e1));
@@ -957,14 +1150,26 @@ int rl_cup_plan_stats(int64_t m, int64_t n, int64_t lda, uint32_t p, int64_t* st
     return guard([&] {
         check_field(p);
         check_dims(m, n, lda);
-        std::lock_guard<std::mutex> lk(g_mu);
-        CupEngine& e = engine_for(m, n, lda, p);
-        const auto& st = e.stats();
+        // the most recently used engine of this shape on this device
+        std::shared_ptr<CupEngine> e;
+        {
+            std::lock_guard<std::mutex> lk(g_engines_mu);
+            unsigned long long best = 0;
+            const int dev = current_device();
+            for (auto& kv : g_engines)
+                if (kv.first.dev == dev && kv.first.m == m && kv.first.n == n && kv.first.lda == lda &&
+                    kv.first.p == p && !kv.first.split && kv.second.used >= best) {
+                    best = kv.second.used;
+                    e = kv.second.e;
+                }
+        }
+        if (!e) e = engine_for(m, n, lda, p, nullptr);
+        const auto& st = e->stats();
         stats[0] = st.gemms;
         stats[1] = st.tc_gemms;
         stats[2] = st.panels;
         stats[3] = st.trsm_leaves;
-        stats[4] = (int64_t)e.workspace_bytes();
+        stats[4] = (int64_t)e->workspace_bytes();
         stats[5] = st.launches;
     });
 }

@@ -24,16 +24,6 @@
 
 namespace rl {
 
-int num_sms() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        RL_CUDA_CHECK(cudaGetDevice(&dev));
-        RL_CUDA_CHECK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
-    }
-    return n;
-}
-
 CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_(p) {
     f_ = make_fp(p);
     L_ = limbs_for(p);
@@ -74,6 +64,7 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
     RL_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     RL_CUDA_CHECK(cudaStreamCreateWithPriority(&s2_, cudaStreamNonBlocking, prio_lo));
     RL_CUDA_CHECK(cudaStreamCreateWithPriority(&s3_, cudaStreamNonBlocking, prio_hi));
+    RL_CUDA_CHECK(cudaEventCreateWithFlags(&done_, cudaEventDisableTiming));
     events_.resize(events_needed_ + 4);
     for (auto& e : events_) RL_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     if (a2_cap_) RL_CUDA_CHECK(cudaMalloc(&a2_, a2_cap_));
@@ -87,6 +78,9 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
 }
 
 CupEngine::~CupEngine() {
+    // an evicted engine may still have an asynchronous run in flight
+    if (done_) cudaEventSynchronize(done_);
+    if (done_) cudaEventDestroy(done_);
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     cudaFree(meta_);
     for (auto& e : events_) cudaEventDestroy(e);
@@ -480,6 +474,7 @@ void CupEngine::set_host_overlap(const NodeEvents& waits, const NodeEvents& done
 void CupEngine::run(u32* dA, cudaStream_t s, bool use_graph) {
     if (!use_graph) {
         enqueue(dA, s);
+        RL_CUDA_CHECK(cudaEventRecord(done_, s));
         return;
     }
     if (!graph_exec_ || graph_A_ != dA) {
@@ -507,6 +502,7 @@ void CupEngine::run(u32* dA, cudaStream_t s, bool use_graph) {
         graph_A_ = dA;
     }
     RL_CUDA_CHECK(cudaGraphLaunch(graph_exec_, s));
+    RL_CUDA_CHECK(cudaEventRecord(done_, s));
 }
 
 void CupEngine::results(i64* rank, u32* rrp_host, u32* ipiv_host, cudaStream_t s) {

@@ -138,6 +138,7 @@ private:
     cudaStream_t work_stream() const { return lane_ ? lane_->st : s_; }
     cudaGraphExec_t graph_exec_ = nullptr;
     u32* graph_A_ = nullptr;
+    cudaEvent_t done_ = nullptr;  // end of the last run: the destructor waits for it
     Stats stats_;
 };
 

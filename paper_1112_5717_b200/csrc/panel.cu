@@ -571,13 +571,12 @@ void panel_uinv(const PanelArgs& a, cudaStream_t s) {
     // tail-kernel CTA (launched right after it) shares its SM: this latency-bound
     // chain ran ~3x slower beside the tail's multiply-add streams.
     const size_t smem = std::max<size_t>(sizeof(u32) * 3 * PB * (PB + 1), 200 * 1024);
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr_once{0};
+    if (first_on_device(attr_once)) {
         RL_CUDA_CHECK(cudaFuncSetAttribute(panel_uinv_kernel<true>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         RL_CUDA_CHECK(cudaFuncSetAttribute(panel_uinv_kernel<false>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
     }
     if (a.f.p <= 65536u) panel_uinv_kernel<true><<<1, 512, smem, s>>>(a);
     else panel_uinv_kernel<false><<<1, 512, smem, s>>>(a);
@@ -588,13 +587,12 @@ void panel_tail(const PanelArgs& a, cudaStream_t s) {
     // tiles: Minv + P tile; the U^{-1} CTA: U, X, T (3 blocks of PB x (PB+1))
     const size_t smem = std::max<size_t>(sizeof(u32) * (PB * MIP + PB * (TT + 4)) + 2 * (PB + TT) * BPI,
                                          sizeof(u32) * 3 * PB * (PB + 1));
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr_once{0};
+    if (first_on_device(attr_once)) {
         RL_CUDA_CHECK(cudaFuncSetAttribute(panel_tail_kernel<true>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         RL_CUDA_CHECK(cudaFuncSetAttribute(panel_tail_kernel<false>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
     }
     const int grid = std::max(1, std::min((a.N + TT - 1) / TT, 8 * num_sms())) + 1;
     RL_ONCE_MAX_SMEM(panel_tail_kernel<true>);

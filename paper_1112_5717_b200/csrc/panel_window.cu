@@ -809,15 +809,14 @@ void build_inv_table(uint16_t* table, u32 p, cudaStream_t s) {
 void panel_window(const PanelArgs& a, cudaStream_t s) {
     const bool sp = a.f.p <= 65536u;
     const size_t smem = sizeof(u32) * PB * RP + (sp ? 65536 * 2 : 0);
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr_once{0};
+    if (first_on_device(attr_once)) {
         RL_CUDA_CHECK(cudaFuncSetAttribute(panel_window_kernel<true>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)(sizeof(u32) * PB * RP + 65536 * 2)));
         RL_CUDA_CHECK(cudaFuncSetAttribute(panel_window_kernel<false>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)(sizeof(u32) * PB * RP)));
-        attr = true;
     }
     RL_ONCE_MAX_SMEM(panel_window_kernel<true>);
     RL_ONCE_MAX_SMEM(panel_window_kernel<false>);

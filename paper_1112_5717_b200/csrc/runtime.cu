@@ -1,0 +1,86 @@
+// runtime.cu -- per-device and per-stream host state of the library.
+//
+// The reference's threading contract (proj/README.md:164-168): no internal
+// threads, disjoint views may be processed concurrently.  Here that means no
+// process-global mutable state on the compute path: caches are keyed by the
+// device, workspaces by (device, stream), so concurrent calls on distinct
+// streams -- or distinct host threads using cudaStreamPerThread -- proceed in
+// parallel (SURVEY.md 8(b) "Threading").
+#include <map>
+#include <memory>
+#include <thread>
+#include <tuple>
+
+#include "common.cuh"
+#include "runtime.h"
+
+namespace rl {
+
+int current_device() {
+    int d = 0;
+    RL_CUDA_CHECK(cudaGetDevice(&d));
+    return d;
+}
+
+int num_sms() {
+    static std::atomic<int> cache[64] = {};
+    const int d = current_device() & 63;
+    int n = cache[d].load(std::memory_order_relaxed);
+    if (!n) {
+        RL_CUDA_CHECK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, current_device()));
+        cache[d].store(n, std::memory_order_relaxed);
+    }
+    return n;
+}
+
+namespace {
+struct ScratchKey {
+    int dev;
+    cudaStream_t s;
+    std::thread::id tid;  // only for cudaStreamPerThread
+    bool operator<(const ScratchKey& o) const {
+        return std::tie(dev, s, tid) < std::tie(o.dev, o.s, o.tid);
+    }
+};
+std::mutex g_scratch_mu;
+std::map<ScratchKey, std::unique_ptr<Scratch>>& scratch_map() {
+    static auto* m = new std::map<ScratchKey, std::unique_ptr<Scratch>>();  // never destroyed:
+    return *m;  // CUDA objects must not be released after the driver shut down
+}
+}  // namespace
+
+Scratch& scratch_for(cudaStream_t s) {
+    ScratchKey k{current_device(), s, s == cudaStreamPerThread ? std::this_thread::get_id() : std::thread::id()};
+    std::lock_guard<std::mutex> lk(g_scratch_mu);
+    auto& m = scratch_map();
+    auto it = m.find(k);
+    if (it != m.end()) return *it->second;
+    auto sc = std::make_unique<Scratch>();
+    sc->device = k.dev;
+    Scratch& ref = *sc;
+    m.emplace(k, std::move(sc));
+    return ref;
+}
+
+cudaStream_t Scratch::aux_stream(int i) {
+    if (!aux[i]) RL_CUDA_CHECK(cudaStreamCreateWithFlags(&aux[i], cudaStreamNonBlocking));
+    return aux[i];
+}
+
+cudaEvent_t Scratch::event(int i) {
+    if (!ev[i]) RL_CUDA_CHECK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    return ev[i];
+}
+
+void* Scratch::pinned_ring(size_t bytes) {
+    if (bytes > pinned_cap) {
+        if (pinned) cudaFreeHost(pinned);
+        pinned = nullptr;
+        pinned_cap = 0;
+        if (cudaMallocHost(&pinned, bytes) != cudaSuccess) throw Error(8 /*RL_ENOMEM*/, "cudaMallocHost failed");
+        pinned_cap = bytes;
+    }
+    return pinned;
+}
+
+}  // namespace rl

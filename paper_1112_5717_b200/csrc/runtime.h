@@ -3,6 +3,8 @@
 #include <utility>
 #include <cuda_runtime.h>
 
+#include <atomic>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 
@@ -21,23 +23,45 @@ struct CudaError : Error {
                                     file + ":" + std::to_string(line) + " (" + what + ")") {}
 };
 
+// The calling thread's current device (every per-device cache is keyed by it).
+int current_device();
+// SM count of the current device (cached per device).
 int num_sms();
+
+// True exactly once per (call site, device): function attributes
+// (cudaFuncSetAttribute) are per device, so "set once" is per device too.
+inline bool first_on_device(std::atomic<unsigned long long>& mask) {
+    const int d = current_device() & 63;
+    const unsigned long long bit = 1ull << d;
+    if (mask.load(std::memory_order_acquire) & bit) return false;
+    return !(mask.fetch_or(bit, std::memory_order_acq_rel) & bit);
+}
+#define RL_ONCE_PER_DEVICE()                                 \
+    ([]() -> std::atomic<unsigned long long>& {              \
+        static std::atomic<unsigned long long> m_{0};        \
+        return m_;                                           \
+    }())
 
 // Every kernel of the CUP path prefers the maximum shared-memory carveout, so
 // consecutive launches (1 KB ... 200 KB of shared memory) never make an SM
-// reconfigure its L1/shared split between kernels.  Once per kernel.
+// reconfigure its L1/shared split between kernels.  Once per kernel and device.
 template <class F>
 inline void prefer_max_smem(F* kernel) {
     cudaFuncSetAttribute(reinterpret_cast<const void*>(kernel),
                          cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
-#define RL_ONCE_MAX_SMEM(kernel)          \
-    do {                                  \
-        static bool once_ = false;        \
-        if (!once_) {                     \
-            prefer_max_smem(kernel);      \
-            once_ = true;                 \
-        }                                 \
+#define RL_ONCE_MAX_SMEM(kernel)                                     \
+    do {                                                             \
+        static std::atomic<unsigned long long> once_{0};             \
+        if (first_on_device(once_)) prefer_max_smem(kernel);         \
+    } while (0)
+// cudaFuncSetAttribute(kernel, MaxDynamicSharedMemorySize, bytes) once per device.
+#define RL_ONCE_SMEM_LIMIT(kernel, bytes)                                                   \
+    do {                                                                                    \
+        static std::atomic<unsigned long long> once_{0};                                    \
+        if (first_on_device(once_))                                                         \
+            RL_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                               (int)(bytes)));                              \
     } while (0)
 
 // Launch as a programmatic dependent of the previous kernel on the stream (the
@@ -61,7 +85,7 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 }
 
 // Growable device scratch buffer (workspaces of the host-pointer entry points
-// and of the dense/triangular helpers; callers hold the C-ABI mutex).
+// and of the dense/triangular helpers; one set per call context, see Scratch).
 struct DevBuf {
     void* ptr = nullptr;
     size_t cap = 0;
@@ -76,5 +100,34 @@ struct DevBuf {
         return ptr;
     }
 };
+
+// Per-(device, stream) call context.  The C-ABI entry points hold `mu` for the
+// duration of a call, so calls on DISTINCT streams never share a workspace and
+// never wait for each other, while calls on the same stream (which the GPU
+// serialises anyway) cannot reallocate a buffer under an in-flight call.
+// cudaStreamPerThread is one handle for all threads: its contexts are keyed by
+// the calling thread as well (each thread has its own per-thread stream).
+enum ScratchSlot {
+    SS_A, SS_B, SS_C, SS_META, SS_TRANS,          // host-pointer entry points
+    SS_X, SS_Y, SS_T, SS_IDX, SS_PERM,            // echelon / inverse / trsm seam
+    SS_MM_A2, SS_MM_B2, SS_TRI_W, SS_MOVE,        // dense helpers (tri.cu)
+    SS_PROF_A2, SS_PROF_B2, SS_DIGEST,            // benchmark / test helpers
+    SS_COUNT
+};
+struct Scratch {
+    std::mutex mu;
+    int device = 0;
+    DevBuf buf[SS_COUNT];
+    cudaStream_t aux[4] = {};     // copy streams of the host-buffer paths (lazy)
+    cudaEvent_t ev[24] = {};      // their events (lazy)
+    void* pinned = nullptr;       // pinned staging ring of the pageable-host path (lazy)
+    size_t pinned_cap = 0;
+    void* host_mapped = nullptr;  // mapped pinned result block of the tiny-matrix path (lazy)
+    void* get(int slot, size_t bytes) { return buf[slot].get(bytes); }
+    cudaStream_t aux_stream(int i);
+    cudaEvent_t event(int i);
+    void* pinned_ring(size_t bytes);
+};
+Scratch& scratch_for(cudaStream_t s);
 
 }  // namespace rl

@@ -196,9 +196,11 @@ void mm_dense(const u32* A, i64 lda, const u32* B, i64 ldb, u32* C, i64 ldc, i64
         g.max_ctas = max_ctas;
         const bool tc = kc >= 32 && n >= 32 && m >= 32;
         if (tc) {
-            static DevBuf a2, b2;
-            uint8_t* pa = (uint8_t*)a2.get(tc_a2_bytes(L, m, kc));
-            uint8_t* pb = (uint8_t*)b2.get(tc_b2_bytes(L, n, kc));
+            // workspaces of the calling stream's context: concurrent mm_dense
+            // calls on distinct streams never share them
+            Scratch& sc = scratch_for(s);
+            uint8_t* pa = (uint8_t*)sc.get(SS_MM_A2, tc_a2_bytes(L, m, kc));
+            uint8_t* pb = (uint8_t*)sc.get(SS_MM_B2, tc_b2_bytes(L, n, kc));
             gemm_tc(g, L, kc, n, pa, pb, s);
         } else {
             gemm_simt(g, kc, n, s);
@@ -225,8 +227,7 @@ void tri_inverse(u32* X, i64 ldx, i32 k, bool upper, const Fp& f, cudaStream_t s
     if (f.p <= 65536u) tri_inv_base_kernel<true><<<nb, TB, 0, s>>>(X, ldx, k, upper, f);
     else tri_inv_base_kernel<false><<<nb, TB, 0, s>>>(X, ldx, k, upper, f);
     RL_CUDA_CHECK(cudaGetLastError());
-    static DevBuf wbuf;
-    tri_inv_rec(X, ldx, k, upper, f, wbuf, s);
+    tri_inv_rec(X, ldx, k, upper, f, scratch_for(s).buf[SS_TRI_W], s);
 }
 
 void compress_pivot_rows(u32* A, i64 lda, i32 r, const i32* d_rrp, cudaStream_t s) {
@@ -237,8 +238,7 @@ void compress_pivot_rows(u32* A, i64 lda, i32 r, const i32* d_rrp, cudaStream_t 
 
 void move_rows(u32* A, i64 lda, i64 ncols, const i32* d_idx, i32 count, cudaStream_t s) {
     if (count <= 0 || ncols <= 0) return;
-    static DevBuf tbuf;
-    u32* T = (u32*)tbuf.get((size_t)count * ncols * 4);
+    u32* T = (u32*)scratch_for(s).get(SS_MOVE, (size_t)count * ncols * 4);
     const dim3 grid((unsigned)std::min<i64>((ncols + 255) / 256, 64), (unsigned)std::min(count, 4096));
     gather_rows_kernel<<<grid, 256, 0, s>>>(T, A, lda, ncols, d_idx, count);
     RL_CUDA_CHECK(cudaGetLastError());

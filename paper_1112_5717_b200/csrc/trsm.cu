@@ -274,12 +274,11 @@ void launch_node(const TrsmNodeArgs& a, cudaStream_t s) {
     const int nblk = a.nleaf + a.nleaf * (a.nleaf - 1) / 2;
     const size_t part = KS > 1 ? sizeof(u64) * (KS - 1) * TM * PB : 0;
     const size_t smem = sizeof(u32) * (TM * GW + (size_t)nblk * PB * BW) + part;
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr_once{0};
+    if (first_on_device(attr_once)) {
         const size_t maxs = sizeof(u32) * (TM * GW + (size_t)10 * PB * BW) + part;
         RL_CUDA_CHECK(cudaFuncSetAttribute(trsm_node_kernel<SP, TR, KS>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxs));
-        attr = true;
     }
     // one staging of the U blocks per CTA: about one CTA per SM, each looping
     // over its row tiles

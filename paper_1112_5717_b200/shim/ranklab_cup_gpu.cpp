@@ -16,6 +16,7 @@
 
 #include "ranklab/factor.hpp"
 #include "ranklab_gpu.h"
+#include "rl_errors.hpp"
 
 namespace ranklab {
 
@@ -32,7 +33,7 @@ PackedCup cup(MatView a, OpCounter& ctr) {
     std::uint64_t ops[4] = {0, 0, 0, 0};
     const int st = rl_cup_u32(base, static_cast<std::int64_t>(m), static_cast<std::int64_t>(n),
                               lda, a.field().modulus(), &rank, rrp.data(), sigma.data(), ops);
-    if (st != RL_OK) throw Error(std::string("rl_cup_u32: ") + rl_last_error());
+    if (st != RL_OK) gpu_shim::rethrow(st, "rl_cup_u32", a.field().modulus());
     ctr.n_mul += ops[0];
     ctr.n_addsub += ops[1];
     ctr.n_divinv += ops[2];
@@ -60,7 +61,7 @@ PackedPle ple(MatView a, OpCounter& ctr) {
     std::uint64_t ops[4] = {0, 0, 0, 0};
     const int st = rl_ple_u32(base, static_cast<std::int64_t>(m), static_cast<std::int64_t>(n),
                               lda, a.field().modulus(), &rank, prof.data(), perm.data(), ops);
-    if (st != RL_OK) throw Error(std::string("rl_ple_u32: ") + rl_last_error());
+    if (st != RL_OK) gpu_shim::rethrow(st, "rl_ple_u32", a.field().modulus());
     ctr.n_mul += ops[0];
     ctr.n_addsub += ops[1];
     ctr.n_divinv += ops[2];

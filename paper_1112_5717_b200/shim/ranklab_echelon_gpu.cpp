@@ -19,6 +19,7 @@
 #include "ranklab/errors.hpp"
 #include "ranklab/solvers.hpp"
 #include "ranklab_gpu.h"
+#include "rl_errors.hpp"
 
 namespace ranklab {
 
@@ -49,7 +50,7 @@ T echelon(MatView a, OpCounter& ctr, int reduced) {
                                         static_cast<std::int64_t>(n), stride_of(a),
                                         a.field().modulus(), reduced, &rank, rrp.data(),
                                         sigma.data(), ops);
-    if (st != RL_OK) throw Error(std::string("rl_col_ech_trans_u32: ") + rl_last_error());
+    if (st != RL_OK) gpu_shim::rethrow(st, "rl_col_ech_trans_u32", a.field().modulus());
     charge(ctr, ops);
     out.rank = static_cast<std::size_t>(rank);
     rrp.resize(out.rank);
@@ -76,8 +77,7 @@ void invert_in_place(MatView a, OpCounter& ctr) {
     const int st = rl_invert_u32(&a(0, 0), static_cast<std::int64_t>(n), stride_of(a),
                                  a.field().modulus(), ops);
     charge(ctr, ops);
-    if (st == RL_ESINGULAR) throw SingularMatrix();
-    if (st != RL_OK) throw Error(std::string("rl_invert_u32: ") + rl_last_error());
+    if (st != RL_OK) gpu_shim::rethrow(st, "rl_invert_u32", a.field().modulus());
 }
 
 }  // namespace ranklab

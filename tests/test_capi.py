@@ -138,8 +138,14 @@ def test_trsm_errors_need_no_device():
     t = np.array([[1, 2, 3], [0, 0, 4], [0, 0, 5]], np.uint32)
     b = np.arange(6, dtype=np.uint32).reshape(2, 3)
     keep = b.copy()
-    with pytest.raises(G.SingularMatrix, match="at 1"):  # ascending traversal: first zero is 1
+    # the reference reports the index local to the base block its halving
+    # recursion stops in (kernels.cpp:87-90; pinned against the reference in
+    # oracle/shim_check.cpp): threshold 1 -> block [1] -> index 0, threshold 3 ->
+    # one block [0, 3) -> index 1 (ascending traversal for Right/Upper)
+    with pytest.raises(G.SingularMatrix, match="at 0"):
         G.trsm(G.Side.Right, G.UpLo.Upper, G.Diag.NonUnit, t, b, 7)
+    with pytest.raises(G.SingularMatrix, match="at 1"):
+        G.trsm(G.Side.Right, G.UpLo.Upper, G.Diag.NonUnit, t, b, 7, threshold=3)
     assert np.array_equal(b, keep)
     big = np.ones((4, 4), np.uint32)
     with pytest.raises(G.OverlapError):

@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Device timeline of one warm CUP (CUPTI kernel records via torch.profiler):
 per-kernel busy time, and the idle gaps between consecutive kernels.
-Usage: timeline_cup.py [n] [p] [out.json]"""
+Usage: timeline_cup.py [n|c2] [p] [out.json]"""
 import collections
 import json
 import os
@@ -15,17 +15,23 @@ from torch.profiler import ProfilerActivity, profile  # noqa: E402
 
 import paper_1112_5717_b200 as G  # noqa: E402
 
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
+arg = sys.argv[1] if len(sys.argv) > 1 else "16384"
 p = int(sys.argv[2]) if len(sys.argv) > 2 else 65521
 out = sys.argv[3] if len(sys.argv) > 3 else None
-src = torch.empty((n, n), dtype=torch.int32, device="cuda")
-G.random_matrix_dev(src, n, n, 3, p)
+if arg == "c2":  # config 2: 4096 x 8192, rank 2048, shuffled zero rows
+    from paper_1112_5717_b200 import workloads as WL
+    m, n = 4096, 8192
+    src = WL.c2_dev(m, n, 2048, 2, p)
+else:
+    m = n = int(arg)
+    src = torch.empty((n, n), dtype=torch.int32, device="cuda")
+    G.random_matrix_dev(src, n, n, 3, p)
 work = src.clone()
-G.cup_dev(work, n, n, p)
+G.cup_dev(work, m, n, p)
 work.copy_(src)
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
-    G.cup_dev(work, n, n, p)
+    G.cup_dev(work, m, n, p)
     torch.cuda.synchronize()
 evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
 ks = []
