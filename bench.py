@@ -234,6 +234,22 @@ def reference_arm(args, rank, world):
                          "sample": sample},
         "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if args.workload != "c4":
+        line["config"]["same_config"] = False
+        line["config"]["why_sample"] = ("the reference's single-threaded cup() of the full workload "
+                                        "takes hours (config 3: ~2.7 h per matrix); each host core "
+                                        "factors a bounded sample per step")
+    if args.workload == "c3" and not args.no_batched:
+        per = 4
+        bval, bstep = run_cpu_reference_c4(threads, per, max(1, min(args.steps, 5)), 1,
+                                           WORKLOADS["c4"]["p"], WORKLOADS["c4"]["seed"])
+        bsample = (f"{threads} concurrent processes x {per} reference cup() calls on config-4 "
+                   f"256x256 matrices over GF({WORKLOADS['c4']['p']}) per step")
+        line["batched"] = {"value": bval, "unit": "matrices/s", "ms_per_step": bstep * 1e3,
+                           "cpu_baseline": {"value": bval, "unit": "matrices/s", "cores": threads,
+                                            "kind": "reference", "sample": bsample},
+                           "e2e": {"value": bval, "unit": "matrices/s", "h2d_bytes_per_step": 0,
+                                   "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
 
@@ -332,6 +348,33 @@ def ours(args, rank, world, local_rank):
     value = world * W * args.steps / t_max
     ms_per_step = t_max / args.steps * 1e3
 
+    # parity of the timed result: the body digest (device) and the row profile /
+    # sigma / op counts against the committed CPU digests of this config
+    # (tests/golden/scale_digests.json: reference + blocked restatement)
+    parity = None
+    try:
+        want = json.load(open(os.path.join(ROOT, "tests", "golden", "scale_digests.json"))).get(args.workload)
+        if want is not None:
+            import hashlib
+
+            def sha(x):
+                return hashlib.sha256(np.ascontiguousarray(np.asarray(x, np.uint32)).tobytes()).hexdigest()
+            got = {"rank": r, "rrp_sha256": sha(res.row_profile), "sigma_sha256": sha(res.col_perm),
+                   "ops": [ctr.n_mul, ctr.n_addsub, ctr.n_divinv, ctr.n_ztest],
+                   "body_digest": f"{G.digest_dev(work, m, n):016x}"}
+            parity = {"bit_exact_vs_committed_digest": all(got[k] == want[k] for k in got),
+                      "pinned_by": want.get("by"), "body_digest": got["body_digest"]}
+    except Exception as e:  # pragma: no cover
+        parity = {"error": str(e)}
+
+    # the metric's second half: batched matrices/s (config 4), every rank
+    batched = None
+    if args.workload == "c3" and not args.no_batched:
+        try:
+            batched = batched_record(args, rank, world, dist, max(3, args.steps), max(3, args.warmup))
+        except Exception as e:  # pragma: no cover
+            batched = {"error": str(e)}
+
     if rank != 0:
         if dist is not None:
             dist.barrier()
@@ -355,9 +398,20 @@ def ours(args, rank, world, local_rank):
         "clocks": clk.summary(),
     }
 
+    if parity is not None:
+        line["parity"] = parity
+
     # dominant kernel roofline: root Schur GEMM shape, GEMM kernel alone
     try:
-        peak = measure_int8_peak(torch)
+        cublas = measure_int8_peak(torch)
+        peak, peak_source = cublas, "measured live: cuBLAS int8 dense GEMM 8192^3 (torch._int_mm), burst"
+        try:  # the driver-measured peak: dense int8 = 2 x the measured bf16 rate (same tensor pipe)
+            mp_ = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+            peak = 2.0 * float(mp_["bf16_tflops"])
+            peak_source = ("MEASURED_PEAKS.json: 2 x bf16_tflops (%.1f, burst; int8 dense runs at twice "
+                           "the bf16 rate on B200); live cuBLAS int8 beside it" % float(mp_["bf16_tflops"]))
+        except Exception:
+            pass
         gm = 8192  # the C3 root Schur GEMM shape (same as the committed ncu capture)
         da = torch.empty((gm, gm), dtype=torch.int32, device="cuda")
         db = torch.empty((gm, gm), dtype=torch.int32, device="cuda")
@@ -373,7 +427,8 @@ def ours(args, rank, world, local_rank):
             "achieved": tops, "peak": peak, "unit": "TFLOP/s",
             "unit_note": "int8 tensor TOPS; 1 mod-p MAC = L^2 u8 MACs",
             "frac": tops / peak,
-            "peak_source": "measured live: cuBLAS int8 dense GEMM 8192^3 (torch._int_mm), burst",
+            "peak_source": peak_source,
+            "cublas_int8_live": cublas, "frac_vs_cublas": tops / cublas,
             "shape": [gm, gm, gm], "ms_gemm": ms_gemm, "ms_pack": ms_pack,
             "traffic": _ncu_traffic(),
             "traffic_note": "dram read+write bytes per launch of the same shape from one "
@@ -414,6 +469,29 @@ def ours(args, rank, world, local_rank):
                        "ms_per_step": e2e_t * 1e3, "steps": len(tt),
                        "path": "rl_cup_u32 (host pinned buffers)"}
         del host
+        # the same through PAGEABLE host memory -- what the C++ drop-in receives
+        # from ranklab::Mat's std::vector (matrix.hpp:176): staged through the
+        # library's pinned ring by host threads
+        pg = np.empty((m, n), np.uint32)
+        tp = []
+        for i in range(e2e_steps + 1):
+            np.copyto(pg, src)
+            rk = ctypes.c_int64(0)
+            t0 = time.perf_counter()
+            code = G.lib().rl_cup_u32(ctypes.c_void_p(pg.ctypes.data), m, n, n, p,
+                                      ctypes.byref(rk), ctypes.c_void_p(rrp.ctypes.data),
+                                      ctypes.c_void_p(sig.ctypes.data), None)
+            dt = time.perf_counter() - t0
+            if code != 0:
+                raise RuntimeError(G.lib().rl_last_error().decode())
+            if i > 0:
+                tp.append(dt)
+        pt = sum(tp) / len(tp)
+        line["e2e_pageable"] = {"value": world * W / pt, "unit": "mod-p ops/s", "ms_per_step": pt * 1e3,
+                                "h2d_bytes_per_step": m * n * 4, "d2h_bytes_per_step": m * n * 4,
+                                "steps": len(tp),
+                                "path": "rl_cup_u32 (pageable host buffer, staged through a pinned ring)"}
+        del pg
     except Exception as e:  # pragma: no cover
         line["e2e"] = {"error": str(e)}
 
@@ -433,6 +511,8 @@ def ours(args, rank, world, local_rank):
                           f"single thread, {dt:.1f} s"}
         except Exception as e:  # pragma: no cover
             line["cpu_baseline"] = {"error": str(e)}
+    if batched is not None:
+        line["batched"] = batched
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
@@ -544,17 +624,14 @@ def ours_dist(args, rank, world, local_rank):
         dist.destroy_process_group()
 
 
-def ours_batched(args, rank, world, local_rank):
-    """Config 4: the fixed batch sharded across ranks (contiguous slices)."""
+def batched_record(args, rank, world, dist, steps, warmup):
+    """Config 4 -- the metric's second half ("batched matrices/s"): the fixed
+    batch of 4096 matrices sharded across ranks (contiguous slices, no
+    collective on the data path).  Returns the line (rank 0) or None."""
     import torch
     import paper_1112_5717_b200 as G
     from paper_1112_5717_b200 import workloads as WL
 
-    torch.cuda.set_device(local_rank)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     wl = WORKLOADS["c4"]
     total, m, n, p, seed = wl["batch"], wl["m"], wl["n"], wl["p"], wl["seed"]
     lo, hi = WL.shard_range(total, rank, world)
@@ -562,17 +639,17 @@ def ours_batched(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
     pristine, ranks = WL.c4_dev(total, seed, p, lo, hi)
     work = torch.empty_like(pristine)
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         work.copy_(pristine)
         G.cup_batched_dev(work, cnt, m, n, p, stream=stream, want_meta=False)
     torch.cuda.synchronize()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local_rank) as clk:
-        for i in range(args.steps):
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        for i in range(steps):
             work.copy_(pristine)
             starts[i].record(stream)
             G.cup_batched_dev(work, cnt, m, n, p, stream=stream, want_meta=False)
@@ -582,35 +659,43 @@ def ours_batched(args, rank, world, local_rank):
         dist.barrier()
     elapsed = sum(s_.elapsed_time(e) for s_, e in zip(starts, ends)) / 1e3
     t_local = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
-    # verification: every shard's ranks equal the recipe's r_t (rank = r w.h.p.)
+    # verification: ranks equal the recipe's r_t and every body digest equals the
+    # reference's (tests/golden/scale_digests.json, pinned by tools/pin_scale_digests.py)
     work.copy_(pristine)
     rk, _, _ = G.cup_batched_dev(work, cnt, m, n, p, stream=stream)
     ok = torch.tensor([int(sum(int(a) == b for a, b in zip(rk, ranks)))], dtype=torch.float64,
                       device="cuda")
+    dig_ok = -1
+    try:
+        want = json.load(open(os.path.join(ROOT, "tests", "golden", "scale_digests.json")))["c4"]
+        dig_ok = int(all(f"{G.digest_dev(work[t], m, n):016x}" == want["body_digests"][lo + t]
+                         for t in range(cnt)))
+    except Exception:
+        pass
+    dig = torch.tensor([dig_ok], dtype=torch.float64, device="cuda")
     ops = torch.tensor([sum(model_ops(m, n, int(x)) for x in rk)], dtype=torch.float64,
                        device="cuda")
     if dist is not None:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
         dist.all_reduce(ok, op=dist.ReduceOp.SUM)
+        dist.all_reduce(dig, op=dist.ReduceOp.MIN)
         dist.all_reduce(ops, op=dist.ReduceOp.SUM)
     t_max = float(t_local.item())
     if rank != 0:
-        if dist is not None:
-            dist.barrier()
-            dist.destroy_process_group()
-        return
-    value = total * args.steps / t_max
+        return None
+    value = total * steps / t_max
     line = {
         "metric": METRIC, "value": value, "unit": "matrices/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3,
+        "steps": steps, "warmup": warmup, "ms_per_step": t_max / steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": f"u32 in GF({p}); u64 products, Barrett reduction", "data": "synthetic",
         "config": {"workload": "c4", "desc": wl["desc"], "batch": total, "m": m, "n": n, "p": p,
                    "seed": seed, "parallelism": f"batch sharded {world} ways" if world > 1 else "single",
                    "ranks_match_recipe": int(ok.item()),
-                   "modp_ops_per_s": float(ops.item()) * args.steps / t_max,
+                   "bodies_match_reference_digests": bool(dig.item() == 1) if dig.item() >= 0 else None,
+                   "modp_ops_per_s": float(ops.item()) * steps / t_max,
                    "l2": "256 MB batch > 126 MB L2; batch restored between steps"},
-        "gpu_launches": args.steps,
+        "gpu_launches": steps,
         "clocks": clk.summary(),
     }
     # e2e: host buffers in, factor, bodies + ranks out (this rank's shard), through
@@ -652,7 +737,21 @@ def ours_batched(args, rank, world, local_rank):
                                               f"single thread, {t_sum:.2f} s"}
         except Exception as e:  # pragma: no cover
             line["cpu_baseline"] = {"error": str(e)}
-    print(json.dumps(line), flush=True)
+    return line
+
+
+def ours_batched(args, rank, world, local_rank):
+    """Config 4 alone (--workload c4)."""
+    import torch
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    line = batched_record(args, rank, world, dist, args.steps, args.warmup)
+    if line is not None:
+        print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
@@ -667,6 +766,8 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c3")
     ap.add_argument("--cpu-sample", type=int, default=2048)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-batched", action="store_true",
+                    help="c3: skip the config-4 'batched matrices/s' sub-record")
     ap.add_argument("--dist", action="store_true",
                     help="single-matrix workloads: the distributed column-tile driver even at N=1")
     args = ap.parse_args()

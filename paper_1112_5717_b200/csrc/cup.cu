@@ -41,7 +41,8 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
     const size_t o_ipiv = o_rrp + up(sizeof(i32) * (k + 1));
     const size_t o_ps = o_ipiv + up(sizeof(i32) * (k + 1));
     const size_t o_uinv = o_ps + up(sizeof(PanelScratch));
-    const size_t o_tab = o_uinv + up(sizeof(u32) * PB * PB * (leaf_of_.size() + 1));
+    const size_t o_flags = o_uinv + up(sizeof(u32) * PB * PB * (leaf_of_.size() + 1));
+    const size_t o_tab = o_flags + up(sizeof(i32) * (leaf_of_.size() + 1));
     const size_t o_ninv = o_tab + up(p_ <= 65536u ? 65536 * sizeof(uint16_t) : 0);
     const size_t total = o_ninv + sizeof(u32) * NINV_LD * NINV_LD * ninv_slot_.size();
     RL_CUDA_CHECK(cudaMalloc(&meta_, total));
@@ -52,6 +53,10 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
     ps_ = reinterpret_cast<PanelScratch*>(base + o_ps);
     RL_CUDA_CHECK(cudaMemset(ps_, 0, sizeof(PanelScratch)));
     uinv_ = reinterpret_cast<u32*>(base + o_uinv);
+    swapflags_ = reinterpret_cast<i32*>(base + o_flags);
+    RL_CUDA_CHECK(cudaMemset(swapflags_, 0, sizeof(i32) * (leaf_of_.size() + 1)));
+    leaf_starts_.assign(leaf_of_.size(), 0);
+    for (const auto& kv : leaf_of_) leaf_starts_[kv.second] = kv.first;
     ninv_ = ninv_slot_.empty() ? nullptr : reinterpret_cast<u32*>(base + o_ninv);
     if (p_ <= 65536u) {
         inv_table_ = reinterpret_cast<uint16_t*>(base + o_tab);
@@ -75,6 +80,13 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
         if (l.a2_cap) RL_CUDA_CHECK(cudaMalloc(&l.a2, l.a2_cap));
         if (l.b2_cap) RL_CUDA_CHECK(cudaMalloc(&l.b2, l.b2_cap));
     }
+    if (!big_slot_.empty()) {
+        RL_CUDA_CHECK(cudaMalloc(&big_, sizeof(u32) * BIG_LD * BIG_LD * big_slot_.size()));
+        RL_CUDA_CHECK(cudaMalloc(&big_tmp_, sizeof(u32) * (4 * NINV_LD * NINV_LD + 4 * CH_LD * CH_LD)));
+        RL_CUDA_CHECK(cudaStreamCreateWithPriority(&inv_lane_.st, cudaStreamNonBlocking, prio_lo));
+        if (inv_lane_.a2_cap) RL_CUDA_CHECK(cudaMalloc(&inv_lane_.a2, inv_lane_.a2_cap));
+        if (inv_lane_.b2_cap) RL_CUDA_CHECK(cudaMalloc(&inv_lane_.b2, inv_lane_.b2_cap));
+    }
 }
 
 CupEngine::~CupEngine() {
@@ -93,6 +105,11 @@ CupEngine::~CupEngine() {
         cudaFree(kv.second.a2);
         cudaFree(kv.second.b2);
     }
+    if (inv_lane_.st) cudaStreamDestroy(inv_lane_.st);
+    cudaFree(inv_lane_.a2);
+    cudaFree(inv_lane_.b2);
+    cudaFree(big_);
+    cudaFree(big_tmp_);
 }
 
 cudaEvent_t CupEngine::fork_to(cudaStream_t from, cudaStream_t to) {
@@ -174,6 +191,7 @@ void CupEngine::panel(i32 i0, i32 b) {
     flush_swaps();
     PanelArgs a{};
     a.uinv = uinv_ + (size_t)leaf_of_.at(i0) * PB * PB;
+    a.swapflag = swapflags_ + leaf_of_.at(i0);
     a.inv_table = inv_table_;
     a.A = A_;
     a.lda = lda_;
@@ -202,7 +220,13 @@ void CupEngine::panel(i32 i0, i32 b) {
     stats_.launches += 3;
 }
 
-void CupEngine::swaps_range(i32 row0, i32 M, Dyn j_lo, Dyn j_hi) {
+void CupEngine::leaf_range(i32 piv_lo, i32 piv_hi, SwapArgs& a) const {
+    a.leafflags = swapflags_;
+    a.leaf_lo = (i32)(std::lower_bound(leaf_starts_.begin(), leaf_starts_.end(), piv_lo) - leaf_starts_.begin());
+    a.leaf_hi = (i32)(std::lower_bound(leaf_starts_.begin(), leaf_starts_.end(), piv_hi) - leaf_starts_.begin());
+}
+
+void CupEngine::swaps_range(i32 row0, i32 M, Dyn j_lo, Dyn j_hi, i32 piv_lo, i32 piv_hi) {
     if (dry_ || M <= 0) return;
     SwapArgs a{};
     a.A = A_;
@@ -215,10 +239,11 @@ void CupEngine::swaps_range(i32 row0, i32 M, Dyn j_lo, Dyn j_hi) {
     a.rp = rp_;
     a.ipiv = ipiv_;
     a.Mmax = M;
+    leaf_range(piv_lo, piv_hi, a);
     queue_swaps(a);
 }
 
-void CupEngine::swaps_gather(Dyn g_lo, Dyn g_hi, i32 Mmax, Dyn j_lo, Dyn j_hi) {
+void CupEngine::swaps_gather(Dyn g_lo, Dyn g_hi, i32 Mmax, Dyn j_lo, Dyn j_hi, i32 piv_lo, i32 piv_hi) {
     if (dry_ || Mmax <= 0) return;
     SwapArgs a{};
     a.A = A_;
@@ -231,6 +256,7 @@ void CupEngine::swaps_gather(Dyn g_lo, Dyn g_hi, i32 Mmax, Dyn j_lo, Dyn j_hi) {
     a.rp = rp_;
     a.ipiv = ipiv_;
     a.Mmax = Mmax;
+    leaf_range(piv_lo, piv_hi, a);
     queue_swaps(a);
 }
 
@@ -261,13 +287,13 @@ static void collect_leaves(i32 x0, i32 mx, std::vector<std::pair<i32, i32>>& out
 
 // G <- G * U_X^{-1} as one GEMM against the stored node inverse (in place: the
 // pack kernel snapshots G before the GEMM overwrites it, beta = 0).
-void CupEngine::gemm_ninv(i32 r0, i32 M, i32 x0, i32 mx, const u32* ninv) {
+void CupEngine::gemm_ninv(i32 r0, i32 M, i32 x0, i32 mx, const u32* ninv, i32 ldn) {
     GemmArgs g{};
     g.A = A_;
     g.lda = lda_;
     g.a_row0 = r0;
     g.B = ninv;
-    g.ldb = NINV_LD;
+    g.ldb = ldn;
     g.gather = nullptr;
     g.b_from0 = 1;
     g.C = A_;
@@ -291,6 +317,27 @@ void CupEngine::gemm_ninv(i32 r0, i32 M, i32 x0, i32 mx, const u32* ninv) {
 }
 
 void CupEngine::trsm_right(i32 r0, i32 M, i32 x0, i32 mx) {
+    // a tall TRSM against a node with a big inverse: one GEMM (the inverse is
+    // unique, so the bytes are the reference recursion's)
+    if (big_on_ && use_tc_ && M >= kBigMinRows) {
+        const auto key = std::make_pair(x0, mx);
+        if (big_slot_.count(key)) {
+            if (dry_) {
+                size_t& ac = lane_ ? lane_->a2_cap : a2_cap_;
+                size_t& bc = lane_ ? lane_->b2_cap : b2_cap_;
+                ac = std::max(ac, tc_a2_bytes(L_, M, mx));
+                bc = std::max(bc, tc_b2_bytes(L_, mx, mx));
+                return;
+            }
+            auto it = big_ready_.find(key);
+            if (it != big_ready_.end()) {
+                flush_swaps();
+                RL_CUDA_CHECK(cudaStreamWaitEvent(work_stream(), it->second, 0));
+                gemm_ninv(r0, M, x0, mx, big_ + (size_t)big_slot_.at(key) * BIG_LD * BIG_LD, BIG_LD);
+                return;
+            }
+        }
+    }
     if (fused_trsm_ && mx <= TN_MAXLEAF * PB) {  // <= 4 leaves: one fused kernel
         const auto key = std::make_pair(x0, mx);
         const bool gemm_ok = use_tc_ && M >= kNinvGemmMinRows && mx >= 2 * PB;
@@ -386,7 +433,7 @@ void CupEngine::node(i32 i0, i32 mm) {
         }
     }
     const i32 b0 = i0 + k, bm = mm - k;
-    swaps_range(b0, bm, dyn_rp(i0), dyn_rp(b0));                     // factor.cpp:42
+    swaps_range(b0, bm, dyn_rp(i0), dyn_rp(b0), i0, b0);             // factor.cpp:42
     if (!dry_ && uinv_join_) {
         RL_CUDA_CHECK(cudaStreamWaitEvent(s_, uinv_join_, 0));
         uinv_join_ = nullptr;
@@ -433,7 +480,116 @@ void CupEngine::node(i32 i0, i32 mm) {
         }
     }
     node(b0, bm);                                                     // factor.cpp:53
-    swaps_gather(dyn_rp(i0), dyn_rp(b0), k, dyn_rp(b0), dyn_rp(i0 + mm));  // factor.cpp:56
+    swaps_gather(dyn_rp(i0), dyn_rp(b0), k, dyn_rp(b0), dyn_rp(i0 + mm), b0, i0 + mm);  // factor.cpp:56
+    if (big_on_ && use_tc_ && mm > 8 * PB && mm <= BIG_LD && m_ >= 2 * kBigMinRows) build_big_inverse(i0, mm);
+}
+
+// C <- alpha * A * B (beta = 0) on dense / gathered operands, on stream st
+// with the inverse lane's workspace.
+void CupEngine::gemm_dense(const u32* A, i64 lda, bool a_dense, const u32* B, i64 ldb, bool b_dense,
+                           const i32* gather, u32* C, i64 ldc, i32 M, Dyn k_lo, Dyn k_hi, Dyn n_lo, Dyn n_hi,
+                           i64 Kmax, i64 Nmax, u32 alpha, cudaStream_t st) {
+    if (dry_) {
+        inv_lane_.a2_cap = std::max(inv_lane_.a2_cap, tc_a2_bytes(L_, M, Kmax));
+        inv_lane_.b2_cap = std::max(inv_lane_.b2_cap, tc_b2_bytes(L_, Nmax, Kmax));
+        return;
+    }
+    GemmArgs g{};
+    g.A = A;
+    g.lda = lda;
+    g.a_from0 = a_dense ? 1 : 0;
+    g.B = B;
+    g.ldb = ldb;
+    g.b_from0 = b_dense ? 1 : 0;
+    g.gather = gather;
+    g.C = C;
+    g.ldc = ldc;
+    g.c_from0 = 1;
+    g.M = M;
+    g.k_lo = k_lo;
+    g.k_hi = k_hi;
+    g.n_lo = n_lo;
+    g.n_hi = n_hi;
+    g.rp = rp_;
+    g.alpha = alpha;
+    g.beta = 0;
+    g.f = f_;
+    ++stats_.gemms;
+    ++stats_.tc_gemms;
+    stats_.launches += 2;
+    gemm_tc(g, L_, Kmax, Nmax, inv_lane_.a2, inv_lane_.b2, st);
+}
+
+// X = U^{-1} of the node [a | b] from Xa, Xb:  X = [[Xa, -Xa U_ab Xb], [0, Xb]],
+// U_ab = the U rows of a's pivots (gathered through rrp) at b's pivot columns.
+void CupEngine::combine_inverse(const u32* Xa, i32 la, i32 xa, i32 ma, const u32* Xb, i32 lb, i32 xb, i32 mb,
+                                u32* X, i32 ldx, cudaStream_t st) {
+    u32* T1 = big_tmp_ ? big_tmp_ + 4 * NINV_LD * NINV_LD + 2 * CH_LD * CH_LD : nullptr;
+    u32* T2 = T1 ? T1 + CH_LD * CH_LD : nullptr;
+    gemm_dense(Xa, la, true, A_, lda_, false, rrp_, T1, CH_LD, ma, dyn_rp(xa), dyn_rp(xb), dyn_rp(xb),
+               dyn_rp(xb + mb), ma, mb, 1 % p_, st);
+    gemm_dense(T1, CH_LD, true, Xb, lb, true, nullptr, T2, CH_LD, ma, dyn_rp(xb), dyn_rp(xb + mb), dyn_rp(xb),
+               dyn_rp(xb + mb), mb, mb, p_ - 1, st);
+    if (!dry_) {
+        ninv_assemble(X, ldx, Xa, la, Xb, lb, T2, CH_LD, dyn_rp(xa), dyn_rp(xb), dyn_rp(xb + mb), rp_, ma + mb, st);
+        stats_.launches += 1;
+    }
+}
+
+void CupEngine::build_big_inverse(i32 x0, i32 mm) {
+    const auto key = std::make_pair(x0, mm);
+    if (dry_) {
+        if (!big_slot_.count(key)) big_slot_.emplace(key, (i32)big_slot_.size());
+        events_needed_ += 2;
+    } else {
+        fork_to(s_, inv_lane_.st);  // the node's U rows are final (its swaps flushed)
+        // ... and its last leaf's U^{-1} (still on s3_; s_ joins it later)
+        if (uinv_join_) RL_CUDA_CHECK(cudaStreamWaitEvent(inv_lane_.st, uinv_join_, 0));
+    }
+    cudaStream_t st = inv_lane_.st;
+    const i32 k = mm / 2;
+    const i32 cx[2] = {x0, x0 + k}, cm[2] = {k, mm - k};
+    u32* child[2] = {nullptr, nullptr};
+    for (int c = 0; c < 2; ++c) {
+        // the child's two halves (<= 4 leaves each): inverses by the fused
+        // node solve with no rows (a private copy: the critical path may be
+        // writing the shared slot of the same node at the same time)
+        const i32 h = cm[c] / 2;
+        const i32 gx[2] = {cx[c], cx[c] + h}, gm[2] = {h, cm[c] - h};
+        u32* gi[2];
+        for (int q = 0; q < 2; ++q) {
+            gi[q] = big_tmp_ ? big_tmp_ + (size_t)(2 * c + q) * NINV_LD * NINV_LD : nullptr;
+            if (dry_) continue;
+            std::vector<std::pair<i32, i32>> lv;
+            collect_leaves(gx[q], gm[q], lv);
+            TrsmNodeArgs a{};
+            a.A = A_;
+            a.lda = lda_;
+            a.row0 = 0;
+            a.M = 0;
+            a.nleaf = (int)lv.size();
+            for (int l = 0; l < a.nleaf; ++l) {
+                a.j_lo[l] = dyn_rp(lv[l].first);
+                a.j_hi[l] = dyn_rp(lv[l].first + lv[l].second);
+                a.uinv[l] = uinv_ + (size_t)leaf_of_.at(lv[l].first) * PB * PB;
+            }
+            a.rp = rp_;
+            a.rrp = rrp_;
+            a.f = f_;
+            a.ninv = gi[q];
+            trsm_node(a, st);
+            stats_.launches += 1;
+        }
+        child[c] = big_tmp_ ? big_tmp_ + 4 * NINV_LD * NINV_LD + (size_t)c * CH_LD * CH_LD : nullptr;
+        combine_inverse(gi[0], NINV_LD, gx[0], gm[0], gi[1], NINV_LD, gx[1], gm[1], child[c], CH_LD, st);
+    }
+    u32* X = (big_ && !dry_) ? big_ + (size_t)big_slot_.at(key) * BIG_LD * BIG_LD : nullptr;
+    combine_inverse(child[0], CH_LD, cx[0], cm[0], child[1], CH_LD, cx[1], cm[1], X, BIG_LD, st);
+    if (!dry_) {
+        cudaEvent_t e = events_.at(next_event_++);
+        RL_CUDA_CHECK(cudaEventRecord(e, st));
+        big_ready_[key] = e;
+    }
 }
 
 void CupEngine::enqueue(u32* dA, cudaStream_t s) {
@@ -446,6 +602,7 @@ void CupEngine::enqueue(u32* dA, cudaStream_t s) {
     pending_joins_.clear();
     uinv_join_ = nullptr;
     row_joins_.clear();
+    big_ready_.clear();
     lane_ = nullptr;
     fill_rp0(rp_, s);
     if (m_ > 0 && n_ > 0) {
@@ -454,6 +611,7 @@ void CupEngine::enqueue(u32* dA, cudaStream_t s) {
         pending_joins_.clear();
         if (m_ > PB && split_max_k_ >= PB) fork_to(s2_, s_);  // s2_ joined the capture at a split
         fork_to(s3_, s_);
+        if (!big_ready_.empty()) fork_to(inv_lane_.st, s_);  // the last builds rejoin the capture
         flush_swaps();
         compact_u_rows(A_, lda_, m_, n_, rp_, rrp_, s);
         stats_.launches += 1;

@@ -56,12 +56,22 @@ private:
     void node(i32 i0, i32 m);
     void panel(i32 i0, i32 b);
     void trsm_right(i32 r0, i32 M, i32 x0, i32 mx);
-    void gemm_ninv(i32 r0, i32 M, i32 x0, i32 mx, const u32* ninv);
+    void gemm_ninv(i32 r0, i32 M, i32 x0, i32 mx, const u32* ninv, i32 ldn = NINV_LD);
+    // big node inverses (nodes of (8, 16] leaves): built on a side lane right
+    // after the node is factored, used by the tall TRSMs of the levels above
+    void build_big_inverse(i32 x0, i32 mm);
+    void combine_inverse(const u32* Xa, i32 la, i32 xa, i32 ma, const u32* Xb, i32 lb, i32 xb, i32 mb, u32* X,
+                         i32 ldx, cudaStream_t st);
+    void gemm_dense(const u32* A, i64 lda, bool a_dense, const u32* B, i64 ldb, bool b_dense, const i32* gather,
+                    u32* C, i64 ldc, i32 M, Dyn k_lo, Dyn k_hi, Dyn n_lo, Dyn n_hi, i64 Kmax, i64 Nmax, u32 alpha,
+                    cudaStream_t st);
     void gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nmax, cudaStream_t st = nullptr,
               i32 n_cap = 0);
     cudaEvent_t fork_to(cudaStream_t from, cudaStream_t to);  // `to` waits for `from`'s work so far
-    void swaps_range(i32 row0, i32 M, Dyn j_lo, Dyn j_hi);
-    void swaps_gather(Dyn g_lo, Dyn g_hi, i32 Mmax, Dyn j_lo, Dyn j_hi);
+    // the transpositions are the pivots of rows [piv_lo, piv_hi) (whole leaves)
+    void swaps_range(i32 row0, i32 M, Dyn j_lo, Dyn j_hi, i32 piv_lo, i32 piv_hi);
+    void swaps_gather(Dyn g_lo, Dyn g_hi, i32 Mmax, Dyn j_lo, Dyn j_hi, i32 piv_lo, i32 piv_hi);
+    void leaf_range(i32 piv_lo, i32 piv_hi, SwapArgs& a) const;
     void queue_swaps(const SwapArgs& a);
     void flush_swaps();
 
@@ -99,6 +109,8 @@ private:
     u32* uinv_ = nullptr;                      // one PB x PB block per leaf
     uint16_t* inv_table_ = nullptr;            // p < 2^16: x -> x^{-1} mod p
     std::unordered_map<i32, i32> leaf_of_;     // leaf start row -> leaf index
+    std::vector<i32> leaf_starts_;             // leaf start rows, increasing (index order)
+    i32* swapflags_ = nullptr;                 // per leaf: made a transposition
     // node inverses U_X^{-1} of <= 4-leaf skeleton nodes X = (x0, mx): computed by
     // the first TRSM against X (as a by-product of its sweep), then reused by the
     // taller TRSMs above as one tensor-core GEMM each
@@ -136,6 +148,21 @@ private:
     Lane* lane_ = nullptr;                       // non-null while enqueueing side work
     std::map<std::pair<i32, i32>, cudaEvent_t> row_joins_;  // child node -> side work done
     cudaStream_t work_stream() const { return lane_ ? lane_->st : s_; }
+#ifndef RL_BIG_INV
+#define RL_BIG_INV 1
+#endif
+    static constexpr i32 BIG_LD = 16 * PB;         // 1024: pitch of a big node inverse
+    static constexpr i32 CH_LD = 8 * PB;           // 512: a child's inverse / the T blocks
+#ifndef RL_BIG_MIN_ROWS
+#define RL_BIG_MIN_ROWS 2048
+#endif
+    static constexpr i32 kBigMinRows = RL_BIG_MIN_ROWS;  // TRSMs at least this tall use them
+    bool big_on_ = RL_BIG_INV != 0;
+    std::map<std::pair<i32, i32>, i32> big_slot_;          // node -> slot (dry run)
+    std::map<std::pair<i32, i32>, cudaEvent_t> big_ready_; // node -> built (one enqueue)
+    u32* big_ = nullptr;                                   // BIG_LD x BIG_LD per slot
+    u32* big_tmp_ = nullptr;                               // 4 x 256^2 + 4 x 512^2 scratch
+    Lane inv_lane_;                                        // stream + GEMM workspace of the builds
     cudaGraphExec_t graph_exec_ = nullptr;
     u32* graph_A_ = nullptr;
     cudaEvent_t done_ = nullptr;  // end of the last run: the destructor waits for it

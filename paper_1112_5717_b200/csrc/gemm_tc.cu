@@ -82,6 +82,9 @@ template <int L>
 __device__ __forceinline__ void pack_a_body(const GemmArgs& g, uint8_t* __restrict__ a2, int bid, int nb) {
     i32 K, N, k_lo, n_lo;
     dyn_shape(g, K, N, k_lo, n_lo);
+    const i32 acol0 = g.a_from0 ? 0 : k_lo, ccol0 = g.c_from0 ? 0 : n_lo;
+    (void)acol0;
+    (void)ccol0;
     if (K <= 0 || N <= 0) return;
     const i32 KB = (K + BK - 1) / BK;
     const i32 MB = (g.M + BM - 1) / BM;
@@ -97,7 +100,7 @@ __device__ __forceinline__ void pack_a_body(const GemmArgs& g, uint8_t* __restri
         const i32 row = mb * BM + r;
         const i32 k0 = kb * BK + c * 16;
         if (idx < total && row < g.M) {
-            const u32* src = g.A + (i64)(g.a_row0 + row) * g.lda + k_lo + k0;
+            const u32* src = g.A + (i64)(g.a_row0 + row) * g.lda + acol0 + k0;
             if (((reinterpret_cast<uintptr_t>(src) & 15) == 0) && k0 + 16 <= K) {
                 const uint4* s4 = reinterpret_cast<const uint4*>(src);
 #pragma unroll
@@ -163,6 +166,9 @@ __device__ __forceinline__ void pack_b_body(const GemmArgs& g, uint8_t* __restri
     __shared__ i32 s_rowoff[KQ];
     i32 K, N, k_lo, n_lo;
     dyn_shape(g, K, N, k_lo, n_lo);
+    const i32 acol0 = g.a_from0 ? 0 : k_lo, ccol0 = g.c_from0 ? 0 : n_lo;
+    (void)acol0;
+    (void)ccol0;
     if (K <= 0 || N <= 0) return;
     const i32 KB = (K + BK - 1) / BK;
     const i32 NB = (N + NT - 1) / NT;
@@ -283,6 +289,9 @@ __global__ void __launch_bounds__(NTHR, 1)
 
     i32 K, N, k_lo, n_lo;
     dyn_shape(g, K, N, k_lo, n_lo);
+    const i32 acol0 = g.a_from0 ? 0 : k_lo, ccol0 = g.c_from0 ? 0 : n_lo;
+    (void)acol0;
+    (void)ccol0;
     if (K <= 0 || N <= 0 || g.M <= 0) return;  // uniform; beta==1 callers only (see gemm_tc)
     const i32 KB = (K + BK - 1) / BK;
     const i32 KT = L * KB;
@@ -395,8 +404,8 @@ __global__ void __launch_bounds__(NTHR, 1)
             tile_coords(tile, MB, NB, mb, nb);
             const i32 row = mb * BM + rloc;
             const bool vrow = row < g.M;
-            u32* cbase = g.C + (i64)(g.c_row0 + mb * BM + q * 32) * g.ldc + n_lo + nb * NT;
-            u32* crow = g.C + (i64)(g.c_row0 + (vrow ? row : 0)) * g.ldc + n_lo + nb * NT;
+            u32* cbase = g.C + (i64)(g.c_row0 + mb * BM + q * 32) * g.ldc + ccol0 + nb * NT;
+            u32* crow = g.C + (i64)(g.c_row0 + (vrow ? row : 0)) * g.ldc + ccol0 + nb * NT;
             // coalesced path: 16-byte aligned rows (the usual case: column origins
             // are multiples of the leaf size and ldc of 4)
             const bool vec = ld_ok && ((reinterpret_cast<uintptr_t>(cbase) & 15) == 0);
@@ -602,6 +611,9 @@ __global__ void __launch_bounds__(256) gemm_imma_kernel(GemmArgs g) {
     pdl_trigger();
     i32 K, N, k_lo, n_lo;
     dyn_shape(g, K, N, k_lo, n_lo);
+    const i32 acol0 = g.a_from0 ? 0 : k_lo, ccol0 = g.c_from0 ? 0 : n_lo;
+    (void)acol0;
+    (void)ccol0;
     if (K <= 0 || N <= 0 || g.M <= 0) return;
     const i32 MB = (g.M + TM - 1) / TM, NB = (N + 63) / 64;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tg = lane & 3;
@@ -609,7 +621,7 @@ __global__ void __launch_bounds__(256) gemm_imma_kernel(GemmArgs g) {
     const int cbw = TM == 64 ? 32 * (warp >> 2) : 8 * warp;
     const Fp f = g.f;
     const i32 bcol0 = g.b_from0 ? 0 : n_lo;
-    const bool avec = ((g.lda & 3) == 0) && (((reinterpret_cast<uintptr_t>(g.A) >> 2) + g.a_row0 * g.lda + k_lo) % 4 == 0);
+    const bool avec = ((g.lda & 3) == 0) && (((reinterpret_cast<uintptr_t>(g.A) >> 2) + g.a_row0 * g.lda + acol0) % 4 == 0);
     const bool bvec = ((g.ldb & 3) == 0) && (((reinterpret_cast<uintptr_t>(g.B) >> 2) + bcol0) % 4 == 0);
     auto lo4 = [](uint4 v) {
         return (v.x & 0xff) | (v.y & 0xff) << 8 | (v.z & 0xff) << 16 | (v.w & 0xff) << 24;
@@ -635,7 +647,7 @@ __global__ void __launch_bounds__(256) gemm_imma_kernel(GemmArgs g) {
                 const int r = e >> 2, kq = (e & 3) * 16;
                 const i32 row = mb * TM + r;
                 uint4 v[4];
-                const u32* src = g.A + (i64)(g.a_row0 + row) * g.lda + k_lo + k0 + kq;
+                const u32* src = g.A + (i64)(g.a_row0 + row) * g.lda + acol0 + k0 + kq;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int kk = k0 + kq + 4 * q;
@@ -724,7 +736,7 @@ __global__ void __launch_bounds__(256) gemm_imma_kernel(GemmArgs g) {
                 const i32 row = mb * TM + 16 * rs + gq + 8 * (e >> 1);
                 const i32 n = nb * 64 + cbw + 8 * t + 2 * tg + (e & 1);
                 if (row >= g.M || n >= N) continue;
-                u32* cp = g.C + (i64)(g.c_row0 + row) * g.ldc + n_lo + n;
+                u32* cp = g.C + (i64)(g.c_row0 + row) * g.ldc + ccol0 + n;
                 const u32 r = red64(acc[t][e], f);
                 const u32 cv = g.beta == 0 ? 0u : (g.beta == 1 ? *cp : mulmod(*cp, g.beta, f));
                 u32 out;
@@ -752,12 +764,15 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
     __shared__ i32 s_brow[SK];
     i32 K, N, k_lo, n_lo;
     dyn_shape(g, K, N, k_lo, n_lo);
+    const i32 acol0 = g.a_from0 ? 0 : k_lo, ccol0 = g.c_from0 ? 0 : n_lo;
+    (void)acol0;
+    (void)ccol0;
     if (K <= 0 || N <= 0 || g.M <= 0) return;
     const i32 MB = (g.M + TM - 1) / TM, NB = (N + 63) / 64;
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const Fp f = g.f;
     const i32 bcol0 = g.b_from0 ? 0 : n_lo;
-    const bool avec = ((g.lda & 3) == 0) && (((reinterpret_cast<uintptr_t>(g.A) >> 2) + g.a_row0 * g.lda + k_lo) % 4 == 0);
+    const bool avec = ((g.lda & 3) == 0) && (((reinterpret_cast<uintptr_t>(g.A) >> 2) + g.a_row0 * g.lda + acol0) % 4 == 0);
     const bool bvec = ((g.ldb & 3) == 0) && (((reinterpret_cast<uintptr_t>(g.B) >> 2) + bcol0) % 4 == 0);
     for (i32 tile = blockIdx.x; tile < MB * NB; tile += gridDim.x) {
         const i32 mb = tile % MB, nb = tile / MB;
@@ -777,7 +792,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
                     const int r = e >> 4, kk = (e & 15) * 4;
                     const i32 row = mb * TM + r;
                     const int bytes = row < g.M ? 4 * max(0, min(4, K - k0 - kk)) : 0;
-                    cp_async16z(&As[r][kk], bytes ? g.A + (i64)(g.a_row0 + row) * g.lda + k_lo + k0 + kk : g.A,
+                    cp_async16z(&As[r][kk], bytes ? g.A + (i64)(g.a_row0 + row) * g.lda + acol0 + k0 + kk : g.A,
                                 bytes);
                 }
             } else {
@@ -785,7 +800,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
                     const int r = e / SK, kk = e % SK;
                     const i32 row = mb * TM + r, k = k0 + kk;
                     const bool ok = row < g.M && k < K;
-                    cp_async4(&As[r][kk], ok ? g.A + (i64)(g.a_row0 + row) * g.lda + k_lo + k : g.A, ok);
+                    cp_async4(&As[r][kk], ok ? g.A + (i64)(g.a_row0 + row) * g.lda + acol0 + k : g.A, ok);
                 }
             }
             __syncthreads();  // s_brow
@@ -831,7 +846,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs g) {
         for (int a = 0; a < RT; ++a) {
             const i32 row = mb * TM + ty + 16 * a;
             if (row >= g.M) continue;
-            u32* crow = g.C + (i64)(g.c_row0 + row) * g.ldc + n_lo;
+            u32* crow = g.C + (i64)(g.c_row0 + row) * g.ldc + ccol0;
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
                 const i32 n = nb * 64 + tx * 4 + b;

@@ -32,6 +32,8 @@ struct GemmArgs {
     u32 alpha, beta;
     Fp f;
     int b_from0;   // B(k, n) = B[k * ldb + n]: a dense K x N operand (no k_lo/n_lo offsets)
+    int a_from0;   // A(r, k) = A[(a_row0 + r) * lda + k]: a dense operand (no k_lo offset)
+    int c_from0;   // C(r, n) = C[(c_row0 + r) * ldc + n]: a dense result (no n_lo offset)
     i32 n_cap;     // > 0: the column range ends at min(n_hi, n_cap)
     i32 max_ctas;  // > 0: grid bound (leave SMs free for a concurrent kernel)
 };
@@ -94,6 +96,7 @@ struct PanelArgs {
     PanelScratch* ps;
     u32* uinv;     // PB x PB: inverse of this leaf's unit upper pivot block
     const uint16_t* inv_table;  // p < 2^16: inv_table[x] = x^{-1} mod p (else unused)
+    i32* swapflag;  // this leaf's "made a transposition" flag (read by the swap jobs)
     Fp f;
     // tail only: the launch has no cross-stream join, so its programmatic
     // predecessor (the window) is the only kernel that may still run when its
@@ -141,7 +144,14 @@ struct TrsmNodeArgs {
     u32* ninv;     // optional: also solve I * U_X^{-1} into ninv (NINV_LD x NINV_LD)
 };
 constexpr int NINV_LD = TN_MAXLEAF * PB;   // 256: pitch of a node inverse
+// (M = 0 with ninv set: only the node inverse)
 void trsm_node(const TrsmNodeArgs& a, cudaStream_t s);
+
+// Inverse of a unit upper block from its two diagonal halves (pivots
+// [a_lo, b_lo) and [b_lo, b_hi), Dyn over rp):  X = [[Xa, T2], [0, Xb]] with
+// T2 = -Xa * U_ab * Xb precomputed; every pitch static, nmax >= the live size.
+void ninv_assemble(u32* X, i32 ldx, const u32* Xa, i32 la, const u32* Xb, i32 lb, const u32* T2, i32 lt,
+                   Dyn a_lo, Dyn b_lo, Dyn b_hi, const i32* rp, i32 nmax, cudaStream_t s);
 
 // ---------------------------------------------------------------- permutation
 // Apply the transpositions T_{j, ipiv[j]} for j in [j_lo, j_hi) in increasing j
@@ -157,6 +167,11 @@ struct SwapArgs {
     const i32* rp;
     const i32* ipiv;
     i32 Mmax;
+    // the job's transpositions are the pivots of leaves [leaf_lo, leaf_hi): when
+    // none of their flags is set (generic inputs) the job is skipped without
+    // scanning ipiv
+    const i32* leafflags;
+    i32 leaf_lo, leaf_hi;
 };
 constexpr int MAX_SWAP_JOBS = 8;
 struct SwapJobs {

@@ -191,6 +191,7 @@ __device__ void panel_fallback(const PanelArgs& a, u32* red_buf) {
             s_pinv = invmod(ri[pc], f);
             a.rrp[pc] = a.i0 + i;
             a.ipiv[pc] = c;
+            if (c != pc) *a.swapflag = 1;
             a.rp[a.i0 + 1 + i] = pc + 1;
         }
         __syncthreads();

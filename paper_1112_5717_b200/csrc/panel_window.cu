@@ -521,6 +521,7 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
     if (W <= 0) {  // rank already n: the rows keep their C data (factor.cpp:47)
         for (int i = tid; i < b; i += blockDim.x) a.rp[a.i0 + 1 + i] = c0;
         if (tid == 0) {
+            *a.swapflag = 0;
             ps->w = 0;
             ps->r = 0;
             ps->spec = 0;
@@ -774,11 +775,16 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
         for (int k = lane; k < b; k += 32)
             if (s_por[k] < 0) mask |= 1ull << k;
         for (int off = 16; off > 0; off >>= 1) mask |= __shfl_xor_sync(FULL, mask, off);
+        bool moved = false;
+        if (!spec)
+            for (int j = lane; j < rt; j += 32) moved |= s_pos[j] != j;
+        moved = __any_sync(FULL, moved);
         if (lane == 0) {
             ps->dead_mask = mask;
             ps->w = w;
             ps->r = rt;
             ps->spec = spec ? 1 : 0;
+            *a.swapflag = moved ? 1 : 0;
         }
     }
 #ifdef RL_TRACE

@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(256 * KS) trsm_node_kernel(TrsmNodeArgs a) {
     }
     const i32 J0 = lo[0];
     const i32 nJ = hi[nl_ - 1] - J0;
-    if (nJ <= 0 || a.M <= 0) return;
+    if (nJ <= 0 || (a.M <= 0 && !a.ninv)) return;
     RL_STAMP(t_enter);
 #ifdef RL_TRACE
     unsigned long long t_leaf[TN_MAXLEAF + 1] = {0, 0, 0, 0, 0};
@@ -268,6 +268,22 @@ __global__ void __launch_bounds__(256 * KS) trsm_node_kernel(TrsmNodeArgs a) {
 #endif
 }
 
+__global__ void ninv_assemble_kernel(u32* X, i32 ldx, const u32* Xa, i32 la, const u32* Xb, i32 lb,
+                                     const u32* T2, i32 lt, Dyn a_lo, Dyn b_lo, Dyn b_hi, const i32* rp,
+                                     i32 nmax) {
+    const i32 a0 = dyn_eval(a_lo, rp), b0 = dyn_eval(b_lo, rp), b1 = dyn_eval(b_hi, rp);
+    const i32 ra = b0 - a0, rx = b1 - a0;
+    for (i64 e = (i64)blockIdx.x * blockDim.x + threadIdx.x; e < (i64)nmax * nmax;
+         e += (i64)gridDim.x * blockDim.x) {
+        const i32 i = (i32)(e / nmax), j = (i32)(e % nmax);
+        if (i >= rx || j >= rx) continue;
+        u32 v;
+        if (i < ra) v = j < ra ? Xa[(i64)i * la + j] : T2[(i64)i * lt + (j - ra)];
+        else v = j < ra ? 0u : Xb[(i64)(i - ra) * lb + (j - ra)];
+        X[(i64)i * ldx + j] = v;
+    }
+}
+
 template <bool SP, int TR, int KS>
 void launch_node(const TrsmNodeArgs& a, cudaStream_t s) {
     constexpr int TM = 16 * TR;
@@ -291,10 +307,17 @@ void launch_node(const TrsmNodeArgs& a, cudaStream_t s) {
 
 }  // namespace
 
+void ninv_assemble(u32* X, i32 ldx, const u32* Xa, i32 la, const u32* Xb, i32 lb, const u32* T2, i32 lt,
+                   Dyn a_lo, Dyn b_lo, Dyn b_hi, const i32* rp, i32 nmax, cudaStream_t s) {
+    const int grid = std::max(1, std::min((nmax * nmax + 255) / 256, 2 * num_sms()));
+    ninv_assemble_kernel<<<grid, 256, 0, s>>>(X, ldx, Xa, la, Xb, lb, T2, lt, a_lo, b_lo, b_hi, rp, nmax);
+    RL_CUDA_CHECK(cudaGetLastError());
+}
+
 // Row tile per CTA: 32 rows for tall G (fewer staged-block loads per row, more
 // products per shared load), 16 otherwise (more CTAs for short G).
 void trsm_node(const TrsmNodeArgs& a, cudaStream_t s) {
-    if (a.M <= 0 || a.nleaf <= 0) return;
+    if ((a.M <= 0 && !a.ninv) || a.nleaf <= 0) return;
     const bool sp = a.f.p <= 65536u;
     if (a.M >= 32 * num_sms()) {
         if (sp) launch_node<true, 2, 1>(a, s);

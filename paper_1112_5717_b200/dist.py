@@ -420,6 +420,8 @@ def dist_cup(x: torch.Tensor, m: int, n: int, p: int, tiles: ColumnTiles, block:
             if beyond is not None:                                  # window mode
                 ls, Ub = beyond
                 if Ub is not None:
+                    if cuda:  # allocated on the side stream, read here on main: keep its
+                        Ub.record_stream(main)  # block from the side pool until main is done
                     x[i0:i0 + rt, ls:].copy_(Ub)
                 x[i0 + rt:i0 + bt, ls:].zero_()
             eng.permute_cols(r, sig_t, [(0, r), (i0 + bt, m)])       # (3)
