@@ -103,6 +103,9 @@ __global__ void __launch_bounds__(256) cup_batched_kernel(u32* A, i64 stride, i3
 // larger p reduce every product.
 constexpr int PR = 32;
 constexpr int BN = 256;
+#ifndef RL_BATCHED_DMMA
+#define RL_BATCHED_DMMA 1  // trailing updates on the FP64 tensor cores (m8n8k4 DMMA)
+#endif
 #ifndef BATCHED_ROWS_PER_WARP
 #define BATCHED_ROWS_PER_WARP 1  // trailing rows per warp (more share the U loads, cost registers)
 #endif
@@ -245,6 +248,65 @@ __global__ void __launch_bounds__(256) cup_batched_blk_kernel(u32* A, i64 stride
                 for (int k = 0; k < PR; ++k) X[k][tid] = 0;
             }
             __syncthreads();
+#if RL_BATCHED_DMMA
+            // (1) multipliers: one warp per trailing row, f = x_piv * U_pp^{-1}
+            // (lane j < np holds f_j); the raw C entries f go to the row's pivot
+            // columns now, the negated multipliers (p - f) to shared memory
+            u32* Fs = reinterpret_cast<u32*>(Up + PR);  // [R][PR], R = m - i0 - pr
+            const i32 rbase = i0 + pr;
+            for (int k0 = rbase + warp; k0 < m; k0 += 8) {
+                u32* row = a + (i64)k0 * n;
+                const u32 pvl = lane < np ? row[r0 + lane] : 0u;
+                u64 sacc = 0;
+                for (int k = 0; k < np; ++k) sacc += (u64)__shfl_sync(0xffffffffu, pvl, k) * X[k][lane];
+                const u32 fv = red64(sacc, f);
+                if (lane < np) row[r0 + lane] = fv;
+                Fs[(k0 - rbase) * PR + lane] = (lane < np && fv) ? f.p - fv : 0u;
+            }
+            __syncthreads();
+            // (2) x_rest += (p - f) * U_rest on the FP64 tensor cores: every term
+            // is an integer < 2^46 and a row sums x + np <= 32 of them (< 2^52),
+            // so the m8n8k4 DMMA accumulation is exact; one reduction per output.
+            {
+                const i32 R = m - rbase, N = n - cend;
+                const int tN = (N + 7) >> 3, tiles = ((R + 7) >> 3) * tN;
+                const int ks_n = (np + 3) >> 2;
+                const double pd = (double)f.p, ipd = 1.0 / pd;
+                const int g = lane >> 2, q4 = lane & 3;
+                for (int tile = warp; tile < tiles; tile += 8) {
+                    const int tr = tile / tN, tn = tile - tr * tN;
+                    const int ra = tr * 8 + g;             // A row / C row of this lane
+                    const int cb = tn * 8 + g;             // B column of this lane
+                    const int cc = tn * 8 + 2 * q4;        // C columns cc, cc + 1
+                    u32* crow = a + (i64)(rbase + ra) * n + cend + cc;
+                    const bool rok = ra < R;
+                    double c0 = (rok && cc < N) ? (double)crow[0] : 0.0;
+                    double c1 = (rok && cc + 1 < N) ? (double)crow[1] : 0.0;
+                    const u32* frow = Fs + ra * PR;
+                    const u32* ucol = Uc + cend + cb;
+                    for (int ks = 0; ks < ks_n; ++ks) {
+                        const int k = 4 * ks + q4;
+                        const double av = (rok && k < np) ? (double)frow[k] : 0.0;
+                        const double bv = (cb < N) ? (double)ucol[k * BN] : 0.0;
+                        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                                     : "+d"(c0), "+d"(c1)
+                                     : "d"(av), "d"(bv));
+                    }
+                    if (rok) {
+                        if (cc < N) {
+                            double r = fma(-floor(c0 * ipd), pd, c0);
+                            r = r < 0.0 ? r + pd : (r >= pd ? r - pd : r);
+                            crow[0] = (u32)r;
+                        }
+                        if (cc + 1 < N) {
+                            double r = fma(-floor(c1 * ipd), pd, c1);
+                            r = r < 0.0 ? r + pd : (r >= pd ? r - pd : r);
+                            crow[1] = (u32)r;
+                        }
+                    }
+                }
+            }
+#else
             const int cpos = r0 + lane, srcl = cpos & 31, qs = cpos >> 5;
             constexpr int RW = BATCHED_ROWS_PER_WARP;
             for (int k0 = i0 + pr + RW * warp; k0 < m; k0 += 8 * RW) {
@@ -312,6 +374,7 @@ __global__ void __launch_bounds__(256) cup_batched_blk_kernel(u32* A, i64 stride
                     }
                 }
             }
+#endif
         } else if (np > 0) {  // one warp per row, pivot by pivot (transpositions, large p)
             for (int t = warp; t < pr; t += 8)
                 for (int c = lane; c < n; c += 32) P[t * BN + c] = a[(i64)(i0 + t) * n + c];

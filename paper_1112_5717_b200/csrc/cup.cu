@@ -319,7 +319,9 @@ void CupEngine::gemm_ninv(i32 r0, i32 M, i32 x0, i32 mx, const u32* ninv, i32 ld
 void CupEngine::trsm_right(i32 r0, i32 M, i32 x0, i32 mx) {
     // a tall TRSM against a node with a big inverse: one GEMM (the inverse is
     // unique, so the bytes are the reference recursion's)
-    if (big_on_ && use_tc_ && M >= kBigMinRows) {
+    // (not the node factored last before this TRSM: its inverse is still being
+    // built, the recursion below is faster than waiting for it)
+    if (big_on_ && use_tc_ && M >= kBigMinRows && x0 + mx < trsm_end_) {
         const auto key = std::make_pair(x0, mx);
         if (big_slot_.count(key)) {
             if (dry_) {
@@ -433,6 +435,7 @@ void CupEngine::node(i32 i0, i32 mm) {
         }
     }
     const i32 b0 = i0 + k, bm = mm - k;
+    trsm_end_ = b0;  // the TRSMs of this node solve against rows [i0, b0)
     swaps_range(b0, bm, dyn_rp(i0), dyn_rp(b0), i0, b0);             // factor.cpp:42
     if (!dry_ && uinv_join_) {
         RL_CUDA_CHECK(cudaStreamWaitEvent(s_, uinv_join_, 0));

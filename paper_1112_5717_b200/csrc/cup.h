@@ -158,6 +158,7 @@ private:
 #endif
     static constexpr i32 kBigMinRows = RL_BIG_MIN_ROWS;  // TRSMs at least this tall use them
     bool big_on_ = RL_BIG_INV != 0;
+    i32 trsm_end_ = 0;  // end row of the triangle the current node's TRSMs solve against
     std::map<std::pair<i32, i32>, i32> big_slot_;          // node -> slot (dry run)
     std::map<std::pair<i32, i32>, cudaEvent_t> big_ready_; // node -> built (one enqueue)
     u32* big_ = nullptr;                                   // BIG_LD x BIG_LD per slot

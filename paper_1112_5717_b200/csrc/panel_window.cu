@@ -480,6 +480,9 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
     extern __shared__ __align__(16) uint8_t dsm[];
     __shared__ u32 s_C[PB][PB + 1];
     __shared__ i32 s_pos[PB], s_rrp[PB], s_rb[PB], s_por[PB];
+    __shared__ i32 s_perm[PB], s_iperm[PB];  // speculative order: live rows first
+    __shared__ unsigned long long s_deadw;
+    __shared__ int s_live;
     __shared__ u32 s_pv[PB], s_pinvA[PB];
     __shared__ i32 s_sig[PW];
     __shared__ int s_c[2];
@@ -545,13 +548,46 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
         acc[s][4] = (lane == k) ? 1u : 0u;
         acc[s][5] = (lane + 32 == k) ? 1u : 0u;
     }
-    // stage [window | identity] for the speculative (generic-case) path
+    // Rows that are zero across the whole window as loaded (e.g. zero rows of a
+    // rank-deficient input: row operations keep them zero) have no pivot in it:
+    // the speculative LU runs on the other rows only, in order ("live" rows
+    // first), so such leaves stay on the fast path.  Whether those rows are also
+    // zero beyond the window is checked by the tail (fallback otherwise).
+    if (tid == 0) s_deadw = 0;
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < RW; ++s) {
+        const int k = warp + NW * s;
+        const bool nz = __any_sync(FULL, acc[s][0] | acc[s][1] | acc[s][2] | acc[s][3]);
+        if (lane == 0 && k < b && !nz) atomicOr(&s_deadw, 1ull << k);
+    }
+    __syncthreads();
+    const u64 deadw = s_deadw;
+    if (tid < PB) {
+        const int k = tid;
+        const u64 below = deadw & ((1ull << k) - 1);
+        const int live_before = k - __popcll(below);
+        const int nlive = b - __popcll(deadw & (b >= 64 ? ~0ull : ((1ull << b) - 1)));
+        if (k < b) {
+            const bool dk = (deadw >> k) & 1;
+            const int pos = dk ? nlive + (k - live_before) : live_before;
+            s_perm[pos] = k;
+            s_iperm[k] = pos;
+        }
+        if (k == 0) s_live = nlive;
+    }
+    __syncthreads();
+    const int bl = s_live;
+    // stage [window | identity] in that order for the speculative path
 #pragma unroll
     for (int s = 0; s < RW; ++s) {
         const int k = warp + NW * s;
         if (k < b) {
+            const int kp = s_iperm[k];
 #pragma unroll
-            for (int q = 0; q < 6; ++q) s_R[k * RP + lane + 32 * q] = (u32)acc[s][q];
+            for (int q = 0; q < 4; ++q) s_R[kp * RP + lane + 32 * q] = (u32)acc[s][q];
+            s_R[kp * RP + PW + lane] = (lane == kp) ? 1u : 0u;
+            s_R[kp * RP + PW + 32 + lane] = (lane + 32 == kp) ? 1u : 0u;
         }
     }
     cp_async_wait_all();
@@ -578,16 +614,32 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
     }
 #endif
     RL_STAMP(t_loaded);
-    const bool spec = spec_lu<SP>(s_R, s_C, s_pv, s_pinvA, S.s_inv, s_M, &s_fail, b, w, f);
+    const bool spec = spec_lu<SP>(s_R, s_C, s_pv, s_pinvA, S.s_inv, s_M, &s_fail, bl, w, f);
     RL_STAMP(t_lu);
     int r = 0;
     if (spec) {
-        r = b;
+        r = bl;
         for (int e = tid; e < b; e += blockDim.x) {
-            s_pos[e] = e;
-            s_rrp[e] = e;
-            s_rb[e] = e;
-            s_por[e] = e;
+            const int kp = s_iperm[e];
+            const bool dk = kp >= bl;
+            s_pos[e] = e;                       // no transposition
+            if (e < bl) s_rrp[e] = s_perm[e];   // pivot e is the e-th live row
+            s_rb[e] = 0;                        // set below
+            s_por[e] = dk ? -1 : kp;
+        }
+        __syncthreads();
+        for (int e = tid; e < b; e += blockDim.x)  // rank before row e = live rows before it
+            s_rb[e] = e - __popcll(deadw & ((1ull << e) - 1));
+        if (deadw) {  // a window-dead row may hold a pivot beyond the window: the
+                      // tail's fallback then needs the original window
+#pragma unroll
+            for (int s2 = 0; s2 < RW; ++s2) {
+                const int k = warp + NW * s2;
+                if (k < b) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) ps->win_orig[k][lane + 32 * q] = (u32)acc[s2][q];
+                }
+            }
         }
         __syncthreads();
     } else {
@@ -705,15 +757,17 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
     unsigned long long t_mid = 0;
 #endif
     if (spec) {
-        // rrp = identity: row k's pivot is column k -- C left of it, the raw pivot,
-        // U = reduced value * pivot^{-1} right of it; Minv row k scaled likewise
+        // live row k' (original row s_perm[k']) has its pivot at column k': C
+        // left of it, the raw pivot, U = reduced value * pivot^{-1} right of it;
+        // Minv row k' scaled likewise.  Dead rows stay zero in the window, their
+        // Minv row is e_k (residual = the row itself).
 #pragma unroll 4
         for (int e = tid; e < PB * PB; e += blockDim.x) {
-            const int k = e / PB, x = e % PB;
-            if (k < b && x < b) {
-                const u32 rv = s_R[k * RP + x];
-                const u32 val = x < k ? s_C[k][x] : (x == k ? rv : mulmod_t<SP>(rv, s_pinvA[k], f));
-                a.A[(i64)(a.i0 + k) * a.lda + c0 + x] = val;
+            const int kp = e / PB, x = e % PB;
+            if (kp < bl && x < bl) {
+                const u32 rv = s_R[kp * RP + x];
+                const u32 val = x < kp ? s_C[kp][x] : (x == kp ? rv : mulmod_t<SP>(rv, s_pinvA[kp], f));
+                a.A[(i64)(a.i0 + s_perm[kp]) * a.lda + c0 + x] = val;
             }
         }
 #ifdef RL_TRACE
@@ -721,8 +775,20 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
 #endif
 #pragma unroll 4
         for (int e = tid; e < PB * PB; e += blockDim.x) {
-            const int k = e / PB, i = e % PB;
-            ps->Minv[k][i] = (k < b && i < b) ? mulmod_t<SP>(s_R[k * RP + PW + i], s_pinvA[k], f) : 0u;
+            const int k = e / PB, i = e % PB;  // original rows
+            u32 mi = 0, mr = 0;
+            if (k < b && i < b) {
+                const int kp = s_iperm[k], ip = s_iperm[i];
+                if (kp < bl) {
+                    mi = ip < bl ? mulmod_t<SP>(s_R[kp * RP + PW + ip], s_pinvA[kp], f) : 0u;
+                    mr = ip == kp ? s_pv[kp] : ((ip < kp) ? s_C[kp][ip] : 0u);
+                } else {
+                    mi = (i == k) ? 1u % f.p : 0u;
+                    mr = (i == k) ? 1u % f.p : 0u;
+                }
+            }
+            ps->Minv[k][i] = mi;
+            if (deadw) ps->Mr[k][i] = mr;  // fallback restore only
         }
     } else {
     const int xend = w;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -64,6 +65,15 @@ inline void prefer_max_smem(F* kernel) {
                                                (int)(bytes)));                              \
     } while (0)
 
+// RL_NO_PDL=1 launches every kernel as a plain dependent (debugging aid).
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("RL_NO_PDL");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
+
 // Launch as a programmatic dependent of the previous kernel on the stream (the
 // kernel must follow the pdl_wait/pdl_trigger protocol, common.cuh): its CTAs
 // may start while the predecessor finishes, hiding launch latency inside the
@@ -80,7 +90,7 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
     RL_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 

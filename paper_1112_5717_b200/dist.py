@@ -37,6 +37,7 @@ libranklab_gpu.so on the rank's GPU); communication through ``torch.distributed`
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -391,14 +392,22 @@ def dist_cup(x: torch.Tensor, m: int, n: int, p: int, tiles: ColumnTiles, block:
             if rb > hi:
                 ops.mm_sub(G[hi - ra:], U, x[hi:rb, ls:])
             return None
+        dbg = os.environ.get("RL_DIST_DEBUG_SYNC", "")
         ev = main.record_event()
         if lo > ra:
             ops.mm_sub(G[:lo - ra], U, x[ra:lo, ls:], max_ctas=max_ctas)
         if rb > hi:
             ops.mm_sub(G[hi - ra:], U, x[hi:rb, ls:], max_ctas=max_ctas)
+        if "evall" in dbg:
+            ev = main.record_event()
         side.wait_event(ev)
+        if "pre" in dbg:
+            torch.cuda.synchronize()
         with torch.cuda.stream(side):
-            return (nb, factor_block(*nb))
+            out = (nb, factor_block(*nb))
+        if "post" in dbg:
+            torch.cuda.synchronize()
+        return out
 
     sigma = np.arange(n, dtype=np.int64)
     rrp: list[np.ndarray] = []
