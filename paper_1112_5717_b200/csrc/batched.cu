@@ -506,12 +506,12 @@ void cup_batched(u32* dA, i64 batch, i32 m, i32 n, i64 stride, u32 p, i32* d_ran
     if (n <= BN) {
         const size_t smem = sizeof(u64) * PR * BN + sizeof(u32) * 8 * BN;
         static std::atomic<unsigned long long> attr_once{0};
-        if (first_on_device(attr_once)) {
+        once_on_device(attr_once, [&] {
             RL_CUDA_CHECK(cudaFuncSetAttribute(cup_batched_blk_kernel<true>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             RL_CUDA_CHECK(cudaFuncSetAttribute(cup_batched_blk_kernel<false>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        }
+        });
         // the per-prime table pays off for real batches; a handful of matrices
         // take the in-kernel extended Euclid inverse (so does every p >= 2^24)
         if (p < (1u << 24))

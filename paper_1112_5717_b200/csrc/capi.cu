@@ -626,7 +626,7 @@ int rl_cup_u32(uint32_t* A, int64_t m, int64_t n, int64_t lda, uint32_t p, int64
             return;
         }
         require_device();
-        cudaStream_t s = cudaStreamPerThread;
+        cudaStream_t s = host_stream();
         Call call(s);
         Scratch& sc = call.sc;
         i64 r = 0;
@@ -678,7 +678,7 @@ int rl_ple_u32(uint32_t* A, int64_t m, int64_t n, int64_t lda, uint32_t p, int64
         if (m == 0 || n == 0) return ple_empty(m, rank, row_perm, ops);
         if (!A) throw Error(RL_EINVAL, "null matrix");
         require_device();
-        cudaStream_t s = cudaStreamPerThread;
+        cudaStream_t s = host_stream();
         Call call(s);
         u32* dA = (u32*)call.sc.get(SS_A, (size_t)m * n * 4);
         copy_h2d_2d(dA, n, A, lda, m, n, s);
@@ -716,7 +716,7 @@ int rl_col_ech_trans_u32(uint32_t* A, int64_t m, int64_t n, int64_t lda, uint32_
         }
         if (!A) throw Error(RL_EINVAL, "null matrix");
         require_device();
-        cudaStream_t s = cudaStreamPerThread;
+        cudaStream_t s = host_stream();
         Call call(s);
         u32* dA = (u32*)call.sc.get(SS_A, (size_t)m * n * 4);
         copy_h2d_2d(dA, n, A, lda, m, n, s);
@@ -748,7 +748,7 @@ int rl_invert_u32(uint32_t* A, int64_t n, int64_t lda, uint32_t p, uint64_t* ops
         if (n == 0) return;
         if (!A) throw Error(RL_EINVAL, "null matrix");
         require_device();
-        cudaStream_t s = cudaStreamPerThread;
+        cudaStream_t s = host_stream();
         Call call(s);
         u32* dA = (u32*)call.sc.get(SS_A, (size_t)n * n * 4);
         copy_h2d_2d(dA, n, A, lda, n, n, s);
@@ -811,7 +811,7 @@ int rl_trsm_u32(int side, int uplo, int diag, const uint32_t* T, int64_t ldt, ui
         }
         trsm_ops(side, uplo, diag, m, n, threshold, ops);
         require_device();
-        cudaStream_t s = cudaStreamPerThread;
+        cudaStream_t s = host_stream();
         Call call(s);
         u32* dT = (u32*)call.sc.get(SS_A, (size_t)k * k * 4);
         u32* dB = (u32*)call.sc.get(SS_B, (size_t)m * n * 4);
@@ -945,7 +945,7 @@ int rl_mm_u32(const uint32_t* A, int64_t lda, const uint32_t* B, int64_t ldb, ui
         }
         if (m == 0 || n == 0) return;
         require_device();
-        cudaStream_t s = cudaStreamPerThread;
+        cudaStream_t s = host_stream();
         Call call(s);
         u32* dA = (u32*)call.sc.get(SS_A, (size_t)std::max<i64>(m * l, 1) * 4);
         u32* dB = (u32*)call.sc.get(SS_B, (size_t)std::max<i64>(l * n, 1) * 4);
@@ -1051,7 +1051,7 @@ int rl_cup_batched_u32(uint32_t* A, int64_t batch, int64_t m, int64_t n, int64_t
         }
         if (!A) throw Error(RL_EINVAL, "null matrix");
         require_device();
-        Call call(cudaStreamPerThread);
+        Call call(host_stream());
         cudaStream_t sh = call.sc.aux_stream(0), sc = call.sc.aux_stream(1), sd = call.sc.aux_stream(2);
         u32* dA = (u32*)call.sc.get(SS_A, (size_t)batch * stride * 4);
         i32* dmeta = (i32*)call.sc.get(SS_META, (size_t)batch * (1 + 2 * kcap) * 4);

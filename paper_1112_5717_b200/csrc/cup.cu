@@ -51,18 +51,23 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
     rrp_ = reinterpret_cast<i32*>(base + o_rrp);
     ipiv_ = reinterpret_cast<i32*>(base + o_ipiv);
     ps_ = reinterpret_cast<PanelScratch*>(base + o_ps);
-    RL_CUDA_CHECK(cudaMemset(ps_, 0, sizeof(PanelScratch)));
+    // set-up work on a private non-blocking stream: nothing here touches the
+    // legacy stream (another host thread may be capturing a graph meanwhile)
+    cudaStream_t init_s = nullptr;
+    RL_CUDA_CHECK(cudaStreamCreateWithFlags(&init_s, cudaStreamNonBlocking));
+    RL_CUDA_CHECK(cudaMemsetAsync(ps_, 0, sizeof(PanelScratch), init_s));
     uinv_ = reinterpret_cast<u32*>(base + o_uinv);
     swapflags_ = reinterpret_cast<i32*>(base + o_flags);
-    RL_CUDA_CHECK(cudaMemset(swapflags_, 0, sizeof(i32) * (leaf_of_.size() + 1)));
+    RL_CUDA_CHECK(cudaMemsetAsync(swapflags_, 0, sizeof(i32) * (leaf_of_.size() + 1), init_s));
     leaf_starts_.assign(leaf_of_.size(), 0);
     for (const auto& kv : leaf_of_) leaf_starts_[kv.second] = kv.first;
     ninv_ = ninv_slot_.empty() ? nullptr : reinterpret_cast<u32*>(base + o_ninv);
     if (p_ <= 65536u) {
         inv_table_ = reinterpret_cast<uint16_t*>(base + o_tab);
-        build_inv_table(inv_table_, p_, nullptr);
-        RL_CUDA_CHECK(cudaDeviceSynchronize());
+        build_inv_table(inv_table_, p_, init_s);
     }
+    RL_CUDA_CHECK(cudaStreamSynchronize(init_s));
+    RL_CUDA_CHECK(cudaStreamDestroy(init_s));
     // the critical path (s_, s3_) outranks the wide updates (s2_) at the CTA
     // scheduler: a window CTA takes the first SM that frees up
     int prio_lo = 0, prio_hi = 0;
@@ -76,7 +81,15 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
     if (b2_cap_) RL_CUDA_CHECK(cudaMalloc(&b2_, b2_cap_));
     for (auto& kv : lanes_) {
         Lane& l = kv.second;
-        RL_CUDA_CHECK(cudaStreamCreateWithPriority(&l.st, cudaStreamNonBlocking, prio_lo));
+        // a short lane's pieces are needed sooner: lanes of height 128, 256, ...
+        // get the priorities right below the critical path's, the tall ones the lowest
+        int prio = prio_lo;
+        if (lane_prio_) {
+            int lvl = 0;
+            for (i32 h = kv.first; h > 2 * PB; h /= 2) ++lvl;
+            prio = std::min(prio_lo, prio_hi + 1 + lvl);
+        }
+        RL_CUDA_CHECK(cudaStreamCreateWithPriority(&l.st, cudaStreamNonBlocking, prio));
         if (l.a2_cap) RL_CUDA_CHECK(cudaMalloc(&l.a2, l.a2_cap));
         if (l.b2_cap) RL_CUDA_CHECK(cudaMalloc(&l.b2, l.b2_cap));
     }
@@ -444,7 +457,49 @@ void CupEngine::node(i32 i0, i32 mm) {
     // factor.cpp:51-52, split: the first window of the bottom half reads only
     // columns [rp[b0], rp[b0] + PW), so that slice is updated first and the rest
     // runs on s2_ beside that window (joined before its tail)
-    if (k > split_max_k_ && row_split_min_ > 0 && bm >= row_split_min_ && bm > 2 * PB) {
+    if (geo_split_ && bm > PB && k <= geo_max_k_) {
+        // Geometric row split.  The bottom recursion node(b0, bm) first touches
+        // its rows in the order of its left spine: the leaf [b0, b0 + s_L), then
+        // the bottom half [b0 + s/2, b0 + s) of node(b0, s) for s = 2 s_L, ..., bm
+        // (each right after node(b0, s)'s top half is factored).  Only the first
+        // leaf's TRSM + window-slice update runs on the critical path; every
+        // later piece's TRSM + full-width Schur update runs, smallest (= needed
+        // soonest) first, on the low-priority lane of height bm and is joined by
+        // node(b0, s) right before its first touch of those rows (row_joins_).
+        // Value-neutral: row blocks of a right TRSM and of a Schur update are
+        // independent, and no piece row is read or written by anything else
+        // before its join.
+        std::vector<i32> spine;  // s = bm, bm/2, ... (> PB): node(b0, s) on the left spine
+        for (i32 s = bm; s > PB; s /= 2) spine.push_back(s);
+        const i32 leaf = spine.back() / 2;  // node(b0, leaf) is the first leaf
+        trsm_right(b0, leaf, i0, k);                                   // factor.cpp:45-46
+        gemm(b0, leaf, i0, b0, dyn_rp(b0), Dyn{b0, PW}, std::min<i64>(PW, n_), s_, n_);
+        if (dry_) {
+            events_needed_ += 2;
+            gemm(b0, leaf, i0, b0, Dyn{b0, PW}, dyn_c(n_), n_, s2_);
+        } else {
+            fork_to(s_, s2_);
+            gemm(b0, leaf, i0, b0, Dyn{b0, PW}, dyn_c(n_), n_, s2_);
+            cudaEvent_t e = events_.at(next_event_++);
+            RL_CUDA_CHECK(cudaEventRecord(e, s2_));
+            pending_joins_.push_back(e);
+        }
+        Lane& ln = lanes_[bm];
+        if (dry_) events_needed_ += 1 + spine.size();
+        else fork_to(s_, ln.st);
+        lane_ = &ln;
+        for (size_t q = spine.size(); q-- > 0;) {
+            const i32 s = spine[q], h = s / 2;
+            trsm_right(b0 + h, s - h, i0, k);
+            gemm(b0 + h, s - h, i0, b0, dyn_rp(b0), dyn_c(n_), n_);
+            if (!dry_) {
+                cudaEvent_t e = events_.at(next_event_++);
+                RL_CUDA_CHECK(cudaEventRecord(e, ln.st));
+                row_joins_[{b0, s}] = e;
+            }
+        }
+        lane_ = nullptr;
+    } else if (k > split_max_k_ && row_split_min_ > 0 && bm >= row_split_min_ && bm > 2 * PB) {
         // rows [b0, b0 + h) now; rows [b0 + h, b0 + bm) on the lane of height bm,
         // joined in node(b0, bm) after its top half (rows [b0, b0 + h)) is factored
         const i32 h = bm / 2;

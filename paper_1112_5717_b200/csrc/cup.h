@@ -133,6 +133,20 @@ private:
 #define RL_ROW_SPLIT_MIN_ROWS 4096
 #endif
     i32 row_split_min_ = RL_ROW_SPLIT_MIN_ROWS;  // 0: off
+    // geometric row split (node()): every bottom half is updated piece by piece
+    // in the order the recursion below first touches its rows
+#ifndef RL_GEO_SPLIT
+#define RL_GEO_SPLIT 0
+#endif
+    bool geo_split_ = RL_GEO_SPLIT != 0;
+#ifndef RL_GEO_MAX_K
+#define RL_GEO_MAX_K 512
+#endif
+    i32 geo_max_k_ = RL_GEO_MAX_K;  // only nodes whose top half has at most this many rows
+#ifndef RL_LANE_PRIO
+#define RL_LANE_PRIO 1
+#endif
+    bool lane_prio_ = RL_LANE_PRIO != 0;  // lane stream priority by height (else all lowest)
 #ifndef RL_LANE_CTAS
 #define RL_LANE_CTAS 110
 #endif

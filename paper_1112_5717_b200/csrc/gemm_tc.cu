@@ -550,11 +550,11 @@ void launch_tc(const GemmArgs& g, i64 Kmax, i64 Nmax, uint8_t* a2, uint8_t* b2, 
     }
     if (phase == 0) return;
     static std::atomic<unsigned long long> attr_once{0};
-    if (first_on_device(attr_once)) {
+    once_on_device(attr_once, [&] {
         RL_CUDA_CHECK(cudaFuncSetAttribute(gemm_tc_kernel<L>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)C_::SMEM));
-    }
+    });
     RL_ONCE_MAX_SMEM(gemm_tc_kernel<L>);
     launch_pdl(gemm_tc_kernel<L>, dim3(grid), dim3(NTHR), C_::SMEM, s, g, (const uint8_t*)a2, (const uint8_t*)b2,
                sc[1], sc[2], sc[3]);

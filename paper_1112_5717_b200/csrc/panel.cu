@@ -573,12 +573,12 @@ void panel_uinv(const PanelArgs& a, cudaStream_t s) {
     // chain ran ~3x slower beside the tail's multiply-add streams.
     const size_t smem = std::max<size_t>(sizeof(u32) * 3 * PB * (PB + 1), 200 * 1024);
     static std::atomic<unsigned long long> attr_once{0};
-    if (first_on_device(attr_once)) {
+    once_on_device(attr_once, [&] {
         RL_CUDA_CHECK(cudaFuncSetAttribute(panel_uinv_kernel<true>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         RL_CUDA_CHECK(cudaFuncSetAttribute(panel_uinv_kernel<false>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    }
+    });
     if (a.f.p <= 65536u) panel_uinv_kernel<true><<<1, 512, smem, s>>>(a);
     else panel_uinv_kernel<false><<<1, 512, smem, s>>>(a);
     RL_CUDA_CHECK(cudaGetLastError());
@@ -589,12 +589,12 @@ void panel_tail(const PanelArgs& a, cudaStream_t s) {
     const size_t smem = std::max<size_t>(sizeof(u32) * (PB * MIP + PB * (TT + 4)) + 2 * (PB + TT) * BPI,
                                          sizeof(u32) * 3 * PB * (PB + 1));
     static std::atomic<unsigned long long> attr_once{0};
-    if (first_on_device(attr_once)) {
+    once_on_device(attr_once, [&] {
         RL_CUDA_CHECK(cudaFuncSetAttribute(panel_tail_kernel<true>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         RL_CUDA_CHECK(cudaFuncSetAttribute(panel_tail_kernel<false>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    }
+    });
     const int grid = std::max(1, std::min((a.N + TT - 1) / TT, 8 * num_sms())) + 1;
     RL_ONCE_MAX_SMEM(panel_tail_kernel<true>);
     RL_ONCE_MAX_SMEM(panel_tail_kernel<false>);

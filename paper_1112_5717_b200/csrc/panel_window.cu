@@ -882,14 +882,14 @@ void panel_window(const PanelArgs& a, cudaStream_t s) {
     const bool sp = a.f.p <= 65536u;
     const size_t smem = sizeof(u32) * PB * RP + (sp ? 65536 * 2 : 0);
     static std::atomic<unsigned long long> attr_once{0};
-    if (first_on_device(attr_once)) {
+    once_on_device(attr_once, [&] {
         RL_CUDA_CHECK(cudaFuncSetAttribute(panel_window_kernel<true>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)(sizeof(u32) * PB * RP + 65536 * 2)));
         RL_CUDA_CHECK(cudaFuncSetAttribute(panel_window_kernel<false>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)(sizeof(u32) * PB * RP)));
-    }
+    });
     RL_ONCE_MAX_SMEM(panel_window_kernel<true>);
     RL_ONCE_MAX_SMEM(panel_window_kernel<false>);
     if (sp) launch_pdl(panel_window_kernel<true>, dim3(1), dim3(NW * 32), smem, s, a);

@@ -62,6 +62,13 @@ Scratch& scratch_for(cudaStream_t s) {
     return ref;
 }
 
+cudaStream_t host_stream() {
+    thread_local cudaStream_t per_dev[64] = {};
+    const int d = current_device() & 63;
+    if (!per_dev[d]) RL_CUDA_CHECK(cudaStreamCreateWithFlags(&per_dev[d], cudaStreamNonBlocking));
+    return per_dev[d];
+}
+
 cudaStream_t Scratch::aux_stream(int i) {
     if (!aux[i]) RL_CUDA_CHECK(cudaStreamCreateWithFlags(&aux[i], cudaStreamNonBlocking));
     return aux[i];

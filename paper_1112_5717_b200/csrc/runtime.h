@@ -29,13 +29,18 @@ int current_device();
 // SM count of the current device (cached per device).
 int num_sms();
 
-// True exactly once per (call site, device): function attributes
-// (cudaFuncSetAttribute) are per device, so "set once" is per device too.
-inline bool first_on_device(std::atomic<unsigned long long>& mask) {
-    const int d = current_device() & 63;
-    const unsigned long long bit = 1ull << d;
-    if (mask.load(std::memory_order_acquire) & bit) return false;
-    return !(mask.fetch_or(bit, std::memory_order_acq_rel) & bit);
+// Runs fn exactly once per (call site, device); a concurrent caller on another
+// host thread WAITS until that first run completed (a kernel must not be
+// launched before its shared-memory attribute is set).
+template <class F>
+inline void once_on_device(std::atomic<unsigned long long>& done, F&& fn) {
+    const unsigned long long bit = 1ull << (current_device() & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    static std::mutex mu;  // one per F (call site), shared by the devices
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.load(std::memory_order_relaxed) & bit) return;
+    fn();
+    done.fetch_or(bit, std::memory_order_release);
 }
 #define RL_ONCE_PER_DEVICE()                                 \
     ([]() -> std::atomic<unsigned long long>& {              \
@@ -54,15 +59,16 @@ inline void prefer_max_smem(F* kernel) {
 #define RL_ONCE_MAX_SMEM(kernel)                                     \
     do {                                                             \
         static std::atomic<unsigned long long> once_{0};             \
-        if (first_on_device(once_)) prefer_max_smem(kernel);         \
+        once_on_device(once_, [&] { prefer_max_smem(kernel); });     \
     } while (0)
 // cudaFuncSetAttribute(kernel, MaxDynamicSharedMemorySize, bytes) once per device.
 #define RL_ONCE_SMEM_LIMIT(kernel, bytes)                                                   \
     do {                                                                                    \
         static std::atomic<unsigned long long> once_{0};                                    \
-        if (first_on_device(once_))                                                         \
+        once_on_device(once_, [&] {                                                         \
             RL_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                                (int)(bytes)));                              \
+        });                                                                                 \
     } while (0)
 
 // RL_NO_PDL=1 launches every kernel as a plain dependent (debugging aid).
@@ -139,5 +145,9 @@ struct Scratch {
     void* pinned_ring(size_t bytes);
 };
 Scratch& scratch_for(cudaStream_t s);
+// The host-buffer entry points' stream: one NON-blocking stream per (host
+// thread, device), so those calls never synchronise implicitly with the legacy
+// stream (or with work another thread is capturing into a graph).
+cudaStream_t host_stream();
 
 }  // namespace rl

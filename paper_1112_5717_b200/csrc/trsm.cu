@@ -291,11 +291,11 @@ void launch_node(const TrsmNodeArgs& a, cudaStream_t s) {
     const size_t part = KS > 1 ? sizeof(u64) * (KS - 1) * TM * PB : 0;
     const size_t smem = sizeof(u32) * (TM * GW + (size_t)nblk * PB * BW) + part;
     static std::atomic<unsigned long long> attr_once{0};
-    if (first_on_device(attr_once)) {
+    once_on_device(attr_once, [&] {
         const size_t maxs = sizeof(u32) * (TM * GW + (size_t)10 * PB * BW) + part;
         RL_CUDA_CHECK(cudaFuncSetAttribute(trsm_node_kernel<SP, TR, KS>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxs));
-    }
+    });
     // one staging of the U blocks per CTA: about one CTA per SM, each looping
     // over its row tiles
     const int per_sm = nblk >= 6 ? 1 : (nblk >= 3 ? 2 : 4);
