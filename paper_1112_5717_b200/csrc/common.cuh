@@ -181,6 +181,50 @@ __device__ __forceinline__ i32 dyn_eval(const Dyn& d, const i32* rp) {
     return (d.idx >= 0 ? __ldcg(rp + d.idx) : 0) + d.cst;
 }
 
+
+
+// Leaf-chain probe (tuning builds, -DRL_LEAFTRACE): per kernel and leaf, the
+// globaltimer after pdl_wait and at exit, in a per-file device table read back
+// by rl_lt_dump_<file>() (tools/leaftrace.py).
+#ifdef RL_LEAFTRACE
+__device__ __forceinline__ unsigned long long rl_gt() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define LT_TABLE(name)                                                        \
+    static __device__ unsigned long long g_lt[1024][8];                       \
+    extern "C" int rl_lt_dump_##name(unsigned long long* h) {                 \
+        return (int)cudaMemcpyFromSymbol(h, g_lt, sizeof(g_lt));             \
+    }
+#define LT_BEGIN() const unsigned long long lt_t0 = rl_gt()
+#define LT_MARK(key, i)                                                       \
+    do {                                                                      \
+        if (threadIdx.x == 0 && (key) >= 0 && (key) < 1024) g_lt[(key)][(i)] = rl_gt(); \
+    } while (0)
+#define LT_END(key)                                                           \
+    do {                                                                      \
+        if (threadIdx.x == 0 && (key) >= 0 && (key) < 1024) {                 \
+            g_lt[(key)][0] = lt_t0;                                           \
+            g_lt[(key)][1] = rl_gt();                                         \
+        }                                                                     \
+    } while (0)
+#else
+#define LT_TABLE(name)
+#define LT_BEGIN()
+#define LT_MARK(key, i)
+#define LT_END(key)
+#endif
+
+// Critical-path probes (tuning builds only): busy-wait ns nanoseconds.
+__device__ __forceinline__ void rl_spin_ns(unsigned long long ns) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < ns);
+}
+
 #define RL_CUDA_CHECK(x)                                                  \
     do {                                                                  \
         cudaError_t _e = (x);                                             \

@@ -166,14 +166,25 @@ void CupEngine::gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nm
     g.rp = rp_;
     g.n_cap = n_cap;
     // on the side stream the persistent GEMM leaves one SM for the window kernel
-    g.max_ctas = (st == s_) ? 0 : (ln && lane_ctas_ > 0) ? lane_ctas_ : num_sms() - 1;
+#ifndef RL_SIDE_FREE_SMS
+#define RL_SIDE_FREE_SMS 1
+#endif
+    g.max_ctas = (st == s_) ? 0 : (ln && lane_ctas_ > 0) ? lane_ctas_ : num_sms() - RL_SIDE_FREE_SMS;
     g.alpha = p_ - 1;  // C <- C - A*B  (mm(..., neg_one, one), factor.cpp:51)
     g.beta = 1 % p_;
     g.f = f_;
     // skinny K (one leaf): the SIMT kernel reads the operands directly and
     // beats packing them for the tensor cores
     // ... and so are the 128-column window slices of the split updates up to K = 256
-    const bool tc = use_tc_ && Kmax > PB && Nmax >= 64 && M >= 64 && !(Nmax <= PW && Kmax <= 4 * PB);
+#ifndef RL_IMMA_MAX_K
+#define RL_IMMA_MAX_K PB
+#endif
+#ifndef RL_IMMA_MAX_MK
+#define RL_IMMA_MAX_MK 0
+#endif
+    // (p <= 2^16: small updates, K <= RL_IMMA_MAX_K or M*K <= RL_IMMA_MAX_MK, skip the packing too)
+    const bool small = p_ <= 65536u && (Kmax <= RL_IMMA_MAX_K || (i64)M * Kmax <= (i64)RL_IMMA_MAX_MK);
+    const bool tc = use_tc_ && !small && Kmax > PB && Nmax >= 64 && M >= 64 && !(Nmax <= PW && Kmax <= 4 * PB);
     if (dry_) {
         if (tc) {
             size_t& ac = ln ? ln->a2_cap : a2_cap_;
@@ -449,7 +460,10 @@ void CupEngine::node(i32 i0, i32 mm) {
     }
     const i32 b0 = i0 + k, bm = mm - k;
     trsm_end_ = b0;  // the TRSMs of this node solve against rows [i0, b0)
-    swaps_range(b0, bm, dyn_rp(i0), dyn_rp(b0), i0, b0);             // factor.cpp:42
+    // a leaf pair (top = one leaf, p <= 2^16): swaps, TRSM and the window slice's
+    // update in one launch (bridge.cu)
+    const bool br = bridge_on_ && k <= PB && bm <= PB && p_ <= 65536u && use_tc_;
+    if (!br) swaps_range(b0, bm, dyn_rp(i0), dyn_rp(b0), i0, b0);   // factor.cpp:42
     if (!dry_ && uinv_join_) {
         RL_CUDA_CHECK(cudaStreamWaitEvent(s_, uinv_join_, 0));
         uinv_join_ = nullptr;
@@ -519,6 +533,38 @@ void CupEngine::node(i32 i0, i32 mm) {
             cudaEvent_t e = events_.at(next_event_++);
             RL_CUDA_CHECK(cudaEventRecord(e, ln.st));
             row_joins_[{b0, bm}] = e;
+        }
+    } else if (br) {
+        if (!dry_) {
+            BridgeArgs a{};
+            a.A = A_;
+            a.lda = lda_;
+            a.row0 = b0;
+            a.M = bm;
+            a.j_lo = dyn_rp(i0);
+            a.j_hi = dyn_rp(b0);
+            a.n_lo = dyn_rp(b0);
+            a.N = n_;
+            a.rp = rp_;
+            a.rrp = rrp_;
+            a.ipiv = ipiv_;
+            a.uinv = uinv_ + (size_t)leaf_of_.at(i0) * PB * PB;
+            a.swapflag = swapflags_ + leaf_of_.at(i0);
+            a.ps = ps_;
+            a.f = f_;
+            flush_swaps();
+            bridge(a, s_);
+            stats_.launches += 1;
+        }
+        if (dry_) {
+            events_needed_ += 2;
+            gemm(b0, bm, i0, b0, Dyn{b0, PW}, dyn_c(n_), n_, s2_);
+        } else {
+            fork_to(s_, s2_);
+            gemm(b0, bm, i0, b0, Dyn{b0, PW}, dyn_c(n_), n_, s2_);
+            cudaEvent_t e = events_.at(next_event_++);
+            RL_CUDA_CHECK(cudaEventRecord(e, s2_));
+            pending_joins_.push_back(e);
         }
     } else if (k > split_max_k_) {
         trsm_right(b0, bm, i0, k);                                    // factor.cpp:45-46

@@ -143,6 +143,10 @@ private:
 #define RL_GEO_MAX_K 512
 #endif
     i32 geo_max_k_ = RL_GEO_MAX_K;  // only nodes whose top half has at most this many rows
+#ifndef RL_BRIDGE
+#define RL_BRIDGE 1
+#endif
+    bool bridge_on_ = RL_BRIDGE != 0;  // leaf pairs: swaps + TRSM + slice update fused (bridge.cu)
 #ifndef RL_LANE_PRIO
 #define RL_LANE_PRIO 1
 #endif

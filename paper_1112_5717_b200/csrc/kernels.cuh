@@ -153,6 +153,27 @@ void trsm_node(const TrsmNodeArgs& a, cudaStream_t s);
 void ninv_assemble(u32* X, i32 ldx, const u32* Xa, i32 la, const u32* Xb, i32 lb, const u32* T2, i32 lt,
                    Dyn a_lo, Dyn b_lo, Dyn b_hi, const i32* rp, i32 nmax, cudaStream_t s);
 
+// The step between the two leaves of a leaf-pair node in ONE launch (bridge.cu,
+// p <= 2^16): the top leaf's transpositions on the bottom rows (if its flag is
+// set), G <- X * U_top^{-1} at the top pivots (written in place) and the window
+// slice [n_lo, n_lo + PW) of the bottom rows updated by -G * U_top.
+struct BridgeArgs {
+    u32* A;
+    i64 lda;
+    i32 row0, M;     // bottom rows [row0, row0 + M), M <= PB
+    Dyn j_lo, j_hi;  // the top leaf's pivots
+    Dyn n_lo;        // slice start
+    i32 N;           // matrix columns
+    const i32* rp;
+    const i32* rrp;
+    const i32* ipiv;
+    const u32* uinv;      // the top leaf's U^{-1} (PB x PB)
+    const i32* swapflag;  // the top leaf's "made a transposition" flag
+    const PanelScratch* ps;  // the top leaf's panel scratch (dead_mask)
+    Fp f;
+};
+void bridge(const BridgeArgs& a, cudaStream_t s);
+
 // ---------------------------------------------------------------- permutation
 // Apply the transpositions T_{j, ipiv[j]} for j in [j_lo, j_hi) in increasing j
 // to rows of A (perm_apply_cols of factor.cpp:42 / :56).  Rows are either the

@@ -27,6 +27,8 @@
 
 namespace rl {
 
+LT_TABLE(window)
+
 namespace {
 
 // row pitch (words) of the staged window: WT = 192 would put every row of a
@@ -511,6 +513,7 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
         for (int e = tid; e < 65536 * 2 / 16; e += blockDim.x) cp_async16(dst + e, src + e);
     }
     pdl_wait();
+    LT_BEGIN();
     const i32 c0 = __ldcg(a.rp + a.i0);
     const i32 W = a.N - c0;
     const int b = a.b;
@@ -826,6 +829,9 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
     }
     }
     RL_STAMP(t_f2);
+#ifdef RL_WIN_DELAY_NS
+    if (threadIdx.x == 0) rl_spin_ns(RL_WIN_DELAY_NS);
+#endif
     for (int e = tid; e < PB; e += blockDim.x) {
         const bool real = e < b;
         ps->piv_of_row[e] = real ? s_por[e] : -1;
@@ -853,6 +859,7 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
             *a.swapflag = moved ? 1 : 0;
         }
     }
+    LT_END(a.i0 / PB);
 #ifdef RL_TRACE
     if (a.i0 == RL_TRACE_I0 && tid == 0) {
         RL_STAMP(t_exit);
