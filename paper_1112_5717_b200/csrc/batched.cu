@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(256) cup_batched_kernel(u32* A, i64 stride, i3
 constexpr int PR = 32;
 constexpr int BN = 256;
 #ifndef RL_BATCHED_DMMA
-#define RL_BATCHED_DMMA 1  // trailing updates on the FP64 tensor cores (m8n8k4 DMMA)
+#define RL_BATCHED_DMMA 2  // trailing updates on the FP64 tensor cores (m8n8k4 DMMA); 2: trailing_dmma
 #endif
 #ifndef BATCHED_ROWS_PER_WARP
 #define BATCHED_ROWS_PER_WARP 1  // trailing rows per warp (more share the U loads, cost registers)
@@ -114,6 +114,175 @@ template <bool LAZY>
 __device__ __forceinline__ u64 lazy_fma(u64 acc, u32 nf, u32 u, const Fp& f) {
     if (LAZY) return acc + (u64)nf * u;
     return addmod((u32)acc, mulmod(nf, u, f), f);
+}
+
+// x mod p for an integer-valued double 0 <= x < 2^52
+__device__ __forceinline__ double dmod(double x, double pd, double ipd) {
+    double r = fma(-floor(x * ipd), pd, x);
+    r = r < 0.0 ? r + pd : r;
+    return r >= pd ? r - pd : r;
+}
+__device__ __forceinline__ void dmma844(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+constexpr int XDS = 40;   // Xd row stride (doubles): rows 4 apart in banks -> 2 wavefronts per fragment load
+constexpr int UDS = 232;  // Ud row stride (doubles), >= BN - PR, = 8 (mod 16)
+
+// The trailing rows of one panel (p < 2^24, no transposition in the panel), all
+// products on the FP64 tensor cores (mma.sync m8n8k4): with U_pp the panel's
+// unit upper pivot block (np x np) and U_rest its U rows right of it,
+//   F = X_piv * U_pp^{-1}         (the C entries, the multipliers' negatives)
+//   X_rest <- X_rest - F * U_rest
+// -- the unique solution of the pivot-by-pivot elimination, so the bytes are
+// the reference's.  Every term is an integer < 2^46 and a sum has at most
+// 32 + 1 of them (< 2^52): exact in double, one reduction per output.  Warp =
+// 8 trailing rows at a time: F (4 n8 tiles) by 32 DMMA against U_pp^{-1}, then
+// its negation moves from the accumulator layout to the A-operand layout by
+// shuffles and sweeps the row block's column tiles (C prefetched one tile ahead).
+// smem: Ud = U_rest as doubles [PR][UDS], Xd = U_pp^{-1} as doubles [PR][XDS].
+__device__ __noinline__ void trailing_dmma(u32* a, int m, int n, const Fp& f, int i0, int pr, int r0, int np,
+                                           const i32* s_prow, double* sm) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q4 = lane & 3;
+    const int cend = r0 + np, N = n - cend;
+    const double pd = (double)f.p, ipd = 1.0 / pd;
+    double* Ud = sm;                 // [PR][UDS]
+    double* Xd = sm + PR * UDS;      // [PR][XDS]
+    // (a) U_rest -> Ud; U_pp^{-1} by recursive doubling into Xd (identity past np)
+    for (int e = tid; e < PR * (UDS / 8); e += 256) {
+        const int j = e / (UDS / 8), c0 = (e % (UDS / 8)) * 8;
+        const u32* src = a + (i64)(i0 + (j < np ? s_prow[j] : 0)) * n + cend + c0;
+#pragma unroll
+        for (int z = 0; z < 8; ++z) Ud[j * UDS + c0 + z] = (j < np && c0 + z < N) ? (double)__ldcg(src + z) : 0.0;
+    }
+    {   // diagonal 8 x 8 blocks: thread = (block, column), back substitution
+        const int t = tid;
+        if (t < PR) {
+            const int b = t >> 3, c = t & 7, j = 8 * b + c;
+            double x[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) x[k] = 0.0;
+            x[c] = 1.0;
+            // X[k][j] = -sum_{i=k+1..j} U[k][i] X[i][j]  (U[k][i] = pivot row k at column r0 + i)
+#pragma unroll
+            for (int kk = 7; kk >= 0; --kk) {
+                if (kk < c) {
+                    const int k = 8 * b + kk;
+                    double acc = 0.0;
+#pragma unroll
+                    for (int ii = kk + 1; ii < 8; ++ii) {
+                        if (ii <= c) {
+                            const int i = 8 * b + ii;
+                            const double u = (k < np && i < np)
+                                ? (double)__ldcg(a + (i64)(i0 + s_prow[k]) * n + r0 + i) : 0.0;
+                            acc = fma(u, x[ii], acc);
+                        }
+                    }
+                    const double r = dmod(acc, pd, ipd);
+                    x[kk] = r != 0.0 ? pd - r : 0.0;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < PR; ++k) Xd[k * XDS + j] = (k >> 3) == b ? x[k & 7] : 0.0;
+        }
+    }
+    __syncthreads();
+    // two doubling levels: X_AB = -X_AA * (U_AB * X_BB) for blocks of 8, then 16
+    double* T = sm + PR * UDS + PR * XDS;  // scratch [16][16] (in the Ud tail is not free: own area)
+#pragma unroll
+    for (int h = 8; h <= 16; h *= 2) {
+        // pairs (A = [q*2h, q*2h+h), B = [q*2h+h, q*2h+2h)), entries of T = U_AB * X_BB
+        const int npair = PR / (2 * h);
+        for (int e = tid; e < npair * h * h; e += 256) {
+            const int q = e / (h * h), rr = (e / h) % h, cc = e % h;
+            const int ka = q * 2 * h + rr, jb = q * 2 * h + h + cc;
+            double acc = 0.0;
+            for (int i = 0; i < h; ++i) {
+                const int ib = q * 2 * h + h + i;
+                const double u = (ka < np && ib < np)
+                    ? (double)__ldcg(a + (i64)(i0 + s_prow[ka]) * n + r0 + ib) : 0.0;
+                acc = fma(u, Xd[ib * XDS + jb], acc);
+            }
+            T[(q * h + rr) * 16 + cc] = dmod(acc, pd, ipd);
+        }
+        __syncthreads();
+        for (int e = tid; e < npair * h * h; e += 256) {
+            const int q = e / (h * h), rr = (e / h) % h, cc = e % h;
+            const int ka = q * 2 * h + rr, jb = q * 2 * h + h + cc;
+            double acc = 0.0;
+            for (int i = 0; i < h; ++i) acc = fma(Xd[ka * XDS + q * 2 * h + i], T[(q * h + i) * 16 + cc], acc);
+            const double r = dmod(acc, pd, ipd);
+            Xd[ka * XDS + jb] = r != 0.0 ? pd - r : 0.0;
+        }
+        __syncthreads();
+    }
+    // (b) row blocks of 8 trailing rows per warp
+    const int rbase = i0 + pr;
+    const int R = m - rbase;
+    const int ks_n = (np + 3) >> 2, tN = (N + 7) >> 3;
+    for (int rb = warp; rb * 8 < R; rb += 8) {
+        const int row = rbase + rb * 8 + g;
+        const bool rok = row < m;
+        u32* xr = a + (i64)row * n;
+        // F = X_piv * U_pp^{-1}: four n8 tiles
+        double fa[8];
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+            const int k = 4 * ks + q4;
+            fa[ks] = (rok && k < np) ? (double)__ldcg(xr + r0 + k) : 0.0;
+        }
+        double F[4][2];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            F[t][0] = F[t][1] = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks)
+                if (ks < ks_n) dmma844(F[t][0], F[t][1], fa[ks], Xd[(4 * ks + q4) * XDS + 8 * t + g]);
+        }
+        // raw C entries to the pivot columns; negated multipliers in the A layout
+        u32 nf[4][2];
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int c = 8 * t + 2 * q4 + e;
+                const u32 fv = (u32)dmod(F[t][e], pd, ipd);
+                if (rok && c < np) xr[r0 + c] = fv;
+                nf[t][e] = (c < np && fv) ? f.p - fv : 0u;
+            }
+        double na[8];
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+            const int src = g * 4 + (ks & 1) * 2 + (q4 >> 1);
+            const u32 v0 = __shfl_sync(0xffffffffu, nf[ks >> 1][0], src);
+            const u32 v1 = __shfl_sync(0xffffffffu, nf[ks >> 1][1], src);
+            na[ks] = (double)((q4 & 1) ? v1 : v0);
+        }
+        // sweep the column tiles: C <- C + (p - F) * U_rest
+        u32* cr = xr + cend + 2 * q4;
+        u32 n0 = 0, n1 = 0;
+        if (rok && tN > 0) {
+            n0 = 2 * q4 < N ? __ldcg(cr) : 0u;
+            n1 = 2 * q4 + 1 < N ? __ldcg(cr + 1) : 0u;
+        }
+        for (int tn = 0; tn < tN; ++tn) {
+            const int cc = 8 * tn + 2 * q4;
+            double c0 = (double)n0, c1 = (double)n1;
+            if (tn + 1 < tN && rok) {  // next tile's C in flight during this one's products
+                n0 = cc + 8 < N ? __ldcg(cr + 8 * (tn + 1)) : 0u;
+                n1 = cc + 9 < N ? __ldcg(cr + 8 * (tn + 1) + 1) : 0u;
+            }
+            const double* ub = Ud + q4 * UDS + 8 * tn + g;
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks)
+                if (ks < ks_n) dmma844(c0, c1, na[ks], ub[4 * ks * UDS]);
+            if (rok) {
+                if (cc < N) cr[8 * tn] = (u32)dmod(c0, pd, ipd);
+                if (cc + 1 < N) cr[8 * tn + 1] = (u32)dmod(c1, pd, ipd);
+            }
+        }
+    }
 }
 
 template <bool LAZY>
@@ -214,7 +383,9 @@ __global__ void __launch_bounds__(256) cup_batched_blk_kernel(u32* A, i64 stride
         const int np = r - r0;
         bool any_swap = false;
         for (int j = r0; j < r; ++j) any_swap |= (s_ipiv[j] != j);
-        if (LAZY && np > 0 && !any_swap) {
+        if (LAZY && np > 0 && !any_swap && RL_BATCHED_DMMA == 2) {
+            trailing_dmma(a, m, n, f, i0, pr, r0, np, s_prow, reinterpret_cast<double*>(P));
+        } else if (LAZY && np > 0 && !any_swap) {
             // TRSM-then-GEMM form, two rows per warp: the multipliers of a row are
             // f = x_piv * U_pp^{-1} (U_pp = the panel's unit upper pivot block,
             // inverted once per panel), then x_rest -= f * U_rest.  Same values as
