@@ -101,7 +101,10 @@ __global__ void __launch_bounds__(256) cup_batched_kernel(u32* A, i64 stride, i3
 // reduced exactly when it is read) instead of once per pivot through memory.
 // Lazy sums hold < 2^52 for p < 2^24 (at most 32 products < 2^46 per panel);
 // larger p reduce every product.
-constexpr int PR = 32;
+#ifndef RL_BATCHED_PR
+#define RL_BATCHED_PR 32
+#endif
+constexpr int PR = RL_BATCHED_PR;  // panel rows (16 or 32)
 constexpr int BN = 256;
 #ifndef RL_BATCHED_DMMA
 #define RL_BATCHED_DMMA 2  // trailing updates on the FP64 tensor cores (m8n8k4 DMMA); 2: trailing_dmma
@@ -128,7 +131,7 @@ __device__ __forceinline__ void dmma844(double& c0, double& c1, double a, double
                  : "d"(a), "d"(b));
 }
 constexpr int XDS = 40;   // Xd row stride (doubles): rows 4 apart in banks -> 2 wavefronts per fragment load
-constexpr int UDS = 232;  // Ud row stride (doubles), >= BN - PR, = 8 (mod 16)
+constexpr int UDS = BN - PR + 8;  // Ud row stride (doubles), >= BN - PR, = 8 (mod 16)
 
 // The trailing rows of one panel (p < 2^24, no transposition in the panel), all
 // products on the FP64 tensor cores (mma.sync m8n8k4): with U_pp the panel's
@@ -191,7 +194,7 @@ __device__ __noinline__ void trailing_dmma(u32* a, int m, int n, const Fp& f, in
     // two doubling levels: X_AB = -X_AA * (U_AB * X_BB) for blocks of 8, then 16
     double* T = sm + PR * UDS + PR * XDS;  // scratch [16][16] (in the Ud tail is not free: own area)
 #pragma unroll
-    for (int h = 8; h <= 16; h *= 2) {
+    for (int h = 8; h <= PR / 2; h *= 2) {
         // pairs (A = [q*2h, q*2h+h), B = [q*2h+h, q*2h+2h)), entries of T = U_AB * X_BB
         const int npair = PR / (2 * h);
         for (int e = tid; e < npair * h * h; e += 256) {
@@ -226,24 +229,25 @@ __device__ __noinline__ void trailing_dmma(u32* a, int m, int n, const Fp& f, in
         const bool rok = row < m;
         u32* xr = a + (i64)row * n;
         // F = X_piv * U_pp^{-1}: four n8 tiles
-        double fa[8];
+        constexpr int KS = PR / 4, FT = PR / 8;
+        double fa[KS];
 #pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {
+        for (int ks = 0; ks < KS; ++ks) {
             const int k = 4 * ks + q4;
             fa[ks] = (rok && k < np) ? (double)__ldcg(xr + r0 + k) : 0.0;
         }
-        double F[4][2];
+        double F[FT][2];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
+        for (int t = 0; t < FT; ++t) {
             F[t][0] = F[t][1] = 0.0;
 #pragma unroll
-            for (int ks = 0; ks < 8; ++ks)
+            for (int ks = 0; ks < KS; ++ks)
                 if (ks < ks_n) dmma844(F[t][0], F[t][1], fa[ks], Xd[(4 * ks + q4) * XDS + 8 * t + g]);
         }
         // raw C entries to the pivot columns; negated multipliers in the A layout
-        u32 nf[4][2];
+        u32 nf[FT][2];
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
+        for (int t = 0; t < FT; ++t)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int c = 8 * t + 2 * q4 + e;
@@ -251,9 +255,9 @@ __device__ __noinline__ void trailing_dmma(u32* a, int m, int n, const Fp& f, in
                 if (rok && c < np) xr[r0 + c] = fv;
                 nf[t][e] = (c < np && fv) ? f.p - fv : 0u;
             }
-        double na[8];
+        double na[KS];
 #pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {
+        for (int ks = 0; ks < KS; ++ks) {
             const int src = g * 4 + (ks & 1) * 2 + (q4 >> 1);
             const u32 v0 = __shfl_sync(0xffffffffu, nf[ks >> 1][0], src);
             const u32 v1 = __shfl_sync(0xffffffffu, nf[ks >> 1][1], src);
@@ -275,7 +279,7 @@ __device__ __noinline__ void trailing_dmma(u32* a, int m, int n, const Fp& f, in
             }
             const double* ub = Ud + q4 * UDS + 8 * tn + g;
 #pragma unroll
-            for (int ks = 0; ks < 8; ++ks)
+            for (int ks = 0; ks < KS; ++ks)
                 if (ks < ks_n) dmma844(c0, c1, na[ks], ub[4 * ks * UDS]);
             if (rok) {
                 if (cc < N) cr[8 * tn] = (u32)dmod(c0, pd, ipd);
@@ -383,6 +387,7 @@ __global__ void __launch_bounds__(256) cup_batched_blk_kernel(u32* A, i64 stride
         const int np = r - r0;
         bool any_swap = false;
         for (int j = r0; j < r; ++j) any_swap |= (s_ipiv[j] != j);
+        static_assert(RL_BATCHED_DMMA == 2 || PR == 32, "the pre-v2 trailing paths assume 32-row panels");
         if (LAZY && np > 0 && !any_swap && RL_BATCHED_DMMA == 2) {
             trailing_dmma(a, m, n, f, i0, pr, r0, np, s_prow, reinterpret_cast<double*>(P));
         } else if (LAZY && np > 0 && !any_swap) {
