@@ -93,6 +93,9 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
         if (l.a2_cap) RL_CUDA_CHECK(cudaMalloc(&l.a2, l.a2_cap));
         if (l.b2_cap) RL_CUDA_CHECK(cudaMalloc(&l.b2, l.b2_cap));
     }
+    for (auto& kv : early_)
+        if (kv.second.cap) RL_CUDA_CHECK(cudaMalloc(&kv.second.buf, kv.second.cap));
+    if (!early_.empty()) RL_CUDA_CHECK(cudaStreamCreateWithPriority(&sb_, cudaStreamNonBlocking, prio_hi));
     if (!big_slot_.empty()) {
         RL_CUDA_CHECK(cudaMalloc(&big_, sizeof(u32) * BIG_LD * BIG_LD * big_slot_.size()));
         RL_CUDA_CHECK(cudaMalloc(&big_tmp_, sizeof(u32) * (4 * NINV_LD * NINV_LD + 4 * CH_LD * CH_LD)));
@@ -123,6 +126,8 @@ CupEngine::~CupEngine() {
     cudaFree(inv_lane_.b2);
     cudaFree(big_);
     cudaFree(big_tmp_);
+    for (auto& kv : early_) cudaFree(kv.second.buf);
+    if (sb_) cudaStreamDestroy(sb_);
 }
 
 cudaEvent_t CupEngine::fork_to(cudaStream_t from, cudaStream_t to) {
@@ -134,13 +139,14 @@ cudaEvent_t CupEngine::fork_to(cudaStream_t from, cudaStream_t to) {
 }
 
 void CupEngine::gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nmax, cudaStream_t st,
-                     i32 n_cap) {
+                     i32 n_cap, const EarlyPack* ep) {
     if (!st) st = work_stream();
     // K = pivots of rows [x0, x1) = [rp[x0], rp[x1]); split along the skeleton
     // while the s32 exactness bound could be exceeded.
     const i64 Kmax = x1 - x0;
     if (Kmax <= 0 || M <= 0 || Nmax <= 0) return;
     if (Kmax > tc_kmax(L_)) {
+        if (ep) throw Error(7 /*RL_EINVAL*/, "early B pack of a K-split GEMM");
         const i32 xm = x0 + (x1 - x0) / 2;
         gemm(row0, M, x0, xm, n_lo, n_hi, Nmax, st, n_cap);
         gemm(row0, M, xm, x1, n_lo, n_hi, Nmax, st, n_cap);
@@ -196,7 +202,12 @@ void CupEngine::gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nm
     }
     if (st == s_) flush_swaps();
     ++stats_.gemms;
-    if (tc) {
+    if (tc && ep && ep->buf) {  // B packed earlier on sb_
+        ++stats_.tc_gemms;
+        stats_.launches += 2;
+        RL_CUDA_CHECK(cudaStreamWaitEvent(st, ep->ev, 0));
+        gemm_tc_split(g, L_, Kmax, Nmax, ln ? ln->a2 : a2_, ep->buf, st, 3);
+    } else if (tc) {
         ++stats_.tc_gemms;
         stats_.launches += 2;
         gemm_tc(g, L_, Kmax, Nmax, ln ? ln->a2 : a2_, ln ? ln->b2 : b2_, st);
@@ -433,6 +444,45 @@ void CupEngine::trsm_right(i32 r0, i32 M, i32 x0, i32 mx) {
     trsm_right(r0, M, x0 + kx, mx - kx);
 }
 
+// The limb image of the Schur update's B operand (the U rows of node (i0, mm)'s
+// top half [i0, i0 + k), gathered through rrp, at columns [rp[i0 + k], n)) on
+// sb_, right after the top half is factored: the GEMMs that read it (the
+// critical one and the row-split lane's) then pack only their A operand.
+// Same GemmArgs fields as gemm() builds for them, so the same image.
+CupEngine::EarlyPack CupEngine::early_pack_b(i32 i0, i32 k, i32 mm) {
+    EarlyPack ep{};
+    const i32 b0 = i0 + k;
+    EarlyBuf& eb = early_[mm];
+    if (dry_) {
+        eb.cap = std::max(eb.cap, tc_b2_bytes(L_, n_, k));
+        events_needed_ += 2;
+        return ep;
+    }
+    GemmArgs g{};
+    g.A = A_;
+    g.lda = lda_;
+    g.B = A_;
+    g.ldb = lda_;
+    g.gather = rrp_;
+    g.C = A_;
+    g.ldc = lda_;
+    g.M = 1;
+    g.k_lo = dyn_rp(i0);
+    g.k_hi = dyn_rp(b0);
+    g.n_lo = dyn_rp(b0);
+    g.n_hi = dyn_c(n_);
+    g.rp = rp_;
+    g.f = f_;
+    fork_to(s_, sb_);  // the top half's U rows are final (its swaps flushed)
+    gemm_tc_split(g, L_, k, n_, nullptr, eb.buf, sb_, 4);
+    stats_.launches += 1;
+    ep.buf = eb.buf;
+    ep.ev = events_.at(next_event_++);
+    RL_CUDA_CHECK(cudaEventRecord(ep.ev, sb_));
+    early_used_ = true;
+    return ep;
+}
+
 void CupEngine::node(i32 i0, i32 mm) {
     if (mm <= PB) {
         panel(i0, mm);
@@ -460,10 +510,22 @@ void CupEngine::node(i32 i0, i32 mm) {
     }
     const i32 b0 = i0 + k, bm = mm - k;
     trsm_end_ = b0;  // the TRSMs of this node solve against rows [i0, b0)
+    // the wide Schur update (k > split_max_k_, tensor cores, one K chunk): its
+    // B operand is packed now, beside the TRSM
+    EarlyPack ep{};
+    if (early_b_on_ && use_tc_ && !geo_split_ && k > split_max_k_ && k > PB && k <= tc_kmax(L_) && bm >= 64 &&
+        n_ - k >= 64)
+        ep = early_pack_b(i0, k, mm);
+    const EarlyPack* epp = (ep.buf || dry_) ? &ep : nullptr;
     // a leaf pair (top = one leaf, p <= 2^16): swaps, TRSM and the window slice's
     // update in one launch (bridge.cu)
     const bool br = bridge_on_ && k <= PB && bm <= PB && p_ <= 65536u && use_tc_;
-    if (!br) swaps_range(b0, bm, dyn_rp(i0), dyn_rp(b0), i0, b0);   // factor.cpp:42
+    if (!br) {
+        swaps_range(b0, bm, dyn_rp(i0), dyn_rp(b0), i0, b0);   // factor.cpp:42
+        // launched now, so it runs beside the last leaf's U^{-1} (joined below)
+        // instead of after it on the critical path
+        flush_swaps();
+    }
     if (!dry_ && uinv_join_) {
         RL_CUDA_CHECK(cudaStreamWaitEvent(s_, uinv_join_, 0));
         uinv_join_ = nullptr;
@@ -518,7 +580,7 @@ void CupEngine::node(i32 i0, i32 mm) {
         // joined in node(b0, bm) after its top half (rows [b0, b0 + h)) is factored
         const i32 h = bm / 2;
         trsm_right(b0, h, i0, k);                                     // factor.cpp:45-46
-        gemm(b0, h, i0, b0, dyn_rp(b0), dyn_c(n_), n_);
+        gemm(b0, h, i0, b0, dyn_rp(b0), dyn_c(n_), n_, nullptr, 0, epp);
         Lane& ln = lanes_[bm];
         if (dry_) {
             events_needed_ += 2;
@@ -527,7 +589,7 @@ void CupEngine::node(i32 i0, i32 mm) {
         }
         lane_ = &ln;
         trsm_right(b0 + h, bm - h, i0, k);
-        gemm(b0 + h, bm - h, i0, b0, dyn_rp(b0), dyn_c(n_), n_);
+        gemm(b0 + h, bm - h, i0, b0, dyn_rp(b0), dyn_c(n_), n_, nullptr, 0, epp);
         lane_ = nullptr;
         if (!dry_) {
             cudaEvent_t e = events_.at(next_event_++);
@@ -568,7 +630,7 @@ void CupEngine::node(i32 i0, i32 mm) {
         }
     } else if (k > split_max_k_) {
         trsm_right(b0, bm, i0, k);                                    // factor.cpp:45-46
-        gemm(b0, bm, i0, b0, dyn_rp(b0), dyn_c(n_), n_);
+        gemm(b0, bm, i0, b0, dyn_rp(b0), dyn_c(n_), n_, nullptr, 0, epp);
     } else {
         trsm_right(b0, bm, i0, k);                                    // factor.cpp:45-46
         gemm(b0, bm, i0, b0, dyn_rp(b0), Dyn{b0, PW}, std::min<i64>(PW, n_), s_, n_);
@@ -708,6 +770,7 @@ void CupEngine::enqueue(u32* dA, cudaStream_t s) {
     row_joins_.clear();
     big_ready_.clear();
     lane_ = nullptr;
+    early_used_ = false;
     fill_rp0(rp_, s);
     if (m_ > 0 && n_ > 0) {
         node(0, m_);
@@ -716,6 +779,7 @@ void CupEngine::enqueue(u32* dA, cudaStream_t s) {
         if (m_ > PB && split_max_k_ >= PB) fork_to(s2_, s_);  // s2_ joined the capture at a split
         fork_to(s3_, s_);
         if (!big_ready_.empty()) fork_to(inv_lane_.st, s_);  // the last builds rejoin the capture
+        if (early_used_) fork_to(sb_, s_);
         flush_swaps();
         compact_u_rows(A_, lda_, m_, n_, rp_, rrp_, s);
         stats_.launches += 1;

@@ -65,8 +65,14 @@ private:
     void gemm_dense(const u32* A, i64 lda, bool a_dense, const u32* B, i64 ldb, bool b_dense, const i32* gather,
                     u32* C, i64 ldc, i32 M, Dyn k_lo, Dyn k_hi, Dyn n_lo, Dyn n_hi, i64 Kmax, i64 Nmax, u32 alpha,
                     cudaStream_t st);
+    // a B operand packed ahead of its GEMM (early_pack_b) and its ready event
+    struct EarlyPack {
+        uint8_t* buf = nullptr;
+        cudaEvent_t ev = nullptr;
+    };
     void gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nmax, cudaStream_t st = nullptr,
-              i32 n_cap = 0);
+              i32 n_cap = 0, const EarlyPack* ep = nullptr);
+    EarlyPack early_pack_b(i32 i0, i32 k, i32 mm);
     cudaEvent_t fork_to(cudaStream_t from, cudaStream_t to);  // `to` waits for `from`'s work so far
     // the transpositions are the pivots of rows [piv_lo, piv_hi) (whole leaves)
     void swaps_range(i32 row0, i32 M, Dyn j_lo, Dyn j_hi, i32 piv_lo, i32 piv_hi);
@@ -182,6 +188,23 @@ private:
     u32* big_ = nullptr;                                   // BIG_LD x BIG_LD per slot
     u32* big_tmp_ = nullptr;                               // 4 x 256^2 + 4 x 512^2 scratch
     Lane inv_lane_;                                        // stream + GEMM workspace of the builds
+    // Early B packs.  The Schur update of a node whose top half has more than
+    // split_max_k_ rows reads the top half's U rows as B; they are final once
+    // the top half is factored, so their limb image is packed on a side stream
+    // right then, beside the TRSM, instead of on the critical path after it
+    // (and once for the critical and the row-split lane GEMM together).  One
+    // workspace per node height: all GEMMs of a node finish inside the node.
+#ifndef RL_EARLY_B
+#define RL_EARLY_B 1
+#endif
+    bool early_b_on_ = RL_EARLY_B != 0;
+    struct EarlyBuf {
+        uint8_t* buf = nullptr;
+        size_t cap = 0;
+    };
+    std::map<i32, EarlyBuf> early_;              // node height -> B image workspace
+    cudaStream_t sb_ = nullptr;                  // the B-pack stream
+    bool early_used_ = false;                    // during one enqueue
     cudaGraphExec_t graph_exec_ = nullptr;
     u32* graph_A_ = nullptr;
     cudaEvent_t done_ = nullptr;  // end of the last run: the destructor waits for it

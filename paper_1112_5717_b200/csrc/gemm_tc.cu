@@ -540,15 +540,17 @@ void launch_tc(const GemmArgs& g, i64 Kmax, i64 Nmax, uint8_t* a2, uint8_t* b2, 
     u32 sc[4] = {1, 0, 0, 0};
     for (int i = 1; i < 4; ++i) sc[i] = (u32)(((u64)sc[i - 1] << 8) % g.f.p);
     const int grid = (int)std::max<i64>(1, std::min<i64>(MB * NB, g.max_ctas > 0 ? g.max_ctas : nsm));
+    // phases: 0 pack A and B, 1 GEMM only, 2 pack A and B + GEMM,
+    // 3 pack A + GEMM (B packed earlier), 4 pack B only
     if (phase != 1) {
         const i64 awork = MB * KB * BM * 8;
-        const int ga = (int)std::max<i64>(1, std::min<i64>((awork + 255) / 256, (i64)nsm * 8));
-        const int gb = (int)std::max<i64>(1, std::min<i64>(KB * 4 * NB, (i64)nsm * 8));
+        const int ga = phase == 4 ? 0 : (int)std::max<i64>(1, std::min<i64>((awork + 255) / 256, (i64)nsm * 8));
+        const int gb = phase == 3 ? 0 : (int)std::max<i64>(1, std::min<i64>(KB * 4 * NB, (i64)nsm * 8));
         RL_ONCE_MAX_SMEM(pack_kernel<L>);
         launch_pdl(pack_kernel<L>, dim3(ga + gb), dim3(256), 0, s, g, a2, b2, sc[1], sc[2], sc[3], ga);
         RL_CUDA_CHECK(cudaGetLastError());
     }
-    if (phase == 0) return;
+    if (phase == 0 || phase == 4) return;
     static std::atomic<unsigned long long> attr_once{0};
     once_on_device(attr_once, [&] {
         RL_CUDA_CHECK(cudaFuncSetAttribute(gemm_tc_kernel<L>,

@@ -5,10 +5,12 @@
 // transpositions T_{j, ipiv[j]} recorded by the pivot rule (perm.cpp:21-26,
 // factor.cpp:23-24), in increasing j.  A job whose leaves made no
 // transposition (per-leaf flags written by the panel kernels) returns at once;
-// otherwise each chunk of 256 positions is composed into one gather map and
-// applied by one warp per row (coalesced loads/stores of the moved positions).  The shift of factor.cpp:62-70, composed over the whole
+// otherwise each chunk of 256 positions is composed into one gather map (in
+// parallel, far targets included) and applied by one warp per row (all loads of
+// the moved positions in flight together, then all stores).  The shift of factor.cpp:62-70, composed over the whole
 // recursion, is one pass at the end (compact_kernel): per column, increasing j.
 #include <algorithm>
+#include <climits>
 
 #include "kernels.cuh"
 #include "runtime.h"
@@ -53,11 +55,45 @@ __device__ __forceinline__ int collect_flag(bool take, int* warp_cnt) {
 }
 
 // One swap job: the ordered transpositions [j_lo, j_hi) on one set of rows.
-__device__ __forceinline__ void swap_job(const SwapArgs& a, i32* list, int* warp_cnt) {
+//
+// The transpositions of one chunk of (up to 256) consecutive positions j are
+// composed ONCE per CTA into a gather map over SLOTS: slot u < SW is position
+// j0 + u (the dense window the chunk's own positions and its near targets fall
+// in), slots SW + i are the distinct far targets ipiv[j] >= j0 + SW (sorted).
+// After the chunk, slot u holds the value that was at slot src[u] (laswp order:
+// increasing j, each T_{j, ipiv[j]} with ipiv[j] >= j).  The map is built in
+// parallel: every touched slot walks the chunk's transpositions backwards
+// (cur <- the other end of each transposition that touches cur), so no thread
+// runs a serial chain of dependent shared-memory swaps.  Then one WARP per row
+// moves only the positions the chunk changes: every value is read before any
+// is written, the loads and stores of a row are issued together by 32 lanes
+// (independent, in flight at once) instead of one thread walking the swaps of
+// its row one dependent pair at a time.
+constexpr int NFAR = 256;          // far slots: at most one per transposition
+constexpr int NSLOT = SW + NFAR;
+constexpr int MV_PER_LANE = NSLOT / 32;
+
+struct SwapSmem {
+    i32 list[256];      // positions j of the chunk with ipiv[j] != j, increasing
+    int2 tr[256];       // their transpositions as (slot of j, slot of ipiv[j])
+    i32 farv[256];      // per transposition: its far target (INT_MAX if near)
+    i32 ffv[256];       // the same at the first occurrence of each value only
+    i32 farpos[NFAR];   // distinct far targets, increasing (slot SW + i)
+    i32 src[NSLOT];     // composed gather map (slots)
+    i32 mov[NSLOT];     // slots whose value changes, compacted
+    int warp_cnt[8];
+    int nfar, nmov;
+};
+
+__device__ __forceinline__ i32 slot_pos(const SwapSmem& S, i32 j0, i32 u) {
+    return u < SW ? j0 + u : S.farpos[u - SW];
+}
+
+__device__ __forceinline__ void swap_job(const SwapArgs& a, SwapSmem& S) {
+    const int tid = threadIdx.x;
     if (a.leafflags) {  // no leaf of this job made a transposition: nothing to do
         int any = 0;
-        for (i32 l = a.leaf_lo + (i32)threadIdx.x; l < a.leaf_hi; l += blockDim.x)
-            any |= __ldcg(a.leafflags + l);
+        for (i32 l = a.leaf_lo + (i32)tid; l < a.leaf_hi; l += blockDim.x) any |= __ldcg(a.leafflags + l);
         if (!__syncthreads_or(any)) return;  // uniform
     }
     const i32 j_lo = dyn_eval(a.j_lo, a.rp), j_hi = dyn_eval(a.j_hi, a.rp);
@@ -70,80 +106,65 @@ __device__ __forceinline__ void swap_job(const SwapArgs& a, i32* list, int* warp
         M = a.M;
     }
     if (M <= 0) return;  // uniform
-    // The transpositions of one chunk of (up to 256) consecutive positions are
-    // composed ONCE per CTA into a gather map over a dense window of positions
-    // [j0, j0 + SW): after the chunk, position j0 + u holds the value that was at
-    // j0 + src[u] (laswp order: increasing j, each T_{j, ipiv[j]} with ipiv[j] >= j).
-    // Then one WARP per row moves only the positions the chunk changes: loads
-    // and stores of a row are issued together by 32 lanes (coalesced within the
-    // window) instead of one thread walking the swaps of its row one dependent
-    // pair at a time.  A chunk whose targets leave the window (a pivot found far
-    // to the right) takes the per-row sequential walk.
-    __shared__ i32 s_src[SW];
-    __shared__ i32 s_mov[SW];
-    __shared__ int s_far, s_nmov;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+    const int warp = tid >> 5, lane = tid & 31, nwarp = blockDim.x >> 5;
     for (i32 j0 = j_lo; j0 < j_hi; j0 += 256) {
         const i32* ip = a.ipiv;
         const int cnt = collect_ordered(
-            j0, min(j_hi, j0 + 256), [ip](i32 j) { return __ldcg(ip + j) != j; }, list, warp_cnt);
+            j0, min(j_hi, j0 + 256), [ip](i32 j) { return __ldcg(ip + j) != j; }, S.list, S.warp_cnt);
         if (!cnt) continue;  // uniform (collect_ordered ends with a barrier)
-        for (int u = threadIdx.x; u < SW; u += blockDim.x) s_src[u] = u;
-        if (threadIdx.x == 0) s_far = 0;
+        // far targets: distinct values, ranked
+        const i32 y = tid < cnt ? __ldcg(ip + S.list[tid]) : 0;
+        const bool far = tid < cnt && y >= j0 + SW;
+        S.farv[tid] = far ? y : INT_MAX;
+        for (int u = tid; u < NSLOT; u += blockDim.x) S.src[u] = u;
         __syncthreads();
-        if (threadIdx.x < cnt && __ldcg(ip + list[threadIdx.x]) >= j0 + SW) s_far = 1;
+        bool first = far;  // first occurrence of its value
+        if (far)
+            for (int q = 0; q < tid; ++q) first &= S.farv[q] != y;
+        S.ffv[tid] = first ? y : INT_MAX;
+        const int nfar = __syncthreads_count(first);
+        int rk = 0;  // distinct far targets below y
+        if (far)
+            for (int q = 0; q < cnt; ++q) rk += S.ffv[q] < y ? 1 : 0;
+        if (first) S.farpos[rk] = y;
+        if (tid < cnt) S.tr[tid] = make_int2(S.list[tid] - j0, far ? SW + rk : y - j0);
         __syncthreads();
-        if (!s_far) {
-            if (threadIdx.x == 0) {  // compose in order (positions are window-relative)
-                for (int q = 0; q < cnt; ++q) {
-                    const int x = list[q] - j0, y = __ldcg(ip + list[q]) - j0;
-                    const i32 t = s_src[x];
-                    s_src[x] = s_src[y];
-                    s_src[y] = t;
-                }
+        // composed map, in parallel: slot u's final value came from the slot
+        // reached by walking the transpositions backwards from u
+        for (int u = tid; u < SW + nfar; u += blockDim.x) {
+            i32 cur = u;
+            for (int q = cnt - 1; q >= 0; --q) {
+                const int2 t = S.tr[q];
+                cur = cur == t.x ? t.y : (cur == t.y ? t.x : cur);
             }
-            __syncthreads();
-            // the positions that change, compacted
-            int nm = 0;
-            for (int u0 = 0; u0 < SW; u0 += blockDim.x) {
-                const int u = u0 + threadIdx.x;
-                const bool mv = u < SW && s_src[u] != u;
-                const int k = collect_flag(mv, warp_cnt);
-                if (mv) s_mov[nm + k] = u;
-                nm += __syncthreads_count(mv);
-            }
-            if (threadIdx.x == 0) s_nmov = nm;
-            __syncthreads();
-            const int nmov = s_nmov;
-            for (i32 t = blockIdx.x * nwarp + warp; t < M; t += gridDim.x * nwarp) {
-                const i32 row = a.gather ? __ldcg(a.gather + g_lo + t) : a.row0 + t;
-                u32* rr = a.A + (i64)row * a.lda + j0;
-                // every value of the window is read before any is written
-                u32 v[SW / 32];
+            S.src[u] = cur;
+        }
+        __syncthreads();
+        // the slots that change, compacted
+        int nm = 0;
+        for (int u0 = 0; u0 < SW + nfar; u0 += blockDim.x) {
+            const int u = u0 + tid;
+            const bool mv = u < SW + nfar && S.src[u] != u;
+            const int k = collect_flag(mv, S.warp_cnt);
+            if (mv) S.mov[nm + k] = u;
+            nm += __syncthreads_count(mv);
+        }
+        const int nmov = nm;
+        for (i32 t = blockIdx.x * nwarp + warp; t < M; t += gridDim.x * nwarp) {
+            const i32 row = a.gather ? __ldcg(a.gather + g_lo + t) : a.row0 + t;
+            u32* rr = a.A + (i64)row * a.lda;
+            // every value of the row's moved slots is read before any is written
+            u32 v[MV_PER_LANE];
 #pragma unroll
-                for (int q = 0; q < SW / 32; ++q) {
-                    const int k = lane + 32 * q;
-                    if (k < nmov) v[q] = rr[s_src[s_mov[k]]];
-                }
-                __syncwarp();
-#pragma unroll
-                for (int q = 0; q < SW / 32; ++q) {
-                    const int k = lane + 32 * q;
-                    if (k < nmov) rr[s_mov[k]] = v[q];
-                }
+            for (int q = 0; q < MV_PER_LANE; ++q) {
+                const int k = lane + 32 * q;
+                if (k < nmov) v[q] = rr[slot_pos(S, j0, S.src[S.mov[k]])];
             }
-        } else {
-            const i32 row_t = blockIdx.x * blockDim.x + threadIdx.x;
-            for (i32 t = row_t; t < M; t += gridDim.x * blockDim.x) {
-                const i32 row = a.gather ? __ldcg(a.gather + g_lo + t) : a.row0 + t;
-                u32* rr = a.A + (i64)row * a.lda;
-                for (int q = 0; q < cnt; ++q) {
-                    const i32 j = list[q];
-                    const i32 c = __ldcg(ip + j);
-                    const u32 tmp = rr[j];
-                    rr[j] = rr[c];
-                    rr[c] = tmp;
-                }
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < MV_PER_LANE; ++q) {
+                const int k = lane + 32 * q;
+                if (k < nmov) rr[slot_pos(S, j0, S.mov[k])] = v[q];
             }
         }
         __syncthreads();
@@ -152,13 +173,12 @@ __device__ __forceinline__ void swap_job(const SwapArgs& a, i32* list, int* warp
 
 // Consecutive swap jobs of the recursion touch disjoint row sets (the top
 // halves of nested nodes, then a bottom half), so one launch runs them all;
-// within a job every row is owned by one thread, which keeps the order.
+// within a job every row is owned by one warp, which keeps the order.
 __global__ void __launch_bounds__(256) swaps_kernel(SwapJobs jobs) {
-    __shared__ i32 list[256];
-    __shared__ int warp_cnt[8];
+    __shared__ SwapSmem S;
     pdl_wait();
     pdl_trigger();
-    for (int q = 0; q < jobs.n; ++q) swap_job(jobs.job[q], list, warp_cnt);
+    for (int q = 0; q < jobs.n; ++q) swap_job(jobs.job[q], S);
 }
 
 // One CTA per 32-column block.  The moves "row j <- row rrp[j] on columns > j,
