@@ -513,10 +513,12 @@ void CupEngine::node(i32 i0, i32 mm) {
     // the wide Schur update (k > split_max_k_, tensor cores, one K chunk): its
     // B operand is packed now, beside the TRSM
     EarlyPack ep{};
-    if (early_b_on_ && use_tc_ && !geo_split_ && k > split_max_k_ && k > PB && k <= tc_kmax(L_) && bm >= 64 &&
-        n_ - k >= 64)
-        ep = early_pack_b(i0, k, mm);
-    const EarlyPack* epp = (ep.buf || dry_) ? &ep : nullptr;
+    const bool early = early_b_on_ && use_tc_ && !geo_split_ && k > split_max_k_ && k > PB &&
+                       k <= tc_kmax(L_) && bm >= 64 && n_ - k >= 64;
+    if (early) ep = early_pack_b(i0, k, mm);
+    // (dry run: ep.buf is null but the GEMM sizing must see the early pack too;
+    // a K-split GEMM never gets one)
+    const EarlyPack* epp = early && (ep.buf || dry_) ? &ep : nullptr;
     // a leaf pair (top = one leaf, p <= 2^16): swaps, TRSM and the window slice's
     // update in one launch (bridge.cu)
     const bool br = bridge_on_ && k <= PB && bm <= PB && p_ <= 65536u && use_tc_;
