@@ -29,7 +29,16 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
     L_ = limbs_for(p);
     // dry run to size the GEMM workspaces
     dry_ = true;
-    if (m_ > 0 && n_ > 0) node(0, m_);
+    // tuning / test knobs of the tiled top level
+    if (const char* e = getenv("RL_TILE_G")) tile_g_ = atoi(e);
+    if (const char* e = getenv("RL_TILE_MIN_M")) tile_min_m_ = atoi(e);
+    if (const char* e = getenv("RL_TILE_MAX_M")) tile_max_m_ = atoi(e);
+    if (tile_g_ > 0) tile_g_ = std::max(PB, tile_g_ / PB * PB);  // whole leaves
+    if (const char* e = getenv("RL_TILE_CTAS")) tile_ctas_ = atoi(e);
+    if (m_ > 0 && n_ > 0) {
+        if (tiled_on()) tiled(tile_g_);
+        else node(0, m_);
+    }
     dry_ = false;
     const i32 k = std::min(m_, n_);
     // All per-factorization metadata (rank prefix, profile, transpositions, panel
@@ -84,7 +93,7 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
         // a short lane's pieces are needed sooner: lanes of height 128, 256, ...
         // get the priorities right below the critical path's, the tall ones the lowest
         int prio = prio_lo;
-        if (lane_prio_) {
+        if (lane_prio_ && kv.first != kTileLane) {
             int lvl = 0;
             for (i32 h = kv.first; h > 2 * PB; h /= 2) ++lvl;
             prio = std::min(prio_lo, prio_hi + 1 + lvl);
@@ -175,7 +184,10 @@ void CupEngine::gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nm
 #ifndef RL_SIDE_FREE_SMS
 #define RL_SIDE_FREE_SMS 1
 #endif
-    g.max_ctas = (st == s_) ? 0 : (ln && lane_ctas_ > 0) ? lane_ctas_ : num_sms() - RL_SIDE_FREE_SMS;
+    g.max_ctas = (st == s_)                           ? 0
+                 : (ln && ln == tile_lane_)            ? tile_ctas_
+                 : (ln && lane_ctas_ > 0)              ? lane_ctas_
+                                                       : num_sms() - RL_SIDE_FREE_SMS;
     g.alpha = p_ - 1;  // C <- C - A*B  (mm(..., neg_one, one), factor.cpp:51)
     g.beta = 1 % p_;
     g.f = f_;
@@ -347,7 +359,7 @@ void CupEngine::gemm_ninv(i32 r0, i32 M, i32 x0, i32 mx, const u32* ninv, i32 ld
     ++stats_.gemms;
     ++stats_.tc_gemms;
     stats_.launches += 2;
-    if (lane_) g.max_ctas = lane_ctas_ > 0 ? lane_ctas_ : num_sms() - 1;
+    if (lane_) g.max_ctas = lane_ == tile_lane_ ? tile_ctas_ : lane_ctas_ > 0 ? lane_ctas_ : num_sms() - 1;
     gemm_tc(g, L_, mx, mx, lane_ ? lane_->a2 : a2_, lane_ ? lane_->b2 : b2_, work_stream());
 }
 
@@ -490,7 +502,7 @@ void CupEngine::node(i32 i0, i32 mm) {
     }
     const i32 k = mm / 2;                    // factor.cpp:35
     node(i0, k);                             // factor.cpp:39
-    if (!dry_ && !dones_.empty()) {  // this node's top half is factored
+    if (!dry_ && !dones_.empty() && !tiling_) {  // this node's top half is factored
         auto it = dones_.find({i0, mm});
         if (it != dones_.end()) {
             flush_swaps();
@@ -760,6 +772,94 @@ void CupEngine::build_big_inverse(i32 x0, i32 mm) {
     }
 }
 
+// Tiled top level.  The reference's recursion (factor.cpp:35-53) updates the
+// bottom half of a node only after its whole top half is factored, so at the
+// upper levels the next leaf waits for a tall TRSM (a chain of dependent
+// GEMMs along the top half's skeleton) and a wide Schur GEMM.  Here the rows
+// are cut into tiles P_0, P_1, ... of g rows; P_j is factored by node() (the
+// recursion, unchanged), then every row below receives P_j's transpositions,
+// its TRSM against U_Pj and its Schur update (right-looking at the tile
+// level).  Only the NEXT tile's rows are updated on the critical path; the
+// rows below it are updated on a side lane beside the next tile's recursion
+// (which leaves most SMs idle: its leaf chain is latency-bound).  The
+// elimination is the same, grouped differently: with the reference's pivot
+// rule the packed [C\U], the row profile and sigma are unique (SURVEY.md 8(c),
+// "iterative formulation"), so the bytes are the recursion's.  The OpCounter
+// is computed from the reference skeleton (cup_opcount), not from this order.
+void CupEngine::tiled(i32 g) {
+    Lane& ln = lanes_[kTileLane];
+    tile_lane_ = &ln;
+    tiling_ = true;  // node() leaves the host-overlap "done" records to this loop
+    if (dry_) events_needed_ += 1;  // the lane's final join (enqueue)
+    cudaEvent_t side = nullptr;  // last side-lane update (rows below the next tile)
+    bool waited_host = false;
+    for (i32 i0 = 0; i0 < m_; i0 += g) {
+        const i32 mm = std::min(g, m_ - i0), a = i0 + mm;
+        node(i0, mm);
+        if (!dry_) {
+            // host-buffer path: the top halves of the right-spine nodes that are
+            // complete now may go back (see set_host_overlap)
+            for (const auto& kv : dones_) {
+                const i32 top_end = kv.first.first + kv.first.second / 2;
+                if (top_end > i0 && top_end <= a) {
+                    flush_swaps();
+                    RL_CUDA_CHECK(cudaEventRecordWithFlags(kv.second, s_, cudaEventRecordExternal));
+                }
+            }
+            // the side lane reads the earlier tiles' U rows and writes the rows below
+            if (side) RL_CUDA_CHECK(cudaStreamWaitEvent(s_, side, 0));
+            side = nullptr;
+        }
+        // P_j's transpositions onto the U rows of the earlier tiles (the V1 swaps
+        // of factor.cpp:56 at the tile level)
+        if (i0 > 0) swaps_gather(dyn_rp(0), dyn_rp(i0), i0, dyn_rp(i0), dyn_rp(a), i0, a);
+        if (a >= m_) break;
+        if (!dry_ && !waited_host) {  // every row below may still be arriving from the host
+            for (const auto& kv : waits_) RL_CUDA_CHECK(cudaStreamWaitEvent(s_, kv.second, cudaEventWaitExternal));
+            waited_host = true;
+        }
+        swaps_range(a, m_ - a, dyn_rp(i0), dyn_rp(a), i0, a);     // factor.cpp:42
+        flush_swaps();
+        if (!dry_ && uinv_join_) {  // the last leaf's U^{-1}
+            RL_CUDA_CHECK(cudaStreamWaitEvent(s_, uinv_join_, 0));
+            uinv_join_ = nullptr;
+        }
+        const i32 g2 = std::min(g, m_ - a);
+        // the next tile: TRSM (factor.cpp:45-46), then the slice its first window
+        // reads, the rest of its columns on s2_ (joined before its first tail)
+        trsm_end_ = a;
+        trsm_right(a, g2, i0, mm);
+        gemm(a, g2, i0, a, dyn_rp(a), Dyn{a, PW}, std::min<i64>(PW, n_), s_, n_);
+        if (dry_) {
+            events_needed_ += 2;
+            gemm(a, g2, i0, a, Dyn{a, PW}, dyn_c(n_), n_, s2_);
+        } else {
+            fork_to(s_, s2_);
+            gemm(a, g2, i0, a, Dyn{a, PW}, dyn_c(n_), n_, s2_);
+            cudaEvent_t e = events_.at(next_event_++);
+            RL_CUDA_CHECK(cudaEventRecord(e, s2_));
+            pending_joins_.push_back(e);
+        }
+        // the rows below the next tile, on the side lane: their TRSM may wait for
+        // P_j's big inverse (built on inv_lane_) and is one GEMM then
+        const i32 b0 = a + g2;
+        if (b0 < m_) {
+            if (dry_) events_needed_ += 2;
+            else fork_to(s_, ln.st);
+            lane_ = &ln;
+            trsm_end_ = a + 1;
+            trsm_right(b0, m_ - b0, i0, mm);
+            gemm(b0, m_ - b0, i0, a, dyn_rp(a), dyn_c(n_), n_);
+            lane_ = nullptr;
+            if (!dry_) {
+                side = events_.at(next_event_++);
+                RL_CUDA_CHECK(cudaEventRecord(side, ln.st));
+            }
+        }
+    }
+    tiling_ = false;
+}
+
 void CupEngine::enqueue(u32* dA, cudaStream_t s) {
     A_ = dA;
     s_ = s;
@@ -775,8 +875,11 @@ void CupEngine::enqueue(u32* dA, cudaStream_t s) {
     early_used_ = false;
     fill_rp0(rp_, s);
     if (m_ > 0 && n_ > 0) {
-        node(0, m_);
+        const bool tl = tiled_on();
+        if (tl) tiled(tile_g_);
+        else node(0, m_);
         for (cudaEvent_t e : pending_joins_) RL_CUDA_CHECK(cudaStreamWaitEvent(s_, e, 0));
+        if (tl && lanes_.count(kTileLane)) fork_to(lanes_.at(kTileLane).st, s_);
         pending_joins_.clear();
         if (m_ > PB && split_max_k_ >= PB) fork_to(s2_, s_);  // s2_ joined the capture at a split
         fork_to(s3_, s_);

@@ -54,6 +54,9 @@ public:
 private:
     void enqueue(u32* dA, cudaStream_t s);
     void node(i32 i0, i32 m);
+    // Tiled top level (right-looking over row tiles of tile_g_ rows, each tile
+    // factored by node()): see cup.cu
+    void tiled(i32 g);
     void panel(i32 i0, i32 b);
     void trsm_right(i32 r0, i32 M, i32 x0, i32 mx);
     void gemm_ninv(i32 r0, i32 M, i32 x0, i32 mx, const u32* ninv, i32 ldn = NINV_LD);
@@ -205,6 +208,26 @@ private:
     std::map<i32, EarlyBuf> early_;              // node height -> B image workspace
     cudaStream_t sb_ = nullptr;                  // the B-pack stream
     bool early_used_ = false;                    // during one enqueue
+    // Tiled top level: matrices with tile_min_m_ <= m <= tile_max_m_ rows are
+    // factored tile by tile (tiles of tile_g_ rows); 0 disables.
+#ifndef RL_TILE_G
+#define RL_TILE_G 1024
+#endif
+#ifndef RL_TILE_MIN_M
+#define RL_TILE_MIN_M 4096
+#endif
+#ifndef RL_TILE_MAX_M
+#define RL_TILE_MAX_M 16384
+#endif
+    i32 tile_g_ = RL_TILE_G, tile_min_m_ = RL_TILE_MIN_M, tile_max_m_ = RL_TILE_MAX_M;
+    bool tiled_on() const { return tile_g_ > 0 && m_ >= tile_min_m_ && m_ <= tile_max_m_ && m_ > tile_g_; }
+    static constexpr i32 kTileLane = -1;         // lanes_ key of the tiles' side lane
+    bool tiling_ = false;                        // inside tiled()
+#ifndef RL_TILE_CTAS
+#define RL_TILE_CTAS 110
+#endif
+    i32 tile_ctas_ = RL_TILE_CTAS;               // persistent GEMM CTAs of the tiles' side lane
+    Lane* tile_lane_ = nullptr;
     cudaGraphExec_t graph_exec_ = nullptr;
     u32* graph_A_ = nullptr;
     cudaEvent_t done_ = nullptr;  // end of the last run: the destructor waits for it

@@ -617,6 +617,7 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
     }
 #endif
     RL_STAMP(t_loaded);
+    LT_MARK(a.i0 / PB, 2);
     const bool spec = spec_lu<SP>(s_R, s_C, s_pv, s_pinvA, S.s_inv, s_M, &s_fail, bl, w, f);
     RL_STAMP(t_lu);
     int r = 0;
@@ -723,10 +724,13 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
 
     // ------------------------------------------------------------ finalize
     RL_STAMP(t_fact);
+    LT_MARK(a.i0 / PB, 3);
     // the tail kernel (a programmatic dependent launch) may start now: it only
     // prefetches columns this kernel does not write on the speculative path,
     // and waits for this grid's completion before reading anything else
+#ifndef RL_WIN_LATE_TRIGGER
     pdl_trigger();
+#endif
     const int rt = r;
     // (the speculative path made no transposition: both loops are identities)
     if (!spec && warp == 1 && lane == 0) {  // window column permutation
@@ -776,6 +780,7 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
 #ifdef RL_TRACE
         t_mid = rl_now();
 #endif
+        LT_MARK(a.i0 / PB, 4);
 #pragma unroll 4
         for (int e = tid; e < PB * PB; e += blockDim.x) {
             const int k = e / PB, i = e % PB;  // original rows
@@ -829,6 +834,7 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
     }
     }
     RL_STAMP(t_f2);
+    LT_MARK(a.i0 / PB, 5);
 #ifdef RL_WIN_DELAY_NS
     if (threadIdx.x == 0) rl_spin_ns(RL_WIN_DELAY_NS);
 #endif
@@ -859,6 +865,9 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
             *a.swapflag = moved ? 1 : 0;
         }
     }
+#ifdef RL_WIN_LATE_TRIGGER
+    pdl_trigger();
+#endif
     LT_END(a.i0 / PB);
 #ifdef RL_TRACE
     if (a.i0 == RL_TRACE_I0 && tid == 0) {

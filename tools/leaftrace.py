@@ -67,6 +67,13 @@ for lvl in sorted(gap):
           f"window avg {sum(d)/len(d)/1e3:5.1f} us")
 print(f"  total: windows {td/1e6:.2f} ms + gaps {tg/1e6:.2f} ms; first window start -> last window end "
       f"{(W[-1][1][1] - t0)/1e6:.2f} ms")
+wph = [v for _, v in W if len(v) > 5 and v[2] and v[3] and v[5]]
+if wph:
+    import statistics
+    names = ("loaded", "LU done", "A written", "Minv written", "exit")
+    cols = (2, 3, 4, 5, 1)
+    print("  window phases (us from its pdl_wait, median over leaves): " + ", ".join(
+        f"{nm} {statistics.median([(v[c] - v[0]) / 1e3 for v in wph if v[c]]):.2f}" for nm, c in zip(names, cols)))
 if "B" in ev:
     bd = [v[1] - v[0] for v in ev["B"].values()]
     print(f"  bridge avg {sum(bd)/len(bd)/1e3:.1f} us")
