@@ -175,6 +175,28 @@ int rl_random_matrix_u32_dev(uint32_t* dA, int64_t m, int64_t n, int64_t lda, ui
 int rl_digest_u32_dev(const uint32_t* dA, int64_t m, int64_t n, int64_t lda, uint64_t* digest,
                       void* stream);
 
+/* Data plane of the distributed CUP (config 5, paper_1112_5717_b200/dist.py),
+ * enqueued on `stream`, no synchronisation.  Not a reference interface: the
+ * reference has no multi-GPU path; these replace the eager tensor ops around
+ * the NCCL collectives.
+ *   pack:   dst (rows x cols, contiguous) <- src (ld lds); wire16 != 0: int16
+ *           words x - 2^15 (p <= 2^16), else uint32.
+ *   unpack: dst[r * ldd + colmap[c] - off] <- src[r * cols + c] (colmap NULL:
+ *           c), undoing the 16-bit offset when wire16.
+ *   select: dst[r * ldd + c] <- src[r * lds + colmap[c] - off], c < cols.
+ *   shift:  for each column l < cols and j < min(rt, gpos[l] - r):
+ *           x[r + j][l] <- x[i0 + j][l], x[i0 + j][l] <- 0, j increasing (the
+ *           U-row move of factor.cpp:62-70 on one rank's columns; gpos[l] is
+ *           column l's global position). */
+int rl_dist_pack_u32_dev(const uint32_t* src, int64_t lds, int64_t rows, int64_t cols, int wire16, void* dst,
+                         void* stream);
+int rl_dist_unpack_u32_dev(const void* src, int64_t rows, int64_t cols, int wire16, uint32_t* dst, int64_t ldd,
+                           const int64_t* colmap, int64_t off, void* stream);
+int rl_dist_select_cols_u32_dev(const uint32_t* src, int64_t lds, int64_t rows, const int64_t* colmap,
+                                int64_t off, int64_t cols, uint32_t* dst, int64_t ldd, void* stream);
+int rl_dist_shift_u_rows_dev(uint32_t* x, int64_t ldx, int64_t cols, int64_t r, int64_t i0, int64_t rt,
+                             const int64_t* gpos, void* stream);
+
 /* Message of the last failing call on this thread ("" if none). */
 const char* rl_last_error(void);
 

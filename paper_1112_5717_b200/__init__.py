@@ -134,7 +134,8 @@ EXPORTS = ["rl_cup_u32", "rl_cup_u32_dev", "rl_cup_batched_u32_dev", "rl_cup_bat
            "rl_profile_gemm_dev", "rl_cup_opcount", "rl_col_ech_trans_u32",
            "rl_col_ech_trans_u32_dev", "rl_invert_u32", "rl_invert_u32_dev", "rl_trsm_u32",
            "rl_trsm_u32_dev", "rl_trsm_opcount", "rl_echelon_opcount", "rl_ple_u32",
-           "rl_ple_u32_dev", "rl_digest_u32_dev"]
+           "rl_ple_u32_dev", "rl_digest_u32_dev", "rl_dist_pack_u32_dev", "rl_dist_unpack_u32_dev",
+           "rl_dist_select_cols_u32_dev", "rl_dist_shift_u_rows_dev"]
 
 
 def lib():
@@ -177,6 +178,10 @@ def lib():
     L.rl_ple_u32.argtypes = [_vp, _i64, _i64, _i64, _u32, C.POINTER(_i64), _vp, _vp, _vp]
     L.rl_ple_u32_dev.argtypes = [_vp, _i64, _i64, _i64, _u32, C.POINTER(_i64), _vp, _vp, _vp, _vp]
     L.rl_digest_u32_dev.argtypes = [_vp, _i64, _i64, _i64, C.POINTER(C.c_uint64), _vp]
+    L.rl_dist_pack_u32_dev.argtypes = [_vp, _i64, _i64, _i64, C.c_int, _vp, _vp]
+    L.rl_dist_unpack_u32_dev.argtypes = [_vp, _i64, _i64, C.c_int, _vp, _i64, _vp, _i64, _vp]
+    L.rl_dist_select_cols_u32_dev.argtypes = [_vp, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _vp]
+    L.rl_dist_shift_u_rows_dev.argtypes = [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp]
     _lib = L
     return L
 
@@ -534,6 +539,49 @@ def digest_dev(d_a, m: int, n: int, lda: int | None = None, stream=None) -> int:
     _check(lib().rl_digest_u32_dev(C.c_void_p(ptr), m, n, n if lda is None else lda, C.byref(h),
                                    _stream_ptr(stream)))
     return h.value
+
+
+# Data plane of the distributed CUP (dist.py): torch CUDA tensors, enqueued on
+# `stream` (torch's current stream when None), no synchronisation.
+def _dp(t) -> C.c_void_p:
+    return C.c_void_p(t.data_ptr())
+
+
+def _cur(stream):
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream()
+    return _stream_ptr(stream)
+
+
+def dist_pack_dev(src, dst, wire16: bool, stream=None) -> None:
+    """dst (rows x cols, contiguous; int16 words x - 2^15 when wire16) <- src
+    (a row-major view with unit column stride)."""
+    rows, cols = src.shape
+    _check(lib().rl_dist_pack_u32_dev(_dp(src), src.stride(0), rows, cols, int(wire16), _dp(dst),
+                                      _cur(stream)))
+
+
+def dist_unpack_dev(src, dst, wire16: bool, colmap=None, off: int = 0, stream=None) -> None:
+    """dst[r, colmap[c] - off] <- src[r, c] (colmap: int64 device tensor, or None for c)."""
+    rows, cols = src.shape
+    _check(lib().rl_dist_unpack_u32_dev(_dp(src), rows, cols, int(wire16), _dp(dst), dst.stride(0),
+                                        None if colmap is None else _dp(colmap), off, _cur(stream)))
+
+
+def dist_select_cols_dev(src, colmap, dst, off: int = 0, stream=None) -> None:
+    """dst[r, c] <- src[r, colmap[c] - off] for c < colmap.numel()."""
+    rows = dst.shape[0]
+    _check(lib().rl_dist_select_cols_u32_dev(_dp(src), src.stride(0), rows, _dp(colmap), off, colmap.numel(),
+                                             _dp(dst), dst.stride(0), _cur(stream)))
+
+
+def dist_shift_u_rows_dev(x, cols_from: int, r: int, i0: int, rt: int, gpos, stream=None) -> None:
+    """The U-row move of factor.cpp:62-70 on the local columns from cols_from on
+    (gpos: their global positions, int64 device tensor)."""
+    v = x[:, cols_from:]
+    _check(lib().rl_dist_shift_u_rows_dev(_dp(v), x.stride(0), v.shape[1], r, i0, rt, _dp(gpos),
+                                          _cur(stream)))
 
 
 def plan_stats(m: int, n: int, p: int, lda: int | None = None) -> dict:

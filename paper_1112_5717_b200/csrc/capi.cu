@@ -989,6 +989,43 @@ int rl_digest_u32_dev(const uint32_t* dA, int64_t m, int64_t n, int64_t lda, uin
     });
 }
 
+int rl_dist_pack_u32_dev(const uint32_t* src, int64_t lds, int64_t rows, int64_t cols, int wire16, void* dst,
+                         void* stream) {
+    return guard([&] {
+        if (rows < 0 || cols < 0 || lds < cols) throw Error(RL_EDIM, "bad piece shape");
+        if (rows > 0 && cols > 0 && (!src || !dst)) throw Error(RL_EINVAL, "null buffer");
+        require_device();
+        dist_pack(src, lds, rows, cols, wire16, dst, (cudaStream_t)stream);
+    });
+}
+int rl_dist_unpack_u32_dev(const void* src, int64_t rows, int64_t cols, int wire16, uint32_t* dst, int64_t ldd,
+                           const int64_t* colmap, int64_t off, void* stream) {
+    return guard([&] {
+        if (rows < 0 || cols < 0 || (!colmap && ldd < cols)) throw Error(RL_EDIM, "bad piece shape");
+        if (rows > 0 && cols > 0 && (!src || !dst)) throw Error(RL_EINVAL, "null buffer");
+        require_device();
+        dist_unpack(src, rows, cols, wire16, dst, ldd, colmap, off, (cudaStream_t)stream);
+    });
+}
+int rl_dist_select_cols_u32_dev(const uint32_t* src, int64_t lds, int64_t rows, const int64_t* colmap,
+                                int64_t off, int64_t cols, uint32_t* dst, int64_t ldd, void* stream) {
+    return guard([&] {
+        if (rows < 0 || cols < 0 || ldd < cols) throw Error(RL_EDIM, "bad piece shape");
+        if (rows > 0 && cols > 0 && (!src || !dst || !colmap)) throw Error(RL_EINVAL, "null buffer");
+        require_device();
+        dist_select(src, lds, rows, colmap, off, cols, dst, ldd, (cudaStream_t)stream);
+    });
+}
+int rl_dist_shift_u_rows_dev(uint32_t* x, int64_t ldx, int64_t cols, int64_t r, int64_t i0, int64_t rt,
+                             const int64_t* gpos, void* stream) {
+    return guard([&] {
+        if (cols < 0 || rt < 0 || r < 0 || i0 < r || ldx < cols) throw Error(RL_EDIM, "bad shift");
+        if (cols && rt && (!x || !gpos)) throw Error(RL_EINVAL, "null buffer");
+        require_device();
+        dist_shift_u_rows(x, ldx, cols, r, i0, rt, gpos, (cudaStream_t)stream);
+    });
+}
+
 int rl_cup_batched_u32_dev(uint32_t* dA, int64_t batch, int64_t m, int64_t n, int64_t stride,
                            uint32_t p, int64_t* ranks, uint32_t* rrp, uint32_t* sigma,
                            void* stream) {

@@ -35,6 +35,9 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
     if (const char* e = getenv("RL_TILE_MAX_M")) tile_max_m_ = atoi(e);
     if (tile_g_ > 0) tile_g_ = std::max(PB, tile_g_ / PB * PB);  // whole leaves
     if (const char* e = getenv("RL_TILE_CTAS")) tile_ctas_ = atoi(e);
+    if (const char* e = getenv("RL_TILE_AFTER_REST")) tile_after_rest_ = atoi(e) != 0;
+    if (const char* e = getenv("RL_REST_PIECES")) rest_pieces_ = atoi(e) != 0;
+    if (const char* e = getenv("RL_S2_PRIO")) s2_prio_ = atoi(e) != 0;
     if (m_ > 0 && n_ > 0) {
         if (tiled_on()) tiled(tile_g_);
         else node(0, m_);
@@ -81,7 +84,10 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
     // scheduler: a window CTA takes the first SM that frees up
     int prio_lo = 0, prio_hi = 0;
     RL_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-    RL_CUDA_CHECK(cudaStreamCreateWithPriority(&s2_, cudaStreamNonBlocking, prio_lo));
+    // s2_ (the rest of each Schur update, joined before the next tail) ranks
+    // above the lanes when s2_prio_ (CTA dispatch order when SMs free up)
+    RL_CUDA_CHECK(cudaStreamCreateWithPriority(&s2_, cudaStreamNonBlocking,
+                                               s2_prio_ ? std::min(prio_lo, prio_hi + 1) : prio_lo));
     RL_CUDA_CHECK(cudaStreamCreateWithPriority(&s3_, cudaStreamNonBlocking, prio_hi));
     RL_CUDA_CHECK(cudaEventCreateWithFlags(&done_, cudaEventDisableTiming));
     events_.resize(events_needed_ + 4);
@@ -93,7 +99,7 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
         // a short lane's pieces are needed sooner: lanes of height 128, 256, ...
         // get the priorities right below the critical path's, the tall ones the lowest
         int prio = prio_lo;
-        if (lane_prio_ && kv.first != kTileLane) {
+        if (lane_prio_ && kv.first > 0) {
             int lvl = 0;
             for (i32 h = kv.first; h > 2 * PB; h /= 2) ++lvl;
             prio = std::min(prio_lo, prio_hi + 1 + lvl);
@@ -185,7 +191,7 @@ void CupEngine::gemm(i32 row0, i32 M, i32 x0, i32 x1, Dyn n_lo, Dyn n_hi, i64 Nm
 #define RL_SIDE_FREE_SMS 1
 #endif
     g.max_ctas = (st == s_)                           ? 0
-                 : (ln && ln == tile_lane_)            ? tile_ctas_
+                 : (ln && is_tile_lane(ln))            ? tile_ctas_
                  : (ln && lane_ctas_ > 0)              ? lane_ctas_
                                                        : num_sms() - RL_SIDE_FREE_SMS;
     g.alpha = p_ - 1;  // C <- C - A*B  (mm(..., neg_one, one), factor.cpp:51)
@@ -290,6 +296,27 @@ void CupEngine::swaps_range(i32 row0, i32 M, Dyn j_lo, Dyn j_hi, i32 piv_lo, i32
     queue_swaps(a);
 }
 
+// swaps_range as its own launch on stream st (side-lane work)
+void CupEngine::swaps_range_on(cudaStream_t st, i32 row0, i32 M, Dyn j_lo, Dyn j_hi, i32 piv_lo, i32 piv_hi) {
+    if (dry_ || M <= 0) return;
+    SwapJobs jobs{};
+    SwapArgs& a = jobs.job[0];
+    a.A = A_;
+    a.lda = lda_;
+    a.row0 = row0;
+    a.M = M;
+    a.gather = nullptr;
+    a.j_lo = j_lo;
+    a.j_hi = j_hi;
+    a.rp = rp_;
+    a.ipiv = ipiv_;
+    a.Mmax = M;
+    leaf_range(piv_lo, piv_hi, a);
+    jobs.n = 1;
+    apply_swaps(jobs, st);
+    stats_.launches += 1;
+}
+
 void CupEngine::swaps_gather(Dyn g_lo, Dyn g_hi, i32 Mmax, Dyn j_lo, Dyn j_hi, i32 piv_lo, i32 piv_hi) {
     if (dry_ || Mmax <= 0) return;
     SwapArgs a{};
@@ -359,7 +386,7 @@ void CupEngine::gemm_ninv(i32 r0, i32 M, i32 x0, i32 mx, const u32* ninv, i32 ld
     ++stats_.gemms;
     ++stats_.tc_gemms;
     stats_.launches += 2;
-    if (lane_) g.max_ctas = lane_ == tile_lane_ ? tile_ctas_ : lane_ctas_ > 0 ? lane_ctas_ : num_sms() - 1;
+    if (lane_) g.max_ctas = is_tile_lane(lane_) ? tile_ctas_ : lane_ctas_ > 0 ? lane_ctas_ : num_sms() - 1;
     gemm_tc(g, L_, mx, mx, lane_ ? lane_->a2 : a2_, lane_ ? lane_->b2 : b2_, work_stream());
 }
 
@@ -368,7 +395,7 @@ void CupEngine::trsm_right(i32 r0, i32 M, i32 x0, i32 mx) {
     // unique, so the bytes are the reference recursion's)
     // (not the node factored last before this TRSM: its inverse is still being
     // built, the recursion below is faster than waiting for it)
-    if (big_on_ && use_tc_ && M >= kBigMinRows && x0 + mx < trsm_end_) {
+    if (big_on_ && use_tc_ && (M >= kBigMinRows || is_tile_lane(lane_)) && x0 + mx < trsm_end_) {
         const auto key = std::make_pair(x0, mx);
         if (big_slot_.count(key)) {
             if (dry_) {
@@ -648,20 +675,62 @@ void CupEngine::node(i32 i0, i32 mm) {
     } else {
         trsm_right(b0, bm, i0, k);                                    // factor.cpp:45-46
         gemm(b0, bm, i0, b0, dyn_rp(b0), Dyn{b0, PW}, std::min<i64>(PW, n_), s_, n_);
-        if (dry_) {
-            events_needed_ += 2;
-            gemm(b0, bm, i0, b0, Dyn{b0, PW}, dyn_c(n_), n_, s2_);
-        } else {
-            fork_to(s_, s2_);
-            gemm(b0, bm, i0, b0, Dyn{b0, PW}, dyn_c(n_), n_, s2_);
-            cudaEvent_t e = events_.at(next_event_++);
-            RL_CUDA_CHECK(cudaEventRecord(e, s2_));
-            pending_joins_.push_back(e);
-        }
+        rest_update(b0, bm, i0, b0);
     }
     node(b0, bm);                                                     // factor.cpp:53
     swaps_gather(dyn_rp(i0), dyn_rp(b0), k, dyn_rp(b0), dyn_rp(i0 + mm), b0, i0 + mm);  // factor.cpp:56
     if (big_on_ && use_tc_ && mm > 8 * PB && mm <= BIG_LD && m_ >= 2 * kBigMinRows) build_big_inverse(i0, mm);
+}
+
+// The Schur update of rows [b0, b0 + bm) against the pivots of rows [x0, x1)
+// beyond the slice the next window reads (columns >= rp[b0] + PW), on s2_
+// beside that window.  In pieces along node(b0, bm)'s left spine when
+// rest_pieces_: the first leaf's rows first (joined before its tail), then
+// the bottom half of node(b0, s) for s = 2 x leaf, ..., bm (joined by node(b0, s)
+// right before its first touch of those rows, see node()), so a leaf's tail
+// never waits for rows it does not read -- the pieces needed first are the
+// smallest and are done first even when a side lane holds most SMs.
+// Returns the event of the last piece.
+cudaEvent_t CupEngine::rest_update(i32 b0, i32 bm, i32 x0, i32 x1) {
+    std::vector<i32> spine;  // s_0 = bm, s_{t+1} = s_t / 2 (node()'s split) down to the first leaf
+    if (rest_pieces_) {
+        for (i32 s = bm;; s /= 2) {
+            spine.push_back(s);
+            if (s <= PB) break;
+        }
+    } else {
+        spine.push_back(bm);
+    }
+    if (dry_) events_needed_ += 2 + spine.size();
+    else fork_to(s_, s2_);
+    cudaEvent_t e = nullptr;
+    auto record = [&](cudaStream_t st) {
+        if (dry_) return (cudaEvent_t) nullptr;
+        cudaEvent_t ev = events_.at(next_event_++);
+        RL_CUDA_CHECK(cudaEventRecord(ev, st));
+        return ev;
+    };
+    const i32 l0 = spine.back();
+    gemm(b0, l0, x0, x1, Dyn{b0, PW}, dyn_c(n_), n_, s2_);
+    e = record(s2_);
+    if (!dry_) pending_joins_.push_back(e);
+    if (spine.size() > 1) {
+        // the later pieces on the lane of this height (own stream and GEMM
+        // workspace): they are joined deep in the recursion, while s_ and s2_
+        // keep packing into their own workspaces
+        Lane& ln = lanes_[bm];
+        if (!dry_) fork_to(s_, ln.st);
+        Lane* saved = lane_;
+        lane_ = &ln;
+        for (int t = (int)spine.size() - 2; t >= 0; --t) {
+            const i32 lo = spine[t + 1], hi = spine[t];
+            gemm(b0 + lo, hi - lo, x0, x1, Dyn{b0, PW}, dyn_c(n_), n_);
+            e = record(ln.st);
+            if (!dry_) row_joins_[{b0, hi}] = e;
+        }
+        lane_ = saved;
+    }
+    return e;
 }
 
 // C <- alpha * A * B (beta = 0) on dense / gathered operands, on stream st
@@ -787,18 +856,42 @@ void CupEngine::build_big_inverse(i32 x0, i32 mm) {
 // "iterative formulation"), so the bytes are the recursion's.  The OpCounter
 // is computed from the reference skeleton (cup_opcount), not from this order.
 void CupEngine::tiled(i32 g) {
-    Lane& ln = lanes_[kTileLane];
-    tile_lane_ = &ln;
     tiling_ = true;  // node() leaves the host-overlap "done" records to this loop
-    if (dry_) events_needed_ += 1;  // the lane's final join (enqueue)
-    cudaEvent_t side = nullptr;  // last side-lane update (rows below the next tile)
-    bool waited_host = false;
+    // host-buffer path: rows [sz/2, sz) of the left-spine node (0, sz) arrive with
+    // its wait event (set_host_overlap); rows below the smallest such sz/2 are
+    // resident before the run starts
+    std::vector<std::pair<std::pair<i32, i32>, cudaEvent_t>> arrive;
+    for (const auto& kv : waits_)
+        if (kv.first.first == 0) arrive.push_back({{kv.first.second / 2, kv.first.second}, kv.second});
+    auto wait_rows = [&](cudaStream_t st, i32 lo, i32 hi) {
+        if (dry_) return;
+        for (const auto& e : arrive)
+            if (e.first.first < hi && lo < e.first.second)
+                RL_CUDA_CHECK(cudaStreamWaitEvent(st, e.second, cudaEventWaitExternal));
+    };
+    // The rows below the next tile are updated on a side lane.  With rows still
+    // arriving from the host they are cut at the arrival boundaries, one lane
+    // (stream + GEMM workspace) per piece: a piece waiting for its rows never
+    // holds up the updates of rows that are already there.
+    std::vector<i32> cuts;
+    for (const auto& e : arrive) cuts.push_back(e.first.first);
+    std::sort(cuts.begin(), cuts.end());
+    while ((int)cuts.size() + 1 > kTilePieces) cuts.erase(cuts.begin());  // (lanes sized by the dry run)
+    auto piece_of = [&](i32 row) {
+        return (int)(std::upper_bound(cuts.begin(), cuts.end(), row) - cuts.begin());
+    };
+    const int npieces = (int)cuts.size() + 1;
+    if (dry_)  // the lanes of every piece a host-buffer run may cut (same sizes)
+        for (int q = 0; q < kTilePieces; ++q) lanes_[kTileLane - q];
+    tile_lane_ = &lanes_[kTileLane];
+    std::vector<std::pair<std::pair<i32, i32>, cudaEvent_t>> side;  // last iteration's pieces
+    std::vector<char> used(npieces, 0);  // lanes that joined the launch sequence
     for (i32 i0 = 0; i0 < m_; i0 += g) {
         const i32 mm = std::min(g, m_ - i0), a = i0 + mm;
         node(i0, mm);
         if (!dry_) {
-            // host-buffer path: the top halves of the right-spine nodes that are
-            // complete now may go back (see set_host_overlap)
+            // the top halves of the right-spine nodes complete now may go back
+            // to the host (see set_host_overlap)
             for (const auto& kv : dones_) {
                 const i32 top_end = kv.first.first + kv.first.second / 2;
                 if (top_end > i0 && top_end <= a) {
@@ -806,56 +899,77 @@ void CupEngine::tiled(i32 g) {
                     RL_CUDA_CHECK(cudaEventRecordWithFlags(kv.second, s_, cudaEventRecordExternal));
                 }
             }
-            // the side lane reads the earlier tiles' U rows and writes the rows below
-            if (side) RL_CUDA_CHECK(cudaStreamWaitEvent(s_, side, 0));
-            side = nullptr;
         }
-        // P_j's transpositions onto the U rows of the earlier tiles (the V1 swaps
-        // of factor.cpp:56 at the tile level)
-        if (i0 > 0) swaps_gather(dyn_rp(0), dyn_rp(i0), i0, dyn_rp(i0), dyn_rp(a), i0, a);
         if (a >= m_) break;
-        if (!dry_ && !waited_host) {  // every row below may still be arriving from the host
-            for (const auto& kv : waits_) RL_CUDA_CHECK(cudaStreamWaitEvent(s_, kv.second, cudaEventWaitExternal));
-            waited_host = true;
-        }
-        swaps_range(a, m_ - a, dyn_rp(i0), dyn_rp(a), i0, a);     // factor.cpp:42
+        const i32 g2 = std::min(g, m_ - a), b0 = a + g2;
+        // the next tile's rows: updated against the tile before by the side lane
+        // (the pieces holding them), possibly still arriving from the host
+        for (const auto& sp : side)
+            if (!dry_ && sp.first.first < b0 && a < sp.first.second)
+                RL_CUDA_CHECK(cudaStreamWaitEvent(s_, sp.second, 0));
+        side.clear();
+        wait_rows(s_, a, b0);
+        swaps_range(a, g2, dyn_rp(i0), dyn_rp(a), i0, a);           // factor.cpp:42
         flush_swaps();
         if (!dry_ && uinv_join_) {  // the last leaf's U^{-1}
             RL_CUDA_CHECK(cudaStreamWaitEvent(s_, uinv_join_, 0));
             uinv_join_ = nullptr;
         }
-        const i32 g2 = std::min(g, m_ - a);
         // the next tile: TRSM (factor.cpp:45-46), then the slice its first window
         // reads, the rest of its columns on s2_ (joined before its first tail)
         trsm_end_ = a;
         trsm_right(a, g2, i0, mm);
         gemm(a, g2, i0, a, dyn_rp(a), Dyn{a, PW}, std::min<i64>(PW, n_), s_, n_);
-        if (dry_) {
-            events_needed_ += 2;
-            gemm(a, g2, i0, a, Dyn{a, PW}, dyn_c(n_), n_, s2_);
-        } else {
-            fork_to(s_, s2_);
-            gemm(a, g2, i0, a, Dyn{a, PW}, dyn_c(n_), n_, s2_);
-            cudaEvent_t e = events_.at(next_event_++);
-            RL_CUDA_CHECK(cudaEventRecord(e, s2_));
-            pending_joins_.push_back(e);
-        }
-        // the rows below the next tile, on the side lane: their TRSM may wait for
-        // P_j's big inverse (built on inv_lane_) and is one GEMM then
-        const i32 b0 = a + g2;
-        if (b0 < m_) {
-            if (dry_) events_needed_ += 2;
-            else fork_to(s_, ln.st);
+        const cudaEvent_t rest_ev = rest_update(a, g2, i0, a);
+        // the rows below the next tile, beside its recursion (each lane FIFO: after
+        // the same rows' updates against the earlier tiles); their TRSM may wait
+        // for P_j's big inverse (built on inv_lane_) and is one GEMM then
+        trsm_end_ = a + 1;
+        for (i32 lo = b0; lo < m_;) {
+            const int q = piece_of(lo);
+            const i32 hi = q < (int)cuts.size() ? std::min(m_, cuts[q]) : m_;
+            Lane& ln = lanes_.at(kTileLane - q);
+            used[q] = 1;
+            if (dry_) {
+                events_needed_ += 2 * kTilePieces;  // (a host run may cut up to kTilePieces pieces)
+            } else {
+                fork_to(s_, ln.st);
+                // ... after the next tile's rest (s2_) has the GPU: the lane's
+                // persistent GEMM would otherwise take most SMs first
+                if (tile_after_rest_) RL_CUDA_CHECK(cudaStreamWaitEvent(ln.st, rest_ev, 0));
+            }
+            wait_rows(ln.st, lo, hi);
             lane_ = &ln;
-            trsm_end_ = a + 1;
-            trsm_right(b0, m_ - b0, i0, mm);
-            gemm(b0, m_ - b0, i0, a, dyn_rp(a), dyn_c(n_), n_);
+            swaps_range_on(ln.st, lo, hi - lo, dyn_rp(i0), dyn_rp(a), i0, a);
+            trsm_right(lo, hi - lo, i0, mm);
+            gemm(lo, hi - lo, i0, a, dyn_rp(a), dyn_c(n_), n_);
             lane_ = nullptr;
             if (!dry_) {
-                side = events_.at(next_event_++);
-                RL_CUDA_CHECK(cudaEventRecord(side, ln.st));
+                cudaEvent_t e = events_.at(next_event_++);
+                RL_CUDA_CHECK(cudaEventRecord(e, ln.st));
+                side.push_back({{lo, hi}, e});
             }
+            lo = hi;
         }
+    }
+    // The tiles' transpositions onto the U rows of the earlier tiles (the V1
+    // swaps of factor.cpp:56 at the tile level), deferred to the end: tile t's U
+    // rows are read by nothing after its own iteration, and the transpositions of
+    // all later pivots in increasing order are one job per tile (disjoint rows).
+    for (int q = 0; q < npieces; ++q)
+        if (!dry_ && used[q]) fork_to(lanes_.at(kTileLane - q).st, s_);  // their GEMMs read those rows
+    if (dry_) {
+        const Lane& l0 = lanes_.at(kTileLane);
+        for (int q = 1; q < kTilePieces; ++q) {
+            Lane& l = lanes_.at(kTileLane - q);
+            l.a2_cap = std::max(l.a2_cap, l0.a2_cap);
+            l.b2_cap = std::max(l.b2_cap, l0.b2_cap);
+        }
+        events_needed_ += kTilePieces;
+    }
+    for (i32 i0 = 0; i0 + g < m_; i0 += g) {
+        const i32 a = i0 + g;
+        swaps_gather(dyn_rp(i0), dyn_rp(a), g, dyn_rp(a), dyn_rp(m_), a, m_);
     }
     tiling_ = false;
 }
@@ -879,7 +993,7 @@ void CupEngine::enqueue(u32* dA, cudaStream_t s) {
         if (tl) tiled(tile_g_);
         else node(0, m_);
         for (cudaEvent_t e : pending_joins_) RL_CUDA_CHECK(cudaStreamWaitEvent(s_, e, 0));
-        if (tl && lanes_.count(kTileLane)) fork_to(lanes_.at(kTileLane).st, s_);
+        // (the tile lanes joined s_ at the end of tiled())
         pending_joins_.clear();
         if (m_ > PB && split_max_k_ >= PB) fork_to(s2_, s_);  // s2_ joined the capture at a split
         fork_to(s3_, s_);

@@ -79,6 +79,7 @@ private:
     cudaEvent_t fork_to(cudaStream_t from, cudaStream_t to);  // `to` waits for `from`'s work so far
     // the transpositions are the pivots of rows [piv_lo, piv_hi) (whole leaves)
     void swaps_range(i32 row0, i32 M, Dyn j_lo, Dyn j_hi, i32 piv_lo, i32 piv_hi);
+    void swaps_range_on(cudaStream_t st, i32 row0, i32 M, Dyn j_lo, Dyn j_hi, i32 piv_lo, i32 piv_hi);
     void swaps_gather(Dyn g_lo, Dyn g_hi, i32 Mmax, Dyn j_lo, Dyn j_hi, i32 piv_lo, i32 piv_hi);
     void leaf_range(i32 piv_lo, i32 piv_hi, SwapArgs& a) const;
     void queue_swaps(const SwapArgs& a);
@@ -223,11 +224,30 @@ private:
     bool tiled_on() const { return tile_g_ > 0 && m_ >= tile_min_m_ && m_ <= tile_max_m_ && m_ > tile_g_; }
     static constexpr i32 kTileLane = -1;         // lanes_ key of the tiles' side lane
     bool tiling_ = false;                        // inside tiled()
+    static constexpr int kTilePieces = 4;        // host-arrival pieces (capi: 3 copy events)
 #ifndef RL_TILE_CTAS
-#define RL_TILE_CTAS 110
+#define RL_TILE_CTAS 100
 #endif
     i32 tile_ctas_ = RL_TILE_CTAS;               // persistent GEMM CTAs of the tiles' side lane
     Lane* tile_lane_ = nullptr;
+    // tile lanes: lanes_ keys kTileLane, kTileLane - 1, ... (one per host-arrival piece)
+    bool is_tile_lane(const Lane* l) const {
+        if (!l) return false;
+        for (const auto& kv : lanes_)
+            if (kv.first <= kTileLane && &kv.second == l) return true;
+        return false;
+    }
+    bool tile_after_rest_ = true;                // the lane starts after the next tile's rest GEMM
+#ifndef RL_REST_PIECES
+#define RL_REST_PIECES 0
+#endif
+    // (measured slower: C3 24.2 vs 21.6 ms -- the bridge then waits for its piece)
+    bool rest_pieces_ = RL_REST_PIECES != 0;     // rest_update() in left-spine pieces
+    cudaEvent_t rest_update(i32 b0, i32 bm, i32 x0, i32 x1);
+#ifndef RL_S2_PRIO
+#define RL_S2_PRIO 0
+#endif
+    bool s2_prio_ = RL_S2_PRIO != 0;             // s2_ above the lanes at the CTA scheduler
     cudaGraphExec_t graph_exec_ = nullptr;
     u32* graph_A_ = nullptr;
     cudaEvent_t done_ = nullptr;  // end of the last run: the destructor waits for it

@@ -213,4 +213,12 @@ void gen_random_matrix(u32* A, i64 lda, i64 m, i64 n, u64 seed, u32 p, cudaStrea
 
 void fill_rp0(i32* rp, cudaStream_t s);
 
+// Data plane of the distributed CUP (dist.cu, paper_1112_5717_b200/dist.py).
+void dist_pack(const u32* src, i64 lds, i64 rows, i64 cols, int wire16, void* dst, cudaStream_t s);
+void dist_unpack(const void* src, i64 rows, i64 cols, int wire16, u32* dst, i64 ldd, const i64* colmap, i64 off,
+                 cudaStream_t s);
+void dist_select(const u32* src, i64 lds, i64 rows, const i64* colmap, i64 off, i64 cols, u32* dst, i64 ldd,
+                 cudaStream_t s);
+void dist_shift_u_rows(u32* x, i64 ldx, i64 cols, i64 r, i64 i0, i64 rt, const i64* gpos, cudaStream_t s);
+
 }  // namespace rl

@@ -132,10 +132,55 @@ class _Engine:
                  dist, p: int = 0):
         self.x, self.m, self.n, self.tiles, self.ops = x, m, n, tiles, ops
         self.wire = torch.float16 if 0 < p <= 65536 else x.dtype
+        self.wire16 = self.wire == torch.float16
         self.rank, self.dist, self.world = rank, dist, tiles.world
         dev = x.device
         self.gpos_t = [torch.as_tensor(gp, dtype=torch.int64, device=dev) for gp in tiles.gpos]
         self.mine = tiles.gpos[rank]
+        # on the GPU the data plane around the collectives is one hand-written
+        # kernel per piece (csrc/dist.cu); the CPU tests (gloo) use tensor ops
+        # point-to-point sends where the backend has them for these tensors
+        self.p2p = dist is not None and (not x.is_cuda or dist.get_backend() == "nccl")
+        self.G = None
+        if x.is_cuda:
+            import sys
+            self.G = sys.modules[__package__]  # the package's C-ABI bindings
+
+    def _place(self, piece: torch.Tensor, out: torch.Tensor, g: int, la: int, lb: int, c0: int) -> None:
+        """out[:, gpos_g[la:lb] - c0] <- the received wire piece."""
+        if self.G is not None:
+            self.G.dist_unpack_dev(piece, out, self.wire16, self.gpos_t[g][la:lb], c0)
+        else:
+            out.index_copy_(1, self.gpos_t[g][la:lb] - c0, self._unpack(piece))
+
+    def gather_cols_to(self, dst: int, ra: int, rb: int, c0: int, c1: int, out) -> None:
+        """Rows [ra, rb) x global columns [c0, c1) onto rank ``dst`` only (into
+        ``out``, global order): every other owner sends its piece point to point."""
+        if rb == ra or c1 == c0:
+            return
+        for g in range(self.world):
+            la, lb = self.tiles.lsuf(g, c0), self.tiles.lsuf(g, c1)
+            if lb == la:
+                continue
+            if g == dst:
+                if self.rank == dst:
+                    out.index_copy_(1, self.gpos_t[g][la:lb] - c0, self.x[ra:rb, la:lb])
+                continue
+            if self.p2p:
+                if self.rank == g:
+                    self.dist.send(self._pack(self.x[ra:rb, la:lb]), dst=dst)
+                elif self.rank == dst:
+                    piece = torch.empty((rb - ra, lb - la), dtype=self.wire, device=self.x.device)
+                    self.dist.recv(piece, src=g)
+                    self._place(piece, out, g, la, lb, c0)
+            else:  # gloo has no point-to-point for CUDA tensors: a broadcast, kept by dst only
+                if self.rank == g:
+                    piece = self._pack(self.x[ra:rb, la:lb])
+                else:
+                    piece = torch.empty((rb - ra, lb - la), dtype=self.wire, device=self.x.device)
+                self.dist.broadcast(piece, src=g)
+                if self.rank == dst:
+                    self._place(piece, out, g, la, lb, c0)
 
     def gather_cols(self, ra: int, rb: int, c0: int, c1: int, out=None) -> torch.Tensor:
         """Rows [ra, rb) x global columns [c0, c1) in global order, on every rank
@@ -160,21 +205,43 @@ class _Engine:
             else:
                 piece = torch.empty((rb - ra, lb - la), dtype=self.wire, device=self.x.device)
             self.dist.broadcast(piece, src=g)
-            out.index_copy_(1, self.gpos_t[g][la:lb] - c0, self._unpack(piece))
+            self._place(piece, out, g, la, lb, c0)
         return out
 
     # p <= 2^16: field elements cross the links as 16-bit words (half the
     # NVLink volume of the broadcasts and gathers): x - 2^15 fits int16 exactly,
     # carried bit for bit in a 16-bit float tensor (collectives only move bytes)
-    def _pack(self, t: torch.Tensor) -> torch.Tensor:
+    def _pack(self, t: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        if self.G is not None:
+            if out is None:
+                out = torch.empty(t.shape, dtype=self.wire, device=t.device)
+            self.G.dist_pack_dev(t, out, self.wire16)
+            return out
         if self.wire == torch.float16:
-            return (t - 32768).to(torch.int16).view(torch.float16)
-        return t.contiguous()
+            w = (t - 32768).to(torch.int16).view(torch.float16)
+        else:
+            w = t.contiguous()
+        if out is None:
+            return w
+        out.copy_(w)
+        return out
 
     def _unpack(self, t: torch.Tensor) -> torch.Tensor:
         if self.wire == torch.float16:
             return t.view(torch.int16).to(torch.int32) + 32768
         return t
+
+    def bcast_block(self, R: torch.Tensor, src: int) -> None:
+        """R (a contiguous block, identical layout on every rank) from rank src."""
+        if R.numel() == 0:
+            return
+        w = self._pack(R) if self.rank == src else torch.empty(R.shape, dtype=self.wire, device=R.device)
+        self.dist.broadcast(w, src=src)
+        if self.rank != src:
+            if self.G is not None:
+                self.G.dist_unpack_dev(w, R, self.wire16)
+            else:
+                R.copy_(self._unpack(w))
 
     def put_cols(self, full: torch.Tensor, ra: int, c0: int) -> None:
         """Write this rank's columns of ``full`` (rows [ra, ..), global columns
@@ -187,6 +254,8 @@ class _Engine:
             dst = self.x[ra:ra + rows, la:lb]
             if dst.data_ptr() != full.data_ptr() or dst.stride() != full.stride():
                 dst.copy_(full)
+        elif self.G is not None:
+            self.G.dist_select_cols_dev(full, self.gpos_t[self.rank][la:lb], self.x[ra:ra + rows, la:lb], c0)
         else:
             self.x[ra:ra + rows, la:lb].copy_(
                 full.index_select(1, self.gpos_t[self.rank][la:lb] - c0))
@@ -208,9 +277,13 @@ class _Engine:
         if hi > lo:
             part = B1[lo:hi]
             self.ops.trsm_right_upper_unit(U, part)
-            mine[:hi - lo].copy_(self._pack(part))
+            self._pack(part, mine[:hi - lo])
         out = torch.empty((sl * self.world, k), dtype=self.wire, device=self.x.device)
         self.dist.all_gather(list(out.split(sl)), mine)
+        if self.G is not None:
+            G = torch.empty((rows, k), dtype=self.x.dtype, device=self.x.device)
+            self.G.dist_unpack_dev(out[:rows], G, self.wire16)
+            return G
         return self._unpack(out[:rows]).contiguous()
 
     def permute_cols(self, r: int, sig: np.ndarray, row_ranges) -> None:
@@ -251,6 +324,9 @@ class _Engine:
         if ls == self.x.shape[1]:
             return
         gp = self.gpos_t[self.rank][ls:]
+        if self.G is not None:
+            self.G.dist_shift_u_rows_dev(self.x, ls, r, i0, rt, gp)
+            return
         j = torch.arange(rt, device=self.x.device, dtype=torch.int64)
         mask = gp[None, :] > (r + j)[:, None]
         src = self.x[i0:i0 + rt, ls:]
@@ -327,10 +403,32 @@ def dist_cup(x: torch.Tensor, m: int, n: int, p: int, tiles: ColumnTiles, block:
 
     def factor_window(i0, bt, r, ww):
         """The block on its first ww columns + this rank's U rows beyond them;
-        None when a pivot lies beyond the window (on any rank)."""
+        None when a pivot lies beyond the window (on any rank).  With more than
+        one rank only the owner f of column r factors the window (its pieces
+        sent to f point to point); f broadcasts the rank, profile, sigma and the
+        factored window, so the other ranks' SMs stay on their trailing updates."""
         R = wbuf[:bt * ww].view(bt, ww)
-        eng.gather_cols(i0, i0 + bt, r, r + ww, out=R)
-        rt, rrp_t, sig_t = ops.cup(R)
+        if world > 1:
+            f = int(tiles.owner[r])
+            eng.gather_cols_to(f, i0, i0 + bt, r, r + ww, R)
+            meta = torch.full((1 + bt + ww,), -1, dtype=torch.int64, device=x.device)
+            if rank == f:
+                rt, rrp_t, sig_t = ops.cup(R)
+                host = np.full(1 + bt + ww, -1, np.int64)
+                host[0] = rt
+                host[1:1 + rt] = rrp_t[:rt]
+                host[1 + bt:] = sig_t[:ww]
+                meta.copy_(torch.from_numpy(host))
+            dist.broadcast(meta, src=f)
+            eng.bcast_block(R, src=f)
+            if rank != f:
+                host = meta.cpu().numpy()
+                rt = int(host[0])
+                rrp_t = host[1:1 + bt].copy()
+                sig_t = host[1 + bt:].copy()
+        else:
+            eng.gather_cols(i0, i0 + bt, r, r + ww, out=R)
+            rt, rrp_t, sig_t = ops.cup(R)
         ls = tiles.lsuf(rank, r + ww)
         Rb = x[i0:i0 + bt, ls:]
         bad = 0
@@ -438,8 +536,8 @@ def dist_cup(x: torch.Tensor, m: int, n: int, p: int, tiles: ColumnTiles, block:
             eng.shift_u_rows(r, i0, rt)                             # (4)
             nb = next_block(i0 + bt, r + rt, s_end)
             if rt and s_end > i0 + bt:                              # (5) + (6) in the SB
-                B1 = eng.gather_cols(i0 + bt, s_end, r, r + rt)
-                ops.trsm_right_upper_unit(R[:rt, :rt], B1)
+                # G = B1 * U11^{-1}: row slices solved one per rank, all-gathered
+                B1 = eng.solve_rows(i0 + bt, s_end, r, r + rt, R[:rt, :rt])
                 eng.put_cols(B1, i0 + bt, r)
                 if tiles.lsuf(rank, r + rt) < x.shape[1]:
                     ahead = update(B1, i0 + bt, s_end, r, r + rt, nb)

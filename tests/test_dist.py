@@ -144,7 +144,7 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 def test_gloo_multi_rank_equals_reference(world):
     import torch.multiprocessing as mp
     with socket.socket() as sk:

@@ -130,3 +130,44 @@ def test_dist_world1_large_equals_engine(n, p, block, sb):
     assert np.array_equal(res.row_profile, g.row_profile)
     assert np.array_equal(res.col_perm, g.col_perm)
     assert torch.equal(x, eng)
+
+
+def test_data_plane_kernels_match_tensor_ops():
+    """csrc/dist.cu (pack / unpack / select / U-row shift) against the tensor-op
+    formulation the CPU tests use, on strided views and both wire formats."""
+    torch.cuda.set_device(0)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randint(0, 65521, (300, 700), dtype=torch.int32, device="cuda", generator=g)
+    v = x[17:217, 33:433]
+    for wire16, dt in ((True, torch.float16), (False, torch.int32)):
+        w = torch.empty(v.shape, dtype=dt, device="cuda")
+        G.dist_pack_dev(v, w, wire16)
+        want = (v - 32768).to(torch.int16).view(torch.float16) if wire16 else v.contiguous()
+        assert torch.equal(w.view(torch.int16) if wire16 else w, want.view(torch.int16) if wire16 else want)
+        cm = torch.randperm(600, device="cuda", generator=g)[:400].to(torch.int64) + 50
+        out = torch.zeros((200, 700), dtype=torch.int32, device="cuda")
+        G.dist_unpack_dev(w, out, wire16, cm, 50)
+        ref = torch.zeros_like(out)
+        ref.index_copy_(1, cm - 50, v.contiguous())
+        assert torch.equal(out, ref)
+    cm = torch.randperm(700, device="cuda", generator=g)[:256].to(torch.int64) + 9
+    dst = x[40:140, 100:356]
+    ref = x[40:140].index_select(1, cm - 9)  # computed before dst is overwritten
+    src = x[40:140].clone()
+    G.dist_select_cols_dev(src, cm, dst, 9)
+    assert torch.equal(x[40:140, 100:356], ref)
+    # U-row shift with overlapping source / target rows (i0 - r < rt)
+    for r, i0, rt in ((10, 30, 50), (5, 300 - 64, 64), (0, 1, 120)):
+        y = torch.randint(0, 65521, (300, 500), dtype=torch.int32, device="cuda", generator=g)
+        gp = torch.sort(torch.randperm(2000, device="cuda", generator=g)[:420]).values.to(torch.int64)
+        ls = 80
+        want = y.clone()
+        src_ = want[i0:i0 + rt, ls:]
+        j = torch.arange(rt, device="cuda", dtype=torch.int64)
+        mask = gp[None, :] > (r + j)[:, None]
+        moved = torch.where(mask, src_, torch.zeros_like(src_))
+        src_.masked_fill_(mask, 0)
+        d = want[r:r + rt, ls:]
+        d.copy_(torch.where(mask, moved, d))
+        G.dist_shift_u_rows_dev(y, ls, r, i0, rt, gp)
+        assert torch.equal(y, want), (r, i0, rt)

@@ -1,0 +1,8 @@
+#!/bin/bash
+set -u
+OUT=gpurun_out/r4k
+mkdir -p $OUT
+timeout -s KILL 900 python -m pytest tests/test_gpu_tiled.py tests/test_gpu_scale.py tests/test_gpu_boundary.py -q -x -p no:cacheprovider > $OUT/pytest.txt 2>&1; echo rc=$? >> $OUT/pytest.txt
+for i in 1 2; do timeout -s KILL 200 python tools/variant_time.py paper_1112_5717_b200/libranklab_gpu.so >> $OUT/sweep.txt 2>&1; done
+timeout -s KILL 900 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > $OUT/bench.json 2> $OUT/bench.err
+timeout -s KILL 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_dist.py -q -x -p no:cacheprovider > $OUT/pytest2.txt 2>&1; echo rc=$? >> $OUT/pytest2.txt

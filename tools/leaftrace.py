@@ -67,6 +67,9 @@ for lvl in sorted(gap):
           f"window avg {sum(d)/len(d)/1e3:5.1f} us")
 print(f"  total: windows {td/1e6:.2f} ms + gaps {tg/1e6:.2f} ms; first window start -> last window end "
       f"{(W[-1][1][1] - t0)/1e6:.2f} ms")
+slow = sorted(((W[k][1][0] - W[k - 1][1][1], k) for k in range(1, len(W))), reverse=True)[:24]
+print("  slowest transitions (us, leaf index: level): " +
+      ", ".join(f"{g/1e3:.0f} @{k}:{(k & -k).bit_length() - 1}" for g, k in slow))
 wph = [v for _, v in W if len(v) > 5 and v[2] and v[3] and v[5]]
 if wph:
     import statistics
