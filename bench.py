@@ -46,6 +46,10 @@ import sys
 import threading
 import time
 
+# the factorization's launch sequence spans ~20 streams: 32 hardware work
+# queues instead of 8 (set before any CUDA context; see csrc/runtime.cu)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))

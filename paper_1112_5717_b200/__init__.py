@@ -28,6 +28,14 @@ library cannot be loaded raises, and every compute call without a GPU returns
 """
 from __future__ import annotations
 
+import os as _os
+
+# ~20 streams per factorization: raise the hardware work queues from 8 to 32
+# before any CUDA context exists (csrc/runtime.cu does the same when the
+# library is loaded first); a user-set value wins.
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
+
 import ctypes as C
 import os
 from dataclasses import dataclass, field

@@ -374,8 +374,17 @@ void tiny_cup(const u32* A, i64 m, i64 n, i64 lda, u32 p, Scratch& sc, cudaStrea
 // Out: each right-spine node's top half goes back as soon as it is factored
 // (final unless a later transposition or U-row move reaches it: then it is
 // copied again).  Copy streams and events belong to the calling stream's context.
+void cup_host_overlapped_tiles(u32* A, i64 m, i64 n, i64 lda, u32 p, u32* dA, Scratch& sc, cudaStream_t s,
+                               i64* r, std::vector<u32>& rrp_h, std::vector<u32>& ipiv_h,
+                               const std::shared_ptr<CupEngine>& e);
+
 void cup_host_overlapped(u32* A, i64 m, i64 n, i64 lda, u32 p, u32* dA, Scratch& sc, cudaStream_t s, i64* r,
                          std::vector<u32>& rrp_h, std::vector<u32>& ipiv_h) {
+    {
+        auto e = engine_for(m, n, n, p, s, true);
+        if (e->tile_rows() > 0 && (m + e->tile_rows() - 1) / e->tile_rows() <= 40)
+            return cup_host_overlapped_tiles(A, m, n, lda, p, dA, sc, s, r, rrp_h, ipiv_h, e);
+    }
     constexpr int D = 3;
     cudaStream_t cs = sc.aux_stream(0), cs2 = sc.aux_stream(1);
     cudaEvent_t top = sc.event(2 * kRing);
@@ -415,6 +424,63 @@ void cup_host_overlapped(u32* A, i64 m, i64 n, i64 lda, u32 p, u32* dA, Scratch&
         copy_d2h_2d(A + lo[d] * lda, lda, dA + lo[d] * n, n, len[d] / 2, n, cs2);
         cut = lo[d] + len[d] / 2;
     }
+    e->results(r, rrp_h.data(), ipiv_h.data(), s);  // synchronises s
+    copy_d2h_2d(A + cut * lda, lda, dA + cut * n, n, m - cut, n, s);
+    RL_CUDA_CHECK(cudaStreamSynchronize(cs2));
+    bool ident = true;
+    for (i64 j = 0; j < *r && ident; ++j) ident = ipiv_h[(size_t)j] == (u32)j && rrp_h[(size_t)j] == (u32)j;
+    if (!ident) copy_d2h_2d(A, lda, dA, n, cut, n, s);
+}
+
+// The same for an engine with the tiled top level (cup.cu, CupEngine::tiled):
+// tile 0 is copied first; every later tile crosses the link in order on a copy
+// stream with its own event, which the launch sequence waits on right before it
+// first touches those rows (the side lane of the tile's piece, or the critical
+// path); each tile goes back as soon as it is factored (final unless a later
+// transposition or U-row move reaches it: then everything is copied again).
+bool host_graph() {
+    static const bool v = [] {
+        const char* e = getenv("RL_HOST_GRAPH");
+        return !e || atoi(e) != 0;
+    }();
+    return v;
+}
+
+void cup_host_overlapped_tiles(u32* A, i64 m, i64 n, i64 lda, u32 p, u32* dA, Scratch& sc, cudaStream_t s,
+                               i64* r, std::vector<u32>& rrp_h, std::vector<u32>& ipiv_h,
+                               const std::shared_ptr<CupEngine>& e) {
+    const i64 g = e->tile_rows();
+    const i64 T = (m + g - 1) / g;
+    cudaStream_t cs = sc.aux_stream(0), cs2 = sc.aux_stream(1);
+    cudaEvent_t top = sc.event(2 * kRing);
+    CupEngine::RowEvents in, out;
+    copy_h2d_2d(dA, n, A, lda, std::min(g, m), n, s);
+    RL_CUDA_CHECK(cudaEventRecord(top, s));
+    RL_CUDA_CHECK(cudaStreamWaitEvent(cs, top, 0));
+    for (i64 t = 1; t < T; ++t) {
+        const i64 lo = t * g, hi = std::min(m, lo + g);
+        copy_h2d_2d(dA + lo * n, n, A + lo * lda, lda, hi - lo, n, cs);
+        cudaEvent_t ev = sc.event(2 * kRing + 1 + (int)t);
+        RL_CUDA_CHECK(cudaEventRecord(ev, cs));
+        in.push_back({{(i32)lo, (i32)hi}, ev});
+    }
+    for (i64 t = 0; t + 1 < T; ++t)
+        out.push_back({{(i32)(t * g), (i32)std::min(m, t * g + g)}, sc.event(2 * kRing + 1 + (int)T + (int)t)});
+    const i64 kcap = std::min(m, n);
+    rrp_h.assign((size_t)kcap, 0);
+    ipiv_h.assign((size_t)kcap, 0);
+    e->set_host_rows(in, out);
+    // (The tile lanes wait on late copy events: with the default 8 hardware
+    // work queues a blocked lane stalls the streams sharing its queue, the
+    // critical path among them -- runtime.cu raises CUDA_DEVICE_MAX_CONNECTIONS
+    // to 32 before the context exists: C3 e2e 40.6 -> 27.4 ms.)
+    e->run(dA, s, host_graph());
+    for (const auto& o : out) {
+        RL_CUDA_CHECK(cudaStreamWaitEvent(cs2, o.second, 0));
+        copy_d2h_2d(A + (i64)o.first.first * lda, lda, dA + (i64)o.first.first * n, n,
+                    o.first.second - o.first.first, n, cs2);
+    }
+    const i64 cut = (T - 1) * g;
     e->results(r, rrp_h.data(), ipiv_h.data(), s);  // synchronises s
     copy_d2h_2d(A + cut * lda, lda, dA + cut * n, n, m - cut, n, s);
     RL_CUDA_CHECK(cudaStreamSynchronize(cs2));

@@ -145,6 +145,22 @@ CupEngine::~CupEngine() {
     if (sb_) cudaStreamDestroy(sb_);
 }
 
+// Events shared with work outside the launch sequence (the host-buffer copy
+// streams): external event nodes when the sequence is captured into a graph,
+// plain records / waits when it is enqueued directly.
+static bool capturing(cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    RL_CUDA_CHECK(cudaStreamIsCapturing(s, &st));
+    return st == cudaStreamCaptureStatusActive;
+}
+void CupEngine::record_ext(cudaEvent_t e, cudaStream_t st) {
+    if (capturing(st)) RL_CUDA_CHECK(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
+    else RL_CUDA_CHECK(cudaEventRecord(e, st));
+}
+void CupEngine::wait_ext(cudaStream_t st, cudaEvent_t e) {
+    RL_CUDA_CHECK(cudaStreamWaitEvent(st, e, capturing(st) ? cudaEventWaitExternal : 0));
+}
+
 cudaEvent_t CupEngine::fork_to(cudaStream_t from, cudaStream_t to) {
     if (from == s_) flush_swaps();
     cudaEvent_t e = events_.at(next_event_++);
@@ -533,12 +549,12 @@ void CupEngine::node(i32 i0, i32 mm) {
         auto it = dones_.find({i0, mm});
         if (it != dones_.end()) {
             flush_swaps();
-            RL_CUDA_CHECK(cudaEventRecordWithFlags(it->second, s_, cudaEventRecordExternal));
+            record_ext(it->second, s_);
         }
     }
     if (!dry_ && !waits_.empty()) {  // its bottom rows may still be arriving from the host
         auto it = waits_.find({i0, mm});
-        if (it != waits_.end()) RL_CUDA_CHECK(cudaStreamWaitEvent(s_, it->second, cudaEventWaitExternal));
+        if (it != waits_.end()) wait_ext(s_, it->second);
     }
     if (!dry_) {  // the lower rows' TRSM + Schur update ran on a side lane
         auto it = row_joins_.find({i0, mm});
@@ -857,52 +873,67 @@ void CupEngine::build_big_inverse(i32 x0, i32 mm) {
 // is computed from the reference skeleton (cup_opcount), not from this order.
 void CupEngine::tiled(i32 g) {
     tiling_ = true;  // node() leaves the host-overlap "done" records to this loop
-    // host-buffer path: rows [sz/2, sz) of the left-spine node (0, sz) arrive with
-    // its wait event (set_host_overlap); rows below the smallest such sz/2 are
-    // resident before the run starts
-    std::vector<std::pair<std::pair<i32, i32>, cudaEvent_t>> arrive;
-    for (const auto& kv : waits_)
-        if (kv.first.first == 0) arrive.push_back({{kv.first.second / 2, kv.first.second}, kv.second});
+    const i32 ntiles = (m_ + g - 1) / g;
+    // Rows still arriving from the host (host-buffer path): pieces [lo, hi) with
+    // the event of their copy; rows below the first piece are resident at launch.
+    // Either per tile (set_host_rows) or the left-spine halves (set_host_overlap).
+    std::vector<std::pair<std::pair<i32, i32>, cudaEvent_t>> arrive = host_in_;
+    if (arrive.empty())
+        for (const auto& kv : waits_)
+            if (kv.first.first == 0) arrive.push_back({{kv.first.second / 2, kv.first.second}, kv.second});
+    std::sort(arrive.begin(), arrive.end(),
+              [](const auto& x, const auto& y) { return x.first.first < y.first.first; });
     auto wait_rows = [&](cudaStream_t st, i32 lo, i32 hi) {
         if (dry_) return;
         for (const auto& e : arrive)
             if (e.first.first < hi && lo < e.first.second)
-                RL_CUDA_CHECK(cudaStreamWaitEvent(st, e.second, cudaEventWaitExternal));
+                wait_ext(st, e.second);
     };
-    // The rows below the next tile are updated on a side lane.  With rows still
-    // arriving from the host they are cut at the arrival boundaries, one lane
-    // (stream + GEMM workspace) per piece: a piece waiting for its rows never
-    // holds up the updates of rows that are already there.
-    std::vector<i32> cuts;
-    for (const auto& e : arrive) cuts.push_back(e.first.first);
-    std::sort(cuts.begin(), cuts.end());
-    while ((int)cuts.size() + 1 > kTilePieces) cuts.erase(cuts.begin());  // (lanes sized by the dry run)
+    // The rows below the next tile are updated on side lanes, one lane (stream +
+    // GEMM workspace) per arrival piece (one piece without host rows): a piece
+    // waiting for its rows never holds up the updates of rows already there.
+    std::vector<i32> cuts;  // piece q = rows [cuts[q-1], cuts[q]) (cuts[-1] = 0)
+    for (const auto& e : arrive)
+        if (e.first.first > 0 && (cuts.empty() || e.first.first > cuts.back())) cuts.push_back(e.first.first);
     auto piece_of = [&](i32 row) {
         return (int)(std::upper_bound(cuts.begin(), cuts.end(), row) - cuts.begin());
     };
-    const int npieces = (int)cuts.size() + 1;
-    if (dry_)  // the lanes of every piece a host-buffer run may cut (same sizes)
-        for (int q = 0; q < kTilePieces; ++q) lanes_[kTileLane - q];
-    tile_lane_ = &lanes_[kTileLane];
+    const int max_pieces = ntiles + 1;  // a host run cuts at most at every tile
+    if ((int)cuts.size() + 1 > max_pieces) throw Error(7 /*RL_EINVAL*/, "too many host pieces");
+    if (dry_)
+        for (int q = 0; q < max_pieces; ++q) lanes_[kTileLane - q];
+    tile_lane_ = &lanes_.at(kTileLane);
     std::vector<std::pair<std::pair<i32, i32>, cudaEvent_t>> side;  // last iteration's pieces
-    std::vector<char> used(npieces, 0);  // lanes that joined the launch sequence
+    std::vector<char> used(max_pieces, 0);  // lanes that joined the launch sequence
+    auto update_rows = [&](Lane& ln, i32 lo, i32 hi, i32 i0, i32 mm, i32 a) {
+        lane_ = &ln;
+        swaps_range_on(ln.st, lo, hi - lo, dyn_rp(i0), dyn_rp(a), i0, a);
+        trsm_right(lo, hi - lo, i0, mm);
+        gemm(lo, hi - lo, i0, a, dyn_rp(a), dyn_c(n_), n_);
+        lane_ = nullptr;
+    };
     for (i32 i0 = 0; i0 < m_; i0 += g) {
         const i32 mm = std::min(g, m_ - i0), a = i0 + mm;
         node(i0, mm);
         if (!dry_) {
-            // the top halves of the right-spine nodes complete now may go back
-            // to the host (see set_host_overlap)
+            // rows complete now may go back to the host (see set_host_overlap)
             for (const auto& kv : dones_) {
                 const i32 top_end = kv.first.first + kv.first.second / 2;
                 if (top_end > i0 && top_end <= a) {
                     flush_swaps();
-                    RL_CUDA_CHECK(cudaEventRecordWithFlags(kv.second, s_, cudaEventRecordExternal));
+                    record_ext(kv.second, s_);
+                }
+            }
+            for (const auto& kv : host_out_) {
+                if (kv.first.second > i0 && kv.first.second <= a) {
+                    flush_swaps();
+                    record_ext(kv.second, s_);
                 }
             }
         }
         if (a >= m_) break;
         const i32 g2 = std::min(g, m_ - a), b0 = a + g2;
-        // the next tile's rows: updated against the tile before by the side lane
+        // the next tile's rows: updated against the tile before by the side lanes
         // (the pieces holding them), possibly still arriving from the host
         for (const auto& sp : side)
             if (!dry_ && sp.first.first < b0 && a < sp.first.second)
@@ -925,30 +956,30 @@ void CupEngine::tiled(i32 g) {
         // the same rows' updates against the earlier tiles); their TRSM may wait
         // for P_j's big inverse (built on inv_lane_) and is one GEMM then
         trsm_end_ = a + 1;
+        if (dry_) {
+            // size every lane for both layouts: one piece (device input) and one
+            // piece per tile (host input)
+            events_needed_ += 2 * (max_pieces + 1);
+            if (b0 < m_) update_rows(lanes_.at(kTileLane), b0, m_, i0, mm, a);
+            for (i32 lo = b0; lo < m_; lo += g)
+                update_rows(lanes_.at(kTileLane - std::min(max_pieces - 1, lo / g)), lo, std::min(m_, lo + g), i0,
+                            mm, a);
+            continue;
+        }
         for (i32 lo = b0; lo < m_;) {
             const int q = piece_of(lo);
             const i32 hi = q < (int)cuts.size() ? std::min(m_, cuts[q]) : m_;
             Lane& ln = lanes_.at(kTileLane - q);
             used[q] = 1;
-            if (dry_) {
-                events_needed_ += 2 * kTilePieces;  // (a host run may cut up to kTilePieces pieces)
-            } else {
-                fork_to(s_, ln.st);
-                // ... after the next tile's rest (s2_) has the GPU: the lane's
-                // persistent GEMM would otherwise take most SMs first
-                if (tile_after_rest_) RL_CUDA_CHECK(cudaStreamWaitEvent(ln.st, rest_ev, 0));
-            }
+            fork_to(s_, ln.st);
+            // ... after the next tile's rest (s2_) has the GPU: the lane's
+            // persistent GEMM would otherwise take most SMs first
+            if (tile_after_rest_) RL_CUDA_CHECK(cudaStreamWaitEvent(ln.st, rest_ev, 0));
             wait_rows(ln.st, lo, hi);
-            lane_ = &ln;
-            swaps_range_on(ln.st, lo, hi - lo, dyn_rp(i0), dyn_rp(a), i0, a);
-            trsm_right(lo, hi - lo, i0, mm);
-            gemm(lo, hi - lo, i0, a, dyn_rp(a), dyn_c(n_), n_);
-            lane_ = nullptr;
-            if (!dry_) {
-                cudaEvent_t e = events_.at(next_event_++);
-                RL_CUDA_CHECK(cudaEventRecord(e, ln.st));
-                side.push_back({{lo, hi}, e});
-            }
+            update_rows(ln, lo, hi, i0, mm, a);
+            cudaEvent_t e = events_.at(next_event_++);
+            RL_CUDA_CHECK(cudaEventRecord(e, ln.st));
+            side.push_back({{lo, hi}, e});
             lo = hi;
         }
     }
@@ -956,17 +987,9 @@ void CupEngine::tiled(i32 g) {
     // swaps of factor.cpp:56 at the tile level), deferred to the end: tile t's U
     // rows are read by nothing after its own iteration, and the transpositions of
     // all later pivots in increasing order are one job per tile (disjoint rows).
-    for (int q = 0; q < npieces; ++q)
+    if (dry_) events_needed_ += max_pieces;
+    for (int q = 0; q < max_pieces; ++q)
         if (!dry_ && used[q]) fork_to(lanes_.at(kTileLane - q).st, s_);  // their GEMMs read those rows
-    if (dry_) {
-        const Lane& l0 = lanes_.at(kTileLane);
-        for (int q = 1; q < kTilePieces; ++q) {
-            Lane& l = lanes_.at(kTileLane - q);
-            l.a2_cap = std::max(l.a2_cap, l0.a2_cap);
-            l.b2_cap = std::max(l.b2_cap, l0.b2_cap);
-        }
-        events_needed_ += kTilePieces;
-    }
     for (i32 i0 = 0; i0 + g < m_; i0 += g) {
         const i32 a = i0 + g;
         swaps_gather(dyn_rp(i0), dyn_rp(a), g, dyn_rp(a), dyn_rp(m_), a, m_);
@@ -1010,6 +1033,17 @@ void CupEngine::set_host_overlap(const NodeEvents& waits, const NodeEvents& done
     waits_ = waits;
     dones_ = dones;
     if (graph_exec_) {  // the captured sequence no longer matches
+        cudaGraphExecDestroy(graph_exec_);
+        graph_exec_ = nullptr;
+        graph_A_ = nullptr;
+    }
+}
+
+void CupEngine::set_host_rows(const RowEvents& in, const RowEvents& out) {
+    if (in == host_in_ && out == host_out_) return;
+    host_in_ = in;
+    host_out_ = out;
+    if (graph_exec_) {
         cudaGraphExecDestroy(graph_exec_);
         graph_exec_ = nullptr;
         graph_A_ = nullptr;

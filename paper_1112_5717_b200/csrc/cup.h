@@ -50,6 +50,13 @@ public:
     // Captured as external event nodes: the events must outlive the graph.
     using NodeEvents = std::map<std::pair<i32, i32>, cudaEvent_t>;
     void set_host_overlap(const NodeEvents& waits, const NodeEvents& dones);
+    // The same at tile granularity (tiled engines, tile_rows() > 0): in = rows
+    // [lo, hi) -> event recorded once they are in device memory (rows below the
+    // first lo are resident at launch); out = rows [lo, hi) -> event the launch
+    // sequence records once they are factored (same validity rule as dones).
+    using RowEvents = std::vector<std::pair<std::pair<i32, i32>, cudaEvent_t>>;
+    void set_host_rows(const RowEvents& in, const RowEvents& out);
+    i32 tile_rows() const { return tiled_on() ? tile_g_ : 0; }
 
 private:
     void enqueue(u32* dA, cudaStream_t s);
@@ -77,6 +84,8 @@ private:
               i32 n_cap = 0, const EarlyPack* ep = nullptr);
     EarlyPack early_pack_b(i32 i0, i32 k, i32 mm);
     cudaEvent_t fork_to(cudaStream_t from, cudaStream_t to);  // `to` waits for `from`'s work so far
+    void record_ext(cudaEvent_t e, cudaStream_t st);
+    void wait_ext(cudaStream_t st, cudaEvent_t e);
     // the transpositions are the pivots of rows [piv_lo, piv_hi) (whole leaves)
     void swaps_range(i32 row0, i32 M, Dyn j_lo, Dyn j_hi, i32 piv_lo, i32 piv_hi);
     void swaps_range_on(cudaStream_t st, i32 row0, i32 M, Dyn j_lo, Dyn j_hi, i32 piv_lo, i32 piv_hi);
@@ -111,6 +120,7 @@ private:
 #endif
     i32 split_max_k_ = RL_SPLIT_MAX_K;
     NodeEvents waits_, dones_;
+    RowEvents host_in_, host_out_;
     void* meta_ = nullptr;                     // one allocation for everything below
     i32* rp_ = nullptr;
     i32* rrp_ = nullptr;
@@ -224,7 +234,6 @@ private:
     bool tiled_on() const { return tile_g_ > 0 && m_ >= tile_min_m_ && m_ <= tile_max_m_ && m_ > tile_g_; }
     static constexpr i32 kTileLane = -1;         // lanes_ key of the tiles' side lane
     bool tiling_ = false;                        // inside tiled()
-    static constexpr int kTilePieces = 4;        // host-arrival pieces (capi: 3 copy events)
 #ifndef RL_TILE_CTAS
 #define RL_TILE_CTAS 100
 #endif

@@ -6,6 +6,7 @@
 // device, workspaces by (device, stream), so concurrent calls on distinct
 // streams -- or distinct host threads using cudaStreamPerThread -- proceed in
 // parallel (SURVEY.md 8(b) "Threading").
+#include <cstdlib>
 #include <map>
 #include <memory>
 #include <thread>
@@ -13,6 +14,16 @@
 
 #include "common.cuh"
 #include "runtime.h"
+
+// The launch sequence of one factorization spans ~20 streams (critical path,
+// side streams, row-split and tile lanes, copy streams); with the default 8
+// hardware work queues, a stream blocked on an event (a tile lane waiting for
+// its rows to arrive from the host) stalls the other streams sharing its
+// queue.  Ask for the maximum (32) when the library is loaded -- before the
+// host program creates its CUDA context -- unless the user chose a value.
+__attribute__((constructor)) static void rl_max_connections() {
+    setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);
+}
 
 namespace rl {
 
@@ -75,6 +86,7 @@ cudaStream_t Scratch::aux_stream(int i) {
 }
 
 cudaEvent_t Scratch::event(int i) {
+    if (i < 0 || i >= (int)(sizeof(ev) / sizeof(ev[0]))) throw Error(7 /*RL_EINVAL*/, "copy event pool exhausted");
     if (!ev[i]) RL_CUDA_CHECK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
     return ev[i];
 }

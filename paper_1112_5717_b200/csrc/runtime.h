@@ -135,7 +135,7 @@ struct Scratch {
     int device = 0;
     DevBuf buf[SS_COUNT];
     cudaStream_t aux[4] = {};     // copy streams of the host-buffer paths (lazy)
-    cudaEvent_t ev[24] = {};      // their events (lazy)
+    cudaEvent_t ev[96] = {};      // their events (lazy)
     void* pinned = nullptr;       // pinned staging ring of the pageable-host path (lazy)
     size_t pinned_cap = 0;
     void* host_mapped = nullptr;  // mapped pinned result block of the tiny-matrix path (lazy)

@@ -1,4 +1,6 @@
 import os
+
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # before any CUDA context (csrc/runtime.cu)
 import sys
 
 import pytest
