@@ -273,8 +273,10 @@ void CupEngine::panel(i32 i0, i32 b) {
     a.ps = ps_;
     a.f = f_;
     panel_window(a, s_);
-    fork_to(s_, s3_);                       // U^{-1} beside the tail
-    panel_uinv(a, s3_);
+    if (!RL_UINV_IN_TAIL) {
+        fork_to(s_, s3_);                   // U^{-1} beside the tail
+        panel_uinv(a, s3_);
+    }
     // a joined side-stream kernel may become a programmatic predecessor of the
     // tail and still be writing these rows when its CTAs start: no prefetch then
     a.prefetch = pending_joins_.empty() ? 1 : 0;
@@ -283,8 +285,12 @@ void CupEngine::panel(i32 i0, i32 b) {
     panel_tail(a, s_);
     // U^{-1} (and the panel scratch it reads) is joined before the next TRSM,
     // which always precedes the next window: the swaps in between overlap it
-    uinv_join_ = events_.at(next_event_++);
-    RL_CUDA_CHECK(cudaEventRecord(uinv_join_, s3_));
+    if (!RL_UINV_IN_TAIL) {
+        uinv_join_ = events_.at(next_event_++);
+        RL_CUDA_CHECK(cudaEventRecord(uinv_join_, s3_));
+    } else {
+        ++next_event_;  // (keeps the dry run's event count valid)
+    }
     stats_.panels++;
     stats_.launches += 3;
 }

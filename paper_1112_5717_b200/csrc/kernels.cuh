@@ -4,6 +4,12 @@
 #pragma once
 #include "common.cuh"
 
+// The leaf's U^{-1} computed by the tail kernel's last CTA (1) instead of a
+// separate kernel on a side stream (0).
+#ifndef RL_UINV_IN_TAIL
+#define RL_UINV_IN_TAIL 0
+#endif
+
 namespace rl {
 
 // ----------------------------------------------------------------------- GEMM

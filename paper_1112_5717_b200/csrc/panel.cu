@@ -295,9 +295,9 @@ __global__ void __launch_bounds__(256) panel_tail_kernel(PanelArgs a) {
     unsigned long long t_loaded = 0, t_mac = 0;
 #endif
     if (blockIdx.x == gridDim.x - 1) {
-        // U^{-1} here only for leaves with window-dead rows (otherwise the
-        // parallel panel_uinv kernel computes it)
-        if (W > 0 && rt > 0 && dead != 0) {
+        // U^{-1} here for leaves with window-dead rows; with RL_UINV_IN_TAIL for
+        // every leaf (otherwise the parallel panel_uinv kernel computes it)
+        if (W > 0 && rt > 0 && (RL_UINV_IN_TAIL || dead != 0)) {
             leaf_uinv<SP>(a, c0, rt, Us, Xs, Ts);
         }
     } else if (W > 0) {
