@@ -261,7 +261,7 @@ def reference_arm(args, rank, world):
 def _ncu_traffic():
     """DRAM bytes (read + write) per gemm_tc_kernel launch at 8192^3 from the
     committed ncu --set full capture, or None."""
-    path = os.path.join(ROOT, "profiles", "round1", "gemm_8192_ncu.json")
+    path = os.path.join(ROOT, "profiles", "round2", "gemm_8192_ncu.json")
     try:
         with open(path) as f:
             d = json.load(f)
@@ -436,7 +436,7 @@ def ours(args, rank, world, local_rank):
             "shape": [gm, gm, gm], "ms_gemm": ms_gemm, "ms_pack": ms_pack,
             "traffic": _ncu_traffic(),
             "traffic_note": "dram read+write bytes per launch of the same shape from one "
-                            "ncu --set full capture (profiles/round1/gemm_8192_ncu.json); "
+                            "ncu --set full capture (profiles/round2/gemm_8192_ncu.json); "
                             "algorithmic bytes 0.94e9",
             "cup_frac_of_peak": cup_int8 / peak,
             "cup_modp_peak": peak * 1e12 / (L * L),

@@ -777,7 +777,40 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
 #ifdef RL_TRACE
     unsigned long long t_mid = 0;
 #endif
-    if (spec) {
+    if (spec && bl == PB && b == PB) {
+        // the common case (a full leaf, no window-dead row: row k is live row k):
+        // four columns per thread, 16-byte shared loads and global stores, the
+        // A entries and the Minv row in the same pass
+        const bool av = ((reinterpret_cast<uintptr_t>(a.A) & 15) == 0) && ((a.lda & 3) == 0) && ((c0 & 3) == 0);
+#pragma unroll 2
+        for (int e = tid; e < PB * PB / 4; e += blockDim.x) {
+            const int k = e >> 4, x = (e & 15) << 2;
+            const u32* R = s_R + k * RP;
+            const u32 pi = s_pinvA[k];
+            const uint4 rv = *reinterpret_cast<const uint4*>(R + x);
+            const uint4 iv = *reinterpret_cast<const uint4*>(R + PW + x);
+            u32 v[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int xq = x + q;
+                v[q] = xq < k ? s_C[k][xq] : (xq == k ? v[q] : mulmod_t<SP>(v[q], pi, f));
+            }
+            u32* dst = a.A + (i64)(a.i0 + k) * a.lda + c0 + x;
+            if (av) {
+                *reinterpret_cast<uint4*>(dst) = make_uint4(v[0], v[1], v[2], v[3]);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) dst[q] = v[q];
+            }
+            *reinterpret_cast<uint4*>(&ps->Minv[k][x]) =
+                make_uint4(mulmod_t<SP>(iv.x, pi, f), mulmod_t<SP>(iv.y, pi, f), mulmod_t<SP>(iv.z, pi, f),
+                           mulmod_t<SP>(iv.w, pi, f));
+        }
+#ifdef RL_TRACE
+        t_mid = rl_now();
+#endif
+        LT_MARK(a.i0 / PB, 4);
+    } else if (spec) {
         // live row k' (original row s_perm[k']) has its pivot at column k': C
         // left of it, the raw pivot, U = reduced value * pivot^{-1} right of it;
         // Minv row k' scaled likewise.  Dead rows stay zero in the window, their
