@@ -494,7 +494,7 @@ def ours(args, rank, world, local_rank):
         line["e2e_pageable"] = {"value": world * W / pt, "unit": "mod-p ops/s", "ms_per_step": pt * 1e3,
                                 "h2d_bytes_per_step": m * n * 4, "d2h_bytes_per_step": m * n * 4,
                                 "steps": len(tp),
-                                "path": "rl_cup_u32 (pageable host buffer, staged through a pinned ring)"}
+                                "path": "rl_cup_u32 (pageable host buffer: tile pipeline through two pinned rings filled/drained by host threads)"}
         del pg
     except Exception as e:  # pragma: no cover
         line["e2e"] = {"error": str(e)}

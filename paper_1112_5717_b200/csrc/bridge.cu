@@ -69,18 +69,12 @@ __device__ __forceinline__ void mma64(u64 (&acc)[NT][4], const uint8_t (*Al)[BP]
 }
 
 // raw operand staging (u32, row pitch +4 words: 16-byte aligned rows)
-constexpr int XP = PB + 4;
-template <int SW>
-constexpr size_t raw_bytes() {  // X, U^{-1}, U slice, C slice; then the U-slice byte planes
-    return sizeof(u32) * (2 * PB * XP + 2 * PB * (SW + 4)) + 2 * SW * BP;
-}
+constexpr int XP = PB + 4, UP = PW + 4;
+constexpr size_t RAW_BYTES = sizeof(u32) * (2 * PB * XP + 2 * PB * UP);  // X, U^{-1}, U slice, C slice
 #ifndef RL_BRIDGE_SMEM
 #define RL_BRIDGE_SMEM 0  // (a larger request keeps other CTAs off its SM)
 #endif
-template <int SW>
-constexpr size_t bridge_smem() {
-    return raw_bytes<SW>() > RL_BRIDGE_SMEM ? raw_bytes<SW>() : RL_BRIDGE_SMEM;
-}
+constexpr size_t BRIDGE_SMEM = RAW_BYTES > RL_BRIDGE_SMEM ? RAW_BYTES : RL_BRIDGE_SMEM;
 
 // rows [0, rows) x words [0, cols) of a row-major global block (row r at
 // base + rowoff(r), cols valid of width) into smem dst[r][.] with pitch dp;
@@ -107,11 +101,7 @@ __device__ __forceinline__ void stage(u32* dst, int dp, int rows, int cols, int 
     }
 }
 
-// SW: slice width (PW, or 192 for the eager bridge of a two-leaf top, which also
-// covers the second leaf's pivot columns)
-template <int SW>
 __global__ void __launch_bounds__(256, 1) bridge_kernel(BridgeArgs a) {
-    constexpr int UP = SW + 4;
     extern __shared__ __align__(16) u32 raw[];
     u32* Xr = raw;              // [PB][XP]  X at the top pivots
     u32* Ir = Xr + PB * XP;     // [PB][XP]  U_top^{-1}
@@ -119,8 +109,7 @@ __global__ void __launch_bounds__(256, 1) bridge_kernel(BridgeArgs a) {
     u32* Cr = Ur + PB * UP;     // [PB][UP]  the bottom rows at the slice
     __shared__ __align__(16) uint8_t Xl[PB][BP], Xh[PB][BP];   // X, then G  [row][k]
     __shared__ __align__(16) uint8_t Il[PB][BP], Ih[PB][BP];   // U^{-1}     [col][k]
-    uint8_t (*Ul)[BP] = reinterpret_cast<uint8_t (*)[BP]>(Cr + PB * UP);  // U slice [col][k]
-    uint8_t (*Uh)[BP] = Ul + SW;
+    __shared__ __align__(16) uint8_t Ul[PW][BP], Uh[PW][BP];   // U slice    [col][k]
     __shared__ i32 s_urow[PB];
     LT_BEGIN();
     // Launched as a programmatic dependent of the top leaf's tail, which starts
@@ -145,8 +134,7 @@ __global__ void __launch_bounds__(256, 1) bridge_kernel(BridgeArgs a) {
         return;
     }
     const i32 n_lo = dyn_eval(a.n_lo, a.rp);
-    const i32 n_end = a.has_n_hi ? min(a.N, dyn_eval(a.n_hi, a.rp)) : a.N;
-    const int ns = max(0, min(SW, n_end - n_lo));  // live slice width
+    const int ns = max(0, min(PW, a.N - n_lo));  // live slice width
     const bool swapped = __ldcg(a.swapflag) != 0;
     if (tid < PB) s_urow[tid] = tid < nl ? __ldcg(a.rrp + j_lo + tid) : -1;
     // (1) the top leaf's transpositions on the bottom rows, in increasing j (all
@@ -173,10 +161,10 @@ __global__ void __launch_bounds__(256, 1) bridge_kernel(BridgeArgs a) {
     stage(Xr, XP, PB, PB, M, nl, lda4 && (j_lo & 3) == 0, [&](int r) { return A + (row0 + r) * lda + j_lo; });
     stage(Ir, XP, PB, PB, nl, nl, (reinterpret_cast<uintptr_t>(a.uinv) & 15) == 0,
           [&](int r) { return a.uinv + r * PB; });
-    stage(Cr, UP, PB, SW, M, ns, lda4 && (n_lo & 3) == 0, [&](int r) { return A + (row0 + r) * lda + n_lo; });
+    stage(Cr, UP, PB, PW, M, ns, lda4 && (n_lo & 3) == 0, [&](int r) { return A + (row0 + r) * lda + n_lo; });
     if (early) pdl_wait();
     pdl_trigger();
-    stage(Ur, UP, PB, SW, nl, ns, lda4 && (n_lo & 3) == 0,
+    stage(Ur, UP, PB, PW, nl, ns, lda4 && (n_lo & 3) == 0,
           [&](int r) { return A + (i64)s_urow[r] * lda + n_lo; });
     cp_async_wait_all();
     __syncthreads();
@@ -187,8 +175,8 @@ __global__ void __launch_bounds__(256, 1) bridge_kernel(BridgeArgs a) {
         *reinterpret_cast<u32*>(&Xl[r][k]) = lo4(v.x, v.y, v.z, v.w);
         *reinterpret_cast<u32*>(&Xh[r][k]) = hi4(v.x, v.y, v.z, v.w);
     }
-    for (int e = tid; e < (PB / 4) * (PB + SW); e += 256) {
-        const int k = (e / (PB + SW)) * 4, n = e % (PB + SW);
+    for (int e = tid; e < (PB / 4) * (PB + PW); e += 256) {
+        const int k = (e / (PB + PW)) * 4, n = e % (PB + PW);
         const bool inv = n < PB;
         const u32* src = inv ? Ir + n : Ur + (n - PB);
         const int sp = inv ? XP : UP;
@@ -222,24 +210,21 @@ __global__ void __launch_bounds__(256, 1) bridge_kernel(BridgeArgs a) {
         if (c < nl) a.A[(row0 + r) * lda + j_lo + c] = Xr[r * XP + c];
     }
     LT_MARK(a.row0 / PB, 4);
-    // (4) slice -= G * U_top[:, slice], 64-column groups over the two warp columns
+    // (4) slice -= G * U_top[:, slice]
+    if (ns > 64 * cw) {
+        u64 acc[8][4];
+        mma64<8>(acc, Xl, Xh, Ul, Uh, 16 * rs, 64 * cw, gq, tg);
 #pragma unroll
-    for (int cg = cw; cg < SW / 64; cg += 2) {
-        if (ns > 64 * cg) {
-            u64 acc[8][4];
-            mma64<8>(acc, Xl, Xh, Ul, Uh, 16 * rs, 64 * cg, gq, tg);
+        for (int t = 0; t < 8; ++t)
 #pragma unroll
-            for (int t = 0; t < 8; ++t)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int r = 16 * rs + gq + 8 * (e >> 1), c = 64 * cg + 8 * t + 2 * tg + (e & 1);
-                    Cr[r * UP + c] = submod(Cr[r * UP + c], red_sp(acc[t][e], f), f);
-                }
-        }
+            for (int e = 0; e < 4; ++e) {
+                const int r = 16 * rs + gq + 8 * (e >> 1), c = 64 * cw + 8 * t + 2 * tg + (e & 1);
+                Cr[r * UP + c] = submod(Cr[r * UP + c], red_sp(acc[t][e], f), f);
+            }
     }
     __syncthreads();
-    for (int e = tid; e < M * SW; e += 256) {
-        const int r = e / SW, c = e % SW;
+    for (int e = tid; e < M * PW; e += 256) {
+        const int r = e / PW, c = e % PW;
         if (c < ns) a.A[(row0 + r) * lda + n_lo + c] = Cr[r * UP + c];
     }
     LT_END(a.row0 / PB);
@@ -248,13 +233,8 @@ __global__ void __launch_bounds__(256, 1) bridge_kernel(BridgeArgs a) {
 }  // namespace
 
 void bridge(const BridgeArgs& a, cudaStream_t s) {
-    if (a.wide) {
-        RL_ONCE_SMEM_LIMIT(bridge_kernel<192>, bridge_smem<192>());
-        launch_pdl(bridge_kernel<192>, dim3(1), dim3(256), bridge_smem<192>(), s, a);
-    } else {
-        RL_ONCE_SMEM_LIMIT(bridge_kernel<PW>, bridge_smem<PW>());
-        launch_pdl(bridge_kernel<PW>, dim3(1), dim3(256), bridge_smem<PW>(), s, a);
-    }
+    RL_ONCE_SMEM_LIMIT(bridge_kernel, BRIDGE_SMEM);
+    launch_pdl(bridge_kernel, dim3(1), dim3(256), BRIDGE_SMEM, s, a);
     RL_CUDA_CHECK(cudaGetLastError());
 }
 

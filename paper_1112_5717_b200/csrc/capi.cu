@@ -5,7 +5,11 @@
 // SingularMatrix, NotPrime/ModulusOutOfRange), field validation follows
 // PrimeField (proj/src/field.cpp:24-58).  Engines (plans + workspaces + graphs)
 // are cached per (m, n, lda, p) behind a mutex; calls are re-entrant per stream.
+#include <cuda.h>
+
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <functional>
 #include <cstring>
 #include <map>
@@ -489,6 +493,103 @@ void cup_host_overlapped_tiles(u32* A, i64 m, i64 n, i64 lda, u32 p, u32* dA, Sc
     if (!ident) copy_d2h_2d(A, lda, dA, n, cut, n, s);
 }
 
+// Pageable host buffers (a std::vector-backed ranklab::Mat, matrix.hpp:176) with a
+// tiled engine: the tile pipeline of cup_host_overlapped_tiles, staged through two
+// pinned rings of kPgSlots tiles.  Every copy is enqueued BEFORE the launch
+// sequence (so its events are recorded before the graph waits on them); a copy
+// stream holds each DMA back with a stream-memory wait on a mapped host word
+// until the host threads have filled (in) or drained (out) the slot.  The host
+// then fills tile t + 1 while tile t crosses the link and the factorization runs.
+constexpr int kPgSlots = 3;
+
+void cup_host_pageable_tiles(u32* A, i64 m, i64 n, i64 lda, u32 p, u32* dA, Scratch& sc, cudaStream_t s,
+                             i64* r, std::vector<u32>& rrp_h, std::vector<u32>& ipiv_h,
+                             const std::shared_ptr<CupEngine>& e) {
+    const i64 g = e->tile_rows();
+    const i64 T = (m + g - 1) / g;
+    const size_t slot = (size_t)g * n;  // words
+    u32* ring_in = (u32*)sc.pinned_ring(kPgSlots * slot * 4);
+    u32* ring_out = (u32*)sc.pinned_ring_out(kPgSlots * slot * 4);
+    volatile unsigned* flags = sc.flags();  // [0]: tiles staged, [1]: tiles drained
+    CUdeviceptr f_in = 0, f_out = 0;
+    {
+        void* dp = nullptr;
+        RL_CUDA_CHECK(cudaHostGetDevicePointer(&dp, (void*)flags, 0));
+        f_in = (CUdeviceptr)dp;
+        f_out = f_in + sizeof(unsigned);
+    }
+    cudaStream_t cs = sc.aux_stream(0), cs2 = sc.aux_stream(1);
+    auto rows_of = [&](i64 t) { return std::min(g, m - t * g); };
+    // tile 0 first, synchronously staged
+    par_copy_rows(ring_in, n, A, lda, rows_of(0), n);
+    copy_h2d_2d(dA, n, ring_in, n, rows_of(0), n, s);
+    cudaEvent_t top = sc.event(2 * kRing);
+    RL_CUDA_CHECK(cudaEventRecord(top, s));
+    RL_CUDA_CHECK(cudaStreamWaitEvent(cs, top, 0));
+    CupEngine::RowEvents in, out;
+    std::vector<cudaEvent_t> ev_in(T, nullptr), ev_d2h(T, nullptr);
+    for (i64 t = 1; t < T; ++t) {
+        auto st = cuStreamWaitValue32((CUstream)cs, f_in, (cuuint32_t)t, CU_STREAM_WAIT_VALUE_GEQ);
+        if (st != CUDA_SUCCESS) throw Error(RL_ECUDA, "cuStreamWaitValue32 failed");
+        copy_h2d_2d(dA + t * g * n, n, ring_in + (size_t)(t % kPgSlots) * slot, n, rows_of(t), n, cs);
+        ev_in[t] = sc.event(2 * kRing + 1 + (int)t);
+        RL_CUDA_CHECK(cudaEventRecord(ev_in[t], cs));
+        in.push_back({{(i32)(t * g), (i32)(t * g + rows_of(t))}, ev_in[t]});
+    }
+    for (i64 t = 0; t + 1 < T; ++t)
+        out.push_back({{(i32)(t * g), (i32)(t * g + rows_of(t))}, sc.event(2 * kRing + 1 + (int)T + (int)t)});
+    const i64 kcap = std::min(m, n);
+    rrp_h.assign((size_t)kcap, 0);
+    ipiv_h.assign((size_t)kcap, 0);
+    e->set_host_rows(in, out);
+    e->run(dA, s, host_graph());
+    // device -> host, enqueued after the launch sequence that records the events
+    for (i64 t = 0; t + 1 < T; ++t) {
+        RL_CUDA_CHECK(cudaStreamWaitEvent(cs2, out[(size_t)t].second, 0));
+        if (t >= kPgSlots) {  // the slot's previous tile drained by the host
+            auto st = cuStreamWaitValue32((CUstream)cs2, f_out, (cuuint32_t)(t - kPgSlots + 1),
+                                          CU_STREAM_WAIT_VALUE_GEQ);
+            if (st != CUDA_SUCCESS) throw Error(RL_ECUDA, "cuStreamWaitValue32 failed");
+        }
+        copy_d2h_2d(ring_out + (size_t)(t % kPgSlots) * slot, n, dA + t * g * n, n, rows_of(t), n, cs2);
+        ev_d2h[t] = sc.event(2 * kRing + 1 + 2 * (int)T + (int)t);
+        RL_CUDA_CHECK(cudaEventRecord(ev_d2h[t], cs2));
+    }
+    // host side: fill the in-ring ahead of the DMA, drain the out-ring behind it
+    i64 t_in = 1, t_out = 0;
+    while (t_in < T || t_out + 1 < T) {
+        bool progressed = false;
+        // slot t % kPgSlots last held tile t - kPgSlots: its DMA must be done
+        auto slot_free = [&](i64 t) {
+            if (t < kPgSlots) return true;
+            const i64 prev = t - kPgSlots;
+            return cudaEventQuery(prev == 0 ? top : ev_in[prev]) == cudaSuccess;
+        };
+        if (t_in < T && slot_free(t_in)) {
+            par_copy_rows(ring_in + (size_t)(t_in % kPgSlots) * slot, n, A + t_in * g * lda, lda, rows_of(t_in), n);
+            std::atomic_thread_fence(std::memory_order_seq_cst);
+            flags[0] = (unsigned)t_in;
+            ++t_in;
+            progressed = true;
+        }
+        if (t_out + 1 < T && cudaEventQuery(ev_d2h[t_out]) == cudaSuccess) {
+            par_copy_rows(A + t_out * g * lda, lda, ring_out + (size_t)(t_out % kPgSlots) * slot, n, rows_of(t_out),
+                          n);
+            std::atomic_thread_fence(std::memory_order_seq_cst);
+            flags[1] = (unsigned)(t_out + 1);
+            ++t_out;
+            progressed = true;
+        }
+        if (!progressed) std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+    e->results(r, rrp_h.data(), ipiv_h.data(), s);  // synchronises s
+    const i64 cut = (T - 1) * g;
+    staged_d2h(A + cut * lda, lda, dA + cut * n, n, m - cut, n, sc, s);
+    bool ident = true;
+    for (i64 j = 0; j < *r && ident; ++j) ident = ipiv_h[(size_t)j] == (u32)j && rrp_h[(size_t)j] == (u32)j;
+    if (!ident) staged_d2h(A, lda, dA, n, cut, n, sc, s);
+}
+
 // ple (factor.cpp:87-156) is cup's column-split mirror: the recursion splits
 // columns at k = n/2 where cup splits rows at m/2, the base case searches a
 // column where cup searches a row, L is normalised where U is, E keeps raw
@@ -701,7 +802,12 @@ int rl_cup_u32(uint32_t* A, int64_t m, int64_t n, int64_t lda, uint32_t p, int64
             tiny_cup(A, m, n, lda, p, sc, s, &r, rrp_h, ipiv_h);
         } else {
             u32* dA = (u32*)sc.get(SS_A, (size_t)m * n * 4);
-            if (!host_pinned(A) && !pageable_direct()) {
+            std::shared_ptr<CupEngine> te;
+            const bool pageable = !host_pinned(A) && !pageable_direct();
+            if (pageable && m * n >= (1 << 22) && (te = engine_for(m, n, n, p, s, true))->tile_rows() > 0 &&
+                (m + te->tile_rows() - 1) / te->tile_rows() <= 24) {
+                cup_host_pageable_tiles(A, m, n, lda, p, dA, sc, s, &r, rrp_h, ipiv_h, te);
+            } else if (pageable) {
                 // pageable storage (ranklab::Mat is a std::vector, matrix.hpp:176): staged
                 // through the context's pinned ring by host threads, chunk by chunk
                 staged_h2d(dA, n, A, lda, m, n, sc, s);

@@ -38,7 +38,6 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
     if (const char* e = getenv("RL_TILE_AFTER_REST")) tile_after_rest_ = atoi(e) != 0;
     if (const char* e = getenv("RL_REST_PIECES")) rest_pieces_ = atoi(e) != 0;
     if (const char* e = getenv("RL_S2_PRIO")) s2_prio_ = atoi(e) != 0;
-    if (const char* e = getenv("RL_EAGER_L1")) eager_l1_ = atoi(e) != 0;
     if (m_ > 0 && n_ > 0) {
         if (tiled_on()) tiled(tile_g_);
         else node(0, m_);
@@ -90,7 +89,6 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
     RL_CUDA_CHECK(cudaStreamCreateWithPriority(&s2_, cudaStreamNonBlocking,
                                                s2_prio_ ? std::min(prio_lo, prio_hi + 1) : prio_lo));
     RL_CUDA_CHECK(cudaStreamCreateWithPriority(&s3_, cudaStreamNonBlocking, prio_hi));
-    RL_CUDA_CHECK(cudaStreamCreateWithPriority(&se_, cudaStreamNonBlocking, prio_hi));
     RL_CUDA_CHECK(cudaEventCreateWithFlags(&done_, cudaEventDisableTiming));
     events_.resize(events_needed_ + 4);
     for (auto& e : events_) RL_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -131,7 +129,6 @@ CupEngine::~CupEngine() {
     for (auto& e : events_) cudaEventDestroy(e);
     if (s2_) cudaStreamDestroy(s2_);
     if (s3_) cudaStreamDestroy(s3_);
-    if (se_) cudaStreamDestroy(se_);
     cudaFree(a2_);
     cudaFree(b2_);
     for (auto& kv : lanes_) {
@@ -508,16 +505,16 @@ void CupEngine::trsm_right(i32 r0, i32 M, i32 x0, i32 mx) {
     trsm_right(r0, M, x0 + kx, mx - kx);
 }
 
-// The bridge of leaf `leaf` (its pivots, U^{-1}, transposition flag) into rows
-// [row0, row0 + M), slice from n_lo (bridge.cu).
-BridgeArgs CupEngine::leaf_bridge(i32 leaf, i32 row0, i32 M, Dyn n_lo) const {
+// The bridge of the leaf of rows [leaf, leaf_end) (its pivots, U^{-1},
+// transposition flag) into rows [row0, row0 + M), slice from n_lo (bridge.cu).
+BridgeArgs CupEngine::leaf_bridge(i32 leaf, i32 leaf_end, i32 row0, i32 M, Dyn n_lo) const {
     BridgeArgs a{};
     a.A = A_;
     a.lda = lda_;
     a.row0 = row0;
     a.M = M;
     a.j_lo = dyn_rp(leaf);
-    a.j_hi = dyn_rp(leaf + PB);
+    a.j_hi = dyn_rp(leaf_end);
     a.n_lo = n_lo;
     a.N = n_;
     a.rp = rp_;
@@ -575,21 +572,7 @@ void CupEngine::node(i32 i0, i32 mm) {
         return;
     }
     const i32 k = mm / 2;                    // factor.cpp:35
-    // A node of two leaf pairs (p <= 2^16): the bottom rows receive the top pair's
-    // first leaf EAGERLY (a bridge on se_ beside the second leaf's window, which
-    // also covers the second leaf's pivot columns), so the transition into the
-    // bottom half is one bridge like a leaf pair's (see leaf_bridge_l1 below)
-    const bool l1 = eager_l1_ && mm == 4 * PB && k == 2 * PB && p_ <= 65536u && use_tc_ && bridge_on_ &&
-                    !geo_split_ && k <= split_max_k_;
-    if (l1) eager_req_ = {i0 + k, mm - k};
     node(i0, k);                             // factor.cpp:39
-    if (l1 && !dry_) {
-        // joined before anything else on s_: the top pair's queued V1 swaps
-        // (factor.cpp:56) rewrite the U rows the eager bridges read
-        if (!eager_ev_) throw Error(7 /*RL_EINVAL*/, "eager bridge not issued");
-        RL_CUDA_CHECK(cudaStreamWaitEvent(s_, eager_ev_, 0));
-        eager_ev_ = nullptr;
-    }
     if (!dry_ && !dones_.empty() && !tiling_) {  // this node's top half is factored
         auto it = dones_.find({i0, mm});
         if (it != dones_.end()) {
@@ -622,7 +605,7 @@ void CupEngine::node(i32 i0, i32 mm) {
     // a leaf pair (top = one leaf, p <= 2^16): swaps, TRSM and the window slice's
     // update in one launch (bridge.cu)
     const bool br = bridge_on_ && k <= PB && bm <= PB && p_ <= 65536u && use_tc_;
-    if (!br && !l1) {
+    if (!br) {
         swaps_range(b0, bm, dyn_rp(i0), dyn_rp(b0), i0, b0);   // factor.cpp:42
         // launched now, so it runs beside the last leaf's U^{-1} (joined below)
         // instead of after it on the critical path
@@ -635,40 +618,7 @@ void CupEngine::node(i32 i0, i32 mm) {
     // factor.cpp:51-52, split: the first window of the bottom half reads only
     // columns [rp[b0], rp[b0] + PW), so that slice is updated first and the rest
     // runs on s2_ beside that window (joined before its tail)
-    if (l1) {
-        // The top pair's first leaf a reached the bottom rows eagerly (slice
-        // [rp[i0+PB], rp[i0+PB] + 192): the second leaf's pivot columns and
-        // every column the bottom's first window can read); now its second leaf
-        // b: one bridge for the bottom's first leaf rows on the critical path,
-        // the other bridge and the Schur update of the columns beyond the slice
-        // (K = both leaves) on s2_, joined before the bottom's first tail.
-        const Dyn slice_end{i0 + PB, 192};
-        if (!dry_) {
-            BridgeArgs c = leaf_bridge(i0 + PB, b0, std::min(PB, bm), dyn_rp(b0));
-            c.n_hi = slice_end;
-            c.has_n_hi = 1;
-            c.wide = 1;
-            flush_swaps();
-            bridge(c, s_);
-            stats_.launches += 1;
-            fork_to(s_, s2_);
-            if (bm > PB) {
-                BridgeArgs d = c;
-                d.row0 = b0 + PB;
-                d.M = bm - PB;
-                bridge(d, s2_);
-                stats_.launches += 1;
-            }
-        } else {
-            events_needed_ += 2;
-        }
-        gemm(b0, bm, i0, b0, slice_end, dyn_c(n_), n_, s2_);
-        if (!dry_) {
-            cudaEvent_t e = events_.at(next_event_++);
-            RL_CUDA_CHECK(cudaEventRecord(e, s2_));
-            pending_joins_.push_back(e);
-        }
-    } else if (geo_split_ && bm > PB && k <= geo_max_k_) {
+    if (geo_split_ && bm > PB && k <= geo_max_k_) {
         // Geometric row split.  The bottom recursion node(b0, bm) first touches
         // its rows in the order of its left spine: the leaf [b0, b0 + s_L), then
         // the bottom half [b0 + s/2, b0 + s) of node(b0, s) for s = 2 s_L, ..., bm
@@ -733,29 +683,10 @@ void CupEngine::node(i32 i0, i32 mm) {
         }
     } else if (br) {
         if (!dry_) {
-            BridgeArgs a = leaf_bridge(i0, b0, bm, dyn_rp(b0));
+            BridgeArgs a = leaf_bridge(i0, b0, b0, bm, dyn_rp(b0));
             flush_swaps();
             bridge(a, s_);
             stats_.launches += 1;
-        }
-        // this pair is the top half of a node of two pairs (l1 above): leaf i0
-        // reaches that node's bottom rows now, on se_, beside leaf b0's window
-        if (eager_req_.second > 0 && eager_req_.first == i0 + mm) {
-            if (!dry_) {
-                fork_to(s_, se_);  // after leaf i0's tail (and U^{-1}): its U rows are final
-                for (i32 h = 0; h < eager_req_.second; h += PB) {
-                    BridgeArgs e = leaf_bridge(i0, eager_req_.first + h, std::min(PB, eager_req_.second - h),
-                                               dyn_rp(b0));
-                    e.wide = 1;
-                    bridge(e, se_);
-                    stats_.launches += 1;
-                }
-                eager_ev_ = events_.at(next_event_++);
-                RL_CUDA_CHECK(cudaEventRecord(eager_ev_, se_));
-            } else {
-                events_needed_ += 2;
-            }
-            eager_req_ = {0, 0};
         }
         if (dry_) {
             events_needed_ += 2;
@@ -1088,8 +1019,6 @@ void CupEngine::enqueue(u32* dA, cudaStream_t s) {
     next_event_ = 0;
     pending_joins_.clear();
     uinv_join_ = nullptr;
-    eager_ev_ = nullptr;
-    eager_req_ = {0, 0};
     row_joins_.clear();
     big_ready_.clear();
     lane_ = nullptr;

@@ -257,16 +257,7 @@ private:
 #define RL_S2_PRIO 0
 #endif
     bool s2_prio_ = RL_S2_PRIO != 0;             // s2_ above the lanes at the CTA scheduler
-    // Eager bridge of the first leaf of a two-pair node's top into its bottom rows
-    // (node()): requested by the node, issued by its top pair, joined by the node.
-#ifndef RL_EAGER_L1
-#define RL_EAGER_L1 1
-#endif
-    bool eager_l1_ = RL_EAGER_L1 != 0;
-    std::pair<i32, i32> eager_req_{0, 0};        // (bottom row0, rows) of the requesting node
-    cudaEvent_t eager_ev_ = nullptr;
-    cudaStream_t se_ = nullptr;                  // the eager bridges' stream
-    BridgeArgs leaf_bridge(i32 leaf, i32 row0, i32 M, Dyn n_lo) const;
+    BridgeArgs leaf_bridge(i32 leaf, i32 leaf_end, i32 row0, i32 M, Dyn n_lo) const;
     cudaGraphExec_t graph_exec_ = nullptr;
     u32* graph_A_ = nullptr;
     cudaEvent_t done_ = nullptr;  // end of the last run: the destructor waits for it

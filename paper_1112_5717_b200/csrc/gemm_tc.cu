@@ -253,7 +253,16 @@ __global__ void __launch_bounds__(256) pack_kernel(GemmArgs g, uint8_t* __restri
 // band, then N.  The ~#SM concurrent tiles cover a BAND x (#SM/BAND) rectangle,
 // the band's A panels stay L2-resident while the N panels stream past once per
 // band (instead of every A panel being re-streamed by every wave).
-constexpr int BAND = 16;
+#ifndef RL_GEMM_BAND
+#define RL_GEMM_BAND 16
+#endif
+constexpr int BAND = RL_GEMM_BAND;
+// L2 hints on the bulk copies: the band's A panels are kept (evict_last), the B
+// panels streamed past them (evict_first), so the A panels are not re-read
+// from DRAM by every wave of the band.
+#ifndef RL_GEMM_L2HINT
+#define RL_GEMM_L2HINT 0
+#endif
 __device__ __forceinline__ void tile_coords(i32 tile, i32 MB, i32 NB, i32& mb, i32& nb) {
     const i32 band = MB < BAND ? MB : BAND;
     const i32 b = tile / (band * NB), r = tile - b * band * NB;
@@ -323,6 +332,9 @@ __global__ void __launch_bounds__(NTHR, 1)
         if (lane == 0) {  // ---- producer: bulk async copies of pre-swizzled tiles
             int s = 0;
             uint32_t ph = 0;
+#if RL_GEMM_L2HINT
+            const uint64_t pol_a = ptx::l2_evict_last(), pol_b = ptx::l2_evict_first();
+#endif
             for (i32 tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
                 i32 mb, nb;
                 tile_coords(tile, MB, NB, mb, nb);
@@ -332,8 +344,13 @@ __global__ void __launch_bounds__(NTHR, 1)
                     ptx::mbar_wait(&empty[s], ph ^ 1);
                     uint8_t* sa = smem + s * STAGE;
                     ptx::mbar_arrive_expect_tx(&full[s], STAGE);
+#if RL_GEMM_L2HINT
+                    ptx::bulk_g2s_hint(sa, asrc + (i64)kt * A_TILE, A_TILE, &full[s], pol_a);
+                    ptx::bulk_g2s_hint(sa + A_TILE, bsrc + (i64)kt * C_::B_TILE, C_::B_TILE, &full[s], pol_b);
+#else
                     ptx::bulk_g2s(sa, asrc + (i64)kt * A_TILE, A_TILE, &full[s]);
                     ptx::bulk_g2s(sa + A_TILE, bsrc + (i64)kt * C_::B_TILE, C_::B_TILE, &full[s]);
+#endif
                     if (++s == STAGES) {
                         s = 0;
                         ph ^= 1;

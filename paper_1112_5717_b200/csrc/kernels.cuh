@@ -169,9 +169,6 @@ struct BridgeArgs {
     i32 row0, M;     // bottom rows [row0, row0 + M), M <= PB
     Dyn j_lo, j_hi;  // the top leaf's pivots
     Dyn n_lo;        // slice start
-    Dyn n_hi;        // slice end (exclusive) when has_n_hi, else n_lo + the slice width
-    int has_n_hi;
-    int wide;        // slice width 192 (the eager bridge of a two-leaf top) instead of PW
     i32 N;           // matrix columns
     const i32* rp;
     const i32* rrp;

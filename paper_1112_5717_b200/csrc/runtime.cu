@@ -102,4 +102,26 @@ void* Scratch::pinned_ring(size_t bytes) {
     return pinned;
 }
 
+void* Scratch::pinned_ring_out(size_t bytes) {
+    if (bytes > pinned_out_cap) {
+        if (pinned_out) cudaFreeHost(pinned_out);
+        pinned_out = nullptr;
+        pinned_out_cap = 0;
+        if (cudaMallocHost(&pinned_out, bytes) != cudaSuccess) throw Error(8 /*RL_ENOMEM*/, "cudaMallocHost failed");
+        pinned_out_cap = bytes;
+    }
+    return pinned_out;
+}
+
+unsigned* Scratch::flags() {
+    if (!host_flags) {
+        void* p = nullptr;
+        if (cudaHostAlloc(&p, 64, cudaHostAllocMapped) != cudaSuccess)
+            throw Error(8 /*RL_ENOMEM*/, "cudaHostAlloc (mapped) failed");
+        host_flags = static_cast<unsigned*>(p);
+    }
+    for (int i = 0; i < 16; ++i) host_flags[i] = 0;
+    return host_flags;
+}
+
 }  // namespace rl

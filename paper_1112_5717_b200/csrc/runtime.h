@@ -138,11 +138,16 @@ struct Scratch {
     cudaEvent_t ev[96] = {};      // their events (lazy)
     void* pinned = nullptr;       // pinned staging ring of the pageable-host path (lazy)
     size_t pinned_cap = 0;
+    void* pinned_out = nullptr;   // its device -> host ring (pipelined pageable path, lazy)
+    size_t pinned_out_cap = 0;
+    unsigned* host_flags = nullptr;  // mapped pinned words the copy streams wait on (lazy)
     void* host_mapped = nullptr;  // mapped pinned result block of the tiny-matrix path (lazy)
     void* get(int slot, size_t bytes) { return buf[slot].get(bytes); }
     cudaStream_t aux_stream(int i);
     cudaEvent_t event(int i);
     void* pinned_ring(size_t bytes);
+    void* pinned_ring_out(size_t bytes);
+    unsigned* flags();  // 16 words of mapped pinned memory, zeroed
 };
 Scratch& scratch_for(cudaStream_t s);
 // The host-buffer entry points' stream: one NON-blocking stream per (host

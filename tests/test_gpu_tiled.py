@@ -79,6 +79,14 @@ for a, p in big:
         if not ok:
             bad += 1
             print(f"HOST PATH MISMATCH p={p} shape={a.shape} rep {rep}")
+        # pageable memory: the staged tile pipeline (pinned rings, host-filled)
+        pg = a.copy()
+        gp = G.cup(pg, p)
+        ok = (gp.rank == gd.rank and np.array_equal(gp.row_profile, gd.row_profile)
+              and np.array_equal(gp.col_perm, gd.col_perm) and np.array_equal(pg, want))
+        if not ok:
+            bad += 1
+            print(f"PAGEABLE PATH MISMATCH p={p} shape={a.shape} rep {rep}")
 print(f"checked {len(cases)} + {len(big)} cases, {bad} mismatches")
 sys.exit(1 if bad else 0)
 """

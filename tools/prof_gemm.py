@@ -9,6 +9,8 @@ import torch  # noqa: E402
 
 import paper_1112_5717_b200 as G  # noqa: E402
 
+G.LIB_PATH = os.environ.get("RL_LIB", G.LIB_PATH)  # (variant builds)
+
 m, l, n = (int(x) for x in (sys.argv[1:4] if len(sys.argv) > 3 else (8192, 8192, 8192)))
 p = int(sys.argv[4]) if len(sys.argv) > 4 else 65521
 a = torch.empty((m, l), dtype=torch.int32, device="cuda")
