@@ -152,6 +152,8 @@ struct TrsmNodeArgs {
 constexpr int NINV_LD = TN_MAXLEAF * PB;   // 256: pitch of a node inverse
 // (M = 0 with ninv set: only the node inverse)
 void trsm_node(const TrsmNodeArgs& a, cudaStream_t s);
+// The same on the legacy tensor cores (trsm_tc.cu, p <= 2^16).
+void trsm_node_tc(const TrsmNodeArgs& a, cudaStream_t s);
 
 // Inverse of a unit upper block from its two diagonal halves (pivots
 // [a_lo, b_lo) and [b_lo, b_hi), Dyn over rp):  X = [[Xa, T2], [0, Xb]] with

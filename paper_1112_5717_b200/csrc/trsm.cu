@@ -316,9 +316,17 @@ void ninv_assemble(u32* X, i32 ldx, const u32* Xa, i32 la, const u32* Xb, i32 lb
 
 // Row tile per CTA: 32 rows for tall G (fewer staged-block loads per row, more
 // products per shared load), 16 otherwise (more CTAs for short G).
+// p <= 2^16 takes the tensor-core form (trsm_tc.cu) unless RL_TRSM_TC=0
+#ifndef RL_TRSM_TC
+#define RL_TRSM_TC 1
+#endif
 void trsm_node(const TrsmNodeArgs& a, cudaStream_t s) {
     if ((a.M <= 0 && !a.ninv) || a.nleaf <= 0) return;
     const bool sp = a.f.p <= 65536u;
+    if (RL_TRSM_TC && sp) {
+        trsm_node_tc(a, s);
+        return;
+    }
     if (a.M >= 32 * num_sms()) {
         if (sp) launch_node<true, 2, 1>(a, s);
         else launch_node<false, 2, 1>(a, s);

@@ -9,7 +9,7 @@ OUT=$ROOT/tools/variants/build_$NAME
 mkdir -p $OUT
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 pids=()
-for f in runtime util gemm_tc bridge panel panel_window trsm perm cup batched tri dist capi; do
+for f in runtime util gemm_tc bridge trsm_tc panel panel_window trsm perm cup batched tri dist capi; do
   /usr/local/cuda/bin/nvcc $ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr $FLAGS \
     -c -o $OUT/$f.o $SRC/$f.cu &
   pids+=($!)
