@@ -473,9 +473,11 @@ void CupEngine::trsm_right(i32 r0, i32 M, i32 x0, i32 mx) {
         a.f = f_;
         flush_swaps();
         // first TRSM against X also leaves U_X^{-1} -- only where a taller TRSM can
-        // use it (gemm_ninv needs >= 2 leaves): one-leaf solves skip the extra rows
-        a.ninv = (have || mx < 2 * PB) ? nullptr : ninv;
-        ninv_done_.insert(key);
+        // use it: a node of more than two leaves (a TRSM against a node of <= 2
+        // leaves solves at most as many rows as the node has, M < kNinvGemmMinRows)
+        const bool want = !have && mx > 2 * PB;
+        a.ninv = want ? ninv : nullptr;
+        if (want) ninv_done_.insert(key);
         trsm_node(a, work_stream());
         stats_.trsm_leaves++;
         stats_.launches += 1;
