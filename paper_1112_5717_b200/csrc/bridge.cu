@@ -159,6 +159,10 @@ __global__ void __launch_bounds__(256, 1) bridge_kernel(BridgeArgs a) {
     const u32* A = a.A;
     const i64 lda = a.lda, row0 = a.row0;
     stage(Xr, XP, PB, PB, M, nl, lda4 && (j_lo & 3) == 0, [&](int r) { return A + (row0 + r) * lda + j_lo; });
+    if (a.uready) {  // the leaf's U^{-1} comes from a kernel on another stream
+        if (tid == 0) uready_wait(a.uready, a.epoch);
+        __syncthreads();
+    }
     stage(Ir, XP, PB, PB, nl, nl, (reinterpret_cast<uintptr_t>(a.uinv) & 15) == 0,
           [&](int r) { return a.uinv + r * PB; });
     stage(Cr, UP, PB, PW, M, ns, lda4 && (n_lo & 3) == 0, [&](int r) { return A + (row0 + r) * lda + n_lo; });

@@ -177,6 +177,22 @@ __device__ __forceinline__ void imma16832(int (&d)[4], const u32 (&a)[4], const 
         : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
 }
+// U^{-1}-ready flags (cup.cu): a leaf's flag holds the factorization's epoch once
+// its U^{-1} is in global memory; consumers wait on it instead of on a stream event.
+__device__ __forceinline__ void uready_set(i32* flag, const i32* epoch) {
+    __threadfence();
+    const i32 v = __ldcg(epoch);
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
+}
+__device__ __forceinline__ void uready_wait(const i32* flag, const i32* epoch) {
+    const i32 want = __ldcg(epoch);
+    for (;;) {
+        i32 v;
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+        if (v == want) break;
+        __nanosleep(64);
+    }
+}
 __device__ __forceinline__ i32 dyn_eval(const Dyn& d, const i32* rp) {
     return (d.idx >= 0 ? __ldcg(rp + d.idx) : 0) + d.cst;
 }

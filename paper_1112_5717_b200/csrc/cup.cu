@@ -54,7 +54,8 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
     const size_t o_ps = o_ipiv + up(sizeof(i32) * (k + 1));
     const size_t o_uinv = o_ps + up(sizeof(PanelScratch));
     const size_t o_flags = o_uinv + up(sizeof(u32) * PB * PB * (leaf_of_.size() + 1));
-    const size_t o_tab = o_flags + up(sizeof(i32) * (leaf_of_.size() + 1));
+    const size_t o_uready = o_flags + up(sizeof(i32) * (leaf_of_.size() + 1));
+    const size_t o_tab = o_uready + up(sizeof(i32) * (leaf_of_.size() + 2));
     const size_t o_ninv = o_tab + up(p_ <= 65536u ? 65536 * sizeof(uint16_t) : 0);
     const size_t total = o_ninv + sizeof(u32) * NINV_LD * NINV_LD * ninv_slot_.size();
     RL_CUDA_CHECK(cudaMalloc(&meta_, total));
@@ -71,6 +72,10 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
     uinv_ = reinterpret_cast<u32*>(base + o_uinv);
     swapflags_ = reinterpret_cast<i32*>(base + o_flags);
     RL_CUDA_CHECK(cudaMemsetAsync(swapflags_, 0, sizeof(i32) * (leaf_of_.size() + 1), init_s));
+    uready_ = reinterpret_cast<i32*>(base + o_uready);
+    epoch_ = uready_ + leaf_of_.size() + 1;
+    RL_CUDA_CHECK(cudaMemsetAsync(uready_, 0, sizeof(i32) * (leaf_of_.size() + 2), init_s));
+    uflags_ = p_ <= 65536u && fused_trsm_ && RL_UREADY;
     leaf_starts_.assign(leaf_of_.size(), 0);
     for (const auto& kv : leaf_of_) leaf_starts_[kv.second] = kv.first;
     ninv_ = ninv_slot_.empty() ? nullptr : reinterpret_cast<u32*>(base + o_ninv);
@@ -261,6 +266,8 @@ void CupEngine::panel(i32 i0, i32 b) {
     PanelArgs a{};
     a.uinv = uinv_ + (size_t)leaf_of_.at(i0) * PB * PB;
     a.swapflag = swapflags_ + leaf_of_.at(i0);
+    a.uready = uready_ + leaf_of_.at(i0);
+    a.epoch = epoch_;
     a.inv_table = inv_table_;
     a.A = A_;
     a.lda = lda_;
@@ -467,7 +474,9 @@ void CupEngine::trsm_right(i32 r0, i32 M, i32 x0, i32 mx) {
             a.j_lo[l] = dyn_rp(lv[l].first);
             a.j_hi[l] = dyn_rp(lv[l].first + lv[l].second);
             a.uinv[l] = uinv_ + (size_t)leaf_of_.at(lv[l].first) * PB * PB;
+            a.uready[l] = uflags_ ? uready_ + leaf_of_.at(lv[l].first) : nullptr;
         }
+        a.epoch = epoch_;
         a.rp = rp_;
         a.rrp = rrp_;
         a.f = f_;
@@ -523,6 +532,8 @@ BridgeArgs CupEngine::leaf_bridge(i32 leaf, i32 leaf_end, i32 row0, i32 M, Dyn n
     a.rrp = rrp_;
     a.ipiv = ipiv_;
     a.uinv = uinv_ + (size_t)leaf_of_.at(leaf) * PB * PB;
+    a.uready = uflags_ ? uready_ + leaf_of_.at(leaf) : nullptr;
+    a.epoch = epoch_;
     a.swapflag = swapflags_ + leaf_of_.at(leaf);
     a.ps = ps_;
     a.f = f_;
@@ -613,7 +624,7 @@ void CupEngine::node(i32 i0, i32 mm) {
         // instead of after it on the critical path
         flush_swaps();
     }
-    if (!dry_ && uinv_join_) {
+    if (!dry_ && uinv_join_ && !uflags_) {  // (with the flags its readers wait on the device)
         RL_CUDA_CHECK(cudaStreamWaitEvent(s_, uinv_join_, 0));
         uinv_join_ = nullptr;
     }
@@ -852,7 +863,9 @@ void CupEngine::build_big_inverse(i32 x0, i32 mm) {
                 a.j_lo[l] = dyn_rp(lv[l].first);
                 a.j_hi[l] = dyn_rp(lv[l].first + lv[l].second);
                 a.uinv[l] = uinv_ + (size_t)leaf_of_.at(lv[l].first) * PB * PB;
+                a.uready[l] = uflags_ ? uready_ + leaf_of_.at(lv[l].first) : nullptr;
             }
+            a.epoch = epoch_;
             a.rp = rp_;
             a.rrp = rrp_;
             a.f = f_;
@@ -957,7 +970,7 @@ void CupEngine::tiled(i32 g) {
         wait_rows(s_, a, b0);
         swaps_range(a, g2, dyn_rp(i0), dyn_rp(a), i0, a);           // factor.cpp:42
         flush_swaps();
-        if (!dry_ && uinv_join_) {  // the last leaf's U^{-1}
+        if (!dry_ && uinv_join_ && !uflags_) {  // the last leaf's U^{-1}
             RL_CUDA_CHECK(cudaStreamWaitEvent(s_, uinv_join_, 0));
             uinv_join_ = nullptr;
         }
@@ -1026,6 +1039,7 @@ void CupEngine::enqueue(u32* dA, cudaStream_t s) {
     lane_ = nullptr;
     early_used_ = false;
     fill_rp0(rp_, s);
+    bump_epoch(epoch_, s);  // this run's value of the U^{-1}-ready flags
     if (m_ > 0 && n_ > 0) {
         const bool tl = tiled_on();
         if (tl) tiled(tile_g_);

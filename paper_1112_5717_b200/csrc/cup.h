@@ -131,6 +131,15 @@ private:
     std::unordered_map<i32, i32> leaf_of_;     // leaf start row -> leaf index
     std::vector<i32> leaf_starts_;             // leaf start rows, increasing (index order)
     i32* swapflags_ = nullptr;                 // per leaf: made a transposition
+    // per leaf: U^{-1} written (== *epoch_, bumped at the start of every run);
+    // with uflags_ the bridge and the node TRSM wait on these on the device
+    // instead of the critical stream waiting for the U^{-1} kernel's event
+#ifndef RL_UREADY
+#define RL_UREADY 1
+#endif
+    i32* uready_ = nullptr;
+    i32* epoch_ = nullptr;
+    bool uflags_ = false;
     // node inverses U_X^{-1} of <= 4-leaf skeleton nodes X = (x0, mx): computed by
     // the first TRSM against X (as a by-product of its sweep), then reused by the
     // taller TRSMs above as one tensor-core GEMM each

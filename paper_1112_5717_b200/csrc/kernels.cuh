@@ -103,6 +103,8 @@ struct PanelArgs {
     u32* uinv;     // PB x PB: inverse of this leaf's unit upper pivot block
     const uint16_t* inv_table;  // p < 2^16: inv_table[x] = x^{-1} mod p (else unused)
     i32* swapflag;  // this leaf's "made a transposition" flag (read by the swap jobs)
+    i32* uready;    // this leaf's U^{-1}-ready flag (set to *epoch once uinv is written)
+    const i32* epoch;
     Fp f;
     // tail only: the launch has no cross-stream join, so its programmatic
     // predecessor (the window) is the only kernel that may still run when its
@@ -144,6 +146,8 @@ struct TrsmNodeArgs {
     int nleaf;
     Dyn j_lo[TN_MAXLEAF], j_hi[TN_MAXLEAF];
     const u32* uinv[TN_MAXLEAF];
+    const i32* uready[TN_MAXLEAF];  // when set: wait for each leaf's U^{-1} (== *epoch)
+    const i32* epoch;
     const i32* rp;
     const i32* rrp;
     Fp f;
@@ -176,6 +180,8 @@ struct BridgeArgs {
     const i32* rrp;
     const i32* ipiv;
     const u32* uinv;      // the top leaf's U^{-1} (PB x PB)
+    const i32* uready;    // when set: wait for it (== *epoch) before reading uinv
+    const i32* epoch;
     const i32* swapflag;  // the top leaf's "made a transposition" flag
     const PanelScratch* ps;  // the top leaf's panel scratch (dead_mask)
     Fp f;
@@ -220,6 +226,7 @@ void compact_u_rows(u32* A, i64 lda, i32 m, i32 n, const i32* rp, const i32* rrp
 void gen_random_matrix(u32* A, i64 lda, i64 m, i64 n, u64 seed, u32 p, cudaStream_t s);
 
 void fill_rp0(i32* rp, cudaStream_t s);
+void bump_epoch(i32* epoch, cudaStream_t s);
 
 // Data plane of the distributed CUP (dist.cu, paper_1112_5717_b200/dist.py).
 void dist_pack(const u32* src, i64 lds, i64 rows, i64 cols, int wire16, void* dst, cudaStream_t s);

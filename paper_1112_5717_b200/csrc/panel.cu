@@ -491,9 +491,12 @@ __global__ void __launch_bounds__(256) panel_tail_kernel(PanelArgs a) {
         const int r2 = ps->r;
         if (r2 > 0) leaf_uinv<SP>(a, c0, r2, Us, Xs, Ts);
     }
+    __syncthreads();
     if (tid == 0) {
         ps->counter = 0;
         ps->flag = 0;
+        // U^{-1} of a leaf with window-dead rows (or no window) is final only now
+        if (a.uready) uready_set(a.uready, a.epoch);
     }
 }
 
@@ -559,10 +562,14 @@ __global__ void __launch_bounds__(512) panel_uinv_kernel(PanelArgs a) {
     extern __shared__ __align__(16) u32 tsm[];
     const PanelScratch* ps = a.ps;
     const i32 c0 = ps->c0, W = ps->W, rt = ps->r;
-    if (W <= 0 || rt <= 0 || ps->dead_mask != 0) return;
-    leaf_uinv<SP>(a, c0, rt, reinterpret_cast<u32 (*)[PB + 1]>(tsm),
-                  reinterpret_cast<u32 (*)[PB + 1]>(tsm + PB * (PB + 1)),
-                  reinterpret_cast<u32 (*)[PB + 1]>(tsm + 2 * PB * (PB + 1)));
+    // (W <= 0 or window-dead rows: the tail kernel computes U^{-1} and sets the flag)
+    if (W <= 0 || ps->dead_mask != 0) return;
+    if (rt > 0)
+        leaf_uinv<SP>(a, c0, rt, reinterpret_cast<u32 (*)[PB + 1]>(tsm),
+                      reinterpret_cast<u32 (*)[PB + 1]>(tsm + PB * (PB + 1)),
+                      reinterpret_cast<u32 (*)[PB + 1]>(tsm + 2 * PB * (PB + 1)));
+    __syncthreads();
+    if (threadIdx.x == 0 && a.uready) uready_set(a.uready, a.epoch);
 }
 
 }  // namespace

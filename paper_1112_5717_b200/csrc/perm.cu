@@ -265,4 +265,12 @@ void gen_random_matrix(u32* A, i64 lda, i64 m, i64 n, u64 seed, u32 p, cudaStrea
 
 void fill_rp0(i32* rp, cudaStream_t s) { RL_CUDA_CHECK(cudaMemsetAsync(rp, 0, sizeof(i32), s)); }
 
+namespace {
+__global__ void bump_epoch_kernel(i32* e) { *e += 1; }
+}  // namespace
+void bump_epoch(i32* epoch, cudaStream_t s) {
+    bump_epoch_kernel<<<1, 1, 0, s>>>(epoch);
+    RL_CUDA_CHECK(cudaGetLastError());
+}
+
 }  // namespace rl

@@ -117,6 +117,8 @@ __global__ void __launch_bounds__(256, 1) trsm_node_tc_kernel(TrsmNodeArgs a) {
         l2 = r;
     };
     u32* Tmp = Gs;  // TSTAGE blocks of PB x PB words
+    if (tid < nl_ && a.uready[tid] && hi[tid] > lo[tid]) uready_wait(a.uready[tid], a.epoch);
+    __syncthreads();
     const bool al = (a.lda & 3) == 0;
     for (int q0 = 0; q0 < nblk; q0 += TSTAGE) {
         const int nq = min(TSTAGE, nblk - q0);
