@@ -82,6 +82,7 @@ constexpr int WT = PW + PB;   // window + identity block (row transform)
 struct PanelScratch {
     i32 c0, W, w, r, b;
     i32 spec;      // the window took the speculative (no-transposition) path
+    i32 uinv_by_window;  // the window kernel already wrote U^{-1} (and set its flag)
     u32 flag;      // a window-dead row has a nonzero tail residual -> fallback
     u32 counter;   // last-CTA detection in the tail kernel
     u64 dead_mask;          // bit i: row i of the leaf has no pivot in the window

@@ -22,6 +22,7 @@
 
 #include "kernels.cuh"
 #include "runtime.h"
+#include "uinv.cuh"
 
 namespace rl {
 
@@ -29,40 +30,6 @@ namespace {
 
 constexpr int TT = 64;   // tail tile width (columns per CTA tile)
 constexpr int MIP = PB + 4;  // Minv pitch in the tail (16-byte rows for cp.async)
-
-// One doubling level of the unit-upper inverse: for every pair of SZ x SZ
-// diagonal blocks (A, B): X_AB = -X_AA * (U_AB * X_BB).  The sums run over the
-// full block width (X is zero below its diagonal), so the loops are fixed-length
-// and unrolled -- no per-thread trip counts, shared loads pipelined.
-template <bool SP, int SZ>
-__device__ __forceinline__ void uinv_level(u32 (*U)[PB + 1], u32 (*X)[PB + 1], u32 (*T)[PB + 1], int tid,
-                                           int nt, const Fp& f) {
-    constexpr int NOUT = (PB / (2 * SZ)) * SZ * SZ;
-    for (int e = tid; e < NOUT; e += nt) {
-        const int pb = e / (SZ * SZ), rem = e % (SZ * SZ), i = rem / SZ, j = rem % SZ;
-        const int A0 = pb * 2 * SZ, B0 = A0 + SZ;
-        u64 acc = 0;
-#pragma unroll
-        for (int u = 0; u < SZ; ++u) {
-            if (SP) acc += (u64)U[A0 + i][B0 + u] * X[B0 + u][B0 + j];
-            else acc += mulmod(U[A0 + i][B0 + u], X[B0 + u][B0 + j], f);
-        }
-        T[A0 + i][B0 + j] = SP ? red_sp(acc, f) : red64(acc, f);
-    }
-    __syncthreads();
-    for (int e = tid; e < NOUT; e += nt) {
-        const int pb = e / (SZ * SZ), rem = e % (SZ * SZ), i = rem / SZ, j = rem % SZ;
-        const int A0 = pb * 2 * SZ, B0 = A0 + SZ;
-        u64 acc = 0;
-#pragma unroll
-        for (int u = 0; u < SZ; ++u) {
-            if (SP) acc += (u64)X[A0 + i][A0 + u] * T[A0 + u][B0 + j];
-            else acc += mulmod(X[A0 + i][A0 + u], T[A0 + u][B0 + j], f);
-        }
-        X[A0 + i][B0 + j] = negmod(SP ? red_sp(acc, f) : red64(acc, f), f);
-    }
-    __syncthreads();
-}
 
 // Inverse of the leaf's unit upper pivot block U (r x r, rows rrp[c0+j],
 // columns c0+j'), into uinv (PB x PB, zero padded).  Recursive doubling: the
@@ -73,7 +40,7 @@ template <bool SP>
 __device__ void leaf_uinv(const PanelArgs& a, i32 c0, int rt, u32 (*U)[PB + 1], u32 (*X)[PB + 1],
                           u32 (*T)[PB + 1]) {
     const Fp f = a.f;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nt = blockDim.x;
+    const int tid = threadIdx.x, nt = blockDim.x;
     RL_STAMP(u0);
     __shared__ i32 s_row[PB];
     if (tid < PB) s_row[tid] = tid < rt ? __ldcg(a.rrp + c0 + tid) : 0;
@@ -92,31 +59,11 @@ __device__ void leaf_uinv(const PanelArgs& a, i32 c0, int rt, u32 (*U)[PB + 1], 
 #ifdef RL_TRACE
     const long long c2 = clock64();
 #endif
-    // diagonal blocks: warp w, lane c < 8 -> column c of block w
-    if (warp < 8 && lane < 8) {
-        const int base = 8 * warp, c = lane;
-        u32 x[8];
-#pragma unroll
-        for (int i = 7; i >= 0; --i) {
-            u64 acc = 0;
-#pragma unroll
-            for (int k = i + 1; k < 8; ++k)
-                acc += SP ? (u64)U[base + i][base + k] * x[k] : (u64)mulmod(U[base + i][base + k], x[k], f);
-            const u32 sum = SP ? red_sp(acc, f) : red64(acc, f);
-            const u32 d = (i == c && base + i < rt) ? 1u % f.p : 0u;
-            x[i] = i > c ? 0u : submod(d, sum, f);
-        }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) X[base + i][base + c] = x[i];
-    }
-    __syncthreads();
-    RL_STAMP(u3);
+    uinv_solve<SP>(U, X, T, rt, f);
 #ifdef RL_TRACE
     const long long c3 = clock64();
 #endif
-    uinv_level<SP, 8>(U, X, T, tid, nt, f);
-    uinv_level<SP, 16>(U, X, T, tid, nt, f);
-    uinv_level<SP, 32>(U, X, T, tid, nt, f);
+    RL_STAMP(u3);
     RL_STAMP(u4);
     for (int e = tid; e < PB * PB; e += nt) a.uinv[e] = X[e / PB][e % PB];
     __syncthreads();
@@ -563,7 +510,7 @@ __global__ void __launch_bounds__(512) panel_uinv_kernel(PanelArgs a) {
     const PanelScratch* ps = a.ps;
     const i32 c0 = ps->c0, W = ps->W, rt = ps->r;
     // (W <= 0 or window-dead rows: the tail kernel computes U^{-1} and sets the flag)
-    if (W <= 0 || ps->dead_mask != 0) return;
+    if (W <= 0 || ps->dead_mask != 0 || ps->uinv_by_window) return;
     if (rt > 0)
         leaf_uinv<SP>(a, c0, rt, reinterpret_cast<u32 (*)[PB + 1]>(tsm),
                       reinterpret_cast<u32 (*)[PB + 1]>(tsm + PB * (PB + 1)),

@@ -24,6 +24,7 @@
 
 #include "kernels.cuh"
 #include "runtime.h"
+#include "uinv.cuh"
 
 namespace rl {
 
@@ -35,6 +36,14 @@ namespace {
 // update (measured: window LU 21.7 -> 20.1 us, C3 21.66 -> 21.38 ms).
 #ifndef RL_LA_ISOLATE
 #define RL_LA_ISOLATE 1
+#endif
+
+// The leaf's U^{-1} computed at the end of the window kernel for a full
+// speculative leaf (1) or only by the parallel U^{-1} kernel (0).  Measured: the
+// leaf-pair transition drops 22.1 -> 17.4 us, but the window grows 27 -> 35 us
+// (the doubling levels on CUDA cores): C3 21.45 vs 20.15 ms, so off.
+#ifndef RL_WIN_UINV
+#define RL_WIN_UINV 0
 #endif
 
 // row pitch (words) of the staged window: WT = 192 would put every row of a
@@ -534,6 +543,7 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
     if (tid == 0) {
         ps->flag = 0;
         ps->counter = 0;
+        ps->uinv_by_window = 0;
         ps->c0 = c0;
         ps->b = b;
         ps->W = W > 0 ? W : 0;
@@ -810,6 +820,33 @@ __global__ void __launch_bounds__(NW * 32, 1) panel_window_kernel(PanelArgs a) {
         t_mid = rl_now();
 #endif
         LT_MARK(a.i0 / PB, 4);
+#if RL_WIN_UINV
+        if (SP && a.uready) {
+            // The leaf's U^{-1} here, from the normalised pivot block still in shared
+            // memory (the inverse table's space is free after the LU): the readers
+            // (bridge, node TRSM) then need not wait for the parallel U^{-1} kernel
+            u32 (*Uw)[PB + 1] = reinterpret_cast<u32 (*)[PB + 1]>(dsm + PB * RP * 4);
+            u32 (*Xw)[PB + 1] = Uw + PB;
+            u32 (*Tw)[PB + 1] = Xw + PB;
+            for (int e = tid; e < PB * PB; e += blockDim.x) {
+                const int i = e / PB, kk = e % PB;
+                Uw[i][kk] = kk > i ? mulmod_t<SP>(s_R[i * RP + kk], s_pinvA[i], f) : 0u;
+                Xw[i][kk] = 0u;
+            }
+            __syncthreads();
+            uinv_solve<SP>(Uw, Xw, Tw, PB, f);
+            for (int e = tid; e < PB * PB / 4; e += blockDim.x) {
+                const int i = e >> 4, kk = (e & 15) << 2;
+                *reinterpret_cast<uint4*>(a.uinv + i * PB + kk) =
+                    make_uint4(Xw[i][kk], Xw[i][kk + 1], Xw[i][kk + 2], Xw[i][kk + 3]);
+            }
+            __syncthreads();
+            if (tid == 0) {
+                ps->uinv_by_window = 1;
+                uready_set(a.uready, a.epoch);
+            }
+        }
+#endif
     } else if (spec) {
         // live row k' (original row s_perm[k']) has its pivot at column k': C
         // left of it, the raw pivot, U = reduced value * pivot^{-1} right of it;
