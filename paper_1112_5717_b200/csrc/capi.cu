@@ -502,6 +502,23 @@ void cup_host_overlapped_tiles(u32* A, i64 m, i64 n, i64 lda, u32 p, u32* dA, Sc
 // then fills tile t + 1 while tile t crosses the link and the factorization runs.
 constexpr int kPgSlots = 3;
 
+// cuStreamWaitValue32 through the runtime's driver entry-point lookup: no link
+// dependency on libcuda, so the library still loads on a machine without a
+// driver (where every compute entry fails with RL_ECUDA instead).
+using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WaitValueFn wait_value_fn() {
+    static WaitValueFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<WaitValueFn>(p);
+    }();
+    if (!fn) throw Error(RL_ECUDA, "cuStreamWaitValue32 unavailable");
+    return fn;
+}
+
 void cup_host_pageable_tiles(u32* A, i64 m, i64 n, i64 lda, u32 p, u32* dA, Scratch& sc, cudaStream_t s,
                              i64* r, std::vector<u32>& rrp_h, std::vector<u32>& ipiv_h,
                              const std::shared_ptr<CupEngine>& e) {
@@ -529,7 +546,7 @@ void cup_host_pageable_tiles(u32* A, i64 m, i64 n, i64 lda, u32 p, u32* dA, Scra
     CupEngine::RowEvents in, out;
     std::vector<cudaEvent_t> ev_in(T, nullptr), ev_d2h(T, nullptr);
     for (i64 t = 1; t < T; ++t) {
-        auto st = cuStreamWaitValue32((CUstream)cs, f_in, (cuuint32_t)t, CU_STREAM_WAIT_VALUE_GEQ);
+        auto st = wait_value_fn()((CUstream)cs, f_in, (cuuint32_t)t, CU_STREAM_WAIT_VALUE_GEQ);
         if (st != CUDA_SUCCESS) throw Error(RL_ECUDA, "cuStreamWaitValue32 failed");
         copy_h2d_2d(dA + t * g * n, n, ring_in + (size_t)(t % kPgSlots) * slot, n, rows_of(t), n, cs);
         ev_in[t] = sc.event(2 * kRing + 1 + (int)t);
@@ -547,8 +564,8 @@ void cup_host_pageable_tiles(u32* A, i64 m, i64 n, i64 lda, u32 p, u32* dA, Scra
     for (i64 t = 0; t + 1 < T; ++t) {
         RL_CUDA_CHECK(cudaStreamWaitEvent(cs2, out[(size_t)t].second, 0));
         if (t >= kPgSlots) {  // the slot's previous tile drained by the host
-            auto st = cuStreamWaitValue32((CUstream)cs2, f_out, (cuuint32_t)(t - kPgSlots + 1),
-                                          CU_STREAM_WAIT_VALUE_GEQ);
+            auto st = wait_value_fn()((CUstream)cs2, f_out, (cuuint32_t)(t - kPgSlots + 1),
+                                      CU_STREAM_WAIT_VALUE_GEQ);
             if (st != CUDA_SUCCESS) throw Error(RL_ECUDA, "cuStreamWaitValue32 failed");
         }
         copy_d2h_2d(ring_out + (size_t)(t % kPgSlots) * slot, n, dA + t * g * n, n, rows_of(t), n, cs2);

@@ -525,7 +525,10 @@ void panel_uinv(const PanelArgs& a, cudaStream_t s) {
     // The kernel needs 3 blocks of PB x (PB+1); it asks for 200 KB so that no
     // tail-kernel CTA (launched right after it) shares its SM: this latency-bound
     // chain ran ~3x slower beside the tail's multiply-add streams.
-    const size_t smem = std::max<size_t>(sizeof(u32) * 3 * PB * (PB + 1), 200 * 1024);
+#ifndef RL_UINV_SMEM_KB
+#define RL_UINV_SMEM_KB 200
+#endif
+    const size_t smem = std::max<size_t>(sizeof(u32) * 3 * PB * (PB + 1), RL_UINV_SMEM_KB * 1024);
     static std::atomic<unsigned long long> attr_once{0};
     once_on_device(attr_once, [&] {
         RL_CUDA_CHECK(cudaFuncSetAttribute(panel_uinv_kernel<true>,

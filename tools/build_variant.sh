@@ -15,5 +15,5 @@ for f in runtime util gemm_tc bridge trsm_tc panel panel_window trsm perm cup ba
   pids+=($!)
 done
 for p in "${pids[@]}"; do wait $p; done
-/usr/local/cuda/bin/nvcc $ARCH -shared -o $ROOT/tools/variants/lib$NAME.so $OUT/*.o -lcuda
+/usr/local/cuda/bin/nvcc $ARCH -shared -o $ROOT/tools/variants/lib$NAME.so $OUT/*.o
 echo "tools/variants/lib$NAME.so"
