@@ -104,8 +104,13 @@ __global__ void __launch_bounds__(256) cup_batched_kernel(u32* A, i64 stride, i3
 #ifndef RL_BATCHED_PR
 #define RL_BATCHED_PR 32
 #endif
+#ifndef RL_BATCHED_SB
+#define RL_BATCHED_SB 4  // rows per sub-block of a panel (4 or 8): see the panel loop
+#endif
 constexpr int PR = RL_BATCHED_PR;  // panel rows (16 or 32)
 constexpr int BN = 256;
+constexpr int SB = RL_BATCHED_SB;
+static_assert(SB == 4 || SB == 8, "row blocks of 4 or 8");
 #ifndef RL_BATCHED_DMMA
 #define RL_BATCHED_DMMA 2  // trailing updates on the FP64 tensor cores (m8n8k4 DMMA); 2: trailing_dmma
 #endif
@@ -145,6 +150,8 @@ constexpr int UDS = BN - PR + 8;  // Ud row stride (doubles), >= BN - PR, = 8 (m
 // its negation moves from the accumulator layout to the A-operand layout by
 // shuffles and sweeps the row block's column tiles (C prefetched one tile ahead).
 // smem: Ud = U_rest as doubles [PR][UDS], Xd = U_pp^{-1} as doubles [PR][XDS].
+__device__ __forceinline__ int upk_idx(int k, int i) { return k * (2 * PR - 1 - k) / 2 + (i - k - 1); }
+
 __device__ __noinline__ void trailing_dmma(u32* a, int m, int n, const Fp& f, int i0, int pr, int r0, int np,
                                            const i32* s_prow, double* sm) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q4 = lane & 3;
@@ -152,13 +159,37 @@ __device__ __noinline__ void trailing_dmma(u32* a, int m, int n, const Fp& f, in
     const double pd = (double)f.p, ipd = 1.0 / pd;
     double* Ud = sm;                 // [PR][UDS]
     double* Xd = sm + PR * UDS;      // [PR][XDS]
-    // (a) U_rest -> Ud; U_pp^{-1} by recursive doubling into Xd (identity past np)
-    for (int e = tid; e < PR * (UDS / 8); e += 256) {
-        const int j = e / (UDS / 8), c0 = (e % (UDS / 8)) * 8;
-        const u32* src = a + (i64)(i0 + (j < np ? s_prow[j] : 0)) * n + cend + c0;
+    // (a) U_rest -> Ud, converted in place from the panel rows still in shared
+    // memory (P = u64 [PR][BN] under Ud): 16 rows per round, every thread loads
+    // its words, a barrier, then the stores -- a round's destinations end below
+    // the next round's sources (16 (q + 1) * UDS * 8 <= 16 (q + 1) * BN * 8 and pivot
+    // row j sits in panel row s_prow[j] >= j), so one barrier per round is enough.
+    // U_pp (the strict upper triangle, packed) was put aside at Upk by the caller.
+    const u64* Pp = reinterpret_cast<const u64*>(sm);
+    const u32* Upk = reinterpret_cast<const u32*>(sm + PR * UDS + PR * XDS + 256);
+    for (int q = 0; q < PR / 16; ++q) {
+        u32 w[2][8];
 #pragma unroll
-        for (int z = 0; z < 8; ++z) Ud[j * UDS + c0 + z] = (j < np && c0 + z < N) ? (double)__ldcg(src + z) : 0.0;
+        for (int h = 0; h < 2; ++h) {
+            const int e = tid + 256 * h;
+            const int j = 16 * q + e / (UDS / 8), c0 = (e % (UDS / 8)) * 8;
+            const bool on = e < 16 * (UDS / 8) && j < np;
+            const u64* src = Pp + (on ? s_prow[j] : 0) * BN + cend + c0;
+#pragma unroll
+            for (int z = 0; z < 8; ++z) w[h][z] = (on && c0 + z < N) ? (u32)src[z] : 0u;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int e = tid + 256 * h;
+            const int j = 16 * q + e / (UDS / 8), c0 = (e % (UDS / 8)) * 8;
+            if (e < 16 * (UDS / 8)) {
+#pragma unroll
+                for (int z = 0; z < 8; ++z) Ud[j * UDS + c0 + z] = (double)w[h][z];
+            }
+        }
     }
+    // Xd overlaps the last panel rows: every load above is behind a barrier
     {   // diagonal 8 x 8 blocks: thread = (block, column), back substitution
         const int t = tid;
         if (t < PR) {
@@ -177,8 +208,7 @@ __device__ __noinline__ void trailing_dmma(u32* a, int m, int n, const Fp& f, in
                     for (int ii = kk + 1; ii < 8; ++ii) {
                         if (ii <= c) {
                             const int i = 8 * b + ii;
-                            const double u = (k < np && i < np)
-                                ? (double)__ldcg(a + (i64)(i0 + s_prow[k]) * n + r0 + i) : 0.0;
+                            const double u = (k < np && i < np) ? (double)Upk[upk_idx(k, i)] : 0.0;
                             acc = fma(u, x[ii], acc);
                         }
                     }
@@ -203,8 +233,7 @@ __device__ __noinline__ void trailing_dmma(u32* a, int m, int n, const Fp& f, in
             double acc = 0.0;
             for (int i = 0; i < h; ++i) {
                 const int ib = q * 2 * h + h + i;
-                const double u = (ka < np && ib < np)
-                    ? (double)__ldcg(a + (i64)(i0 + s_prow[ka]) * n + r0 + ib) : 0.0;
+                const double u = (ka < np && ib < np) ? (double)Upk[upk_idx(ka, ib)] : 0.0;
                 acc = fma(u, Xd[ib * XDS + jb], acc);
             }
             T[(q * h + rr) * 16 + cc] = dmod(acc, pd, ipd);
@@ -290,11 +319,12 @@ __device__ __noinline__ void trailing_dmma(u32* a, int m, int n, const Fp& f, in
 }
 
 template <bool LAZY>
-__global__ void __launch_bounds__(256) cup_batched_blk_kernel(u32* A, i64 stride, i32 m, i32 n, Fp f,
+__global__ void __launch_bounds__(256, 3) cup_batched_blk_kernel(u32* A, i64 stride, i32 m, i32 n, Fp f,
                                                               i32* ranks, i32* rrp_out, i32* ipiv_out,
                                                               i32 kcap, const u32* __restrict__ inv_tab) {
     extern __shared__ __align__(16) u64 P[];             // [PR][BN] panel rows, lazy sums
     u32* wbuf = reinterpret_cast<u32*>(P + PR * BN);     // [8][BN] per-warp row buffer
+    u32* s_fd = wbuf;  // [PR][SB] during the panel phase: multipliers of the row block's pivots
     __shared__ i32 s_rrp[BN], s_ipiv[BN], s_prow[PR];
     __shared__ u32 s_f[PR];
     __shared__ int s_wmin[8];
@@ -309,9 +339,43 @@ __global__ void __launch_bounds__(256) cup_batched_blk_kernel(u32* A, i64 stride
         for (int t = warp; t < pr; t += 8)
             for (int c = lane; c < n; c += 32) P[t * BN + c] = a[(i64)(i0 + t) * n + c];
         __syncthreads();
-        // ---- panel: rows in order
+        // ---- panel: rows in order, in row blocks of SB.  A pivot updates at once
+        // only what the next steps read: its row block's remaining rows (every
+        // thread its own column) and, for the rows below the row block, the SB
+        // columns [bs_r, bs_r + SB) that hold this block's pivots -- the source of
+        // the multipliers -- one entry per thread.  The other columns of the rows
+        // below get the block's (at most SB) pivots in one pass when the block
+        // ends (flush: one shared-memory round trip per row instead of one per
+        // pivot; the normalised pivot entries of the own column stay in
+        // registers, the multipliers in s_fd).  Same sums, grouped differently.
+        int kb_end = min(SB, pr) - 1, bs_r = r, nb = 0;
+        u32 ureg[SB];
+#pragma unroll
+        for (int j = 0; j < SB; ++j) ureg[j] = 0;
+        auto flush = [&]() {
+            const int c = tid;
+            if (nb > 0 && c < n && c >= bs_r + SB) {
+                for (int t = kb_end + 1; t < pr; ++t) {
+                    u64 x = P[t * BN + c];
+                    u32 fm[SB];
+#pragma unroll
+                    for (int j4 = 0; j4 < SB; j4 += 4)
+                        *reinterpret_cast<uint4*>(fm + j4) = *reinterpret_cast<const uint4*>(s_fd + t * SB + j4);
+#pragma unroll
+                    for (int j = 0; j < SB; ++j)
+                        if (j < nb) x = lazy_fma<LAZY>(x, fm[j], ureg[j], f);
+                    P[t * BN + c] = x;
+                }
+            }
+            nb = 0;
+        };
         for (int k = 0; k < pr && r < n; ++k) {
             const int c = tid;
+            if (k > kb_end) {  // next row block
+                flush();
+                kb_end = min(kb_end + SB, pr - 1);
+                bs_r = r;
+            }
             u32 v = 0;
             if (c < n && c >= r) {
                 v = LAZY ? red64(P[k * BN + c], f) : (u32)P[k * BN + c];
@@ -328,6 +392,9 @@ __global__ void __launch_bounds__(256) cup_batched_blk_kernel(u32* A, i64 stride
                 continue;
             }
             if (pc != r) {  // transposition r <-> pc on the panel rows and earlier U rows
+                flush();    // column pc receives its pending pivots before it moves
+                bs_r = r;
+                __syncthreads();
                 for (int t = tid; t < pr; t += 256) {
                     const u64 x = P[t * BN + r];
                     P[t * BN + r] = P[t * BN + pc];
@@ -355,11 +422,13 @@ __global__ void __launch_bounds__(256) cup_batched_blk_kernel(u32* A, i64 stride
                 u = mulmod((u32)P[k * BN + c], pinv, f);
                 P[k * BN + c] = u;
             }
-            // multipliers of the panel rows below (exact), then their lazy update
+            // multipliers of the panel rows below (exact)
             if (tid > k && tid < pr) {
                 const u32 fk = LAZY ? red64(P[tid * BN + r], f) : (u32)P[tid * BN + r];
                 P[tid * BN + r] = fk;  // raw C entry
-                s_f[tid] = fk ? f.p - fk : 0u;
+                const u32 nfk = fk ? f.p - fk : 0u;
+                s_f[tid] = nfk;
+                if (tid > kb_end) s_fd[tid * SB + nb] = nfk;
             }
             if (tid == 0) {
                 s_rrp[r] = i0 + k;
@@ -368,12 +437,23 @@ __global__ void __launch_bounds__(256) cup_batched_blk_kernel(u32* A, i64 stride
             }
             __syncthreads();
             if (c < n && c > r) {
-                for (int t = k + 1; t < pr; ++t) P[t * BN + c] = lazy_fma<LAZY>(P[t * BN + c], s_f[t], u, f);
+#pragma unroll
+                for (int j = 0; j < SB; ++j)
+                    if (j == nb) ureg[j] = u;
+                for (int t = k + 1; t <= kb_end; ++t)
+                    P[t * BN + c] = lazy_fma<LAZY>(P[t * BN + c], s_f[t], u, f);
             }
+            {   // the block's pivot columns on the rows below the row block
+                const int t = kb_end + 1 + tid / SB, cc = bs_r + tid % SB;
+                if (t < pr && cc > r && cc < n)
+                    P[t * BN + cc] = lazy_fma<LAZY>(P[t * BN + cc], s_f[t], (u32)P[k * BN + cc], f);
+            }
+            ++nb;
             ++r;
             // no barrier: the next row's pivot search reads only this thread's
             // own column, and everything shared is written after the next barrier
         }
+        flush();
         __syncthreads();
         // rows of the panel after the early return (r == n) keep their values;
         // reduce everything that is still lazy and write the panel back
@@ -382,13 +462,27 @@ __global__ void __launch_bounds__(256) cup_batched_blk_kernel(u32* A, i64 stride
                 const u64 x = P[t * BN + c];
                 a[(i64)(i0 + t) * n + c] = LAZY ? red64(x, f) : (u32)x;
             }
+        // the panel's unit upper pivot block U_pp (strict upper triangle, packed) is
+        // put aside for trailing_dmma while the panel is still in shared memory
+        const int np = r - r0;
+        if (LAZY && RL_BATCHED_DMMA == 2) {
+            u32* Upk = reinterpret_cast<u32*>(reinterpret_cast<double*>(P) + PR * UDS + PR * XDS + 256);
+            for (int e = tid; e < PR * PR; e += 256) {
+                const int k = e / PR, i = e % PR;
+                if (k < i && i < np) Upk[upk_idx(k, i)] = (u32)P[s_prow[k] * BN + r0 + i];
+            }
+        }
         __syncthreads();
         // ---- trailing rows
-        const int np = r - r0;
         bool any_swap = false;
         for (int j = r0; j < r; ++j) any_swap |= (s_ipiv[j] != j);
         static_assert(RL_BATCHED_DMMA == 2 || PR == 32, "the pre-v2 trailing paths assume 32-row panels");
-        if (LAZY && np > 0 && !any_swap && RL_BATCHED_DMMA == 2) {
+        static_assert((size_t)(PR * UDS + PR * XDS + 256) * 8 + (size_t)PR * (PR - 1) / 2 * 4 <=
+                          sizeof(u64) * PR * BN + sizeof(u32) * 8 * BN,
+                      "trailing_dmma's shared-memory layout must fit the kernel's dynamic allocation");
+        // trailing_dmma stages at most UDS columns right of the pivot block (a
+        // panel with fewer than PR - 8 pivots in a 256-column matrix has more)
+        if (LAZY && np > 0 && !any_swap && RL_BATCHED_DMMA == 2 && n - r <= UDS) {
             trailing_dmma(a, m, n, f, i0, pr, r0, np, s_prow, reinterpret_cast<double*>(P));
         } else if (LAZY && np > 0 && !any_swap) {
             // TRSM-then-GEMM form, two rows per warp: the multipliers of a row are

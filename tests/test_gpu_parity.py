@@ -211,6 +211,30 @@ def test_batched_small_primes_vs_oracle():
             assert np.array_equal(sig[t], o.sigma) and np.array_equal(body[t], a)
 
 
+def test_batched_wide_first_panel_few_pivots():
+    """256-column matrices whose leading 32-row panels hold few pivots (zero and
+    repeated rows): the trailing update then spans more than 224 columns right of
+    the panel's pivot block."""
+    import torch
+    rng = np.random.default_rng(77)
+    for p, batch in ((8388593, 66), (65521, 5)):
+        mats = rng.integers(0, p, (batch, 96, 256), dtype=np.uint64).astype(np.uint32)
+        mats[0, :16, :] = 0                 # 16 pivots in panel 0: 240 columns right of them
+        mats[1, 1:32, :] = 0                # a single pivot: 255 columns
+        mats[2, 4:32, :] = mats[2, 0, :]    # copies of row 0 eliminate to zero rows
+        mats[3, :40:2, :] = 0
+        mats[4, 8:30, :] = 0
+        dev = torch.from_numpy(mats.view(np.int32).copy()).cuda()
+        rk, rrp, sig = G.cup_batched_dev(dev, batch, 96, 256, p)
+        body = dev.cpu().numpy().view(np.uint32)
+        for t in range(min(batch, 8)):
+            a = mats[t].copy()
+            o = O.port_cup(a, p)
+            assert rk[t] == o.rank and np.array_equal(rrp[t, :o.rank], o.rrp), (p, t)
+            assert np.array_equal(sig[t], o.sigma), (p, t)
+            assert np.array_equal(body[t], a), (p, t, np.argwhere(body[t] != a)[:5])
+
+
 def test_large_properties_dev():
     """At full-size-class dimensions: structural outputs + Freivalds A = C*U*P."""
     import torch

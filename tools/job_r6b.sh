@@ -1,0 +1,8 @@
+#!/bin/bash
+# source-level ncu of the batched (config 4) kernel
+set -u
+OUT=gpurun_out/r6b
+mkdir -p $OUT
+timeout -s KILL 300 python tools/prof_c4.py > $OUT/c4_time.txt 2>&1
+timeout -s KILL 900 ncu --set full --import-source on --clock-control none -k regex:cup_batched_blk -c 1 \
+  -o $OUT/batched python tools/prof_c4.py > $OUT/ncu.log 2>&1
