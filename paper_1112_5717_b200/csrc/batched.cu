@@ -94,29 +94,26 @@ __global__ void __launch_bounds__(256) cup_batched_kernel(u32* A, i64 stride, i3
 // Blocked variant for n <= 256 (config 4): rows are taken in panels of PR = 32.
 // A panel is factored in shared memory row by row with the same pivot rule
 // (first nonzero at position >= r, transposition r <-> c applied to every row
-// that is not final, raw pivot, normalised U row), its rows kept as lazy 64-bit
-// sums that are reduced only when a row becomes the pivot candidate.  Every
-// trailing row is then updated once per panel by one warp (eager elimination
-// by the panel's pivots in order, lazy sums in registers, each multiplier
-// reduced exactly when it is read) instead of once per pivot through memory.
-// Lazy sums hold < 2^52 for p < 2^24 (at most 32 products < 2^46 per panel);
-// larger p reduce every product.
+// that is not final, raw pivot, normalised U row); its rows stay reduced u32
+// words (32 KB), the lazy 64-bit sums live in registers only (see the panel
+// loop).  Every trailing row is then updated once per panel: F = X_piv U_pp^{-1}
+// and X_rest -= F U_rest on the FP64 tensor cores (trailing_dmma), or pivot by
+// pivot by one warp per row when the panel held a transposition, p >= 2^24, or
+// the panel is too wide.  46 KB of shared memory per CTA: four CTAs per SM.
 #ifndef RL_BATCHED_PR
 #define RL_BATCHED_PR 32
 #endif
 #ifndef RL_BATCHED_SB
 #define RL_BATCHED_SB 4  // rows per sub-block of a panel (4 or 8): see the panel loop
 #endif
-constexpr int PR = RL_BATCHED_PR;  // panel rows (16 or 32)
+#ifndef RL_BATCHED_CTAS
+#define RL_BATCHED_CTAS 4  // CTAs per SM the register allocation is bounded for
+#endif
+constexpr int PR = RL_BATCHED_PR;  // panel rows
 constexpr int BN = 256;
 constexpr int SB = RL_BATCHED_SB;
+static_assert(PR == 32, "trailing_dmma's tiling assumes 32-row panels");
 static_assert(SB == 4 || SB == 8, "row blocks of 4 or 8");
-#ifndef RL_BATCHED_DMMA
-#define RL_BATCHED_DMMA 2  // trailing updates on the FP64 tensor cores (m8n8k4 DMMA); 2: trailing_dmma
-#endif
-#ifndef BATCHED_ROWS_PER_WARP
-#define BATCHED_ROWS_PER_WARP 1  // trailing rows per warp (more share the U loads, cost registers)
-#endif
 
 template <bool LAZY>
 __device__ __forceinline__ u64 lazy_fma(u64 acc, u32 nf, u32 u, const Fp& f) {
@@ -136,7 +133,25 @@ __device__ __forceinline__ void dmma844(double& c0, double& c1, double a, double
                  : "d"(a), "d"(b));
 }
 constexpr int XDS = 40;   // Xd row stride (doubles): rows 4 apart in banks -> 2 wavefronts per fragment load
-constexpr int UDS = BN - PR + 8;  // Ud row stride (doubles), >= BN - PR, = 8 (mod 16)
+constexpr int UDS = BN - PR + 8;  // Ud row stride (words), >= BN - PR, = 8 (mod 32): conflict-free fragments
+static_assert(UDS % 32 == 8 && UDS % 8 == 0, "Ud stride");
+// dynamic shared memory of cup_batched_blk_kernel (bytes)
+constexpr int OFF_P = 0;                        // u32 [PR][BN] panel rows (reduced)
+constexpr int OFF_UD = 0;                       // u32 [PR][UDS] U_rest, compacted in place from P
+constexpr int OFF_XD = OFF_P + 4 * PR * BN;     // double [PR][XDS] U_pp^{-1}
+constexpr int OFF_T = OFF_XD + 8 * PR * XDS;    // double [16][16] scratch of the doubling levels
+constexpr int OFF_UPK = OFF_T + 8 * 256;        // u32 [PR (PR - 1) / 2] strict upper triangle of U_pp
+constexpr int SMEM_BLK = OFF_UPK + 2048;
+constexpr int OFF_FD = OFF_XD;                  // u32 [PR][SB] panel phase: multipliers of the row block's pivots
+constexpr int OFF_WBUF = OFF_XD;                // u32 [8][BN] row buffers of the pivot-by-pivot trailing path
+static_assert(4 * PR * (PR - 1) / 2 <= 2048 && OFF_WBUF + 4 * 8 * BN <= SMEM_BLK && 4 * PR * SB <= 8 * PR * XDS,
+              "shared-memory layout");
+
+__device__ __forceinline__ int upk_idx(int k, int i) { return k * (2 * PR - 1 - k) / 2 + (i - k - 1); }
+// exact u32 -> double without the conversion pipe: 2^52 + w, minus 2^52
+__device__ __forceinline__ double u2d(u32 w) {
+    return __hiloint2double(0x43300000, (int)w) - 4503599627370496.0;
+}
 
 // The trailing rows of one panel (p < 2^24, no transposition in the panel), all
 // products on the FP64 tensor cores (mma.sync m8n8k4): with U_pp the panel's
@@ -149,24 +164,22 @@ constexpr int UDS = BN - PR + 8;  // Ud row stride (doubles), >= BN - PR, = 8 (m
 // 8 trailing rows at a time: F (4 n8 tiles) by 32 DMMA against U_pp^{-1}, then
 // its negation moves from the accumulator layout to the A-operand layout by
 // shuffles and sweeps the row block's column tiles (C prefetched one tile ahead).
-// smem: Ud = U_rest as doubles [PR][UDS], Xd = U_pp^{-1} as doubles [PR][XDS].
-__device__ __forceinline__ int upk_idx(int k, int i) { return k * (2 * PR - 1 - k) / 2 + (i - k - 1); }
-
+// U_rest stays u32 in shared memory (one wavefront per B fragment) and becomes
+// a double in the register (u2d).
 __device__ __noinline__ void trailing_dmma(u32* a, int m, int n, const Fp& f, int i0, int pr, int r0, int np,
-                                           const i32* s_prow, double* sm) {
+                                           const i32* s_prow, unsigned char* sm) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q4 = lane & 3;
     const int cend = r0 + np, N = n - cend;
     const double pd = (double)f.p, ipd = 1.0 / pd;
-    double* Ud = sm;                 // [PR][UDS]
-    double* Xd = sm + PR * UDS;      // [PR][XDS]
-    // (a) U_rest -> Ud, converted in place from the panel rows still in shared
-    // memory (P = u64 [PR][BN] under Ud): 16 rows per round, every thread loads
-    // its words, a barrier, then the stores -- a round's destinations end below
-    // the next round's sources (16 (q + 1) * UDS * 8 <= 16 (q + 1) * BN * 8 and pivot
-    // row j sits in panel row s_prow[j] >= j), so one barrier per round is enough.
-    // U_pp (the strict upper triangle, packed) was put aside at Upk by the caller.
-    const u64* Pp = reinterpret_cast<const u64*>(sm);
-    const u32* Upk = reinterpret_cast<const u32*>(sm + PR * UDS + PR * XDS + 256);
+    u32* Ud = reinterpret_cast<u32*>(sm + OFF_UD);        // [PR][UDS]
+    double* Xd = reinterpret_cast<double*>(sm + OFF_XD);  // [PR][XDS]
+    const u32* Pp = reinterpret_cast<const u32*>(sm + OFF_P);
+    const u32* Upk = reinterpret_cast<const u32*>(sm + OFF_UPK);
+    // (a) U_rest -> Ud, compacted in place from the panel rows (P under Ud): 16
+    // rows per round, every thread loads its words, a barrier, then the stores
+    // -- a round's destinations end below the next round's sources (pivot row j
+    // sits in panel row s_prow[j] >= j and UDS <= BN), so one barrier per round
+    // is enough.  U_pp (strict upper triangle, packed) was put aside at Upk.
     for (int q = 0; q < PR / 16; ++q) {
         u32 w[2][8];
 #pragma unroll
@@ -174,9 +187,9 @@ __device__ __noinline__ void trailing_dmma(u32* a, int m, int n, const Fp& f, in
             const int e = tid + 256 * h;
             const int j = 16 * q + e / (UDS / 8), c0 = (e % (UDS / 8)) * 8;
             const bool on = e < 16 * (UDS / 8) && j < np;
-            const u64* src = Pp + (on ? s_prow[j] : 0) * BN + cend + c0;
+            const u32* src = Pp + (on ? s_prow[j] : 0) * BN + cend + c0;
 #pragma unroll
-            for (int z = 0; z < 8; ++z) w[h][z] = (on && c0 + z < N) ? (u32)src[z] : 0u;
+            for (int z = 0; z < 8; ++z) w[h][z] = (on && c0 + z < N) ? src[z] : 0u;
         }
         __syncthreads();
 #pragma unroll
@@ -184,13 +197,12 @@ __device__ __noinline__ void trailing_dmma(u32* a, int m, int n, const Fp& f, in
             const int e = tid + 256 * h;
             const int j = 16 * q + e / (UDS / 8), c0 = (e % (UDS / 8)) * 8;
             if (e < 16 * (UDS / 8)) {
-#pragma unroll
-                for (int z = 0; z < 8; ++z) Ud[j * UDS + c0 + z] = (double)w[h][z];
+                *reinterpret_cast<uint4*>(Ud + j * UDS + c0) = make_uint4(w[h][0], w[h][1], w[h][2], w[h][3]);
+                *reinterpret_cast<uint4*>(Ud + j * UDS + c0 + 4) = make_uint4(w[h][4], w[h][5], w[h][6], w[h][7]);
             }
         }
     }
-    // Xd overlaps the last panel rows: every load above is behind a barrier
-    {   // diagonal 8 x 8 blocks: thread = (block, column), back substitution
+    {   // diagonal 8 x 8 blocks of U_pp^{-1}: thread = (block, column), back substitution
         const int t = tid;
         if (t < PR) {
             const int b = t >> 3, c = t & 7, j = 8 * b + c;
@@ -198,7 +210,7 @@ __device__ __noinline__ void trailing_dmma(u32* a, int m, int n, const Fp& f, in
 #pragma unroll
             for (int k = 0; k < 8; ++k) x[k] = 0.0;
             x[c] = 1.0;
-            // X[k][j] = -sum_{i=k+1..j} U[k][i] X[i][j]  (U[k][i] = pivot row k at column r0 + i)
+            // X[k][j] = -sum_{i=k+1..j} U[k][i] X[i][j]
 #pragma unroll
             for (int kk = 7; kk >= 0; --kk) {
                 if (kk < c) {
@@ -222,7 +234,7 @@ __device__ __noinline__ void trailing_dmma(u32* a, int m, int n, const Fp& f, in
     }
     __syncthreads();
     // two doubling levels: X_AB = -X_AA * (U_AB * X_BB) for blocks of 8, then 16
-    double* T = sm + PR * UDS + PR * XDS;  // scratch [16][16] (in the Ud tail is not free: own area)
+    double* T = reinterpret_cast<double*>(sm + OFF_T);  // scratch [16][16]
 #pragma unroll
     for (int h = 8; h <= PR / 2; h *= 2) {
         // pairs (A = [q*2h, q*2h+h), B = [q*2h+h, q*2h+2h)), entries of T = U_AB * X_BB
@@ -290,7 +302,7 @@ __device__ __noinline__ void trailing_dmma(u32* a, int m, int n, const Fp& f, in
             const int src = g * 4 + (ks & 1) * 2 + (q4 >> 1);
             const u32 v0 = __shfl_sync(0xffffffffu, nf[ks >> 1][0], src);
             const u32 v1 = __shfl_sync(0xffffffffu, nf[ks >> 1][1], src);
-            na[ks] = (double)((q4 & 1) ? v1 : v0);
+            na[ks] = u2d((q4 & 1) ? v1 : v0);
         }
         // sweep the column tiles: C <- C + (p - F) * U_rest
         u32* cr = xr + cend + 2 * q4;
@@ -301,15 +313,15 @@ __device__ __noinline__ void trailing_dmma(u32* a, int m, int n, const Fp& f, in
         }
         for (int tn = 0; tn < tN; ++tn) {
             const int cc = 8 * tn + 2 * q4;
-            double c0 = (double)n0, c1 = (double)n1;
+            double c0 = u2d(n0), c1 = u2d(n1);
             if (tn + 1 < tN && rok) {  // next tile's C in flight during this one's products
                 n0 = cc + 8 < N ? __ldcg(cr + 8 * (tn + 1)) : 0u;
                 n1 = cc + 9 < N ? __ldcg(cr + 8 * (tn + 1) + 1) : 0u;
             }
-            const double* ub = Ud + q4 * UDS + 8 * tn + g;
+            const u32* ub = Ud + q4 * UDS + 8 * tn + g;
 #pragma unroll
             for (int ks = 0; ks < KS; ++ks)
-                if (ks < ks_n) dmma844(c0, c1, na[ks], ub[4 * ks * UDS]);
+                if (ks < ks_n) dmma844(c0, c1, na[ks], u2d(ub[4 * ks * UDS]));
             if (rok) {
                 if (cc < N) cr[8 * tn] = (u32)dmod(c0, pd, ipd);
                 if (cc + 1 < N) cr[8 * tn + 1] = (u32)dmod(c1, pd, ipd);
@@ -318,13 +330,22 @@ __device__ __noinline__ void trailing_dmma(u32* a, int m, int n, const Fp& f, in
     }
 }
 
+// acc + nf * u with the sum kept below 2^64: lazily for p < 2^24 (LAZY), reduced
+// at every product otherwise
 template <bool LAZY>
-__global__ void __launch_bounds__(256, 3) cup_batched_blk_kernel(u32* A, i64 stride, i32 m, i32 n, Fp f,
-                                                              i32* ranks, i32* rrp_out, i32* ipiv_out,
-                                                              i32 kcap, const u32* __restrict__ inv_tab) {
-    extern __shared__ __align__(16) u64 P[];             // [PR][BN] panel rows, lazy sums
-    u32* wbuf = reinterpret_cast<u32*>(P + PR * BN);     // [8][BN] per-warp row buffer
-    u32* s_fd = wbuf;  // [PR][SB] during the panel phase: multipliers of the row block's pivots
+__device__ __forceinline__ u32 fma_red(u32 x, u32 nf, u32 u, const Fp& f) {
+    if (LAZY) return red64((u64)nf * u + x, f);
+    return addmod(x, mulmod(nf, u, f), f);
+}
+
+template <bool LAZY>
+__global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
+    u32* A, i64 stride, i32 m, i32 n, Fp f, i32* ranks, i32* rrp_out, i32* ipiv_out, i32 kcap,
+    const u32* __restrict__ inv_tab) {
+    extern __shared__ __align__(16) unsigned char smem_blk[];
+    u32* P = reinterpret_cast<u32*>(smem_blk + OFF_P);        // [PR][BN] panel rows, reduced
+    u32* s_fd = reinterpret_cast<u32*>(smem_blk + OFF_FD);    // [PR][SB] multipliers of the row block's pivots
+    u32* wbuf = reinterpret_cast<u32*>(smem_blk + OFF_WBUF);  // [8][BN] per-warp row buffer
     __shared__ i32 s_rrp[BN], s_ipiv[BN], s_prow[PR];
     __shared__ u32 s_f[PR];
     __shared__ int s_wmin[8];
@@ -345,9 +366,10 @@ __global__ void __launch_bounds__(256, 3) cup_batched_blk_kernel(u32* A, i64 str
         // columns [bs_r, bs_r + SB) that hold this block's pivots -- the source of
         // the multipliers -- one entry per thread.  The other columns of the rows
         // below get the block's (at most SB) pivots in one pass when the block
-        // ends (flush: one shared-memory round trip per row instead of one per
-        // pivot; the normalised pivot entries of the own column stay in
-        // registers, the multipliers in s_fd).  Same sums, grouped differently.
+        // ends (flush): one shared-memory round trip and one reduction per row
+        // instead of one per pivot, the lazy 64-bit sum (< 2^49 for p < 2^24) in
+        // a register, the normalised pivot entries of the own column in
+        // registers, the multipliers in s_fd.  Same sums, grouped differently.
         int kb_end = min(SB, pr) - 1, bs_r = r, nb = 0;
         u32 ureg[SB];
 #pragma unroll
@@ -356,32 +378,37 @@ __global__ void __launch_bounds__(256, 3) cup_batched_blk_kernel(u32* A, i64 str
             const int c = tid;
             if (nb > 0 && c < n && c >= bs_r + SB) {
                 for (int t = kb_end + 1; t < pr; ++t) {
-                    u64 x = P[t * BN + c];
                     u32 fm[SB];
 #pragma unroll
                     for (int j4 = 0; j4 < SB; j4 += 4)
                         *reinterpret_cast<uint4*>(fm + j4) = *reinterpret_cast<const uint4*>(s_fd + t * SB + j4);
+                    if (LAZY) {
+                        u64 x = P[t * BN + c];
 #pragma unroll
-                    for (int j = 0; j < SB; ++j)
-                        if (j < nb) x = lazy_fma<LAZY>(x, fm[j], ureg[j], f);
-                    P[t * BN + c] = x;
+                        for (int j = 0; j < SB; ++j)
+                            if (j < nb) x += (u64)fm[j] * ureg[j];
+                        P[t * BN + c] = red64(x, f);
+                    } else {
+                        u32 x = P[t * BN + c];
+#pragma unroll
+                        for (int j = 0; j < SB; ++j)
+                            if (j < nb) x = addmod(x, mulmod(fm[j], ureg[j], f), f);
+                        P[t * BN + c] = x;
+                    }
                 }
             }
             nb = 0;
         };
         for (int k = 0; k < pr && r < n; ++k) {
             const int c = tid;
-            if (k > kb_end) {  // next row block
+            if (k > kb_end) {  // next row block (barrier: row k's pivot columns were written by other threads)
+                __syncthreads();
                 flush();
                 kb_end = min(kb_end + SB, pr - 1);
                 bs_r = r;
             }
-            u32 v = 0;
-            if (c < n && c >= r) {
-                v = LAZY ? red64(P[k * BN + c], f) : (u32)P[k * BN + c];
-                P[k * BN + c] = v;
-            }
-            const unsigned msk = __ballot_sync(0xffffffffu, c < n && c >= r && v != 0);
+            const u32 v = (c < n && c >= r) ? P[k * BN + c] : 0u;
+            const unsigned msk = __ballot_sync(0xffffffffu, v != 0);
             if (lane == 0) s_wmin[warp] = msk ? warp * 32 + __ffs(msk) - 1 : BN;
             __syncthreads();
             int pc = s_wmin[0];
@@ -396,7 +423,7 @@ __global__ void __launch_bounds__(256, 3) cup_batched_blk_kernel(u32* A, i64 str
                 bs_r = r;
                 __syncthreads();
                 for (int t = tid; t < pr; t += 256) {
-                    const u64 x = P[t * BN + r];
+                    const u32 x = P[t * BN + r];
                     P[t * BN + r] = P[t * BN + pc];
                     P[t * BN + pc] = x;
                 }
@@ -410,22 +437,21 @@ __global__ void __launch_bounds__(256, 3) cup_batched_blk_kernel(u32* A, i64 str
             }
             u32 pinv;
             if (inv_tab) {  // p < 2^24: every thread loads the inverse (one cached word)
-                pinv = __ldg(inv_tab + (u32)P[k * BN + r]);
+                pinv = __ldg(inv_tab + P[k * BN + r]);
             } else {        // one thread runs the extended Euclid
-                if (tid == 0) s_pinv = inv_euclid((u32)P[k * BN + r], f.p);
+                if (tid == 0) s_pinv = inv_euclid(P[k * BN + r], f.p);
                 __syncthreads();
                 pinv = s_pinv;
             }
-            // normalised U row (reduced)
+            // normalised U row
             u32 u = 0;
             if (c < n && c > r) {
-                u = mulmod((u32)P[k * BN + c], pinv, f);
+                u = mulmod(P[k * BN + c], pinv, f);
                 P[k * BN + c] = u;
             }
-            // multipliers of the panel rows below (exact)
+            // multipliers of the panel rows below: column r holds the raw C entries
             if (tid > k && tid < pr) {
-                const u32 fk = LAZY ? red64(P[tid * BN + r], f) : (u32)P[tid * BN + r];
-                P[tid * BN + r] = fk;  // raw C entry
+                const u32 fk = P[tid * BN + r];
                 const u32 nfk = fk ? f.p - fk : 0u;
                 s_f[tid] = nfk;
                 if (tid > kb_end) s_fd[tid * SB + nb] = nfk;
@@ -441,12 +467,12 @@ __global__ void __launch_bounds__(256, 3) cup_batched_blk_kernel(u32* A, i64 str
                 for (int j = 0; j < SB; ++j)
                     if (j == nb) ureg[j] = u;
                 for (int t = k + 1; t <= kb_end; ++t)
-                    P[t * BN + c] = lazy_fma<LAZY>(P[t * BN + c], s_f[t], u, f);
+                    P[t * BN + c] = fma_red<LAZY>(P[t * BN + c], s_f[t], u, f);
             }
             {   // the block's pivot columns on the rows below the row block
                 const int t = kb_end + 1 + tid / SB, cc = bs_r + tid % SB;
                 if (t < pr && cc > r && cc < n)
-                    P[t * BN + cc] = lazy_fma<LAZY>(P[t * BN + cc], s_f[t], (u32)P[k * BN + cc], f);
+                    P[t * BN + cc] = fma_red<LAZY>(P[t * BN + cc], s_f[t], P[k * BN + cc], f);
             }
             ++nb;
             ++r;
@@ -455,200 +481,28 @@ __global__ void __launch_bounds__(256, 3) cup_batched_blk_kernel(u32* A, i64 str
         }
         flush();
         __syncthreads();
-        // rows of the panel after the early return (r == n) keep their values;
-        // reduce everything that is still lazy and write the panel back
+        // write the panel back (rows after the early return r == n keep their values)
         for (int t = warp; t < pr; t += 8)
-            for (int c = lane; c < n; c += 32) {
-                const u64 x = P[t * BN + c];
-                a[(i64)(i0 + t) * n + c] = LAZY ? red64(x, f) : (u32)x;
-            }
+            for (int c = lane; c < n; c += 32) a[(i64)(i0 + t) * n + c] = P[t * BN + c];
         // the panel's unit upper pivot block U_pp (strict upper triangle, packed) is
         // put aside for trailing_dmma while the panel is still in shared memory
         const int np = r - r0;
-        if (LAZY && RL_BATCHED_DMMA == 2) {
-            u32* Upk = reinterpret_cast<u32*>(reinterpret_cast<double*>(P) + PR * UDS + PR * XDS + 256);
+        if (LAZY) {
+            u32* Upk = reinterpret_cast<u32*>(smem_blk + OFF_UPK);
             for (int e = tid; e < PR * PR; e += 256) {
                 const int k = e / PR, i = e % PR;
-                if (k < i && i < np) Upk[upk_idx(k, i)] = (u32)P[s_prow[k] * BN + r0 + i];
+                if (k < i && i < np) Upk[upk_idx(k, i)] = P[s_prow[k] * BN + r0 + i];
             }
         }
         __syncthreads();
         // ---- trailing rows
         bool any_swap = false;
         for (int j = r0; j < r; ++j) any_swap |= (s_ipiv[j] != j);
-        static_assert(RL_BATCHED_DMMA == 2 || PR == 32, "the pre-v2 trailing paths assume 32-row panels");
-        static_assert((size_t)(PR * UDS + PR * XDS + 256) * 8 + (size_t)PR * (PR - 1) / 2 * 4 <=
-                          sizeof(u64) * PR * BN + sizeof(u32) * 8 * BN,
-                      "trailing_dmma's shared-memory layout must fit the kernel's dynamic allocation");
         // trailing_dmma stages at most UDS columns right of the pivot block (a
         // panel with fewer than PR - 8 pivots in a 256-column matrix has more)
-        if (LAZY && np > 0 && !any_swap && RL_BATCHED_DMMA == 2 && n - r <= UDS) {
-            trailing_dmma(a, m, n, f, i0, pr, r0, np, s_prow, reinterpret_cast<double*>(P));
-        } else if (LAZY && np > 0 && !any_swap) {
-            // TRSM-then-GEMM form, two rows per warp: the multipliers of a row are
-            // f = x_piv * U_pp^{-1} (U_pp = the panel's unit upper pivot block,
-            // inverted once per panel), then x_rest -= f * U_rest.  Same values as
-            // the pivot-by-pivot elimination (the solve is unique); the U loads
-            // from shared memory are shared by the two rows, and no reduction
-            // sits between consecutive pivots.
-            u32* Uc = reinterpret_cast<u32*>(P);                   // [PR][BN], 0 left of r0+np
-            u32 (*X)[PR + 1] = reinterpret_cast<u32 (*)[PR + 1]>(Uc + PR * BN);   // U_pp^{-1}
-            u32 (*Up)[PR + 1] = X + PR;                                          // U_pp
-            const int cend = r0 + np;
-            for (int j = warp; j < np; j += 8) {
-                const u32* src = a + (i64)(i0 + s_prow[j]) * n;
-                for (int c = lane; c < BN; c += 32) {
-                    const u32 v = c < n ? src[c] : 0u;
-                    Uc[j * BN + c] = c >= cend ? v : 0u;
-                    if (c >= r0 && c < cend) Up[j][c - r0] = v;
-                }
-            }
-            __syncthreads();
-            if (tid < np) {  // column j of X = U_pp^{-1} (unit upper), back substitution
-                const int j = tid;
-                X[j][j] = 1u % f.p;
-                for (int k = j - 1; k >= 0; --k) {
-                    u64 acc = 0;
-                    for (int i = k + 1; i <= j; ++i) acc += (u64)Up[k][i] * X[i][j];
-                    const u32 s = red64(acc, f);
-                    X[k][j] = s ? f.p - s : 0u;
-                }
-                for (int k = j + 1; k < PR; ++k) X[k][j] = 0;
-            } else if (tid < PR) {
-                for (int k = 0; k < PR; ++k) X[k][tid] = 0;
-            }
-            __syncthreads();
-#if RL_BATCHED_DMMA
-            // (1) multipliers: one warp per trailing row, f = x_piv * U_pp^{-1}
-            // (lane j < np holds f_j); the raw C entries f go to the row's pivot
-            // columns now, the negated multipliers (p - f) to shared memory
-            u32* Fs = reinterpret_cast<u32*>(Up + PR);  // [R][PR], R = m - i0 - pr
-            const i32 rbase = i0 + pr;
-            for (int k0 = rbase + warp; k0 < m; k0 += 8) {
-                u32* row = a + (i64)k0 * n;
-                const u32 pvl = lane < np ? row[r0 + lane] : 0u;
-                u64 sacc = 0;
-                for (int k = 0; k < np; ++k) sacc += (u64)__shfl_sync(0xffffffffu, pvl, k) * X[k][lane];
-                const u32 fv = red64(sacc, f);
-                if (lane < np) row[r0 + lane] = fv;
-                Fs[(k0 - rbase) * PR + lane] = (lane < np && fv) ? f.p - fv : 0u;
-            }
-            __syncthreads();
-            // (2) x_rest += (p - f) * U_rest on the FP64 tensor cores: every term
-            // is an integer < 2^46 and a row sums x + np <= 32 of them (< 2^52),
-            // so the m8n8k4 DMMA accumulation is exact; one reduction per output.
-            {
-                const i32 R = m - rbase, N = n - cend;
-                const int tN = (N + 7) >> 3, tiles = ((R + 7) >> 3) * tN;
-                const int ks_n = (np + 3) >> 2;
-                const double pd = (double)f.p, ipd = 1.0 / pd;
-                const int g = lane >> 2, q4 = lane & 3;
-                for (int tile = warp; tile < tiles; tile += 8) {
-                    const int tr = tile / tN, tn = tile - tr * tN;
-                    const int ra = tr * 8 + g;             // A row / C row of this lane
-                    const int cb = tn * 8 + g;             // B column of this lane
-                    const int cc = tn * 8 + 2 * q4;        // C columns cc, cc + 1
-                    u32* crow = a + (i64)(rbase + ra) * n + cend + cc;
-                    const bool rok = ra < R;
-                    double c0 = (rok && cc < N) ? (double)crow[0] : 0.0;
-                    double c1 = (rok && cc + 1 < N) ? (double)crow[1] : 0.0;
-                    const u32* frow = Fs + ra * PR;
-                    const u32* ucol = Uc + cend + cb;
-                    for (int ks = 0; ks < ks_n; ++ks) {
-                        const int k = 4 * ks + q4;
-                        const double av = (rok && k < np) ? (double)frow[k] : 0.0;
-                        const double bv = (cb < N) ? (double)ucol[k * BN] : 0.0;
-                        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                                     : "+d"(c0), "+d"(c1)
-                                     : "d"(av), "d"(bv));
-                    }
-                    if (rok) {
-                        if (cc < N) {
-                            double r = fma(-floor(c0 * ipd), pd, c0);
-                            r = r < 0.0 ? r + pd : (r >= pd ? r - pd : r);
-                            crow[0] = (u32)r;
-                        }
-                        if (cc + 1 < N) {
-                            double r = fma(-floor(c1 * ipd), pd, c1);
-                            r = r < 0.0 ? r + pd : (r >= pd ? r - pd : r);
-                            crow[1] = (u32)r;
-                        }
-                    }
-                }
-            }
-#else
-            const int cpos = r0 + lane, srcl = cpos & 31, qs = cpos >> 5;
-            constexpr int RW = BATCHED_ROWS_PER_WARP;
-            for (int k0 = i0 + pr + RW * warp; k0 < m; k0 += 8 * RW) {
-                u32* row[RW];
-                bool ok[RW];
-                u64 x[RW][BN / 32];
-#pragma unroll
-                for (int t = 0; t < RW; ++t) {
-                    ok[t] = k0 + t < m;
-                    row[t] = a + (i64)(k0 + t) * n;
-#pragma unroll
-                    for (int q = 0; q < BN / 32; ++q) {
-                        const int c = lane + 32 * q;
-                        x[t][q] = (ok[t] && q < nq && c < n) ? row[t][c] : 0u;
-                    }
-                }
-                // x at pivot column r0 + lane (values still reduced); every block is
-                // shuffled so that no register array is indexed dynamically
-                u32 pv[RW];
-#pragma unroll
-                for (int t = 0; t < RW; ++t) {
-                    pv[t] = 0;
-#pragma unroll
-                    for (int q = 0; q < BN / 32; ++q) {
-                        const u32 v = __shfl_sync(0xffffffffu, (u32)x[t][q], srcl);
-                        if (q == qs) pv[t] = v;
-                    }
-                }
-                // f_j (lane j) = sum_k x_piv[k] * X[k][j]
-                u64 sacc[RW];
-#pragma unroll
-                for (int t = 0; t < RW; ++t) sacc[t] = 0;
-                for (int k = 0; k < np; ++k) {
-                    const u32 xk = X[k][lane];
-#pragma unroll
-                    for (int t = 0; t < RW; ++t) sacc[t] += (u64)__shfl_sync(0xffffffffu, pv[t], k) * xk;
-                }
-                u32 fv[RW], nf[RW];
-#pragma unroll
-                for (int t = 0; t < RW; ++t) {
-                    fv[t] = red64(sacc[t], f);
-                    nf[t] = fv[t] ? f.p - fv[t] : 0u;
-                }
-                for (int j = 0; j < np; ++j) {
-                    u32 g[RW];
-#pragma unroll
-                    for (int t = 0; t < RW; ++t) g[t] = __shfl_sync(0xffffffffu, nf[t], j);
-                    const u32* U = Uc + j * BN + lane;
-#pragma unroll
-                    for (int q = 0; q < BN / 32; ++q) {
-                        const u32 u = U[32 * q];
-#pragma unroll
-                        for (int t = 0; t < RW; ++t) x[t][q] += (u64)g[t] * u;
-                    }
-                }
-#pragma unroll
-                for (int q = 0; q < BN / 32; ++q) {
-                    const int c = lane + 32 * q;
-                    // pivot columns take the raw C entries f (lane c - r0 holds them)
-                    const bool piv = c >= r0 && c < cend;
-#pragma unroll
-                    for (int t = 0; t < RW; ++t) {
-                        const u32 fc = __shfl_sync(0xffffffffu, fv[t], (c - r0) & 31);
-                        if (ok[t] && q < nq && c < n) row[t][c] = piv ? fc : red64(x[t][q], f);
-                    }
-                }
-            }
-#endif
-        } else if (np > 0) {  // one warp per row, pivot by pivot (transpositions, large p)
-            for (int t = warp; t < pr; t += 8)
-                for (int c = lane; c < n; c += 32) P[t * BN + c] = a[(i64)(i0 + t) * n + c];
-            __syncthreads();
+        if (LAZY && np > 0 && !any_swap && n - r <= UDS) {
+            trailing_dmma(a, m, n, f, i0, pr, r0, np, s_prow, smem_blk);
+        } else if (np > 0) {  // one warp per row, pivot by pivot (transpositions, large p, wide panels)
             u32* wb = wbuf + warp * BN;
             for (int k = i0 + pr + warp; k < m; k += 8) {
                 u32* row = a + (i64)k * n;
@@ -680,12 +534,12 @@ __global__ void __launch_bounds__(256, 3) cup_batched_blk_kernel(u32* A, i64 str
                         const int ll = (r0 + j) & 31;
                         const u32 fj = __shfl_sync(0xffffffffu, LAZY ? red64(x[Q], f) : (u32)x[Q], ll);
                         const u32 nf = fj ? f.p - fj : 0u;
-                        const u64* U = P + s_prow[j] * BN;
+                        const u32* U = P + s_prow[j] * BN;
                         if (lane == ll) x[Q] = fj;  // raw C entry
-                        else if (lane > ll) x[Q] = lazy_fma<LAZY>(x[Q], nf, (u32)U[32 * Q + lane], f);
+                        else if (lane > ll) x[Q] = lazy_fma<LAZY>(x[Q], nf, U[32 * Q + lane], f);
 #pragma unroll
                         for (int q = Q + 1; q < BN / 32; ++q)
-                            x[q] = lazy_fma<LAZY>(x[q], nf, (u32)U[32 * q + lane], f);
+                            x[q] = lazy_fma<LAZY>(x[q], nf, U[32 * q + lane], f);
                     }
                 }
 #pragma unroll
@@ -774,7 +628,7 @@ void cup_batched(u32* dA, i64 batch, i32 m, i32 n, i64 stride, u32 p, i32* d_ran
     // grid: one CTA per matrix (batch <= 2^31-1)
     const Fp f = make_fp(p);
     if (n <= BN) {
-        const size_t smem = sizeof(u64) * PR * BN + sizeof(u32) * 8 * BN;
+        const size_t smem = SMEM_BLK;
         static std::atomic<unsigned long long> attr_once{0};
         once_on_device(attr_once, [&] {
             RL_CUDA_CHECK(cudaFuncSetAttribute(cup_batched_blk_kernel<true>,
