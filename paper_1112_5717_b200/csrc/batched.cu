@@ -106,6 +106,9 @@ __global__ void __launch_bounds__(256) cup_batched_kernel(u32* A, i64 stride, i3
 #ifndef RL_BATCHED_SB
 #define RL_BATCHED_SB 4  // rows per sub-block of a panel (4 or 8): see the panel loop
 #endif
+#ifndef RL_BATCHED_VEC
+#define RL_BATCHED_VEC 1  // 16-byte panel loads and stores
+#endif
 #ifndef RL_BATCHED_CTAS
 #define RL_BATCHED_CTAS 4  // CTAs per SM the register allocation is bounded for
 #endif
@@ -330,17 +333,45 @@ __device__ __noinline__ void trailing_dmma(u32* a, int m, int n, const Fp& f, in
     }
 }
 
-// acc + nf * u with the sum kept below 2^64: lazily for p < 2^24 (LAZY), reduced
-// at every product otherwise
+// Barrett reduction for the LAZY kernel (p < 2^24): with 2^(k-1) <= p < 2^k and
+// x < 2^(2k+6) (up to 64 products of reduced elements), m = floor(2^(2k+6) / p):
+//   q = floor(floor(x / 2^(k-1)) * m / 2^(k+7))  is within [x/p - 2, x/p]
+// (Handbook of Applied Cryptography 14.42 with 6 spare bits), every operand a
+// 32-bit word: two funnel shifts, one 32 x 32 -> 64 product, one 32-bit
+// multiply-subtract -- about half the instructions of the 64-bit red64.
+struct Bar24 {
+    u32 m, s1, s2;
+};
+static Bar24 make_bar24(u32 p) {
+    int k = 0;
+    while ((p >> k) != 0) ++k;
+    Bar24 b;
+    b.m = (u32)((1ull << (2 * k + 6)) / p);
+    b.s1 = (u32)(k - 1);
+    b.s2 = (u32)(k + 7);
+    return b;
+}
+__device__ __forceinline__ u32 red_b(u64 x, u32 p, const Bar24& b) {
+    const u32 lo = (u32)x;
+    const u32 t = __funnelshift_r(lo, (u32)(x >> 32), b.s1);
+    const u64 pq = (u64)t * b.m;
+    const u32 q = __funnelshift_r((u32)pq, (u32)(pq >> 32), b.s2);
+    u32 r = lo - q * p;
+    r = r >= 2 * p ? r - 2 * p : r;
+    return r >= p ? r - p : r;
+}
+
+// x + nf * u mod p: through one product sum for p < 2^24 (LAZY), reduced at every
+// product otherwise
 template <bool LAZY>
-__device__ __forceinline__ u32 fma_red(u32 x, u32 nf, u32 u, const Fp& f) {
-    if (LAZY) return red64((u64)nf * u + x, f);
+__device__ __forceinline__ u32 fma_red(u32 x, u32 nf, u32 u, const Fp& f, const Bar24& b) {
+    if (LAZY) return red_b((u64)nf * u + x, f.p, b);
     return addmod(x, mulmod(nf, u, f), f);
 }
 
 template <bool LAZY>
 __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
-    u32* A, i64 stride, i32 m, i32 n, Fp f, i32* ranks, i32* rrp_out, i32* ipiv_out, i32 kcap,
+    u32* A, i64 stride, i32 m, i32 n, Fp f, Bar24 bar, i32* ranks, i32* rrp_out, i32* ipiv_out, i32 kcap,
     const u32* __restrict__ inv_tab) {
     extern __shared__ __align__(16) unsigned char smem_blk[];
     u32* P = reinterpret_cast<u32*>(smem_blk + OFF_P);        // [PR][BN] panel rows, reduced
@@ -353,12 +384,23 @@ __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     u32* a = A + (i64)blockIdx.x * stride;
     const int nq = (n + 31) / 32;
+    const bool vec_ok = RL_BATCHED_VEC && (n & 3) == 0 && (reinterpret_cast<uintptr_t>(a) & 15) == 0;
     int r = 0;
     for (int i0 = 0; i0 < m && r < n; i0 += PR) {
         const int pr = min(PR, m - i0);
         const int r0 = r;
-        for (int t = warp; t < pr; t += 8)
-            for (int c = lane; c < n; c += 32) P[t * BN + c] = a[(i64)(i0 + t) * n + c];
+        if (vec_ok) {  // 16-byte copies: a warp moves two rows per instruction
+            const int n4 = n >> 2;
+            for (int e = tid; e < pr * 64; e += 256) {
+                const int t = e >> 6, c4 = e & 63;
+                if (c4 < n4)
+                    *reinterpret_cast<uint4*>(P + t * BN + 4 * c4) =
+                        __ldcg(reinterpret_cast<const uint4*>(a + (i64)(i0 + t) * n) + c4);
+            }
+        } else {
+            for (int t = warp; t < pr; t += 8)
+                for (int c = lane; c < n; c += 32) P[t * BN + c] = a[(i64)(i0 + t) * n + c];
+        }
         __syncthreads();
         // ---- panel: rows in order, in row blocks of SB.  A pivot updates at once
         // only what the next steps read: its row block's remaining rows (every
@@ -387,7 +429,7 @@ __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
 #pragma unroll
                         for (int j = 0; j < SB; ++j)
                             if (j < nb) x += (u64)fm[j] * ureg[j];
-                        P[t * BN + c] = red64(x, f);
+                        P[t * BN + c] = red_b(x, f.p, bar);
                     } else {
                         u32 x = P[t * BN + c];
 #pragma unroll
@@ -446,7 +488,7 @@ __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
             // normalised U row
             u32 u = 0;
             if (c < n && c > r) {
-                u = mulmod(P[k * BN + c], pinv, f);
+                u = LAZY ? red_b((u64)P[k * BN + c] * pinv, f.p, bar) : mulmod(P[k * BN + c], pinv, f);
                 P[k * BN + c] = u;
             }
             // multipliers of the panel rows below: column r holds the raw C entries
@@ -467,12 +509,12 @@ __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
                 for (int j = 0; j < SB; ++j)
                     if (j == nb) ureg[j] = u;
                 for (int t = k + 1; t <= kb_end; ++t)
-                    P[t * BN + c] = fma_red<LAZY>(P[t * BN + c], s_f[t], u, f);
+                    P[t * BN + c] = fma_red<LAZY>(P[t * BN + c], s_f[t], u, f, bar);
             }
             {   // the block's pivot columns on the rows below the row block
                 const int t = kb_end + 1 + tid / SB, cc = bs_r + tid % SB;
                 if (t < pr && cc > r && cc < n)
-                    P[t * BN + cc] = fma_red<LAZY>(P[t * BN + cc], s_f[t], P[k * BN + cc], f);
+                    P[t * BN + cc] = fma_red<LAZY>(P[t * BN + cc], s_f[t], P[k * BN + cc], f, bar);
             }
             ++nb;
             ++r;
@@ -482,8 +524,18 @@ __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
         flush();
         __syncthreads();
         // write the panel back (rows after the early return r == n keep their values)
-        for (int t = warp; t < pr; t += 8)
-            for (int c = lane; c < n; c += 32) a[(i64)(i0 + t) * n + c] = P[t * BN + c];
+        if (vec_ok) {
+            const int n4 = n >> 2;
+            for (int e = tid; e < pr * 64; e += 256) {
+                const int t = e >> 6, c4 = e & 63;
+                if (c4 < n4)
+                    *(reinterpret_cast<uint4*>(a + (i64)(i0 + t) * n) + c4) =
+                        *reinterpret_cast<const uint4*>(P + t * BN + 4 * c4);
+            }
+        } else {
+            for (int t = warp; t < pr; t += 8)
+                for (int c = lane; c < n; c += 32) a[(i64)(i0 + t) * n + c] = P[t * BN + c];
+        }
         // the panel's unit upper pivot block U_pp (strict upper triangle, packed) is
         // put aside for trailing_dmma while the panel is still in shared memory
         const int np = r - r0;
@@ -640,11 +692,11 @@ void cup_batched(u32* dA, i64 batch, i32 m, i32 n, i64 stride, u32 p, i32* d_ran
         // take the in-kernel extended Euclid inverse (so does every p >= 2^24)
         if (p < (1u << 24))
             cup_batched_blk_kernel<true><<<(unsigned)batch, 256, smem, s>>>(
-                dA, stride, m, n, f, d_ranks, d_rrp, d_ipiv, kcap,
+                dA, stride, m, n, f, make_bar24(p), d_ranks, d_rrp, d_ipiv, kcap,
                 batch >= kTableMinBatch ? inverse_table(p, s) : nullptr);
         else
-            cup_batched_blk_kernel<false><<<(unsigned)batch, 256, smem, s>>>(dA, stride, m, n, f, d_ranks,
-                                                                            d_rrp, d_ipiv, kcap, nullptr);
+            cup_batched_blk_kernel<false><<<(unsigned)batch, 256, smem, s>>>(dA, stride, m, n, f, Bar24{0, 0, 0},
+                                                                            d_ranks, d_rrp, d_ipiv, kcap, nullptr);
     } else {
         cup_batched_kernel<<<(unsigned)batch, 256, 0, s>>>(dA, stride, m, n, f, d_ranks, d_rrp, d_ipiv,
                                                            kcap);
