@@ -453,9 +453,12 @@ __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
             const unsigned msk = __ballot_sync(0xffffffffu, v != 0);
             if (lane == 0) s_wmin[warp] = msk ? warp * 32 + __ffs(msk) - 1 : BN;
             __syncthreads();
-            int pc = s_wmin[0];
+            int pc = r;
+            if (P[k * BN + r] == 0) {  // (r < n) the usual case needs no scan
+                pc = s_wmin[0];
 #pragma unroll
-            for (int w = 1; w < 8; ++w) pc = min(pc, s_wmin[w]);
+                for (int w = 1; w < 8; ++w) pc = min(pc, s_wmin[w]);
+            }
             if (pc >= n) {  // no pivot: row k is zero at positions >= r
                 __syncthreads();
                 continue;

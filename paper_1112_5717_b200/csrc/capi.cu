@@ -1284,11 +1284,20 @@ int rl_cup_batched_u32(uint32_t* A, int64_t batch, int64_t m, int64_t n, int64_t
         i32* d_ranks = dmeta;
         i32* d_rrp = dmeta + batch;
         i32* d_ipiv = d_rrp + batch * kcap;
-        const i64 chunks = std::min<i64>(batch, 8);
-        std::vector<cudaEvent_t> ev_in((size_t)chunks), ev_out((size_t)chunks);
+        // 16 chunks: H2D of chunk c+1, the factorization of chunk c and D2H of
+        // chunk c-1 overlap on three streams; each chunk's metadata (ranks, row
+        // profiles, transpositions) comes back into pinned memory ahead of its
+        // bodies and is expanded on the host while the later chunks are in flight
+        const i64 chunks = std::min<i64>(batch, 16);
+        i32* h = (i32*)call.sc.pinned_ring_out((size_t)batch * (1 + 2 * kcap) * 4);
+        i32* h_ranks = h;
+        i32* h_rrp = h + batch;
+        i32* h_ipiv = h_rrp + batch * kcap;
+        std::vector<cudaEvent_t> ev_in((size_t)chunks), ev_out((size_t)chunks), ev_meta((size_t)chunks);
         for (i64 c = 0; c < chunks; ++c) {
             RL_CUDA_CHECK(cudaEventCreateWithFlags(&ev_in[c], cudaEventDisableTiming));
             RL_CUDA_CHECK(cudaEventCreateWithFlags(&ev_out[c], cudaEventDisableTiming));
+            RL_CUDA_CHECK(cudaEventCreateWithFlags(&ev_meta[c], cudaEventDisableTiming));
         }
         for (i64 c = 0; c < chunks; ++c) {
             const i64 t0 = batch * c / chunks, t1 = batch * (c + 1) / chunks;
@@ -1303,25 +1312,42 @@ int rl_cup_batched_u32(uint32_t* A, int64_t batch, int64_t m, int64_t n, int64_t
                         d_rrp + t0 * kcap, d_ipiv + t0 * kcap, (i32)kcap, sc);
             RL_CUDA_CHECK(cudaEventRecord(ev_out[c], sc));
             RL_CUDA_CHECK(cudaStreamWaitEvent(sd, ev_out[c], 0));
+            RL_CUDA_CHECK(cudaMemcpyAsync(h_ranks + t0, d_ranks + t0, (size_t)(t1 - t0) * 4,
+                                          cudaMemcpyDeviceToHost, sd));
+            RL_CUDA_CHECK(cudaMemcpyAsync(h_rrp + t0 * kcap, d_rrp + t0 * kcap, (size_t)(t1 - t0) * kcap * 4,
+                                          cudaMemcpyDeviceToHost, sd));
+            RL_CUDA_CHECK(cudaMemcpyAsync(h_ipiv + t0 * kcap, d_ipiv + t0 * kcap, (size_t)(t1 - t0) * kcap * 4,
+                                          cudaMemcpyDeviceToHost, sd));
+            RL_CUDA_CHECK(cudaEventRecord(ev_meta[c], sd));
             RL_CUDA_CHECK(cudaMemcpy2DAsync(A + t0 * stride, pitch, dA + t0 * stride, pitch, width, t1 - t0,
                                             cudaMemcpyDeviceToHost, sd));
         }
-        std::vector<i32> h((size_t)batch * (1 + 2 * kcap));
-        RL_CUDA_CHECK(cudaMemcpyAsync(h.data(), dmeta, h.size() * 4, cudaMemcpyDeviceToHost, sc));
-        RL_CUDA_CHECK(cudaStreamSynchronize(sc));
-        RL_CUDA_CHECK(cudaStreamSynchronize(sd));
+        cudaError_t first_err = cudaSuccess;
+        for (i64 c = 0; c < chunks; ++c) {
+            const i64 t0 = batch * c / chunks, t1 = batch * (c + 1) / chunks;
+            const cudaError_t e = cudaEventSynchronize(ev_meta[c]);
+            if (e != cudaSuccess) {
+                first_err = e;
+                break;
+            }
+            for (i64 t = t0; t < t1; ++t) {
+                const i64 r = h_ranks[t];
+                if (ranks) ranks[t] = r;
+                const u32* rp_t = (const u32*)(h_rrp + t * kcap);
+                const u32* ip_t = (const u32*)(h_ipiv + t * kcap);
+                if (rrp) for (i64 j = 0; j < r; ++j) rrp[t * kcap + j] = rp_t[j];
+                if (sigma) sigma_from_ipiv(n, r, ip_t, sigma + t * n);
+            }
+        }
+        const cudaError_t e_sc = cudaStreamSynchronize(sc), e_sd = cudaStreamSynchronize(sd);
         for (i64 c = 0; c < chunks; ++c) {
             cudaEventDestroy(ev_in[c]);
             cudaEventDestroy(ev_out[c]);
+            cudaEventDestroy(ev_meta[c]);
         }
-        for (i64 t = 0; t < batch; ++t) {
-            const i64 r = h[t];
-            if (ranks) ranks[t] = r;
-            const u32* rp_t = (const u32*)&h[batch + t * kcap];
-            const u32* ip_t = (const u32*)&h[batch + batch * kcap + t * kcap];
-            if (rrp) for (i64 j = 0; j < r; ++j) rrp[t * kcap + j] = rp_t[j];
-            if (sigma) sigma_from_ipiv(n, r, ip_t, sigma + t * n);
-        }
+        RL_CUDA_CHECK(first_err);
+        RL_CUDA_CHECK(e_sc);
+        RL_CUDA_CHECK(e_sd);
     });
 }
 
