@@ -6,6 +6,7 @@
 // U rows are placed at the end (factor.cpp:62-70 composed).  Outputs per
 // matrix: rank, row profile and pivot positions (sigma is composed on the host).
 #include <algorithm>
+#include <cstdio>
 #include <map>
 #include <mutex>
 
@@ -106,11 +107,24 @@ __global__ void __launch_bounds__(256) cup_batched_kernel(u32* A, i64 stride, i3
 #ifndef RL_BATCHED_SB
 #define RL_BATCHED_SB 4  // rows per sub-block of a panel (4 or 8): see the panel loop
 #endif
+#ifndef RL_BATCHED_NOTAB
+#define RL_BATCHED_NOTAB 0  // 1: pivot inverses by the extended Euclid loop instead of the table (experiment)
+#endif
+#ifndef RL_BATCHED_FAST
+#define RL_BATCHED_FAST 0  // 1: warp-level factorization of a panel's pivot window (generic position); measured slower, off
+#endif
 #ifndef RL_BATCHED_VEC
 #define RL_BATCHED_VEC 1  // 16-byte panel loads and stores
 #endif
 #ifndef RL_BATCHED_CTAS
 #define RL_BATCHED_CTAS 4  // CTAs per SM the register allocation is bounded for
+#endif
+#ifdef RL_BATCHED_TRACE  // per-phase cycle counts of a few CTAs (thread 0), printed at the end
+#define BT_DECL long long bt_[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}; long long bt_t = clock64()
+#define BT_MARK(i) do { const long long bt_n = clock64(); bt_[i] += bt_n - bt_t; bt_t = bt_n; } while (0)
+#else
+#define BT_DECL
+#define BT_MARK(i) do { } while (0)
 #endif
 constexpr int PR = RL_BATCHED_PR;  // panel rows
 constexpr int BN = 256;
@@ -146,10 +160,15 @@ constexpr int OFF_T = OFF_XD + 8 * PR * XDS;    // double [16][16] scratch of th
 constexpr int OFF_UPK = OFF_T + 8 * 256;        // u32 [PR (PR - 1) / 2] strict upper triangle of U_pp
 constexpr int SMEM_BLK = OFF_UPK + 2048;
 constexpr int OFF_FD = OFF_XD;                  // u32 [PR][SB] panel phase: multipliers of the row block's pivots
+constexpr int LTS = 36;                         // row stride of Lt (words): 16-byte rows, 4-way store conflicts
+constexpr int OFF_LT = OFF_XD;                  // u32 [PR][LTS] + [PR]: fast panel's multipliers and pivot inverses
 constexpr int OFF_WBUF = OFF_XD;                // u32 [8][BN] row buffers of the pivot-by-pivot trailing path
-static_assert(4 * PR * (PR - 1) / 2 <= 2048 && OFF_WBUF + 4 * 8 * BN <= SMEM_BLK && 4 * PR * SB <= 8 * PR * XDS,
+static_assert(4 * PR * LTS + 4 * PR <= 8 * PR * XDS && 4 * PR * (PR - 1) / 2 <= 2048 && OFF_WBUF + 4 * 8 * BN <= SMEM_BLK && 4 * PR * SB <= 8 * PR * XDS,
               "shared-memory layout");
 
+#ifdef RL_BATCHED_TRACE
+__shared__ long long g_bt_mid;
+#endif
 __device__ __forceinline__ int upk_idx(int k, int i) { return k * (2 * PR - 1 - k) / 2 + (i - k - 1); }
 // exact u32 -> double without the conversion pipe: 2^52 + w, minus 2^52
 __device__ __forceinline__ double u2d(u32 w) {
@@ -264,6 +283,9 @@ __device__ __noinline__ void trailing_dmma(u32* a, int m, int n, const Fp& f, in
         }
         __syncthreads();
     }
+#ifdef RL_BATCHED_TRACE
+    if (tid == 0) g_bt_mid = clock64();
+#endif
     // (b) row blocks of 8 trailing rows per warp
     const int rbase = i0 + pr;
     const int R = m - rbase;
@@ -369,6 +391,114 @@ __device__ __forceinline__ u32 fma_red(u32 x, u32 nf, u32 u, const Fp& f, const 
     return addmod(x, mulmod(nf, u, f), f);
 }
 
+// Fast panel, step 1 (one warp): the panel's window columns [r0, r0 + 32) in
+// place in shared memory, lane = column (see the kernel).  Compact loops on
+// purpose: the fully unrolled register version was 15 K instructions that one
+// warp runs once per panel -- instruction-fetch bound, 2.5x slower overall.
+__device__ __noinline__ void fast_window(u32* P, u32* Lt, u32* pinvr, i32* s_prow, int* s_fast, int pr, int r0,
+                                         int n, const Fp& f, const Bar24& bar, const u32* __restrict__ inv_tab) {
+    constexpr unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int wc = r0 + lane;
+    const bool in = wc < n;
+    int jr = 0, k = 0;
+    bool ok = true;
+    for (; k < pr && ok; ++k) {
+        const u32 xk = in ? P[k * BN + wc] : 0u;
+        const unsigned msk = __ballot_sync(FULL, lane >= jr && xk != 0);
+        u32 mine = 0, pinv = 0;
+        if (msk != 0) {
+            if (__ffs(msk) - 1 != jr) {  // its pivot is not at column r: a transposition
+                ok = false;
+            } else {
+                const u32 pv = __shfl_sync(FULL, xk, jr);
+                pinv = inv_tab ? __ldg(inv_tab + pv) : inv_euclid(pv, f.p);
+                const bool act = in && lane > jr;
+                const u32 u = act ? red_b((u64)xk * pinv, f.p, bar) : 0u;
+                if (act) P[k * BN + wc] = u;
+                // lane t holds row t's multiplier for this pivot (column jr of row t)
+                const u32 fv = (lane > k && lane < pr) ? P[lane * BN + r0 + jr] : 0u;
+                mine = fv ? f.p - fv : 0u;
+                // eight rows at a time, loads before stores: eight independent
+                // chains in flight (the compiler keeps a store ahead of the next load)
+                int t = k + 1;
+                if (t < pr) {  // the next row first: its entry at column jr + 1 is the likely next
+                               // pivot, whose inverse is requested now and arrives under the loop
+                    const u32 nf = __shfl_sync(FULL, mine, t);
+                    u32 x1 = in ? P[t * BN + wc] : 0u;
+                    if (act) {
+                        x1 = red_b((u64)nf * u + x1, f.p, bar);
+                        P[t * BN + wc] = x1;
+                    }
+                    const u32 pvn = __shfl_sync(FULL, x1, jr + 1);
+                    if (inv_tab) {
+                        u32 sink;
+                        asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(sink) : "l"(inv_tab + pvn));
+                        (void)sink;
+                    }
+                    ++t;
+                }
+                for (; t + 7 < pr; t += 8) {
+                    u32 nf[8], xv[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) nf[q] = __shfl_sync(FULL, mine, t + q);
+                    if (act) {
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) xv[q] = P[(t + q) * BN + wc];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) xv[q] = red_b((u64)nf[q] * u + xv[q], f.p, bar);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) P[(t + q) * BN + wc] = xv[q];
+                    }
+                }
+                for (; t < pr; ++t) {
+                    const u32 nf = __shfl_sync(FULL, mine, t);
+                    if (act) P[t * BN + wc] = red_b((u64)nf * u + P[t * BN + wc], f.p, bar);
+                }
+                if (lane == 0) s_prow[jr] = k;
+                ++jr;
+            }
+        }
+        Lt[lane * LTS + k] = mine;
+        if (lane == 0) pinvr[k] = pinv;
+        __syncwarp();
+    }
+    for (; k < PR; ++k) {
+        Lt[lane * LTS + k] = 0;
+        if (lane == 0) pinvr[k] = 0;
+    }
+    if (lane == 0) {
+        s_fast[0] = jr;
+        s_fast[1] = ok ? 1 : 0;
+    }
+}
+
+// Fast panel, step 2 (one thread per column c right of the window): forward
+// substitution down the column against the multipliers of step 1, the finished
+// entries read back from the column itself (a row without a pivot has zero
+// multipliers against it); returns true if a row without a pivot is nonzero
+// here (the panel is not generic).
+__device__ __noinline__ bool fast_column(u32* P, const u32* Lt, const u32* pinvr, int pr, int c, const Fp& f,
+                                         const Bar24& bar) {
+    bool bad = false;
+    for (int t = 0; t < pr; ++t) {
+        u64 acc = P[t * BN + c];
+        for (int j4 = 0; j4 < t; j4 += 4) {  // Lt[t][j] = 0 for j >= t
+            const uint4 m4 = *reinterpret_cast<const uint4*>(Lt + t * LTS + j4);
+            const u32* col = P + j4 * BN + c;
+            acc += (u64)m4.x * col[0];
+            acc += (u64)m4.y * col[BN];
+            acc += (u64)m4.z * col[2 * BN];
+            acc += (u64)m4.w * col[3 * BN];
+        }
+        const u32 v = red_b(acc, f.p, bar);
+        const u32 pi = pinvr[t];
+        bad |= (pi == 0 && v != 0);
+        P[t * BN + c] = pi ? red_b((u64)v * pi, f.p, bar) : v;
+    }
+    return bad;
+}
+
 template <bool LAZY>
 __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
     u32* A, i64 stride, i32 m, i32 n, Fp f, Bar24 bar, i32* ranks, i32* rrp_out, i32* ipiv_out, i32 kcap,
@@ -381,27 +511,72 @@ __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
     __shared__ u32 s_f[PR];
     __shared__ int s_wmin[8];
     __shared__ u32 s_pinv;
+    __shared__ int s_fast[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     u32* a = A + (i64)blockIdx.x * stride;
     const int nq = (n + 31) / 32;
+    BT_DECL;
     const bool vec_ok = RL_BATCHED_VEC && (n & 3) == 0 && (reinterpret_cast<uintptr_t>(a) & 15) == 0;
     int r = 0;
     for (int i0 = 0; i0 < m && r < n; i0 += PR) {
         const int pr = min(PR, m - i0);
         const int r0 = r;
-        if (vec_ok) {  // 16-byte copies: a warp moves two rows per instruction
-            const int n4 = n >> 2;
-            for (int e = tid; e < pr * 64; e += 256) {
-                const int t = e >> 6, c4 = e & 63;
-                if (c4 < n4)
-                    *reinterpret_cast<uint4*>(P + t * BN + 4 * c4) =
-                        __ldcg(reinterpret_cast<const uint4*>(a + (i64)(i0 + t) * n) + c4);
+        auto load_panel = [&]() {
+            if (vec_ok) {  // 16-byte copies: a warp moves two rows per instruction
+                const int n4 = n >> 2;
+                for (int e = tid; e < pr * 64; e += 256) {
+                    const int t = e >> 6, c4 = e & 63;
+                    if (c4 < n4)
+                        *reinterpret_cast<uint4*>(P + t * BN + 4 * c4) =
+                            __ldcg(reinterpret_cast<const uint4*>(a + (i64)(i0 + t) * n) + c4);
+                }
+            } else {
+                for (int t = warp; t < pr; t += 8)
+                    for (int c = lane; c < n; c += 32) P[t * BN + c] = a[(i64)(i0 + t) * n + c];
             }
-        } else {
-            for (int t = warp; t < pr; t += 8)
-                for (int c = lane; c < n; c += 32) P[t * BN + c] = a[(i64)(i0 + t) * n + c];
-        }
+        };
+        load_panel();
         __syncthreads();
+        BT_MARK(0);
+        // ---- fast panel (p < 2^24, pivots in generic position).  Warp 0 factors
+        // the panel's 32-column window [r0, r0 + 32) alone, in registers (lane =
+        // column, one register per row, no barrier on the pivot chain): row k's
+        // pivot must be its first nonzero at window positions >= jr and sit at jr
+        // exactly (no transposition); a row that is zero there is set aside as a
+        // zero row.  Every other thread then finishes its own column right of the
+        // window by one forward substitution against the multipliers warp 0 left
+        // in shared memory (496 lazy products, one reduction per row) and checks
+        // that the set-aside rows are zero there too.  Anything else (a pivot
+        // outside the window, a transposition) reloads the panel and takes the
+        // row-by-row loop below.  Same pivots, same values: each entry is the
+        // same sum of products, grouped differently.
+        bool fast_done = false;
+        if (LAZY && RL_BATCHED_FAST) {
+            u32* Lt = reinterpret_cast<u32*>(smem_blk + OFF_LT);  // [PR][LTS]: p - (C entry of row t for row k's pivot)
+            u32* pinvr = Lt + PR * LTS;                           // [PR]: inverse of row k's pivot, 0 if it has none
+            if (warp == 0) fast_window(P, Lt, pinvr, s_prow, s_fast, pr, r0, n, f, bar, inv_tab);
+            BT_MARK(9);
+            __syncthreads();
+            BT_MARK(7);
+            const int npf = s_fast[0];
+            bool bad = s_fast[1] == 0;
+            if (!bad && tid >= PR && r0 + tid < n) bad = fast_column(P, Lt, pinvr, pr, r0 + tid, f, bar);
+            BT_MARK(8);
+            if (__syncthreads_or(bad ? 1 : 0)) {  // not generic: start the panel over, row by row
+                load_panel();
+                __syncthreads();
+            } else {
+                fast_done = true;
+                for (int j = tid; j < npf; j += 256) {
+                    s_rrp[r0 + j] = i0 + s_prow[j];
+                    s_ipiv[r0 + j] = r0 + j;
+                }
+                r = r0 + npf;
+                __syncthreads();
+            }
+        }
+        BT_MARK(6);
+        if (!fast_done) {
         // ---- panel: rows in order, in row blocks of SB.  A pivot updates at once
         // only what the next steps read: its row block's remaining rows (every
         // thread its own column) and, for the rows below the row block, the SB
@@ -448,6 +623,7 @@ __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
                 flush();
                 kb_end = min(kb_end + SB, pr - 1);
                 bs_r = r;
+                BT_MARK(10);
             }
             const u32 v = (c < n && c >= r) ? P[k * BN + c] : 0u;
             const unsigned msk = __ballot_sync(0xffffffffu, v != 0);
@@ -459,6 +635,7 @@ __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
 #pragma unroll
                 for (int w = 1; w < 8; ++w) pc = min(pc, s_wmin[w]);
             }
+            BT_MARK(6);
             if (pc >= n) {  // no pivot: row k is zero at positions >= r
                 __syncthreads();
                 continue;
@@ -488,6 +665,10 @@ __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
                 __syncthreads();
                 pinv = s_pinv;
             }
+#ifdef RL_BATCHED_TRACE
+            if (pinv == 0xffffffffu) bt_[11] = 1;  // (the load has returned)
+#endif
+            BT_MARK(7);
             // normalised U row
             u32 u = 0;
             if (c < n && c > r) {
@@ -507,6 +688,7 @@ __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
                 s_prow[r - r0] = k;
             }
             __syncthreads();
+            BT_MARK(8);
             if (c < n && c > r) {
 #pragma unroll
                 for (int j = 0; j < SB; ++j)
@@ -519,13 +701,17 @@ __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
                 if (t < pr && cc > r && cc < n)
                     P[t * BN + cc] = fma_red<LAZY>(P[t * BN + cc], s_f[t], P[k * BN + cc], f, bar);
             }
+            BT_MARK(9);
             ++nb;
             ++r;
             // no barrier: the next row's pivot search reads only this thread's
             // own column, and everything shared is written after the next barrier
         }
+        BT_MARK(1);
         flush();
         __syncthreads();
+        }  // !fast_done
+        BT_MARK(1);
         // write the panel back (rows after the early return r == n keep their values)
         if (vec_ok) {
             const int n4 = n >> 2;
@@ -550,6 +736,7 @@ __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
             }
         }
         __syncthreads();
+        BT_MARK(2);
         // ---- trailing rows
         bool any_swap = false;
         for (int j = r0; j < r; ++j) any_swap |= (s_ipiv[j] != j);
@@ -557,6 +744,9 @@ __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
         // panel with fewer than PR - 8 pivots in a 256-column matrix has more)
         if (LAZY && np > 0 && !any_swap && n - r <= UDS) {
             trailing_dmma(a, m, n, f, i0, pr, r0, np, s_prow, smem_blk);
+#ifdef RL_BATCHED_TRACE
+            { const long long mid = g_bt_mid; bt_[3] += mid - bt_t; bt_t = mid; }
+#endif
         } else if (np > 0) {  // one warp per row, pivot by pivot (transpositions, large p, wide panels)
             u32* wb = wbuf + warp * BN;
             for (int k = i0 + pr + warp; k < m; k += 8) {
@@ -606,6 +796,7 @@ __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
             }
         }
         __syncthreads();
+        BT_MARK(4);
     }
     if (tid == 0) ranks[blockIdx.x] = r;
     for (int j = tid; j < r; j += 256) {
@@ -623,6 +814,15 @@ __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
             a[(i64)src * n + col] = 0;
         }
     }
+#ifdef RL_BATCHED_TRACE
+    __syncthreads();
+    BT_MARK(5);
+    if (tid == 0 && (blockIdx.x % 1024) == 700)
+        printf("BT cta %d rank %d: load %lld panel %lld wb+upk %lld trail_setup %lld sweep %lld place %lld | "
+               "pivot steps: search+bar1 %lld pinv %lld norm+mult+bar2 %lld update %lld blockflush %lld\n",
+               blockIdx.x, r, bt_[0], bt_[1] + bt_[6] + bt_[7] + bt_[8] + bt_[9] + bt_[10], bt_[2], bt_[3], bt_[4],
+               bt_[5], bt_[6], bt_[7], bt_[8], bt_[9], bt_[10]);
+#endif
 }
 
 __global__ void inv_table_kernel(u32* tab, u32 p) {
@@ -696,7 +896,7 @@ void cup_batched(u32* dA, i64 batch, i32 m, i32 n, i64 stride, u32 p, i32* d_ran
         if (p < (1u << 24))
             cup_batched_blk_kernel<true><<<(unsigned)batch, 256, smem, s>>>(
                 dA, stride, m, n, f, make_bar24(p), d_ranks, d_rrp, d_ipiv, kcap,
-                batch >= kTableMinBatch ? inverse_table(p, s) : nullptr);
+                (batch >= kTableMinBatch && !RL_BATCHED_NOTAB) ? inverse_table(p, s) : nullptr);
         else
             cup_batched_blk_kernel<false><<<(unsigned)batch, 256, smem, s>>>(dA, stride, m, n, f, Bar24{0, 0, 0},
                                                                             d_ranks, d_rrp, d_ipiv, kcap, nullptr);

@@ -1,6 +1,7 @@
 #!/usr/bin/env python3
 """Warp-state samples of an ncu --set full --import-source capture, summed by
-source line (all launches of the report).  Usage: ncu_src_summary.py rep [top]"""
+source line (all launches of the report).  Usage: ncu_src_summary.py rep [top] [column]
+(column: a source-page column to sum instead, e.g. "Instructions Executed")."""
 import collections
 import csv
 import io
@@ -9,6 +10,7 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
+COL = sys.argv[3] if len(sys.argv) > 3 else "Warp Stall Sampling (All Samples)"  # or "Instructions Executed"
 raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
@@ -22,7 +24,7 @@ for r in rows:
         continue
     if r[0] == "Line No":
         hdr = r
-        si = hdr.index("Warp Stall Sampling (All Samples)")
+        si = hdr.index(COL)
         continue
     if r[0] == "Function Name" or hdr is None or len(r) <= si or not r[0]:
         continue
@@ -34,7 +36,7 @@ for r in rows:
     agg[key] += v
     src[key] = r[1][:100]
     tot += v
-print(f"{rep}: {tot:.0f} warp samples")
+print(f"{rep}: {tot:.0f} {COL}")
 for k, v in agg.most_common(top):
     print(f"{v:7.0f} {100 * v / tot:5.1f}%  {k[0]}:{k[1]}  {src[k]}")
 raw = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
