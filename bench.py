@@ -692,7 +692,7 @@ def batched_record(args, rank, world, dist, steps, warmup):
         "metric": METRIC, "value": value, "unit": "matrices/s", "n_gpus": world,
         "steps": steps, "warmup": warmup, "ms_per_step": t_max / steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": f"u32 in GF({p}); u64 products, Barrett reduction", "data": "synthetic",
+        "dtype": f"u32 in GF({p}); panel: lazy u64 sums, 32-bit Barrett; trailing updates: f64 DMMA (exact, < 2^52)", "data": "synthetic",
         "config": {"workload": "c4", "desc": wl["desc"], "batch": total, "m": m, "n": n, "p": p,
                    "seed": seed, "parallelism": f"batch sharded {world} ways" if world > 1 else "single",
                    "ranks_match_recipe": int(ok.item()),
