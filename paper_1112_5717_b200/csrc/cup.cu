@@ -37,6 +37,7 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
     if (const char* e = getenv("RL_TILE_CTAS")) tile_ctas_ = atoi(e);
     if (const char* e = getenv("RL_TILE_AFTER_REST")) tile_after_rest_ = atoi(e) != 0;
     if (const char* e = getenv("RL_REST_PIECES")) rest_pieces_ = atoi(e) != 0;
+    if (const char* e = getenv("RL_REST_SPLIT")) rest_split_ = atoi(e) != 0;
     if (const char* e = getenv("RL_S2_PRIO")) s2_prio_ = atoi(e) != 0;
     if (m_ > 0 && n_ > 0) {
         if (tiled_on()) tiled(tile_g_);
@@ -752,6 +753,31 @@ cudaEvent_t CupEngine::rest_update(i32 b0, i32 bm, i32 x0, i32 x1) {
         RL_CUDA_CHECK(cudaEventRecord(ev, st));
         return ev;
     };
+    // rest_split_ (one tensor-core K chunk): the rows of the first leaf pair first
+    // -- the first tail waits for that GEMM only -- then the rows below with the B
+    // image the first GEMM packed (same stream, same workspace), joined by the
+    // left-spine node whose bottom half starts there, right before its first
+    // touch of those rows
+    if (rest_split_ && !rest_pieces_ && use_tc_ && x1 - x0 > PB && x1 - x0 <= tc_kmax(L_) && n_ > 2 * PW) {
+        i32 hi = bm, lo = bm / 2;  // node(b0, hi) has its bottom half at b0 + lo
+        while (lo / 2 >= 2 * PB) {
+            hi = lo;
+            lo /= 2;
+        }
+        if (lo >= 2 * PB && lo < bm && (dry_ || row_joins_.find({b0, hi}) == row_joins_.end())) {
+            if (dry_) events_needed_ += 3;
+            gemm(b0, lo, x0, x1, Dyn{b0, PW}, dyn_c(n_), n_, s2_);
+            e = record(s2_);
+            if (!dry_) pending_joins_.push_back(e);
+            EarlyPack ep{};
+            ep.buf = b2_;
+            ep.ev = e;
+            gemm(b0 + lo, bm - lo, x0, x1, Dyn{b0, PW}, dyn_c(n_), n_, s2_, 0, &ep);
+            e = record(s2_);
+            if (!dry_) row_joins_[{b0, hi}] = e;
+            return e;
+        }
+    }
     const i32 l0 = spine.back();
     gemm(b0, l0, x0, x1, Dyn{b0, PW}, dyn_c(n_), n_, s2_);
     e = record(s2_);

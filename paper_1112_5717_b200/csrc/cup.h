@@ -261,6 +261,11 @@ private:
 #endif
     // (measured slower: C3 24.2 vs 21.6 ms -- the bridge then waits for its piece)
     bool rest_pieces_ = RL_REST_PIECES != 0;     // rest_update() in left-spine pieces
+#ifndef RL_REST_SPLIT
+#define RL_REST_SPLIT 0
+#endif
+    // (measured: C3 20.30 vs 20.13 ms, bit-exact -- the slow first transitions of a tile do not wait for the whole rest GEMM)
+    bool rest_split_ = RL_REST_SPLIT != 0;       // rest_update(): the first leaf pair's rows first, B packed once
     cudaEvent_t rest_update(i32 b0, i32 bm, i32 x0, i32 x1);
 #ifndef RL_S2_PRIO
 #define RL_S2_PRIO 0
