@@ -37,7 +37,7 @@ CupEngine::CupEngine(i32 m, i32 n, i64 lda, u32 p) : m_(m), n_(n), lda_(lda), p_
     if (const char* e = getenv("RL_TILE_CTAS")) tile_ctas_ = atoi(e);
     if (const char* e = getenv("RL_TILE_AFTER_REST")) tile_after_rest_ = atoi(e) != 0;
     if (const char* e = getenv("RL_REST_PIECES")) rest_pieces_ = atoi(e) != 0;
-    if (const char* e = getenv("RL_REST_SPLIT")) rest_split_ = atoi(e) != 0;
+    if (const char* e = getenv("RL_REST_SPLIT")) rest_split_ = atoi(e);
     if (const char* e = getenv("RL_S2_PRIO")) s2_prio_ = atoi(e) != 0;
     if (m_ > 0 && n_ > 0) {
         if (tiled_on()) tiled(tile_g_);
@@ -765,15 +765,27 @@ cudaEvent_t CupEngine::rest_update(i32 b0, i32 bm, i32 x0, i32 x1) {
             lo /= 2;
         }
         if (lo >= 2 * PB && lo < bm && (dry_ || row_joins_.find({b0, hi}) == row_joins_.end())) {
-            if (dry_) events_needed_ += 3;
+            if (dry_) events_needed_ += 4;
             gemm(b0, lo, x0, x1, Dyn{b0, PW}, dyn_c(n_), n_, s2_);
             e = record(s2_);
             if (!dry_) pending_joins_.push_back(e);
-            EarlyPack ep{};
-            ep.buf = b2_;
-            ep.ev = e;
-            gemm(b0 + lo, bm - lo, x0, x1, Dyn{b0, PW}, dyn_c(n_), n_, s2_, 0, &ep);
-            e = record(s2_);
+            if (rest_split_ == 2) {
+                // ... on the lane of this height (own stream and workspaces, its own B
+                // pack): the later, smaller rest updates on s2_ do not queue behind it
+                Lane& ln = lanes_[bm];
+                if (!dry_) fork_to(s_, ln.st);
+                Lane* saved = lane_;
+                lane_ = &ln;
+                gemm(b0 + lo, bm - lo, x0, x1, Dyn{b0, PW}, dyn_c(n_), n_);
+                e = record(ln.st);
+                lane_ = saved;
+            } else {
+                EarlyPack ep{};
+                ep.buf = b2_;
+                ep.ev = e;
+                gemm(b0 + lo, bm - lo, x0, x1, Dyn{b0, PW}, dyn_c(n_), n_, s2_, 0, &ep);
+                e = record(s2_);
+            }
             if (!dry_) row_joins_[{b0, hi}] = e;
             return e;
         }

@@ -264,8 +264,8 @@ private:
 #ifndef RL_REST_SPLIT
 #define RL_REST_SPLIT 0
 #endif
-    // (measured: C3 20.30 vs 20.13 ms, bit-exact -- the slow first transitions of a tile do not wait for the whole rest GEMM)
-    bool rest_split_ = RL_REST_SPLIT != 0;       // rest_update(): the first leaf pair's rows first, B packed once
+    // (measured, bit-exact: C3 20.30 ms (1: both GEMMs on s2_) / 20.52 ms (2: the second on a lane) vs 20.13 ms)
+    int rest_split_ = RL_REST_SPLIT;             // rest_update(): the first leaf pair's rows first, B packed once
     cudaEvent_t rest_update(i32 b0, i32 bm, i32 x0, i32 x1);
 #ifndef RL_S2_PRIO
 #define RL_S2_PRIO 0

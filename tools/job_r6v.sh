@@ -2,7 +2,7 @@
 set -u
 OUT=gpurun_out/${1:-r6v}
 mkdir -p $OUT
-for v in 1 0 1 0; do
+for v in ${VARIANTS:-1 0 1 0}; do
   echo "RL_REST_SPLIT=$v" >> $OUT/c3.txt
   RL_REST_SPLIT=$v timeout -s KILL 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline 2>/dev/null | python -c "
 import json,sys

@@ -67,6 +67,16 @@ for lvl in sorted(gap):
           f"window avg {sum(d)/len(d)/1e3:5.1f} us")
 print(f"  total: windows {td/1e6:.2f} ms + gaps {tg/1e6:.2f} ms; first window start -> last window end "
       f"{(W[-1][1][1] - t0)/1e6:.2f} ms")
+if os.environ.get("LT_ALL"):  # every gap, 16 leaves (one 1024-row tile) per line
+    for k0 in range(0, len(W), 16):
+        print(f"  gaps before leaves {k0:3d}..: " + " ".join(
+            f"{(W[k][1][0] - W[k - 1][1][1]) / 1e3:5.0f}" if k else "    -" for k in range(k0, min(k0 + 16, len(W)))))
+    med = collections.defaultdict(list)
+    for k in range(1, len(W)):
+        med[k % 16].append((W[k][1][0] - W[k - 1][1][1]) / 1e3)
+    import statistics as _st
+    print("  median gap by position in the tile: " + " ".join(f"{_st.median(med[q]):.0f}" for q in range(16)))
+    print("  mean   gap by position in the tile: " + " ".join(f"{sum(med[q]) / len(med[q]):.0f}" for q in range(16)))
 slow = sorted(((W[k][1][0] - W[k - 1][1][1], k) for k in range(1, len(W))), reverse=True)[:24]
 print("  slowest transitions (us, leaf index: level): " +
       ", ".join(f"{g/1e3:.0f} @{k}:{(k & -k).bit_length() - 1}" for g, k in slow))
