@@ -62,7 +62,11 @@ struct Cfg {
     static constexpr int B_TILE = UN * BK;
     static constexpr int STAGE = A_TILE + B_TILE;
     static constexpr int STG = 16 * 32 * 16 * 4;  // epilogue staging: 16 warps x 32 rows x 16 cols
-    static constexpr int STAGES = (232448 - 1280 - STG) / STAGE;
+#ifndef RL_GEMM_SMEM_BUDGET
+#define RL_GEMM_SMEM_BUDGET 232448  // bytes per CTA (all of an SM); smaller budgets leave room for a co-resident CTA
+#endif
+    static constexpr int STAGES = (RL_GEMM_SMEM_BUDGET - 1280 - STG) / STAGE;
+    static_assert(STAGES >= 2, "the pipeline needs two stages");
     static constexpr int CH = 16;  // epilogue column chunk
     static constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 256 + STG;
 };
