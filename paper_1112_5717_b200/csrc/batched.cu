@@ -432,9 +432,8 @@ __device__ __noinline__ void fast_window(u32* P, u32* Lt, u32* pinvr, i32* s_pro
                     }
                     const u32 pvn = __shfl_sync(FULL, x1, jr + 1);
                     if (inv_tab) {
-                        u32 sink;
+                        [[maybe_unused]] u32 sink;
                         asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(sink) : "l"(inv_tab + pvn));
-                        (void)sink;
                     }
                     ++t;
                 }
