@@ -235,6 +235,39 @@ def test_batched_wide_first_panel_few_pivots():
             assert np.array_equal(body[t], a), (p, t, np.argwhere(body[t] != a)[:5])
 
 
+def test_batched_shape_and_prime_sweep_vs_oracle():
+    """The blocked batched kernel over ragged shapes (partial last panels, more
+    rows than columns, m > 256), primes on both sides of 2^24 and inputs that
+    force transpositions inside a row sub-block, zero rows and repeated rows."""
+    import torch
+    rng = np.random.default_rng(2027)
+    shapes = [(33, 256), (64, 37), (130, 200), (256, 255), (300, 64), (100, 256), (31, 8), (257, 129)]
+    for p in (2, 3, 251, 65521, 8388593, 16777259, 2147483647):
+        for (m, n) in shapes:
+            batch = 4
+            mats = rng.integers(0, p, (batch, m, n), dtype=np.uint64).astype(np.uint32)
+            mats[1, :, : n // 3] = 0                       # pivots start far right of column 0
+            mats[2, ::3, :] = 0                            # zero rows inside every sub-block
+            mats[2, 1::6, :] = mats[2, 4 % m, :]           # repeated rows
+            if n > 8:                                      # low rank: product of thin factors
+                k = max(1, min(m, n) // 4)
+                lf = rng.integers(0, p, (m, k), dtype=np.uint64)
+                rf = rng.integers(0, p, (k, n), dtype=np.uint64)
+                acc = np.zeros((m, n), dtype=np.uint64)
+                for j in range(k):                         # (products < 2^62: reduce per term)
+                    acc = (acc + (lf[:, j:j + 1] * rf[j:j + 1, :]) % p) % p
+                mats[3] = acc.astype(np.uint32)
+            dev = torch.from_numpy(mats.view(np.int32).copy()).cuda()
+            rk, rrp, sig = G.cup_batched_dev(dev, batch, m, n, p)
+            body = dev.cpu().numpy().view(np.uint32)
+            for t in range(batch):
+                a = mats[t].copy()
+                o = O.port_cup(a, p)
+                assert rk[t] == o.rank and np.array_equal(rrp[t, :o.rank], o.rrp), (p, m, n, t)
+                assert np.array_equal(sig[t], o.sigma), (p, m, n, t)
+                assert np.array_equal(body[t], a), (p, m, n, t, np.argwhere(body[t] != a)[:5])
+
+
 def test_large_properties_dev():
     """At full-size-class dimensions: structural outputs + Freivalds A = C*U*P."""
     import torch
