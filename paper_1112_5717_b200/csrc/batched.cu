@@ -188,7 +188,15 @@ __device__ __forceinline__ double u2d(u32 w) {
 // shuffles and sweeps the row block's column tiles (C prefetched one tile ahead).
 // U_rest stays u32 in shared memory (one wavefront per B fragment) and becomes
 // a double in the register (u2d).
-__device__ __noinline__ void trailing_dmma(u32* a, int m, int n, const Fp& f, int i0, int pr, int r0, int np,
+#ifndef RL_BATCHED_TRAIL_INLINE
+#define RL_BATCHED_TRAIL_INLINE 0  // 1: inline trailing_dmma into the kernel (experiment)
+#endif
+#if RL_BATCHED_TRAIL_INLINE
+#define RL_TRAIL_ATTR __forceinline__
+#else
+#define RL_TRAIL_ATTR __noinline__
+#endif
+__device__ RL_TRAIL_ATTR void trailing_dmma(u32* a, int m, int n, const Fp& f, int i0, int pr, int r0, int np,
                                            const i32* s_prow, unsigned char* sm) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q4 = lane & 3;
     const int cend = r0 + np, N = n - cend;
