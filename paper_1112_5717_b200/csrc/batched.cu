@@ -128,6 +128,12 @@ __global__ void __launch_bounds__(256) cup_batched_kernel(u32* A, i64 stride, i3
 #endif
 constexpr int PR = RL_BATCHED_PR;  // panel rows
 constexpr int BN = 256;
+#ifndef RL_BATCHED_PS
+#define RL_BATCHED_PS 260
+#endif
+constexpr int PS = RL_BATCHED_PS;  // row stride of the panel in shared memory (words): 16-byte rows; 260 puts
+                                   // consecutive rows 4 banks apart (column reads down the rows: 4-way, not 32-way, conflicts)
+static_assert(PS >= BN && PS % 4 == 0, "panel row stride");
 constexpr int SB = RL_BATCHED_SB;
 static_assert(PR == 32, "trailing_dmma's tiling assumes 32-row panels");
 static_assert(SB == 4 || SB == 8, "row blocks of 4 or 8");
@@ -155,7 +161,7 @@ static_assert(UDS % 32 == 8 && UDS % 8 == 0, "Ud stride");
 // dynamic shared memory of cup_batched_blk_kernel (bytes)
 constexpr int OFF_P = 0;                        // u32 [PR][BN] panel rows (reduced)
 constexpr int OFF_UD = 0;                       // u32 [PR][UDS] U_rest, compacted in place from P
-constexpr int OFF_XD = OFF_P + 4 * PR * BN;     // double [PR][XDS] U_pp^{-1}
+constexpr int OFF_XD = OFF_P + 4 * PR * PS;     // double [PR][XDS] U_pp^{-1}
 constexpr int OFF_T = OFF_XD + 8 * PR * XDS;    // double [16][16] scratch of the doubling levels
 constexpr int OFF_UPK = OFF_T + 8 * 256;        // u32 [PR (PR - 1) / 2] strict upper triangle of U_pp
 constexpr int SMEM_BLK = OFF_UPK + 2048;
@@ -217,7 +223,7 @@ __device__ RL_TRAIL_ATTR void trailing_dmma(u32* a, int m, int n, const Fp& f, i
             const int e = tid + 256 * h;
             const int j = 16 * q + e / (UDS / 8), c0 = (e % (UDS / 8)) * 8;
             const bool on = e < 16 * (UDS / 8) && j < np;
-            const u32* src = Pp + (on ? s_prow[j] : 0) * BN + cend + c0;
+            const u32* src = Pp + (on ? s_prow[j] : 0) * PS + cend + c0;
 #pragma unroll
             for (int z = 0; z < 8; ++z) w[h][z] = (on && c0 + z < N) ? src[z] : 0u;
         }
@@ -412,7 +418,7 @@ __device__ __noinline__ void fast_window(u32* P, u32* Lt, u32* pinvr, i32* s_pro
     int jr = 0, k = 0;
     bool ok = true;
     for (; k < pr && ok; ++k) {
-        const u32 xk = in ? P[k * BN + wc] : 0u;
+        const u32 xk = in ? P[k * PS + wc] : 0u;
         const unsigned msk = __ballot_sync(FULL, lane >= jr && xk != 0);
         u32 mine = 0, pinv = 0;
         if (msk != 0) {
@@ -423,9 +429,9 @@ __device__ __noinline__ void fast_window(u32* P, u32* Lt, u32* pinvr, i32* s_pro
                 pinv = inv_tab ? __ldg(inv_tab + pv) : inv_euclid(pv, f.p);
                 const bool act = in && lane > jr;
                 const u32 u = act ? red_b((u64)xk * pinv, f.p, bar) : 0u;
-                if (act) P[k * BN + wc] = u;
+                if (act) P[k * PS + wc] = u;
                 // lane t holds row t's multiplier for this pivot (column jr of row t)
-                const u32 fv = (lane > k && lane < pr) ? P[lane * BN + r0 + jr] : 0u;
+                const u32 fv = (lane > k && lane < pr) ? P[lane * PS + r0 + jr] : 0u;
                 mine = fv ? f.p - fv : 0u;
                 // eight rows at a time, loads before stores: eight independent
                 // chains in flight (the compiler keeps a store ahead of the next load)
@@ -433,10 +439,10 @@ __device__ __noinline__ void fast_window(u32* P, u32* Lt, u32* pinvr, i32* s_pro
                 if (t < pr) {  // the next row first: its entry at column jr + 1 is the likely next
                                // pivot, whose inverse is requested now and arrives under the loop
                     const u32 nf = __shfl_sync(FULL, mine, t);
-                    u32 x1 = in ? P[t * BN + wc] : 0u;
+                    u32 x1 = in ? P[t * PS + wc] : 0u;
                     if (act) {
                         x1 = red_b((u64)nf * u + x1, f.p, bar);
-                        P[t * BN + wc] = x1;
+                        P[t * PS + wc] = x1;
                     }
                     const u32 pvn = __shfl_sync(FULL, x1, jr + 1);
                     if (inv_tab) {
@@ -451,16 +457,16 @@ __device__ __noinline__ void fast_window(u32* P, u32* Lt, u32* pinvr, i32* s_pro
                     for (int q = 0; q < 8; ++q) nf[q] = __shfl_sync(FULL, mine, t + q);
                     if (act) {
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) xv[q] = P[(t + q) * BN + wc];
+                        for (int q = 0; q < 8; ++q) xv[q] = P[(t + q) * PS + wc];
 #pragma unroll
                         for (int q = 0; q < 8; ++q) xv[q] = red_b((u64)nf[q] * u + xv[q], f.p, bar);
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) P[(t + q) * BN + wc] = xv[q];
+                        for (int q = 0; q < 8; ++q) P[(t + q) * PS + wc] = xv[q];
                     }
                 }
                 for (; t < pr; ++t) {
                     const u32 nf = __shfl_sync(FULL, mine, t);
-                    if (act) P[t * BN + wc] = red_b((u64)nf * u + P[t * BN + wc], f.p, bar);
+                    if (act) P[t * PS + wc] = red_b((u64)nf * u + P[t * PS + wc], f.p, bar);
                 }
                 if (lane == 0) s_prow[jr] = k;
                 ++jr;
@@ -489,19 +495,19 @@ __device__ __noinline__ bool fast_column(u32* P, const u32* Lt, const u32* pinvr
                                          const Bar24& bar) {
     bool bad = false;
     for (int t = 0; t < pr; ++t) {
-        u64 acc = P[t * BN + c];
+        u64 acc = P[t * PS + c];
         for (int j4 = 0; j4 < t; j4 += 4) {  // Lt[t][j] = 0 for j >= t
             const uint4 m4 = *reinterpret_cast<const uint4*>(Lt + t * LTS + j4);
-            const u32* col = P + j4 * BN + c;
+            const u32* col = P + j4 * PS + c;
             acc += (u64)m4.x * col[0];
-            acc += (u64)m4.y * col[BN];
-            acc += (u64)m4.z * col[2 * BN];
-            acc += (u64)m4.w * col[3 * BN];
+            acc += (u64)m4.y * col[PS];
+            acc += (u64)m4.z * col[2 * PS];
+            acc += (u64)m4.w * col[3 * PS];
         }
         const u32 v = red_b(acc, f.p, bar);
         const u32 pi = pinvr[t];
         bad |= (pi == 0 && v != 0);
-        P[t * BN + c] = pi ? red_b((u64)v * pi, f.p, bar) : v;
+        P[t * PS + c] = pi ? red_b((u64)v * pi, f.p, bar) : v;
     }
     return bad;
 }
@@ -534,12 +540,12 @@ __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
                 for (int e = tid; e < pr * 64; e += 256) {
                     const int t = e >> 6, c4 = e & 63;
                     if (c4 < n4)
-                        *reinterpret_cast<uint4*>(P + t * BN + 4 * c4) =
+                        *reinterpret_cast<uint4*>(P + t * PS + 4 * c4) =
                             __ldcg(reinterpret_cast<const uint4*>(a + (i64)(i0 + t) * n) + c4);
                 }
             } else {
                 for (int t = warp; t < pr; t += 8)
-                    for (int c = lane; c < n; c += 32) P[t * BN + c] = a[(i64)(i0 + t) * n + c];
+                    for (int c = lane; c < n; c += 32) P[t * PS + c] = a[(i64)(i0 + t) * n + c];
             }
         };
         load_panel();
@@ -607,17 +613,17 @@ __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
                     for (int j4 = 0; j4 < SB; j4 += 4)
                         *reinterpret_cast<uint4*>(fm + j4) = *reinterpret_cast<const uint4*>(s_fd + t * SB + j4);
                     if (LAZY) {
-                        u64 x = P[t * BN + c];
+                        u64 x = P[t * PS + c];
 #pragma unroll
                         for (int j = 0; j < SB; ++j)
                             if (j < nb) x += (u64)fm[j] * ureg[j];
-                        P[t * BN + c] = red_b(x, f.p, bar);
+                        P[t * PS + c] = red_b(x, f.p, bar);
                     } else {
-                        u32 x = P[t * BN + c];
+                        u32 x = P[t * PS + c];
 #pragma unroll
                         for (int j = 0; j < SB; ++j)
                             if (j < nb) x = addmod(x, mulmod(fm[j], ureg[j], f), f);
-                        P[t * BN + c] = x;
+                        P[t * PS + c] = x;
                     }
                 }
             }
@@ -632,12 +638,12 @@ __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
                 bs_r = r;
                 BT_MARK(10);
             }
-            const u32 v = (c < n && c >= r) ? P[k * BN + c] : 0u;
+            const u32 v = (c < n && c >= r) ? P[k * PS + c] : 0u;
             const unsigned msk = __ballot_sync(0xffffffffu, v != 0);
             if (lane == 0) s_wmin[warp] = msk ? warp * 32 + __ffs(msk) - 1 : BN;
             __syncthreads();
             int pc = r;
-            if (P[k * BN + r] == 0) {  // (r < n) the usual case needs no scan
+            if (P[k * PS + r] == 0) {  // (r < n) the usual case needs no scan
                 pc = s_wmin[0];
 #pragma unroll
                 for (int w = 1; w < 8; ++w) pc = min(pc, s_wmin[w]);
@@ -652,9 +658,9 @@ __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
                 bs_r = r;
                 __syncthreads();
                 for (int t = tid; t < pr; t += 256) {
-                    const u32 x = P[t * BN + r];
-                    P[t * BN + r] = P[t * BN + pc];
-                    P[t * BN + pc] = x;
+                    const u32 x = P[t * PS + r];
+                    P[t * PS + r] = P[t * PS + pc];
+                    P[t * PS + pc] = x;
                 }
                 for (int j = tid; j < r0; j += 256) {
                     u32* row = a + (i64)s_rrp[j] * n;
@@ -666,9 +672,9 @@ __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
             }
             u32 pinv;
             if (inv_tab) {  // p < 2^24: every thread loads the inverse (one cached word)
-                pinv = __ldg(inv_tab + P[k * BN + r]);
+                pinv = __ldg(inv_tab + P[k * PS + r]);
             } else {        // one thread runs the extended Euclid
-                if (tid == 0) s_pinv = inv_euclid(P[k * BN + r], f.p);
+                if (tid == 0) s_pinv = inv_euclid(P[k * PS + r], f.p);
                 __syncthreads();
                 pinv = s_pinv;
             }
@@ -679,12 +685,12 @@ __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
             // normalised U row
             u32 u = 0;
             if (c < n && c > r) {
-                u = LAZY ? red_b((u64)P[k * BN + c] * pinv, f.p, bar) : mulmod(P[k * BN + c], pinv, f);
-                P[k * BN + c] = u;
+                u = LAZY ? red_b((u64)P[k * PS + c] * pinv, f.p, bar) : mulmod(P[k * PS + c], pinv, f);
+                P[k * PS + c] = u;
             }
             // multipliers of the panel rows below: column r holds the raw C entries
             if (tid > k && tid < pr) {
-                const u32 fk = P[tid * BN + r];
+                const u32 fk = P[tid * PS + r];
                 const u32 nfk = fk ? f.p - fk : 0u;
                 s_f[tid] = nfk;
                 if (tid > kb_end) s_fd[tid * SB + nb] = nfk;
@@ -701,12 +707,12 @@ __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
                 for (int j = 0; j < SB; ++j)
                     if (j == nb) ureg[j] = u;
                 for (int t = k + 1; t <= kb_end; ++t)
-                    P[t * BN + c] = fma_red<LAZY>(P[t * BN + c], s_f[t], u, f, bar);
+                    P[t * PS + c] = fma_red<LAZY>(P[t * PS + c], s_f[t], u, f, bar);
             }
             {   // the block's pivot columns on the rows below the row block
                 const int t = kb_end + 1 + tid / SB, cc = bs_r + tid % SB;
                 if (t < pr && cc > r && cc < n)
-                    P[t * BN + cc] = fma_red<LAZY>(P[t * BN + cc], s_f[t], P[k * BN + cc], f, bar);
+                    P[t * PS + cc] = fma_red<LAZY>(P[t * PS + cc], s_f[t], P[k * PS + cc], f, bar);
             }
             BT_MARK(9);
             ++nb;
@@ -726,11 +732,11 @@ __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
                 const int t = e >> 6, c4 = e & 63;
                 if (c4 < n4)
                     *(reinterpret_cast<uint4*>(a + (i64)(i0 + t) * n) + c4) =
-                        *reinterpret_cast<const uint4*>(P + t * BN + 4 * c4);
+                        *reinterpret_cast<const uint4*>(P + t * PS + 4 * c4);
             }
         } else {
             for (int t = warp; t < pr; t += 8)
-                for (int c = lane; c < n; c += 32) a[(i64)(i0 + t) * n + c] = P[t * BN + c];
+                for (int c = lane; c < n; c += 32) a[(i64)(i0 + t) * n + c] = P[t * PS + c];
         }
         // the panel's unit upper pivot block U_pp (strict upper triangle, packed) is
         // put aside for trailing_dmma while the panel is still in shared memory
@@ -739,7 +745,7 @@ __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
             u32* Upk = reinterpret_cast<u32*>(smem_blk + OFF_UPK);
             for (int e = tid; e < PR * PR; e += 256) {
                 const int k = e / PR, i = e % PR;
-                if (k < i && i < np) Upk[upk_idx(k, i)] = P[s_prow[k] * BN + r0 + i];
+                if (k < i && i < np) Upk[upk_idx(k, i)] = P[s_prow[k] * PS + r0 + i];
             }
         }
         __syncthreads();
@@ -786,7 +792,7 @@ __global__ void __launch_bounds__(256, RL_BATCHED_CTAS) cup_batched_blk_kernel(
                         const int ll = (r0 + j) & 31;
                         const u32 fj = __shfl_sync(0xffffffffu, LAZY ? red64(x[Q], f) : (u32)x[Q], ll);
                         const u32 nf = fj ? f.p - fj : 0u;
-                        const u32* U = P + s_prow[j] * BN;
+                        const u32* U = P + s_prow[j] * PS;
                         if (lane == ll) x[Q] = fj;  // raw C entry
                         else if (lane > ll) x[Q] = lazy_fma<LAZY>(x[Q], nf, U[32 * Q + lane], f);
 #pragma unroll
